@@ -1,0 +1,149 @@
+"""Pin the CPU oracle (oracle/fsa_oracle.py) to the real reference's outputs.
+
+The fixtures were produced by importing the reference package itself
+(tests/golden/make_golden.py).  Tolerances follow the reference's own tests
+(1e-10 forward, 1e-9 backward, test_kv_major.py / test_acceptance.py).
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+from golden_io import FULL_CASES, case, load, stride_of
+from oracle import fsa_oracle as O
+
+
+def _tol(z):
+    return 1e-10 if z["out"].dtype == np.float64 else 2e-5
+
+
+@pytest.mark.parametrize("name", FULL_CASES)
+def test_selection_and_inverse_bit_exact(name):
+    kw, c, inp, z = case(name)
+    if str(z["sel_mode"]) == "random_uniform":
+        scores = O.make_scores(c, int(z["seed"]))
+    else:
+        cmp = O.compress_kv(inp["K"], inp["V"], c)
+        scores = O.importance_scores(inp["Q"], cmp.K_cmp, c)
+    idx = O.select_topk(scores, c)
+    np.testing.assert_array_equal(idx, z["idx"])
+    inv = O.build_inverse(idx, c)
+    np.testing.assert_array_equal(inv.offsets, z["inv_offsets"])
+    np.testing.assert_array_equal(np.concatenate(inv.tok), z["inv_tok"])
+    np.testing.assert_array_equal(inv.n_valid, z["n_valid"])
+
+
+@pytest.mark.parametrize("name", FULL_CASES)
+def test_forward_backward_match_reference(name):
+    kw, c, inp, z = case(name)
+    st = stride_of(z)
+    tol = _tol(z)
+    idx = z["idx"]
+    out, lse = O.selected_forward(inp["Q"], inp["K"], inp["V"], idx, c)
+    scale = max(1.0, float(np.abs(z["out"]).max()))
+    assert np.abs(out[::st] - z["out"]).max() <= tol * scale
+    assert np.abs(lse - z["lse"]).max() <= tol * max(1.0, float(np.abs(z["lse"]).max()))
+    stats = O.softmax_stats(inp["Q"], inp["K"], idx, c)
+    assert np.abs(stats.m - z["m"]).max() <= tol * 10
+    assert np.abs(stats.l - z["l"]).max() <= tol * 10 * max(1.0, float(z["l"].max()))
+    stats = O.softmax_stats(inp["Q"], inp["K"], idx, c, shared_max=True)
+    np.testing.assert_allclose(stats.m, z["m_sh"], atol=tol * 10)
+    np.testing.assert_allclose(stats.l, z["l_sh"], rtol=tol * 10, atol=tol * 10)
+    dQ, dK, dV = O.selected_backward(inp["Q"], inp["K"], inp["V"], idx, inp["dOut"], c)
+    btol = 1e-9 if z["dQ"].dtype == np.float64 else 5e-5
+    for got, key in ((dQ, "dQ"), (dK, "dK"), (dV, "dV")):
+        ref = z[key]
+        assert np.abs(got[::st] - ref).max() <= btol * max(1.0, float(np.abs(ref).max())), key
+
+
+@pytest.mark.parametrize("name", FULL_CASES)
+def test_branches_match_reference(name):
+    kw, c, inp, z = case(name)
+    st = stride_of(z)
+    tol = _tol(z)
+    cmp = O.compress_kv(inp["K"], inp["V"], c)
+    for key, got in zip(("K_cmp", "V_cmp", "K_prefix", "V_prefix"), cmp):
+        np.testing.assert_allclose(got, z[key], atol=tol, rtol=tol)
+    sc = O.importance_scores(inp["Q"], cmp.K_cmp, c)
+    np.testing.assert_allclose(sc[:, ::st], z["scores_cmp"], atol=tol * 10, rtol=tol)
+    o, l = O.compressed_forward(inp["Q"], cmp, c)
+    np.testing.assert_allclose(o[::st], z["cmp_out"], atol=tol * 10, rtol=tol)
+    np.testing.assert_allclose(l, z["cmp_lse"], atol=tol * 10, rtol=tol)
+    if "slide_out" in z.files:
+        so, sl = O.sliding_forward(inp["Q"], inp["K"], inp["V"], c)
+        np.testing.assert_allclose(so[::st], z["slide_out"], atol=tol * 10, rtol=tol)
+        np.testing.assert_allclose(sl, z["slide_lse"], atol=tol * 10, rtol=tol)
+        g = O.sliding_backward(inp["Q"], inp["K"], inp["V"], inp["dOut"], c)
+        btol = 1e-9 if z["dQ"].dtype == np.float64 else 5e-5
+        for got, key in zip(g, ("slide_dQ", "slide_dK", "slide_dV")):
+            ref = z[key]
+            assert np.abs(got[::st] - ref).max() <= btol * max(1.0, float(np.abs(ref).max())), key
+        sel_out, _ = O.selected_forward(inp["Q"], inp["K"], inp["V"], z["idx"], c)
+        comb, lse = O.gated_combine((o, sel_out, so), inp["tau"], c)
+        np.testing.assert_allclose(comb[::st], z["comb_out"], atol=tol * 10, rtol=tol)
+        assert np.isnan(lse).all()
+
+
+@pytest.mark.parametrize("name", FULL_CASES)
+def test_dense_truth_agrees(name):
+    kw, c, inp, z = case(name)
+    if "dense_out" not in z.files:
+        pytest.skip("large case: dense truth not stored")
+    allow = O.selection_mask(z["idx"], c)
+    out, lse = O.dense_forward(inp["Q"], inp["K"], inp["V"], allow, c)
+    np.testing.assert_allclose(out, z["dense_out"], atol=1e-10)
+    np.testing.assert_allclose(lse, z["dense_lse"], atol=1e-10)
+
+
+@pytest.mark.parametrize("name", FULL_CASES)
+def test_meter_closed_forms(name):
+    kw, c, inp, z = case(name)
+    want_f = json.loads(str(z["meter_fwd"]))
+    want_b = json.loads(str(z["meter_bwd"]))
+    assert O.meter_forward(z["n_valid"], c) == want_f
+    assert O.meter_backward(z["n_valid"], c) == want_b
+
+
+def _kat_scores(z, tag, c):
+    if tag + "__scores" in z.files:
+        return z[tag + "__scores"]
+    seed, f32 = (int(v) for v in z[tag + "__seed"])
+    s = O.make_scores(c, seed)
+    return s.astype(np.float32).astype(np.float64) if f32 else s
+
+
+def test_selection_kats():
+    z = load("selection_kats")
+    tags = sorted({k.split("__")[0] for k in z.files})
+    assert len(tags) >= 9
+    for tag in tags:
+        c = O.cfg_of(**json.loads(str(z[tag + "__cfg"])))
+        idx = O.select_topk(_kat_scores(z, tag, c), c)
+        np.testing.assert_array_equal(idx, z[tag + "__idx"], err_msg=tag)
+
+
+def test_malformed_messages():
+    z = load("malformed")
+    c = O.cfg_of(**json.loads(str(z["cfg"])))
+    msgs = json.loads(str(z["messages"]))
+    for tag, msg in msgs.items():
+        with pytest.raises(O.OracleSelectionError) as exc:
+            O.validate_selection(z["idx_" + tag], c)
+        assert str(exc.value) == msg, tag
+
+
+def test_acceptance_sweep():
+    z = load("acceptance_sweep")
+    for n in range(int(z["count"])):
+        p = f"s{n}__"
+        c = O.cfg_of(**json.loads(str(z[p + "cfg"])))
+        seed = int(z[p + "seed"])
+        Q, K, V = O.make_qkv(c, seed)
+        idx = O.select_topk(O.make_scores(c, seed), c)
+        np.testing.assert_array_equal(idx, z[p + "idx"])
+        out, lse = O.selected_forward(Q, K, V, idx, c)
+        assert np.abs(out - z[p + "out"]).max() <= 1e-10
+        g = O.selected_backward(Q, K, V, idx, O.make_dout(c, seed), c)
+        for got, key in zip(g, ("dQ", "dK", "dV")):
+            assert np.abs(got - z[p + key]).max() <= 1e-9
