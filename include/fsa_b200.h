@@ -1,0 +1,166 @@
+/*
+ * fsa_b200.h -- C-ABI of the B200-native Flash Sparse Attention (NSA) operator path.
+ *
+ * The reference (`blockattn`, /root/reference/pkg/src/blockattn) exposes this
+ * path as Python operator functions over float64 numpy arrays; its only native
+ * boundary is the per-(head, block) Cython kernel set in `_kernels/_core.pyx`
+ * selected through `_kernels/__init__.py:13-56`.  That granularity is one task
+ * per call, far too fine for a GPU launch, so this ABI sits one level up: one
+ * entry point per reference *operator* (cited per function below).  The Python
+ * host layer (paper_2508_18224_b200/*.py) binds these with ctypes and mirrors
+ * the reference's names, argument order and exceptions.
+ *
+ * Conventions
+ *  - Plain C: raw device pointers, int64 sizes, a cudaStream_t passed as void*.
+ *  - The caller allocates every output and workspace; nothing here allocates.
+ *  - Every function returns FSA_OK (0) or an error code; fsa_last_error()
+ *    returns a thread-local message.  Launches are stream-ordered and
+ *    reentrant; there is no global mutable state besides that message.
+ *  - Storage layouts (row-major, last index contiguous).  The reference's
+ *    logical (token, feature, head) tensors are permuted views of these:
+ *      Q   [N][h][d_K]      K [N][h_K][d_K]     V [N][h_K][d_V]
+ *      out [N][h][d_V]      lse, m, l, delta [h][N]
+ *      scores [h_K][N][b]   idx [h_K][N][T] int32 (ascending, -1 padded)
+ *      obuf [h][N][T][d_V]  ml [h][N][T][2]     dq_buf [h][N][T][d_K]
+ *      inverse CSR: offsets [h_K][b+1] int32, qlist [h_K][N*T] int32 holding
+ *      t*T + slot, ascending t inside each block (selection.py:123-169).
+ *  - dtype: FSA_DT_F32 / FSA_DT_F64 / FSA_DT_BF16 for Q/K/V/dOut/out.  The
+ *    "accumulator" type is f64 for f64 inputs and f32 otherwise; lse/m/l/delta,
+ *    compressed KV, scores and gradients are stored in it.
+ */
+#ifndef FSA_B200_H
+#define FSA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FSA_OK 0
+#define FSA_ERR_INVALID 1
+#define FSA_ERR_CUDA 2
+#define FSA_ERR_UNSUPPORTED 3
+
+#define FSA_ABI_VERSION 1
+
+typedef enum { FSA_DT_F32 = 0, FSA_DT_F64 = 1, FSA_DT_BF16 = 2, FSA_DT_I32 = 3 } fsa_dtype;
+
+/* Resolved AttentionConfig (config.py:30-104); scale = 1/sqrt(d_K). */
+typedef struct fsa_shape {
+  int64_t N, d_K, d_V, h, h_K, B_K, T, W;
+  double scale;
+} fsa_shape;
+
+/* Selection-validation flag bits, in the reference's check order (selection.py:59-75). */
+#define FSA_SEL_EMPTY_ROW 1
+#define FSA_SEL_AFTER_SENTINEL 2
+#define FSA_SEL_OUT_OF_RANGE 4
+#define FSA_SEL_NON_CAUSAL 8
+#define FSA_SEL_DUPLICATE 16
+#define FSA_SEL_NOT_INCREASING 32
+
+/* Selected-forward modes (kv_major.py:105-204). */
+#define FSA_FWD_LOCAL 0  /* fused: per-block local (m_i,l_i) + O_i/l_i      */
+#define FSA_FWD_STATS 1  /* compute_softmax_stats partials only (kv_major.py:105-149)      */
+#define FSA_FWD_GLOBAL 2 /* block_pass_forward: exp(z - m_global) @ V_i (kv_major.py:152) */
+
+/* Merge modes (kv_major.py:207-242, :137-149). */
+#define FSA_MERGE_LOCAL 0  /* flash-decoding combine of LOCAL partials -> out, lse (+m,l) */
+#define FSA_MERGE_STATS 1  /* ascending-block (m,l) merge -> m, l (+ shared max)          */
+#define FSA_MERGE_REDUCE 2 /* sum of GLOBAL partials / l -> out, lse = m + log l           */
+
+const char* fsa_last_error(void);
+int fsa_abi_version(void);
+/* 0 when a compute-capability 10.x device is current, else an error code. */
+int fsa_device_check(void);
+
+/* Buffer dtypes the library will read/write for a given problem: obuf (LOCAL
+ * mode) and dq_buf.  bf16 problems on the tensor-core path use bf16 obuf. */
+int fsa_buffer_dtypes(const fsa_shape* s, int dtype, int* obuf_dtype, int* dqbuf_dtype);
+
+/* compress_kv (branches.py:34-44): block means K_cmp/V_cmp [b][h_K][d] and the
+ * running prefix means of the first min(B_K-1, N) rows [n_pref][h_K][d]; acc dtype. */
+int fsa_compress_kv(const fsa_shape* s, int dtype, const void* K, const void* V, void* K_cmp,
+                    void* V_cmp, void* K_prefix, void* V_prefix, void* stream);
+
+/* importance_scores_from_compressed (selection.py:105-120): scores [h_K][N][b]
+ * (acc dtype) = group mean of Q.K_cmp / sqrt(d_K) for every block. */
+int fsa_importance_scores(const fsa_shape* s, int dtype, const void* Q, const void* K_cmp,
+                          void* scores, void* stream);
+
+/* select_topk_blocks (selection.py:78-102): bit-exact own-block + top-(T-1),
+ * ties to the lower block index, -inf/NaN unselectable.  score_dtype F32 or F64. */
+int fsa_select_topk(const fsa_shape* s, int score_dtype, const void* scores, int32_t* idx,
+                    void* stream);
+
+/* validate_selection (selection.py:49-75): ORs FSA_SEL_* bits into *flags (device int32). */
+int fsa_validate_selection(const fsa_shape* s, const int32_t* idx, int32_t* flags, void* stream);
+
+/* build_inverse_index (selection.py:146-169) as CSR; flags as above (nullable). */
+size_t fsa_inverse_workspace_bytes(const fsa_shape* s);
+int fsa_build_inverse(const fsa_shape* s, const int32_t* idx, void* workspace, int32_t* offsets,
+                      int32_t* qlist, int32_t* flags, void* stream);
+
+/* FSA block pass (kv_major.py:105-204, _core.pyx:49-94): one task per
+ * (KV head, block) loads K_i/V_i once and serves all g query heads of the
+ * gathered rows.  m_global ([h][N], acc) only for FSA_FWD_GLOBAL. */
+int fsa_sel_fwd(const fsa_shape* s, int dtype, int mode, const void* Q, const void* K,
+                const void* V, const int32_t* offsets, const int32_t* qlist,
+                const void* m_global, void* obuf, int obuf_dtype, void* ml, void* stream);
+
+/* Merge of per-slot partials in ascending block order (kv_major.py:207-242;
+ * stats merge kv_major.py:137-149, shared max :141-146).  out in the input
+ * dtype, lse/m_out/l_out in acc dtype; m_out/l_out/lse nullable. */
+int fsa_merge_fwd(const fsa_shape* s, int dtype, int mode, const int32_t* idx, const void* obuf,
+                  int obuf_dtype, const void* ml, const void* m_global, const void* l_global,
+                  void* out, void* lse, void* m_out, void* l_out, int shared_max, void* stream);
+
+/* delta = sum_v out * dOut (kv_major.py:284); [h][N] acc. */
+int fsa_bwd_delta(const fsa_shape* s, int dtype, const void* out, const void* dOut, void* delta,
+                  void* stream);
+
+/* Selected backward tasks (kv_major.py:297-324, _core.pyx:97-131), one per
+ * (KV head, block): dq partial rows into dq_buf, dK/dV ([N][h_K][d], acc) as
+ * the single writer of the block (replaces the head sum at kv_major.py:342-354). */
+int fsa_sel_bwd(const fsa_shape* s, int dtype, const void* Q, const void* K, const void* V,
+                const void* dOut, const void* lse, const void* delta, const int32_t* offsets,
+                const int32_t* qlist, void* dq_buf, int dqbuf_dtype, void* dK, void* dV,
+                void* stream);
+
+/* dQ = ascending-block sum of dq partials (kv_major.py:326-340); [N][h][d_K] acc. */
+int fsa_dq_reduce(const fsa_shape* s, int dtype, const int32_t* idx, const void* dq_buf,
+                  int dqbuf_dtype, void* dQ, void* stream);
+
+/* compressed_attention_forward (branches.py:47-78); scores (nullable) receives
+ * importance_scores_from_compressed as a fused epilogue. */
+int fsa_cmp_attn_fwd(const fsa_shape* s, int dtype, const void* Q, const void* K_cmp,
+                     const void* V_cmp, const void* K_prefix, const void* V_prefix, void* out,
+                     void* lse, void* scores, void* stream);
+
+/* sliding_attention_forward (branches.py:81-83 -> oracle.py:39-44, :64-74). */
+int fsa_slide_fwd(const fsa_shape* s, int dtype, const void* Q, const void* K, const void* V,
+                  void* out, void* lse, void* stream);
+
+/* Band-mask dense_backward (oracle.py:102-131 with band_mask); grads acc dtype. */
+int fsa_slide_bwd(const fsa_shape* s, int dtype, const void* Q, const void* K, const void* V,
+                  const void* dOut, const void* lse, const void* delta, void* dQ, void* dK,
+                  void* dV, void* stream);
+
+/* gated_combine (branches.py:95-104): out = sum_c tau[t][c] * out_c; tau [N][3] acc. */
+int fsa_gated_combine(const fsa_shape* s, int dtype, const void* out_cmp, const void* out_sel,
+                      const void* out_slide, const void* tau, void* out, void* stream);
+
+/* Gate backward into branch c: out = tau[t][c] * dOut (branches.py:103); [N][h][d_V]. */
+int fsa_gate_scale(const fsa_shape* s, int dtype, const void* dOut, const void* tau, int col,
+                   void* out, void* stream);
+
+/* Finiteness check for as_headed (config.py:146-155): *flag |= 1 on any non-finite. */
+int fsa_check_finite(int dtype, const void* x, int64_t n, int32_t* flag, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FSA_B200_H */

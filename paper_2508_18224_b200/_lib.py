@@ -1,0 +1,153 @@
+"""ctypes binding of libfsa_b200.so (include/fsa_b200.h).
+
+The shared library is built in-tree by ``python -m paper_2508_18224_b200.build``
+(or ``__graft_entry__.build()``).  There is no fallback: if the library is
+missing or no CUDA device is present, every operator raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfsa_b200.so")
+
+FSA_OK, FSA_ERR_INVALID, FSA_ERR_CUDA, FSA_ERR_UNSUPPORTED = 0, 1, 2, 3
+DT_F32, DT_F64, DT_BF16, DT_I32 = 0, 1, 2, 3
+FWD_LOCAL, FWD_STATS, FWD_GLOBAL = 0, 1, 2
+MERGE_LOCAL, MERGE_STATS, MERGE_REDUCE = 0, 1, 2
+
+SEL_FLAGS = (  # bit, message -- in the reference's check order (selection.py:59-75)
+    (1, "malformed selection: empty row"),
+    (2, "malformed selection: entry after sentinel"),
+    (4, "malformed selection: block index out of range"),
+    (8, "malformed selection: non-causal entry"),
+    (16, "malformed selection: duplicate entry"),
+    (32, "malformed selection: not strictly increasing"),
+)
+
+
+class FsaShape(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in ("N", "d_K", "d_V", "h", "h_K", "B_K", "T", "W")] + [
+        ("scale", ctypes.c_double)]
+
+
+_vp, _i, _i64, _sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_size_t
+_sp = ctypes.POINTER(FsaShape)
+_ip = ctypes.POINTER(ctypes.c_int)
+
+# symbol -> argtypes (restype int unless noted); must match include/fsa_b200.h
+SIGNATURES = {
+    "fsa_last_error": ([], ctypes.c_char_p),
+    "fsa_abi_version": ([], _i),
+    "fsa_device_check": ([], _i),
+    "fsa_buffer_dtypes": ([_sp, _i, _ip, _ip], _i),
+    "fsa_compress_kv": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
+    "fsa_importance_scores": ([_sp, _i, _vp, _vp, _vp, _vp], _i),
+    "fsa_select_topk": ([_sp, _i, _vp, _vp, _vp], _i),
+    "fsa_validate_selection": ([_sp, _vp, _vp, _vp], _i),
+    "fsa_inverse_workspace_bytes": ([_sp], _sz),
+    "fsa_build_inverse": ([_sp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
+    "fsa_sel_fwd": ([_sp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp], _i),
+    "fsa_merge_fwd": ([_sp, _i, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp], _i),
+    "fsa_bwd_delta": ([_sp, _i, _vp, _vp, _vp, _vp], _i),
+    "fsa_sel_bwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp], _i),
+    "fsa_dq_reduce": ([_sp, _i, _vp, _vp, _i, _vp, _vp], _i),
+    "fsa_cmp_attn_fwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
+    "fsa_slide_fwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp], _i),
+    "fsa_slide_bwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
+    "fsa_gated_combine": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp], _i),
+    "fsa_gate_scale": ([_sp, _i, _vp, _vp, _i, _vp, _vp], _i),
+    "fsa_check_finite": ([_i, _vp, _i64, _vp, _vp], _i),
+}
+
+
+class FsaError(RuntimeError):
+    """A CUDA-side failure reported through the C-ABI."""
+
+
+_lib = None
+
+
+def lib():
+    """Load the library once; raise loudly when it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is not built; run `python -m paper_2508_18224_b200.build` "
+                "(the FSA operators have no CPU fallback)")
+        l = ctypes.CDLL(LIB_PATH)
+        for name, (args, res) in SIGNATURES.items():
+            fn = getattr(l, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = l
+    return _lib
+
+
+def last_error() -> str:
+    return lib().fsa_last_error().decode(errors="replace")
+
+
+def call(name, *args):
+    rc = getattr(lib(), name)(*args)
+    if rc != FSA_OK:
+        msg = last_error()
+        if rc == FSA_ERR_INVALID:
+            raise ValueError(f"{name}: {msg}")
+        raise FsaError(f"{name}: {msg}")
+    return rc
+
+
+_checked_devices = set()
+
+
+def require_device():
+    """The operators only run on a CUDA (sm_100a) device."""
+    if not torch.cuda.is_available():
+        raise RuntimeError("the FSA B200 operators need a CUDA device (no CPU fallback)")
+    dev = torch.cuda.current_device()
+    if dev not in _checked_devices:
+        call("fsa_device_check")
+        _checked_devices.add(dev)
+    return torch.device("cuda", dev)
+
+
+def shape_of(cfg) -> FsaShape:
+    return FsaShape(cfg.N, cfg.d_K, cfg.d_V, cfg.h, cfg.h_K, cfg.B_K, cfg.T, cfg.W, cfg.scale)
+
+
+def ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def dt_code(dtype) -> int:
+    if dtype == torch.float32:
+        return DT_F32
+    if dtype == torch.float64:
+        return DT_F64
+    if dtype == torch.bfloat16:
+        return DT_BF16
+    raise ValueError(f"unsupported dtype {dtype} (float32, float64 or bfloat16)")
+
+
+def acc_dtype(dtype):
+    return torch.float64 if dtype == torch.float64 else torch.float32
+
+
+_TORCH_OF = {DT_F32: torch.float32, DT_F64: torch.float64, DT_BF16: torch.bfloat16}
+
+
+def buffer_dtypes(cfg, dtype):
+    s = shape_of(cfg)
+    ob, dq = ctypes.c_int(), ctypes.c_int()
+    call("fsa_buffer_dtypes", ctypes.byref(s), dt_code(dtype), ctypes.byref(ob), ctypes.byref(dq))
+    return (ob.value, _TORCH_OF[ob.value]), (dq.value, _TORCH_OF[dq.value])

@@ -1,0 +1,221 @@
+// KV compression (K1), importance scores (generic), gated combine (K12),
+// finiteness check.  HBM-bound kernels; see DESIGN.md for their byte counts.
+#include "common.cuh"
+
+namespace fsa {
+
+// ---------------------------------------------------------------------------
+// K1 compress_kv: branches.py:34-44.  One CTA per (block i, kv head); threads
+// over features.  Block means in the accumulator type.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void compress_kernel(const T* __restrict__ X, typename Acc<T>::type* __restrict__ Xc,
+                                int64_t B_K, int64_t h_K, int64_t d) {
+  using A = typename Acc<T>::type;
+  const int64_t i = blockIdx.x, kh = blockIdx.y;
+  const A inv = A(1) / A(B_K);
+  for (int64_t c = threadIdx.x; c < d; c += blockDim.x) {
+    A acc = 0;
+    const T* p = X + ((i * B_K) * h_K + kh) * d + c;
+    for (int64_t r = 0; r < B_K; ++r) acc += to_acc(p[r * h_K * d]);
+    Xc[(i * h_K + kh) * d + c] = acc * inv;
+  }
+}
+
+// running prefix means of rows 0..t, t < n_pref (branches.py:40-43)
+template <typename T>
+__global__ void prefix_kernel(const T* __restrict__ X, typename Acc<T>::type* __restrict__ Xp,
+                              int64_t n_pref, int64_t h_K, int64_t d) {
+  using A = typename Acc<T>::type;
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= h_K * d) return;
+  A acc = 0;
+  for (int64_t t = 0; t < n_pref; ++t) {
+    acc += to_acc(X[t * h_K * d + idx]);
+    Xp[t * h_K * d + idx] = acc / A(t + 1);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// importance scores: selection.py:105-120.  CTA = 32 tokens of one kv head x
+// all b blocks (chunks of 64 blocks staged in smem).
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void scores_kernel(const T* __restrict__ Q, const typename Acc<T>::type* __restrict__ Kc,
+                              typename Acc<T>::type* __restrict__ S, fsa_shape s, int64_t b) {
+  using A = typename Acc<T>::type;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  A* qs = reinterpret_cast<A*>(smem_raw);          // [32][d+1]
+  const int64_t d = s.d_K, dp = d + 1;
+  A* ks = qs + 32 * dp;                             // [64][d+1]
+  const int64_t kh = blockIdx.y, t0 = blockIdx.x * 32;
+  const int64_t g = s.h / s.h_K;
+  for (int64_t e = threadIdx.x; e < 32 * d; e += blockDim.x) {
+    int64_t r = e / d, c = e % d, t = t0 + r;
+    A acc = 0;
+    if (t < s.N)
+      for (int64_t hh = 0; hh < g; ++hh) acc += to_acc(Q[(t * s.h + kh * g + hh) * d + c]);
+    qs[r * dp + c] = acc;
+  }
+  const A mul = A(s.scale) / A(g);
+  for (int64_t i0 = 0; i0 < b; i0 += 64) {
+    __syncthreads();
+    for (int64_t e = threadIdx.x; e < 64 * d; e += blockDim.x) {
+      int64_t r = e / d, c = e % d;
+      ks[r * dp + c] = (i0 + r < b) ? Kc[((i0 + r) * s.h_K + kh) * d + c] : A(0);
+    }
+    __syncthreads();
+    const int col = threadIdx.x % 64;
+    for (int r = threadIdx.x / 64; r < 32; r += blockDim.x / 64) {
+      int64_t t = t0 + r, i = i0 + col;
+      if (t >= s.N || i >= b) continue;
+      A acc = 0;
+      for (int64_t c = 0; c < d; ++c) acc += qs[r * dp + c] * ks[col * dp + c];
+      S[(kh * s.N + t) * b + i] = acc * mul;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K12 gated combine: branches.py:95-104 (sum order ((0 + t0*a) + t1*b) + t2*c).
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void combine_kernel(const T* __restrict__ a, const T* __restrict__ bsel,
+                               const T* __restrict__ c, const typename Acc<T>::type* __restrict__ tau,
+                               T* __restrict__ out, int64_t N, int64_t row) {
+  using A = typename Acc<T>::type;
+  const int64_t total = N * row;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = e / row;
+    A acc = A(0) + tau[t * 3 + 0] * to_acc(a[e]);
+    acc = acc + tau[t * 3 + 1] * to_acc(bsel[e]);
+    acc = acc + tau[t * 3 + 2] * to_acc(c[e]);
+    out[e] = from_acc<T>(acc);
+  }
+}
+
+// dOut_c = tau[:, c] * dOut (gate backward into one branch, branches.py:103)
+template <typename T>
+__global__ void gate_scale_kernel(const T* __restrict__ d, const typename Acc<T>::type* __restrict__ tau,
+                                  int col, T* __restrict__ out, int64_t N, int64_t row) {
+  const int64_t total = N * row;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x)
+    out[e] = from_acc<T>(tau[(e / row) * 3 + col] * to_acc(d[e]));
+}
+
+template <typename T>
+__global__ void finite_kernel(const T* __restrict__ x, int64_t n, int32_t* flag) {
+  int bad = 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    bad |= !isfinite((double)to_acc(x[e]));
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+template <typename T>
+int compress_impl(const fsa_shape* s, const void* K, const void* V, void* Kc, void* Vc, void* Kp,
+                  void* Vp, cudaStream_t st) {
+  using A = typename Acc<T>::type;
+  const int64_t b = s->N / s->B_K, n_pref = s->B_K - 1 < s->N ? s->B_K - 1 : s->N;
+  dim3 grid((unsigned)b, (unsigned)s->h_K);
+  compress_kernel<T><<<grid, 128, 0, st>>>((const T*)K, (A*)Kc, s->B_K, s->h_K, s->d_K);
+  compress_kernel<T><<<grid, 128, 0, st>>>((const T*)V, (A*)Vc, s->B_K, s->h_K, s->d_V);
+  if (n_pref > 0) {
+    prefix_kernel<T><<<(unsigned)((s->h_K * s->d_K + 127) / 128), 128, 0, st>>>(
+        (const T*)K, (A*)Kp, n_pref, s->h_K, s->d_K);
+    prefix_kernel<T><<<(unsigned)((s->h_K * s->d_V + 127) / 128), 128, 0, st>>>(
+        (const T*)V, (A*)Vp, n_pref, s->h_K, s->d_V);
+  }
+  FSA_LAUNCH_CHECK("compress_kv");
+  return FSA_OK;
+}
+
+template <typename T>
+int scores_impl(const fsa_shape* s, const void* Q, const void* Kc, void* S, cudaStream_t st) {
+  using A = typename Acc<T>::type;
+  const int64_t b = s->N / s->B_K;
+  size_t smem = (size_t)(32 + 64) * (s->d_K + 1) * sizeof(A);
+  FSA_REQUIRE(smem <= 200 * 1024, "importance scores: d_K=%lld too large", (long long)s->d_K);
+  cudaFuncSetAttribute(scores_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  dim3 grid((unsigned)((s->N + 31) / 32), (unsigned)s->h_K);
+  scores_kernel<T><<<grid, 256, smem, st>>>((const T*)Q, (const A*)Kc, (A*)S, *s, b);
+  FSA_LAUNCH_CHECK("importance_scores");
+  return FSA_OK;
+}
+
+template <typename T>
+int combine_impl(const fsa_shape* s, const void* a, const void* b, const void* c, const void* tau,
+                 void* out, cudaStream_t st) {
+  using A = typename Acc<T>::type;
+  const int64_t row = s->h * s->d_V, total = s->N * row;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  combine_kernel<T><<<(unsigned)blocks, 256, 0, st>>>((const T*)a, (const T*)b, (const T*)c,
+                                                     (const A*)tau, (T*)out, s->N, row);
+  FSA_LAUNCH_CHECK("gated_combine");
+  return FSA_OK;
+}
+
+template <typename T>
+int gate_scale_impl(const fsa_shape* s, const void* d, const void* tau, int col, void* out,
+                    cudaStream_t st) {
+  using A = typename Acc<T>::type;
+  const int64_t row = s->h * s->d_V, total = s->N * row;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  gate_scale_kernel<T><<<(unsigned)blocks, 256, 0, st>>>((const T*)d, (const A*)tau, col, (T*)out,
+                                                        s->N, row);
+  FSA_LAUNCH_CHECK("gate_scale");
+  return FSA_OK;
+}
+
+template <typename T>
+int finite_impl(const void* x, int64_t n, int32_t* flag, cudaStream_t st) {
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks < 1) blocks = 1;
+  finite_kernel<T><<<(unsigned)blocks, 256, 0, st>>>((const T*)x, n, flag);
+  FSA_LAUNCH_CHECK("check_finite");
+  return FSA_OK;
+}
+
+}  // namespace fsa
+
+#define DISPATCH_DT(dt, FN, ...)                                            \
+  switch (dt) {                                                             \
+    case FSA_DT_F32: return fsa::FN<float>(__VA_ARGS__);                    \
+    case FSA_DT_F64: return fsa::FN<double>(__VA_ARGS__);                   \
+    case FSA_DT_BF16: return fsa::FN<__nv_bfloat16>(__VA_ARGS__);           \
+    default: fsa::set_error("unsupported dtype %d", (int)dt); return FSA_ERR_INVALID; \
+  }
+
+extern "C" int fsa_compress_kv(const fsa_shape* s, int dtype, const void* K, const void* V,
+                               void* K_cmp, void* V_cmp, void* K_prefix, void* V_prefix,
+                               void* stream) {
+  DISPATCH_DT(dtype, compress_impl, s, K, V, K_cmp, V_cmp, K_prefix, V_prefix, (cudaStream_t)stream);
+}
+
+extern "C" int fsa_importance_scores(const fsa_shape* s, int dtype, const void* Q, const void* K_cmp,
+                                     void* scores, void* stream) {
+  DISPATCH_DT(dtype, scores_impl, s, Q, K_cmp, scores, (cudaStream_t)stream);
+}
+
+extern "C" int fsa_gated_combine(const fsa_shape* s, int dtype, const void* out_cmp,
+                                 const void* out_sel, const void* out_slide, const void* tau,
+                                 void* out, void* stream) {
+  DISPATCH_DT(dtype, combine_impl, s, out_cmp, out_sel, out_slide, tau, out, (cudaStream_t)stream);
+}
+
+extern "C" int fsa_gate_scale(const fsa_shape* s, int dtype, const void* dOut, const void* tau,
+                              int col, void* out, void* stream) {
+  DISPATCH_DT(dtype, gate_scale_impl, s, dOut, tau, col, out, (cudaStream_t)stream);
+}
+
+extern "C" int fsa_check_finite(int dtype, const void* x, int64_t n, int32_t* flag, void* stream) {
+  if (n == 0) return FSA_OK;
+  DISPATCH_DT(dtype, finite_impl, x, n, flag, (cudaStream_t)stream);
+}

@@ -1,0 +1,213 @@
+// K4 build_inverse_index (selection.py:146-169) as a deterministic, stable
+// counting sort -- no atomics decide any order.
+//
+//   count   : per (kv head, 256-token tile) histogram over blocks, with the
+//             selection validity flags (selection.py:49-75) fused in;
+//   scan    : per (kv head, block) exclusive scan over tiles -> tile bases;
+//   offsets : per kv head exclusive scan over blocks -> CSR offsets;
+//   scatter : each (token, slot) entry lands at
+//             offsets[e] + tile_base[tile][e] + rank-within-tile,
+//             where the in-tile rank is computed in token order (warps take
+//             turns; lanes of a warp rank through a shared-memory lane mask).
+// Queries inside each block therefore come out in ascending token order, the
+// reference's canonical order, independent of scheduling.
+#include "common.cuh"
+
+namespace fsa {
+
+constexpr int kInvTile = 256;  // tokens per CTA (8 warps x 32)
+
+__device__ __forceinline__ bool live_entry(int e, int64_t own) { return e >= 0 && e <= own; }
+
+__device__ __forceinline__ int row_flags(const int32_t* r, int T, int64_t own, int64_t b) {
+  int f = 0;
+  int prev = r[0];
+  bool prev_live = prev != -1;
+  if (!prev_live) f |= FSA_SEL_EMPTY_ROW;
+  if ((prev < 0 && prev != -1) || prev >= b) f |= FSA_SEL_OUT_OF_RANGE;
+  if (prev_live && prev > own) f |= FSA_SEL_NON_CAUSAL;
+  for (int k = 1; k < T; ++k) {
+    const int v = r[k];
+    const bool live = v != -1;
+    if (live && !prev_live) f |= FSA_SEL_AFTER_SENTINEL;
+    if ((v < 0 && v != -1) || v >= b) f |= FSA_SEL_OUT_OF_RANGE;
+    if (live && v > own) f |= FSA_SEL_NON_CAUSAL;
+    if (live && prev_live) {
+      if (v == prev) f |= FSA_SEL_DUPLICATE;
+      if (v < prev) f |= FSA_SEL_NOT_INCREASING;
+    }
+    prev = v;
+    prev_live = live;
+  }
+  return f;
+}
+
+// kScatter = false: histogram + flags.  kScatter = true: write qlist.
+template <bool kScatter>
+__global__ void __launch_bounds__(kInvTile)
+inverse_tile_kernel(const int32_t* __restrict__ idx, int64_t N, int64_t B_K, int64_t b, int T,
+                    int32_t* __restrict__ hist, const int32_t* __restrict__ offsets,
+                    int32_t* __restrict__ qlist, int32_t* flags) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* mask = reinterpret_cast<uint32_t*>(smem_raw);  // [b]
+  int32_t* cnt = reinterpret_cast<int32_t*>(mask + b);     // [b]
+  const int64_t kh = blockIdx.y, tile = blockIdx.x, n_tiles = gridDim.x;
+  const int64_t t0 = tile * kInvTile;
+  for (int64_t e = threadIdx.x; e < b; e += blockDim.x) {
+    mask[e] = 0;
+    cnt[e] = 0;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t t = t0 + threadIdx.x;
+  const bool has_row = t < N;
+  const int64_t own = has_row ? t / B_K : -1;
+  const int32_t* row = idx + (kh * N + (has_row ? t : 0)) * T;
+  if (!kScatter && flags) {
+    int f = has_row ? row_flags(row, T, own, b) : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) f |= __shfl_xor_sync(0xffffffffu, f, o);
+    if (lane == 0 && f) atomicOr(flags, f);
+  }
+  const unsigned lt = lanemask_lt();
+  int32_t* ql = kScatter ? qlist + kh * N * T : nullptr;
+  const int32_t* off = kScatter ? offsets + kh * (b + 1) : nullptr;
+  const int32_t* base = kScatter ? hist + (kh * n_tiles + tile) * b : nullptr;
+  __syncthreads();
+  for (int w = 0; w < kInvTile / 32; ++w) {
+    if (warp == w && has_row) {
+      const unsigned me = 1u << lane;
+      for (int s = 0; s < T; ++s) {
+        const int e = row[s];
+        if (live_entry(e, own)) atomicOr(&mask[e], me);
+      }
+    }
+    __syncwarp();
+    if (warp == w && has_row && kScatter) {
+      for (int s = 0; s < T; ++s) {
+        const int e = row[s];
+        if (!live_entry(e, own)) continue;
+        const int rank = cnt[e] + __popc(mask[e] & lt);
+        ql[off[e] + base[e] + rank] = (int32_t)(t * T + s);
+      }
+    }
+    __syncwarp();
+    if (warp == w && has_row) {  // the lowest lane owning e publishes the warp's count
+      for (int s = 0; s < T; ++s) {
+        const int e = row[s];
+        if (!live_entry(e, own)) continue;
+        const uint32_t m = mask[e];
+        if (lane == __ffs(m) - 1) cnt[e] += __popc(m);
+      }
+    }
+    __syncwarp();
+    if (warp == w && has_row) {
+      for (int s = 0; s < T; ++s) {
+        const int e = row[s];
+        if (live_entry(e, own)) mask[e] = 0;
+      }
+    }
+    __syncthreads();
+  }
+  if (!kScatter) {
+    int32_t* h = hist + (kh * n_tiles + tile) * b;
+    for (int64_t e = threadIdx.x; e < b; e += blockDim.x) h[e] = cnt[e];
+  }
+}
+
+// per (kh, block): exclusive scan over tiles, totals into offsets[kh][e+1]
+__global__ void inverse_scan_tiles_kernel(int32_t* __restrict__ hist, int32_t* __restrict__ offsets,
+                                          int64_t h_K, int64_t n_tiles, int64_t b) {
+  const int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (id >= h_K * b) return;
+  const int64_t kh = id / b, e = id % b;
+  int32_t* h = hist + kh * n_tiles * b + e;
+  int32_t run = 0;
+  int64_t tile = 0;
+  for (; tile + 4 <= n_tiles; tile += 4) {
+    int32_t v0 = h[(tile + 0) * b], v1 = h[(tile + 1) * b], v2 = h[(tile + 2) * b],
+            v3 = h[(tile + 3) * b];
+    h[(tile + 0) * b] = run; run += v0;
+    h[(tile + 1) * b] = run; run += v1;
+    h[(tile + 2) * b] = run; run += v2;
+    h[(tile + 3) * b] = run; run += v3;
+  }
+  for (; tile < n_tiles; ++tile) {
+    int32_t v = h[tile * b];
+    h[tile * b] = run;
+    run += v;
+  }
+  offsets[kh * (b + 1) + e + 1] = run;
+}
+
+// per kh: inclusive scan of offsets[kh][1..b]; offsets[kh][0] = 0
+__global__ void inverse_scan_blocks_kernel(int32_t* __restrict__ offsets, int64_t b) {
+  __shared__ int32_t warp_tot[32];
+  __shared__ int32_t carry_s;
+  int32_t* o = offsets + blockIdx.x * (b + 1);
+  if (threadIdx.x == 0) {
+    o[0] = 0;
+    carry_s = 0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int64_t c0 = 0; c0 < b; c0 += blockDim.x) {
+    const int64_t e = c0 + threadIdx.x;
+    int32_t v = (e < b) ? o[e + 1] : 0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      int32_t u = __shfl_up_sync(0xffffffffu, v, d);
+      if (lane >= d) v += u;
+    }
+    if (lane == 31) warp_tot[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+      int32_t w = lane < nw ? warp_tot[lane] : 0;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        int32_t u = __shfl_up_sync(0xffffffffu, w, d);
+        if (lane >= d) w += u;
+      }
+      if (lane < nw) warp_tot[lane] = w;
+    }
+    __syncthreads();
+    const int32_t carry = carry_s;
+    const int32_t prefix = (warp > 0 ? warp_tot[warp - 1] : 0) + carry;
+    if (e < b) o[e + 1] = v + prefix;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry_s = v + prefix;
+    __syncthreads();
+  }
+}
+
+}  // namespace fsa
+
+static int64_t n_tiles_of(const fsa_shape* s) { return (s->N + fsa::kInvTile - 1) / fsa::kInvTile; }
+
+extern "C" size_t fsa_inverse_workspace_bytes(const fsa_shape* s) {
+  const int64_t b = s->N / s->B_K;
+  return (size_t)(s->h_K * n_tiles_of(s) * b) * sizeof(int32_t);
+}
+
+extern "C" int fsa_build_inverse(const fsa_shape* s, const int32_t* idx, void* workspace,
+                                 int32_t* offsets, int32_t* qlist, int32_t* flags, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t b = s->N / s->B_K, nt = n_tiles_of(s);
+  if (s->N == 0) return FSA_OK;
+  size_t smem = (size_t)b * 8;
+  FSA_REQUIRE(smem <= 200 * 1024, "build_inverse: b=%lld too large", (long long)b);
+  int32_t* hist = (int32_t*)workspace;
+  cudaFuncSetAttribute(fsa::inverse_tile_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  cudaFuncSetAttribute(fsa::inverse_tile_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  dim3 grid((unsigned)nt, (unsigned)s->h_K);
+  fsa::inverse_tile_kernel<false><<<grid, fsa::kInvTile, smem, st>>>(idx, s->N, s->B_K, b, (int)s->T,
+                                                                     hist, nullptr, nullptr, flags);
+  fsa::inverse_scan_tiles_kernel<<<(unsigned)((s->h_K * b + 255) / 256), 256, 0, st>>>(
+      hist, offsets, s->h_K, nt, b);
+  fsa::inverse_scan_blocks_kernel<<<(unsigned)s->h_K, 1024, 0, st>>>(offsets, b);
+  fsa::inverse_tile_kernel<true><<<grid, fsa::kInvTile, smem, st>>>(idx, s->N, s->B_K, b, (int)s->T,
+                                                                    hist, offsets, qlist, nullptr);
+  FSA_LAUNCH_CHECK("build_inverse");
+  return FSA_OK;
+}

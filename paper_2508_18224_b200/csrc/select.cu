@@ -1,0 +1,233 @@
+// K3 top-k block selection (selection.py:78-102) and selection validation
+// (selection.py:49-75).  Integer output, bit-exact with the reference:
+//   * only causal blocks i <= t // B_K compete; the own block scores +inf;
+//   * order = (score desc, block index asc); -inf and NaN are never selected;
+//     -0.0 ties +0.0; a non-own +inf ties the own block and wins on index;
+//   * output ascending, -1 padded.
+// Scores are compared through a monotone integer key, so the comparison is
+// exact for f32 and f64 inputs alike.
+#include "common.cuh"
+
+namespace fsa {
+
+struct SelKey {
+  uint64_t sk;  // 0 = not selectable; larger = better
+  uint32_t ix;  // block index; smaller wins ties
+};
+
+__device__ __forceinline__ uint64_t score_key(float f) {
+  if (isnan(f) || f == -INFINITY) return 0;
+  if (f == 0.0f) f = 0.0f;  // canonicalise -0.0
+  uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? (uint64_t)(~u) : (uint64_t)(u | 0x80000000u);
+}
+__device__ __forceinline__ uint64_t score_key(double f) {
+  if (isnan(f) || f == -(double)INFINITY) return 0;
+  if (f == 0.0) f = 0.0;
+  uint64_t u = (uint64_t)__double_as_longlong(f);
+  return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+}
+template <typename S> __device__ __forceinline__ uint64_t own_key() {
+  return score_key((S)INFINITY);
+}
+
+__device__ __forceinline__ bool better(uint64_t ask, uint32_t aix, uint64_t bsk, uint32_t bix) {
+  return ask > bsk || (ask == bsk && aix < bix);
+}
+
+__device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
+  return __shfl_sync(0xffffffffu, v, src);
+}
+
+// One warp per (kh, t) row, T <= 32.  Lane k holds the k-th best candidate;
+// candidates stream in 32 at a time and only those beating the current T-th
+// best are inserted (a handful per row after the first chunk).
+template <typename S>
+__global__ void topk_warp_kernel(const S* __restrict__ scores, int32_t* __restrict__ idx,
+                                 int64_t rows, int64_t N, int64_t B_K, int64_t b, int T) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int64_t t = row % N;
+  const int64_t own = t / B_K, ncand = own + 1;
+  const S* sr = scores + row * b;
+  uint64_t hsk = 0;
+  uint32_t hix = 0xffffffffu;
+  const uint64_t okey = own_key<S>();
+  for (int64_t base = 0; base < ncand; base += 32) {
+    const int64_t c = base + lane;
+    uint64_t csk = 0;
+    if (c < ncand) csk = (c == own) ? okey : score_key(sr[c]);
+    const uint32_t cix = (uint32_t)c;
+    uint64_t tsk = shfl64(hsk, T - 1);
+    uint32_t tix = __shfl_sync(0xffffffffu, hix, T - 1);
+    unsigned mask = __ballot_sync(0xffffffffu, csk != 0 && better(csk, cix, tsk, tix));
+    while (mask) {
+      const int src = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const uint64_t isk = shfl64(csk, src);
+      const uint32_t iix = __shfl_sync(0xffffffffu, cix, src);
+      tsk = shfl64(hsk, T - 1);
+      tix = __shfl_sync(0xffffffffu, hix, T - 1);
+      if (!better(isk, iix, tsk, tix)) continue;  // warp-uniform
+      const bool bt = lane < T && better(isk, iix, hsk, hix);
+      const uint64_t psk = __shfl_up_sync(0xffffffffu, hsk, 1);
+      const uint32_t pix = __shfl_up_sync(0xffffffffu, hix, 1);
+      const bool pbt = __shfl_up_sync(0xffffffffu, (int)bt, 1) && lane > 0;
+      if (bt) {
+        hsk = pbt ? psk : isk;
+        hix = pbt ? pix : iix;
+      }
+    }
+  }
+  // ascending block order, sentinels last: bitonic sort across the warp
+  int v = (lane < T && hsk != 0) ? (int)hix : 0x7fffffff;
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const int p = __shfl_xor_sync(0xffffffffu, v, j);
+      const bool up = (lane & k) == 0;
+      const bool lo = (lane & j) == 0;
+      v = (lo == up) ? min(v, p) : max(v, p);
+    }
+  }
+  if (lane < T) idx[row * T + lane] = (v == 0x7fffffff) ? -1 : v;
+}
+
+// One CTA per row for T > 32: bitonic sort of all causal candidates in smem.
+template <typename S>
+__global__ void topk_block_kernel(const S* __restrict__ scores, int32_t* __restrict__ idx,
+                                  int64_t N, int64_t B_K, int64_t b, int T, int P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t* ksk = reinterpret_cast<uint64_t*>(smem_raw);
+  uint32_t* kix = reinterpret_cast<uint32_t*>(ksk + P);
+  const int64_t row = blockIdx.x;
+  const int64_t t = row % N, own = t / B_K, ncand = own + 1;
+  const S* sr = scores + row * b;
+  const uint64_t okey = own_key<S>();
+  for (int k = threadIdx.x; k < P; k += blockDim.x) {
+    ksk[k] = (k < ncand) ? (k == own ? okey : score_key(sr[k])) : 0;
+    kix[k] = (uint32_t)k;
+  }
+  __syncthreads();
+  // sort descending under better()
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          const bool desc = (i & k) == 0;
+          const bool sw = desc ? better(ksk[l], kix[l], ksk[i], kix[i])
+                               : better(ksk[i], kix[i], ksk[l], kix[l]);
+          if (sw) {
+            uint64_t a = ksk[i]; ksk[i] = ksk[l]; ksk[l] = a;
+            uint32_t c = kix[i]; kix[i] = kix[l]; kix[l] = c;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // keep the first T selectable entries, then sort those by index ascending
+  int P2 = 1;
+  while (P2 < T) P2 <<= 1;
+  uint32_t* v = kix + P;  // reuse: [P2]
+  for (int k = threadIdx.x; k < P2; k += blockDim.x)
+    v[k] = (k < T && k < P && ksk[k] != 0) ? kix[k] : 0x7fffffffu;
+  __syncthreads();
+  for (int k = 2; k <= P2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < P2; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          const bool asc = (i & k) == 0;
+          if ((v[i] > v[l]) == asc) {
+            uint32_t a = v[i]; v[i] = v[l]; v[l] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int k = threadIdx.x; k < T; k += blockDim.x)
+    idx[row * T + k] = (v[k] == 0x7fffffffu) ? -1 : (int32_t)v[k];
+}
+
+// validate_selection: one thread per row; flags OR-reduced per warp.
+__global__ void validate_kernel(const int32_t* __restrict__ idx, int64_t rows, int64_t N,
+                                int64_t B_K, int64_t b, int T, int32_t* flags) {
+  const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int f = 0;
+  if (row < rows) {
+    const int64_t own = (row % N) / B_K;
+    const int32_t* r = idx + row * T;
+    int prev = r[0];
+    bool prev_live = prev != -1;
+    if (!prev_live) f |= FSA_SEL_EMPTY_ROW;
+    if ((prev < 0 && prev != -1) || prev >= b) f |= FSA_SEL_OUT_OF_RANGE;
+    if (prev_live && prev > own) f |= FSA_SEL_NON_CAUSAL;
+    for (int k = 1; k < T; ++k) {
+      const int v = r[k];
+      const bool live = v != -1;
+      if (live && !prev_live) f |= FSA_SEL_AFTER_SENTINEL;
+      if ((v < 0 && v != -1) || v >= b) f |= FSA_SEL_OUT_OF_RANGE;
+      if (live && v > own) f |= FSA_SEL_NON_CAUSAL;
+      if (live && prev_live) {
+        if (v == prev) f |= FSA_SEL_DUPLICATE;
+        if (v < prev) f |= FSA_SEL_NOT_INCREASING;
+      }
+      prev = v;
+      prev_live = live;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) f |= __shfl_xor_sync(0xffffffffu, f, o);
+  if ((threadIdx.x & 31) == 0 && f) atomicOr(flags, f);
+}
+
+template <typename S>
+int topk_impl(const fsa_shape* s, const void* scores, int32_t* idx, cudaStream_t st) {
+  const int64_t b = s->N / s->B_K, rows = s->h_K * s->N;
+  const int T = (int)s->T;
+  if (rows == 0) return FSA_OK;
+  if (T <= 32) {
+    const int warps = 8;
+    topk_warp_kernel<S><<<(unsigned)((rows + warps - 1) / warps), warps * 32, 0, st>>>(
+        (const S*)scores, idx, rows, s->N, s->B_K, b, T);
+  } else {
+    int P = 1;
+    while (P < b) P <<= 1;
+    int P2 = 1;
+    while (P2 < T) P2 <<= 1;
+    size_t smem = (size_t)P * 12 + (size_t)P2 * 4;
+    FSA_REQUIRE(smem <= 200 * 1024, "select_topk: b=%lld too large for T>32 path", (long long)b);
+    cudaFuncSetAttribute(topk_block_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    topk_block_kernel<S><<<(unsigned)rows, 256, smem, st>>>((const S*)scores, idx, s->N, s->B_K,
+                                                            b, T, P);
+  }
+  FSA_LAUNCH_CHECK("select_topk");
+  return FSA_OK;
+}
+
+}  // namespace fsa
+
+extern "C" int fsa_select_topk(const fsa_shape* s, int score_dtype, const void* scores,
+                               int32_t* idx, void* stream) {
+  switch (score_dtype) {
+    case FSA_DT_F32: return fsa::topk_impl<float>(s, scores, idx, (cudaStream_t)stream);
+    case FSA_DT_F64: return fsa::topk_impl<double>(s, scores, idx, (cudaStream_t)stream);
+    default: fsa::set_error("select_topk: scores must be f32 or f64"); return FSA_ERR_INVALID;
+  }
+}
+
+extern "C" int fsa_validate_selection(const fsa_shape* s, const int32_t* idx, int32_t* flags,
+                                      void* stream) {
+  const int64_t rows = s->h_K * s->N;
+  if (rows == 0) return FSA_OK;
+  fsa::validate_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      idx, rows, s->N, s->B_K, s->N / s->B_K, (int)s->T, flags);
+  FSA_LAUNCH_CHECK("validate_selection");
+  return FSA_OK;
+}

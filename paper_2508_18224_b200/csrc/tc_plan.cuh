@@ -1,0 +1,17 @@
+// Dispatch predicates + entry points of the tcgen05 tensor-core kernels.
+#pragma once
+#include "common.cuh"
+
+namespace fsa {
+
+// bf16, d_K = d_V = 128, B_K = 64: the BASELINE.json shapes (tc_sel_fwd.cu / tc_sel_bwd.cu).
+bool tc_fwd_supported(const fsa_shape& s, int dtype);
+bool tc_bwd_supported(const fsa_shape& s, int dtype);
+
+int tc_sel_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V,
+               const int32_t* offsets, const int32_t* qlist, void* obuf, void* ml, cudaStream_t st);
+int tc_sel_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V, const void* dOut,
+               const void* lse, const void* delta, const int32_t* offsets, const int32_t* qlist,
+               void* dq_buf, int dqbuf_dtype, void* dK, void* dV, cudaStream_t st);
+
+}  // namespace fsa

@@ -1,0 +1,114 @@
+"""One NSA attention forward + backward, end to end on the device.
+
+This is the training-path composition of the reference operators (the
+pipeline of test_branches.py:167-192 / scenario.py:47-56, plus the
+backward the reference provides for the selected and sliding branches):
+
+  forward : compress_kv (K1) -> compressed attention + importance scores (K2)
+            -> top-k (K3) -> inverse index (K4) -> FSA selected forward
+            (K5 + K6) -> sliding window (K10) -> gated combine (K12)
+  backward: gate scaling -> selected backward (K7 + K8 + K9) and sliding
+            backward (K11); dQ/dK/dV summed over the two branches.
+
+The compressed branch and the gates have no backward in the reference
+(SURVEY 2.3 K13); they are not differentiated here either.
+
+Everything operates on storage-layout tensors: Q (N, h, d), K/V (N, h_K, d),
+tau (N, 3) in the accumulator dtype.  No host synchronisation happens inside
+``forward``/``backward`` (the selection is valid by construction, so its
+validity flags are not read back), so a step can be captured in a CUDA graph.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+
+import torch
+
+from . import _lib
+from .kv_major import _backward_core, _fused_forward
+from .branches import _slide_bwd_storage, _slide_fwd_storage
+from .selection import SelectionTensor, build_inverse_index
+
+
+@dataclasses.dataclass
+class NSAContext:
+    cfg: object
+    dtype: torch.dtype
+    q: torch.Tensor
+    k: torch.Tensor
+    v: torch.Tensor
+    tau: torch.Tensor
+    sel: SelectionTensor
+    inv: object
+    out_sel: torch.Tensor
+    lse_sel: torch.Tensor
+    out_slide: torch.Tensor
+    lse_slide: torch.Tensor
+    out_cmp: torch.Tensor
+    scores: torch.Tensor
+
+
+def nsa_forward(q, k, v, tau, cfg):
+    """Returns (combined out (N, h, d_V), ctx)."""
+    dt = q.dtype
+    acc = _lib.acc_dtype(dt)
+    dev = q.device
+    s = _lib.shape_of(cfg)
+    st = _lib.stream()
+    n_pref = min(cfg.B_K - 1, cfg.N)
+    Kc = torch.empty((cfg.b, cfg.h_K, cfg.d_K), dtype=acc, device=dev)
+    Vc = torch.empty((cfg.b, cfg.h_K, cfg.d_V), dtype=acc, device=dev)
+    Kp = torch.empty((max(n_pref, 1), cfg.h_K, cfg.d_K), dtype=acc, device=dev)
+    Vp = torch.empty((max(n_pref, 1), cfg.h_K, cfg.d_V), dtype=acc, device=dev)
+    _lib.call("fsa_compress_kv", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(k), _lib.ptr(v),
+              _lib.ptr(Kc), _lib.ptr(Vc), _lib.ptr(Kp), _lib.ptr(Vp), st)
+    out_cmp = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=dt, device=dev)
+    lse_cmp = torch.empty((cfg.h, cfg.N), dtype=acc, device=dev)
+    scores = torch.empty((cfg.h_K, cfg.N, cfg.b), dtype=acc, device=dev)
+    _lib.call("fsa_cmp_attn_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(q), _lib.ptr(Kc),
+              _lib.ptr(Vc), _lib.ptr(Kp), _lib.ptr(Vp), _lib.ptr(out_cmp), _lib.ptr(lse_cmp),
+              _lib.ptr(scores), st)
+    idx = torch.empty((cfg.h_K, cfg.N, cfg.T), dtype=torch.int32, device=dev)
+    _lib.call("fsa_select_topk", ctypes.byref(s), _lib.dt_code(acc), _lib.ptr(scores),
+              _lib.ptr(idx), st)
+    sel = SelectionTensor(idx)
+    sel._trusted = True
+    inv = build_inverse_index(sel, cfg, validate=False)
+    out_sel, lse_sel = _fused_forward(cfg, dt, q, k, v, sel, inv)
+    out_slide, lse_slide = _slide_fwd_storage(cfg, dt, q, k, v)
+    out = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=dt, device=dev)
+    _lib.call("fsa_gated_combine", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(out_cmp),
+              _lib.ptr(out_sel), _lib.ptr(out_slide), _lib.ptr(tau), _lib.ptr(out), st)
+    ctx = NSAContext(cfg, dt, q, k, v, tau, sel, inv, out_sel, lse_sel, out_slide, lse_slide,
+                     out_cmp, scores)
+    return out, ctx
+
+
+def nsa_backward(ctx: NSAContext, dout):
+    """Returns (dQ, dK, dV) storage tensors in the accumulator dtype."""
+    cfg, dt = ctx.cfg, ctx.dtype
+    s = _lib.shape_of(cfg)
+    st = _lib.stream()
+    d_sel = torch.empty_like(dout)
+    d_slide = torch.empty_like(dout)
+    _lib.call("fsa_gate_scale", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(dout),
+              _lib.ptr(ctx.tau), 1, _lib.ptr(d_sel), st)
+    _lib.call("fsa_gate_scale", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(dout),
+              _lib.ptr(ctx.tau), 2, _lib.ptr(d_slide), st)
+    dQ, dK, dV = _backward_core(cfg, dt, ctx.q, ctx.k, ctx.v, d_sel, ctx.sel, ctx.inv,
+                                ctx.out_sel, ctx.lse_sel)
+    sQ, sK, sV = _slide_bwd_storage(cfg, dt, ctx.q, ctx.k, ctx.v, d_slide, ctx.out_slide,
+                                    ctx.lse_slide)
+    dQ += sQ
+    dK += sK
+    dV += sV
+    return dQ, dK, dV
+
+
+def nsa_forward_backward(q, k, v, tau, dout, cfg):
+    """One full step: forward then backward; returns (out, dQ, dK, dV)."""
+    out, ctx = nsa_forward(q, k, v, tau, cfg)
+    dQ, dK, dV = nsa_backward(ctx, dout)
+    return out, dQ, dK, dV

@@ -1,0 +1,338 @@
+"""GPU parity: the CUDA path against the reference's golden fixtures and the
+CPU oracle on identical inputs.
+
+Selections are compared bit-exactly; floating-point results within the
+north_star tolerances (f64: the reference's own 1e-10/1e-9, f32: rtol 1e-4,
+bf16: rtol 2e-2, each with an RMS-scaled absolute floor -- gpu_util.assert_close).
+All calls go through the package API -> ctypes -> libfsa_b200.so.
+"""
+
+import json
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2508_18224_b200 as fsa
+from paper_2508_18224_b200 import kv_major
+from golden_io import FULL_CASES, case, load, round_inputs, stride_of
+from gpu_util import DT, assert_close, dev, host
+from oracle import fsa_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _cfg(kw):
+    return fsa.make_config(**kw)
+
+
+# ---------------------------------------------------------------------------
+# K3 top-k selection: bit-exact
+# ---------------------------------------------------------------------------
+
+def test_select_topk_golden_kats():
+    z = load("selection_kats")
+    tags = sorted({k.split("__")[0] for k in z.files})
+    for tag in tags:
+        kw = json.loads(str(z[tag + "__cfg"]))
+        cfg = _cfg(kw)
+        c = O.cfg_of(**kw)
+        if tag + "__scores" in z.files:
+            scores = z[tag + "__scores"]
+        else:
+            seed, f32 = (int(v) for v in z[tag + "__seed"])
+            scores = O.make_scores(c, seed)
+            if f32:
+                scores = scores.astype(np.float32).astype(np.float64)
+        sel = fsa.select_topk_blocks(torch.from_numpy(scores).cuda(), cfg)
+        np.testing.assert_array_equal(host(sel.idx), z[tag + "__idx"], err_msg=tag)
+        if np.array_equal(scores.astype(np.float32).astype(np.float64), scores):
+            sel32 = fsa.select_topk_blocks(torch.from_numpy(scores).float().cuda(), cfg)
+            np.testing.assert_array_equal(host(sel32.idx), z[tag + "__idx"], err_msg=tag + " f32")
+
+
+@pytest.mark.parametrize("kw", [
+    dict(N=4096, d_K=8, d_V=8, h=2, h_K=2, B_K=64, T=16),
+    dict(N=2048, d_K=8, d_V=8, h=4, h_K=4, B_K=16, T=7),
+    dict(N=512, d_K=8, d_V=8, h=1, h_K=1, B_K=4, T=32),
+    dict(N=1024, d_K=8, d_V=8, h=1, h_K=1, B_K=8, T=33),
+    dict(N=640, d_K=8, d_V=8, h=2, h_K=1, B_K=5, T=1),
+])
+@pytest.mark.parametrize("sdt", ["f32", "f64"])
+def test_select_topk_random_vs_oracle(kw, sdt):
+    c = O.cfg_of(**kw)
+    rng = np.random.default_rng(kw["N"] + kw["T"])
+    scores = rng.standard_normal((c.h_K, c.N, c.b))
+    scores[rng.uniform(size=scores.shape) < 0.1] = 0.25  # ties
+    scores[rng.uniform(size=scores.shape) < 0.01] = -np.inf
+    scores[rng.uniform(size=scores.shape) < 0.01] = np.nan
+    if sdt == "f32":
+        scores = scores.astype(np.float32).astype(np.float64)
+    want = O.select_topk(scores, c)
+    t = torch.from_numpy(scores).cuda()
+    if sdt == "f32":
+        t = t.float()
+    got = fsa.select_topk_blocks(t, _cfg(kw))
+    np.testing.assert_array_equal(host(got.idx), want)
+
+
+def test_malformed_selection_messages():
+    z = load("malformed")
+    cfg = _cfg(json.loads(str(z["cfg"])))
+    for tag, msg in json.loads(str(z["messages"])).items():
+        sel = fsa.SelectionTensor(z["idx_" + tag])
+        with pytest.raises(fsa.SelectionError) as exc:
+            fsa.validate_selection(sel, cfg)
+        assert str(exc.value) == msg, tag
+        with pytest.raises(fsa.SelectionError) as exc:
+            fsa.build_inverse_index(fsa.SelectionTensor(z["idx_" + tag]), cfg)
+        assert str(exc.value) == msg, tag
+
+
+# ---------------------------------------------------------------------------
+# K4 inverse index: bit-exact CSR
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", FULL_CASES)
+def test_inverse_index_golden(name):
+    kw, c, inp, z = case(name)
+    cfg = _cfg(kw)
+    sel = fsa.SelectionTensor(z["idx"])
+    inv = fsa.build_inverse_index(sel, cfg)
+    assert fsa.build_inverse_index(sel, cfg) is inv
+    np.testing.assert_array_equal(host(inv.offsets).astype(np.int64), z["inv_offsets"])
+    np.testing.assert_array_equal(inv.n_valid, z["n_valid"])
+    toks = np.concatenate([host(inv.qlist[kh, : int(z["inv_offsets"][kh, -1])]) // c.T
+                           for kh in range(c.h_K)])
+    np.testing.assert_array_equal(toks, z["inv_tok"])
+    back = fsa.selection_from_inverse(inv, cfg)
+    np.testing.assert_array_equal(host(back.idx), z["idx"])
+
+
+def test_inverse_large_vs_oracle():
+    kw = dict(N=32768, d_K=8, d_V=8, h=2, h_K=2, B_K=64, T=16)
+    c = O.cfg_of(**kw)
+    idx = O.select_topk(O.make_scores(c, 3), c)
+    want = O.build_inverse(idx, c)
+    inv = fsa.build_inverse_index(fsa.SelectionTensor(idx), _cfg(kw))
+    np.testing.assert_array_equal(host(inv.offsets).astype(np.int64), want.offsets)
+    for kh in range(c.h_K):
+        ql = host(inv.qlist[kh, : want.offsets[kh, -1]])
+        np.testing.assert_array_equal(ql // c.T, want.tok[kh])
+        np.testing.assert_array_equal(ql % c.T, want.slot[kh])
+
+
+# ---------------------------------------------------------------------------
+# selected attention forward / backward
+# ---------------------------------------------------------------------------
+
+def _dtype_for(z, requested):
+    return requested
+
+
+@pytest.mark.parametrize("name", FULL_CASES)
+def test_selected_forward_golden(name):
+    kw, c, inp, z = case(name)
+    cfg = _cfg(kw)
+    st = stride_of(z)
+    dt = "f64" if inp["round_to"] in ("None", "f64") else ("f32" if inp["round_to"] == "f32" else "bf16")
+    for run_dt in sorted({"f64", dt}):
+        tdt = DT[run_dt]
+        Q, K, V = (dev(inp[k], tdt) for k in "QKV")
+        sel = fsa.SelectionTensor(z["idx"])
+        res, meter = kv_major.selected_forward(Q, K, V, sel, cfg)
+        tol_dt = run_dt if run_dt != "f64" or z["out"].dtype == np.float64 else "f32"
+        assert_close(host(res.out)[::st], z["out"], tol_dt, f"{name} out {run_dt}")
+        assert_close(host(res.lse), z["lse"], tol_dt if tol_dt != "bf16" else "f32", f"{name} lse {run_dt}")
+        want = json.loads(str(z["meter_fwd"]))
+        got = {k: dict(bytes_loaded=p.bytes_loaded, bytes_stored=p.bytes_stored, flops=p.flops,
+                       task_count=p.task_count, inner_iterations=p.inner_iterations)
+               for k, p in meter.phases.items()}
+        assert got == want
+
+
+@pytest.mark.parametrize("name", ["case_kv_small", "case_rect_dims", "case_g8_bk1", "case_unit",
+                                  "case_tiny_fp32"])
+def test_phase_api_golden(name):
+    kw, c, inp, z = case(name)
+    cfg = _cfg(kw)
+    st = stride_of(z)
+    Q, K, V = (dev(inp[k]) for k in "QKV")
+    tol = "f64" if z["out"].dtype == np.float64 else "f32"
+    sel = fsa.SelectionTensor(z["idx"])
+    stats = kv_major.compute_softmax_stats(Q, K, sel, cfg)
+    assert_close(host(stats.m), z["m"], tol, "m")
+    assert_close(host(stats.l), z["l"], tol, "l")
+    sh = kv_major.compute_softmax_stats(Q, K, sel, cfg, shared_max=True)
+    assert_close(host(sh.m), z["m_sh"], tol, "m_sh")
+    assert_close(host(sh.l), z["l_sh"], tol, "l_sh")
+    inv = fsa.build_inverse_index(sel, cfg)
+    buf = kv_major.block_pass_forward(Q, K, V, inv, stats, cfg)
+    res = kv_major.reduce_forward(buf, inv, stats, cfg)
+    assert_close(host(res.out)[::st], z["out"], tol, "reduce out")
+    res_sh = kv_major.reduce_forward(kv_major.block_pass_forward(Q, K, V, inv, sh, cfg), inv, sh, cfg)
+    assert_close(host(res_sh.out)[::st], z["out_sh"], tol, "shared-max out")
+
+
+@pytest.mark.parametrize("name", FULL_CASES)
+def test_selected_backward_golden(name):
+    kw, c, inp, z = case(name)
+    cfg = _cfg(kw)
+    st = stride_of(z)
+    tdt = torch.float64
+    Q, K, V, dO = (dev(inp[k], tdt) for k in ("Q", "K", "V", "dOut"))
+    dQ, dK, dV, meter = kv_major.selected_backward(Q, K, V, fsa.SelectionTensor(z["idx"]), dO, cfg)
+    tol = "f64" if z["dQ"].dtype == np.float64 else "f32"
+    for got, key in ((dQ, "dQ"), (dK, "dK"), (dV, "dV")):
+        assert_close(host(got)[::st], z[key], tol, f"{name} {key}")
+    want = json.loads(str(z["meter_bwd"]))
+    got = {k: dict(bytes_loaded=p.bytes_loaded, bytes_stored=p.bytes_stored, flops=p.flops,
+                   task_count=p.task_count, inner_iterations=p.inner_iterations)
+           for k, p in meter.phases.items()}
+    assert got == want
+
+
+@pytest.mark.parametrize("run_dt", ["f32", "bf16"])
+@pytest.mark.parametrize("kw", [
+    dict(N=2048, d_K=64, d_V=64, h=4, h_K=1, B_K=64, T=8, W=128),       # BASELINE cfg 1 (tiny)
+    dict(N=4096, d_K=128, d_V=128, h=8, h_K=2, B_K=64, T=16, W=512),    # Llama-shaped, short
+    dict(N=2048, d_K=128, d_V=128, h=5, h_K=1, B_K=64, T=16, W=512),    # GQA 5 (Qwen3)
+    dict(N=2048, d_K=128, d_V=128, h=2, h_K=2, B_K=64, T=16, W=512),    # GQA 1
+])
+def test_selected_fwd_bwd_vs_oracle(kw, run_dt):
+    """Oracle fed the dtype-rounded inputs, compared in that dtype's tolerance."""
+    c = O.cfg_of(**kw)
+    cfg = _cfg(kw)
+    Q, K, V = (round_inputs(x, run_dt) for x in O.make_qkv(c, 5))
+    dO = round_inputs(O.make_dout(c, 5), run_dt)
+    idx = O.select_topk(O.make_scores(c, 5), c)
+    want_out, want_lse = O.selected_forward(Q, K, V, idx, c)
+    tdt = DT[run_dt]
+    tQ, tK, tV, tdO = (dev(x, tdt) for x in (Q, K, V, dO))
+    sel = fsa.SelectionTensor(idx)
+    res, _ = kv_major.selected_forward(tQ, tK, tV, sel, cfg)
+    assert_close(host(res.out), want_out, run_dt, "out")
+    assert_close(host(res.lse), want_lse, "f32" if run_dt == "bf16" else run_dt, "lse")
+    want = O.selected_backward(Q, K, V, idx, dO, c)
+    got = kv_major.selected_backward(tQ, tK, tV, sel, tdO, cfg)
+    for g_, w_, name in zip(got[:3], want, ("dQ", "dK", "dV")):
+        assert_close(host(g_), w_, run_dt, name)
+
+
+def test_acceptance_sweep_golden():
+    z = load("acceptance_sweep")
+    for n in range(int(z["count"])):
+        p = f"s{n}__"
+        kw = json.loads(str(z[p + "cfg"]))
+        c = O.cfg_of(**kw)
+        cfg = _cfg(kw)
+        seed = int(z[p + "seed"])
+        Q, K, V = (dev(x) for x in O.make_qkv(c, seed))
+        sel = fsa.select_topk_blocks(torch.from_numpy(O.make_scores(c, seed)).cuda(), cfg)
+        np.testing.assert_array_equal(host(sel.idx), z[p + "idx"])
+        res, _ = kv_major.selected_forward(Q, K, V, sel, cfg)
+        assert np.abs(host(res.out) - z[p + "out"]).max() <= 1e-10
+        g = kv_major.selected_backward(Q, K, V, sel, dev(O.make_dout(c, seed)), cfg)
+        for got, key in zip(g[:3], ("dQ", "dK", "dV")):
+            assert np.abs(host(got) - z[p + key]).max() <= 1e-9
+
+
+def test_bit_identical_repeats_and_task_order():
+    kw = dict(N=1024, d_K=128, d_V=128, h=8, h_K=2, B_K=64, T=8)
+    c = O.cfg_of(**kw)
+    cfg = _cfg(kw)
+    Q, K, V = (dev(x, torch.bfloat16) for x in O.make_qkv(c, 1))
+    sel = fsa.SelectionTensor(O.select_topk(O.make_scores(c, 1), c))
+    a, _ = kv_major.selected_forward(Q, K, V, sel, cfg)
+    b, _ = kv_major.selected_forward(Q, K, V, sel, cfg,
+                                     task_order=np.random.default_rng(0).permutation(cfg.h * cfg.b))
+    assert torch.equal(a.out, b.out) and torch.equal(a.lse, b.lse)
+    dO = dev(O.make_dout(c, 1), torch.bfloat16)
+    g1 = kv_major.selected_backward(Q, K, V, sel, dO, cfg)
+    g2 = kv_major.selected_backward(Q, K, V, sel, dO, cfg)
+    for x, y in zip(g1[:3], g2[:3]):
+        assert torch.equal(x, y)
+    with pytest.raises(ValueError, match="task_order must be a permutation"):
+        kv_major.selected_forward(Q, K, V, sel, cfg, task_order=[0, 0, 1])
+
+
+# ---------------------------------------------------------------------------
+# branches
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", FULL_CASES)
+def test_branches_golden(name):
+    kw, c, inp, z = case(name)
+    cfg = _cfg(kw)
+    st = stride_of(z)
+    tol = "f64" if z["out"].dtype == np.float64 else "f32"
+    Q, K, V, dO = (dev(inp[k]) for k in ("Q", "K", "V", "dOut"))
+    cmp = fsa.compress_kv(K, V, cfg)
+    for key in ("K_cmp", "V_cmp", "K_prefix", "V_prefix"):
+        assert_close(host(getattr(cmp, key)), z[key], tol, key)
+    sc = fsa.importance_scores_from_compressed(Q, cmp.K_cmp, cfg)
+    assert_close(host(sc)[:, ::st], z["scores_cmp"], tol, "scores")
+    res, sc2 = fsa.compressed_attention_forward(Q, cmp, cfg, scores_out=True)
+    assert_close(host(res.out)[::st], z["cmp_out"], tol, "cmp out")
+    assert_close(host(res.lse), z["cmp_lse"], tol, "cmp lse")
+    assert_close(host(sc2)[:, ::st], z["scores_cmp"], tol, "fused scores")
+    if "slide_out" in z.files:
+        sl = fsa.sliding_attention_forward(Q, K, V, cfg)
+        assert_close(host(sl.out)[::st], z["slide_out"], tol, "slide out")
+        assert_close(host(sl.lse), z["slide_lse"], tol, "slide lse")
+        g = fsa.sliding_attention_backward(Q, K, V, dO, cfg)
+        for got, key in zip(g, ("slide_dQ", "slide_dK", "slide_dV")):
+            assert_close(host(got)[::st], z[key], tol, key)
+        sel_res, _ = kv_major.selected_forward(Q, K, V, fsa.SelectionTensor(z["idx"]), cfg)
+        comb = fsa.gated_combine((res, sel_res, sl), torch.from_numpy(inp["tau"]).cuda(), cfg)
+        assert_close(host(comb.out)[::st], z["comb_out"], tol, "combined")
+        assert torch.isnan(comb.lse).all()
+
+
+def test_gate_errors():
+    kw = dict(N=32, d_K=8, d_V=8, h=4, h_K=2, B_K=8, T=2)
+    cfg = _cfg(kw)
+    c = O.cfg_of(**kw)
+    Q, K, V = (dev(x) for x in O.make_qkv(c, 12))
+    r = fsa.sliding_attention_forward(Q, K, V, cfg)
+    bad = np.zeros((cfg.N, 3))
+    bad[0, 0] = 1.5
+    with pytest.raises(ValueError, match="gate values"):
+        fsa.gated_combine((r, r, r), bad, cfg)
+    with pytest.raises(ValueError, match="expected exactly three"):
+        fsa.gated_combine((r, r), np.zeros((cfg.N, 3)), cfg)
+
+
+# ---------------------------------------------------------------------------
+# full NSA step (the bench workload) vs the oracle composition
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("run_dt", ["f32", "bf16"])
+def test_nsa_step_vs_oracle(run_dt):
+    kw = dict(N=2048, d_K=128, d_V=128, h=8, h_K=2, B_K=64, T=8, W=256)
+    c = O.cfg_of(**kw)
+    cfg = _cfg(kw)
+    Q, K, V = (round_inputs(x, run_dt) for x in O.make_qkv(c, 9))
+    dO = round_inputs(O.make_dout(c, 9), run_dt)
+    tau = O.make_gates(c, 9)
+    tdt = DT[run_dt]
+    q, k, v, do = (dev(x, tdt).permute(0, 2, 1).contiguous() for x in (Q, K, V, dO))
+    acc = torch.float32
+    out, ctx = fsa.nsa_forward(q, k, v, torch.from_numpy(tau).to("cuda", acc), cfg)
+    # selection parity on the GPU's own scores (SURVEY 8(c) score-path caveat)
+    scores = host(ctx.scores).astype(np.float64)
+    idx = O.select_topk(scores, c)
+    np.testing.assert_array_equal(host(ctx.sel.idx), idx)
+    cmp = O.compress_kv(K, V, c)
+    assert_close(scores, O.importance_scores(Q, cmp.K_cmp, c), "f32" if run_dt == "f32" else "bf16",
+                 "scores")
+    o_cmp, _ = O.compressed_forward(Q, cmp, c)
+    o_sel, _ = O.selected_forward(Q, K, V, idx, c)
+    o_sl, _ = O.sliding_forward(Q, K, V, c)
+    want, _ = O.gated_combine((o_cmp, o_sel, o_sl), tau, c)
+    assert_close(host(out.permute(0, 2, 1)), want, run_dt, "combined")
+    dQ, dK, dV = fsa.nsa_backward(ctx, do)
+    gs = O.selected_backward(Q, K, V, idx, dO * tau[:, 1][:, None, None], c)
+    gl = O.sliding_backward(Q, K, V, dO * tau[:, 2][:, None, None], c)
+    for got, a, b, name in zip((dQ, dK, dV), gs, gl, ("dQ", "dK", "dV")):
+        assert_close(host(got.permute(0, 2, 1)), a + b, run_dt, name)

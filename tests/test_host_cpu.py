@@ -1,0 +1,121 @@
+"""CPU-side tests: the C-ABI library loads and exports what include/ declares,
+host logic (config, meters) matches the reference, and the package refuses
+to compute without a GPU (no CPU fallback)."""
+
+import json
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2508_18224_b200 as fsa
+from paper_2508_18224_b200 import _lib, meter
+from golden_io import FULL_CASES, case
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "fsa_b200.h")
+
+
+def _header_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(fsa_[a-z0-9_]+)\s*\(", text)))
+
+
+@pytest.fixture(scope="module")
+def built():
+    from paper_2508_18224_b200 import build
+    build.build()
+    return _lib.lib()
+
+
+def test_library_exports_every_declared_symbol(built):
+    syms = _header_symbols()
+    assert len(syms) >= 20
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (fsa_[a-z0-9_]+)", out))
+    missing = [s for s in syms if s not in exported]
+    assert not missing, missing
+    assert sorted(_lib.SIGNATURES) == syms
+    assert built.fsa_abi_version() == 1
+
+
+def test_library_is_sm100a_only(built):
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _lib.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    archs = set(re.findall(r"sm_(\d+a?)", out))
+    assert archs == {"100a"}, archs
+
+
+def test_no_cpu_fallback():
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    cfg = fsa.make_config(N=16, d_K=4, d_V=4, h=2, h_K=1, B_K=4, T=2)
+    with pytest.raises(RuntimeError, match="CUDA device"):
+        fsa.select_topk_blocks(np.zeros((1, 16, 4)), cfg)
+
+
+# --- config: mirrors the reference's test_config.py behaviour ---------------
+
+def test_config_derivations_and_errors():
+    cfg = fsa.make_config(N=64, d_K=8, d_V=8, h=4, h_K=2, B_K=16, T=2, B_Q=8, W=16)
+    assert (cfg.g, cfg.b) == (2, 4)
+    with pytest.raises(fsa.ConfigError, match="N not divisible by B_K"):
+        fsa.make_config(N=64, d_K=8, d_V=8, h=4, h_K=2, B_K=48, T=1)
+    with pytest.raises(fsa.ConfigError, match=r"T exceeds b=4"):
+        fsa.make_config(N=64, d_K=8, d_V=8, h=4, h_K=2, B_K=16, T=5)
+    with pytest.raises(fsa.ConfigError, match="h not divisible by h_K"):
+        fsa.make_config(N=64, d_K=8, d_V=8, h=4, h_K=3, B_K=16, T=2)
+    with pytest.raises(fsa.ConfigError, match="bytes_per_elem"):
+        fsa.make_config(N=64, d_K=8, d_V=8, h=4, h_K=2, B_K=16, T=2, bytes_per_elem=3)
+    assert fsa.validate_config(cfg) == cfg
+    small = fsa.make_config(N=8, d_K=4, d_V=4, h=2, h_K=1, B_K=4, T=2)
+    assert (small.B_Q, small.W) == (8, 8)
+    with pytest.raises(fsa.ConfigError, match="non-uniform head dims"):
+        _ = fsa.make_config(N=16, d_K=4, d_V=8, h=2, h_K=1, B_K=4, T=2).d
+    try:
+        fsa.validate_config(fsa.AttentionConfig(N=63, d_K=8, d_V=8, h=4, h_K=3, B_K=16, T=1))
+    except fsa.ConfigError as exc:
+        assert "h not divisible by h_K" in str(exc) and "N not divisible by B_K" in str(exc)
+    else:
+        pytest.fail("expected ConfigError")
+
+
+def test_config_text_parser():
+    text = "# c\nN = 64\nd_K = 8\nd_V = 8\nh = 4\nh_K = 2\nB_K = 16\nT = 2\nB_Q = 8  # x\nW = 16\n"
+    assert fsa.parse_config_text(text) == fsa.make_config(N=64, d_K=8, d_V=8, h=4, h_K=2, B_K=16,
+                                                          T=2, B_Q=8, W=16)
+    with pytest.raises(fsa.ConfigError, match="unknown config key"):
+        fsa.parse_config_text("N = 64\nbogus = 1\n")
+    with pytest.raises(fsa.ConfigError, match="missing required"):
+        fsa.parse_config_text("N = 64\n")
+
+
+# --- meters: closed forms equal the reference's counted meters ---------------
+
+def _as_dict(m):
+    return {k: dict(bytes_loaded=p.bytes_loaded, bytes_stored=p.bytes_stored, flops=p.flops,
+                    task_count=p.task_count, inner_iterations=p.inner_iterations)
+            for k, p in m.phases.items()}
+
+
+@pytest.mark.parametrize("name", FULL_CASES)
+def test_meter_closed_forms_match_reference(name):
+    kw, c, inp, z = case(name)
+    cfg = fsa.make_config(**kw)
+    assert _as_dict(meter.forward_meter(z["n_valid"], cfg)) == json.loads(str(z["meter_fwd"]))
+    assert _as_dict(meter.backward_meter(z["n_valid"], cfg)) == json.loads(str(z["meter_bwd"]))
+
+
+def test_meter_merge_algebra():
+    a = meter.TrafficMeter()
+    a.phase("stats").add(bytes_loaded=3, flops=2)
+    b = meter.TrafficMeter()
+    b.phase("reduce").add(bytes_stored=5)
+    b.phase("stats").add(task_count=1)
+    assert a.merged(b) == b.merged(a)
+    assert a.merged(b).total_bytes == 8
+    assert [n for n, _ in a.merged(b).as_rows()] == ["stats", "reduce"]
