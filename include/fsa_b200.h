@@ -24,9 +24,11 @@
  *      obuf [h][N][T][d_V]  ml [h][N][T][2]     dq_buf [h][N][T][d_K]
  *      inverse CSR: offsets [h_K][b+1] int32, qlist [h_K][N*T] int32 holding
  *      t*T + slot, ascending t inside each block (selection.py:123-169).
- *  - dtype: FSA_DT_F32 / FSA_DT_F64 / FSA_DT_BF16 for Q/K/V/dOut/out.  The
- *    "accumulator" type is f64 for f64 inputs and f32 otherwise; lse/m/l/delta,
- *    compressed KV, scores and gradients are stored in it.
+ *  - dtype: FSA_DT_F32 / FSA_DT_F64 / FSA_DT_BF16 for Q/K/V/dOut.  The
+ *    "accumulator" type is f64 for f64 inputs and f32 otherwise; branch
+ *    outputs (out of merge / compressed / sliding), lse/m/l/delta, compressed
+ *    KV, scores and gradients are stored in it (the reference returns f64
+ *    everywhere; keeping bf16 runs' intermediates in f32 keeps delta exact).
  */
 #ifndef FSA_B200_H
 #define FSA_B200_H
@@ -111,8 +113,8 @@ int fsa_sel_fwd(const fsa_shape* s, int dtype, int mode, const void* Q, const vo
                 const void* m_global, void* obuf, int obuf_dtype, void* ml, void* stream);
 
 /* Merge of per-slot partials in ascending block order (kv_major.py:207-242;
- * stats merge kv_major.py:137-149, shared max :141-146).  out in the input
- * dtype, lse/m_out/l_out in acc dtype; m_out/l_out/lse nullable. */
+ * stats merge kv_major.py:137-149, shared max :141-146).  out, lse, m_out,
+ * l_out in acc dtype; m_out/l_out/lse nullable. */
 int fsa_merge_fwd(const fsa_shape* s, int dtype, int mode, const int32_t* idx, const void* obuf,
                   int obuf_dtype, const void* ml, const void* m_global, const void* l_global,
                   void* out, void* lse, void* m_out, void* l_out, int shared_max, void* stream);
@@ -148,9 +150,11 @@ int fsa_slide_bwd(const fsa_shape* s, int dtype, const void* Q, const void* K, c
                   const void* dOut, const void* lse, const void* delta, void* dQ, void* dK,
                   void* dV, void* stream);
 
-/* gated_combine (branches.py:95-104): out = sum_c tau[t][c] * out_c; tau [N][3] acc. */
+/* gated_combine (branches.py:95-104): out = sum_c tau[t][c] * out_c; branch
+ * outputs and tau [N][3] in acc dtype; out in acc dtype if out_acc else dtype. */
 int fsa_gated_combine(const fsa_shape* s, int dtype, const void* out_cmp, const void* out_sel,
-                      const void* out_slide, const void* tau, void* out, void* stream);
+                      const void* out_slide, const void* tau, void* out, int out_acc,
+                      void* stream);
 
 /* Gate backward into branch c: out = tau[t][c] * dOut (branches.py:103); [N][h][d_V]. */
 int fsa_gate_scale(const fsa_shape* s, int dtype, const void* dOut, const void* tau, int col,

@@ -63,7 +63,7 @@ def compressed_attention_forward(Q, cmp: CompressedKV, cfg, *, scores_out: bool 
     acc = _lib.acc_dtype(dt)
     Kc, Vc, Kp, Vp = _cmp_storage(cmp, acc)
     dev = q.device
-    out = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=dt, device=dev)
+    out = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=acc, device=dev)
     lse = torch.empty((cfg.h, cfg.N), dtype=acc, device=dev)
     scores = torch.empty((cfg.h_K, cfg.N, cfg.b), dtype=acc, device=dev) if scores_out else None
     s = _lib.shape_of(cfg)
@@ -87,7 +87,7 @@ def sliding_attention_forward(Q, K, V, cfg) -> AttentionOutput:
 
 def _slide_fwd_storage(cfg, dt, q, k, v):
     dev, acc = q.device, _lib.acc_dtype(dt)
-    out = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=dt, device=dev)
+    out = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=acc, device=dev)
     lse = torch.empty((cfg.h, cfg.N), dtype=acc, device=dev)
     s = _lib.shape_of(cfg)
     _lib.call("fsa_slide_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(q), _lib.ptr(k),
@@ -146,13 +146,12 @@ def gated_combine(outs, tau, cfg) -> AttentionOutput:
     if len(shapes) != 1:
         raise ValueError(f"shape mismatch across branches: {sorted(shapes)}")
     xs = [to_device(o.out) for o in outs]
-    dt = compute_dtype(*xs)
-    st = [as_headed(x, cfg.N, cfg.d_V, cfg.h, "out", dt) for x in xs]
-    acc = _lib.acc_dtype(dt)
+    acc = _lib.acc_dtype(compute_dtype(*xs))
+    st = [as_headed(x, cfg.N, cfg.d_V, cfg.h, "out", acc) for x in xs]
     tt = t.to(acc).contiguous()
     out = torch.empty_like(st[0])
     s = _lib.shape_of(cfg)
-    _lib.call("fsa_gated_combine", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(st[0]),
-              _lib.ptr(st[1]), _lib.ptr(st[2]), _lib.ptr(tt), _lib.ptr(out), _lib.stream())
+    _lib.call("fsa_gated_combine", ctypes.byref(s), _lib.dt_code(acc), _lib.ptr(st[0]),
+              _lib.ptr(st[1]), _lib.ptr(st[2]), _lib.ptr(tt), _lib.ptr(out), 1, _lib.stream())
     lse = torch.full((cfg.h, cfg.N), float("nan"), dtype=acc, device=out.device)
     return AttentionOutput(out=logical(out), lse=lse)

@@ -23,7 +23,7 @@ template <typename T>
 __global__ void cmp_fwd_generic(const T* __restrict__ Q, const typename Acc<T>::type* __restrict__ Kc,
                                 const typename Acc<T>::type* __restrict__ Vc,
                                 const typename Acc<T>::type* __restrict__ Kp,
-                                const typename Acc<T>::type* __restrict__ Vp, T* __restrict__ out,
+                                const typename Acc<T>::type* __restrict__ Vp, typename Acc<T>::type* __restrict__ out,
                                 typename Acc<T>::type* __restrict__ lse, fsa_shape s) {
   using A = typename Acc<T>::type;
   const int lane = threadIdx.x & 31;
@@ -32,7 +32,7 @@ __global__ void cmp_fwd_generic(const T* __restrict__ Q, const typename Acc<T>::
   const int64_t j = wid / s.N, t = wid % s.N, g = s.h / s.h_K, kh = j / g;
   const int64_t dK = s.d_K, dV = s.d_V;
   const T* q = Q + (t * s.h + j) * dK;
-  T* o = out + (t * s.h + j) * dV;
+  A* o = out + (t * s.h + j) * dV;
   const int64_t nf = (t + 1) / s.B_K;
   const A scale = A(s.scale);
   if (nf == 0) {
@@ -40,7 +40,7 @@ __global__ void cmp_fwd_generic(const T* __restrict__ Q, const typename Acc<T>::
     A acc = 0;
     for (int64_t c = lane; c < dK; c += 32) acc += to_acc(q[c]) * kp[c];
     acc = warp_sum(acc);
-    for (int64_t c = lane; c < dV; c += 32) o[c] = from_acc<T>(Vp[(t * s.h_K + kh) * dV + c]);
+    for (int64_t c = lane; c < dV; c += 32) o[c] = Vp[(t * s.h_K + kh) * dV + c];
     if (lane == 0) lse[j * s.N + t] = acc * scale;
     return;
   }
@@ -62,7 +62,7 @@ __global__ void cmp_fwd_generic(const T* __restrict__ Q, const typename Acc<T>::
       }
     }
     if (c0 == 0) l = warp_sum(l);
-    if (c0 + lane < dV) o[c0 + lane] = from_acc<T>(acc / l);
+    if (c0 + lane < dV) o[c0 + lane] = acc / l;
   }
   if (lane == 0) lse[j * s.N + t] = m + log_acc(l);
 }
@@ -72,7 +72,7 @@ __global__ void cmp_fwd_generic(const T* __restrict__ Q, const typename Acc<T>::
 // ---------------------------------------------------------------------------
 template <typename T>
 __global__ void slide_fwd_generic(const T* __restrict__ Q, const T* __restrict__ K,
-                                  const T* __restrict__ V, T* __restrict__ out,
+                                  const T* __restrict__ V, typename Acc<T>::type* __restrict__ out,
                                   typename Acc<T>::type* __restrict__ lse, fsa_shape s) {
   using A = typename Acc<T>::type;
   const int lane = threadIdx.x & 31;
@@ -102,7 +102,7 @@ __global__ void slide_fwd_generic(const T* __restrict__ Q, const T* __restrict__
       }
     }
     if (c0 == 0) l = warp_sum(l);
-    if (c0 + lane < dV) out[(t * s.h + j) * dV + c0 + lane] = from_acc<T>(acc / l);
+    if (c0 + lane < dV) out[(t * s.h + j) * dV + c0 + lane] = acc / l;
   }
   if (lane == 0) lse[j * s.N + t] = m + log_acc(l);
 }
@@ -195,7 +195,7 @@ int cmp_fwd_impl(const fsa_shape* s, const void* Q, const void* Kc, const void* 
   const int64_t rows = s->h * s->N;
   if (rows == 0) return FSA_OK;
   cmp_fwd_generic<T><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(
-      (const T*)Q, (const A*)Kc, (const A*)Vc, (const A*)Kp, (const A*)Vp, (T*)out, (A*)lse, *s);
+      (const T*)Q, (const A*)Kc, (const A*)Vc, (const A*)Kp, (const A*)Vp, (A*)out, (A*)lse, *s);
   FSA_LAUNCH_CHECK("cmp_attn_fwd");
   if (scores) {
     int dt = sizeof(T) == 8 ? FSA_DT_F64 : (sizeof(T) == 4 ? FSA_DT_F32 : FSA_DT_BF16);
@@ -211,7 +211,7 @@ int slide_fwd_impl(const fsa_shape* s, const void* Q, const void* K, const void*
   const int64_t rows = s->h * s->N;
   if (rows == 0) return FSA_OK;
   slide_fwd_generic<T><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>((const T*)Q, (const T*)K,
-                                                                   (const T*)V, (T*)out, (A*)lse, *s);
+                                                                   (const T*)V, (A*)out, (A*)lse, *s);
   FSA_LAUNCH_CHECK("slide_fwd");
   return FSA_OK;
 }

@@ -79,19 +79,20 @@ __global__ void scores_kernel(const T* __restrict__ Q, const typename Acc<T>::ty
 // ---------------------------------------------------------------------------
 // K12 gated combine: branches.py:95-104 (sum order ((0 + t0*a) + t1*b) + t2*c).
 // ---------------------------------------------------------------------------
-template <typename T>
-__global__ void combine_kernel(const T* __restrict__ a, const T* __restrict__ bsel,
-                               const T* __restrict__ c, const typename Acc<T>::type* __restrict__ tau,
-                               T* __restrict__ out, int64_t N, int64_t row) {
-  using A = typename Acc<T>::type;
+// Branch outputs arrive in the accumulator dtype; the combined output is
+// written in TO (the input dtype, or the accumulator dtype).
+template <typename A, typename TO>
+__global__ void combine_kernel(const A* __restrict__ a, const A* __restrict__ bsel,
+                               const A* __restrict__ c, const A* __restrict__ tau,
+                               TO* __restrict__ out, int64_t N, int64_t row) {
   const int64_t total = N * row;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = e / row;
-    A acc = A(0) + tau[t * 3 + 0] * to_acc(a[e]);
-    acc = acc + tau[t * 3 + 1] * to_acc(bsel[e]);
-    acc = acc + tau[t * 3 + 2] * to_acc(c[e]);
-    out[e] = from_acc<T>(acc);
+    A acc = A(0) + tau[t * 3 + 0] * a[e];
+    acc = acc + tau[t * 3 + 1] * bsel[e];
+    acc = acc + tau[t * 3 + 2] * c[e];
+    out[e] = from_acc<TO>(acc);
   }
 }
 
@@ -147,14 +148,18 @@ int scores_impl(const fsa_shape* s, const void* Q, const void* Kc, void* S, cuda
 
 template <typename T>
 int combine_impl(const fsa_shape* s, const void* a, const void* b, const void* c, const void* tau,
-                 void* out, cudaStream_t st) {
+                 void* out, int out_acc, cudaStream_t st) {
   using A = typename Acc<T>::type;
   const int64_t row = s->h * s->d_V, total = s->N * row;
   int64_t blocks = (total + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
-  combine_kernel<T><<<(unsigned)blocks, 256, 0, st>>>((const T*)a, (const T*)b, (const T*)c,
-                                                     (const A*)tau, (T*)out, s->N, row);
+  if (out_acc)
+    combine_kernel<A, A><<<(unsigned)blocks, 256, 0, st>>>((const A*)a, (const A*)b, (const A*)c,
+                                                          (const A*)tau, (A*)out, s->N, row);
+  else
+    combine_kernel<A, T><<<(unsigned)blocks, 256, 0, st>>>((const A*)a, (const A*)b, (const A*)c,
+                                                          (const A*)tau, (T*)out, s->N, row);
   FSA_LAUNCH_CHECK("gated_combine");
   return FSA_OK;
 }
@@ -206,8 +211,9 @@ extern "C" int fsa_importance_scores(const fsa_shape* s, int dtype, const void* 
 
 extern "C" int fsa_gated_combine(const fsa_shape* s, int dtype, const void* out_cmp,
                                  const void* out_sel, const void* out_slide, const void* tau,
-                                 void* out, void* stream) {
-  DISPATCH_DT(dtype, combine_impl, s, out_cmp, out_sel, out_slide, tau, out, (cudaStream_t)stream);
+                                 void* out, int out_acc, void* stream) {
+  DISPATCH_DT(dtype, combine_impl, s, out_cmp, out_sel, out_slide, tau, out, out_acc,
+              (cudaStream_t)stream);
 }
 
 extern "C" int fsa_gate_scale(const fsa_shape* s, int dtype, const void* dOut, const void* tau,

@@ -103,7 +103,7 @@ template <typename T, typename OB>
 __global__ void merge_generic(int mode, const int32_t* __restrict__ idx, const OB* __restrict__ obuf,
                               const typename Acc<T>::type* __restrict__ ml,
                               const typename Acc<T>::type* __restrict__ m_global,
-                              const typename Acc<T>::type* __restrict__ l_global, T* __restrict__ out,
+                              const typename Acc<T>::type* __restrict__ l_global, typename Acc<T>::type* __restrict__ out,
                               typename Acc<T>::type* __restrict__ lse,
                               typename Acc<T>::type* __restrict__ m_out,
                               typename Acc<T>::type* __restrict__ l_out, int shared_max, fsa_shape s) {
@@ -144,7 +144,7 @@ __global__ void merge_generic(int mode, const int32_t* __restrict__ idx, const O
           const A w = ml[(rb + k) * 2 + 1] * exp_acc(ml[(rb + k) * 2] - M);
           acc += w * to_acc(obuf[(rb + k) * dV + c]);
         }
-        out[(t * s.h + j) * dV + c] = from_acc<T>(acc * invL);
+        out[(t * s.h + j) * dV + c] = acc * invL;
       }
       if (lane == 0) {
         if (lse) lse[j * s.N + t] = M + log_acc(L);
@@ -156,7 +156,7 @@ __global__ void merge_generic(int mode, const int32_t* __restrict__ idx, const O
       for (int64_t c = lane; c < dV; c += 32) {
         A acc = 0;
         for (int64_t k = 0; k < len; ++k) acc += to_acc(obuf[(rb + k) * dV + c]);
-        out[(t * s.h + j) * dV + c] = from_acc<T>(acc / l);
+        out[(t * s.h + j) * dV + c] = acc / l;
       }
       if (lane == 0 && lse) lse[j * s.N + t] = m + log_acc(l);
     }
@@ -171,14 +171,14 @@ __global__ void merge_generic(int mode, const int32_t* __restrict__ idx, const O
 }
 
 template <typename T>
-__global__ void delta_kernel(const T* __restrict__ out, const T* __restrict__ dOut,
+__global__ void delta_kernel(const typename Acc<T>::type* __restrict__ out, const T* __restrict__ dOut,
                              typename Acc<T>::type* __restrict__ delta, fsa_shape s) {
   using A = typename Acc<T>::type;
   const int lane = threadIdx.x & 31;
   const int64_t wid = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (wid >= s.h * s.N) return;
   const int64_t j = wid / s.N, t = wid % s.N;
-  const T* o = out + (t * s.h + j) * s.d_V;
+  const A* o = out + (t * s.h + j) * s.d_V;
   const T* d = dOut + (t * s.h + j) * s.d_V;
   A acc = 0;
   for (int64_t c = lane; c < s.d_V; c += 32) acc += to_acc(o[c]) * to_acc(d[c]);
@@ -191,7 +191,7 @@ __global__ void delta_kernel(const T* __restrict__ out, const T* __restrict__ dO
 // the whole CTA so every dK/dV element has one owner thread and a fixed
 // accumulation order (deterministic, no atomics).
 // ---------------------------------------------------------------------------
-template <typename T>
+template <typename T, bool kStage>
 __global__ void __launch_bounds__(128)
 sel_bwd_generic(const T* __restrict__ Q, const T* __restrict__ K, const T* __restrict__ V,
                 const T* __restrict__ dOut, const typename Acc<T>::type* __restrict__ lse,
@@ -212,22 +212,31 @@ sel_bwd_generic(const T* __restrict__ Q, const T* __restrict__ K, const T* __res
       dV[((i * BK + e / dVd) * s.h_K + kh) * dVd + e % dVd] = 0;
     return;
   }
-  A* Ks = reinterpret_cast<A*>(smem_raw);  // [BK][dK+1]
-  A* Vs = Ks + BK * (dKd + 1);             // [BK][dV+1]
-  A* dKs = Vs + BK * (dVd + 1);            // [BK][dK]
+  // kStage: K_i/V_i staged in smem; otherwise (large f64 tiles) read through L1
+  A* Ks = reinterpret_cast<A*>(smem_raw);              // [BK][dK+1]
+  A* Vs = Ks + (kStage ? BK * (dKd + 1) : 0);          // [BK][dV+1]
+  A* dKs = Vs + (kStage ? BK * (dVd + 1) : 0);         // [BK][dK]
   A* dVs = dKs + BK * dKd;                 // [BK][dV]
   A* qs = dVs + BK * dVd;                  // [dK]
   A* dos = qs + dKd;                       // [dV]
   A* ps = dos + dVd;                       // [BK]
   A* dzs = ps + BK;                        // [BK]
+  const T* Kg = K + (i * BK * s.h_K + kh) * dKd;  // row r at Kg + r*h_K*dK
+  const T* Vg = V + (i * BK * s.h_K + kh) * dVd;
+  auto kv = [&](int64_t r, int64_t c) -> A {
+    return kStage ? Ks[r * (dKd + 1) + c] : to_acc(Kg[r * s.h_K * dKd + c]);
+  };
+  auto vv = [&](int64_t r, int64_t c) -> A {
+    return kStage ? Vs[r * (dVd + 1) + c] : to_acc(Vg[r * s.h_K * dVd + c]);
+  };
   for (int64_t e = threadIdx.x; e < BK * dKd; e += blockDim.x) {
     const int64_t r = e / dKd, c = e % dKd;
-    Ks[r * (dKd + 1) + c] = to_acc(K[((i * BK + r) * s.h_K + kh) * dKd + c]);
+    if (kStage) Ks[r * (dKd + 1) + c] = to_acc(Kg[r * s.h_K * dKd + c]);
     dKs[e] = 0;
   }
   for (int64_t e = threadIdx.x; e < BK * dVd; e += blockDim.x) {
     const int64_t r = e / dVd, c = e % dVd;
-    Vs[r * (dVd + 1) + c] = to_acc(V[((i * BK + r) * s.h_K + kh) * dVd + c]);
+    if (kStage) Vs[r * (dVd + 1) + c] = to_acc(Vg[r * s.h_K * dVd + c]);
     dVs[e] = 0;
   }
   const A scale = A(s.scale);
@@ -245,8 +254,8 @@ sel_bwd_generic(const T* __restrict__ Q, const T* __restrict__ K, const T* __res
       A p = 0, dz = 0;
       if (c < vis) {
         A z = 0, dp = 0;
-        for (int64_t k = 0; k < dKd; ++k) z += qs[k] * Ks[c * (dKd + 1) + k];
-        for (int64_t k = 0; k < dVd; ++k) dp += dos[k] * Vs[c * (dVd + 1) + k];
+        for (int64_t k = 0; k < dKd; ++k) z += qs[k] * kv(c, k);
+        for (int64_t k = 0; k < dVd; ++k) dp += dos[k] * vv(c, k);
         p = exp_acc(z * scale - lrow);
         dz = p * (dp - drow);
       }
@@ -257,7 +266,7 @@ sel_bwd_generic(const T* __restrict__ Q, const T* __restrict__ K, const T* __res
     A* dqr = dq_buf + ((j * s.N + t) * TT + slot) * dKd;
     for (int64_t c = threadIdx.x; c < dKd; c += blockDim.x) {
       A acc = 0;
-      for (int64_t k = 0; k < vis; ++k) acc += dzs[k] * Ks[k * (dKd + 1) + c];
+      for (int64_t k = 0; k < vis; ++k) acc += dzs[k] * kv(k, c);
       dqr[c] = acc * scale;
     }
     for (int64_t e = threadIdx.x; e < BK * dKd; e += blockDim.x)
@@ -324,11 +333,11 @@ int merge_impl(const fsa_shape* s, int mode, const int32_t* idx, const void* obu
   const unsigned grid = (unsigned)((rows + 7) / 8);
   if (obuf_dtype == FSA_DT_BF16) {
     merge_generic<T, __nv_bfloat16><<<grid, 256, 0, st>>>(
-        mode, idx, (const __nv_bfloat16*)obuf, (const A*)ml, (const A*)mg, (const A*)lg, (T*)out,
+        mode, idx, (const __nv_bfloat16*)obuf, (const A*)ml, (const A*)mg, (const A*)lg, (A*)out,
         (A*)lse, (A*)m_out, (A*)l_out, shared_max, *s);
   } else {
     merge_generic<T, A><<<grid, 256, 0, st>>>(mode, idx, (const A*)obuf, (const A*)ml, (const A*)mg,
-                                              (const A*)lg, (T*)out, (A*)lse, (A*)m_out, (A*)l_out,
+                                              (const A*)lg, (A*)out, (A*)lse, (A*)m_out, (A*)l_out,
                                               shared_max, *s);
   }
   FSA_LAUNCH_CHECK("merge_fwd");
@@ -340,7 +349,7 @@ int delta_impl(const fsa_shape* s, const void* out, const void* dOut, void* delt
   using A = typename Acc<T>::type;
   const int64_t rows = s->h * s->N;
   if (rows == 0) return FSA_OK;
-  delta_kernel<T><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>((const T*)out, (const T*)dOut,
+  delta_kernel<T><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>((const A*)out, (const T*)dOut,
                                                               (A*)delta, *s);
   FSA_LAUNCH_CHECK("bwd_delta");
   return FSA_OK;
@@ -352,13 +361,16 @@ int sel_bwd_impl(const fsa_shape* s, const void* Q, const void* K, const void* V
                  void* dq_buf, void* dK, void* dV, cudaStream_t st) {
   using A = typename Acc<T>::type;
   const int64_t b = s->N / s->B_K;
-  size_t smem = sizeof(A) * (size_t)(s->B_K * (s->d_K + 1 + s->d_V + 1 + s->d_K + s->d_V) +
-                                     s->d_K + s->d_V + 2 * s->B_K);
+  const size_t acc_elems = (size_t)(s->B_K * (s->d_K + s->d_V) + s->d_K + s->d_V + 2 * s->B_K);
+  const size_t stage_elems = (size_t)(s->B_K * (s->d_K + 1 + s->d_V + 1));
+  const bool stage = sizeof(A) * (acc_elems + stage_elems) <= 220 * 1024;
+  const size_t smem = sizeof(A) * (acc_elems + (stage ? stage_elems : 0));
   FSA_REQUIRE(smem <= 220 * 1024, "selected backward: B_K=%lld d=%lld exceeds shared memory",
               (long long)s->B_K, (long long)s->d_K);
-  cudaFuncSetAttribute(sel_bwd_generic<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kern = stage ? sel_bwd_generic<T, true> : sel_bwd_generic<T, false>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid((unsigned)b, (unsigned)s->h_K);
-  sel_bwd_generic<T><<<grid, 128, smem, st>>>((const T*)Q, (const T*)K, (const T*)V,
+  kern<<<grid, 128, smem, st>>>((const T*)Q, (const T*)K, (const T*)V,
                                               (const T*)dOut, (const A*)lse, (const A*)delta,
                                               offsets, qlist, (A*)dq_buf, (A*)dK, (A*)dV, *s);
   FSA_LAUNCH_CHECK("sel_bwd");

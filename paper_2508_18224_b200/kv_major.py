@@ -101,7 +101,8 @@ def _intake(cfg, Q, K, V=None, dOut=None):
 
 
 def _fused_forward(cfg, dt, q, k, v, sel, inv):
-    """K5 (LOCAL) + K6 (LOCAL merge): returns out storage (N, h, d_V), lse (h, N)."""
+    """K5 (LOCAL) + K6 (LOCAL merge): returns out storage (N, h, d_V) and lse
+    (h, N), both in the accumulator dtype (f32 for bf16 inputs)."""
     dev = q.device
     acc = _lib.acc_dtype(dt)
     (ob_code, ob_dtype), _ = _lib.buffer_dtypes(cfg, dt)
@@ -112,7 +113,7 @@ def _fused_forward(cfg, dt, q, k, v, sel, inv):
     _lib.call("fsa_sel_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.FWD_LOCAL, _lib.ptr(q),
               _lib.ptr(k), _lib.ptr(v), _lib.ptr(inv.offsets), _lib.ptr(inv.qlist), None,
               _lib.ptr(obuf), ob_code, _lib.ptr(ml), st)
-    out = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=dt, device=dev)
+    out = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=acc, device=dev)
     lse = torch.empty((cfg.h, cfg.N), dtype=acc, device=dev)
     _lib.call("fsa_merge_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.MERGE_LOCAL,
               _lib.ptr(sel.idx), _lib.ptr(obuf), ob_code, _lib.ptr(ml), None, None, _lib.ptr(out),

@@ -64,7 +64,7 @@ def nsa_forward(q, k, v, tau, cfg):
     Vp = torch.empty((max(n_pref, 1), cfg.h_K, cfg.d_V), dtype=acc, device=dev)
     _lib.call("fsa_compress_kv", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(k), _lib.ptr(v),
               _lib.ptr(Kc), _lib.ptr(Vc), _lib.ptr(Kp), _lib.ptr(Vp), st)
-    out_cmp = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=dt, device=dev)
+    out_cmp = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=acc, device=dev)
     lse_cmp = torch.empty((cfg.h, cfg.N), dtype=acc, device=dev)
     scores = torch.empty((cfg.h_K, cfg.N, cfg.b), dtype=acc, device=dev)
     _lib.call("fsa_cmp_attn_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(q), _lib.ptr(Kc),
@@ -80,7 +80,7 @@ def nsa_forward(q, k, v, tau, cfg):
     out_slide, lse_slide = _slide_fwd_storage(cfg, dt, q, k, v)
     out = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=dt, device=dev)
     _lib.call("fsa_gated_combine", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(out_cmp),
-              _lib.ptr(out_sel), _lib.ptr(out_slide), _lib.ptr(tau), _lib.ptr(out), st)
+              _lib.ptr(out_sel), _lib.ptr(out_slide), _lib.ptr(tau), _lib.ptr(out), 0, st)
     ctx = NSAContext(cfg, dt, q, k, v, tau, sel, inv, out_sel, lse_sel, out_slide, lse_slide,
                      out_cmp, scores)
     return out, ctx
