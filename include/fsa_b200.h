@@ -100,16 +100,20 @@ int fsa_select_topk(const fsa_shape* s, int score_dtype, const void* scores, int
 /* validate_selection (selection.py:49-75): ORs FSA_SEL_* bits into *flags (device int32). */
 int fsa_validate_selection(const fsa_shape* s, const int32_t* idx, int32_t* flags, void* stream);
 
-/* build_inverse_index (selection.py:146-169) as CSR; flags as above (nullable). */
+/* build_inverse_index (selection.py:146-169) as CSR; flags as above (nullable).
+ * work (nullable, [h_K*b + 1] int32) receives the tensor-core work plan: tasks
+ * ordered block-major (task = i*h_K + kh, heavy early blocks first), each cut
+ * into ceil(n_valid / (128/g)) items of <= 128 (token, head) rows; work[task]
+ * is the exclusive prefix of item counts. */
 size_t fsa_inverse_workspace_bytes(const fsa_shape* s);
 int fsa_build_inverse(const fsa_shape* s, const int32_t* idx, void* workspace, int32_t* offsets,
-                      int32_t* qlist, int32_t* flags, void* stream);
+                      int32_t* qlist, int32_t* work, int32_t* flags, void* stream);
 
 /* FSA block pass (kv_major.py:105-204, _core.pyx:49-94): one task per
  * (KV head, block) loads K_i/V_i once and serves all g query heads of the
  * gathered rows.  m_global ([h][N], acc) only for FSA_FWD_GLOBAL. */
 int fsa_sel_fwd(const fsa_shape* s, int dtype, int mode, const void* Q, const void* K,
-                const void* V, const int32_t* offsets, const int32_t* qlist,
+                const void* V, const int32_t* offsets, const int32_t* qlist, const int32_t* work,
                 const void* m_global, void* obuf, int obuf_dtype, void* ml, void* stream);
 
 /* Merge of per-slot partials in ascending block order (kv_major.py:207-242;
@@ -128,8 +132,8 @@ int fsa_bwd_delta(const fsa_shape* s, int dtype, const void* out, const void* dO
  * the single writer of the block (replaces the head sum at kv_major.py:342-354). */
 int fsa_sel_bwd(const fsa_shape* s, int dtype, const void* Q, const void* K, const void* V,
                 const void* dOut, const void* lse, const void* delta, const int32_t* offsets,
-                const int32_t* qlist, void* dq_buf, int dqbuf_dtype, void* dK, void* dV,
-                void* stream);
+                const int32_t* qlist, const int32_t* work, void* dq_buf, int dqbuf_dtype,
+                void* dK, void* dV, void* stream);
 
 /* dQ = ascending-block sum of dq partials (kv_major.py:326-340); [N][h][d_K] acc. */
 int fsa_dq_reduce(const fsa_shape* s, int dtype, const int32_t* idx, const void* dq_buf,

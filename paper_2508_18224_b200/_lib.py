@@ -50,11 +50,11 @@ SIGNATURES = {
     "fsa_select_topk": ([_sp, _i, _vp, _vp, _vp], _i),
     "fsa_validate_selection": ([_sp, _vp, _vp, _vp], _i),
     "fsa_inverse_workspace_bytes": ([_sp], _sz),
-    "fsa_build_inverse": ([_sp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
-    "fsa_sel_fwd": ([_sp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp], _i),
+    "fsa_build_inverse": ([_sp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
+    "fsa_sel_fwd": ([_sp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp], _i),
     "fsa_merge_fwd": ([_sp, _i, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp], _i),
     "fsa_bwd_delta": ([_sp, _i, _vp, _vp, _vp, _vp], _i),
-    "fsa_sel_bwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp], _i),
+    "fsa_sel_bwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp], _i),
     "fsa_dq_reduce": ([_sp, _i, _vp, _vp, _i, _vp, _vp], _i),
     "fsa_cmp_attn_fwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "fsa_slide_fwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp], _i),

@@ -179,6 +179,53 @@ __global__ void inverse_scan_blocks_kernel(int32_t* __restrict__ offsets, int64_
   }
 }
 
+// Work plan for the persistent tensor-core kernels: tasks in heavy-first
+// order (task = block * h_K + kv head; early blocks attract the most rows),
+// each split into ceil(n_valid / tpi) items of tpi tokens x g heads <= 128 rows.
+// work[task] = exclusive prefix of the item counts; work[h_K * b] = total.
+__global__ void work_plan_kernel(const int32_t* __restrict__ offsets, int64_t h_K, int64_t b,
+                                 int tpi, int32_t* __restrict__ work) {
+  __shared__ int32_t warp_tot[32];
+  __shared__ int32_t carry_s;
+  const int64_t ntask = h_K * b;
+  if (threadIdx.x == 0) carry_s = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int64_t c0 = 0; c0 < ntask; c0 += blockDim.x) {
+    const int64_t task = c0 + threadIdx.x;
+    int32_t v = 0;
+    if (task < ntask) {
+      const int64_t i = task / h_K, kh = task % h_K;
+      const int32_t n = offsets[kh * (b + 1) + i + 1] - offsets[kh * (b + 1) + i];
+      v = (n + tpi - 1) / tpi;
+    }
+    const int32_t own = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      int32_t u = __shfl_up_sync(0xffffffffu, v, d);
+      if (lane >= d) v += u;
+    }
+    if (lane == 31) warp_tot[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+      int32_t w = lane < nw ? warp_tot[lane] : 0;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        int32_t u = __shfl_up_sync(0xffffffffu, w, d);
+        if (lane >= d) w += u;
+      }
+      if (lane < nw) warp_tot[lane] = w;
+    }
+    __syncthreads();
+    const int32_t incl = v + (warp > 0 ? warp_tot[warp - 1] : 0) + carry_s;
+    if (task < ntask) work[task] = incl - own;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry_s = incl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) work[ntask] = carry_s;
+}
+
 }  // namespace fsa
 
 static int64_t n_tiles_of(const fsa_shape* s) { return (s->N + fsa::kInvTile - 1) / fsa::kInvTile; }
@@ -189,7 +236,8 @@ extern "C" size_t fsa_inverse_workspace_bytes(const fsa_shape* s) {
 }
 
 extern "C" int fsa_build_inverse(const fsa_shape* s, const int32_t* idx, void* workspace,
-                                 int32_t* offsets, int32_t* qlist, int32_t* flags, void* stream) {
+                                 int32_t* offsets, int32_t* qlist, int32_t* work, int32_t* flags,
+                                 void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t b = s->N / s->B_K, nt = n_tiles_of(s);
   if (s->N == 0) return FSA_OK;
@@ -208,6 +256,11 @@ extern "C" int fsa_build_inverse(const fsa_shape* s, const int32_t* idx, void* w
   fsa::inverse_scan_blocks_kernel<<<(unsigned)s->h_K, 1024, 0, st>>>(offsets, b);
   fsa::inverse_tile_kernel<true><<<grid, fsa::kInvTile, smem, st>>>(idx, s->N, s->B_K, b, (int)s->T,
                                                                     hist, offsets, qlist, nullptr);
+  if (work) {
+    const int64_t g = s->h / s->h_K;
+    const int tpi = g >= 128 ? 1 : (int)(128 / g);
+    fsa::work_plan_kernel<<<1, 1024, 0, st>>>(offsets, s->h_K, b, tpi, work);
+  }
   FSA_LAUNCH_CHECK("build_inverse");
   return FSA_OK;
 }

@@ -405,8 +405,8 @@ int dq_reduce_impl(const fsa_shape* s, const int32_t* idx, const void* dq_buf, i
 
 extern "C" int fsa_sel_fwd(const fsa_shape* s, int dtype, int mode, const void* Q, const void* K,
                            const void* V, const int32_t* offsets, const int32_t* qlist,
-                           const void* m_global, void* obuf, int obuf_dtype, void* ml,
-                           void* stream) {
+                           const int32_t* work, const void* m_global, void* obuf, int obuf_dtype,
+                           void* ml, void* stream) {
   if (mode < FSA_FWD_LOCAL || mode > FSA_FWD_GLOBAL) {
     fsa::set_error("sel_fwd: bad mode %d", mode);
     return FSA_ERR_INVALID;
@@ -416,7 +416,7 @@ extern "C" int fsa_sel_fwd(const fsa_shape* s, int dtype, int mode, const void* 
       fsa::set_error("sel_fwd: bf16 partial buffer only on the tensor-core LOCAL path");
       return FSA_ERR_INVALID;
     }
-    return fsa::tc_sel_fwd(s, Q, K, V, offsets, qlist, obuf, ml, (cudaStream_t)stream);
+    return fsa::tc_sel_fwd(s, Q, K, V, offsets, qlist, work, obuf, ml, (cudaStream_t)stream);
   }
   DISPATCH_DT(dtype, sel_fwd_impl, s, mode, Q, K, V, offsets, qlist, m_global, obuf, ml,
               (cudaStream_t)stream);
@@ -441,11 +441,11 @@ extern "C" int fsa_bwd_delta(const fsa_shape* s, int dtype, const void* out, con
 
 extern "C" int fsa_sel_bwd(const fsa_shape* s, int dtype, const void* Q, const void* K,
                            const void* V, const void* dOut, const void* lse, const void* delta,
-                           const int32_t* offsets, const int32_t* qlist, void* dq_buf,
-                           int dqbuf_dtype, void* dK, void* dV, void* stream) {
+                           const int32_t* offsets, const int32_t* qlist, const int32_t* work,
+                           void* dq_buf, int dqbuf_dtype, void* dK, void* dV, void* stream) {
   if (fsa::tc_bwd_supported(*s, dtype))
-    return fsa::tc_sel_bwd(s, Q, K, V, dOut, lse, delta, offsets, qlist, dq_buf, dqbuf_dtype, dK,
-                           dV, (cudaStream_t)stream);
+    return fsa::tc_sel_bwd(s, Q, K, V, dOut, lse, delta, offsets, qlist, work, dq_buf, dqbuf_dtype,
+                           dK, dV, (cudaStream_t)stream);
   FSA_REQUIRE(dqbuf_dtype == (dtype == FSA_DT_F64 ? FSA_DT_F64 : FSA_DT_F32),
               "sel_bwd: dq buffer dtype mismatch");
   DISPATCH_DT(dtype, sel_bwd_impl, s, Q, K, V, dOut, lse, delta, offsets, qlist, dq_buf, dK, dV,

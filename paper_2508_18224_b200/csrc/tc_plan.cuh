@@ -9,9 +9,13 @@ bool tc_fwd_supported(const fsa_shape& s, int dtype);
 bool tc_bwd_supported(const fsa_shape& s, int dtype);
 
 int tc_sel_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V,
-               const int32_t* offsets, const int32_t* qlist, void* obuf, void* ml, cudaStream_t st);
+               const int32_t* offsets, const int32_t* qlist, const int32_t* work, void* obuf,
+               void* ml, cudaStream_t st);
 int tc_sel_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V, const void* dOut,
                const void* lse, const void* delta, const int32_t* offsets, const int32_t* qlist,
-               void* dq_buf, int dqbuf_dtype, void* dK, void* dV, cudaStream_t st);
+               const int32_t* work, void* dq_buf, int dqbuf_dtype, void* dK, void* dV,
+               cudaStream_t st);
+
+int num_sms();
 
 }  // namespace fsa

@@ -111,8 +111,8 @@ def _fused_forward(cfg, dt, q, k, v, sel, inv):
     s = _lib.shape_of(cfg)
     st = _lib.stream()
     _lib.call("fsa_sel_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.FWD_LOCAL, _lib.ptr(q),
-              _lib.ptr(k), _lib.ptr(v), _lib.ptr(inv.offsets), _lib.ptr(inv.qlist), None,
-              _lib.ptr(obuf), ob_code, _lib.ptr(ml), st)
+              _lib.ptr(k), _lib.ptr(v), _lib.ptr(inv.offsets), _lib.ptr(inv.qlist), _lib.ptr(inv.work),
+              None, _lib.ptr(obuf), ob_code, _lib.ptr(ml), st)
     out = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=acc, device=dev)
     lse = torch.empty((cfg.h, cfg.N), dtype=acc, device=dev)
     _lib.call("fsa_merge_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.MERGE_LOCAL,
@@ -136,7 +136,8 @@ def compute_softmax_stats(Q, K, sel: SelectionTensor, cfg, *, shared_max: bool =
     st = _lib.stream()
     acc_code = _lib.dt_code(acc)
     _lib.call("fsa_sel_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.FWD_STATS, _lib.ptr(q),
-              _lib.ptr(k), _lib.ptr(k), _lib.ptr(inv.offsets), _lib.ptr(inv.qlist), None, None,
+              _lib.ptr(k), _lib.ptr(k), _lib.ptr(inv.offsets), _lib.ptr(inv.qlist), _lib.ptr(inv.work),
+              None, None,
               acc_code, _lib.ptr(ml), st)
     m = torch.empty((cfg.h, cfg.N), dtype=acc, device=dev)
     l = torch.empty_like(m)
@@ -165,7 +166,8 @@ def block_pass_forward(Q, K, V, inv: InverseIndex, stats: SoftmaxStats, cfg, *,
     obuf = torch.zeros((cfg.h, cfg.N, cfg.T, cfg.d_V), dtype=acc, device=dev)
     s = _lib.shape_of(cfg)
     _lib.call("fsa_sel_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.FWD_GLOBAL, _lib.ptr(q),
-              _lib.ptr(k), _lib.ptr(v), _lib.ptr(inv.offsets), _lib.ptr(inv.qlist), _lib.ptr(mg),
+              _lib.ptr(k), _lib.ptr(v), _lib.ptr(inv.offsets), _lib.ptr(inv.qlist), _lib.ptr(inv.work),
+              _lib.ptr(mg),
               _lib.ptr(obuf), _lib.dt_code(acc), None, _lib.stream())
     if meter is not None:
         meter_block_pass(meter, inv.n_valid, cfg)
@@ -235,7 +237,7 @@ def _backward_core(cfg, dt, q, k, v, do, sel, inv, out, lse):
     dV = torch.empty((cfg.N, cfg.h_K, cfg.d_V), dtype=acc, device=dev)
     _lib.call("fsa_sel_bwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(q), _lib.ptr(k),
               _lib.ptr(v), _lib.ptr(do), _lib.ptr(lse), _lib.ptr(delta), _lib.ptr(inv.offsets),
-              _lib.ptr(inv.qlist), _lib.ptr(dq_buf), dq_code, _lib.ptr(dK), _lib.ptr(dV), st)
+              _lib.ptr(inv.qlist), _lib.ptr(inv.work), _lib.ptr(dq_buf), dq_code, _lib.ptr(dK), _lib.ptr(dV), st)
     dQ = torch.empty((cfg.N, cfg.h, cfg.d_K), dtype=acc, device=dev)
     _lib.call("fsa_dq_reduce", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(sel.idx),
               _lib.ptr(dq_buf), dq_code, _lib.ptr(dQ), st)

@@ -17,7 +17,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .config import CHECK_FINITE, as_headed, to_device
+from .config import as_headed, to_device
 
 SENTINEL = -1
 
@@ -118,9 +118,10 @@ class InverseIndex:
     built on first use.
     """
 
-    def __init__(self, offsets: torch.Tensor, qlist: torch.Tensor, cfg):
+    def __init__(self, offsets: torch.Tensor, qlist: torch.Tensor, cfg, work=None):
         self.offsets = offsets
         self.qlist = qlist
+        self.work = work  # tensor-core work plan (include/fsa_b200.h)
         self._cfg = cfg
         self._n_valid = None
         self._queries = None
@@ -168,14 +169,15 @@ def build_inverse_index(sel: SelectionTensor, cfg, *, validate: bool | None = No
     ws = torch.empty(max(1, ws_bytes), dtype=torch.uint8, device=dev)
     offsets = torch.empty((cfg.h_K, cfg.b + 1), dtype=torch.int32, device=dev)
     qlist = torch.empty((cfg.h_K, cfg.N * cfg.T), dtype=torch.int32, device=dev)
+    work = torch.empty((cfg.h_K * cfg.b + 1,), dtype=torch.int32, device=dev)
     flags = torch.zeros(1, dtype=torch.int32, device=dev)
     _lib.call("fsa_build_inverse", ctypes.byref(s), _lib.ptr(sel.idx), _lib.ptr(ws),
-              _lib.ptr(offsets), _lib.ptr(qlist), _lib.ptr(flags), _lib.stream())
+              _lib.ptr(offsets), _lib.ptr(qlist), _lib.ptr(work), _lib.ptr(flags), _lib.stream())
     if validate is None:
         validate = not getattr(sel, "_trusted", False)
     if validate:
         _raise_flags(int(flags.item()))
-    inv = InverseIndex(offsets, qlist, cfg)
+    inv = InverseIndex(offsets, qlist, cfg, work)
     sel._inverse_cache = inv
     return inv
 
