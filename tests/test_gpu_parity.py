@@ -184,7 +184,7 @@ def test_selected_backward_golden(name):
     dQ, dK, dV, meter = kv_major.selected_backward(Q, K, V, fsa.SelectionTensor(z["idx"]), dO, cfg)
     tol = "f64" if z["dQ"].dtype == np.float64 else "f32"
     for got, key in ((dQ, "dQ"), (dK, "dK"), (dV, "dV")):
-        assert_close(host(got)[::st], z[key], tol, f"{name} {key}")
+        assert_close(host(got)[::st], z[key], tol, f"{name} {key}", grad=True)
     want = json.loads(str(z["meter_bwd"]))
     got = {k: dict(bytes_loaded=p.bytes_loaded, bytes_stored=p.bytes_stored, flops=p.flops,
                    task_count=p.task_count, inner_iterations=p.inner_iterations)
@@ -216,7 +216,7 @@ def test_selected_fwd_bwd_vs_oracle(kw, run_dt):
     want = O.selected_backward(Q, K, V, idx, dO, c)
     got = kv_major.selected_backward(tQ, tK, tV, sel, tdO, cfg)
     for g_, w_, name in zip(got[:3], want, ("dQ", "dK", "dV")):
-        assert_close(host(g_), w_, run_dt, name)
+        assert_close(host(g_), w_, run_dt, name, grad=True)
 
 
 def test_acceptance_sweep_golden():
@@ -335,4 +335,4 @@ def test_nsa_step_vs_oracle(run_dt):
     gs = O.selected_backward(Q, K, V, idx, dO * tau[:, 1][:, None, None], c)
     gl = O.sliding_backward(Q, K, V, dO * tau[:, 2][:, None, None], c)
     for got, a, b, name in zip((dQ, dK, dV), gs, gl, ("dQ", "dK", "dV")):
-        assert_close(host(got.permute(0, 2, 1)), a + b, run_dt, name)
+        assert_close(host(got.permute(0, 2, 1)), a + b, run_dt, name, grad=True)
