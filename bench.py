@@ -143,10 +143,14 @@ def run_ours(args, rank, world, local_rank):
         with profile(activities=[ProfilerActivity.CUDA]) as prof:
             step()
             torch.cuda.synchronize()
+        kernel_ms = {}
         for e in prof.key_averages():
             if e.device_type is not None and "fsa" in e.key and e.count:
                 kernel_names[e.key[:80]] = kernel_names.get(e.key[:80], 0) + e.count
+                t_us = getattr(e, "device_time_total", None) or getattr(e, "cuda_time_total", 0)
+                kernel_ms[e.key[:80]] = round(t_us / 1e3, 4)
         gpu_launches = sum(kernel_names.values()) * args.steps
+        kernel_names = {"launches": kernel_names, "device_ms_profiled": kernel_ms}
     except Exception as exc:  # pragma: no cover
         kernel_names = {"profiler_error": str(exc)[:120]}
 

@@ -1,0 +1,449 @@
+// FSA selected-attention backward on tcgen05 tensor cores (K8), bf16,
+// d = 128, B_K = 64.  Replaces kv_major.py:297-324 / _core.pyx:97-131 and the
+// per-group dK/dV head sum (kv_major.py:342-354): one task = one (kv head,
+// block i); all g query heads of every gathered row are processed against
+// K_i / V_i held in shared memory, and dK_i, dV_i accumulate in TMEM across
+// the whole task (single writer, fixed order -> deterministic).
+//
+// Per 128-row item (TPI tokens x g heads), rows = gathered (token, slot):
+//   S   = Q K^T          M128 N64  K128   TMEM
+//   dP  = dO V^T         M128 N64  K128   TMEM
+//   P   = exp(S*scale - lse),  dS = P * (dP - delta)      (softmax warps, bf16 -> smem)
+//   dV^T += dO^T P       M128(d) N64 K128(rows)  TMEM accumulator
+//   dK^T += Q^T dS       M128(d) N64 K128(rows)  TMEM accumulator
+//   dQ_i  = dS K         M128 N128 K64           TMEM -> bf16 partial row of dq_buf
+// dQ partials are summed over the token's selected blocks in ascending block
+// order by the dq_reduce kernel (kv_major.py:326-340).
+//
+// Roles: warps 0-3 softmax/dS + epilogues (thread = TMEM lane), warps 4-7
+// cp.async gather loaders (Q and dO rows of an item, K/V per task), warp 8
+// MMA issuer (S/dP of item n+1 issued ahead of the dV/dK/dQ products of n).
+// Tasks are claimed dynamically, head-major (tc_sched.cuh).
+#include "tc_plan.cuh"
+#include "tc_sched.cuh"
+
+namespace fsa {
+namespace {
+
+using namespace tc;
+
+constexpr int kD = 128, kBK = 64, kRows = 128;
+constexpr int kThreads = 9 * 32;
+
+constexpr uint32_t kTile = kRows * kD * 2;  // 32768: [2 halves][128][128 B]
+constexpr uint32_t kOffQ = 0;               // Q[2]
+constexpr uint32_t kOffDO = 2 * kTile;      // dO[2]
+constexpr uint32_t kOffK = 4 * kTile;       // K [2 halves][64][128 B] = 16384
+constexpr uint32_t kOffV = kOffK + 16384;
+constexpr uint32_t kOffP = kOffV + 16384;   // P  [128][128 B]
+constexpr uint32_t kOffDS = kOffP + 16384;  // dS [128][128 B]
+constexpr uint32_t kStStride = 80;          // dq staging: 32 rows x (64 + 16) B per warp
+constexpr uint32_t kOffSt = kOffDS + 16384;
+constexpr uint32_t kOffBar = kOffSt + 4 * 32 * kStStride;
+enum {
+  B_QDF = 0, B_QDE = 2, B_KVF = 4, B_KVE = 5, B_SDF = 6, B_SDE = 8, B_PDF = 10, B_PDE = 11,
+  B_DQF = 12, B_DQE = 13, B_KAF = 14, B_KAE = 15, B_RF = 16, B_RE = 20, kNumBars = 24
+};
+constexpr uint32_t kOffRing = kOffBar + kNumBars * 8;
+constexpr uint32_t kOffTmem = kOffRing + 16;
+constexpr uint32_t kSmemBytes = kOffTmem + 16 + 1024;
+
+// TMEM columns
+constexpr uint32_t kColS = 0, kColDP = 128, kColDQ = 256, kColDK = 384, kColDV = 448;
+
+constexpr uint32_t kIdS = idesc_bf16(128, 64, false, false);     // S, dP
+constexpr uint32_t kIdKV = idesc_bf16(128, 64, true, true);      // dV^T, dK^T
+constexpr uint32_t kIdQ = idesc_bf16(128, 128, false, true);     // dQ
+
+struct Params {
+  const __nv_bfloat16 *Q, *K, *V, *dO;
+  const float *lse, *delta;
+  const int32_t *offsets, *qlist;
+  int32_t* counter;
+  __nv_bfloat16* dq;  // [h][N][T][128]
+  float *dK, *dV;     // [N][h_K][128]
+  int64_t N, h, h_K, T, b, g, ntask;
+  int tpi;
+  float scale, scale_log2;
+};
+
+// FIFO of non-empty tasks handed from the MMA thread's look-ahead iterator
+struct TaskFifo {
+  int32_t task[4];
+  int head = 0, tail = 0;
+  __device__ void push(int32_t t) { task[tail++ & 3] = t; }
+  __device__ int32_t pop() { return task[head++ & 3]; }
+};
+
+__device__ __forceinline__ void load_rows(uint32_t dst, const __nv_bfloat16* src, int r, bool ok,
+                                          uint32_t half_stride) {
+#pragma unroll
+  for (int c = 0; c < 16; ++c)
+    cp_async16_zfill(dst + (c >> 3) * half_stride + sw128_off(r, c & 7), ok ? src + c * 8 : src,
+                     ok ? 16u : 0u);
+}
+
+__global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sb = smem_u32(smem);
+  auto bar = [&](int k) { return sb + kOffBar + 8u * (uint32_t)k; };
+  Ring ring{bar(B_RF), bar(B_RE), reinterpret_cast<volatile int32_t*>(smem + kOffRing)};
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffTmem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(bar(B_QDF + s), 128);
+      mbar_init(bar(B_QDE + s), 1);
+      mbar_init(bar(B_SDF + s), 1);
+      mbar_init(bar(B_SDE + s), 128);
+    }
+    mbar_init(bar(B_KVF), 128);
+    mbar_init(bar(B_KVE), 1);
+    mbar_init(bar(B_PDF), 128);
+    mbar_init(bar(B_PDE), 1);
+    mbar_init(bar(B_DQF), 1);
+    mbar_init(bar(B_DQE), 128);
+    mbar_init(bar(B_KAF), 1);
+    mbar_init(bar(B_KAE), 128);
+    for (int k = 0; k < kRingDepth; ++k) {
+      mbar_init(bar(B_RF + k), 1);
+      mbar_init(bar(B_RE + k), 257);  // 128 compute + 128 loader + 1 MMA
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc<512>(smem_u32(tmem_slot));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp >= 4 && warp < 8) {
+    // ================================================================ loaders
+    const int lr = threadIdx.x - 128;
+    int64_t n = 0, kseq = 0;
+    for (int k = 0;; ++k) {
+      if (lr == 0) ring.produce(k, p.counter, p.ntask);
+      const int32_t task = ring.consume(k);
+      if (task < 0) break;
+      const TaskRows tr = task_rows(task, p.offsets, p.b, p.tpi);
+      if (tr.nitems == 0) continue;
+      mbar_wait(bar(B_KVE), (uint32_t)((kseq & 1) ^ 1));
+      {
+        const int rr = lr & 63;
+        const __nv_bfloat16* src = (lr < 64 ? p.K : p.V) + ((tr.i * kBK + rr) * p.h_K + tr.kh) * kD;
+        load_rows(sb + (lr < 64 ? kOffK : kOffV), src, rr, true, 8192u);
+      }
+      for (int c = 0; c < tr.nitems; ++c, ++n) {
+        const int s = (int)(n & 1);
+        mbar_wait(bar(B_QDE + s), (uint32_t)(((n >> 1) & 1) ^ 1));
+        const int64_t kt = lr / p.g, hh = lr % p.g;
+        const int64_t pos = (int64_t)c * p.tpi + kt;
+        const bool ok = kt < p.tpi && pos < tr.ntok;
+        int64_t row = 0;
+        if (ok) {
+          const int32_t ent = p.qlist[tr.kh * p.N * p.T + tr.beg + pos];
+          row = (ent / p.T) * p.h + tr.kh * p.g + hh;
+        }
+        load_rows(sb + kOffQ + s * kTile, p.Q + row * kD, lr, ok, 16384u);
+        load_rows(sb + kOffDO + s * kTile, p.dO + row * kD, lr, ok, 16384u);
+        cp_async_wait_all();
+        fence_proxy_async();
+        if (c == 0) mbar_arrive(bar(B_KVF));
+        mbar_arrive(bar(B_QDF + s));
+      }
+      ++kseq;
+    }
+  } else if (warp == 8) {
+    // ================================================================ MMA issuer
+    if (lane == 0) {
+      const uint32_t tS = tmem + kColS, tDP = tmem + kColDP, tQ = tmem + kColDQ;
+      const uint32_t tK = tmem + kColDK, tV = tmem + kColDV;
+      TaskFifo fifo;
+      // look-ahead iterator (S/dP)
+      int ka = 0;
+      int32_t a_task = -1;
+      TaskRows a_tr{};
+      int a_c = 0;
+      bool a_done = false;
+      int64_t a_kseq = -1;
+      auto a_next = [&]() -> bool {  // advance to the next item; false when exhausted
+        if (a_done) return false;
+        if (a_task >= 0 && a_c + 1 < a_tr.nitems) {
+          ++a_c;
+          return true;
+        }
+        for (;;) {
+          const int32_t t = ring.consume(ka++);
+          if (t < 0) {
+            a_done = true;
+            return false;
+          }
+          const TaskRows tr = task_rows(t, p.offsets, p.b, p.tpi);
+          if (tr.nitems == 0) continue;
+          a_task = t;
+          a_tr = tr;
+          a_c = 0;
+          ++a_kseq;
+          fifo.push(t);
+          return true;
+        }
+      };
+      auto issue_sdp = [&](int64_t n, int64_t kseq) {
+        const int s = (int)(n & 1);
+        mbar_wait(bar(B_KVF), (uint32_t)(kseq & 1));
+        mbar_wait(bar(B_QDF + s), (uint32_t)((n >> 1) & 1));
+        mbar_wait(bar(B_SDE + s), (uint32_t)(((n >> 1) & 1) ^ 1));
+        tc_fence_after();
+        const uint32_t q = sb + kOffQ + s * kTile, o = sb + kOffDO + s * kTile;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t ko = (k >> 2) * 16384u + (k & 3) * 32u, kk = (k >> 2) * 8192u + (k & 3) * 32u;
+          mma_bf16(tS + s * 64, desc_kmajor(q + ko), desc_kmajor(sb + kOffK + kk), kIdS, k > 0);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t ko = (k >> 2) * 16384u + (k & 3) * 32u, kk = (k >> 2) * 8192u + (k & 3) * 32u;
+          mma_bf16(tDP + s * 64, desc_kmajor(o + ko), desc_kmajor(sb + kOffV + kk), kIdS, k > 0);
+        }
+        mma_commit(bar(B_SDF + s));
+      };
+      bool have = a_next();
+      int64_t n_ahead = 0;
+      if (have) issue_sdp(0, a_kseq);
+      int64_t kseq_b = -1;
+      TaskRows b_tr{};
+      int b_c = 0;
+      for (int64_t n = 0; have; ++n) {
+        // identify item n for the back half (follows the FIFO of non-empty tasks)
+        if (n == 0 || b_c + 1 >= b_tr.nitems) {
+          const int32_t t = fifo.pop();
+          b_tr = task_rows(t, p.offsets, p.b, p.tpi);
+          b_c = 0;
+          ++kseq_b;
+        } else {
+          ++b_c;
+        }
+        const bool first = b_c == 0, last = b_c + 1 == b_tr.nitems;
+        // look ahead: S/dP of item n+1
+        have = a_next();
+        if (have) issue_sdp(++n_ahead, a_kseq);
+        // back half of item n
+        const int s = (int)(n & 1);
+        mbar_wait(bar(B_PDF), (uint32_t)(n & 1));
+        mbar_wait(bar(B_DQE), (uint32_t)((n & 1) ^ 1));
+        if (first) mbar_wait(bar(B_KAE), (uint32_t)((kseq_b & 1) ^ 1));
+        tc_fence_after();
+        const uint32_t q = sb + kOffQ + s * kTile, o = sb + kOffDO + s * kTile;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          mma_bf16(tV, desc_mnmajor(o + k * 2048u, 16384u), desc_mnmajor(sb + kOffP + k * 2048u, 8192u),
+                   kIdKV, (first && k == 0) ? 0u : 1u);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          mma_bf16(tK, desc_mnmajor(q + k * 2048u, 16384u), desc_mnmajor(sb + kOffDS + k * 2048u, 8192u),
+                   kIdKV, (first && k == 0) ? 0u : 1u);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          mma_bf16(tQ, desc_kmajor(sb + kOffDS + k * 32u), desc_mnmajor(sb + kOffK + k * 2048u, 8192u),
+                   kIdQ, k > 0);
+        mma_commit(bar(B_DQF));
+        mma_commit(bar(B_PDE));
+        mma_commit(bar(B_QDE + s));
+        if (last) {
+          mma_commit(bar(B_KAF));
+          mma_commit(bar(B_KVE));
+        }
+      }
+    }
+  } else {
+    // ================================================================ softmax / dS / epilogues
+    const int r = threadIdx.x;
+    const uint32_t lb = (uint32_t)(warp * 32) << 16;
+    unsigned char* st = smem + kOffSt + warp * 32 * kStStride;
+    int64_t n = 0, kseq = 0;
+    // pending epilogue of the previous item
+    int64_t pend_row = -1;  // dq_buf row of this thread's row, -1 if invalid
+    bool pend = false, pend_last = false;
+    TaskRows pend_tr{};
+    auto dq_epilogue = [&](int64_t m) {
+      mbar_wait(bar(B_DQF), (uint32_t)(m & 1));
+      tc_fence_after();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float v[32];
+        tmem_ld32(tmem + lb + kColDQ + q * 32, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint4 u = make_uint4(pack_bf16(v[8 * c] * p.scale, v[8 * c + 1] * p.scale),
+                               pack_bf16(v[8 * c + 2] * p.scale, v[8 * c + 3] * p.scale),
+                               pack_bf16(v[8 * c + 4] * p.scale, v[8 * c + 5] * p.scale),
+                               pack_bf16(v[8 * c + 6] * p.scale, v[8 * c + 7] * p.scale));
+          *reinterpret_cast<uint4*>(st + lane * kStStride + c * 16) = u;
+        }
+        __syncwarp();
+        // 32 rows x 64 B: 8 rows per instruction, 16 B per lane
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const int rr = it * 8 + (lane >> 2), ch = lane & 3;
+          const int64_t drow = __shfl_sync(0xffffffffu, pend_row, rr);
+          const uint4 u = *reinterpret_cast<const uint4*>(st + rr * kStStride + ch * 16);
+          if (drow >= 0) *reinterpret_cast<uint4*>(p.dq + drow * kD + q * 32 + ch * 8) = u;
+        }
+        __syncwarp();
+      }
+      tc_fence_before();
+      mbar_arrive(bar(B_DQE));
+    };
+    auto kv_epilogue = [&](const TaskRows& tr, int64_t ks) {
+      mbar_wait(bar(B_KAF), (uint32_t)(ks & 1));
+      tc_fence_after();
+      float* dk = p.dK + ((tr.i * kBK) * p.h_K + tr.kh) * kD + r;
+      float* dv = p.dV + ((tr.i * kBK) * p.h_K + tr.kh) * kD + r;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        float v[32];
+        tmem_ld32(tmem + lb + kColDK + q * 32, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 32; ++c) dk[(q * 32 + c) * p.h_K * kD] = v[c] * p.scale;
+        tmem_ld32(tmem + lb + kColDV + q * 32, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 32; ++c) dv[(q * 32 + c) * p.h_K * kD] = v[c];
+      }
+      tc_fence_before();
+      mbar_arrive(bar(B_KAE));
+    };
+    for (int k = 0;; ++k) {
+      const int32_t task = ring.consume(k);
+      if (task < 0) break;
+      const TaskRows tr = task_rows(task, p.offsets, p.b, p.tpi);
+      if (tr.nitems == 0) {  // no attending rows: the block's gradients are zero
+        float* dk = p.dK + ((tr.i * kBK) * p.h_K + tr.kh) * kD + r;
+        float* dv = p.dV + ((tr.i * kBK) * p.h_K + tr.kh) * kD + r;
+        for (int key = 0; key < kBK; ++key) {
+          dk[key * p.h_K * kD] = 0.f;
+          dv[key * p.h_K * kD] = 0.f;
+        }
+        continue;
+      }
+      for (int c = 0; c < tr.nitems; ++c, ++n) {
+        const int s = (int)(n & 1);
+        const int64_t kt = r / p.g, hh = r % p.g;
+        const int64_t pos = (int64_t)c * p.tpi + kt;
+        const bool ok = kt < p.tpi && pos < tr.ntok;
+        int vis = 0;
+        int64_t drow = -1;
+        float lse_r = 0.f, dl = 0.f;
+        if (ok) {
+          const int32_t ent = p.qlist[tr.kh * p.N * p.T + tr.beg + pos];
+          const int64_t t = ent / p.T, slot = ent % p.T, j = tr.kh * p.g + hh;
+          drow = (j * p.N + t) * p.T + slot;
+          const int64_t v = t - tr.i * kBK + 1;
+          vis = v < kBK ? (int)v : kBK;
+          lse_r = p.lse[j * p.N + t] * 1.4426950408889634f;
+          dl = p.delta[j * p.N + t];
+        }
+        mbar_wait(bar(B_SDF + s), (uint32_t)((n >> 1) & 1));
+        tc_fence_after();
+        float sv[64], dp[64];
+        tmem_ld32(tmem + lb + kColS + s * 64, sv);
+        tmem_ld32(tmem + lb + kColS + s * 64 + 32, sv + 32);
+        tmem_ld32(tmem + lb + kColDP + s * 64, dp);
+        tmem_ld32(tmem + lb + kColDP + s * 64 + 32, dp + 32);
+        tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive(bar(B_SDE + s));
+        uint32_t pp[32], ds[32];
+#pragma unroll
+        for (int c2 = 0; c2 < 64; c2 += 2) {
+          const float p0 = c2 < vis ? ex2(fmaf(sv[c2], p.scale_log2, -lse_r)) : 0.f;
+          const float p1 = c2 + 1 < vis ? ex2(fmaf(sv[c2 + 1], p.scale_log2, -lse_r)) : 0.f;
+          pp[c2 >> 1] = pack_bf16(p0, p1);
+          ds[c2 >> 1] = pack_bf16(p0 * (dp[c2] - dl), p1 * (dp[c2 + 1] - dl));
+        }
+        mbar_wait(bar(B_PDE), (uint32_t)((n & 1) ^ 1));
+#pragma unroll
+        for (int c4 = 0; c4 < 8; ++c4) {
+          *reinterpret_cast<uint4*>(smem + kOffP + sw128_off(r, c4)) =
+              make_uint4(pp[4 * c4], pp[4 * c4 + 1], pp[4 * c4 + 2], pp[4 * c4 + 3]);
+          *reinterpret_cast<uint4*>(smem + kOffDS + sw128_off(r, c4)) =
+              make_uint4(ds[4 * c4], ds[4 * c4 + 1], ds[4 * c4 + 2], ds[4 * c4 + 3]);
+        }
+        fence_proxy_async();
+        mbar_arrive(bar(B_PDF));
+        if (pend) {
+          dq_epilogue(n - 1);
+          if (pend_last) kv_epilogue(pend_tr, kseq - 1);
+        }
+        pend = true;
+        pend_row = drow;
+        pend_last = c + 1 == tr.nitems;
+        pend_tr = tr;
+      }
+      ++kseq;
+    }
+    if (pend) {
+      dq_epilogue(n - 1);
+      if (pend_last) kv_epilogue(pend_tr, kseq - 1);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+}  // namespace
+
+bool tc_bwd_supported(const fsa_shape& s, int dtype) { return tc_fwd_supported(s, dtype); }
+
+int tc_sel_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V, const void* dOut,
+               const void* lse, const void* delta, const int32_t* offsets, const int32_t* qlist,
+               const int32_t* work, void* dq_buf, int dqbuf_dtype, void* dK, void* dV,
+               cudaStream_t st) {
+  FSA_REQUIRE(work != nullptr, "tensor-core backward needs the inverse work buffer");
+  FSA_REQUIRE(dqbuf_dtype == FSA_DT_BF16, "tensor-core backward writes bf16 dq partials");
+  Params p;
+  p.Q = (const __nv_bfloat16*)Q;
+  p.K = (const __nv_bfloat16*)K;
+  p.V = (const __nv_bfloat16*)V;
+  p.dO = (const __nv_bfloat16*)dOut;
+  p.lse = (const float*)lse;
+  p.delta = (const float*)delta;
+  p.offsets = offsets;
+  p.qlist = qlist;
+  p.dq = (__nv_bfloat16*)dq_buf;
+  p.dK = (float*)dK;
+  p.dV = (float*)dV;
+  p.N = s->N;
+  p.h = s->h;
+  p.h_K = s->h_K;
+  p.T = s->T;
+  p.b = s->N / s->B_K;
+  p.g = s->h / s->h_K;
+  p.ntask = p.h_K * p.b;
+  p.tpi = (int)(kRows / p.g);
+  p.scale = (float)s->scale;
+  p.scale_log2 = (float)(s->scale * 1.4426950408889634);
+  p.counter = const_cast<int32_t*>(work) + p.ntask + 1;
+  cudaMemsetAsync(p.counter, 0, sizeof(int32_t), st);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(tc_sel_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kSmemBytes);
+    attr = true;
+  }
+  tc_sel_bwd_kernel<<<num_sms(), kThreads, kSmemBytes, st>>>(p);
+  FSA_LAUNCH_CHECK("tc_sel_bwd");
+  return FSA_OK;
+}
+
+}  // namespace fsa

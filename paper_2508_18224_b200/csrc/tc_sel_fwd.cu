@@ -402,13 +402,4 @@ int tc_sel_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V,
   return FSA_OK;
 }
 
-bool tc_bwd_supported(const fsa_shape&, int) { return false; }
-
-int tc_sel_bwd(const fsa_shape*, const void*, const void*, const void*, const void*, const void*,
-               const void*, const int32_t*, const int32_t*, const int32_t*, void*, int, void*,
-               void*, cudaStream_t) {
-  set_error("tensor-core backward not available");
-  return FSA_ERR_UNSUPPORTED;
-}
-
 }  // namespace fsa
