@@ -227,9 +227,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
           ++b_c;
         }
         const bool first = b_c == 0, last = b_c + 1 == b_tr.nitems;
-        // look ahead: S/dP of item n+1
+        // look ahead: S/dP of item n+1 -- unless it starts a new task: K/V are
+        // single-buffered and only released by the back half of item n
         have = a_next();
-        if (have) issue_sdp(++n_ahead, a_kseq);
+        const bool defer = have && a_c == 0;
+        if (have && !defer) issue_sdp(++n_ahead, a_kseq);
         // back half of item n
         const int s = (int)(n & 1);
         mbar_wait(bar(B_PDF), (uint32_t)(n & 1));
@@ -256,6 +258,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
           mma_commit(bar(B_KAF));
           mma_commit(bar(B_KVE));
         }
+        if (defer) issue_sdp(++n_ahead, a_kseq);
       }
     }
   } else {

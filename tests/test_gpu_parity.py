@@ -198,6 +198,7 @@ def test_selected_backward_golden(name):
     dict(N=4096, d_K=128, d_V=128, h=8, h_K=2, B_K=64, T=16, W=512),    # Llama-shaped, short
     dict(N=2048, d_K=128, d_V=128, h=5, h_K=1, B_K=64, T=16, W=512),    # GQA 5 (Qwen3)
     dict(N=2048, d_K=128, d_V=128, h=2, h_K=2, B_K=64, T=16, W=512),    # GQA 1
+    dict(N=16384, d_K=128, d_V=128, h=8, h_K=4, B_K=64, T=16, W=512),   # >> tasks than SMs
 ])
 def test_selected_fwd_bwd_vs_oracle(kw, run_dt):
     """Oracle fed the dtype-rounded inputs, compared in that dtype's tolerance."""
