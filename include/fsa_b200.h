@@ -140,10 +140,15 @@ int fsa_dq_reduce(const fsa_shape* s, int dtype, const int32_t* idx, const void*
                   int dqbuf_dtype, void* dQ, void* stream);
 
 /* compressed_attention_forward (branches.py:47-78); scores (nullable) receives
- * importance_scores_from_compressed as a fused epilogue. */
+ * importance_scores_from_compressed as a fused epilogue -- on the tensor-core
+ * path only for the blocks a token's top-k can read (i < (t+1)//B_K, covered
+ * by the formed key tiles); call fsa_importance_scores for every block.
+ * workspace (fsa_cmp_workspace_bytes, nullable = SIMT path) holds bf16 copies
+ * of the pooled K/V for the tcgen05 kernel. */
+size_t fsa_cmp_workspace_bytes(const fsa_shape* s);
 int fsa_cmp_attn_fwd(const fsa_shape* s, int dtype, const void* Q, const void* K_cmp,
                      const void* V_cmp, const void* K_prefix, const void* V_prefix, void* out,
-                     void* lse, void* scores, void* stream);
+                     void* lse, void* scores, void* workspace, void* stream);
 
 /* sliding_attention_forward (branches.py:81-83 -> oracle.py:39-44, :64-74). */
 int fsa_slide_fwd(const fsa_shape* s, int dtype, const void* Q, const void* K, const void* V,

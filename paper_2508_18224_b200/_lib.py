@@ -56,7 +56,8 @@ SIGNATURES = {
     "fsa_bwd_delta": ([_sp, _i, _vp, _vp, _vp, _vp], _i),
     "fsa_sel_bwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp], _i),
     "fsa_dq_reduce": ([_sp, _i, _vp, _vp, _i, _vp, _vp], _i),
-    "fsa_cmp_attn_fwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
+    "fsa_cmp_workspace_bytes": ([_sp], _sz),
+    "fsa_cmp_attn_fwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "fsa_slide_fwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "fsa_slide_bwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "fsa_gated_combine": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp], _i),

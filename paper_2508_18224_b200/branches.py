@@ -47,6 +47,12 @@ def compress_kv(K, V, cfg) -> CompressedKV:
     return CompressedKV(logical(Kc), logical(Vc), logical(Kp), logical(Vp))
 
 
+def _cmp_workspace(cfg, dev):
+    s = _lib.shape_of(cfg)
+    n = _lib.lib().fsa_cmp_workspace_bytes(ctypes.byref(s))
+    return torch.empty(max(1, n), dtype=torch.uint8, device=dev)
+
+
 def _cmp_storage(cmp: CompressedKV, acc):
     return tuple(to_device(x, acc).permute(0, 2, 1).contiguous()
                  for x in (cmp.K_cmp, cmp.V_cmp, cmp.K_prefix, cmp.V_prefix))
@@ -65,11 +71,16 @@ def compressed_attention_forward(Q, cmp: CompressedKV, cfg, *, scores_out: bool 
     dev = q.device
     out = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=acc, device=dev)
     lse = torch.empty((cfg.h, cfg.N), dtype=acc, device=dev)
-    scores = torch.empty((cfg.h_K, cfg.N, cfg.b), dtype=acc, device=dev) if scores_out else None
     s = _lib.shape_of(cfg)
+    ws = _cmp_workspace(cfg, dev)
     _lib.call("fsa_cmp_attn_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(q), _lib.ptr(Kc),
-              _lib.ptr(Vc), _lib.ptr(Kp), _lib.ptr(Vp), _lib.ptr(out), _lib.ptr(lse),
-              _lib.ptr(scores), _lib.stream())
+              _lib.ptr(Vc), _lib.ptr(Kp), _lib.ptr(Vp), _lib.ptr(out), _lib.ptr(lse), None,
+              _lib.ptr(ws), _lib.stream())
+    scores = None
+    if scores_out:  # every block, causal or not (selection.py:105-120)
+        scores = torch.empty((cfg.h_K, cfg.N, cfg.b), dtype=acc, device=dev)
+        _lib.call("fsa_importance_scores", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(q),
+                  _lib.ptr(Kc), _lib.ptr(scores), _lib.stream())
     res = AttentionOutput(out=logical(out), lse=lse)
     return (res, scores) if scores_out else res
 

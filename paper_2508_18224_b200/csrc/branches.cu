@@ -24,12 +24,14 @@ __global__ void cmp_fwd_generic(const T* __restrict__ Q, const typename Acc<T>::
                                 const typename Acc<T>::type* __restrict__ Vc,
                                 const typename Acc<T>::type* __restrict__ Kp,
                                 const typename Acc<T>::type* __restrict__ Vp, typename Acc<T>::type* __restrict__ out,
-                                typename Acc<T>::type* __restrict__ lse, fsa_shape s) {
+                                typename Acc<T>::type* __restrict__ lse, fsa_shape s,
+                                int64_t ntok) {
+  // ntok < N: only the first ntok tokens (the pending ones on the tensor-core path)
   using A = typename Acc<T>::type;
   const int lane = threadIdx.x & 31;
   const int64_t wid = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (wid >= s.h * s.N) return;
-  const int64_t j = wid / s.N, t = wid % s.N, g = s.h / s.h_K, kh = j / g;
+  if (wid >= s.h * ntok) return;
+  const int64_t j = wid / ntok, t = wid % ntok, g = s.h / s.h_K, kh = j / g;
   const int64_t dK = s.d_K, dV = s.d_V;
   const T* q = Q + (t * s.h + j) * dK;
   A* o = out + (t * s.h + j) * dV;
@@ -190,15 +192,25 @@ __global__ void slide_bwd_dkdv_generic(const T* __restrict__ Q, const T* __restr
 
 template <typename T>
 int cmp_fwd_impl(const fsa_shape* s, const void* Q, const void* Kc, const void* Vc, const void* Kp,
-                 const void* Vp, void* out, void* lse, void* scores, cudaStream_t st) {
+                 const void* Vp, void* out, void* lse, void* scores, void* workspace,
+                 cudaStream_t st) {
   using A = typename Acc<T>::type;
-  const int64_t rows = s->h * s->N;
-  if (rows == 0) return FSA_OK;
-  cmp_fwd_generic<T><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(
-      (const T*)Q, (const A*)Kc, (const A*)Vc, (const A*)Kp, (const A*)Vp, (A*)out, (A*)lse, *s);
+  const int dt = sizeof(T) == 8 ? FSA_DT_F64 : (sizeof(T) == 4 ? FSA_DT_F32 : FSA_DT_BF16);
+  const bool tc = tc_qo_supported(*s, dt) && workspace != nullptr;
+  // tensor-core path: formed tokens on tcgen05, the < B_K - 1 pending ones here
+  const int64_t ntok = tc ? (s->B_K - 1 < s->N ? s->B_K - 1 : s->N) : s->N;
+  const int64_t rows = s->h * ntok;
+  if (rows > 0)
+    cmp_fwd_generic<T><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(
+        (const T*)Q, (const A*)Kc, (const A*)Vc, (const A*)Kp, (const A*)Vp, (A*)out, (A*)lse, *s,
+        ntok);
   FSA_LAUNCH_CHECK("cmp_attn_fwd");
+  if (tc) {
+    const bool fused = scores != nullptr && tc_cmp_scores_fused(*s);
+    int rc = tc_cmp_fwd(s, Q, Kc, Vc, out, lse, fused ? scores : nullptr, workspace, st);
+    if (rc || fused || scores == nullptr) return rc;
+  }
   if (scores) {
-    int dt = sizeof(T) == 8 ? FSA_DT_F64 : (sizeof(T) == 4 ? FSA_DT_F32 : FSA_DT_BF16);
     return fsa_importance_scores(s, dt, Q, Kc, scores, st);
   }
   return FSA_OK;
@@ -245,13 +257,20 @@ int slide_bwd_impl(const fsa_shape* s, const void* Q, const void* K, const void*
 
 extern "C" int fsa_cmp_attn_fwd(const fsa_shape* s, int dtype, const void* Q, const void* K_cmp,
                                 const void* V_cmp, const void* K_prefix, const void* V_prefix,
-                                void* out, void* lse, void* scores, void* stream) {
+                                void* out, void* lse, void* scores, void* workspace,
+                                void* stream) {
   DISPATCH_DT(dtype, cmp_fwd_impl, s, Q, K_cmp, V_cmp, K_prefix, V_prefix, out, lse, scores,
-              (cudaStream_t)stream);
+              workspace, (cudaStream_t)stream);
+}
+
+extern "C" size_t fsa_cmp_workspace_bytes(const fsa_shape* s) {
+  return fsa::tc_cmp_workspace_bytes(s);
 }
 
 extern "C" int fsa_slide_fwd(const fsa_shape* s, int dtype, const void* Q, const void* K,
                              const void* V, void* out, void* lse, void* stream) {
+  if (fsa::tc_qo_supported(*s, dtype))
+    return fsa::tc_slide_fwd(s, Q, K, V, out, lse, (cudaStream_t)stream);
   DISPATCH_DT(dtype, slide_fwd_impl, s, Q, K, V, out, lse, (cudaStream_t)stream);
 }
 

@@ -16,6 +16,15 @@ int tc_sel_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V, 
                const int32_t* work, void* dq_buf, int dqbuf_dtype, void* dK, void* dV,
                cudaStream_t st);
 
+// query-outer forward (tc_qo_fwd.cu): sliding window and compressed attention
+bool tc_qo_supported(const fsa_shape& s, int dtype);
+bool tc_cmp_scores_fused(const fsa_shape& s);
+int tc_slide_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V, void* out,
+                 void* lse, cudaStream_t st);
+size_t tc_cmp_workspace_bytes(const fsa_shape* s);
+int tc_cmp_fwd(const fsa_shape* s, const void* Q, const void* Kc, const void* Vc, void* out,
+               void* lse, void* scores, void* workspace, cudaStream_t st);
+
 int num_sms();
 
 }  // namespace fsa

@@ -28,7 +28,7 @@ import torch
 
 from . import _lib
 from .kv_major import _backward_core, _fused_forward
-from .branches import _slide_bwd_storage, _slide_fwd_storage
+from .branches import _cmp_workspace, _slide_bwd_storage, _slide_fwd_storage
 from .selection import SelectionTensor, build_inverse_index
 
 
@@ -67,9 +67,10 @@ def nsa_forward(q, k, v, tau, cfg):
     out_cmp = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=acc, device=dev)
     lse_cmp = torch.empty((cfg.h, cfg.N), dtype=acc, device=dev)
     scores = torch.empty((cfg.h_K, cfg.N, cfg.b), dtype=acc, device=dev)
+    ws = _cmp_workspace(cfg, dev)
     _lib.call("fsa_cmp_attn_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(q), _lib.ptr(Kc),
               _lib.ptr(Vc), _lib.ptr(Kp), _lib.ptr(Vp), _lib.ptr(out_cmp), _lib.ptr(lse_cmp),
-              _lib.ptr(scores), st)
+              _lib.ptr(scores), _lib.ptr(ws), st)
     idx = torch.empty((cfg.h_K, cfg.N, cfg.T), dtype=torch.int32, device=dev)
     _lib.call("fsa_select_topk", ctypes.byref(s), _lib.dt_code(acc), _lib.ptr(scores),
               _lib.ptr(idx), st)
