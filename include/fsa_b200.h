@@ -154,10 +154,15 @@ int fsa_cmp_attn_fwd(const fsa_shape* s, int dtype, const void* Q, const void* K
 int fsa_slide_fwd(const fsa_shape* s, int dtype, const void* Q, const void* K, const void* V,
                   void* out, void* lse, void* stream);
 
-/* Band-mask dense_backward (oracle.py:102-131 with band_mask); grads acc dtype. */
+/* Band-mask dense_backward (oracle.py:102-131 with band_mask); grads acc dtype.
+ * The bf16 tensor-core path runs the FSA backward kernel over each KV block's
+ * window of tokens and needs fsa_slide_bwd_workspace_bytes of workspace (the
+ * per-window-slot dQ partials); accumulate != 0 adds into dQ/dK/dV (sums the
+ * sliding branch onto the selected branch's gradients) -- tensor-core path only. */
+size_t fsa_slide_bwd_workspace_bytes(const fsa_shape* s, int dtype);
 int fsa_slide_bwd(const fsa_shape* s, int dtype, const void* Q, const void* K, const void* V,
                   const void* dOut, const void* lse, const void* delta, void* dQ, void* dK,
-                  void* dV, void* stream);
+                  void* dV, void* workspace, int accumulate, void* stream);
 
 /* gated_combine (branches.py:95-104): out = sum_c tau[t][c] * out_c; branch
  * outputs and tau [N][3] in acc dtype; out in acc dtype if out_acc else dtype. */

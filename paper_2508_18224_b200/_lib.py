@@ -59,7 +59,8 @@ SIGNATURES = {
     "fsa_cmp_workspace_bytes": ([_sp], _sz),
     "fsa_cmp_attn_fwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "fsa_slide_fwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp], _i),
-    "fsa_slide_bwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
+    "fsa_slide_bwd_workspace_bytes": ([_sp, _i], _sz),
+    "fsa_slide_bwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp], _i),
     "fsa_gated_combine": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp], _i),
     "fsa_gate_scale": ([_sp, _i, _vp, _vp, _i, _vp, _vp], _i),
     "fsa_check_finite": ([_i, _vp, _i64, _vp, _vp], _i),

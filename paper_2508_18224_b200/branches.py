@@ -106,19 +106,34 @@ def _slide_fwd_storage(cfg, dt, q, k, v):
     return out, lse
 
 
-def _slide_bwd_storage(cfg, dt, q, k, v, do, out, lse):
+def _slide_bwd_storage(cfg, dt, q, k, v, do, out, lse, accumulate_into=None):
+    """K11.  With ``accumulate_into=(dQ, dK, dV)`` the sliding gradients are
+    added onto those tensors in-kernel (tensor-core path) and they are returned."""
     dev, acc = q.device, _lib.acc_dtype(dt)
     s = _lib.shape_of(cfg)
     st = _lib.stream()
     delta = torch.empty((cfg.h, cfg.N), dtype=acc, device=dev)
     _lib.call("fsa_bwd_delta", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(out), _lib.ptr(do),
               _lib.ptr(delta), st)
-    dQ = torch.empty((cfg.N, cfg.h, cfg.d_K), dtype=acc, device=dev)
-    dK = torch.empty((cfg.N, cfg.h_K, cfg.d_K), dtype=acc, device=dev)
-    dV = torch.empty((cfg.N, cfg.h_K, cfg.d_V), dtype=acc, device=dev)
+    nws = _lib.lib().fsa_slide_bwd_workspace_bytes(ctypes.byref(s), _lib.dt_code(dt))
+    ws = torch.empty(nws, dtype=torch.uint8, device=dev) if nws else None
+    if accumulate_into is not None and ws is not None:
+        dQ, dK, dV = accumulate_into
+        accumulate = 1
+    else:
+        dQ = torch.empty((cfg.N, cfg.h, cfg.d_K), dtype=acc, device=dev)
+        dK = torch.empty((cfg.N, cfg.h_K, cfg.d_K), dtype=acc, device=dev)
+        dV = torch.empty((cfg.N, cfg.h_K, cfg.d_V), dtype=acc, device=dev)
+        accumulate = 0
     _lib.call("fsa_slide_bwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(q), _lib.ptr(k),
               _lib.ptr(v), _lib.ptr(do), _lib.ptr(lse), _lib.ptr(delta), _lib.ptr(dQ), _lib.ptr(dK),
-              _lib.ptr(dV), st)
+              _lib.ptr(dV), _lib.ptr(ws), accumulate, st)
+    if accumulate_into is not None and not accumulate:
+        aQ, aK, aV = accumulate_into
+        aQ += dQ
+        aK += dK
+        aV += dV
+        return aQ, aK, aV
     return dQ, dK, dV
 
 

@@ -274,8 +274,19 @@ extern "C" int fsa_slide_fwd(const fsa_shape* s, int dtype, const void* Q, const
   DISPATCH_DT(dtype, slide_fwd_impl, s, Q, K, V, out, lse, (cudaStream_t)stream);
 }
 
+extern "C" size_t fsa_slide_bwd_workspace_bytes(const fsa_shape* s, int dtype) {
+  return fsa::tc_bwd_supported(*s, dtype) ? fsa::tc_slide_bwd_workspace_bytes(s) : 0;
+}
+
 extern "C" int fsa_slide_bwd(const fsa_shape* s, int dtype, const void* Q, const void* K,
                              const void* V, const void* dOut, const void* lse, const void* delta,
-                             void* dQ, void* dK, void* dV, void* stream) {
+                             void* dQ, void* dK, void* dV, void* workspace, int accumulate,
+                             void* stream) {
+  if (fsa::tc_bwd_supported(*s, dtype)) {
+    FSA_REQUIRE(workspace != nullptr, "slide_bwd: tensor-core path needs its workspace");
+    return fsa::tc_slide_bwd(s, Q, K, V, dOut, lse, delta, dQ, dK, dV, workspace, accumulate,
+                             (cudaStream_t)stream);
+  }
+  FSA_REQUIRE(!accumulate, "slide_bwd: accumulate only on the tensor-core path");
   DISPATCH_DT(dtype, slide_bwd_impl, s, Q, K, V, dOut, lse, delta, dQ, dK, dV, (cudaStream_t)stream);
 }

@@ -25,6 +25,12 @@ size_t tc_cmp_workspace_bytes(const fsa_shape* s);
 int tc_cmp_fwd(const fsa_shape* s, const void* Q, const void* Kc, const void* Vc, void* out,
                void* lse, void* scores, void* workspace, cudaStream_t st);
 
+// sliding-window backward on the FSA backward kernel (tc_sel_bwd.cu)
+size_t tc_slide_bwd_workspace_bytes(const fsa_shape* s);
+int tc_slide_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V,
+                 const void* dOut, const void* lse, const void* delta, void* dQ, void* dK,
+                 void* dV, void* workspace, int accumulate, cudaStream_t st);
+
 int num_sms();
 
 }  // namespace fsa

@@ -63,9 +63,38 @@ struct Params {
   __nv_bfloat16* dq;  // [h][N][T][128]
   float *dK, *dV;     // [N][h_K][128]
   int64_t N, h, h_K, T, b, g, ntask;
-  int tpi;
+  int64_t W;   // sliding mode: window; T is then the number of window slots
+  int tpi, slide, accumulate;  // accumulate: dK/dV += (sliding branch onto the selected one)
   float scale, scale_log2;
 };
+
+// Rows of a task: the selected mode reads them from the inverse CSR; the
+// sliding mode (band-mask backward, oracle.py:102-131) uses the contiguous
+// window of tokens [64 i, 64 i + 63 + W - 1] that can see block i.
+__device__ __forceinline__ TaskRows rows_of(const Params& p, int32_t task) {
+  if (!p.slide) return task_rows(task, p.offsets, p.b, p.tpi);
+  TaskRows r;
+  r.kh = task / p.b;
+  r.i = task % p.b;
+  r.beg = r.i * kBK;
+  const int64_t end = r.beg + kBK + p.W - 1 < p.N ? r.beg + kBK + p.W - 1 : p.N;
+  r.ntok = end - r.beg;
+  r.nitems = (int)((r.ntok + p.tpi - 1) / p.tpi);
+  return r;
+}
+// token and slot of list position pos of a task
+__device__ __forceinline__ void token_of(const Params& p, const TaskRows& tr, int64_t pos,
+                                         int64_t& t, int64_t& slot) {
+  if (!p.slide) {
+    const int32_t ent = p.qlist[tr.kh * p.N * p.T + tr.beg + pos];
+    t = ent / p.T;
+    slot = ent % p.T;
+  } else {
+    t = tr.beg + pos;
+    const int64_t first = (t - p.W + 1 > 0 ? t - p.W + 1 : 0) / kBK;
+    slot = tr.i - first;
+  }
+}
 
 // FIFO of non-empty tasks handed from the MMA thread's look-ahead iterator
 struct TaskFifo {
@@ -128,7 +157,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
       if (lr == 0) ring.produce(k, p.counter, p.ntask);
       const int32_t task = ring.consume(k);
       if (task < 0) break;
-      const TaskRows tr = task_rows(task, p.offsets, p.b, p.tpi);
+      const TaskRows tr = rows_of(p, task);
       if (tr.nitems == 0) continue;
       mbar_wait(bar(B_KVE), (uint32_t)((kseq & 1) ^ 1));
       {
@@ -144,8 +173,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
         const bool ok = kt < p.tpi && pos < tr.ntok;
         int64_t row = 0;
         if (ok) {
-          const int32_t ent = p.qlist[tr.kh * p.N * p.T + tr.beg + pos];
-          row = (ent / p.T) * p.h + tr.kh * p.g + hh;
+          int64_t t, slot;
+          token_of(p, tr, pos, t, slot);
+          row = t * p.h + tr.kh * p.g + hh;
         }
         load_rows(sb + kOffQ + s * kTile, p.Q + row * kD, lr, ok, 16384u);
         load_rows(sb + kOffDO + s * kTile, p.dO + row * kD, lr, ok, 16384u);
@@ -181,7 +211,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
             a_done = true;
             return false;
           }
-          const TaskRows tr = task_rows(t, p.offsets, p.b, p.tpi);
+          const TaskRows tr = rows_of(p, t);
           if (tr.nitems == 0) continue;
           a_task = t;
           a_tr = tr;
@@ -220,7 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
         // identify item n for the back half (follows the FIFO of non-empty tasks)
         if (n == 0 || b_c + 1 >= b_tr.nitems) {
           const int32_t t = fifo.pop();
-          b_tr = task_rows(t, p.offsets, p.b, p.tpi);
+          b_tr = rows_of(p, t);
           b_c = 0;
           ++kseq_b;
         } else {
@@ -311,12 +341,22 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
         float v[32];
         tmem_ld32(tmem + lb + kColDK + q * 32, v);
         tmem_wait_ld();
+        if (p.accumulate) {
 #pragma unroll
-        for (int c = 0; c < 32; ++c) dk[(q * 32 + c) * p.h_K * kD] = v[c] * p.scale;
+          for (int c = 0; c < 32; ++c) dk[(q * 32 + c) * p.h_K * kD] += v[c] * p.scale;
+        } else {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) dk[(q * 32 + c) * p.h_K * kD] = v[c] * p.scale;
+        }
         tmem_ld32(tmem + lb + kColDV + q * 32, v);
         tmem_wait_ld();
+        if (p.accumulate) {
 #pragma unroll
-        for (int c = 0; c < 32; ++c) dv[(q * 32 + c) * p.h_K * kD] = v[c];
+          for (int c = 0; c < 32; ++c) dv[(q * 32 + c) * p.h_K * kD] += v[c];
+        } else {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) dv[(q * 32 + c) * p.h_K * kD] = v[c];
+        }
       }
       tc_fence_before();
       mbar_arrive(bar(B_KAE));
@@ -324,8 +364,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
     for (int k = 0;; ++k) {
       const int32_t task = ring.consume(k);
       if (task < 0) break;
-      const TaskRows tr = task_rows(task, p.offsets, p.b, p.tpi);
+      const TaskRows tr = rows_of(p, task);
       if (tr.nitems == 0) {  // no attending rows: the block's gradients are zero
+        if (p.accumulate) continue;
         float* dk = p.dK + ((tr.i * kBK) * p.h_K + tr.kh) * kD + r;
         float* dv = p.dV + ((tr.i * kBK) * p.h_K + tr.kh) * kD + r;
         for (int key = 0; key < kBK; ++key) {
@@ -339,15 +380,20 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
         const int64_t kt = r / p.g, hh = r % p.g;
         const int64_t pos = (int64_t)c * p.tpi + kt;
         const bool ok = kt < p.tpi && pos < tr.ntok;
-        int vis = 0;
+        int klo = 0, khi = -1;  // visible keys of the block: [klo, khi]
         int64_t drow = -1;
         float lse_r = 0.f, dl = 0.f;
         if (ok) {
-          const int32_t ent = p.qlist[tr.kh * p.N * p.T + tr.beg + pos];
-          const int64_t t = ent / p.T, slot = ent % p.T, j = tr.kh * p.g + hh;
+          int64_t t, slot;
+          token_of(p, tr, pos, t, slot);
+          const int64_t j = tr.kh * p.g + hh;
           drow = (j * p.N + t) * p.T + slot;
-          const int64_t v = t - tr.i * kBK + 1;
-          vis = v < kBK ? (int)v : kBK;
+          const int64_t hi = t - tr.i * kBK;
+          khi = hi < kBK - 1 ? (int)hi : kBK - 1;
+          if (p.slide) {
+            const int64_t lo = t - p.W + 1 - tr.i * kBK;
+            klo = lo > 0 ? (int)lo : 0;
+          }
           lse_r = p.lse[j * p.N + t] * 1.4426950408889634f;
           dl = p.delta[j * p.N + t];
         }
@@ -364,8 +410,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
         uint32_t pp[32], ds[32];
 #pragma unroll
         for (int c2 = 0; c2 < 64; c2 += 2) {
-          const float p0 = c2 < vis ? ex2(fmaf(sv[c2], p.scale_log2, -lse_r)) : 0.f;
-          const float p1 = c2 + 1 < vis ? ex2(fmaf(sv[c2 + 1], p.scale_log2, -lse_r)) : 0.f;
+          const float p0 = (c2 >= klo && c2 <= khi) ? ex2(fmaf(sv[c2], p.scale_log2, -lse_r)) : 0.f;
+          const float p1 = (c2 + 1 >= klo && c2 + 1 <= khi) ? ex2(fmaf(sv[c2 + 1], p.scale_log2, -lse_r)) : 0.f;
           pp[c2 >> 1] = pack_bf16(p0, p1);
           ds[c2 >> 1] = pack_bf16(p0 * (dp[c2] - dl), p1 * (dp[c2 + 1] - dl));
         }
@@ -408,21 +454,17 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
 
 bool tc_bwd_supported(const fsa_shape& s, int dtype) { return tc_fwd_supported(s, dtype); }
 
-int tc_sel_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V, const void* dOut,
-               const void* lse, const void* delta, const int32_t* offsets, const int32_t* qlist,
-               const int32_t* work, void* dq_buf, int dqbuf_dtype, void* dK, void* dV,
-               cudaStream_t st) {
-  FSA_REQUIRE(work != nullptr, "tensor-core backward needs the inverse work buffer");
-  FSA_REQUIRE(dqbuf_dtype == FSA_DT_BF16, "tensor-core backward writes bf16 dq partials");
-  Params p;
+namespace {
+Params make_params(const fsa_shape* s, const void* Q, const void* K, const void* V,
+                   const void* dOut, const void* lse, const void* delta, void* dq_buf, void* dK,
+                   void* dV) {
+  Params p{};
   p.Q = (const __nv_bfloat16*)Q;
   p.K = (const __nv_bfloat16*)K;
   p.V = (const __nv_bfloat16*)V;
   p.dO = (const __nv_bfloat16*)dOut;
   p.lse = (const float*)lse;
   p.delta = (const float*)delta;
-  p.offsets = offsets;
-  p.qlist = qlist;
   p.dq = (__nv_bfloat16*)dq_buf;
   p.dK = (float*)dK;
   p.dV = (float*)dV;
@@ -436,7 +478,10 @@ int tc_sel_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V, 
   p.tpi = (int)(kRows / p.g);
   p.scale = (float)s->scale;
   p.scale_log2 = (float)(s->scale * 1.4426950408889634);
-  p.counter = const_cast<int32_t*>(work) + p.ntask + 1;
+  return p;
+}
+
+int launch_bwd(Params& p, cudaStream_t st) {
   cudaMemsetAsync(p.counter, 0, sizeof(int32_t), st);
   static bool attr = false;
   if (!attr) {
@@ -446,6 +491,71 @@ int tc_sel_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V, 
   }
   tc_sel_bwd_kernel<<<num_sms(), kThreads, kSmemBytes, st>>>(p);
   FSA_LAUNCH_CHECK("tc_sel_bwd");
+  return FSA_OK;
+}
+
+// sliding-window dQ: ascending-block sum of the window-slot partials
+__global__ void slide_dq_reduce_kernel(const __nv_bfloat16* __restrict__ dq, float* __restrict__ dQ,
+                                       int64_t N, int64_t h, int64_t W, int64_t S, int accumulate) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (wid >= h * N) return;
+  const int64_t j = wid / N, t = wid % N;
+  const int64_t first = (t - W + 1 > 0 ? t - W + 1 : 0) / kBK, own = t / kBK;
+  const __nv_bfloat16* src = dq + ((j * N + t) * S) * kD + lane * 4;
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  for (int64_t k = 0; k <= own - first; ++k) {
+    const uint2 u = *reinterpret_cast<const uint2*>(src + k * kD);
+    const float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+    const float2 y = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+    a0 += x.x; a1 += x.y; a2 += y.x; a3 += y.y;
+  }
+  float4* o = reinterpret_cast<float4*>(dQ + (t * h + j) * kD + lane * 4);
+  if (accumulate) {
+    const float4 c = *o;
+    a0 += c.x; a1 += c.y; a2 += c.z; a3 += c.w;
+  }
+  *o = make_float4(a0, a1, a2, a3);
+}
+}  // namespace
+
+int tc_sel_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V, const void* dOut,
+               const void* lse, const void* delta, const int32_t* offsets, const int32_t* qlist,
+               const int32_t* work, void* dq_buf, int dqbuf_dtype, void* dK, void* dV,
+               cudaStream_t st) {
+  FSA_REQUIRE(work != nullptr, "tensor-core backward needs the inverse work buffer");
+  FSA_REQUIRE(dqbuf_dtype == FSA_DT_BF16, "tensor-core backward writes bf16 dq partials");
+  Params p = make_params(s, Q, K, V, dOut, lse, delta, dq_buf, dK, dV);
+  p.offsets = offsets;
+  p.qlist = qlist;
+  p.counter = const_cast<int32_t*>(work) + p.ntask + 1;
+  return launch_bwd(p, st);
+}
+
+int64_t tc_slide_slots(const fsa_shape* s) { return (s->W - 1) / kBK + 2; }
+
+size_t tc_slide_bwd_workspace_bytes(const fsa_shape* s) {
+  return (size_t)s->h * s->N * tc_slide_slots(s) * kD * sizeof(__nv_bfloat16) + 256;
+}
+
+int tc_slide_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V,
+                 const void* dOut, const void* lse, const void* delta, void* dQ, void* dK,
+                 void* dV, void* workspace, int accumulate, cudaStream_t st) {
+  const int64_t S = tc_slide_slots(s);
+  __nv_bfloat16* dq = (__nv_bfloat16*)workspace;
+  int32_t* counter = (int32_t*)((char*)workspace + (size_t)s->h * s->N * S * kD * 2);
+  Params p = make_params(s, Q, K, V, dOut, lse, delta, dq, dK, dV);
+  p.slide = 1;
+  p.accumulate = accumulate;
+  p.W = s->W;
+  p.T = S;
+  p.counter = counter;
+  int rc = launch_bwd(p, st);
+  if (rc) return rc;
+  const int64_t rows = s->h * s->N;
+  slide_dq_reduce_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(dq, (float*)dQ, s->N, s->h,
+                                                                     s->W, S, accumulate);
+  FSA_LAUNCH_CHECK("tc_slide_bwd");
   return FSA_OK;
 }
 

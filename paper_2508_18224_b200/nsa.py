@@ -100,12 +100,8 @@ def nsa_backward(ctx: NSAContext, dout):
               _lib.ptr(ctx.tau), 2, _lib.ptr(d_slide), st)
     dQ, dK, dV = _backward_core(cfg, dt, ctx.q, ctx.k, ctx.v, d_sel, ctx.sel, ctx.inv,
                                 ctx.out_sel, ctx.lse_sel)
-    sQ, sK, sV = _slide_bwd_storage(cfg, dt, ctx.q, ctx.k, ctx.v, d_slide, ctx.out_slide,
-                                    ctx.lse_slide)
-    dQ += sQ
-    dK += sK
-    dV += sV
-    return dQ, dK, dV
+    return _slide_bwd_storage(cfg, dt, ctx.q, ctx.k, ctx.v, d_slide, ctx.out_slide,
+                              ctx.lse_slide, accumulate_into=(dQ, dK, dV))
 
 
 def nsa_forward_backward(q, k, v, tau, dout, cfg):

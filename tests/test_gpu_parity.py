@@ -381,3 +381,20 @@ def test_tc_window_branches_vs_oracle(kw):
         if own:
             assert_close(fused[:, t, :own], kc16_scores[:, t, :own], "bf16", f"fused scores t={t}")
     assert full.shape == fused.shape
+
+
+@pytest.mark.parametrize("kw", [
+    dict(N=2048, d_K=128, d_V=128, h=8, h_K=2, B_K=64, T=8, W=512),
+    dict(N=1280, d_K=128, d_V=128, h=2, h_K=2, B_K=64, T=8, W=100),
+    dict(N=8192, d_K=128, d_V=128, h=8, h_K=4, B_K=64, T=8, W=512),     # many tasks per CTA
+])
+def test_tc_sliding_backward_vs_oracle(kw):
+    c = O.cfg_of(**kw)
+    cfg = _cfg(kw)
+    Q, K, V = (round_inputs(x, "bf16") for x in O.make_qkv(c, 22))
+    dO = round_inputs(O.make_dout(c, 22), "bf16")
+    tQ, tK, tV, tdO = (dev(x, torch.bfloat16) for x in (Q, K, V, dO))
+    got = fsa.sliding_attention_backward(tQ, tK, tV, tdO, cfg)
+    want = O.sliding_backward(Q, K, V, dO, c)
+    for g_, w_, name in zip(got, want, ("dQ", "dK", "dV")):
+        assert_close(host(g_), w_, "bf16", name, grad=True)
