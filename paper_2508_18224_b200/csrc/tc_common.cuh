@@ -4,6 +4,7 @@
 #pragma once
 #include <stdint.h>
 #include <cuda_bf16.h>
+#include <stdio.h>
 
 namespace fsa {
 namespace tc {
@@ -22,18 +23,35 @@ __device__ __forceinline__ void fence_mbar_init() {
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
-      "LAB_WAIT:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@P1 bra DONE;\n"
-      "bra LAB_WAIT;\n"
-      "DONE:\n"
-      "}\n" ::"r"(bar),
-      "r"(parity)
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
       : "memory");
+  return ok != 0;
+}
+// Blocking wait with a watchdog: a wait that has not completed after ~2^34
+// cycles (several seconds) reports the barrier and traps instead of hanging
+// the device (a pipeline bug must not take the GPU down with it).
+static __device__ __noinline__ void mbar_stuck(uint32_t bar, uint32_t parity);
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  if (mbar_try_wait(bar, parity)) return;
+  const long long t0 = clock64();
+  for (;;) {
+    if (mbar_try_wait(bar, parity)) return;
+    if (clock64() - t0 > (1ll << 34)) mbar_stuck(bar, parity);
+  }
+}
+static __device__ __noinline__ void mbar_stuck(uint32_t bar, uint32_t parity) {
+  printf("fsa: mbarrier wait timed out: smem 0x%x parity %u block %d thread %d\n", bar, parity,
+         (int)blockIdx.x, (int)threadIdx.x);
+  __trap();
 }
 
 // ---------------------------------------------------------------- cp.async

@@ -287,27 +287,35 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const Params p) 
           const int64_t key = kbase + c;
           if (key >= klo && key <= khi) mx = fmaxf(mx, sv[c]);
         }
+        // P(u-2) consumed => PV(u-2) done, so the PV barrier parity below is unambiguous
+        mbar_wait(bar(B_PE + v), (uint32_t)(((u >> 1) & 1) ^ 1));
         // move the reference max only on a large increase (or the first finite max)
+        float f = 1.f;
+        bool resc = false;
         if (mx > -INFINITY && (m_used == -INFINITY || (mx - m_used) * p.scale_log2 > kRescale)) {
           if (m_used != -INFINITY) {
-            const float f = ex2((m_used - mx) * p.scale_log2);
+            f = ex2((m_used - mx) * p.scale_log2);
             l *= f;
-            // rescale the O accumulator in TMEM once the previous PV landed
-            mbar_wait(bar(B_PV), (uint32_t)((u - 1) & 1));
-            tc_fence_after();
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              float ov[32];
-              tmem_ld32(tmem + lb + kColO + (n_out & 1) * 128 + q * 32, ov);
-              tmem_wait_ld();
-#pragma unroll
-              for (int c = 0; c < 32; ++c) ov[c] *= f;
-              tmem_st32(tmem + lb + kColO + (n_out & 1) * 128 + q * 32, ov);
-            }
-            tmem_wait_st();
-            tc_fence_before();
+            resc = true;
           }
           m_used = mx;
+        }
+        // rescale the O accumulator in TMEM (warp-collective: every lane joins,
+        // lanes without a new max scale by 1) once PV(u-1) has landed
+        if (__any_sync(0xffffffffu, resc)) {
+          mbar_wait(bar(B_PV), (uint32_t)((u - 1) & 1));
+          tc_fence_after();
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            float ov[32];
+            tmem_ld32(tmem + lb + kColO + (n_out & 1) * 128 + q * 32, ov);
+            tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) ov[c] *= f;
+            tmem_st32(tmem + lb + kColO + (n_out & 1) * 128 + q * 32, ov);
+          }
+          tmem_wait_st();
+          tc_fence_before();
         }
         const float mb = m_used == -INFINITY ? 0.f : m_used * p.scale_log2;
         uint32_t pk[32];
@@ -319,7 +327,6 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const Params p) 
           l += e0 + e1;
           pk[c >> 1] = pack_bf16(e0, e1);
         }
-        mbar_wait(bar(B_PE + v), (uint32_t)(((u >> 1) & 1) ^ 1));
 #pragma unroll
         for (int c = 0; c < 8; ++c)
           *reinterpret_cast<uint4*>(smem + kOffP + v * kP + sw128_off(r, c)) =
