@@ -325,8 +325,11 @@ def test_nsa_step_vs_oracle(run_dt):
     idx = O.select_topk(scores, c)
     np.testing.assert_array_equal(host(ctx.sel.idx), idx)
     cmp = O.compress_kv(K, V, c)
-    assert_close(scores, O.importance_scores(Q, cmp.K_cmp, c), "f32" if run_dt == "f32" else "bf16",
-                 "scores")
+    # the fused pipeline fills the blocks top-k can read: i < own block
+    causal = np.arange(c.b)[None, None, :] < (np.arange(c.N) // c.B_K)[None, :, None]
+    causal = np.broadcast_to(causal, scores.shape)
+    assert_close(scores[causal], O.importance_scores(Q, cmp.K_cmp, c)[causal],
+                 "f32" if run_dt == "f32" else "bf16", "scores")
     o_cmp, _ = O.compressed_forward(Q, cmp, c)
     o_sel, _ = O.selected_forward(Q, K, V, idx, c)
     o_sl, _ = O.sliding_forward(Q, K, V, c)
@@ -375,11 +378,10 @@ def test_tc_window_branches_vs_oracle(kw):
                                torch.full((cfg.N, 3), 1.0 / 3, device="cuda"), cfg)
     fused = host(ctx.scores)
     full = host(sc)
-    kc16_scores = O.importance_scores(Q, kc16, c)
-    for t in range(cfg.N):
-        own = t // cfg.B_K
-        if own:
-            assert_close(fused[:, t, :own], kc16_scores[:, t, :own], "bf16", f"fused scores t={t}")
+    causal = np.arange(c.b)[None, None, :] < (np.arange(c.N) // c.B_K)[None, :, None]
+    causal = np.broadcast_to(causal, fused.shape)
+    assert_close(fused[causal], O.importance_scores(Q, host(cmp.K_cmp).astype(np.float64), c)[causal],
+                 "bf16", "fused scores")
     assert full.shape == fused.shape
 
 
