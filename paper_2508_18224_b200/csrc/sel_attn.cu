@@ -331,6 +331,8 @@ int merge_impl(const fsa_shape* s, int mode, const int32_t* idx, const void* obu
   const int64_t rows = s->h_K * s->N;
   if (rows == 0) return FSA_OK;
   const unsigned grid = (unsigned)((rows + 7) / 8);
+  if (obuf_dtype == FSA_DT_BF16 && mode == FSA_MERGE_LOCAL && fast_reduce_ok(*s))
+    return merge_bf16_fast(s, idx, obuf, ml, out, lse, m_out, l_out, st);
   if (obuf_dtype == FSA_DT_BF16) {
     merge_generic<T, __nv_bfloat16><<<grid, 256, 0, st>>>(
         mode, idx, (const __nv_bfloat16*)obuf, (const A*)ml, (const A*)mg, (const A*)lg, (A*)out,
@@ -384,6 +386,8 @@ int dq_reduce_impl(const fsa_shape* s, const int32_t* idx, const void* dq_buf, i
   const int64_t rows = s->h * s->N;
   if (rows == 0) return FSA_OK;
   const unsigned grid = (unsigned)((rows + 7) / 8);
+  if (dqbuf_dtype == FSA_DT_BF16 && fast_reduce_ok(*s))
+    return dq_reduce_bf16_fast(s, idx, dq_buf, dQ, st);
   if (dqbuf_dtype == FSA_DT_BF16)
     dq_reduce_kernel<T, __nv_bfloat16><<<grid, 256, 0, st>>>(idx, (const __nv_bfloat16*)dq_buf,
                                                              (A*)dQ, *s);

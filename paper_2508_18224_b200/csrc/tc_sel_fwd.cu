@@ -6,18 +6,16 @@
 //
 // Persistent, warp-specialised, one CTA per SM:
 //   warps 0-3  softmax + epilogue, one TMEM lane (= MMA row) per thread
-//   warps 4-7  loaders: cp.async gather of the 128 query rows of an item
-//              (tokens x group heads) and, on a task change, the K_i / V_i block
+//   warps 4-7  loaders: cp.async gather of an item's 128 query rows (TPI
+//              tokens x g group heads); one item's gather stays in flight while
+//              the next is issued (3 Q stages); K_i/V_i per task (2 stages)
 //   warp  8    MMA issuer (one thread): S = Q K^T (M128 N64 K128) and
-//              O = P V (M128 N128 K64) into TMEM, tcgen05.commit -> mbarriers
-// Stages: Q, P, S, O double-buffered; K/V double-buffered per task.  The
-// epilogue of item n-1 overlaps the PV MMA of item n and the S MMA of n+1.
-//
-// Work: the inverse build's plan (include/fsa_b200.h, fsa_build_inverse) lists
-// items of <= 128 rows, heavy blocks first; CTA c owns the contiguous item
-// range [c W / G, (c+1) W / G), so consecutive items share K_i / V_i.
-#include "tc_common.cuh"
+//              O = P V (M128 N128 K64) into TMEM, tcgen05.commit -> mbarriers;
+//              S of item n+1 is issued before PV of item n
+// Tasks (kv head, block) are claimed dynamically in head-major order
+// (tc_sched.cuh), so the gathered Q rows of the current kv group stay in L2.
 #include "tc_plan.cuh"
+#include "tc_sched.cuh"
 
 namespace fsa {
 namespace {
@@ -25,112 +23,60 @@ namespace {
 using namespace tc;
 
 constexpr int kD = 128, kBK = 64, kRows = 128;
-constexpr int kComputeWarps = 4, kLoadWarps = 4;
-constexpr int kThreads = (kComputeWarps + kLoadWarps + 1) * 32;  // 288
+constexpr int kThreads = 9 * 32;
+constexpr int kQStages = 3;
 
-// shared-memory map (bytes from a 1024-aligned base)
-constexpr uint32_t kQBytes = kRows * kD * 2;         // 32768: [2 halves][128 rows][128 B]
-constexpr uint32_t kKVBytes = 2 * kBK * kD * 2;      // 32768: K [2][64][128 B], V [2][64][128 B]
-constexpr uint32_t kPBytes = kRows * kBK * 2;        // 16384: [128 rows][128 B]
-constexpr uint32_t kOStride = 272;                   // padded staging row (bank-conflict free)
-constexpr uint32_t kOStageBytes = kComputeWarps * 32 * kOStride;
+constexpr uint32_t kQBytes = kRows * kD * 2;     // 32768: [2 halves][128 rows][128 B]
+constexpr uint32_t kKVBytes = 2 * kBK * kD * 2;  // 32768: K [2][64][128 B], V [2][64][128 B]
+constexpr uint32_t kPBytes = kRows * kBK * 2;    // 16384: [128 rows][128 B]
+constexpr uint32_t kStStride = 80;               // epilogue staging: 32 rows x (64 + 16) B per warp
 constexpr uint32_t kOffQ = 0;
-constexpr uint32_t kOffKV = kOffQ + 2 * kQBytes;
+constexpr uint32_t kOffKV = kOffQ + kQStages * kQBytes;
 constexpr uint32_t kOffP = kOffKV + 2 * kKVBytes;
-constexpr uint32_t kOffO = kOffP + 2 * kPBytes;
-constexpr uint32_t kOffBar = kOffO + kOStageBytes;
-constexpr uint32_t kNumBars = 20;
-constexpr uint32_t kOffTmem = kOffBar + kNumBars * 8;
-constexpr uint32_t kSmemBytes = kOffTmem + 16 + 1024;  // + alignment slack
-
-// barrier indices (x2 stages each)
-enum { B_QF = 0, B_QE = 2, B_KVF = 4, B_KVE = 6, B_SF = 8, B_SE = 10, B_PF = 12, B_PE = 14,
-       B_OF = 16, B_OE = 18 };
+constexpr uint32_t kOffSt = kOffP + 2 * kPBytes;
+constexpr uint32_t kOffBar = kOffSt + 4 * 32 * kStStride;
+enum { B_QF = 0, B_QE = 3, B_KVF = 6, B_KVE = 8, B_SF = 10, B_SE = 12, B_PF = 14, B_PE = 16,
+       B_OF = 18, B_OE = 20, B_RF = 22, B_RE = 26, kNumBars = 30 };
+constexpr uint32_t kOffRing = kOffBar + kNumBars * 8;
+constexpr uint32_t kOffTmem = kOffRing + 16;
+constexpr uint32_t kSmemBytes = kOffTmem + 16 + 1024;
 
 constexpr uint32_t kIdescS = idesc_bf16(128, 64, false, false);
 constexpr uint32_t kIdescPV = idesc_bf16(128, 128, false, true);
 
 struct Params {
-  const __nv_bfloat16* Q;
-  const __nv_bfloat16* K;
-  const __nv_bfloat16* V;
-  const int32_t* offsets;
-  const int32_t* qlist;
-  const int32_t* work;
+  const __nv_bfloat16 *Q, *K, *V;
+  const int32_t *offsets, *qlist;
+  int32_t* counter;
   __nv_bfloat16* obuf;
   float* ml;
-  int64_t N, h, h_K, T, b, g;
-  int tpi;
+  int N, h, h_K, T, b, g, ntask, tpi;
   float scale_log2, scale;
 };
 
-// Walks the contiguous item range of this CTA; tracks task changes (kseq).
-struct Walker {
-  const int32_t* work;
-  int64_t ntask, task, w, w_end;
-  int64_t kseq;
-  bool first;
-  __device__ void init(const Params& p) {
-    work = p.work;
-    ntask = p.h_K * p.b;
-    const int64_t W = work[ntask];
-    const int64_t G = gridDim.x, c = blockIdx.x;
-    w = W * c / G;
-    w_end = W * (c + 1) / G;
-    int64_t lo = 0, hi = ntask - 1;
-    while (lo < hi) {  // largest task with work[task] <= w
-      const int64_t mid = (lo + hi + 1) >> 1;
-      if (work[mid] <= w) lo = mid; else hi = mid - 1;
-    }
-    task = lo;
-    kseq = -1;
-    first = true;
-  }
-  __device__ bool valid() const { return w < w_end; }
-  // position on item w; returns true when the task changed (new K/V block)
-  __device__ bool settle() {
-    bool changed = first;
-    while (work[task + 1] <= w) {
-      ++task;
-      changed = true;
-    }
-    first = false;
-    if (changed) ++kseq;
-    return changed;
-  }
-  __device__ bool last_of_task() const { return w + 1 >= w_end || work[task + 1] <= w + 1; }
-  __device__ int64_t chunk() const { return w - work[task]; }
+struct TaskFifo {
+  int32_t task[4];
+  int head = 0, tail = 0;
+  __device__ void push(int32_t t) { task[tail++ & 3] = t; }
+  __device__ int32_t pop() { return task[head++ & 3]; }
 };
-
-struct Item {
-  int64_t i, kh, beg, ntok, p0, nrows_tok;
-};
-__device__ __forceinline__ Item item_of(const Params& p, const Walker& wk) {
-  Item it;
-  it.i = wk.task / p.h_K;
-  it.kh = wk.task % p.h_K;
-  const int32_t* off = p.offsets + it.kh * (p.b + 1) + it.i;
-  it.beg = off[0];
-  it.ntok = off[1] - off[0];
-  it.p0 = wk.chunk() * p.tpi;
-  it.nrows_tok = min((int64_t)p.tpi, it.ntok - it.p0);
-  return it;
-}
 
 __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const Params p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t sbase = smem_u32(smem);
-  const uint32_t bar0 = sbase + kOffBar;
-  auto bar = [&](int k) { return bar0 + 8u * (uint32_t)k; };
+  const uint32_t sb = smem_u32(smem);
+  auto bar = [&](int k) { return sb + kOffBar + 8u * (uint32_t)k; };
+  Ring ring{bar(B_RF), bar(B_RE), reinterpret_cast<volatile int32_t*>(smem + kOffRing)};
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffTmem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < kQStages; ++s) {
       mbar_init(bar(B_QF + s), 128);
       mbar_init(bar(B_QE + s), 1);
+    }
+    for (int s = 0; s < 2; ++s) {
       mbar_init(bar(B_KVF + s), 128);
       mbar_init(bar(B_KVE + s), 1);
       mbar_init(bar(B_SF + s), 1);
@@ -140,6 +86,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const Params p)
       mbar_init(bar(B_OF + s), 1);
       mbar_init(bar(B_OE + s), 128);
     }
+    for (int k = 0; k < kRingDepth; ++k) {
+      mbar_init(bar(B_RF + k), 1);
+      mbar_init(bar(B_RE + k), 257);
+    }
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc<512>(smem_u32(tmem_slot));
@@ -148,120 +98,196 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const Params p)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp >= kComputeWarps && warp < kComputeWarps + kLoadWarps) {
+  if (warp >= 4 && warp < 8) {
     // ------------------------------------------------------------ loaders
-    const int r = threadIdx.x - kComputeWarps * 32;  // 0..127
-    Walker wk;
-    wk.init(p);
-    for (int64_t n = 0; wk.valid(); ++n, ++wk.w) {
-      const bool newkv = wk.settle();
-      const Item it = item_of(p, wk);
-      const int s = (int)(n & 1);
-      const int kvs = (int)(wk.kseq & 1);
-      if (newkv) {
-        mbar_wait(bar(B_KVE + kvs), (uint32_t)(((wk.kseq >> 1) & 1) ^ 1));
-        const int rr = r & 63;
-        const __nv_bfloat16* src = (r < 64 ? p.K : p.V) + ((it.i * kBK + rr) * p.h_K + it.kh) * kD;
-        const uint32_t dst = sbase + kOffKV + kvs * kKVBytes + (r < 64 ? 0u : 16384u);
+    const int lr = threadIdx.x - 128;
+    const int kt_row = lr / p.g, hh = lr % p.g;
+    int n = 0, kseq = 0;
+    int prev_stage = -1;
+    for (int k = 0;; ++k) {
+      if (lr == 0) ring.produce(k, p.counter, p.ntask);
+      const int32_t task = ring.consume(k);
+      if (task < 0) break;
+      const TaskRows tr = task_rows(task, p.offsets, p.b, p.tpi);
+      if (tr.nitems == 0) continue;
+      const int kvs = kseq & 1;
+      mbar_wait(bar(B_KVE + kvs), (uint32_t)(((kseq >> 1) & 1) ^ 1));
+      {
+        const int rr = lr & 63;
+        const __nv_bfloat16* src =
+            (lr < 64 ? p.K : p.V) + ((int)(tr.i * kBK + rr) * p.h_K + (int)tr.kh) * kD;
+        const uint32_t dst = sb + kOffKV + kvs * kKVBytes + (lr < 64 ? 0u : 16384u);
 #pragma unroll
-        for (int c = 0; c < 16; ++c)
-          cp_async16(dst + (c >> 3) * 8192u + sw128_off(rr, c & 7), src + c * 8);
+        for (int c = 0; c < 16; ++c) cp_async16(dst + (c >> 3) * 8192u + sw128_off(rr, c & 7), src + c * 8);
+        asm volatile("cp.async.commit_group;" ::: "memory");
       }
-      mbar_wait(bar(B_QE + s), (uint32_t)(((n >> 1) & 1) ^ 1));
-      const int64_t k = r / p.g, hh = r % p.g;
-      if (k < it.nrows_tok) {
-        const int32_t ent = p.qlist[it.kh * p.N * p.T + it.beg + it.p0 + k];
-        const int64_t t = ent / p.T;
-        const __nv_bfloat16* src = p.Q + (t * p.h + it.kh * p.g + hh) * kD;
-        const uint32_t dst = sbase + kOffQ + s * kQBytes;
+      bool kv_pending = true;
+      const int32_t* ql = p.qlist + (int64_t)tr.kh * p.N * p.T + tr.beg;
+      for (int c = 0; c < tr.nitems; ++c, ++n) {
+        const int s = n % kQStages;
+        mbar_wait(bar(B_QE + s), (uint32_t)(((n / kQStages) & 1) ^ 1));
+        const int pos = c * p.tpi + kt_row;
+        if (kt_row < p.tpi && pos < tr.ntok) {
+          const int t = __ldg(ql + pos) / p.T;
+          const __nv_bfloat16* src = p.Q + (t * p.h + (int)tr.kh * p.g + hh) * kD;
+          const uint32_t dst = sb + kOffQ + s * kQBytes;
 #pragma unroll
-        for (int c = 0; c < 16; ++c)
-          cp_async16(dst + (c >> 3) * 16384u + sw128_off(r, c & 7), src + c * 8);
+          for (int cc = 0; cc < 16; ++cc)
+            cp_async16(dst + (cc >> 3) * 16384u + sw128_off(lr, cc & 7), src + cc * 8);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        // everything but this item's gather has landed: publish it
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        fence_proxy_async();
+        if (kv_pending) {
+          mbar_arrive(bar(B_KVF + kvs));
+          kv_pending = false;
+        }
+        if (prev_stage >= 0) mbar_arrive(bar(B_QF + prev_stage));
+        prev_stage = s;
       }
-      cp_async_wait_all();
-      fence_proxy_async();
-      if (newkv) mbar_arrive(bar(B_KVF + kvs));
-      mbar_arrive(bar(B_QF + s));
+      ++kseq;
     }
-  } else if (warp == kComputeWarps + kLoadWarps) {
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    fence_proxy_async();
+    if (prev_stage >= 0) mbar_arrive(bar(B_QF + prev_stage));
+  } else if (warp == 8) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
-      Walker ws, wp;  // S runs one item ahead of PV
-      ws.init(p);
-      wp.init(p);
       const uint32_t tS = tmem, tO = tmem + 128;
-      auto issue_S = [&](int64_t n) {
-        ws.settle();
-        const int s = (int)(n & 1);
-        const int kvs = (int)(ws.kseq & 1);
-        mbar_wait(bar(B_KVF + kvs), (uint32_t)((ws.kseq >> 1) & 1));
-        mbar_wait(bar(B_QF + s), (uint32_t)((n >> 1) & 1));
-        mbar_wait(bar(B_SE + s), (uint32_t)(((n >> 1) & 1) ^ 1));
-        tc_fence_after();
-        fence_proxy_async();
-        const uint32_t qa = sbase + kOffQ + s * kQBytes;
-        const uint32_t ka = sbase + kOffKV + kvs * kKVBytes;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint64_t ad = desc_kmajor(qa + (k >> 2) * 16384u + (k & 3) * 32u);
-          const uint64_t bd = desc_kmajor(ka + (k >> 2) * 8192u + (k & 3) * 32u);
-          mma_bf16(tS + s * 64, ad, bd, kIdescS, k > 0);
+      TaskFifo fifo;
+      int ka = 0, a_c = 0, a_kseq = -1;
+      TaskRows a_tr{};
+      bool a_done = false, a_started = false;
+      auto a_next = [&]() -> bool {
+        if (a_done) return false;
+        if (a_started && a_c + 1 < a_tr.nitems) {
+          ++a_c;
+          return true;
         }
-        mma_commit(bar(B_SF + s));
-        mma_commit(bar(B_QE + s));
-        ++ws.w;
+        for (;;) {
+          const int32_t t = ring.consume(ka++);
+          if (t < 0) {
+            a_done = true;
+            return false;
+          }
+          const TaskRows tr = task_rows(t, p.offsets, p.b, p.tpi);
+          if (tr.nitems == 0) continue;
+          a_tr = tr;
+          a_c = 0;
+          a_started = true;
+          ++a_kseq;
+          fifo.push(t);
+          return true;
+        }
       };
-      int64_t n = 0;
-      if (ws.valid()) issue_S(0);
-      for (; wp.valid(); ++n, ++wp.w) {
-        wp.settle();
-        if (ws.valid()) issue_S(n + 1);
-        const int s = (int)(n & 1);
-        const int kvs = (int)(wp.kseq & 1);
-        mbar_wait(bar(B_PF + s), (uint32_t)((n >> 1) & 1));
-        mbar_wait(bar(B_OE + s), (uint32_t)(((n >> 1) & 1) ^ 1));
+      auto issue_s = [&](int n, int kseq) {
+        const int s = n % kQStages, v = n & 1, kvs = kseq & 1;
+        mbar_wait(bar(B_KVF + kvs), (uint32_t)((kseq >> 1) & 1));
+        mbar_wait(bar(B_QF + s), (uint32_t)((n / kQStages) & 1));
+        mbar_wait(bar(B_SE + v), (uint32_t)(((n >> 1) & 1) ^ 1));
         tc_fence_after();
-        const uint32_t pa = sbase + kOffP + s * kPBytes;
-        const uint32_t va = sbase + kOffKV + kvs * kKVBytes + 16384u;
+        const uint32_t qa = sb + kOffQ + s * kQBytes;
+        const uint32_t ka_ = sb + kOffKV + kvs * kKVBytes;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const uint64_t ad = desc_kmajor(pa + k * 32u);
-          const uint64_t bd = desc_mnmajor(va + k * 2048u, 8192u);
-          mma_bf16(tO + s * 128, ad, bd, kIdescPV, k > 0);
+        for (int k = 0; k < 8; ++k)
+          mma_bf16(tS + v * 64, desc_kmajor(qa + (k >> 2) * 16384u + (k & 3) * 32u),
+                   desc_kmajor(ka_ + (k >> 2) * 8192u + (k & 3) * 32u), kIdescS, k > 0);
+        mma_commit(bar(B_SF + v));
+        mma_commit(bar(B_QE + s));
+      };
+      bool have = a_next();
+      int n_ahead = 0;
+      if (have) issue_s(0, a_kseq);
+      int b_kseq = -1, b_c = 0;
+      TaskRows b_tr{};
+      for (int n = 0; have; ++n) {
+        if (n == 0 || b_c + 1 >= b_tr.nitems) {
+          b_tr = task_rows(fifo.pop(), p.offsets, p.b, p.tpi);
+          b_c = 0;
+          ++b_kseq;
+        } else {
+          ++b_c;
         }
-        mma_commit(bar(B_OF + s));
-        mma_commit(bar(B_PE + s));
-        if (wp.last_of_task()) mma_commit(bar(B_KVE + kvs));
+        const bool last = b_c + 1 == b_tr.nitems;
+        have = a_next();
+        if (have) issue_s(++n_ahead, a_kseq);
+        const int v = n & 1, kvs = b_kseq & 1;
+        mbar_wait(bar(B_PF + v), (uint32_t)((n >> 1) & 1));
+        mbar_wait(bar(B_OE + v), (uint32_t)(((n >> 1) & 1) ^ 1));
+        tc_fence_after();
+        const uint32_t pa = sb + kOffP + v * kPBytes;
+        const uint32_t va = sb + kOffKV + kvs * kKVBytes + 16384u;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          mma_bf16(tO + v * 128, desc_kmajor(pa + k * 32u), desc_mnmajor(va + k * 2048u, 8192u),
+                   kIdescPV, k > 0);
+        mma_commit(bar(B_OF + v));
+        mma_commit(bar(B_PE + v));
+        if (last) mma_commit(bar(B_KVE + kvs));
       }
     }
   } else {
     // ------------------------------------------------------------ softmax + epilogue
     const int r = threadIdx.x;  // MMA row == TMEM lane
     const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-    unsigned char* ost = smem + kOffO + warp * 32 * kOStride;
-    Walker wk;
-    wk.init(p);
-    // row state carried from item n-1 into its epilogue
-    int64_t prow = -1;  // obuf row index of the previous item's row, or -1
+    unsigned char* st = smem + kOffSt + warp * 32 * kStStride;
+    const int kt_row = r / p.g, hh = r % p.g;
+    int64_t prow = -1;  // obuf row of this thread's row in the pending item
     float pm = 0.f, pl = 1.f;
-    int64_t n = 0;
-    for (;; ++n) {
-      const bool have = wk.valid();
-      int64_t orow = -1;
-      float mrow = 0.f, lrow = 1.f;
-      if (have) {
-        wk.settle();
-        const Item it = item_of(p, wk);
-        const int s = (int)(n & 1);
-        const int64_t k = r / p.g, hh = r % p.g;
+    bool pend = false;
+    int n = 0;
+    auto epilogue = [&](int m1) {
+      const int s1 = m1 & 1;
+      mbar_wait(bar(B_OF + s1), (uint32_t)((m1 >> 1) & 1));
+      tc_fence_after();
+      const float inv = 1.f / pl;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float ov[32];
+        tmem_ld32(tmem + lane_base + 128 + s1 * 128 + q * 32, ov);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const uint4 v4 = make_uint4(pack_bf16(ov[8 * c] * inv, ov[8 * c + 1] * inv),
+                                      pack_bf16(ov[8 * c + 2] * inv, ov[8 * c + 3] * inv),
+                                      pack_bf16(ov[8 * c + 4] * inv, ov[8 * c + 5] * inv),
+                                      pack_bf16(ov[8 * c + 6] * inv, ov[8 * c + 7] * inv));
+          *reinterpret_cast<uint4*>(st + lane * kStStride + c * 16) = v4;
+        }
+        if (q == 3) {
+          tc_fence_before();
+          mbar_arrive(bar(B_OE + s1));
+        }
+        __syncwarp();
+        // 32 rows x 64 B of this column chunk: 8 rows per instruction
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const int rr = it * 8 + (lane >> 2), ch = lane & 3;
+          const int64_t drow = __shfl_sync(0xffffffffu, prow, rr);
+          const uint4 v4 = *reinterpret_cast<const uint4*>(st + rr * kStStride + ch * 16);
+          if (drow >= 0) *reinterpret_cast<uint4*>(p.obuf + drow * kD + q * 32 + ch * 8) = v4;
+        }
+        __syncwarp();
+      }
+      if (prow >= 0) *reinterpret_cast<float2*>(p.ml + 2 * prow) = make_float2(pm, pl);
+    };
+    for (int k = 0;; ++k) {
+      const int32_t task = ring.consume(k);
+      if (task < 0) break;
+      const TaskRows tr = task_rows(task, p.offsets, p.b, p.tpi);
+      const int32_t* ql = p.qlist + (int64_t)tr.kh * p.N * p.T + tr.beg;
+      for (int c = 0; c < tr.nitems; ++c, ++n) {
+        const int s = n & 1;
+        const int pos = c * p.tpi + kt_row;
+        int64_t orow = -1;
         int vis = kBK;
-        if (k < it.nrows_tok) {
-          const int32_t ent = p.qlist[it.kh * p.N * p.T + it.beg + it.p0 + k];
-          const int64_t t = ent / p.T, slot = ent % p.T;
-          const int64_t j = it.kh * p.g + hh;
-          orow = (j * p.N + t) * p.T + slot;
-          const int64_t v = t - it.i * kBK + 1;
-          vis = v < kBK ? (int)v : kBK;
+        if (kt_row < p.tpi && pos < tr.ntok) {
+          const int ent = __ldg(ql + pos);
+          const int t = ent / p.T, slot = ent - t * p.T;
+          orow = ((int64_t)((int)tr.kh * p.g + hh) * p.N + t) * p.T + slot;
+          const int v = t - (int)tr.i * kBK + 1;
+          vis = v < kBK ? v : kBK;
         }
         mbar_wait(bar(B_SF + s), (uint32_t)((n >> 1) & 1));
         tc_fence_after();
@@ -273,74 +299,34 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const Params p)
         mbar_arrive(bar(B_SE + s));
         float mx = -INFINITY;
 #pragma unroll
-        for (int c = 0; c < 64; ++c)
-          if (c < vis) mx = fmaxf(mx, sv[c]);
+        for (int c2 = 0; c2 < 64; ++c2) mx = fmaxf(mx, c2 < vis ? sv[c2] : -INFINITY);
         if (orow < 0) mx = 0.f;
         const float mb = mx * p.scale_log2;
         float sum = 0.f;
         uint32_t pk[32];
 #pragma unroll
-        for (int c = 0; c < 64; c += 2) {
-          const float e0 = (c < vis && orow >= 0) ? ex2(fmaf(sv[c], p.scale_log2, -mb)) : 0.f;
-          const float e1 = (c + 1 < vis && orow >= 0) ? ex2(fmaf(sv[c + 1], p.scale_log2, -mb)) : 0.f;
+        for (int c2 = 0; c2 < 64; c2 += 2) {
+          const float e0 = c2 < vis ? ex2(fmaf(sv[c2], p.scale_log2, -mb)) : 0.f;
+          const float e1 = c2 + 1 < vis ? ex2(fmaf(sv[c2 + 1], p.scale_log2, -mb)) : 0.f;
           sum += e0 + e1;
-          pk[c >> 1] = pack_bf16(e0, e1);
+          pk[c2 >> 1] = pack_bf16(e0, e1);
         }
-        mrow = mx * p.scale;
-        lrow = sum;
         mbar_wait(bar(B_PE + s), (uint32_t)(((n >> 1) & 1) ^ 1));
-        unsigned char* prow_s = smem + kOffP + s * kPBytes;
+        unsigned char* prs = smem + kOffP + s * kPBytes;
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          uint4 v4 = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-          *reinterpret_cast<uint4*>(prow_s + sw128_off(r, c)) = v4;
-        }
+        for (int c4 = 0; c4 < 8; ++c4)
+          *reinterpret_cast<uint4*>(prs + sw128_off(r, c4)) =
+              make_uint4(pk[4 * c4], pk[4 * c4 + 1], pk[4 * c4 + 2], pk[4 * c4 + 3]);
         fence_proxy_async();
         mbar_arrive(bar(B_PF + s));
+        if (pend) epilogue(n - 1);
+        pend = true;
+        prow = orow;
+        pm = mx * p.scale;
+        pl = sum;
       }
-      if (n > 0) {
-        // epilogue of item n-1: O / l -> bf16 staging -> coalesced global rows
-        const int64_t m1 = n - 1;
-        const int s1 = (int)(m1 & 1);
-        mbar_wait(bar(B_OF + s1), (uint32_t)((m1 >> 1) & 1));
-        tc_fence_after();
-        const float inv = 1.f / pl;
-        unsigned char* mine = ost + lane * kOStride;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          float ov[32];
-          tmem_ld32(tmem + lane_base + 128 + s1 * 128 + q * 32, ov);
-          tmem_wait_ld();
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            uint4 v4 = make_uint4(pack_bf16(ov[8 * c] * inv, ov[8 * c + 1] * inv),
-                                  pack_bf16(ov[8 * c + 2] * inv, ov[8 * c + 3] * inv),
-                                  pack_bf16(ov[8 * c + 4] * inv, ov[8 * c + 5] * inv),
-                                  pack_bf16(ov[8 * c + 6] * inv, ov[8 * c + 7] * inv));
-            *reinterpret_cast<uint4*>(mine + q * 64 + c * 16) = v4;
-          }
-        }
-        tc_fence_before();
-        mbar_arrive(bar(B_OE + s1));
-        if (prow >= 0) *reinterpret_cast<float2*>(p.ml + 2 * prow) = make_float2(pm, pl);
-        __syncwarp();
-        // 32 rows x 256 B: two rows per warp instruction, 16 B per lane
-#pragma unroll 4
-        for (int it2 = 0; it2 < 16; ++it2) {
-          const int rr = it2 * 2 + (lane >> 4), ch = lane & 15;
-          const int64_t dst_row = __shfl_sync(0xffffffffu, prow, rr);
-          const uint4 v4 = *reinterpret_cast<const uint4*>(ost + rr * kOStride + ch * 16);
-          if (dst_row >= 0)
-            *reinterpret_cast<uint4*>(p.obuf + dst_row * kD + ch * 8) = v4;
-        }
-        __syncwarp();
-      }
-      if (!have) break;
-      prow = orow;
-      pm = mrow;
-      pl = lrow;
-      ++wk.w;
     }
+    if (pend) epilogue(n - 1);
   }
 
   tc_fence_before();
@@ -366,31 +352,33 @@ int num_sms() {
 
 bool tc_fwd_supported(const fsa_shape& s, int dtype) {
   return dtype == FSA_DT_BF16 && s.d_K == kD && s.d_V == kD && s.B_K == kBK && s.h_K > 0 &&
-         s.h % s.h_K == 0 && s.h / s.h_K <= kRows;
+         s.h % s.h_K == 0 && s.h / s.h_K <= kRows && (int64_t)s.N * s.h < (1ll << 23);
 }
 
 int tc_sel_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V,
                const int32_t* offsets, const int32_t* qlist, const int32_t* work, void* obuf,
                void* ml, cudaStream_t st) {
-  FSA_REQUIRE(work != nullptr, "tensor-core forward needs the inverse work plan");
-  Params p;
+  FSA_REQUIRE(work != nullptr, "tensor-core forward needs the inverse work buffer");
+  Params p{};
   p.Q = (const __nv_bfloat16*)Q;
   p.K = (const __nv_bfloat16*)K;
   p.V = (const __nv_bfloat16*)V;
   p.offsets = offsets;
   p.qlist = qlist;
-  p.work = work;
   p.obuf = (__nv_bfloat16*)obuf;
   p.ml = (float*)ml;
-  p.N = s->N;
-  p.h = s->h;
-  p.h_K = s->h_K;
-  p.T = s->T;
-  p.b = s->N / s->B_K;
-  p.g = s->h / s->h_K;
-  p.tpi = (int)(kRows / p.g);
+  p.N = (int)s->N;
+  p.h = (int)s->h;
+  p.h_K = (int)s->h_K;
+  p.T = (int)s->T;
+  p.b = (int)(s->N / s->B_K);
+  p.g = (int)(s->h / s->h_K);
+  p.ntask = p.h_K * p.b;
+  p.tpi = kRows / p.g;
   p.scale = (float)s->scale;
   p.scale_log2 = (float)(s->scale * 1.4426950408889634);
+  p.counter = const_cast<int32_t*>(work) + p.ntask + 1;
+  cudaMemsetAsync(p.counter, 0, sizeof(int32_t), st);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(tc_sel_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
