@@ -146,11 +146,14 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const Params p)
         if (prev_stage >= 0) mbar_arrive(bar(B_QF + prev_stage));
         prev_stage = s;
       }
+      // publish the in-flight item before any wait that depends on consumers
+      // (next task's K/V stage, task ring): the MMA's look-ahead needs it
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      fence_proxy_async();
+      mbar_arrive(bar(B_QF + prev_stage));
+      prev_stage = -1;
       ++kseq;
     }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    fence_proxy_async();
-    if (prev_stage >= 0) mbar_arrive(bar(B_QF + prev_stage));
   } else if (warp == 8) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
