@@ -70,6 +70,20 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// n / d for 0 <= n < 2^31 and a runtime divisor d >= 1 (multiply-shift)
+struct FastDiv {
+  uint32_t d, m, s;
+  __host__ __device__ void init(uint32_t div) {
+    d = div;
+    s = 0;
+    while ((1u << s) < div) ++s;
+    m = (uint32_t)((((uint64_t)1 << 32) * (((uint64_t)1 << s) - div)) / div + 1);
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    return (__umulhi(n, m) + n) >> s;
+  }
+};
+
 // ---------------------------------------------------------------- tcgen05
 template <int kCols>
 __device__ __forceinline__ void tmem_alloc(uint32_t dst_smem) {
@@ -132,6 +146,27 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
 // per row per half, 16-byte chunk c of row r at ((c ^ (r & 7)) << 4).
 __device__ __forceinline__ uint32_t sw128_off(uint32_t row, uint32_t chunk) {
   return row * 128u + ((chunk ^ (row & 7u)) << 4);
+}
+
+// Warp-cooperative gather of 32 rows of 128 bf16 (256 B) into an SW128 tile
+// laid out [2 halves][rows][128 B] (half_stride bytes apart), rows
+// row0..row0+31.  Lane L names row L (src, ok); each instruction copies two
+// whole rows (16 lanes x 16 B per row), i.e. 4 full 128 B lines, instead of 32
+// scattered 16 B pieces.  Rows with ok == false are zero-filled.
+__device__ __forceinline__ void warp_gather_rows32(uint32_t dst, uint32_t half_stride, int row0,
+                                                   const void* src, bool ok, int lane) {
+  const unsigned long long sp = reinterpret_cast<unsigned long long>(src);
+  const unsigned okm = __ballot_sync(0xffffffffu, ok);
+  const int sub = lane >> 4, c = lane & 15;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int r = 2 * i + sub;
+    const unsigned long long rp = __shfl_sync(0xffffffffu, sp, r);
+    const bool rok = (okm >> r) & 1u;
+    const char* s = reinterpret_cast<const char*>(rp) + (rok ? c * 16 : 0);
+    cp_async16_zfill(dst + (uint32_t)(c >> 3) * half_stride + sw128_off(row0 + r, c & 7), s,
+                     rok ? 16u : 0u);
+  }
 }
 
 // K-major operand (rows = M or N, 64-element K slab per 128 B row).

@@ -25,9 +25,11 @@ using namespace tc;
 constexpr int kD = 128, kRows = 128;
 constexpr int kThreads = 9 * 32;
 constexpr uint32_t kQ = 32768, kKV = 32768, kP = 16384;
-constexpr uint32_t kOffQ = 0, kOffKV = 2 * kQ, kOffP = kOffKV + 2 * kKV, kOffBar = kOffP + 2 * kP;
-enum { B_QF = 0, B_QE = 2, B_KF = 4, B_KE = 6, B_SF = 8, B_SE = 10, B_PF = 12, B_PE = 14, B_OF = 16,
-       B_OE = 18, B_PV = 20, kNumBars = 21 };
+constexpr int kKVStages = 3;
+constexpr uint32_t kOffQ = 0, kOffKV = 2 * kQ, kOffP = kOffKV + kKVStages * kKV,
+                   kOffBar = kOffP + 2 * kP;
+enum { B_QF = 0, B_QE = 2, B_KF = 4, B_KE = 7, B_SF = 10, B_SE = 12, B_PF = 14, B_PE = 16,
+       B_OF = 18, B_OE = 20, B_PV = 22, kNumBars = 23 };
 constexpr uint32_t kOffTmem = kOffBar + kNumBars * 8;
 constexpr uint32_t kSmemBytes = kOffTmem + 16 + 1024;
 constexpr uint32_t kColS = 0, kColO = 128;  // S[2] 0..127, O[2] 128..383
@@ -98,14 +100,16 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const Params p) 
     for (int s = 0; s < 2; ++s) {
       mbar_init(bar(B_QF + s), 128);
       mbar_init(bar(B_QE + s), 1);
-      mbar_init(bar(B_KF + s), 128);
-      mbar_init(bar(B_KE + s), 1);
       mbar_init(bar(B_SF + s), 1);
       mbar_init(bar(B_SE + s), 128);
       mbar_init(bar(B_PF + s), 128);
       mbar_init(bar(B_PE + s), 1);
       mbar_init(bar(B_OF + s), 1);
       mbar_init(bar(B_OE + s), 128);
+    }
+    for (int s = 0; s < kKVStages; ++s) {
+      mbar_init(bar(B_KF + s), 128);
+      mbar_init(bar(B_KE + s), 1);
     }
     mbar_init(bar(B_PV), 1);
     fence_mbar_init();
@@ -119,8 +123,20 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const Params p) 
 
   if (warp >= 4 && warp < 8) {
     // ------------------------------------------------------------ loaders
+    // Each gather is its own cp.async group; the newest one stays in flight
+    // while the previous one is published (one-group-deep software pipeline).
+    // Blocking waits (Q stage, K/V stage) only depend on work the MMA can
+    // finish without the in-flight group (3 K/V stages, look-ahead of one).
     const int lr = threadIdx.x - 128;
     int64_t u = 0, nq = 0;  // tile counter, counter of items with at least one tile
+    uint32_t pend = 0;      // barrier of the in-flight group (0: none)
+    auto push_group = [&](uint32_t b) {
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+      fence_proxy_async();
+      if (pend) mbar_arrive(pend);
+      pend = b;
+    };
     ItemInfo it;
     for (int64_t n = 0; item_of(p, blockIdx.x + n * G, it); ++n) {
       if (it.k0 == it.k1) continue;
@@ -131,32 +147,24 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const Params p) 
         const int64_t kt = lr / p.g, hh = lr % p.g, t = it.t0 + kt;
         const bool ok = kt < p.tpi && t < p.N;
         const __nv_bfloat16* src = p.Q + ((ok ? t : 0) * p.h + it.kh * p.g + hh) * kD;
-        const uint32_t dst = sb + kOffQ + s * kQ;
-#pragma unroll
-        for (int c = 0; c < 16; ++c)
-          cp_async16_zfill(dst + (c >> 3) * 16384u + sw128_off(lr, c & 7), ok ? src + c * 8 : src,
-                           ok ? 16u : 0u);
+        warp_gather_rows32(sb + kOffQ + s * kQ, 16384u, lr & ~31, src, ok, lane);
       }
-      cp_async_wait_all();
-      fence_proxy_async();
-      mbar_arrive(bar(B_QF + s));
+      push_group(bar(B_QF + s));
       for (int64_t kt = it.k0; kt < it.k1; ++kt, ++u) {
-        const int v = (int)(u & 1);
-        mbar_wait(bar(B_KE + v), (uint32_t)(((u >> 1) & 1) ^ 1));
-        const int rr = lr & 63;
-        const int64_t key = kt * 64 + rr;
+        const int v = (int)(u % kKVStages);
+        mbar_wait(bar(B_KE + v), (uint32_t)(((u / kKVStages) & 1) ^ 1));
+        const int lw = warp - 4, row0 = (lw & 1) * 32;  // warps 4,5: K; 6,7: V
+        const int64_t key = kt * 64 + row0 + lane;
         const bool ok = key < p.n_keys;
-        const __nv_bfloat16* src = (lr < 64 ? p.Kx : p.Vx) + ((ok ? key : 0) * p.h_K + it.kh) * kD;
-        const uint32_t dst = sb + kOffKV + v * kKV + (lr < 64 ? 0u : 16384u);
-#pragma unroll
-        for (int c = 0; c < 16; ++c)
-          cp_async16_zfill(dst + (c >> 3) * 8192u + sw128_off(rr, c & 7), ok ? src + c * 8 : src,
-                           ok ? 16u : 0u);
-        cp_async_wait_all();
-        fence_proxy_async();
-        mbar_arrive(bar(B_KF + v));
+        const __nv_bfloat16* src = (lw < 2 ? p.Kx : p.Vx) + ((ok ? key : 0) * p.h_K + it.kh) * kD;
+        warp_gather_rows32(sb + kOffKV + v * kKV + (lw < 2 ? 0u : 16384u), 8192u, row0, src, ok,
+                           lane);
+        push_group(bar(B_KF + v));
       }
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    fence_proxy_async();
+    if (pend) mbar_arrive(pend);
   } else if (warp == 8) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
@@ -173,12 +181,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const Params p) 
       if (ha) ka = ia.k0;
       if (hb) kb = ib.k0;
       auto issue_s = [&]() {
-        const int s = (int)(qa & 1), v = (int)(ua & 1);
+        const int s = (int)(qa & 1), v = (int)(ua & 1), kv = (int)(ua % kKVStages);
         if (ka == ia.k0) mbar_wait(bar(B_QF + s), (uint32_t)((qa >> 1) & 1));
-        mbar_wait(bar(B_KF + v), (uint32_t)((ua >> 1) & 1));
+        mbar_wait(bar(B_KF + kv), (uint32_t)((ua / kKVStages) & 1));
         mbar_wait(bar(B_SE + v), (uint32_t)(((ua >> 1) & 1) ^ 1));
         tc_fence_after();
-        const uint32_t q = sb + kOffQ + s * kQ, k = sb + kOffKV + v * kKV;
+        const uint32_t q = sb + kOffQ + s * kQ, k = sb + kOffKV + kv * kKV;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
           mma_bf16(tmem + kColS + v * 64,
@@ -198,18 +206,18 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const Params p) 
       if (ha) issue_s();
       for (int64_t u = 0; hb; ++u) {
         if (ha) issue_s();
-        const int v = (int)(u & 1), so = (int)(qb & 1);
+        const int v = (int)(u & 1), so = (int)(qb & 1), kv = (int)(u % kKVStages);
         const bool first = kb == ib.k0, last = kb + 1 == ib.k1;
         mbar_wait(bar(B_PF + v), (uint32_t)((u >> 1) & 1));
         if (first) mbar_wait(bar(B_OE + so), (uint32_t)(((qb >> 1) & 1) ^ 1));
         tc_fence_after();
-        const uint32_t pp = sb + kOffP + v * kP, vv = sb + kOffKV + v * kKV + 16384u;
+        const uint32_t pp = sb + kOffP + v * kP, vv = sb + kOffKV + kv * kKV + 16384u;
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
           mma_bf16(tmem + kColO + so * 128, desc_kmajor(pp + kk * 32u),
                    desc_mnmajor(vv + kk * 2048u, 8192u), kIdPV, (first && kk == 0) ? 0u : 1u);
         mma_commit(bar(B_PE + v));
-        mma_commit(bar(B_KE + v));
+        mma_commit(bar(B_KE + kv));
         mma_commit(bar(B_PV));
         if (last) mma_commit(bar(B_OF + so));
         if (++kb == ib.k1) {

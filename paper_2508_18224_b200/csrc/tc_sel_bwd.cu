@@ -65,6 +65,7 @@ struct Params {
   int64_t N, h, h_K, T, b, g, ntask;
   int64_t W;   // sliding mode: window; T is then the number of window slots
   int tpi, slide, accumulate;  // accumulate: dK/dV += (sliding branch onto the selected one)
+  FastDiv fdT;
   float scale, scale_log2;
 };
 
@@ -87,8 +88,8 @@ __device__ __forceinline__ void token_of(const Params& p, const TaskRows& tr, in
                                          int64_t& t, int64_t& slot) {
   if (!p.slide) {
     const int32_t ent = p.qlist[tr.kh * p.N * p.T + tr.beg + pos];
-    t = ent / p.T;
-    slot = ent % p.T;
+    t = p.fdT.div((uint32_t)ent);
+    slot = ent - t * p.T;
   } else {
     t = tr.beg + pos;
     const int64_t first = (t - p.W + 1 > 0 ? t - p.W + 1 : 0) / kBK;
@@ -103,14 +104,6 @@ struct TaskFifo {
   __device__ void push(int32_t t) { task[tail++ & 3] = t; }
   __device__ int32_t pop() { return task[head++ & 3]; }
 };
-
-__device__ __forceinline__ void load_rows(uint32_t dst, const __nv_bfloat16* src, int r, bool ok,
-                                          uint32_t half_stride) {
-#pragma unroll
-  for (int c = 0; c < 16; ++c)
-    cp_async16_zfill(dst + (c >> 3) * half_stride + sw128_off(r, c & 7), ok ? src + c * 8 : src,
-                     ok ? 16u : 0u);
-}
 
 __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -160,10 +153,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
       const TaskRows tr = rows_of(p, task);
       if (tr.nitems == 0) continue;
       mbar_wait(bar(B_KVE), (uint32_t)((kseq & 1) ^ 1));
-      {
-        const int rr = lr & 63;
-        const __nv_bfloat16* src = (lr < 64 ? p.K : p.V) + ((tr.i * kBK + rr) * p.h_K + tr.kh) * kD;
-        load_rows(sb + (lr < 64 ? kOffK : kOffV), src, rr, true, 8192u);
+      {  // warps 4,5: K rows 0-31, 32-63; warps 6,7: V rows 0-31, 32-63
+        const int lw = warp - 4, row0 = (lw & 1) * 32;
+        const __nv_bfloat16* src =
+            (lw < 2 ? p.K : p.V) + ((tr.i * kBK + row0 + lane) * p.h_K + tr.kh) * kD;
+        warp_gather_rows32(sb + (lw < 2 ? kOffK : kOffV), 8192u, row0, src, true, lane);
       }
       for (int c = 0; c < tr.nitems; ++c, ++n) {
         const int s = (int)(n & 1);
@@ -177,8 +171,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
           token_of(p, tr, pos, t, slot);
           row = t * p.h + tr.kh * p.g + hh;
         }
-        load_rows(sb + kOffQ + s * kTile, p.Q + row * kD, lr, ok, 16384u);
-        load_rows(sb + kOffDO + s * kTile, p.dO + row * kD, lr, ok, 16384u);
+        warp_gather_rows32(sb + kOffQ + s * kTile, 16384u, lr & ~31, p.Q + row * kD, ok, lane);
+        warp_gather_rows32(sb + kOffDO + s * kTile, 16384u, lr & ~31, p.dO + row * kD, ok, lane);
         cp_async_wait_all();
         fence_proxy_async();
         if (c == 0) mbar_arrive(bar(B_KVF));
@@ -478,6 +472,7 @@ Params make_params(const fsa_shape* s, const void* Q, const void* K, const void*
   p.tpi = (int)(kRows / p.g);
   p.scale = (float)s->scale;
   p.scale_log2 = (float)(s->scale * 1.4426950408889634);
+  p.fdT.init((uint32_t)s->T);
   return p;
 }
 
@@ -549,6 +544,7 @@ int tc_slide_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V
   p.accumulate = accumulate;
   p.W = s->W;
   p.T = S;
+  p.fdT.init((uint32_t)S);
   p.counter = counter;
   int rc = launch_bwd(p, st);
   if (rc) return rc;

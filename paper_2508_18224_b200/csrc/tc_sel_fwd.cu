@@ -51,6 +51,7 @@ struct Params {
   __nv_bfloat16* obuf;
   float* ml;
   int N, h, h_K, T, b, g, ntask, tpi;
+  FastDiv fdT;  // entry -> token (entries are t * T + slot)
   float scale_log2, scale;
 };
 
@@ -112,13 +113,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const Params p)
       if (tr.nitems == 0) continue;
       const int kvs = kseq & 1;
       mbar_wait(bar(B_KVE + kvs), (uint32_t)(((kseq >> 1) & 1) ^ 1));
-      {
-        const int rr = lr & 63;
+      {  // warps 4,5: K rows 0-31, 32-63; warps 6,7: V rows 0-31, 32-63
+        const int lw = warp - 4, row0 = (lw & 1) * 32;
         const __nv_bfloat16* src =
-            (lr < 64 ? p.K : p.V) + ((int)(tr.i * kBK + rr) * p.h_K + (int)tr.kh) * kD;
-        const uint32_t dst = sb + kOffKV + kvs * kKVBytes + (lr < 64 ? 0u : 16384u);
-#pragma unroll
-        for (int c = 0; c < 16; ++c) cp_async16(dst + (c >> 3) * 8192u + sw128_off(rr, c & 7), src + c * 8);
+            (lw < 2 ? p.K : p.V) + ((int)(tr.i * kBK + row0 + lane) * p.h_K + (int)tr.kh) * kD;
+        warp_gather_rows32(sb + kOffKV + kvs * kKVBytes + (lw < 2 ? 0u : 16384u), 8192u, row0, src,
+                           true, lane);
         asm volatile("cp.async.commit_group;" ::: "memory");
       }
       bool kv_pending = true;
@@ -127,14 +127,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const Params p)
         const int s = n % kQStages;
         mbar_wait(bar(B_QE + s), (uint32_t)(((n / kQStages) & 1) ^ 1));
         const int pos = c * p.tpi + kt_row;
-        if (kt_row < p.tpi && pos < tr.ntok) {
-          const int t = __ldg(ql + pos) / p.T;
-          const __nv_bfloat16* src = p.Q + (t * p.h + (int)tr.kh * p.g + hh) * kD;
-          const uint32_t dst = sb + kOffQ + s * kQBytes;
-#pragma unroll
-          for (int cc = 0; cc < 16; ++cc)
-            cp_async16(dst + (cc >> 3) * 16384u + sw128_off(lr, cc & 7), src + cc * 8);
-        }
+        const bool ok = kt_row < p.tpi && pos < tr.ntok;
+        const int t = ok ? (int)p.fdT.div((uint32_t)__ldg(ql + pos)) : 0;
+        warp_gather_rows32(sb + kOffQ + s * kQBytes, 16384u, lr & ~31,
+                           p.Q + (t * p.h + (int)tr.kh * p.g + hh) * kD, ok, lane);
         asm volatile("cp.async.commit_group;" ::: "memory");
         // everything but this item's gather has landed: publish it
         asm volatile("cp.async.wait_group 1;" ::: "memory");
@@ -287,7 +283,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const Params p)
         int vis = kBK;
         if (kt_row < p.tpi && pos < tr.ntok) {
           const int ent = __ldg(ql + pos);
-          const int t = ent / p.T, slot = ent - t * p.T;
+          const int t = (int)p.fdT.div((uint32_t)ent), slot = ent - t * p.T;
           orow = ((int64_t)((int)tr.kh * p.g + hh) * p.N + t) * p.T + slot;
           const int v = t - (int)tr.i * kBK + 1;
           vis = v < kBK ? v : kBK;
@@ -378,6 +374,7 @@ int tc_sel_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V,
   p.g = (int)(s->h / s->h_K);
   p.ntask = p.h_K * p.b;
   p.tpi = kRows / p.g;
+  p.fdT.init((uint32_t)p.T);
   p.scale = (float)s->scale;
   p.scale_log2 = (float)(s->scale * 1.4426950408889634);
   p.counter = const_cast<int32_t*>(work) + p.ntask + 1;
