@@ -23,7 +23,7 @@ namespace {
 using namespace tc;
 
 constexpr int kD = 128, kBK = 64, kRows = 128;
-constexpr int kThreads = 9 * 32;
+constexpr int kThreads = 13 * 32;  // 2 softmax warpgroups, 4 loader warps, 1 MMA warp
 constexpr int kQStages = 3;
 
 constexpr uint32_t kQBytes = kRows * kD * 2;     // 32768: [2 halves][128 rows][128 B]
@@ -34,7 +34,7 @@ constexpr uint32_t kOffQ = 0;
 constexpr uint32_t kOffKV = kOffQ + kQStages * kQBytes;
 constexpr uint32_t kOffP = kOffKV + 2 * kKVBytes;
 constexpr uint32_t kOffSt = kOffP + 2 * kPBytes;
-constexpr uint32_t kOffBar = kOffSt + 4 * 32 * kStStride;
+constexpr uint32_t kOffBar = kOffSt + 8 * 32 * kStStride;
 enum { B_QF = 0, B_QE = 3, B_KVF = 6, B_KVE = 8, B_SF = 10, B_SE = 12, B_PF = 14, B_PE = 16,
        B_OF = 18, B_OE = 20, B_RF = 22, B_RE = 26, kNumBars = 30 };
 constexpr uint32_t kOffRing = kOffBar + kNumBars * 8;
@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const Params p)
     }
     for (int k = 0; k < kRingDepth; ++k) {
       mbar_init(bar(B_RF + k), 1);
-      mbar_init(bar(B_RE + k), 257);
+      mbar_init(bar(B_RE + k), 385);  // 256 softmax + 128 loader + 1 MMA
     }
     fence_mbar_init();
   }
@@ -99,9 +99,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const Params p)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp >= 4 && warp < 8) {
+  if (warp >= 8 && warp < 12) {
     // ------------------------------------------------------------ loaders
-    const int lr = threadIdx.x - 128;
+    const int lr = threadIdx.x - 256;
     const int kt_row = lr / p.g, hh = lr % p.g;
     int n = 0, kseq = 0;
     int prev_stage = -1;
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const Params p)
       const int kvs = kseq & 1;
       mbar_wait(bar(B_KVE + kvs), (uint32_t)(((kseq >> 1) & 1) ^ 1));
       {  // warps 4,5: K rows 0-31, 32-63; warps 6,7: V rows 0-31, 32-63
-        const int lw = warp - 4, row0 = (lw & 1) * 32;
+        const int lw = warp - 8, row0 = (lw & 1) * 32;
         const __nv_bfloat16* src =
             (lw < 2 ? p.K : p.V) + ((int)(tr.i * kBK + row0 + lane) * p.h_K + (int)tr.kh) * kD;
         warp_gather_rows32(sb + kOffKV + kvs * kKVBytes + (lw < 2 ? 0u : 16384u), 8192u, row0, src,
@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const Params p)
       prev_stage = -1;
       ++kseq;
     }
-  } else if (warp == 8) {
+  } else if (warp == 12) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       const uint32_t tS = tmem, tO = tmem + 128;
@@ -228,13 +228,18 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const Params p)
     }
   } else {
     // ------------------------------------------------------------ softmax + epilogue
-    const int r = threadIdx.x;  // MMA row == TMEM lane
-    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    // Two warpgroups ping-pong over items (wg handles items n with n % 2 == wg):
+    // each SM sub-partition runs two softmax warps, so one's TMEM loads,
+    // exponentials and stores overlap the other's.
+    const int wg = warp >> 2;
+    const int r = threadIdx.x & 127;  // MMA row == TMEM lane
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     unsigned char* st = smem + kOffSt + warp * 32 * kStStride;
     const int kt_row = r / p.g, hh = r % p.g;
     int64_t prow = -1;  // obuf row of this thread's row in the pending item
     float pm = 0.f, pl = 1.f;
     bool pend = false;
+    int pend_n = 0;
     int n = 0;
     auto epilogue = [&](int m1) {
       const int s1 = m1 & 1;
@@ -277,6 +282,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const Params p)
       const TaskRows tr = task_rows(task, p.offsets, p.b, p.tpi);
       const int32_t* ql = p.qlist + (int64_t)tr.kh * p.N * p.T + tr.beg;
       for (int c = 0; c < tr.nitems; ++c, ++n) {
+        if ((n & 1) != wg) continue;
         const int s = n & 1;
         const int pos = c * p.tpi + kt_row;
         int64_t orow = -1;
@@ -296,20 +302,40 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const Params p)
         tmem_wait_ld();
         tc_fence_before();
         mbar_arrive(bar(B_SE + s));
+        // only rows whose token lies in block i see a causal prefix (vis < 64);
+        // warps without such rows take the unmasked path
+        const bool masked = __any_sync(0xffffffffu, vis < kBK);
         float mx = -INFINITY;
-#pragma unroll
-        for (int c2 = 0; c2 < 64; ++c2) mx = fmaxf(mx, c2 < vis ? sv[c2] : -INFINITY);
-        if (orow < 0) mx = 0.f;
-        const float mb = mx * p.scale_log2;
-        float sum = 0.f;
+        float sum = 0.f, s2 = 0.f;
         uint32_t pk[32];
+        if (!masked) {
 #pragma unroll
-        for (int c2 = 0; c2 < 64; c2 += 2) {
-          const float e0 = c2 < vis ? ex2(fmaf(sv[c2], p.scale_log2, -mb)) : 0.f;
-          const float e1 = c2 + 1 < vis ? ex2(fmaf(sv[c2 + 1], p.scale_log2, -mb)) : 0.f;
-          sum += e0 + e1;
-          pk[c2 >> 1] = pack_bf16(e0, e1);
+          for (int c2 = 0; c2 < 64; ++c2) mx = fmaxf(mx, sv[c2]);
+          if (orow < 0) mx = 0.f;
+          const float mb = mx * p.scale_log2;
+#pragma unroll
+          for (int c2 = 0; c2 < 64; c2 += 2) {
+            const float e0 = ex2(fmaf(sv[c2], p.scale_log2, -mb));
+            const float e1 = ex2(fmaf(sv[c2 + 1], p.scale_log2, -mb));
+            sum += e0;
+            s2 += e1;
+            pk[c2 >> 1] = pack_bf16(e0, e1);
+          }
+        } else {
+#pragma unroll
+          for (int c2 = 0; c2 < 64; ++c2) mx = fmaxf(mx, c2 < vis ? sv[c2] : -INFINITY);
+          if (orow < 0) mx = 0.f;
+          const float mb = mx * p.scale_log2;
+#pragma unroll
+          for (int c2 = 0; c2 < 64; c2 += 2) {
+            const float e0 = c2 < vis ? ex2(fmaf(sv[c2], p.scale_log2, -mb)) : 0.f;
+            const float e1 = c2 + 1 < vis ? ex2(fmaf(sv[c2 + 1], p.scale_log2, -mb)) : 0.f;
+            sum += e0;
+            s2 += e1;
+            pk[c2 >> 1] = pack_bf16(e0, e1);
+          }
         }
+        sum += s2;
         mbar_wait(bar(B_PE + s), (uint32_t)(((n >> 1) & 1) ^ 1));
         unsigned char* prs = smem + kOffP + s * kPBytes;
 #pragma unroll
@@ -318,14 +344,15 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const Params p)
               make_uint4(pk[4 * c4], pk[4 * c4 + 1], pk[4 * c4 + 2], pk[4 * c4 + 3]);
         fence_proxy_async();
         mbar_arrive(bar(B_PF + s));
-        if (pend) epilogue(n - 1);
+        if (pend) epilogue(pend_n);
         pend = true;
+        pend_n = n;
         prow = orow;
         pm = mx * p.scale;
         pl = sum;
       }
     }
-    if (pend) epilogue(n - 1);
+    if (pend) epilogue(pend_n);
   }
 
   tc_fence_before();
