@@ -24,7 +24,7 @@ using namespace tc;
 
 constexpr int kD = 128, kBK = 64, kRows = 128;
 constexpr int kThreads = 13 * 32;  // 2 softmax warpgroups, 4 loader warps, 1 MMA warp
-constexpr int kQStages = 3;
+constexpr int kQStages = 4;
 
 constexpr uint32_t kQBytes = kRows * kD * 2;     // 32768: [2 halves][128 rows][128 B]
 constexpr uint32_t kKVBytes = 2 * kBK * kD * 2;  // 32768: K [2][64][128 B], V [2][64][128 B]
@@ -32,15 +32,15 @@ constexpr uint32_t kPBytes = kRows * kBK * 2;    // 16384: [128 rows][128 B]
 constexpr uint32_t kStStride = 80;               // epilogue staging: 32 rows x (64 + 16) B per warp
 constexpr uint32_t kOffQ = 0;
 constexpr uint32_t kOffKV = kOffQ + kQStages * kQBytes;
-constexpr uint32_t kOffP = kOffKV + 2 * kKVBytes;
-constexpr uint32_t kOffSt = kOffP + 2 * kPBytes;
+constexpr uint32_t kOffSt = kOffKV + 2 * kKVBytes;  // P lives in TMEM (A operand of PV)
 constexpr uint32_t kOffBar = kOffSt + 8 * 32 * kStStride;
-enum { B_QF = 0, B_QE = 3, B_KVF = 6, B_KVE = 8, B_SF = 10, B_SE = 12, B_PF = 14, B_PE = 16,
-       B_OF = 18, B_OE = 20, B_RF = 22, B_RE = 26, kNumBars = 30 };
+enum { B_QF = 0, B_QE = 4, B_KVF = 8, B_KVE = 10, B_SF = 12, B_SE = 14, B_PF = 16, B_PE = 18,
+       B_OF = 20, B_OE = 22, B_RF = 24, B_RE = 28, kNumBars = 32 };
 constexpr uint32_t kOffRing = kOffBar + kNumBars * 8;
 constexpr uint32_t kOffTmem = kOffRing + 16;
 constexpr uint32_t kSmemBytes = kOffTmem + 16 + 1024;
 
+constexpr uint32_t kColP = 384;  // TMEM: S[2] 0..127, O[2] 128..383, P[2] 384..447
 constexpr uint32_t kIdescS = idesc_bf16(128, 64, false, false);
 constexpr uint32_t kIdescPV = idesc_bf16(128, 128, false, true);
 
@@ -215,11 +215,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const Params p)
         mbar_wait(bar(B_PF + v), (uint32_t)((n >> 1) & 1));
         mbar_wait(bar(B_OE + v), (uint32_t)(((n >> 1) & 1) ^ 1));
         tc_fence_after();
-        const uint32_t pa = sb + kOffP + v * kPBytes;
         const uint32_t va = sb + kOffKV + kvs * kKVBytes + 16384u;
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          mma_bf16(tO + v * 128, desc_kmajor(pa + k * 32u), desc_mnmajor(va + k * 2048u, 8192u),
+          mma_bf16_ts(tO + v * 128, tmem + kColP + v * 32 + k * 8, desc_mnmajor(va + k * 2048u, 8192u),
                    kIdescPV, k > 0);
         mma_commit(bar(B_OF + v));
         mma_commit(bar(B_PE + v));
@@ -337,12 +336,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const Params p)
         }
         sum += s2;
         mbar_wait(bar(B_PE + s), (uint32_t)(((n >> 1) & 1) ^ 1));
-        unsigned char* prs = smem + kOffP + s * kPBytes;
-#pragma unroll
-        for (int c4 = 0; c4 < 8; ++c4)
-          *reinterpret_cast<uint4*>(prs + sw128_off(r, c4)) =
-              make_uint4(pk[4 * c4], pk[4 * c4 + 1], pk[4 * c4 + 2], pk[4 * c4 + 3]);
-        fence_proxy_async();
+        tmem_st32u(tmem + lane_base + kColP + s * 32, pk);  // bf16 pairs, K-packed
+        tmem_wait_st_();
+        tc_fence_before();
         mbar_arrive(bar(B_PF + s));
         if (pend) epilogue(pend_n);
         pend = true;
