@@ -6,19 +6,24 @@
 // the whole task (single writer, fixed order -> deterministic).
 //
 // Per 128-row item (TPI tokens x g heads), rows = gathered (token, slot):
-//   S   = Q K^T          M128 N64  K128   TMEM
-//   dP  = dO V^T         M128 N64  K128   TMEM
+//   S   = Q K^T          M128 N64  K128   TMEM stage s, cols [0, 64)
+//   dP  = dO V^T         M128 N64  K128   TMEM stage s, cols [64, 128)
 //   P   = exp(S*scale - lse),  dS = P * (dP - delta)      (softmax warps, bf16 -> smem)
 //   dV^T += dO^T P       M128(d) N64 K128(rows)  TMEM accumulator
 //   dK^T += Q^T dS       M128(d) N64 K128(rows)  TMEM accumulator
-//   dQ_i  = dS K         M128 N128 K64           TMEM -> bf16 partial row of dq_buf
+//   dQ_i  = dS K         M128 N128 K64  -> TMEM stage s (over the consumed S/dP)
+//                                        -> bf16 partial row of dq_buf
 // dQ partials are summed over the token's selected blocks in ascending block
 // order by the dq_reduce kernel (kv_major.py:326-340).
 //
-// Roles: warps 0-3 softmax/dS + epilogues (thread = TMEM lane), warps 4-7
-// cp.async gather loaders (Q and dO rows of an item, K/V per task), warp 8
-// MMA issuer (S/dP of item n+1 issued ahead of the dV/dK/dQ products of n).
-// Tasks are claimed dynamically, head-major (tc_sched.cuh).
+// Roles: warps 0-7 two softmax warpgroups that ping-pong over items (wg owns
+// items n with n % 2 == wg and its own Q/dO, S/dP and P/dS stages; after its
+// item's products land it stages the dQ epilogue in its now-free P/dS smem),
+// warps 8-11 cp.async gather loaders (one item's gather kept in flight), warp
+// 12 MMA issuer (S/dP of item n+1 issued ahead of the products of item n).
+// Tasks are claimed dynamically, head-major (tc_sched.cuh).  The sliding
+// branch's backward runs the same kernel with each block's contiguous token
+// window as its rows and a band mask (oracle.py:102-131).
 #include "tc_plan.cuh"
 #include "tc_sched.cuh"
 
@@ -28,32 +33,31 @@ namespace {
 using namespace tc;
 
 constexpr int kD = 128, kBK = 64, kRows = 128;
-constexpr int kThreads = 9 * 32;
+constexpr int kThreads = 13 * 32;
 
 constexpr uint32_t kTile = kRows * kD * 2;  // 32768: [2 halves][128][128 B]
 constexpr uint32_t kOffQ = 0;               // Q[2]
 constexpr uint32_t kOffDO = 2 * kTile;      // dO[2]
 constexpr uint32_t kOffK = 4 * kTile;       // K [2 halves][64][128 B] = 16384
 constexpr uint32_t kOffV = kOffK + 16384;
-constexpr uint32_t kOffP = kOffV + 16384;   // P  [128][128 B]
-constexpr uint32_t kOffDS = kOffP + 16384;  // dS [128][128 B]
-constexpr uint32_t kStStride = 80;          // dq staging: 32 rows x (64 + 16) B per warp
-constexpr uint32_t kOffSt = kOffDS + 16384;
-constexpr uint32_t kOffBar = kOffSt + 4 * 32 * kStStride;
+constexpr uint32_t kOffP = kOffV + 16384;   // P[2]  [128][128 B]
+constexpr uint32_t kOffDS = kOffP + 32768;  // dS[2] [128][128 B]
+constexpr uint32_t kStStride = 80;          // dq staging (inside the wg's P stage)
+constexpr uint32_t kOffBar = kOffDS + 32768;
 enum {
-  B_QDF = 0, B_QDE = 2, B_KVF = 4, B_KVE = 5, B_SDF = 6, B_SDE = 8, B_PDF = 10, B_PDE = 11,
-  B_DQF = 12, B_DQE = 13, B_KAF = 14, B_KAE = 15, B_RF = 16, B_RE = 20, kNumBars = 24
+  B_QDF = 0, B_QDE = 2, B_KVF = 4, B_KVE = 5, B_SDF = 6, B_SDE = 8, B_PDF = 10, B_DQF = 12,
+  B_KAF = 14, B_KAE = 15, B_RF = 16, B_RE = 20, kNumBars = 24
 };
 constexpr uint32_t kOffRing = kOffBar + kNumBars * 8;
 constexpr uint32_t kOffTmem = kOffRing + 16;
 constexpr uint32_t kSmemBytes = kOffTmem + 16 + 1024;
 
-// TMEM columns
-constexpr uint32_t kColS = 0, kColDP = 128, kColDQ = 256, kColDK = 384, kColDV = 448;
+// TMEM columns: stage s at 128 s (S | dP, later dQ), dK^T 256, dV^T 320
+constexpr uint32_t kColDK = 256, kColDV = 320;
 
-constexpr uint32_t kIdS = idesc_bf16(128, 64, false, false);     // S, dP
-constexpr uint32_t kIdKV = idesc_bf16(128, 64, true, true);      // dV^T, dK^T
-constexpr uint32_t kIdQ = idesc_bf16(128, 128, false, true);     // dQ
+constexpr uint32_t kIdS = idesc_bf16(128, 64, false, false);  // S, dP
+constexpr uint32_t kIdKV = idesc_bf16(128, 64, true, true);   // dV^T, dK^T
+constexpr uint32_t kIdQ = idesc_bf16(128, 128, false, true);  // dQ
 
 struct Params {
   const __nv_bfloat16 *Q, *K, *V, *dO;
@@ -70,8 +74,7 @@ struct Params {
 };
 
 // Rows of a task: the selected mode reads them from the inverse CSR; the
-// sliding mode (band-mask backward, oracle.py:102-131) uses the contiguous
-// window of tokens [64 i, 64 i + 63 + W - 1] that can see block i.
+// sliding mode uses the contiguous window of tokens [64 i, 64 i + 63 + W - 1].
 __device__ __forceinline__ TaskRows rows_of(const Params& p, int32_t task) {
   if (!p.slide) return task_rows(task, p.offsets, p.b, p.tpi);
   TaskRows r;
@@ -87,7 +90,7 @@ __device__ __forceinline__ TaskRows rows_of(const Params& p, int32_t task) {
 __device__ __forceinline__ void token_of(const Params& p, const TaskRows& tr, int64_t pos,
                                          int64_t& t, int64_t& slot) {
   if (!p.slide) {
-    const int32_t ent = p.qlist[tr.kh * p.N * p.T + tr.beg + pos];
+    const int32_t ent = __ldg(p.qlist + tr.kh * p.N * p.T + tr.beg + pos);
     t = p.fdT.div((uint32_t)ent);
     slot = ent - t * p.T;
   } else {
@@ -121,18 +124,16 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
       mbar_init(bar(B_QDE + s), 1);
       mbar_init(bar(B_SDF + s), 1);
       mbar_init(bar(B_SDE + s), 128);
+      mbar_init(bar(B_PDF + s), 128);
+      mbar_init(bar(B_DQF + s), 1);
     }
     mbar_init(bar(B_KVF), 128);
     mbar_init(bar(B_KVE), 1);
-    mbar_init(bar(B_PDF), 128);
-    mbar_init(bar(B_PDE), 1);
-    mbar_init(bar(B_DQF), 1);
-    mbar_init(bar(B_DQE), 128);
     mbar_init(bar(B_KAF), 1);
     mbar_init(bar(B_KAE), 128);
     for (int k = 0; k < kRingDepth; ++k) {
       mbar_init(bar(B_RF + k), 1);
-      mbar_init(bar(B_RE + k), 257);  // 128 compute + 128 loader + 1 MMA
+      mbar_init(bar(B_RE + k), 385);  // 256 softmax + 128 loader + 1 MMA
     }
     fence_mbar_init();
   }
@@ -142,10 +143,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp >= 4 && warp < 8) {
+  if (warp >= 8 && warp < 12) {
     // ================================================================ loaders
-    const int lr = threadIdx.x - 128;
+    const int lr = threadIdx.x - 256;
+    const int kt = lr / (int)p.g, hh = lr % (int)p.g;
     int64_t n = 0, kseq = 0;
+    int prev = -1;
     for (int k = 0;; ++k) {
       if (lr == 0) ring.produce(k, p.counter, p.ntask);
       const int32_t task = ring.consume(k);
@@ -153,16 +156,17 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
       const TaskRows tr = rows_of(p, task);
       if (tr.nitems == 0) continue;
       mbar_wait(bar(B_KVE), (uint32_t)((kseq & 1) ^ 1));
-      {  // warps 4,5: K rows 0-31, 32-63; warps 6,7: V rows 0-31, 32-63
-        const int lw = warp - 4, row0 = (lw & 1) * 32;
+      {  // warps 8,9: K rows 0-31, 32-63; warps 10,11: V rows 0-31, 32-63
+        const int lw = warp - 8, row0 = (lw & 1) * 32;
         const __nv_bfloat16* src =
             (lw < 2 ? p.K : p.V) + ((tr.i * kBK + row0 + lane) * p.h_K + tr.kh) * kD;
         warp_gather_rows32(sb + (lw < 2 ? kOffK : kOffV), 8192u, row0, src, true, lane);
+        asm volatile("cp.async.commit_group;" ::: "memory");
       }
+      bool kv_pending = true;
       for (int c = 0; c < tr.nitems; ++c, ++n) {
         const int s = (int)(n & 1);
         mbar_wait(bar(B_QDE + s), (uint32_t)(((n >> 1) & 1) ^ 1));
-        const int64_t kt = lr / p.g, hh = lr % p.g;
         const int64_t pos = (int64_t)c * p.tpi + kt;
         const bool ok = kt < p.tpi && pos < tr.ntok;
         int64_t row = 0;
@@ -173,29 +177,35 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
         }
         warp_gather_rows32(sb + kOffQ + s * kTile, 16384u, lr & ~31, p.Q + row * kD, ok, lane);
         warp_gather_rows32(sb + kOffDO + s * kTile, 16384u, lr & ~31, p.dO + row * kD, ok, lane);
-        cp_async_wait_all();
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
         fence_proxy_async();
-        if (c == 0) mbar_arrive(bar(B_KVF));
-        mbar_arrive(bar(B_QDF + s));
+        if (kv_pending) {
+          mbar_arrive(bar(B_KVF));
+          kv_pending = false;
+        }
+        if (prev >= 0) mbar_arrive(bar(B_QDF + prev));
+        prev = s;
       }
+      // publish the in-flight item before waits that depend on consumers
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      fence_proxy_async();
+      mbar_arrive(bar(B_QDF + prev));
+      prev = -1;
       ++kseq;
     }
-  } else if (warp == 8) {
+  } else if (warp == 12) {
     // ================================================================ MMA issuer
     if (lane == 0) {
-      const uint32_t tS = tmem + kColS, tDP = tmem + kColDP, tQ = tmem + kColDQ;
       const uint32_t tK = tmem + kColDK, tV = tmem + kColDV;
       TaskFifo fifo;
-      // look-ahead iterator (S/dP)
-      int ka = 0;
-      int32_t a_task = -1;
-      TaskRows a_tr{};
-      int a_c = 0;
-      bool a_done = false;
+      int ka = 0, a_c = 0;
       int64_t a_kseq = -1;
-      auto a_next = [&]() -> bool {  // advance to the next item; false when exhausted
+      TaskRows a_tr{};
+      bool a_done = false, a_started = false;
+      auto a_next = [&]() -> bool {
         if (a_done) return false;
-        if (a_task >= 0 && a_c + 1 < a_tr.nitems) {
+        if (a_started && a_c + 1 < a_tr.nitems) {
           ++a_c;
           return true;
         }
@@ -207,9 +217,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
           }
           const TaskRows tr = rows_of(p, t);
           if (tr.nitems == 0) continue;
-          a_task = t;
           a_tr = tr;
           a_c = 0;
+          a_started = true;
           ++a_kseq;
           fifo.push(t);
           return true;
@@ -222,15 +232,16 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
         mbar_wait(bar(B_SDE + s), (uint32_t)(((n >> 1) & 1) ^ 1));
         tc_fence_after();
         const uint32_t q = sb + kOffQ + s * kTile, o = sb + kOffDO + s * kTile;
+        const uint32_t tS = tmem + 128u * s;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const uint32_t ko = (k >> 2) * 16384u + (k & 3) * 32u, kk = (k >> 2) * 8192u + (k & 3) * 32u;
-          mma_bf16(tS + s * 64, desc_kmajor(q + ko), desc_kmajor(sb + kOffK + kk), kIdS, k > 0);
+          mma_bf16(tS, desc_kmajor(q + ko), desc_kmajor(sb + kOffK + kk), kIdS, k > 0);
         }
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const uint32_t ko = (k >> 2) * 16384u + (k & 3) * 32u, kk = (k >> 2) * 8192u + (k & 3) * 32u;
-          mma_bf16(tDP + s * 64, desc_kmajor(o + ko), desc_kmajor(sb + kOffV + kk), kIdS, k > 0);
+          mma_bf16(tS + 64, desc_kmajor(o + ko), desc_kmajor(sb + kOffV + kk), kIdS, k > 0);
         }
         mma_commit(bar(B_SDF + s));
       };
@@ -241,10 +252,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
       TaskRows b_tr{};
       int b_c = 0;
       for (int64_t n = 0; have; ++n) {
-        // identify item n for the back half (follows the FIFO of non-empty tasks)
         if (n == 0 || b_c + 1 >= b_tr.nitems) {
-          const int32_t t = fifo.pop();
-          b_tr = rows_of(p, t);
+          b_tr = rows_of(p, fifo.pop());
           b_c = 0;
           ++kseq_b;
         } else {
@@ -252,31 +261,29 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
         }
         const bool first = b_c == 0, last = b_c + 1 == b_tr.nitems;
         // look ahead: S/dP of item n+1 -- unless it starts a new task: K/V are
-        // single-buffered and only released by the back half of item n
+        // single-buffered and only released by the products of item n
         have = a_next();
         const bool defer = have && a_c == 0;
         if (have && !defer) issue_sdp(++n_ahead, a_kseq);
-        // back half of item n
         const int s = (int)(n & 1);
-        mbar_wait(bar(B_PDF), (uint32_t)(n & 1));
-        mbar_wait(bar(B_DQE), (uint32_t)((n & 1) ^ 1));
+        mbar_wait(bar(B_PDF + s), (uint32_t)((n >> 1) & 1));
         if (first) mbar_wait(bar(B_KAE), (uint32_t)((kseq_b & 1) ^ 1));
         tc_fence_after();
         const uint32_t q = sb + kOffQ + s * kTile, o = sb + kOffDO + s * kTile;
+        const uint32_t pp = sb + kOffP + s * 16384u, ds = sb + kOffDS + s * 16384u;
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-          mma_bf16(tV, desc_mnmajor(o + k * 2048u, 16384u), desc_mnmajor(sb + kOffP + k * 2048u, 8192u),
+          mma_bf16(tV, desc_mnmajor(o + k * 2048u, 16384u), desc_mnmajor(pp + k * 2048u, 8192u),
                    kIdKV, (first && k == 0) ? 0u : 1u);
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-          mma_bf16(tK, desc_mnmajor(q + k * 2048u, 16384u), desc_mnmajor(sb + kOffDS + k * 2048u, 8192u),
+          mma_bf16(tK, desc_mnmajor(q + k * 2048u, 16384u), desc_mnmajor(ds + k * 2048u, 8192u),
                    kIdKV, (first && k == 0) ? 0u : 1u);
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          mma_bf16(tQ, desc_kmajor(sb + kOffDS + k * 32u), desc_mnmajor(sb + kOffK + k * 2048u, 8192u),
-                   kIdQ, k > 0);
-        mma_commit(bar(B_DQF));
-        mma_commit(bar(B_PDE));
+          mma_bf16(tmem + 128u * s, desc_kmajor(ds + k * 32u),
+                   desc_mnmajor(sb + kOffK + k * 2048u, 8192u), kIdQ, k > 0);
+        mma_commit(bar(B_DQF + s));
         mma_commit(bar(B_QDE + s));
         if (last) {
           mma_commit(bar(B_KAF));
@@ -286,45 +293,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
       }
     }
   } else {
-    // ================================================================ softmax / dS / epilogues
-    const int r = threadIdx.x;
-    const uint32_t lb = (uint32_t)(warp * 32) << 16;
-    unsigned char* st = smem + kOffSt + warp * 32 * kStStride;
+    // ================================================================ softmax warpgroups
+    const int wg = warp >> 2;
+    const int r = threadIdx.x & 127;
+    const uint32_t lb = (uint32_t)((warp & 3) * 32) << 16;
+    const int kt = r / (int)p.g, hh = r % (int)p.g;
     int64_t n = 0, kseq = 0;
-    // pending epilogue of the previous item
-    int64_t pend_row = -1;  // dq_buf row of this thread's row, -1 if invalid
-    bool pend = false, pend_last = false;
-    TaskRows pend_tr{};
-    auto dq_epilogue = [&](int64_t m) {
-      mbar_wait(bar(B_DQF), (uint32_t)(m & 1));
-      tc_fence_after();
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        float v[32];
-        tmem_ld32(tmem + lb + kColDQ + q * 32, v);
-        tmem_wait_ld();
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint4 u = make_uint4(pack_bf16(v[8 * c] * p.scale, v[8 * c + 1] * p.scale),
-                               pack_bf16(v[8 * c + 2] * p.scale, v[8 * c + 3] * p.scale),
-                               pack_bf16(v[8 * c + 4] * p.scale, v[8 * c + 5] * p.scale),
-                               pack_bf16(v[8 * c + 6] * p.scale, v[8 * c + 7] * p.scale));
-          *reinterpret_cast<uint4*>(st + lane * kStStride + c * 16) = u;
-        }
-        __syncwarp();
-        // 32 rows x 64 B: 8 rows per instruction, 16 B per lane
-#pragma unroll
-        for (int it = 0; it < 4; ++it) {
-          const int rr = it * 8 + (lane >> 2), ch = lane & 3;
-          const int64_t drow = __shfl_sync(0xffffffffu, pend_row, rr);
-          const uint4 u = *reinterpret_cast<const uint4*>(st + rr * kStStride + ch * 16);
-          if (drow >= 0) *reinterpret_cast<uint4*>(p.dq + drow * kD + q * 32 + ch * 8) = u;
-        }
-        __syncwarp();
-      }
-      tc_fence_before();
-      mbar_arrive(bar(B_DQE));
-    };
     auto kv_epilogue = [&](const TaskRows& tr, int64_t ks) {
       mbar_wait(bar(B_KAF), (uint32_t)(ks & 1));
       tc_fence_after();
@@ -360,7 +334,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
       if (task < 0) break;
       const TaskRows tr = rows_of(p, task);
       if (tr.nitems == 0) {  // no attending rows: the block's gradients are zero
-        if (p.accumulate) continue;
+        if (p.accumulate || wg != 0) continue;
         float* dk = p.dK + ((tr.i * kBK) * p.h_K + tr.kh) * kD + r;
         float* dv = p.dV + ((tr.i * kBK) * p.h_K + tr.kh) * kD + r;
         for (int key = 0; key < kBK; ++key) {
@@ -370,8 +344,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
         continue;
       }
       for (int c = 0; c < tr.nitems; ++c, ++n) {
+        if ((int)(n & 1) != wg) continue;
         const int s = (int)(n & 1);
-        const int64_t kt = r / p.g, hh = r % p.g;
         const int64_t pos = (int64_t)c * p.tpi + kt;
         const bool ok = kt < p.tpi && pos < tr.ntok;
         int klo = 0, khi = -1;  // visible keys of the block: [klo, khi]
@@ -391,48 +365,76 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
           lse_r = p.lse[j * p.N + t] * 1.4426950408889634f;
           dl = p.delta[j * p.N + t];
         }
+        const bool full = __all_sync(0xffffffffu, klo == 0 && khi == kBK - 1);
         mbar_wait(bar(B_SDF + s), (uint32_t)((n >> 1) & 1));
         tc_fence_after();
-        float sv[64], dp[64];
-        tmem_ld32(tmem + lb + kColS + s * 64, sv);
-        tmem_ld32(tmem + lb + kColS + s * 64 + 32, sv + 32);
-        tmem_ld32(tmem + lb + kColDP + s * 64, dp);
-        tmem_ld32(tmem + lb + kColDP + s * 64 + 32, dp + 32);
-        tmem_wait_ld();
-        tc_fence_before();
-        mbar_arrive(bar(B_SDE + s));
-        uint32_t pp[32], ds[32];
+        unsigned char* prow = smem + kOffP + s * 16384u;
+        unsigned char* drw = smem + kOffDS + s * 16384u;
 #pragma unroll
-        for (int c2 = 0; c2 < 64; c2 += 2) {
-          const float p0 = (c2 >= klo && c2 <= khi) ? ex2(fmaf(sv[c2], p.scale_log2, -lse_r)) : 0.f;
-          const float p1 = (c2 + 1 >= klo && c2 + 1 <= khi) ? ex2(fmaf(sv[c2 + 1], p.scale_log2, -lse_r)) : 0.f;
-          pp[c2 >> 1] = pack_bf16(p0, p1);
-          ds[c2 >> 1] = pack_bf16(p0 * (dp[c2] - dl), p1 * (dp[c2 + 1] - dl));
-        }
-        mbar_wait(bar(B_PDE), (uint32_t)((n & 1) ^ 1));
+        for (int hf = 0; hf < 2; ++hf) {  // 32 key columns at a time (register budget)
+          float sv[32], dp[32];
+          tmem_ld32(tmem + lb + 128u * s + hf * 32, sv);
+          tmem_ld32(tmem + lb + 128u * s + 64 + hf * 32, dp);
+          tmem_wait_ld();
+          uint32_t pp[16], dd[16];
 #pragma unroll
-        for (int c4 = 0; c4 < 8; ++c4) {
-          *reinterpret_cast<uint4*>(smem + kOffP + sw128_off(r, c4)) =
-              make_uint4(pp[4 * c4], pp[4 * c4 + 1], pp[4 * c4 + 2], pp[4 * c4 + 3]);
-          *reinterpret_cast<uint4*>(smem + kOffDS + sw128_off(r, c4)) =
-              make_uint4(ds[4 * c4], ds[4 * c4 + 1], ds[4 * c4 + 2], ds[4 * c4 + 3]);
+          for (int c2 = 0; c2 < 32; c2 += 2) {
+            const int key = hf * 32 + c2;
+            float p0 = ex2(fmaf(sv[c2], p.scale_log2, -lse_r));
+            float p1 = ex2(fmaf(sv[c2 + 1], p.scale_log2, -lse_r));
+            if (!full) {
+              p0 = (key >= klo && key <= khi) ? p0 : 0.f;
+              p1 = (key + 1 >= klo && key + 1 <= khi) ? p1 : 0.f;
+            }
+            if (!ok) p0 = p1 = 0.f;
+            pp[c2 >> 1] = pack_bf16(p0, p1);
+            dd[c2 >> 1] = pack_bf16(p0 * (dp[c2] - dl), p1 * (dp[c2 + 1] - dl));
+          }
+#pragma unroll
+          for (int c4 = 0; c4 < 4; ++c4) {
+            *reinterpret_cast<uint4*>(prow + sw128_off(r, hf * 4 + c4)) =
+                make_uint4(pp[4 * c4], pp[4 * c4 + 1], pp[4 * c4 + 2], pp[4 * c4 + 3]);
+            *reinterpret_cast<uint4*>(drw + sw128_off(r, hf * 4 + c4)) =
+                make_uint4(dd[4 * c4], dd[4 * c4 + 1], dd[4 * c4 + 2], dd[4 * c4 + 3]);
+          }
         }
         fence_proxy_async();
-        mbar_arrive(bar(B_PDF));
-        if (pend) {
-          dq_epilogue(n - 1);
-          if (pend_last) kv_epilogue(pend_tr, kseq - 1);
+        mbar_arrive(bar(B_PDF + s));
+        // products of this item landed -> dQ partial out of TMEM; stage the
+        // bf16 rows in this wg's (now consumed) P buffer for coalesced stores
+        mbar_wait(bar(B_DQF + s), (uint32_t)((n >> 1) & 1));
+        tc_fence_after();
+        unsigned char* st = prow + (warp & 3) * 32 * kStStride;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float v[32];
+          tmem_ld32(tmem + lb + 128u * s + q * 32, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int c4 = 0; c4 < 4; ++c4) {
+            const uint4 u = make_uint4(pack_bf16(v[8 * c4] * p.scale, v[8 * c4 + 1] * p.scale),
+                                       pack_bf16(v[8 * c4 + 2] * p.scale, v[8 * c4 + 3] * p.scale),
+                                       pack_bf16(v[8 * c4 + 4] * p.scale, v[8 * c4 + 5] * p.scale),
+                                       pack_bf16(v[8 * c4 + 6] * p.scale, v[8 * c4 + 7] * p.scale));
+            *reinterpret_cast<uint4*>(st + lane * kStStride + c4 * 16) = u;
+          }
+          if (q == 3) {
+            tc_fence_before();
+            mbar_arrive(bar(B_SDE + s));  // stage s TMEM free for S/dP of item n+2
+          }
+          __syncwarp();
+#pragma unroll
+          for (int it = 0; it < 4; ++it) {
+            const int rr = it * 8 + (lane >> 2), ch = lane & 3;
+            const int64_t d = __shfl_sync(0xffffffffu, drow, rr);
+            const uint4 u = *reinterpret_cast<const uint4*>(st + rr * kStStride + ch * 16);
+            if (d >= 0) *reinterpret_cast<uint4*>(p.dq + d * kD + q * 32 + ch * 8) = u;
+          }
+          __syncwarp();
         }
-        pend = true;
-        pend_row = drow;
-        pend_last = c + 1 == tr.nitems;
-        pend_tr = tr;
+        if (c + 1 == tr.nitems) kv_epilogue(tr, kseq);
       }
       ++kseq;
-    }
-    if (pend) {
-      dq_epilogue(n - 1);
-      if (pend_last) kv_epilogue(pend_tr, kseq - 1);
     }
   }
 
