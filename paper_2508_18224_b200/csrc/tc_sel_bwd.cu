@@ -177,21 +177,18 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
         }
         warp_gather_rows32(sb + kOffQ + s * kTile, 16384u, lr & ~31, p.Q + row * kD, ok, lane);
         warp_gather_rows32(sb + kOffDO + s * kTile, 16384u, lr & ~31, p.dO + row * kD, ok, lane);
+        // publish as soon as it lands: with two Q/dO stages an unpublished
+        // gather would block the MMA's look-ahead (it needs item n+1 before
+        // it can release item n's stage)
         asm volatile("cp.async.commit_group;" ::: "memory");
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
         fence_proxy_async();
         if (kv_pending) {
           mbar_arrive(bar(B_KVF));
           kv_pending = false;
         }
-        if (prev >= 0) mbar_arrive(bar(B_QDF + prev));
-        prev = s;
+        mbar_arrive(bar(B_QDF + s));
       }
-      // publish the in-flight item before waits that depend on consumers
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-      fence_proxy_async();
-      mbar_arrive(bar(B_QDF + prev));
-      prev = -1;
       ++kseq;
     }
   } else if (warp == 12) {
