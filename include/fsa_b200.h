@@ -174,6 +174,14 @@ int fsa_gated_combine(const fsa_shape* s, int dtype, const void* out_cmp, const 
 int fsa_gate_scale(const fsa_shape* s, int dtype, const void* dOut, const void* tau, int col,
                    void* out, void* stream);
 
+/* Fused gate backward + delta for the selected and sliding branches
+ * (branches.py:103, kv_major.py:284): d_sel = tau[t][1] dOut, d_slide =
+ * tau[t][2] dOut (dtype), delta_c[j][t] = sum_v out_c * d_c (acc dtype, from
+ * the rounded d_c).  out_sel/out_slide [N][h][d_V] acc dtype. */
+int fsa_gate_backward(const fsa_shape* s, int dtype, const void* dOut, const void* tau,
+                      const void* out_sel, const void* out_slide, void* d_sel, void* d_slide,
+                      void* delta_sel, void* delta_slide, void* stream);
+
 /* Finiteness check for as_headed (config.py:146-155): *flag |= 1 on any non-finite. */
 int fsa_check_finite(int dtype, const void* x, int64_t n, int32_t* flag, void* stream);
 

@@ -106,15 +106,17 @@ def _slide_fwd_storage(cfg, dt, q, k, v):
     return out, lse
 
 
-def _slide_bwd_storage(cfg, dt, q, k, v, do, out, lse, accumulate_into=None):
+def _slide_bwd_storage(cfg, dt, q, k, v, do, out, lse, accumulate_into=None, delta=None):
     """K11.  With ``accumulate_into=(dQ, dK, dV)`` the sliding gradients are
-    added onto those tensors in-kernel (tensor-core path) and they are returned."""
+    added onto those tensors in-kernel (tensor-core path) and they are returned.
+    ``delta`` (h, N) may be passed precomputed (fsa_gate_backward)."""
     dev, acc = q.device, _lib.acc_dtype(dt)
     s = _lib.shape_of(cfg)
     st = _lib.stream()
-    delta = torch.empty((cfg.h, cfg.N), dtype=acc, device=dev)
-    _lib.call("fsa_bwd_delta", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(out), _lib.ptr(do),
-              _lib.ptr(delta), st)
+    if delta is None:
+        delta = torch.empty((cfg.h, cfg.N), dtype=acc, device=dev)
+        _lib.call("fsa_bwd_delta", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(out), _lib.ptr(do),
+                  _lib.ptr(delta), st)
     nws = _lib.lib().fsa_slide_bwd_workspace_bytes(ctypes.byref(s), _lib.dt_code(dt))
     ws = torch.empty(nws, dtype=torch.uint8, device=dev) if nws else None
     if accumulate_into is not None and ws is not None:

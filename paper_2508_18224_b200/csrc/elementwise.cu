@@ -85,14 +85,16 @@ template <typename A, typename TO>
 __global__ void combine_kernel(const A* __restrict__ a, const A* __restrict__ bsel,
                                const A* __restrict__ c, const A* __restrict__ tau,
                                TO* __restrict__ out, int64_t N, int64_t row) {
-  const int64_t total = N * row;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t t = e / row;
-    A acc = A(0) + tau[t * 3 + 0] * a[e];
-    acc = acc + tau[t * 3 + 1] * bsel[e];
-    acc = acc + tau[t * 3 + 2] * c[e];
-    out[e] = from_acc<TO>(acc);
+  // one CTA per token row (grid-stride): no per-element index division
+  for (int64_t t = blockIdx.x; t < N; t += gridDim.x) {
+    const A t0 = tau[t * 3 + 0], t1 = tau[t * 3 + 1], t2 = tau[t * 3 + 2];
+    const int64_t base = t * row;
+    for (int64_t e = threadIdx.x; e < row; e += blockDim.x) {
+      A acc = A(0) + t0 * a[base + e];
+      acc = acc + t1 * bsel[base + e];
+      acc = acc + t2 * c[base + e];
+      out[base + e] = from_acc<TO>(acc);
+    }
   }
 }
 
@@ -100,10 +102,84 @@ __global__ void combine_kernel(const A* __restrict__ a, const A* __restrict__ bs
 template <typename T>
 __global__ void gate_scale_kernel(const T* __restrict__ d, const typename Acc<T>::type* __restrict__ tau,
                                   int col, T* __restrict__ out, int64_t N, int64_t row) {
-  const int64_t total = N * row;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x)
-    out[e] = from_acc<T>(tau[(e / row) * 3 + col] * to_acc(d[e]));
+  for (int64_t t = blockIdx.x; t < N; t += gridDim.x) {
+    const auto w = tau[t * 3 + col];
+    const int64_t base = t * row;
+    for (int64_t e = threadIdx.x; e < row; e += blockDim.x)
+      out[base + e] = from_acc<T>(w * to_acc(d[base + e]));
+  }
+}
+
+// Fused gate backward + delta for the two differentiated branches
+// (branches.py:103 then kv_major.py:284 / oracle.py:102-131):
+//   dO_sel = tau[t,1] dOut,  dO_slide = tau[t,2] dOut   (rounded to T)
+//   delta_sel[j,t] = sum_v out_sel[t,j,v] dO_sel[t,j,v], delta_slide alike,
+// from the ROUNDED branch cotangents (the values the backward kernels read).
+// One warp per (token, head) row.
+template <typename T>
+__global__ void gate_backward_kernel(const T* __restrict__ dOut,
+                                     const typename Acc<T>::type* __restrict__ tau,
+                                     const typename Acc<T>::type* __restrict__ out_sel,
+                                     const typename Acc<T>::type* __restrict__ out_slide,
+                                     T* __restrict__ d_sel, T* __restrict__ d_slide,
+                                     typename Acc<T>::type* __restrict__ delta_sel,
+                                     typename Acc<T>::type* __restrict__ delta_slide, int64_t N,
+                                     int64_t h, int64_t dv) {
+  using A = typename Acc<T>::type;
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (wid >= N * h) return;
+  const int64_t t = wid / h, j = wid - t * h;
+  const A w1 = tau[t * 3 + 1], w2 = tau[t * 3 + 2];
+  const int64_t base = wid * dv;
+  A s1 = 0, s2 = 0;
+  if constexpr (sizeof(T) == 2) {
+    if ((dv & 127) == 0) {
+      for (int64_t c = lane * 4; c < dv; c += 128) {
+        const uint2 u = *reinterpret_cast<const uint2*>(dOut + base + c);
+        const float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+        const float2 y = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+        const float4 o1 = *reinterpret_cast<const float4*>(out_sel + base + c);
+        const float4 o2 = *reinterpret_cast<const float4*>(out_slide + base + c);
+        const __nv_bfloat162 a0 = __floats2bfloat162_rn(w1 * x.x, w1 * x.y);
+        const __nv_bfloat162 a1 = __floats2bfloat162_rn(w1 * y.x, w1 * y.y);
+        const __nv_bfloat162 b0 = __floats2bfloat162_rn(w2 * x.x, w2 * x.y);
+        const __nv_bfloat162 b1 = __floats2bfloat162_rn(w2 * y.x, w2 * y.y);
+        uint2 ua, ub;
+        ua.x = *reinterpret_cast<const uint32_t*>(&a0);
+        ua.y = *reinterpret_cast<const uint32_t*>(&a1);
+        ub.x = *reinterpret_cast<const uint32_t*>(&b0);
+        ub.y = *reinterpret_cast<const uint32_t*>(&b1);
+        *reinterpret_cast<uint2*>(d_sel + base + c) = ua;
+        *reinterpret_cast<uint2*>(d_slide + base + c) = ub;
+        const float2 fa0 = __bfloat1622float2(a0), fa1 = __bfloat1622float2(a1);
+        const float2 fb0 = __bfloat1622float2(b0), fb1 = __bfloat1622float2(b1);
+        s1 += o1.x * fa0.x + o1.y * fa0.y + o1.z * fa1.x + o1.w * fa1.y;
+        s2 += o2.x * fb0.x + o2.y * fb0.y + o2.z * fb1.x + o2.w * fb1.y;
+      }
+      s1 = warp_sum(s1);
+      s2 = warp_sum(s2);
+      if (lane == 0) {
+        delta_sel[j * N + t] = s1;
+        delta_slide[j * N + t] = s2;
+      }
+      return;
+    }
+  }
+  for (int64_t c = lane; c < dv; c += 32) {
+    const A x = to_acc(dOut[base + c]);
+    const T a = from_acc<T>(w1 * x), b = from_acc<T>(w2 * x);
+    d_sel[base + c] = a;
+    d_slide[base + c] = b;
+    s1 += out_sel[base + c] * to_acc(a);
+    s2 += out_slide[base + c] * to_acc(b);
+  }
+  s1 = warp_sum(s1);
+  s2 = warp_sum(s2);
+  if (lane == 0) {
+    delta_sel[j * N + t] = s1;
+    delta_slide[j * N + t] = s2;
+  }
 }
 
 template <typename T>
@@ -150,10 +226,9 @@ template <typename T>
 int combine_impl(const fsa_shape* s, const void* a, const void* b, const void* c, const void* tau,
                  void* out, int out_acc, cudaStream_t st) {
   using A = typename Acc<T>::type;
-  const int64_t row = s->h * s->d_V, total = s->N * row;
-  int64_t blocks = (total + 255) / 256;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  if (blocks < 1) blocks = 1;
+  const int64_t row = s->h * s->d_V;
+  int64_t blocks = s->N < 148 * 16 ? s->N : 148 * 16;
+  if (blocks < 1) return FSA_OK;
   if (out_acc)
     combine_kernel<A, A><<<(unsigned)blocks, 256, 0, st>>>((const A*)a, (const A*)b, (const A*)c,
                                                           (const A*)tau, (A*)out, s->N, row);
@@ -168,13 +243,26 @@ template <typename T>
 int gate_scale_impl(const fsa_shape* s, const void* d, const void* tau, int col, void* out,
                     cudaStream_t st) {
   using A = typename Acc<T>::type;
-  const int64_t row = s->h * s->d_V, total = s->N * row;
-  int64_t blocks = (total + 255) / 256;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  if (blocks < 1) blocks = 1;
+  const int64_t row = s->h * s->d_V;
+  int64_t blocks = s->N < 148 * 16 ? s->N : 148 * 16;
+  if (blocks < 1) return FSA_OK;
   gate_scale_kernel<T><<<(unsigned)blocks, 256, 0, st>>>((const T*)d, (const A*)tau, col, (T*)out,
                                                         s->N, row);
   FSA_LAUNCH_CHECK("gate_scale");
+  return FSA_OK;
+}
+
+template <typename T>
+int gate_backward_impl(const fsa_shape* s, const void* dOut, const void* tau, const void* out_sel,
+                       const void* out_slide, void* d_sel, void* d_slide, void* delta_sel,
+                       void* delta_slide, cudaStream_t st) {
+  using A = typename Acc<T>::type;
+  const int64_t rows = s->N * s->h;
+  if (rows == 0) return FSA_OK;
+  gate_backward_kernel<T><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(
+      (const T*)dOut, (const A*)tau, (const A*)out_sel, (const A*)out_slide, (T*)d_sel,
+      (T*)d_slide, (A*)delta_sel, (A*)delta_slide, s->N, s->h, s->d_V);
+  FSA_LAUNCH_CHECK("gate_backward");
   return FSA_OK;
 }
 
@@ -219,6 +307,13 @@ extern "C" int fsa_gated_combine(const fsa_shape* s, int dtype, const void* out_
 extern "C" int fsa_gate_scale(const fsa_shape* s, int dtype, const void* dOut, const void* tau,
                               int col, void* out, void* stream) {
   DISPATCH_DT(dtype, gate_scale_impl, s, dOut, tau, col, out, (cudaStream_t)stream);
+}
+
+extern "C" int fsa_gate_backward(const fsa_shape* s, int dtype, const void* dOut, const void* tau,
+                                 const void* out_sel, const void* out_slide, void* d_sel,
+                                 void* d_slide, void* delta_sel, void* delta_slide, void* stream) {
+  DISPATCH_DT(dtype, gate_backward_impl, s, dOut, tau, out_sel, out_slide, d_sel, d_slide, delta_sel,
+              delta_slide, (cudaStream_t)stream);
 }
 
 extern "C" int fsa_check_finite(int dtype, const void* x, int64_t n, int32_t* flag, void* stream) {

@@ -95,6 +95,112 @@ __global__ void topk_warp_kernel(const S* __restrict__ scores, int32_t* __restri
   if (lane < T) idx[row * T + lane] = (v == 0x7fffffff) ? -1 : v;
 }
 
+// 32-bit monotone key of an f32 score (0 = not selectable: NaN / -inf).
+__device__ __forceinline__ uint32_t score_key32(float f) {
+  if (isnan(f) || f == -INFINITY) return 0u;
+  if (f == 0.0f) f = 0.0f;  // canonicalise -0.0
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+// f32 scores, b <= 32 * PER, T <= 32: one warp per (kh, t) row, the row's
+// causal candidates held in registers (candidate c = k * 32 + lane in
+// register k), and the T-th best key found by an exact 4-pass 8-bit radix
+// select over a per-warp shared-memory histogram.  Then
+//   selected = {key > kth} + the lowest-index (need) candidates with key == kth,
+// which is exactly the first T of the stable (score desc, index asc) order.
+// The ascending output falls out of a ballot compaction in index order.
+template <int PER>
+__global__ void __launch_bounds__(256) topk_radix_kernel(const float* __restrict__ scores,
+                                                         int32_t* __restrict__ idx, int64_t rows,
+                                                         int64_t N, int64_t B_K, int64_t b, int T) {
+  __shared__ uint32_t hist_all[8][256];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t row = blockIdx.x * 8ll + wib;
+  if (row >= rows) return;
+  uint32_t* hist = hist_all[wib];
+  const int64_t t = row % N;
+  const int own = (int)(t / B_K), ncand = own + 1;
+  const float* sr = scores + row * b;
+  uint32_t key[PER];
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int c = k * 32 + lane;
+    key[k] = c < ncand ? (c == own ? 0xFF800000u : score_key32(__ldg(sr + c))) : 0u;
+  }
+  int nsel = 0;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) nsel += __popc(__ballot_sync(0xffffffffu, key[k] != 0u));
+  uint32_t kth = 1u;  // keys >= kth are candidates for selection
+  int need = 0;       // how many keys == kth to take (lowest index first)
+  if (nsel > T) {
+    uint32_t prefix = 0u, pmask = 0u;
+    need = T;
+#pragma unroll 1
+    for (int shift = 24; shift >= 0; shift -= 8) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) hist[lane * 8 + q] = 0u;
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < PER; ++k)
+        if (key[k] != 0u && (key[k] & pmask) == prefix) atomicAdd(&hist[(key[k] >> shift) & 255u], 1u);
+      __syncwarp();
+      // lane L owns digits 255 - 8L .. 248 - 8L (descending); inclusive scan
+      uint32_t cnt[8], tot = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        cnt[q] = hist[255 - lane * 8 - q];
+        tot += cnt[q];
+      }
+      uint32_t incl = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const uint32_t excl = incl - tot;
+      const unsigned hit = __ballot_sync(0xffffffffu, excl < (uint32_t)need && incl >= (uint32_t)need);
+      const int src = __ffs(hit) - 1;
+      uint32_t digit = 0u, above = 0u;
+      if (lane == src) {
+        uint32_t run = excl;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (run + cnt[q] >= (uint32_t)need) {
+            digit = 255u - (uint32_t)(lane * 8 + q);
+            above = run;
+            break;
+          }
+          run += cnt[q];
+        }
+      }
+      digit = __shfl_sync(0xffffffffu, digit, src);
+      above = __shfl_sync(0xffffffffu, above, src);
+      need -= (int)above;
+      prefix |= digit << shift;
+      pmask |= 0xFFu << shift;
+      __syncwarp();
+    }
+    kth = prefix;
+  }
+  // compaction in ascending index order
+  int taken_eq = 0, out = 0;
+  const unsigned lt = (1u << lane) - 1u;
+  int32_t* dst = idx + row * T;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const bool eq = nsel > T && key[k] == kth;
+    const unsigned me = __ballot_sync(0xffffffffu, eq);
+    const bool sel = key[k] != 0u && (key[k] > kth || (eq && taken_eq + __popc(me & lt) < need) ||
+                                      (nsel <= T));
+    taken_eq += __popc(me);
+    const unsigned ms = __ballot_sync(0xffffffffu, sel);
+    if (sel) dst[out + __popc(ms & lt)] = k * 32 + lane;
+    out += __popc(ms);
+  }
+  if (lane >= out && lane < T) dst[lane] = -1;
+}
+
 // One CTA per row for T > 32: bitonic sort of all causal candidates in smem.
 template <typename S>
 __global__ void topk_block_kernel(const S* __restrict__ scores, int32_t* __restrict__ idx,
@@ -191,7 +297,16 @@ int topk_impl(const fsa_shape* s, const void* scores, int32_t* idx, cudaStream_t
   const int64_t b = s->N / s->B_K, rows = s->h_K * s->N;
   const int T = (int)s->T;
   if (rows == 0) return FSA_OK;
-  if (T <= 32) {
+  if (sizeof(S) == 4 && T <= 32 && b <= 1024) {
+    const float* sc = (const float*)scores;
+    const unsigned grid = (unsigned)((rows + 7) / 8);
+    if (b <= 32) topk_radix_kernel<1><<<grid, 256, 0, st>>>(sc, idx, rows, s->N, s->B_K, b, T);
+    else if (b <= 64) topk_radix_kernel<2><<<grid, 256, 0, st>>>(sc, idx, rows, s->N, s->B_K, b, T);
+    else if (b <= 128) topk_radix_kernel<4><<<grid, 256, 0, st>>>(sc, idx, rows, s->N, s->B_K, b, T);
+    else if (b <= 256) topk_radix_kernel<8><<<grid, 256, 0, st>>>(sc, idx, rows, s->N, s->B_K, b, T);
+    else if (b <= 512) topk_radix_kernel<16><<<grid, 256, 0, st>>>(sc, idx, rows, s->N, s->B_K, b, T);
+    else topk_radix_kernel<32><<<grid, 256, 0, st>>>(sc, idx, rows, s->N, s->B_K, b, T);
+  } else if (T <= 32) {
     const int warps = 8;
     topk_warp_kernel<S><<<(unsigned)((rows + warps - 1) / warps), warps * 32, 0, st>>>(
         (const S*)scores, idx, rows, s->N, s->B_K, b, T);

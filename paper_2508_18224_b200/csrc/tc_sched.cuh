@@ -32,6 +32,13 @@ struct Ring {
     slots[k & (kRingDepth - 1)] = (t < ntask) ? t : -1;
     mbar_arrive(full(k));
   }
+  // consumer side, non-blocking: false if slot k is not filled yet
+  __device__ bool try_consume(int k, int32_t& t) const {
+    if (!mbar_try_wait(full(k), (uint32_t)((k / kRingDepth) & 1))) return false;
+    t = slots[k & (kRingDepth - 1)];
+    mbar_arrive(empty(k));
+    return true;
+  }
   // consumer side
   __device__ int32_t consume(int k) const {
     mbar_wait(full(k), (uint32_t)((k / kRingDepth) & 1));

@@ -86,11 +86,14 @@ __device__ __forceinline__ TaskRows rows_of(const Params& p, int32_t task) {
   r.nitems = (int)((r.ntok + p.tpi - 1) / p.tpi);
   return r;
 }
-// token and slot of list position pos of a task
+// query-list entry at position pos of a task (selected mode; loaded ahead of use)
+__device__ __forceinline__ int32_t entry_at(const Params& p, const TaskRows& tr, int64_t pos) {
+  return (p.slide || pos >= tr.ntok) ? 0 : __ldg(p.qlist + tr.kh * p.N * p.T + tr.beg + pos);
+}
+// token and slot of list position pos of a task (ent = entry_at(pos))
 __device__ __forceinline__ void token_of(const Params& p, const TaskRows& tr, int64_t pos,
-                                         int64_t& t, int64_t& slot) {
+                                         int32_t ent, int64_t& t, int64_t& slot) {
   if (!p.slide) {
-    const int32_t ent = __ldg(p.qlist + tr.kh * p.N * p.T + tr.beg + pos);
     t = p.fdT.div((uint32_t)ent);
     slot = ent - t * p.T;
   } else {
@@ -164,15 +167,18 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
         asm volatile("cp.async.commit_group;" ::: "memory");
       }
       bool kv_pending = true;
+      int32_t ent_next = kt < p.tpi ? entry_at(p, tr, kt) : 0;
       for (int c = 0; c < tr.nitems; ++c, ++n) {
         const int s = (int)(n & 1);
-        mbar_wait(bar(B_QDE + s), (uint32_t)(((n >> 1) & 1) ^ 1));
         const int64_t pos = (int64_t)c * p.tpi + kt;
         const bool ok = kt < p.tpi && pos < tr.ntok;
+        const int32_t ent = ent_next;
+        ent_next = kt < p.tpi ? entry_at(p, tr, pos + p.tpi) : 0;
+        mbar_wait(bar(B_QDE + s), (uint32_t)(((n >> 1) & 1) ^ 1));
         int64_t row = 0;
         if (ok) {
           int64_t t, slot;
-          token_of(p, tr, pos, t, slot);
+          token_of(p, tr, pos, ent, t, slot);
           row = t * p.h + tr.kh * p.g + hh;
         }
         warp_gather_rows32(sb + kOffQ + s * kTile, 16384u, lr & ~31, p.Q + row * kD, ok, lane);
@@ -193,100 +199,117 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
     }
   } else if (warp == 12) {
     // ================================================================ MMA issuer
+    // Two independent in-order streams, polled without blocking:
+    //   S stream : S/dP of item m (needs its Q/dO gather, the task's K/V, and
+    //              a free S/dP TMEM stage -- at most 2 items ahead of P);
+    //   P stream : products of item m (needs the softmax's P/dS of item m).
+    // Products never wait for the next item's gather, so a stage is released
+    // (and its next gather started) as soon as the softmax is done with it.
     if (lane == 0) {
       const uint32_t tK = tmem + kColDK, tV = tmem + kColDV;
       TaskFifo fifo;
-      int ka = 0, a_c = 0;
-      int64_t a_kseq = -1;
-      TaskRows a_tr{};
-      bool a_done = false, a_started = false;
-      auto a_next = [&]() -> bool {
-        if (a_done) return false;
-        if (a_started && a_c + 1 < a_tr.nitems) {
-          ++a_c;
-          return true;
-        }
-        for (;;) {
-          const int32_t t = ring.consume(ka++);
-          if (t < 0) {
-            a_done = true;
-            return false;
-          }
-          const TaskRows tr = rows_of(p, t);
-          if (tr.nitems == 0) continue;
-          a_tr = tr;
-          a_c = 0;
-          a_started = true;
-          ++a_kseq;
-          fifo.push(t);
-          return true;
-        }
-      };
-      auto issue_sdp = [&](int64_t n, int64_t kseq) {
-        const int s = (int)(n & 1);
-        mbar_wait(bar(B_KVF), (uint32_t)(kseq & 1));
-        mbar_wait(bar(B_QDF + s), (uint32_t)((n >> 1) & 1));
-        mbar_wait(bar(B_SDE + s), (uint32_t)(((n >> 1) & 1) ^ 1));
-        tc_fence_after();
-        const uint32_t q = sb + kOffQ + s * kTile, o = sb + kOffDO + s * kTile;
-        const uint32_t tS = tmem + 128u * s;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint32_t ko = (k >> 2) * 16384u + (k & 3) * 32u, kk = (k >> 2) * 8192u + (k & 3) * 32u;
-          mma_bf16(tS, desc_kmajor(q + ko), desc_kmajor(sb + kOffK + kk), kIdS, k > 0);
-        }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint32_t ko = (k >> 2) * 16384u + (k & 3) * 32u, kk = (k >> 2) * 8192u + (k & 3) * 32u;
-          mma_bf16(tS + 64, desc_kmajor(o + ko), desc_kmajor(sb + kOffV + kk), kIdS, k > 0);
-        }
-        mma_commit(bar(B_SDF + s));
-      };
-      bool have = a_next();
-      int64_t n_ahead = 0;
-      if (have) issue_sdp(0, a_kseq);
-      int64_t kseq_b = -1;
+      int ka = 0, a_c = 0, a_n = 0;  // ring index, item in task, items in task
+      int64_t a_kseq = -1, ns = 0;   // K/V sequence of the S stream, next S item
+      bool a_done = false;
       TaskRows b_tr{};
       int b_c = 0;
-      for (int64_t n = 0; have; ++n) {
-        if (n == 0 || b_c + 1 >= b_tr.nitems) {
-          b_tr = rows_of(p, fifo.pop());
-          b_c = 0;
-          ++kseq_b;
-        } else {
-          ++b_c;
+      int64_t kseq_b = -1, np = 0;   // next products item
+      long long idle_since = 0;
+      for (;;) {
+        bool progressed = false;
+        // ---- S stream
+        if (!a_done && ns < np + 2) {
+          bool have = a_c < a_n;
+          while (!have) {
+            int32_t t;
+            if (!ring.try_consume(ka, t)) break;
+            ++ka;
+            if (t < 0) {
+              a_done = true;
+              break;
+            }
+            const TaskRows tr = rows_of(p, t);
+            if (tr.nitems == 0) continue;
+            a_c = 0;
+            a_n = tr.nitems;
+            ++a_kseq;
+            fifo.push(t);
+            have = true;
+          }
+          if (have) {
+            const int s = (int)(ns & 1);
+            if (mbar_try_wait(bar(B_KVF), (uint32_t)(a_kseq & 1)) &&
+                mbar_try_wait(bar(B_QDF + s), (uint32_t)((ns >> 1) & 1)) &&
+                mbar_try_wait(bar(B_SDE + s), (uint32_t)(((ns >> 1) & 1) ^ 1))) {
+              tc_fence_after();
+              const uint32_t q = sb + kOffQ + s * kTile, o = sb + kOffDO + s * kTile;
+              const uint32_t tS = tmem + 128u * s;
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                const uint32_t ko = (k >> 2) * 16384u + (k & 3) * 32u, kk = (k >> 2) * 8192u + (k & 3) * 32u;
+                mma_bf16(tS, desc_kmajor(q + ko), desc_kmajor(sb + kOffK + kk), kIdS, k > 0);
+              }
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                const uint32_t ko = (k >> 2) * 16384u + (k & 3) * 32u, kk = (k >> 2) * 8192u + (k & 3) * 32u;
+                mma_bf16(tS + 64, desc_kmajor(o + ko), desc_kmajor(sb + kOffV + kk), kIdS, k > 0);
+              }
+              mma_commit(bar(B_SDF + s));
+              ++a_c;
+              ++ns;
+              progressed = true;
+            }
+          }
         }
-        const bool first = b_c == 0, last = b_c + 1 == b_tr.nitems;
-        // look ahead: S/dP of item n+1 -- unless it starts a new task: K/V are
-        // single-buffered and only released by the products of item n
-        have = a_next();
-        const bool defer = have && a_c == 0;
-        if (have && !defer) issue_sdp(++n_ahead, a_kseq);
-        const int s = (int)(n & 1);
-        mbar_wait(bar(B_PDF + s), (uint32_t)((n >> 1) & 1));
-        if (first) mbar_wait(bar(B_KAE), (uint32_t)((kseq_b & 1) ^ 1));
-        tc_fence_after();
-        const uint32_t q = sb + kOffQ + s * kTile, o = sb + kOffDO + s * kTile;
-        const uint32_t pp = sb + kOffP + s * 16384u, ds = sb + kOffDS + s * 16384u;
+        // ---- P stream
+        if (np < ns) {
+          const bool first = np == 0 || b_c + 1 >= b_tr.nitems;
+          const int s = (int)(np & 1);
+          const bool ready = mbar_try_wait(bar(B_PDF + s), (uint32_t)((np >> 1) & 1)) &&
+                             (!first || mbar_try_wait(bar(B_KAE), (uint32_t)(((kseq_b + 1) & 1) ^ 1)));
+          if (ready) {
+            if (first) {
+              b_tr = rows_of(p, fifo.pop());
+              b_c = 0;
+              ++kseq_b;
+            } else {
+              ++b_c;
+            }
+            const bool last = b_c + 1 == b_tr.nitems;
+            tc_fence_after();
+            const uint32_t q = sb + kOffQ + s * kTile, o = sb + kOffDO + s * kTile;
+            const uint32_t pp = sb + kOffP + s * 16384u, ds = sb + kOffDS + s * 16384u;
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          mma_bf16(tV, desc_mnmajor(o + k * 2048u, 16384u), desc_mnmajor(pp + k * 2048u, 8192u),
-                   kIdKV, (first && k == 0) ? 0u : 1u);
+            for (int k = 0; k < 8; ++k)
+              mma_bf16(tV, desc_mnmajor(o + k * 2048u, 16384u), desc_mnmajor(pp + k * 2048u, 8192u),
+                       kIdKV, (first && k == 0) ? 0u : 1u);
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          mma_bf16(tK, desc_mnmajor(q + k * 2048u, 16384u), desc_mnmajor(ds + k * 2048u, 8192u),
-                   kIdKV, (first && k == 0) ? 0u : 1u);
+            for (int k = 0; k < 8; ++k)
+              mma_bf16(tK, desc_mnmajor(q + k * 2048u, 16384u), desc_mnmajor(ds + k * 2048u, 8192u),
+                       kIdKV, (first && k == 0) ? 0u : 1u);
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          mma_bf16(tmem + 128u * s, desc_kmajor(ds + k * 32u),
-                   desc_mnmajor(sb + kOffK + k * 2048u, 8192u), kIdQ, k > 0);
-        mma_commit(bar(B_DQF + s));
-        mma_commit(bar(B_QDE + s));
-        if (last) {
-          mma_commit(bar(B_KAF));
-          mma_commit(bar(B_KVE));
+            for (int k = 0; k < 4; ++k)
+              mma_bf16(tmem + 128u * s, desc_kmajor(ds + k * 32u),
+                       desc_mnmajor(sb + kOffK + k * 2048u, 8192u), kIdQ, k > 0);
+            mma_commit(bar(B_DQF + s));
+            mma_commit(bar(B_QDE + s));
+            if (last) {
+              mma_commit(bar(B_KAF));
+              mma_commit(bar(B_KVE));
+            }
+            ++np;
+            progressed = true;
+          }
         }
-        if (defer) issue_sdp(++n_ahead, a_kseq);
+        if (a_done && np == ns) break;
+        // watchdog: trap instead of hanging if neither stream can move for seconds
+        if (progressed) {
+          idle_since = 0;
+        } else if (idle_since == 0) {
+          idle_since = clock64();
+        } else if (clock64() - idle_since > (1ll << 34)) {
+          mbar_stuck(bar(B_SDF), 0);
+        }
       }
     }
   } else {
@@ -340,17 +363,22 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
         }
         continue;
       }
+      // entries of this warpgroup's items (every other item), one own item ahead
+      const int c0 = (int)((wg - n) & 1);
+      int32_t ent_next = kt < p.tpi ? entry_at(p, tr, (int64_t)c0 * p.tpi + kt) : 0;
       for (int c = 0; c < tr.nitems; ++c, ++n) {
         if ((int)(n & 1) != wg) continue;
         const int s = (int)(n & 1);
         const int64_t pos = (int64_t)c * p.tpi + kt;
         const bool ok = kt < p.tpi && pos < tr.ntok;
+        const int32_t ent = ent_next;
+        ent_next = kt < p.tpi ? entry_at(p, tr, pos + 2 * p.tpi) : 0;
         int klo = 0, khi = -1;  // visible keys of the block: [klo, khi]
         int64_t drow = -1;
         float lse_r = 0.f, dl = 0.f;
         if (ok) {
           int64_t t, slot;
-          token_of(p, tr, pos, t, slot);
+          token_of(p, tr, pos, ent, t, slot);
           const int64_t j = tr.kh * p.g + hh;
           drow = (j * p.N + t) * p.T + slot;
           const int64_t hi = t - tr.i * kBK;

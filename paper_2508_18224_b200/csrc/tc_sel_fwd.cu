@@ -123,12 +123,18 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const Params p)
       }
       bool kv_pending = true;
       const int32_t* ql = p.qlist + (int64_t)tr.kh * p.N * p.T + tr.beg;
+      // the query-list entry of the next item is loaded one item ahead, so its
+      // latency hides behind the current item's stage wait and gather
+      int ent_next = (kt_row < p.tpi && kt_row < tr.ntok) ? __ldg(ql + kt_row) : 0;
       for (int c = 0; c < tr.nitems; ++c, ++n) {
         const int s = n % kQStages;
-        mbar_wait(bar(B_QE + s), (uint32_t)(((n / kQStages) & 1) ^ 1));
         const int pos = c * p.tpi + kt_row;
         const bool ok = kt_row < p.tpi && pos < tr.ntok;
-        const int t = ok ? (int)p.fdT.div((uint32_t)__ldg(ql + pos)) : 0;
+        const int ent = ent_next;
+        const int pos1 = pos + p.tpi;
+        ent_next = (kt_row < p.tpi && pos1 < tr.ntok) ? __ldg(ql + pos1) : 0;
+        mbar_wait(bar(B_QE + s), (uint32_t)(((n / kQStages) & 1) ^ 1));
+        const int t = ok ? (int)p.fdT.div((uint32_t)ent) : 0;
         warp_gather_rows32(sb + kOffQ + s * kQBytes, 16384u, lr & ~31,
                            p.Q + (t * p.h + (int)tr.kh * p.g + hh) * kD, ok, lane);
         asm volatile("cp.async.commit_group;" ::: "memory");
@@ -152,77 +158,92 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const Params p)
     }
   } else if (warp == 12) {
     // ------------------------------------------------------------ MMA issuer
+    // Two in-order streams polled without blocking (as in tc_sel_bwd.cu):
+    // S = Q K^T of item m needs its gather, the task's K/V stage and a free S
+    // TMEM stage; O = P V of item m needs the softmax's P.  PV never waits for
+    // the next item's gather.
     if (lane == 0) {
       const uint32_t tS = tmem, tO = tmem + 128;
       TaskFifo fifo;
-      int ka = 0, a_c = 0, a_kseq = -1;
-      TaskRows a_tr{};
-      bool a_done = false, a_started = false;
-      auto a_next = [&]() -> bool {
-        if (a_done) return false;
-        if (a_started && a_c + 1 < a_tr.nitems) {
-          ++a_c;
-          return true;
-        }
-        for (;;) {
-          const int32_t t = ring.consume(ka++);
-          if (t < 0) {
-            a_done = true;
-            return false;
-          }
-          const TaskRows tr = task_rows(t, p.offsets, p.b, p.tpi);
-          if (tr.nitems == 0) continue;
-          a_tr = tr;
-          a_c = 0;
-          a_started = true;
-          ++a_kseq;
-          fifo.push(t);
-          return true;
-        }
-      };
-      auto issue_s = [&](int n, int kseq) {
-        const int s = n % kQStages, v = n & 1, kvs = kseq & 1;
-        mbar_wait(bar(B_KVF + kvs), (uint32_t)((kseq >> 1) & 1));
-        mbar_wait(bar(B_QF + s), (uint32_t)((n / kQStages) & 1));
-        mbar_wait(bar(B_SE + v), (uint32_t)(((n >> 1) & 1) ^ 1));
-        tc_fence_after();
-        const uint32_t qa = sb + kOffQ + s * kQBytes;
-        const uint32_t ka_ = sb + kOffKV + kvs * kKVBytes;
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          mma_bf16(tS + v * 64, desc_kmajor(qa + (k >> 2) * 16384u + (k & 3) * 32u),
-                   desc_kmajor(ka_ + (k >> 2) * 8192u + (k & 3) * 32u), kIdescS, k > 0);
-        mma_commit(bar(B_SF + v));
-        mma_commit(bar(B_QE + s));
-      };
-      bool have = a_next();
-      int n_ahead = 0;
-      if (have) issue_s(0, a_kseq);
-      int b_kseq = -1, b_c = 0;
+      int ka = 0, a_c = 0, a_n = 0, a_kseq = -1, ns = 0;
+      bool a_done = false;
       TaskRows b_tr{};
-      for (int n = 0; have; ++n) {
-        if (n == 0 || b_c + 1 >= b_tr.nitems) {
-          b_tr = task_rows(fifo.pop(), p.offsets, p.b, p.tpi);
-          b_c = 0;
-          ++b_kseq;
-        } else {
-          ++b_c;
-        }
-        const bool last = b_c + 1 == b_tr.nitems;
-        have = a_next();
-        if (have) issue_s(++n_ahead, a_kseq);
-        const int v = n & 1, kvs = b_kseq & 1;
-        mbar_wait(bar(B_PF + v), (uint32_t)((n >> 1) & 1));
-        mbar_wait(bar(B_OE + v), (uint32_t)(((n >> 1) & 1) ^ 1));
-        tc_fence_after();
-        const uint32_t va = sb + kOffKV + kvs * kKVBytes + 16384u;
+      int b_c = 0, b_kseq = -1, np = 0;
+      long long idle_since = 0;
+      for (;;) {
+        bool progressed = false;
+        if (!a_done && ns < np + 2) {
+          bool have = a_c < a_n;
+          while (!have) {
+            int32_t t;
+            if (!ring.try_consume(ka, t)) break;
+            ++ka;
+            if (t < 0) {
+              a_done = true;
+              break;
+            }
+            const TaskRows tr = task_rows(t, p.offsets, p.b, p.tpi);
+            if (tr.nitems == 0) continue;
+            a_c = 0;
+            a_n = tr.nitems;
+            ++a_kseq;
+            fifo.push(t);
+            have = true;
+          }
+          if (have) {
+            const int s = ns % kQStages, v = ns & 1, kvs = a_kseq & 1;
+            if (mbar_try_wait(bar(B_KVF + kvs), (uint32_t)((a_kseq >> 1) & 1)) &&
+                mbar_try_wait(bar(B_QF + s), (uint32_t)((ns / kQStages) & 1)) &&
+                mbar_try_wait(bar(B_SE + v), (uint32_t)(((ns >> 1) & 1) ^ 1))) {
+              tc_fence_after();
+              const uint32_t qa = sb + kOffQ + s * kQBytes;
+              const uint32_t ka_ = sb + kOffKV + kvs * kKVBytes;
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          mma_bf16_ts(tO + v * 128, tmem + kColP + v * 32 + k * 8, desc_mnmajor(va + k * 2048u, 8192u),
-                   kIdescPV, k > 0);
-        mma_commit(bar(B_OF + v));
-        mma_commit(bar(B_PE + v));
-        if (last) mma_commit(bar(B_KVE + kvs));
+              for (int k = 0; k < 8; ++k)
+                mma_bf16(tS + v * 64, desc_kmajor(qa + (k >> 2) * 16384u + (k & 3) * 32u),
+                         desc_kmajor(ka_ + (k >> 2) * 8192u + (k & 3) * 32u), kIdescS, k > 0);
+              mma_commit(bar(B_SF + v));
+              mma_commit(bar(B_QE + s));
+              ++a_c;
+              ++ns;
+              progressed = true;
+            }
+          }
+        }
+        if (np < ns) {
+          const int v = np & 1;
+          if (mbar_try_wait(bar(B_PF + v), (uint32_t)((np >> 1) & 1)) &&
+              mbar_try_wait(bar(B_OE + v), (uint32_t)(((np >> 1) & 1) ^ 1))) {
+            if (np == 0 || b_c + 1 >= b_tr.nitems) {
+              b_tr = task_rows(fifo.pop(), p.offsets, p.b, p.tpi);
+              b_c = 0;
+              ++b_kseq;
+            } else {
+              ++b_c;
+            }
+            const bool last = b_c + 1 == b_tr.nitems;
+            const int kvs = b_kseq & 1;
+            tc_fence_after();
+            const uint32_t va = sb + kOffKV + kvs * kKVBytes + 16384u;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              mma_bf16_ts(tO + v * 128, tmem + kColP + v * 32 + k * 8,
+                          desc_mnmajor(va + k * 2048u, 8192u), kIdescPV, k > 0);
+            mma_commit(bar(B_OF + v));
+            mma_commit(bar(B_PE + v));
+            if (last) mma_commit(bar(B_KVE + kvs));
+            ++np;
+            progressed = true;
+          }
+        }
+        if (a_done && np == ns) break;
+        if (progressed) {
+          idle_since = 0;
+        } else if (idle_since == 0) {
+          idle_since = clock64();
+        } else if (clock64() - idle_since > (1ll << 34)) {
+          mbar_stuck(bar(B_SF), 0);
+        }
       }
     }
   } else {
@@ -280,14 +301,23 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const Params p)
       if (task < 0) break;
       const TaskRows tr = task_rows(task, p.offsets, p.b, p.tpi);
       const int32_t* ql = p.qlist + (int64_t)tr.kh * p.N * p.T + tr.beg;
+      // entries of this warpgroup's items (every other item) are loaded one
+      // own item ahead
+      const int c0 = (int)((wg - n) & 1);
+      int ent_next = (c0 < tr.nitems && kt_row < p.tpi && c0 * p.tpi + kt_row < tr.ntok)
+                         ? __ldg(ql + c0 * p.tpi + kt_row) : 0;
       for (int c = 0; c < tr.nitems; ++c, ++n) {
         if ((n & 1) != wg) continue;
         const int s = n & 1;
         const int pos = c * p.tpi + kt_row;
+        const int ent = ent_next;
+        {
+          const int pos2 = pos + 2 * p.tpi;
+          ent_next = (kt_row < p.tpi && pos2 < tr.ntok) ? __ldg(ql + pos2) : 0;
+        }
         int64_t orow = -1;
         int vis = kBK;
         if (kt_row < p.tpi && pos < tr.ntok) {
-          const int ent = __ldg(ql + pos);
           const int t = (int)p.fdT.div((uint32_t)ent), slot = ent - t * p.T;
           orow = ((int64_t)((int)tr.kh * p.g + hh) * p.N + t) * p.T + slot;
           const int v = t - (int)tr.i * kBK + 1;

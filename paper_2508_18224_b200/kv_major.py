@@ -223,14 +223,16 @@ def selected_forward(Q, K, V, sel: SelectionTensor, cfg, *, shared_max: bool = F
     return AttentionOutput(out=logical(out), lse=lse), forward_meter(inv.n_valid, cfg)
 
 
-def _backward_core(cfg, dt, q, k, v, do, sel, inv, out, lse):
-    """K7 + K8 + K9 on storage-layout tensors; returns dQ, dK, dV storage (acc dtype)."""
+def _backward_core(cfg, dt, q, k, v, do, sel, inv, out, lse, delta=None):
+    """K7 + K8 + K9 on storage-layout tensors; returns dQ, dK, dV storage (acc dtype).
+    ``delta`` (h, N) may be passed precomputed (fsa_gate_backward)."""
     dev, acc = q.device, _lib.acc_dtype(dt)
     s = _lib.shape_of(cfg)
     st = _lib.stream()
-    delta = torch.empty((cfg.h, cfg.N), dtype=acc, device=dev)
-    _lib.call("fsa_bwd_delta", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(out), _lib.ptr(do),
-              _lib.ptr(delta), st)
+    if delta is None:
+        delta = torch.empty((cfg.h, cfg.N), dtype=acc, device=dev)
+        _lib.call("fsa_bwd_delta", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(out), _lib.ptr(do),
+                  _lib.ptr(delta), st)
     _, (dq_code, dq_dtype) = _lib.buffer_dtypes(cfg, dt)
     dq_buf = torch.empty((cfg.h, cfg.N, cfg.T, cfg.d_K), dtype=dq_dtype, device=dev)
     dK = torch.empty((cfg.N, cfg.h_K, cfg.d_K), dtype=acc, device=dev)

@@ -92,16 +92,19 @@ def nsa_backward(ctx: NSAContext, dout):
     cfg, dt = ctx.cfg, ctx.dtype
     s = _lib.shape_of(cfg)
     st = _lib.stream()
+    acc = _lib.acc_dtype(dt)
     d_sel = torch.empty_like(dout)
     d_slide = torch.empty_like(dout)
-    _lib.call("fsa_gate_scale", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(dout),
-              _lib.ptr(ctx.tau), 1, _lib.ptr(d_sel), st)
-    _lib.call("fsa_gate_scale", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(dout),
-              _lib.ptr(ctx.tau), 2, _lib.ptr(d_slide), st)
+    delta_sel = torch.empty((cfg.h, cfg.N), dtype=acc, device=dout.device)
+    delta_slide = torch.empty_like(delta_sel)
+    # gate backward into both differentiated branches + their deltas, one pass
+    _lib.call("fsa_gate_backward", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(dout),
+              _lib.ptr(ctx.tau), _lib.ptr(ctx.out_sel), _lib.ptr(ctx.out_slide), _lib.ptr(d_sel),
+              _lib.ptr(d_slide), _lib.ptr(delta_sel), _lib.ptr(delta_slide), st)
     dQ, dK, dV = _backward_core(cfg, dt, ctx.q, ctx.k, ctx.v, d_sel, ctx.sel, ctx.inv,
-                                ctx.out_sel, ctx.lse_sel)
+                                ctx.out_sel, ctx.lse_sel, delta=delta_sel)
     return _slide_bwd_storage(cfg, dt, ctx.q, ctx.k, ctx.v, d_slide, ctx.out_slide,
-                              ctx.lse_slide, accumulate_into=(dQ, dK, dV))
+                              ctx.lse_slide, accumulate_into=(dQ, dK, dV), delta=delta_slide)
 
 
 def nsa_forward_backward(q, k, v, tau, dout, cfg):

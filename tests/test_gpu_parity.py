@@ -76,6 +76,29 @@ def test_select_topk_random_vs_oracle(kw, sdt):
     np.testing.assert_array_equal(host(got.idx), want)
 
 
+@pytest.mark.parametrize("kw", [
+    dict(N=16384, d_K=8, d_V=8, h=2, h_K=2, B_K=16, T=16),   # b = 1024 (32 candidates / lane)
+    dict(N=4800, d_K=8, d_V=8, h=1, h_K=1, B_K=16, T=32),    # b = 300, T = 32
+    dict(N=2048, d_K=8, d_V=8, h=1, h_K=1, B_K=64, T=1),     # b = 32, T = 1
+])
+def test_select_topk_ties_and_specials(kw):
+    """Radix-select path (f32): heavy exact ties at the T-th key, +inf
+    (ties the own block; wins on index), -0.0 vs +0.0, -inf / NaN."""
+    c = O.cfg_of(**kw)
+    rng = np.random.default_rng(kw["b"] if "b" in kw else kw["N"])
+    scores = np.round(rng.standard_normal((c.h_K, c.N, c.b)) * 2) / 2  # few distinct values
+    u = rng.uniform(size=scores.shape)
+    scores[u < 0.02] = np.inf
+    scores[(u >= 0.02) & (u < 0.05)] = -0.0
+    scores[(u >= 0.05) & (u < 0.08)] = 0.0
+    scores[(u >= 0.08) & (u < 0.10)] = -np.inf
+    scores[(u >= 0.10) & (u < 0.11)] = np.nan
+    scores = scores.astype(np.float32).astype(np.float64)
+    want = O.select_topk(scores, c)
+    got = fsa.select_topk_blocks(torch.from_numpy(scores).float().cuda(), _cfg(kw))
+    np.testing.assert_array_equal(host(got.idx), want)
+
+
 def test_malformed_selection_messages():
     z = load("malformed")
     cfg = _cfg(json.loads(str(z["cfg"])))

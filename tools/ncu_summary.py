@@ -56,20 +56,34 @@ def main():
             vals.append(f"{v * scale:>10.3f}")
         print("  ".join(vals) + "  " + (r[name_i][:60] if name_i is not None else ""))
     if "--source" in sys.argv:
+        which = 0
+        for a in sys.argv:
+            if a.startswith("--kernel="):
+                which = int(a.split("=")[1])
         src = _csv(["-i", rep, "--page", "source", "--csv", "--print-source", "sass"])
-        if not src:
+        sections, cur = [], None
+        for r in src:
+            if r and r[0] == "Kernel Name":
+                cur = {"hdr": None, "rows": []}
+                sections.append(cur)
+            elif cur is not None and r and r[0] == "Address":
+                cur["hdr"] = r
+            elif cur is not None and cur["hdr"] and len(r) == len(cur["hdr"]):
+                cur["rows"].append(r)
+        if not sections:
+            print("no source page")
             return
-        h = src[0]
+        sec = sections[min(which, len(sections) - 1)]
+        h = sec["hdr"]
         ci = {x: i for i, x in enumerate(h)}
         key = "Warp Stall Sampling (All Samples)"
-        if key not in ci:
-            print("no stall sampling column")
-            return
-        body = [r for r in src[1:] if len(r) == len(h) and r[ci[key]].replace(".", "").isdigit()]
+        body = [r for r in sec["rows"] if r[ci[key]].replace(".", "").isdigit()]
         tot = sum(float(r[ci[key]]) for r in body) or 1.0
-        body.sort(key=lambda r: -float(r[ci[key]]))
-        for r in body[:25]:
-            print(f"{100 * float(r[ci[key]]) / tot:6.2f}%  {r[ci.get('Address', 0)]}  {r[ci.get('Source', 1)][:90]}")
+        order = sorted(range(len(body)), key=lambda k: -float(body[k][ci[key]]))
+        print(f"stall samples: {tot:.0f} ({len(sections)} kernel sections, showing #{which})")
+        for k in order[:int(dict(a.split("=") for a in sys.argv if a.startswith("--top=")).get("--top", 30))]:
+            r = body[k]
+            print(f"{100 * float(r[ci[key]]) / tot:6.2f}%  [{k:5d}] {r[ci['Source']].strip()[:100]}")
 
 
 if __name__ == "__main__":
