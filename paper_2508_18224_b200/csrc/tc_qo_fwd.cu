@@ -5,15 +5,23 @@
 //   mode CMP  : compressed_attention_forward (branches.py:47-78): token t sees
 //               the (t+1) // B_K formed pooled rows, with the importance
 //               scores of selection.py:105-120 as a fused epilogue   (K2)
-// One item = TPI = 128/g consecutive tokens x the g query heads of one kv head
-// (128 MMA rows sharing every key tile).  Per 64-key tile: S = Q K^T (TMEM),
-// softmax warps mask + exponentiate into bf16 P (smem), O += P V accumulates
-// in TMEM across the item's tiles.  The running max is only moved when it
-// grows by more than 2^8 (exp2 units), so O is rescaled (TMEM ld/st) almost
-// never; P <= 256 stays exact enough in bf16 and the fp32 sums cannot overflow.
 //
-// Roles as in tc_sel_fwd.cu: warps 0-3 softmax/epilogue (thread = TMEM lane),
-// 4-7 cp.async loaders, 8 MMA issuer (S of tile u+1 issued ahead of PV of u).
+// Work unit = a *super item*: 2 sub-items of TPI = 128/g consecutive tokens x
+// the g query heads of one kv head (128 MMA rows each).  The two sub-items
+// share one stream of 64-key K/V tiles (the union of their key ranges), so
+// every K/V tile is loaded once for 256 rows.  Softmax warpgroup w owns
+// sub-item w:
+//   S_w = Q_w K^T  (M128 N64 K128) -> TMEM stage v of wg w
+//   softmax: mask, lazy running max (moved only on a > 2^8 increase, so the
+//            O accumulator is rescaled almost never), P = exp2(...) packed
+//            bf16 written back over S in TMEM (tcgen05.st)
+//   O_w += P V     (M128 N128 K64, A operand = P read from TMEM)
+// The MMA thread runs four in-order streams (S_0, S_1, PV_0, PV_1) polled
+// without blocking, so neither warpgroup waits for the other.
+//
+// Roles: warps 0-3 / 4-7 softmax + epilogue of sub-item 0 / 1 (thread = TMEM
+// lane = MMA row), warps 8-10 cp.async loaders, warp 11 the MMA issuer.
+// TMEM: wg w owns columns [256 w, 256 w + 256): S/P stages at +0 / +64, O at +128.
 #include "tc_plan.cuh"
 #include "tc_sched.cuh"
 
@@ -23,16 +31,18 @@ namespace {
 using namespace tc;
 
 constexpr int kD = 128, kRows = 128;
-constexpr int kThreads = 9 * 32;
-constexpr uint32_t kQ = 32768, kKV = 32768, kP = 16384;
+constexpr int kThreads = 12 * 32;  // 2 softmax warpgroups, 3 loader warps, 1 MMA warp
+constexpr int kLoaders = 96;
+constexpr uint32_t kQ = 32768, kKV = 32768;
 constexpr int kKVStages = 3;
-constexpr uint32_t kOffQ = 0, kOffKV = 2 * kQ, kOffP = kOffKV + kKVStages * kKV,
-                   kOffBar = kOffP + 2 * kP;
-enum { B_QF = 0, B_QE = 2, B_KF = 4, B_KE = 7, B_SF = 10, B_SE = 12, B_PF = 14, B_PE = 16,
-       B_OF = 18, B_OE = 20, B_PV = 22, kNumBars = 23 };
+constexpr uint32_t kOffQ = 0;                           // [2 stages][2 subs] x kQ
+constexpr uint32_t kOffKV = 4 * kQ;                     // [3 stages] x (K | V)
+constexpr uint32_t kOffBar = kOffKV + kKVStages * kKV;  // 229376
+enum { B_QF = 0, B_QE = 2, B_KF = 4, B_KE = 7, B_SF = 10, B_PF = 14, B_OF = 18, B_OE = 20,
+       B_PV = 22, kNumBars = 24 };
 constexpr uint32_t kOffTmem = kOffBar + kNumBars * 8;
 constexpr uint32_t kSmemBytes = kOffTmem + 16 + 1024;
-constexpr uint32_t kColS = 0, kColO = 128;  // S[2] 0..127, O[2] 128..383
+static_assert(kSmemBytes <= 232448, "shared memory budget");
 constexpr uint32_t kIdS = idesc_bf16(128, 64, false, false);
 constexpr uint32_t kIdPV = idesc_bf16(128, 128, false, true);
 constexpr float kRescale = 8.f;  // exp2 units
@@ -42,50 +52,72 @@ enum Mode { SLIDE = 0, CMP = 1 };
 struct Params {
   const __nv_bfloat16 *Q, *Kx, *Vx;  // keys/values: K,V [N][h_K][128] or pooled [b][h_K][128]
   float *out, *lse, *scores;
-  int64_t N, h, h_K, g, W, B_K, b, n_keys, n_tiles_tok;
+  int64_t N, h, h_K, g, W, B_K, b, n_keys, n_super;
   int tpi, mode;
   float scale, scale_log2;
 };
 
-struct ItemInfo {
-  int64_t kh, t0, tlast;
-  int64_t k0, k1;  // key tiles [k0, k1)
+struct Sub {
+  int t0, tlast;  // tokens [t0, tlast] (tlast < t0: none)
+  int k0, k1;     // key tiles [k0, k1)
+};
+struct Super {
+  int kh;
+  Sub s[2];
+  int u0, u1;  // union of the key-tile ranges
 };
 
-__device__ __forceinline__ bool item_of(const Params& p, int64_t id, ItemInfo& it) {
-  const int64_t total = p.h_K * p.n_tiles_tok;
-  if (id >= total) return false;
-  it.kh = id % p.h_K;
-  int64_t tile = id / p.h_K;
-  if (p.mode == CMP) tile = p.n_tiles_tok - 1 - tile;  // heavy (late) tokens first
-  it.t0 = tile * p.tpi;
-  it.tlast = min(it.t0 + p.tpi, p.N) - 1;
-  if (p.mode == SLIDE) {
-    const int64_t lo = it.t0 - p.W + 1 > 0 ? it.t0 - p.W + 1 : 0;
-    it.k0 = lo / 64;
-    it.k1 = it.tlast / 64 + 1;
-  } else {
-    const int64_t nf = (it.tlast + 1) / p.B_K;
-    it.k0 = 0;
-    it.k1 = (nf + 63) / 64;
+__device__ __forceinline__ bool super_of(const Params& p, int id, Super& it) {
+  if (id >= p.h_K * p.n_super) return false;
+  it.kh = id % (int)p.h_K;
+  int st = id / (int)p.h_K;
+  if (p.mode == CMP) st = (int)p.n_super - 1 - st;  // heavy (late) tokens first
+  it.u0 = INT32_MAX;
+  it.u1 = 0;
+#pragma unroll
+  for (int w = 0; w < 2; ++w) {
+    Sub& s = it.s[w];
+    s.t0 = (2 * st + w) * p.tpi;
+    s.tlast = min(s.t0 + p.tpi, (int)p.N) - 1;
+    s.k0 = s.k1 = 0;
+    if (s.tlast >= s.t0) {
+      if (p.mode == SLIDE) {
+        s.k0 = (s.t0 - (int)p.W + 1 > 0 ? s.t0 - (int)p.W + 1 : 0) / 64;
+        s.k1 = s.tlast / 64 + 1;
+      } else {
+        s.k1 = ((s.tlast + 1) / (int)p.B_K + 63) / 64;
+      }
+    }
+    if (s.k0 < s.k1) {
+      it.u0 = min(it.u0, s.k0);
+      it.u1 = max(it.u1, s.k1);
+    }
   }
+  if (it.u0 >= it.u1) it.u0 = it.u1 = 0;
   return true;
 }
 
+// Position of one stream in the CTA's sequence of non-empty super items.
+struct Cursor {
+  int n = -1;    // enumeration index
+  int seq = -1;  // index among non-empty super items (Q stage sequence)
+  int rbase = 0, rnext = 0;  // ring index of it.u0 / of the next item's u0
+  Super it;
+  __device__ bool advance(const Params& p, int G) {
+    for (;;) {
+      ++n;
+      if (!super_of(p, (int)blockIdx.x + n * G, it)) return false;
+      if (it.u0 == it.u1) continue;
+      ++seq;
+      rbase = rnext;
+      rnext += it.u1 - it.u0;
+      return true;
+    }
+  }
+};
+
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
-      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
-      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
-      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]),
-      "f"(v[8]), "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]),
-      "f"(v[15]), "f"(v[16]), "f"(v[17]), "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]),
-      "f"(v[22]), "f"(v[23]), "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]),
-      "f"(v[29]), "f"(v[30]), "f"(v[31])
-      : "memory");
-}
-__device__ __forceinline__ void tmem_wait_st() {
-  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  tmem_st32u(taddr, reinterpret_cast<const uint32_t*>(v));
 }
 
 __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const Params p) {
@@ -98,20 +130,20 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const Params p) 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < 2; ++s) {
-      mbar_init(bar(B_QF + s), 128);
-      mbar_init(bar(B_QE + s), 1);
-      mbar_init(bar(B_SF + s), 1);
-      mbar_init(bar(B_SE + s), 128);
-      mbar_init(bar(B_PF + s), 128);
-      mbar_init(bar(B_PE + s), 1);
+      mbar_init(bar(B_QF + s), kLoaders);
+      mbar_init(bar(B_QE + s), 2);  // one commit per S stream
       mbar_init(bar(B_OF + s), 1);
       mbar_init(bar(B_OE + s), 128);
+      mbar_init(bar(B_PV + s), 1);
+    }
+    for (int s = 0; s < 4; ++s) {
+      mbar_init(bar(B_SF + s), 1);
+      mbar_init(bar(B_PF + s), 128);
     }
     for (int s = 0; s < kKVStages; ++s) {
-      mbar_init(bar(B_KF + s), 128);
-      mbar_init(bar(B_KE + s), 1);
+      mbar_init(bar(B_KF + s), kLoaders);
+      mbar_init(bar(B_KE + s), 2);  // one commit per PV stream
     }
-    mbar_init(bar(B_PV), 1);
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc<512>(smem_u32(tmem_slot));
@@ -119,17 +151,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const Params p) 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int64_t G = gridDim.x;
+  const int G = (int)gridDim.x;
 
-  if (warp >= 4 && warp < 8) {
+  if (warp >= 8 && warp < 11) {
     // ------------------------------------------------------------ loaders
-    // Each gather is its own cp.async group; the newest one stays in flight
-    // while the previous one is published (one-group-deep software pipeline).
-    // Blocking waits (Q stage, K/V stage) only depend on work the MMA can
-    // finish without the in-flight group (3 K/V stages, look-ahead of one).
-    const int lr = threadIdx.x - 128;
-    int64_t u = 0, nq = 0;  // tile counter, counter of items with at least one tile
-    uint32_t pend = 0;      // barrier of the in-flight group (0: none)
+    // Each gather is its own cp.async group; the newest stays in flight while
+    // the previous one is published.
+    uint32_t pend = 0;
     auto push_group = [&](uint32_t b) {
       asm volatile("cp.async.commit_group;" ::: "memory");
       asm volatile("cp.async.wait_group 1;" ::: "memory");
@@ -137,141 +165,195 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const Params p) 
       if (pend) mbar_arrive(pend);
       pend = b;
     };
-    ItemInfo it;
-    for (int64_t n = 0; item_of(p, blockIdx.x + n * G, it); ++n) {
-      if (it.k0 == it.k1) continue;
-      const int s = (int)(nq & 1);
-      mbar_wait(bar(B_QE + s), (uint32_t)(((nq >> 1) & 1) ^ 1));
-      ++nq;
-      {
-        const int64_t kt = lr / p.g, hh = lr % p.g, t = it.t0 + kt;
-        const bool ok = kt < p.tpi && t < p.N;
-        const __nv_bfloat16* src = p.Q + ((ok ? t : 0) * p.h + it.kh * p.g + hh) * kD;
-        warp_gather_rows32(sb + kOffQ + s * kQ, 16384u, lr & ~31, src, ok, lane);
+    // a stage wait that would block first publishes the in-flight gather
+    auto wait_stage = [&](uint32_t b, uint32_t par) {
+      if (mbar_try_wait(b, par)) return;
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      fence_proxy_async();
+      if (pend) mbar_arrive(pend);
+      pend = 0;
+      mbar_wait(b, par);
+    };
+    Cursor c;
+    int r = 0;
+    while (c.advance(p, G)) {
+      const int qs = (int)(c.seq & 1);
+      wait_stage(bar(B_QE + qs), (uint32_t)(((c.seq >> 1) & 1) ^ 1));
+      // 8 gathers of 32 rows (2 sub-items x 128 rows) over the 3 loader warps
+      for (int cidx = warp - 8; cidx < 8; cidx += 3) {
+        const Sub& s = c.it.s[cidx >> 2];
+        const int row = (cidx & 3) * 32 + lane;
+        const int kt = row / (int)p.g, hh = row % (int)p.g;
+        const int t = s.t0 + kt;
+        const bool ok = kt < p.tpi && t <= s.tlast;
+        const __nv_bfloat16* src = p.Q + ((int64_t)(ok ? t : 0) * p.h + c.it.kh * p.g + hh) * kD;
+        warp_gather_rows32(sb + kOffQ + (qs * 2 + (cidx >> 2)) * kQ, 16384u, (cidx & 3) * 32, src,
+                           ok, lane);
       }
-      push_group(bar(B_QF + s));
-      for (int64_t kt = it.k0; kt < it.k1; ++kt, ++u) {
-        const int v = (int)(u % kKVStages);
-        mbar_wait(bar(B_KE + v), (uint32_t)(((u / kKVStages) & 1) ^ 1));
-        const int lw = warp - 4, row0 = (lw & 1) * 32;  // warps 4,5: K; 6,7: V
-        const int64_t key = kt * 64 + row0 + lane;
-        const bool ok = key < p.n_keys;
-        const __nv_bfloat16* src = (lw < 2 ? p.Kx : p.Vx) + ((ok ? key : 0) * p.h_K + it.kh) * kD;
-        warp_gather_rows32(sb + kOffKV + v * kKV + (lw < 2 ? 0u : 16384u), 8192u, row0, src, ok,
-                           lane);
+      push_group(bar(B_QF + qs));
+      for (int u = c.it.u0; u < c.it.u1; ++u, ++r) {
+        const int v = (int)(r % kKVStages);
+        wait_stage(bar(B_KE + v), (uint32_t)(((r / kKVStages) & 1) ^ 1));
+        // 4 gathers (K rows 0-31 / 32-63, V rows 0-31 / 32-63) over 3 warps
+        for (int cidx = warp - 8; cidx < 4; cidx += 3) {
+          const int row0 = (cidx & 1) * 32;
+          const int key = u * 64 + row0 + lane;
+          const bool ok = key < p.n_keys;
+          const __nv_bfloat16* src =
+              (cidx < 2 ? p.Kx : p.Vx) + ((int64_t)(ok ? key : 0) * p.h_K + c.it.kh) * kD;
+          warp_gather_rows32(sb + kOffKV + v * kKV + (cidx < 2 ? 0u : 16384u), 8192u, row0, src,
+                             ok, lane);
+        }
         push_group(bar(B_KF + v));
       }
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     fence_proxy_async();
     if (pend) mbar_arrive(pend);
-  } else if (warp == 8) {
+  } else if (warp == 11) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
-      // flat walk over (item, tile) of the items that have tiles; S runs one
-      // tile ahead of PV.  na/nb index items, qa/qb count non-empty items
-      // (the Q and O stage sequence).
-      ItemInfo ia, ib;
-      int64_t na = 0, nb = 0, ka = 0, kb = 0, ua = 0, qa = 0, qb = 0;
-      bool ha = item_of(p, blockIdx.x, ia);
-      while (ha && ia.k0 == ia.k1) ha = item_of(p, blockIdx.x + (++na) * G, ia);
-      bool hb = ha;
-      ib = ia;
-      nb = na;
-      if (ha) ka = ia.k0;
-      if (hb) kb = ib.k0;
-      auto issue_s = [&]() {
-        const int s = (int)(qa & 1), v = (int)(ua & 1), kv = (int)(ua % kKVStages);
-        if (ka == ia.k0) mbar_wait(bar(B_QF + s), (uint32_t)((qa >> 1) & 1));
-        mbar_wait(bar(B_KF + kv), (uint32_t)((ua / kKVStages) & 1));
-        mbar_wait(bar(B_SE + v), (uint32_t)(((ua >> 1) & 1) ^ 1));
-        tc_fence_after();
-        const uint32_t q = sb + kOffQ + s * kQ, k = sb + kOffKV + kv * kKV;
+      // S stream w: for each super item, S tiles [k0_w, k1_w), then one QE
+      // commit.  PV stream w: for each union tile r in [u0, u1): PV if r is in
+      // the sub-item's range, else a pass-by KE commit (KE counts 2 arrivals).
+      Cursor cs[2], cp[2];
+      bool ls[2], lp[2];
+      int su[2], pu[2];      // next tile of each stream (su == k1: QE commit due)
+      int ns[2] = {0, 0};    // S tiles issued (stage / parity sequence)
+      int np[2] = {0, 0};    // PV tiles issued
+      int nsub[2] = {0, 0};  // non-empty sub-items started by the PV stream
+      for (int w = 0; w < 2; ++w) {
+        ls[w] = cs[w].advance(p, G);
+        su[w] = ls[w] ? cs[w].it.s[w].k0 : 0;
+        lp[w] = cp[w].advance(p, G);
+        pu[w] = lp[w] ? cp[w].it.u0 : 0;
+      }
+      long long idle_since = 0;
+      for (;;) {
+        bool progressed = false;
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          mma_bf16(tmem + kColS + v * 64,
-                   desc_kmajor(q + (kk >> 2) * 16384u + (kk & 3) * 32u),
-                   desc_kmajor(k + (kk >> 2) * 8192u + (kk & 3) * 32u), kIdS, kk > 0);
-        mma_commit(bar(B_SF + v));
-        if (ka + 1 == ia.k1) mma_commit(bar(B_QE + s));
-        ++ua;
-        if (++ka == ia.k1) {  // next item with at least one tile
-          ++qa;
-          do {
-            ha = item_of(p, blockIdx.x + (++na) * G, ia);
-          } while (ha && ia.k0 == ia.k1);
-          if (ha) ka = ia.k0;
+        for (int w = 0; w < 2; ++w) {
+          // ---- S stream w
+          if (ls[w]) {
+            const Sub& s = cs[w].it.s[w];
+            const int qs = (int)(cs[w].seq & 1);
+            const uint32_t qpar = (uint32_t)((cs[w].seq >> 1) & 1);
+            if (su[w] < s.k1) {
+              const int rr = cs[w].rbase + (su[w] - cs[w].it.u0);
+              const int kv = (int)(rr % kKVStages), v = (int)(ns[w] & 1);
+              if (ns[w] < np[w] + 2 && mbar_try_wait(bar(B_QF + qs), qpar) &&
+                  mbar_try_wait(bar(B_KF + kv), (uint32_t)((rr / kKVStages) & 1))) {
+                tc_fence_after();
+                const uint32_t q = sb + kOffQ + (qs * 2 + w) * kQ, k = sb + kOffKV + kv * kKV;
+                const uint32_t tS = tmem + 256u * w + 64u * v;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                  mma_bf16(tS, desc_kmajor(q + (kk >> 2) * 16384u + (kk & 3) * 32u),
+                           desc_kmajor(k + (kk >> 2) * 8192u + (kk & 3) * 32u), kIdS, kk > 0);
+                mma_commit(bar(B_SF + 2 * w + v));
+                ++ns[w];
+                ++su[w];
+                progressed = true;
+              }
+            } else if (s.k0 < s.k1 || mbar_try_wait(bar(B_QF + qs), qpar)) {
+              mma_commit(bar(B_QE + qs));  // this stream is done with the Q stage
+              ls[w] = cs[w].advance(p, G);
+              su[w] = ls[w] ? cs[w].it.s[w].k0 : 0;
+              progressed = true;
+            }
+          }
+          // ---- PV stream w
+          if (lp[w]) {
+            const Sub& s = cp[w].it.s[w];
+            const int rr = cp[w].rbase + (pu[w] - cp[w].it.u0);
+            const int kv = (int)(rr % kKVStages);
+            if (pu[w] >= s.k0 && pu[w] < s.k1) {
+              const int v = (int)(np[w] & 1);
+              const bool first = pu[w] == s.k0, last = pu[w] + 1 == s.k1;
+              if (np[w] < ns[w] &&
+                  mbar_try_wait(bar(B_PF + 2 * w + v), (uint32_t)((np[w] >> 1) & 1)) &&
+                  (!first || mbar_try_wait(bar(B_OE + w), (uint32_t)((nsub[w] & 1) ^ 1)))) {
+                tc_fence_after();
+                const uint32_t vv = sb + kOffKV + kv * kKV + 16384u;
+                const uint32_t tS = tmem + 256u * w + 64u * v, tO = tmem + 256u * w + 128u;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+                  mma_bf16_ts(tO, tS + kk * 8, desc_mnmajor(vv + kk * 2048u, 8192u), kIdPV,
+                              (first && kk == 0) ? 0u : 1u);
+                mma_commit(bar(B_KE + kv));
+                mma_commit(bar(B_PV + w));
+                if (last) {
+                  mma_commit(bar(B_OF + w));
+                  ++nsub[w];
+                }
+                ++np[w];
+                ++pu[w];
+                progressed = true;
+              }
+            } else if (mbar_try_wait(bar(B_KF + kv), (uint32_t)((rr / kKVStages) & 1))) {
+              mma_commit(bar(B_KE + kv));  // pass-by: tile not used by this sub-item
+              ++pu[w];
+              progressed = true;
+            }
+            if (pu[w] == cp[w].it.u1) {
+              lp[w] = cp[w].advance(p, G);
+              pu[w] = lp[w] ? cp[w].it.u0 : 0;
+            }
+          }
         }
-      };
-      if (ha) issue_s();
-      for (int64_t u = 0; hb; ++u) {
-        if (ha) issue_s();
-        const int v = (int)(u & 1), so = (int)(qb & 1), kv = (int)(u % kKVStages);
-        const bool first = kb == ib.k0, last = kb + 1 == ib.k1;
-        mbar_wait(bar(B_PF + v), (uint32_t)((u >> 1) & 1));
-        if (first) mbar_wait(bar(B_OE + so), (uint32_t)(((qb >> 1) & 1) ^ 1));
-        tc_fence_after();
-        const uint32_t pp = sb + kOffP + v * kP, vv = sb + kOffKV + kv * kKV + 16384u;
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          mma_bf16(tmem + kColO + so * 128, desc_kmajor(pp + kk * 32u),
-                   desc_mnmajor(vv + kk * 2048u, 8192u), kIdPV, (first && kk == 0) ? 0u : 1u);
-        mma_commit(bar(B_PE + v));
-        mma_commit(bar(B_KE + kv));
-        mma_commit(bar(B_PV));
-        if (last) mma_commit(bar(B_OF + so));
-        if (++kb == ib.k1) {
-          ++qb;
-          do {
-            hb = item_of(p, blockIdx.x + (++nb) * G, ib);
-          } while (hb && ib.k0 == ib.k1);
-          if (hb) kb = ib.k0;
+        if (!ls[0] && !ls[1] && !lp[0] && !lp[1]) break;
+        if (progressed) {
+          idle_since = 0;
+        } else if (idle_since == 0) {
+          idle_since = clock64();
+        } else if (clock64() - idle_since > (1ll << 34)) {
+          mbar_stuck(bar(B_SF), 0);
         }
       }
     }
   } else {
     // ------------------------------------------------------------ softmax / epilogue
-    const int r = threadIdx.x;
-    const uint32_t lb = (uint32_t)(warp * 32) << 16;
-    const int64_t kt_row = r / p.g, hh = r % p.g;
-    int64_t u = 0, n_out = 0;
-    ItemInfo it;
-    for (int64_t n = 0; item_of(p, blockIdx.x + n * G, it); ++n) {
-      if (it.k0 == it.k1) continue;  // only pending tokens: handled by the SIMT kernel
-      const int64_t t = it.t0 + kt_row;
-      const bool ok = kt_row < p.tpi && t < p.N;
-      const int64_t j = it.kh * p.g + hh;
-      // visible key range [klo, khi]
-      int64_t klo, khi;
+    const int w = warp >> 2;
+    const int r = threadIdx.x & 127;
+    const uint32_t lb = ((uint32_t)((warp & 3) * 32) << 16) + 256u * w;
+    const int kt_row = r / (int)p.g, hh = r % (int)p.g;
+    int u = 0, n_out = 0;  // tiles processed / sub-items finished by this wg
+    Cursor c;
+    while (c.advance(p, G)) {
+      const Sub& s = c.it.s[w];
+      if (s.k0 >= s.k1) continue;
+      const int t = s.t0 + kt_row;
+      const bool ok = kt_row < p.tpi && t <= s.tlast;
+      const int64_t j = (int64_t)c.it.kh * p.g + hh;
+      int klo, khi;  // visible keys [klo, khi]
       if (p.mode == SLIDE) {
-        klo = t - p.W + 1 > 0 ? t - p.W + 1 : 0;
+        klo = t - (int)p.W + 1 > 0 ? t - (int)p.W + 1 : 0;
         khi = t;
       } else {
         klo = 0;
-        khi = (t + 1) / p.B_K - 1;
+        khi = (t + 1) / (int)p.B_K - 1;
       }
       if (!ok) khi = -1;
       float m_used = -INFINITY, l = 0.f;
-      for (int64_t kt = it.k0; kt < it.k1; ++kt, ++u) {
+      for (int kt = s.k0; kt < s.k1; ++kt, ++u) {
         const int v = (int)(u & 1);
-        mbar_wait(bar(B_SF + v), (uint32_t)((u >> 1) & 1));
+        const uint32_t tS = tmem + lb + 64u * v;
+        mbar_wait(bar(B_SF + 2 * w + v), (uint32_t)((u >> 1) & 1));
         tc_fence_after();
         float sv[64];
-        tmem_ld32(tmem + lb + kColS + v * 64, sv);
-        tmem_ld32(tmem + lb + kColS + v * 64 + 32, sv + 32);
+        tmem_ld32(tS, sv);
+        tmem_ld32(tS + 32, sv + 32);
         tmem_wait_ld();
-        tc_fence_before();
-        mbar_arrive(bar(B_SE + v));
-        const int64_t kbase = kt * 64;
+        const int kbase = kt * 64;
         if (p.mode == CMP && p.scores != nullptr) {
           // group mean over the g heads of this token (rows of a token are
           // adjacent lanes; g divides 32), written by the token's first row
           const float gm = p.scale / (float)p.g;
-          float* dst = p.scores + (it.kh * p.N + t) * p.b + kbase;
+          float* dst = p.scores + ((int64_t)c.it.kh * p.N + t) * p.b + kbase;
           const bool wr = ok && hh == 0;
 #pragma unroll
-          for (int c = 0; c < 64; c += 4) {
-            float x0 = sv[c], x1 = sv[c + 1], x2 = sv[c + 2], x3 = sv[c + 3];
+          for (int cc = 0; cc < 64; cc += 4) {
+            float x0 = sv[cc], x1 = sv[cc + 1], x2 = sv[cc + 2], x3 = sv[cc + 3];
             for (int o = 1; o < p.g; o <<= 1) {
               x0 += __shfl_xor_sync(0xffffffffu, x0, o);
               x1 += __shfl_xor_sync(0xffffffffu, x1, o);
@@ -279,24 +361,30 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const Params p) 
               x3 += __shfl_xor_sync(0xffffffffu, x3, o);
             }
             if (wr) {
-              if (kbase + c + 3 < p.b) {
-                *reinterpret_cast<float4*>(dst + c) = make_float4(x0 * gm, x1 * gm, x2 * gm, x3 * gm);
+              if (kbase + cc + 3 < p.b) {
+                *reinterpret_cast<float4*>(dst + cc) = make_float4(x0 * gm, x1 * gm, x2 * gm, x3 * gm);
               } else {
-                if (kbase + c < p.b) dst[c] = x0 * gm;
-                if (kbase + c + 1 < p.b) dst[c + 1] = x1 * gm;
-                if (kbase + c + 2 < p.b) dst[c + 2] = x2 * gm;
+                if (kbase + cc < p.b) dst[cc] = x0 * gm;
+                if (kbase + cc + 1 < p.b) dst[cc + 1] = x1 * gm;
+                if (kbase + cc + 2 < p.b) dst[cc + 2] = x2 * gm;
               }
             }
           }
         }
+        // rows whose visible range covers the whole tile skip the masking
+        const bool full = __all_sync(0xffffffffu, klo <= kbase && kbase + 63 <= khi);
         float mx = -INFINITY;
+        if (full) {
 #pragma unroll
-        for (int c = 0; c < 64; ++c) {
-          const int64_t key = kbase + c;
-          if (key >= klo && key <= khi) mx = fmaxf(mx, sv[c]);
+          for (int cc = 0; cc < 64; ++cc) mx = fmaxf(mx, sv[cc]);
+        } else {
+#pragma unroll
+          for (int cc = 0; cc < 64; ++cc) {
+            const bool vis = kbase + cc >= klo && kbase + cc <= khi;
+            sv[cc] = vis ? sv[cc] : -INFINITY;
+            mx = fmaxf(mx, sv[cc]);
+          }
         }
-        // P(u-2) consumed => PV(u-2) done, so the PV barrier parity below is unambiguous
-        mbar_wait(bar(B_PE + v), (uint32_t)(((u >> 1) & 1) ^ 1));
         // move the reference max only on a large increase (or the first finite max)
         float f = 1.f;
         bool resc = false;
@@ -308,61 +396,58 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const Params p) 
           }
           m_used = mx;
         }
-        // rescale the O accumulator in TMEM (warp-collective: every lane joins,
-        // lanes without a new max scale by 1) once PV(u-1) has landed
+        // rescale O in TMEM once PV(u-1) has landed (warp-collective)
         if (__any_sync(0xffffffffu, resc)) {
-          mbar_wait(bar(B_PV), (uint32_t)((u - 1) & 1));
+          mbar_wait(bar(B_PV + w), (uint32_t)((u - 1) & 1));
           tc_fence_after();
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             float ov[32];
-            tmem_ld32(tmem + lb + kColO + (n_out & 1) * 128 + q * 32, ov);
+            tmem_ld32(tmem + lb + 128u + q * 32, ov);
             tmem_wait_ld();
 #pragma unroll
-            for (int c = 0; c < 32; ++c) ov[c] *= f;
-            tmem_st32(tmem + lb + kColO + (n_out & 1) * 128 + q * 32, ov);
+            for (int cc = 0; cc < 32; ++cc) ov[cc] *= f;
+            tmem_st32(tmem + lb + 128u + q * 32, ov);
           }
-          tmem_wait_st();
-          tc_fence_before();
+          tmem_wait_st_();
         }
         const float mb = m_used == -INFINITY ? 0.f : m_used * p.scale_log2;
         uint32_t pk[32];
+        float l0 = 0.f, l1 = 0.f;
 #pragma unroll
-        for (int c = 0; c < 64; c += 2) {
-          const int64_t key = kbase + c;
-          const float e0 = (key >= klo && key <= khi) ? ex2(fmaf(sv[c], p.scale_log2, -mb)) : 0.f;
-          const float e1 = (key + 1 >= klo && key + 1 <= khi) ? ex2(fmaf(sv[c + 1], p.scale_log2, -mb)) : 0.f;
-          l += e0 + e1;
-          pk[c >> 1] = pack_bf16(e0, e1);
+        for (int cc = 0; cc < 64; cc += 2) {
+          const float e0 = ex2(fmaf(sv[cc], p.scale_log2, -mb));  // -inf -> 0
+          const float e1 = ex2(fmaf(sv[cc + 1], p.scale_log2, -mb));
+          l0 += e0;
+          l1 += e1;
+          pk[cc >> 1] = pack_bf16(e0, e1);
         }
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-          *reinterpret_cast<uint4*>(smem + kOffP + v * kP + sw128_off(r, c)) =
-              make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-        fence_proxy_async();
-        mbar_arrive(bar(B_PF + v));
+        l += l0 + l1;
+        tmem_st32u(tS, pk);  // P over S: bf16 pairs, K-packed
+        tmem_wait_st_();
+        tc_fence_before();
+        mbar_arrive(bar(B_PF + 2 * w + v));
       }
       // epilogue: out = O / l, lse = m + ln l
-      const int so = (int)(n_out & 1);
-      mbar_wait(bar(B_OF + so), (uint32_t)((n_out >> 1) & 1));
+      mbar_wait(bar(B_OF + w), (uint32_t)(n_out & 1));
       tc_fence_after();
       const bool write = ok && l > 0.f;
       const float inv = write ? 1.f / l : 0.f;
-      float* orow = p.out + (t * p.h + j) * kD;
+      float* orow = p.out + ((int64_t)t * p.h + j) * kD;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         float ov[32];
-        tmem_ld32(tmem + lb + kColO + so * 128 + q * 32, ov);
+        tmem_ld32(tmem + lb + 128u + q * 32, ov);
         tmem_wait_ld();
         if (write) {
 #pragma unroll
-          for (int c = 0; c < 32; c += 4)
-            *reinterpret_cast<float4*>(orow + q * 32 + c) =
-                make_float4(ov[c] * inv, ov[c + 1] * inv, ov[c + 2] * inv, ov[c + 3] * inv);
+          for (int cc = 0; cc < 32; cc += 4)
+            *reinterpret_cast<float4*>(orow + q * 32 + cc) =
+                make_float4(ov[cc] * inv, ov[cc + 1] * inv, ov[cc + 2] * inv, ov[cc + 3] * inv);
         }
       }
       tc_fence_before();
-      mbar_arrive(bar(B_OE + so));
+      mbar_arrive(bar(B_OE + w));
       if (write) p.lse[j * p.N + t] = m_used * p.scale + __logf(l);
       ++n_out;
     }
@@ -389,7 +474,7 @@ int launch(const Params& p, cudaStream_t st) {
                          (int)kSmemBytes);
     attr = true;
   }
-  int64_t items = p.h_K * p.n_tiles_tok;
+  int64_t items = p.h_K * p.n_super;
   int grid = num_sms();
   if (items < grid) grid = (int)items;
   if (grid < 1) return FSA_OK;
@@ -407,7 +492,7 @@ Params base_params(const fsa_shape* s) {
   p.B_K = s->B_K;
   p.b = s->N / s->B_K;
   p.tpi = (int)(kRows / p.g);
-  p.n_tiles_tok = (p.N + p.tpi - 1) / p.tpi;
+  p.n_super = (p.N + 2 * p.tpi - 1) / (2 * p.tpi);
   p.scale = (float)s->scale;
   p.scale_log2 = (float)(s->scale * 1.4426950408889634);
   return p;
@@ -417,7 +502,7 @@ Params base_params(const fsa_shape* s) {
 
 bool tc_qo_supported(const fsa_shape& s, int dtype) {
   return dtype == FSA_DT_BF16 && s.d_K == kD && s.d_V == kD && s.h_K > 0 && s.h % s.h_K == 0 &&
-         s.h / s.h_K <= kRows;
+         s.h / s.h_K <= kRows && s.N < (1ll << 30);
 }
 bool tc_cmp_scores_fused(const fsa_shape& s) {
   const int64_t g = s.h / s.h_K;
