@@ -15,7 +15,7 @@ namespace {
 constexpr int kD = 128;
 
 __device__ __forceinline__ float4 ld_bf16x4(const __nv_bfloat16* p) {
-  const uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
+  const uint2 u = __ldcs(reinterpret_cast<const uint2*>(p));  // read once: evict first
   const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
   const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
   return make_float4(a.x, a.y, b.x, b.y);

@@ -31,6 +31,10 @@ int tc_slide_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V
                  const void* dOut, const void* lse, const void* delta, void* dQ, void* dK,
                  void* dV, void* workspace, int accumulate, cudaStream_t st);
 
+// query-outer sliding-window dQ (tc_slide_dq.cu); accumulate: dQ += (fp32)
+int tc_slide_dq(const fsa_shape* s, const void* Q, const void* K, const void* V, const void* dOut,
+                const void* lse, const void* delta, void* dQ, int accumulate, cudaStream_t st);
+
 // vectorised bf16 merge / dQ reduce for d = 128, T <= 32 (merge_fast.cu)
 bool fast_reduce_ok(const fsa_shape& s);
 int merge_bf16_fast(const fsa_shape* s, const int32_t* idx, const void* obuf, const void* ml,

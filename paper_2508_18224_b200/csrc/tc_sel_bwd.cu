@@ -69,6 +69,7 @@ struct Params {
   int64_t N, h, h_K, T, b, g, ntask;
   int64_t W;   // sliding mode: window; T is then the number of window slots
   int tpi, slide, accumulate;  // accumulate: dK/dV += (sliding branch onto the selected one)
+  int no_dq;                   // sliding mode: dQ comes from the query-outer kernel (tc_slide_dq.cu)
   FastDiv fdT;
   float scale, scale_log2;
 };
@@ -287,10 +288,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
             for (int k = 0; k < 8; ++k)
               mma_bf16(tK, desc_mnmajor(q + k * 2048u, 16384u), desc_mnmajor(ds + k * 2048u, 8192u),
                        kIdKV, (first && k == 0) ? 0u : 1u);
+            if (!p.no_dq) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              mma_bf16(tmem + 128u * s, desc_kmajor(ds + k * 32u),
-                       desc_mnmajor(sb + kOffK + k * 2048u, 8192u), kIdQ, k > 0);
+              for (int k = 0; k < 4; ++k)
+                mma_bf16(tmem + 128u * s, desc_kmajor(ds + k * 32u),
+                         desc_mnmajor(sb + kOffK + k * 2048u, 8192u), kIdQ, k > 0);
+            }
             mma_commit(bar(B_DQF + s));
             mma_commit(bar(B_QDE + s));
             if (last) {
@@ -423,12 +426,20 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
                 make_uint4(dd[4 * c4], dd[4 * c4 + 1], dd[4 * c4 + 2], dd[4 * c4 + 3]);
           }
         }
+        if (p.no_dq) {  // S/dP consumed: the TMEM stage is free right away
+          tc_fence_before();
+          mbar_arrive(bar(B_SDE + s));
+        }
         fence_proxy_async();
         mbar_arrive(bar(B_PDF + s));
         // products of this item landed -> dQ partial out of TMEM; stage the
         // bf16 rows in this wg's (now consumed) P buffer for coalesced stores
         mbar_wait(bar(B_DQF + s), (uint32_t)((n >> 1) & 1));
         tc_fence_after();
+        if (p.no_dq) {
+          if (c + 1 == tr.nitems) kv_epilogue(tr, kseq);
+          continue;
+        }
         unsigned char* st = prow + (warp & 3) * 32 * kStStride;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -453,7 +464,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
             const int rr = it * 8 + (lane >> 2), ch = lane & 3;
             const int64_t d = __shfl_sync(0xffffffffu, drow, rr);
             const uint4 u = *reinterpret_cast<const uint4*>(st + rr * kStStride + ch * 16);
-            if (d >= 0) *reinterpret_cast<uint4*>(p.dq + d * kD + q * 32 + ch * 8) = u;
+            if (d >= 0) __stcs(reinterpret_cast<uint4*>(p.dq + d * kD + q * 32 + ch * 8), u);  // streaming: keep Q/dO in L2
           }
           __syncwarp();
         }
@@ -516,29 +527,6 @@ int launch_bwd(Params& p, cudaStream_t st) {
   return FSA_OK;
 }
 
-// sliding-window dQ: ascending-block sum of the window-slot partials
-__global__ void slide_dq_reduce_kernel(const __nv_bfloat16* __restrict__ dq, float* __restrict__ dQ,
-                                       int64_t N, int64_t h, int64_t W, int64_t S, int accumulate) {
-  const int lane = threadIdx.x & 31;
-  const int64_t wid = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (wid >= h * N) return;
-  const int64_t j = wid / N, t = wid % N;
-  const int64_t first = (t - W + 1 > 0 ? t - W + 1 : 0) / kBK, own = t / kBK;
-  const __nv_bfloat16* src = dq + ((j * N + t) * S) * kD + lane * 4;
-  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-  for (int64_t k = 0; k <= own - first; ++k) {
-    const uint2 u = *reinterpret_cast<const uint2*>(src + k * kD);
-    const float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
-    const float2 y = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
-    a0 += x.x; a1 += x.y; a2 += y.x; a3 += y.y;
-  }
-  float4* o = reinterpret_cast<float4*>(dQ + (t * h + j) * kD + lane * 4);
-  if (accumulate) {
-    const float4 c = *o;
-    a0 += c.x; a1 += c.y; a2 += c.z; a3 += c.w;
-  }
-  *o = make_float4(a0, a1, a2, a3);
-}
 }  // namespace
 
 int tc_sel_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V, const void* dOut,
@@ -554,32 +542,25 @@ int tc_sel_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V, 
   return launch_bwd(p, st);
 }
 
-int64_t tc_slide_slots(const fsa_shape* s) { return (s->W - 1) / kBK + 2; }
+size_t tc_slide_bwd_workspace_bytes(const fsa_shape* s) { return 256; }  // scheduler counter
 
-size_t tc_slide_bwd_workspace_bytes(const fsa_shape* s) {
-  return (size_t)s->h * s->N * tc_slide_slots(s) * kD * sizeof(__nv_bfloat16) + 256;
-}
-
+// K11: dK/dV on the KV-block-outer FSA backward kernel over each block's
+// window of tokens (no dQ there), then dQ query-outer (tc_slide_dq.cu).
 int tc_slide_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V,
                  const void* dOut, const void* lse, const void* delta, void* dQ, void* dK,
                  void* dV, void* workspace, int accumulate, cudaStream_t st) {
-  const int64_t S = tc_slide_slots(s);
-  __nv_bfloat16* dq = (__nv_bfloat16*)workspace;
-  int32_t* counter = (int32_t*)((char*)workspace + (size_t)s->h * s->N * S * kD * 2);
-  Params p = make_params(s, Q, K, V, dOut, lse, delta, dq, dK, dV);
+  const int64_t S = (s->W - 1) / kBK + 2;  // window slots of a token (for the row bookkeeping)
+  Params p = make_params(s, Q, K, V, dOut, lse, delta, nullptr, dK, dV);
   p.slide = 1;
+  p.no_dq = 1;
   p.accumulate = accumulate;
   p.W = s->W;
   p.T = S;
   p.fdT.init((uint32_t)S);
-  p.counter = counter;
+  p.counter = (int32_t*)workspace;
   int rc = launch_bwd(p, st);
   if (rc) return rc;
-  const int64_t rows = s->h * s->N;
-  slide_dq_reduce_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(dq, (float*)dQ, s->N, s->h,
-                                                                     s->W, S, accumulate);
-  FSA_LAUNCH_CHECK("tc_slide_bwd");
-  return FSA_OK;
+  return tc_slide_dq(s, Q, K, V, dOut, lse, delta, dQ, accumulate, st);
 }
 
 }  // namespace fsa

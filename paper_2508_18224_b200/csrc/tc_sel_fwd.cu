@@ -290,11 +290,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const Params p)
           const int rr = it * 8 + (lane >> 2), ch = lane & 3;
           const int64_t drow = __shfl_sync(0xffffffffu, prow, rr);
           const uint4 v4 = *reinterpret_cast<const uint4*>(st + rr * kStStride + ch * 16);
-          if (drow >= 0) *reinterpret_cast<uint4*>(p.obuf + drow * kD + q * 32 + ch * 8) = v4;
+          if (drow >= 0) __stcs(reinterpret_cast<uint4*>(p.obuf + drow * kD + q * 32 + ch * 8), v4);  // streaming: keep Q in L2
         }
         __syncwarp();
       }
-      if (prow >= 0) *reinterpret_cast<float2*>(p.ml + 2 * prow) = make_float2(pm, pl);
+      if (prow >= 0) __stcs(reinterpret_cast<float2*>(p.ml + 2 * prow), make_float2(pm, pl));
     };
     for (int k = 0;; ++k) {
       const int32_t task = ring.consume(k);

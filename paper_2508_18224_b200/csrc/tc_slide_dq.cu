@@ -1,0 +1,405 @@
+// Sliding-window dQ on tcgen05 tensor cores (part of K11), bf16, d = 128.
+// The band-mask dense_backward of oracle.py:102-131 restricted to dQ:
+//   P  = exp(S scale - lse),  dS = P * (dO V^T - delta),  dQ = scale * dS K
+// computed query-outer, so every dQ row is produced by exactly one CTA and
+// accumulated in TMEM over its window's key tiles: no per-slot partials, no
+// reduction pass, deterministic.  (dK / dV come from the KV-block-outer FSA
+// backward kernel in its sliding mode, tc_sel_bwd.cu, without its dQ.)
+//
+// Structure as the window forward (tc_qo_fwd.cu): a super item = 2 sub-items
+// of TPI = 128/g tokens x g heads of one kv head sharing one stream of 64-key
+// K/V tiles; softmax warpgroup w owns sub-item w.  Per tile:
+//   S_w = Q_w K^T, dP_w = dO_w V^T      (2 x M128 N64 K128) -> TMEM of wg w
+//   softmax: dS (bf16) written back over S in TMEM
+//   dQ_w += dS K                        (M128 N128 K64, A = dS from TMEM)
+// TMEM per wg (256 columns at 256 w): S +0, dP +64, dQ accumulator +128.
+// Roles: warps 0-3 / 4-7 softmax + epilogue, 8-10 loaders, 11 MMA issuer.
+#include "tc_plan.cuh"
+#include "tc_sched.cuh"
+
+namespace fsa {
+namespace {
+
+using namespace tc;
+
+constexpr int kD = 128, kRows = 128;
+constexpr int kThreads = 12 * 32;
+constexpr int kLoaders = 96;
+constexpr uint32_t kT = 32768;                          // one 128-row tile [2 halves][128][128 B]
+constexpr uint32_t kKV = 32768;                         // K | V tile of 64 keys
+constexpr int kKVStages = 3;
+constexpr uint32_t kOffQ = 0;                           // Q sub 0, Q sub 1, dO sub 0, dO sub 1
+constexpr uint32_t kOffKV = 4 * kT;
+constexpr uint32_t kOffBar = kOffKV + kKVStages * kKV;
+enum { B_QF = 0, B_QE = 1, B_KF = 2, B_KE = 5, B_SF = 8, B_PF = 10, B_OF = 12, B_OE = 14,
+       kNumBars = 16 };
+constexpr uint32_t kOffTmem = kOffBar + kNumBars * 8;
+constexpr uint32_t kSmemBytes = kOffTmem + 16 + 1024;
+static_assert(kSmemBytes <= 232448, "shared memory budget");
+constexpr uint32_t kIdS = idesc_bf16(128, 64, false, false);
+constexpr uint32_t kIdQ = idesc_bf16(128, 128, false, true);
+
+struct Params {
+  const __nv_bfloat16 *Q, *K, *V, *dO;
+  const float *lse, *delta;
+  float* dQ;  // [N][h][128]
+  int64_t N, h, h_K, g, W, n_super;
+  int tpi, accumulate;
+  float scale, scale_log2;
+};
+
+struct Sub {
+  int t0, tlast;  // tokens [t0, tlast]
+  int k0, k1;     // key tiles [k0, k1)
+};
+struct Super {
+  int kh;
+  Sub s[2];
+  int u0, u1;
+};
+
+__device__ __forceinline__ bool super_of(const Params& p, int id, Super& it) {
+  if (id >= p.h_K * p.n_super) return false;
+  it.kh = id % (int)p.h_K;
+  const int st = id / (int)p.h_K;
+  it.u0 = INT32_MAX;
+  it.u1 = 0;
+#pragma unroll
+  for (int w = 0; w < 2; ++w) {
+    Sub& s = it.s[w];
+    s.t0 = (2 * st + w) * p.tpi;
+    s.tlast = min(s.t0 + p.tpi, (int)p.N) - 1;
+    s.k0 = s.k1 = 0;
+    if (s.tlast >= s.t0) {
+      s.k0 = (s.t0 - (int)p.W + 1 > 0 ? s.t0 - (int)p.W + 1 : 0) / 64;
+      s.k1 = s.tlast / 64 + 1;
+      it.u0 = min(it.u0, s.k0);
+      it.u1 = max(it.u1, s.k1);
+    }
+  }
+  if (it.u0 >= it.u1) it.u0 = it.u1 = 0;
+  return true;
+}
+
+struct Cursor {
+  int n = -1, seq = -1, rbase = 0, rnext = 0;
+  Super it;
+  __device__ bool advance(const Params& p, int G) {
+    for (;;) {
+      ++n;
+      if (!super_of(p, (int)blockIdx.x + n * G, it)) return false;
+      if (it.u0 == it.u1) continue;
+      ++seq;
+      rbase = rnext;
+      rnext += it.u1 - it.u0;
+      return true;
+    }
+  }
+};
+
+__global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const Params p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sb = smem_u32(smem);
+  auto bar = [&](int k) { return sb + kOffBar + 8u * (uint32_t)k; };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffTmem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    mbar_init(bar(B_QF), kLoaders);
+    mbar_init(bar(B_QE), 2);
+    for (int w = 0; w < 2; ++w) {
+      mbar_init(bar(B_SF + w), 1);
+      mbar_init(bar(B_PF + w), 128);
+      mbar_init(bar(B_OF + w), 1);
+      mbar_init(bar(B_OE + w), 128);
+    }
+    for (int s = 0; s < kKVStages; ++s) {
+      mbar_init(bar(B_KF + s), kLoaders);
+      mbar_init(bar(B_KE + s), 2);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc<512>(smem_u32(tmem_slot));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int G = (int)gridDim.x;
+
+  if (warp >= 8 && warp < 11) {
+    // ------------------------------------------------------------ loaders
+    uint32_t pend = 0;
+    auto push_group = [&](uint32_t b) {
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+      fence_proxy_async();
+      if (pend) mbar_arrive(pend);
+      pend = b;
+    };
+    auto wait_stage = [&](uint32_t b, uint32_t par) {
+      if (mbar_try_wait(b, par)) return;
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      fence_proxy_async();
+      if (pend) mbar_arrive(pend);
+      pend = 0;
+      mbar_wait(b, par);
+    };
+    Cursor c;
+    int r = 0;
+    while (c.advance(p, G)) {
+      wait_stage(bar(B_QE), (uint32_t)((c.seq & 1) ^ 1));
+      // 16 gathers of 32 rows: {Q, dO} x 2 sub-items x 128 rows, over 3 warps
+      for (int cidx = warp - 8; cidx < 16; cidx += 3) {
+        const int op = cidx >> 3, w = (cidx >> 2) & 1;
+        const Sub& s = c.it.s[w];
+        const int row = (cidx & 3) * 32 + lane;
+        const int kt = row / (int)p.g, hh = row % (int)p.g;
+        const int t = s.t0 + kt;
+        const bool ok = kt < p.tpi && t <= s.tlast;
+        const __nv_bfloat16* src =
+            (op ? p.dO : p.Q) + ((int64_t)(ok ? t : 0) * p.h + c.it.kh * p.g + hh) * kD;
+        warp_gather_rows32(sb + kOffQ + (op * 2 + w) * kT, 16384u, (cidx & 3) * 32, src, ok, lane);
+      }
+      push_group(bar(B_QF));
+      for (int u = c.it.u0; u < c.it.u1; ++u, ++r) {
+        const int v = r % kKVStages;
+        wait_stage(bar(B_KE + v), (uint32_t)(((r / kKVStages) & 1) ^ 1));
+        for (int cidx = warp - 8; cidx < 4; cidx += 3) {
+          const int row0 = (cidx & 1) * 32;
+          const int key = u * 64 + row0 + lane;
+          const bool ok = key < p.N;
+          const __nv_bfloat16* src =
+              (cidx < 2 ? p.K : p.V) + ((int64_t)(ok ? key : 0) * p.h_K + c.it.kh) * kD;
+          warp_gather_rows32(sb + kOffKV + v * kKV + (cidx < 2 ? 0u : 16384u), 8192u, row0, src,
+                             ok, lane);
+        }
+        push_group(bar(B_KF + v));
+      }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    fence_proxy_async();
+    if (pend) mbar_arrive(pend);
+  } else if (warp == 11) {
+    // ------------------------------------------------------------ MMA issuer
+    // S stream w: S/dP of each tile of sub-item w (single TMEM stage: the next
+    // S/dP only after this wg's previous dQ product was issued), then a QE
+    // commit.  D stream w: per union tile, dQ += dS K or a pass-by KE commit.
+    if (lane == 0) {
+      Cursor cs[2], cd[2];
+      bool ls[2], ld[2];
+      int su[2], du[2];
+      int ns[2] = {0, 0}, nd[2] = {0, 0}, nsub[2] = {0, 0};
+      for (int w = 0; w < 2; ++w) {
+        ls[w] = cs[w].advance(p, G);
+        su[w] = ls[w] ? cs[w].it.s[w].k0 : 0;
+        ld[w] = cd[w].advance(p, G);
+        du[w] = ld[w] ? cd[w].it.u0 : 0;
+      }
+      long long idle_since = 0;
+      for (;;) {
+        bool progressed = false;
+#pragma unroll
+        for (int w = 0; w < 2; ++w) {
+          if (ls[w]) {
+            const Sub& s = cs[w].it.s[w];
+            const uint32_t qpar = (uint32_t)(cs[w].seq & 1);
+            if (su[w] < s.k1) {
+              const int rr = cs[w].rbase + (su[w] - cs[w].it.u0);
+              const int kv = rr % kKVStages;
+              if (ns[w] == nd[w] && mbar_try_wait(bar(B_QF), qpar) &&
+                  mbar_try_wait(bar(B_KF + kv), (uint32_t)((rr / kKVStages) & 1))) {
+                tc_fence_after();
+                const uint32_t q = sb + kOffQ + w * kT, o = sb + kOffQ + (2 + w) * kT;
+                const uint32_t k = sb + kOffKV + kv * kKV, vv = k + 16384u;
+                const uint32_t tS = tmem + 256u * w;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                  mma_bf16(tS, desc_kmajor(q + (kk >> 2) * 16384u + (kk & 3) * 32u),
+                           desc_kmajor(k + (kk >> 2) * 8192u + (kk & 3) * 32u), kIdS, kk > 0);
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                  mma_bf16(tS + 64, desc_kmajor(o + (kk >> 2) * 16384u + (kk & 3) * 32u),
+                           desc_kmajor(vv + (kk >> 2) * 8192u + (kk & 3) * 32u), kIdS, kk > 0);
+                mma_commit(bar(B_SF + w));
+                ++ns[w];
+                ++su[w];
+                progressed = true;
+              }
+            } else if (s.k0 < s.k1 || mbar_try_wait(bar(B_QF), qpar)) {
+              mma_commit(bar(B_QE));
+              ls[w] = cs[w].advance(p, G);
+              su[w] = ls[w] ? cs[w].it.s[w].k0 : 0;
+              progressed = true;
+            }
+          }
+          if (ld[w]) {
+            const Sub& s = cd[w].it.s[w];
+            const int rr = cd[w].rbase + (du[w] - cd[w].it.u0);
+            const int kv = rr % kKVStages;
+            if (du[w] >= s.k0 && du[w] < s.k1) {
+              const bool first = du[w] == s.k0, last = du[w] + 1 == s.k1;
+              if (nd[w] < ns[w] && mbar_try_wait(bar(B_PF + w), (uint32_t)(nd[w] & 1)) &&
+                  (!first || mbar_try_wait(bar(B_OE + w), (uint32_t)((nsub[w] & 1) ^ 1)))) {
+                tc_fence_after();
+                const uint32_t k = sb + kOffKV + kv * kKV;
+                const uint32_t tS = tmem + 256u * w, tQ = tmem + 256u * w + 128u;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+                  mma_bf16_ts(tQ, tS + kk * 8, desc_mnmajor(k + kk * 2048u, 8192u), kIdQ,
+                              (first && kk == 0) ? 0u : 1u);
+                mma_commit(bar(B_KE + kv));
+                if (last) {
+                  mma_commit(bar(B_OF + w));
+                  ++nsub[w];
+                }
+                ++nd[w];
+                ++du[w];
+                progressed = true;
+              }
+            } else if (mbar_try_wait(bar(B_KF + kv), (uint32_t)((rr / kKVStages) & 1))) {
+              mma_commit(bar(B_KE + kv));
+              ++du[w];
+              progressed = true;
+            }
+            if (du[w] == cd[w].it.u1) {
+              ld[w] = cd[w].advance(p, G);
+              du[w] = ld[w] ? cd[w].it.u0 : 0;
+            }
+          }
+        }
+        if (!ls[0] && !ls[1] && !ld[0] && !ld[1]) break;
+        if (progressed) {
+          idle_since = 0;
+        } else if (idle_since == 0) {
+          idle_since = clock64();
+        } else if (clock64() - idle_since > (1ll << 34)) {
+          mbar_stuck(bar(B_SF), 0);
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ softmax / epilogue
+    const int w = warp >> 2;
+    const int r = threadIdx.x & 127;
+    const uint32_t lb = ((uint32_t)((warp & 3) * 32) << 16) + 256u * w;
+    const int kt_row = r / (int)p.g, hh = r % (int)p.g;
+    int u = 0, n_out = 0;
+    Cursor c;
+    while (c.advance(p, G)) {
+      const Sub& s = c.it.s[w];
+      if (s.k0 >= s.k1) continue;
+      const int t = s.t0 + kt_row;
+      const bool ok = kt_row < p.tpi && t <= s.tlast;
+      const int64_t j = (int64_t)c.it.kh * p.g + hh;
+      const int klo = t - (int)p.W + 1 > 0 ? t - (int)p.W + 1 : 0;
+      const int khi = ok ? t : -1;
+      const float lse_r = ok ? p.lse[j * p.N + t] * 1.4426950408889634f : 0.f;
+      const float dl = ok ? p.delta[j * p.N + t] : 0.f;
+      for (int kt = s.k0; kt < s.k1; ++kt, ++u) {
+        mbar_wait(bar(B_SF + w), (uint32_t)(u & 1));
+        tc_fence_after();
+        const int kbase = kt * 64;
+        const bool full = __all_sync(0xffffffffu, klo <= kbase && kbase + 63 <= khi);
+        uint32_t dd[32];
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          float sv[32], dp[32];
+          tmem_ld32(tmem + lb + hf * 32, sv);
+          tmem_ld32(tmem + lb + 64 + hf * 32, dp);
+          tmem_wait_ld();
+#pragma unroll
+          for (int cc = 0; cc < 32; cc += 2) {
+            const int key = kbase + hf * 32 + cc;
+            float p0 = ex2(fmaf(sv[cc], p.scale_log2, -lse_r));
+            float p1 = ex2(fmaf(sv[cc + 1], p.scale_log2, -lse_r));
+            if (!full) {
+              p0 = (key >= klo && key <= khi) ? p0 : 0.f;
+              p1 = (key + 1 >= klo && key + 1 <= khi) ? p1 : 0.f;
+            }
+            dd[hf * 16 + (cc >> 1)] = pack_bf16(p0 * (dp[cc] - dl), p1 * (dp[cc + 1] - dl));
+          }
+        }
+        tmem_st32u(tmem + lb, dd);  // dS over S: bf16 pairs, K-packed
+        tmem_wait_st_();
+        tc_fence_before();
+        mbar_arrive(bar(B_PF + w));
+      }
+      // epilogue: dQ (+)= scale * accumulator
+      mbar_wait(bar(B_OF + w), (uint32_t)(n_out & 1));
+      tc_fence_after();
+      float* orow = p.dQ + ((int64_t)t * p.h + j) * kD;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float ov[32];
+        tmem_ld32(tmem + lb + 128u + q * 32, ov);
+        tmem_wait_ld();
+        if (ok) {
+#pragma unroll
+          for (int cc = 0; cc < 32; cc += 4) {
+            float4 x = make_float4(ov[cc] * p.scale, ov[cc + 1] * p.scale, ov[cc + 2] * p.scale,
+                                   ov[cc + 3] * p.scale);
+            float4* dst = reinterpret_cast<float4*>(orow + q * 32 + cc);
+            if (p.accumulate) {
+              const float4 y = *dst;
+              x.x += y.x;
+              x.y += y.y;
+              x.z += y.z;
+              x.w += y.w;
+            }
+            *dst = x;
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(bar(B_OE + w));
+      ++n_out;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+}  // namespace
+
+int tc_slide_dq(const fsa_shape* s, const void* Q, const void* K, const void* V, const void* dOut,
+                const void* lse, const void* delta, void* dQ, int accumulate, cudaStream_t st) {
+  Params p{};
+  p.Q = (const __nv_bfloat16*)Q;
+  p.K = (const __nv_bfloat16*)K;
+  p.V = (const __nv_bfloat16*)V;
+  p.dO = (const __nv_bfloat16*)dOut;
+  p.lse = (const float*)lse;
+  p.delta = (const float*)delta;
+  p.dQ = (float*)dQ;
+  p.N = s->N;
+  p.h = s->h;
+  p.h_K = s->h_K;
+  p.g = s->h / s->h_K;
+  p.W = s->W;
+  p.tpi = (int)(kRows / p.g);
+  p.n_super = (p.N + 2 * p.tpi - 1) / (2 * p.tpi);
+  p.accumulate = accumulate;
+  p.scale = (float)s->scale;
+  p.scale_log2 = (float)(s->scale * 1.4426950408889634);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(tc_slide_dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kSmemBytes);
+    attr = true;
+  }
+  int64_t items = p.h_K * p.n_super;
+  int grid = num_sms();
+  if (items < grid) grid = (int)items;
+  if (grid < 1) return FSA_OK;
+  tc_slide_dq_kernel<<<grid, kThreads, kSmemBytes, st>>>(p);
+  FSA_LAUNCH_CHECK("tc_slide_dq");
+  return FSA_OK;
+}
+
+}  // namespace fsa
