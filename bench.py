@@ -124,8 +124,7 @@ def run_ours(args, rank, world, local_rank):
             dist.barrier()
 
     # per-step timing of the dominant kernel (K5) on the launching stream
-    k5_events = []
-    orig_fused = kv_major._fused_forward
+    orig_partials = nsa._sel_partials
 
     def step():
         out, ctx = nsa.nsa_forward(q, k, v, tau, cfg)
@@ -154,11 +153,7 @@ def run_ours(args, rank, world, local_rank):
     except Exception as exc:  # pragma: no cover
         kernel_names = {"profiler_error": str(exc)[:120]}
 
-    # K5 share: time the selected-forward kernel alone inside the same loop
-    s = _lib.shape_of(cfg)
-    import ctypes
-    sel_probe = None
-
+    # K5 is timed inside the same loop with CUDA events on the launching stream
     sampler = ClockSampler(local_rank)
     barrier()
     torch.cuda.synchronize()
@@ -167,34 +162,22 @@ def run_ours(args, rank, world, local_rank):
     stop = torch.cuda.Event(enable_timing=True)
     k5s = []
 
-    def timed_fused(cfg_, dt_, q_, k_, v_, sel_, inv_):
+    def timed_partials(cfg_, dt_, q_, k_, v_, inv_):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        acc = _lib.acc_dtype(dt_)
-        (ob_code, ob_dtype), _ = _lib.buffer_dtypes(cfg_, dt_)
-        obuf = torch.empty((cfg_.h, cfg_.N, cfg_.T, cfg_.d_V), dtype=ob_dtype, device=q_.device)
-        ml = torch.empty((cfg_.h, cfg_.N, cfg_.T, 2), dtype=acc, device=q_.device)
-        st = _lib.stream()
         e0.record()
-        _lib.call("fsa_sel_fwd", ctypes.byref(s), _lib.dt_code(dt_), _lib.FWD_LOCAL, _lib.ptr(q_),
-                  _lib.ptr(k_), _lib.ptr(v_), _lib.ptr(inv_.offsets), _lib.ptr(inv_.qlist),
-                  _lib.ptr(inv_.work), None, _lib.ptr(obuf), ob_code, _lib.ptr(ml), st)
+        res = orig_partials(cfg_, dt_, q_, k_, v_, inv_)
         e1.record()
         k5s.append((e0, e1, inv_))
-        out = torch.empty((cfg_.N, cfg_.h, cfg_.d_V), dtype=acc, device=q_.device)
-        lse = torch.empty((cfg_.h, cfg_.N), dtype=acc, device=q_.device)
-        _lib.call("fsa_merge_fwd", ctypes.byref(s), _lib.dt_code(dt_), _lib.MERGE_LOCAL,
-                  _lib.ptr(sel_.idx), _lib.ptr(obuf), ob_code, _lib.ptr(ml), None, None,
-                  _lib.ptr(out), _lib.ptr(lse), None, None, 0, st)
-        return out, lse
+        return res
 
-    nsa._fused_forward = timed_fused
+    nsa._sel_partials = timed_partials
     start.record()
     for _ in range(args.steps):
         step()
     stop.record()
     torch.cuda.synchronize()
-    nsa._fused_forward = orig_fused
+    nsa._sel_partials = orig_partials
     clocks = sampler.stop()
     ms = start.elapsed_time(stop) / args.steps
     if world > 1:

@@ -123,6 +123,15 @@ int fsa_merge_fwd(const fsa_shape* s, int dtype, int mode, const int32_t* idx, c
                   int obuf_dtype, const void* ml, const void* m_global, const void* l_global,
                   void* out, void* lse, void* m_out, void* l_out, int shared_max, void* stream);
 
+/* K6 + K12 fused for the NSA step: the LOCAL merge (as fsa_merge_fwd) writes the
+ * selected branch's out_sel / lse (acc dtype) and, in the same pass, the gated
+ * combine (branches.py:95-104) out = tau0 out_cmp + tau1 out_sel + tau2 out_slide
+ * in dtype.  out_cmp / out_slide / tau in acc dtype. */
+int fsa_merge_combine_fwd(const fsa_shape* s, int dtype, const int32_t* idx, const void* obuf,
+                          int obuf_dtype, const void* ml, const void* out_cmp,
+                          const void* out_slide, const void* tau, void* out_sel, void* lse,
+                          void* out, void* stream);
+
 /* delta = sum_v out * dOut (kv_major.py:284); [h][N] acc. */
 int fsa_bwd_delta(const fsa_shape* s, int dtype, const void* out, const void* dOut, void* delta,
                   void* stream);

@@ -53,6 +53,7 @@ SIGNATURES = {
     "fsa_build_inverse": ([_sp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "fsa_sel_fwd": ([_sp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp], _i),
     "fsa_merge_fwd": ([_sp, _i, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp], _i),
+    "fsa_merge_combine_fwd": ([_sp, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "fsa_bwd_delta": ([_sp, _i, _vp, _vp, _vp, _vp], _i),
     "fsa_sel_bwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp], _i),
     "fsa_dq_reduce": ([_sp, _i, _vp, _vp, _i, _vp, _vp], _i),

@@ -27,10 +27,20 @@ __device__ __forceinline__ int row_len(const int32_t* row, int T, int lane) {
   return __popc(live);  // entries are a prefix (validated selection)
 }
 
-__global__ void merge_bf16_kernel(const int32_t* __restrict__ idx, const __nv_bfloat16* __restrict__ obuf,
-                                  const float2* __restrict__ ml, float* __restrict__ out,
-                                  float* __restrict__ lse, float* __restrict__ m_out,
-                                  float* __restrict__ l_out, int64_t N, int64_t h, int64_t g, int T) {
+// Gated-combine epilogue (branches.py:95-104): with cmb.out != null the warp
+// also writes out = ((0 + tau0 out_cmp) + tau1 out_sel) + tau2 out_slide (bf16).
+struct Combine {
+  const float* out_cmp;
+  const float* out_slide;
+  const float* tau;
+  __nv_bfloat16* out;
+};
+
+__global__ void __launch_bounds__(256) merge_bf16_kernel(
+    const int32_t* __restrict__ idx, const __nv_bfloat16* __restrict__ obuf,
+    const float2* __restrict__ ml, float* __restrict__ out, float* __restrict__ lse,
+    float* __restrict__ m_out, float* __restrict__ l_out, int64_t N, int64_t h, int64_t g, int T,
+    Combine cmb) {
   const int lane = threadIdx.x & 31;
   const int64_t wid = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (wid >= h * N) return;
@@ -38,7 +48,24 @@ __global__ void merge_bf16_kernel(const int32_t* __restrict__ idx, const __nv_bf
   const int64_t t = wid / h, j = wid % h, kh = j / g;
   const int len = row_len(idx + (kh * N + t) * T, T, lane);
   const int64_t rb = (j * N + t) * (int64_t)T;
+  const __nv_bfloat16* src = obuf + rb * kD + lane * 4;
+  // every partial row of this (head, token) is requested before the slot
+  // statistics are reduced: one memory latency per warp, not two
+  uint2 raw[32];
+#pragma unroll
+  for (int s = 0; s < 32; ++s)
+    if (s < len) raw[s] = __ldcs(reinterpret_cast<const uint2*>(src + s * kD));
   float2 st = lane < len ? __ldg(ml + rb + lane) : make_float2(-INFINITY, 0.f);
+  float cm[4], cs[4], tw[3];
+  if (cmb.out) {
+    const float4 a = *reinterpret_cast<const float4*>(cmb.out_cmp + (t * h + j) * kD + lane * 4);
+    const float4 b = *reinterpret_cast<const float4*>(cmb.out_slide + (t * h + j) * kD + lane * 4);
+    cm[0] = a.x; cm[1] = a.y; cm[2] = a.z; cm[3] = a.w;
+    cs[0] = b.x; cs[1] = b.y; cs[2] = b.z; cs[3] = b.w;
+    tw[0] = __ldg(cmb.tau + t * 3);
+    tw[1] = __ldg(cmb.tau + t * 3 + 1);
+    tw[2] = __ldg(cmb.tau + t * 3 + 2);
+  }
   float M = st.x;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
@@ -46,27 +73,35 @@ __global__ void merge_bf16_kernel(const int32_t* __restrict__ idx, const __nv_bf
   float L = w;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
-  const __nv_bfloat16* src = obuf + rb * kD + lane * 4;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  int s = 0;
-  for (; s + 4 <= len; s += 4) {  // four independent 256 B rows in flight
-    const float4 a = ld_bf16x4(src + (s + 0) * kD), b = ld_bf16x4(src + (s + 1) * kD);
-    const float4 c = ld_bf16x4(src + (s + 2) * kD), d = ld_bf16x4(src + (s + 3) * kD);
-    const float wa = __shfl_sync(0xffffffffu, w, s), wb = __shfl_sync(0xffffffffu, w, s + 1);
-    const float wc = __shfl_sync(0xffffffffu, w, s + 2), wd = __shfl_sync(0xffffffffu, w, s + 3);
-    acc.x += wa * a.x; acc.y += wa * a.y; acc.z += wa * a.z; acc.w += wa * a.w;
-    acc.x += wb * b.x; acc.y += wb * b.y; acc.z += wb * b.z; acc.w += wb * b.w;
-    acc.x += wc * c.x; acc.y += wc * c.y; acc.z += wc * c.z; acc.w += wc * c.w;
-    acc.x += wd * d.x; acc.y += wd * d.y; acc.z += wd * d.z; acc.w += wd * d.w;
-  }
-  for (; s < len; ++s) {
-    const float4 a = ld_bf16x4(src + s * kD);
-    const float wa = __shfl_sync(0xffffffffu, w, s);
-    acc.x += wa * a.x; acc.y += wa * a.y; acc.z += wa * a.z; acc.w += wa * a.w;
+#pragma unroll
+  for (int s = 0; s < 32; ++s) {  // ascending block order
+    if (s < len) {
+      const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw[s].x));
+      const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw[s].y));
+      const float ws = __shfl_sync(0xffffffffu, w, s);
+      acc.x += ws * a.x; acc.y += ws * a.y; acc.z += ws * b.x; acc.w += ws * b.y;
+    }
   }
   const float inv = 1.f / L;
-  *reinterpret_cast<float4*>(out + (t * h + j) * kD + lane * 4) =
-      make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+  const float4 o = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+  *reinterpret_cast<float4*>(out + (t * h + j) * kD + lane * 4) = o;
+  if (cmb.out) {
+    const float ov[4] = {o.x, o.y, o.z, o.w};
+    float r[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      float x = 0.f + tw[0] * cm[c];
+      x = x + tw[1] * ov[c];
+      r[c] = x + tw[2] * cs[c];
+    }
+    const __nv_bfloat162 p0 = __floats2bfloat162_rn(r[0], r[1]);
+    const __nv_bfloat162 p1 = __floats2bfloat162_rn(r[2], r[3]);
+    uint2 u;
+    u.x = *reinterpret_cast<const uint32_t*>(&p0);
+    u.y = *reinterpret_cast<const uint32_t*>(&p1);
+    *reinterpret_cast<uint2*>(cmb.out + (t * h + j) * kD + lane * 4) = u;
+  }
   if (lane == 0) {
     if (lse) lse[j * N + t] = M + __logf(L);
     if (m_out) m_out[j * N + t] = M;
@@ -110,8 +145,21 @@ int merge_bf16_fast(const fsa_shape* s, const int32_t* idx, const void* obuf, co
   if (rows == 0) return FSA_OK;
   merge_bf16_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(
       idx, (const __nv_bfloat16*)obuf, (const float2*)ml, (float*)out, (float*)lse, (float*)m_out,
-      (float*)l_out, s->N, s->h, s->h / s->h_K, (int)s->T);
+      (float*)l_out, s->N, s->h, s->h / s->h_K, (int)s->T, Combine{});
   FSA_LAUNCH_CHECK("merge_bf16");
+  return FSA_OK;
+}
+
+int merge_combine_bf16_fast(const fsa_shape* s, const int32_t* idx, const void* obuf,
+                            const void* ml, const void* out_cmp, const void* out_slide,
+                            const void* tau, void* out_sel, void* lse, void* out, cudaStream_t st) {
+  const int64_t rows = s->h * s->N;
+  if (rows == 0) return FSA_OK;
+  Combine c{(const float*)out_cmp, (const float*)out_slide, (const float*)tau, (__nv_bfloat16*)out};
+  merge_bf16_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(
+      idx, (const __nv_bfloat16*)obuf, (const float2*)ml, (float*)out_sel, (float*)lse, nullptr,
+      nullptr, s->N, s->h, s->h / s->h_K, (int)s->T, c);
+  FSA_LAUNCH_CHECK("merge_combine_bf16");
   return FSA_OK;
 }
 

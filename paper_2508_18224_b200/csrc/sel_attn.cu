@@ -438,6 +438,20 @@ extern "C" int fsa_merge_fwd(const fsa_shape* s, int dtype, int mode, const int3
               m_out, l_out, shared_max, (cudaStream_t)stream);
 }
 
+extern "C" int fsa_merge_combine_fwd(const fsa_shape* s, int dtype, const int32_t* idx,
+                                     const void* obuf, int obuf_dtype, const void* ml,
+                                     const void* out_cmp, const void* out_slide, const void* tau,
+                                     void* out_sel, void* lse, void* out, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == FSA_DT_BF16 && obuf_dtype == FSA_DT_BF16 && fsa::fast_reduce_ok(*s))
+    return fsa::merge_combine_bf16_fast(s, idx, obuf, ml, out_cmp, out_slide, tau, out_sel, lse,
+                                        out, st);
+  int rc = fsa_merge_fwd(s, dtype, FSA_MERGE_LOCAL, idx, obuf, obuf_dtype, ml, nullptr, nullptr,
+                         out_sel, lse, nullptr, nullptr, 0, stream);
+  if (rc) return rc;
+  return fsa_gated_combine(s, dtype, out_cmp, out_sel, out_slide, tau, out, 0, stream);
+}
+
 extern "C" int fsa_bwd_delta(const fsa_shape* s, int dtype, const void* out, const void* dOut,
                              void* delta, void* stream) {
   DISPATCH_DT(dtype, delta_impl, s, out, dOut, delta, (cudaStream_t)stream);

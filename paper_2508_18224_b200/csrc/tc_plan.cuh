@@ -39,6 +39,9 @@ int tc_slide_dq(const fsa_shape* s, const void* Q, const void* K, const void* V,
 bool fast_reduce_ok(const fsa_shape& s);
 int merge_bf16_fast(const fsa_shape* s, const int32_t* idx, const void* obuf, const void* ml,
                     void* out, void* lse, void* m_out, void* l_out, cudaStream_t st);
+int merge_combine_bf16_fast(const fsa_shape* s, const int32_t* idx, const void* obuf,
+                            const void* ml, const void* out_cmp, const void* out_slide,
+                            const void* tau, void* out_sel, void* lse, void* out, cudaStream_t st);
 int dq_reduce_bf16_fast(const fsa_shape* s, const int32_t* idx, const void* dq, void* dQ,
                         cudaStream_t st);
 

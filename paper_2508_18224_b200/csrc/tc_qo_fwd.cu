@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const Params p) 
     };
     // a stage wait that would block first publishes the in-flight gather
     auto wait_stage = [&](uint32_t b, uint32_t par) {
-      if (mbar_try_wait(b, par)) return;
+      if (mbar_test(b, par)) return;
       asm volatile("cp.async.wait_group 0;" ::: "memory");
       fence_proxy_async();
       if (pend) mbar_arrive(pend);
@@ -241,8 +241,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const Params p) 
             if (su[w] < s.k1) {
               const int rr = cs[w].rbase + (su[w] - cs[w].it.u0);
               const int kv = (int)(rr % kKVStages), v = (int)(ns[w] & 1);
-              if (ns[w] < np[w] + 2 && mbar_try_wait(bar(B_QF + qs), qpar) &&
-                  mbar_try_wait(bar(B_KF + kv), (uint32_t)((rr / kKVStages) & 1))) {
+              if (ns[w] < np[w] + 2 && mbar_test(bar(B_QF + qs), qpar) &&
+                  mbar_test(bar(B_KF + kv), (uint32_t)((rr / kKVStages) & 1))) {
                 tc_fence_after();
                 const uint32_t q = sb + kOffQ + (qs * 2 + w) * kQ, k = sb + kOffKV + kv * kKV;
                 const uint32_t tS = tmem + 256u * w + 64u * v;
@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const Params p) 
                 ++su[w];
                 progressed = true;
               }
-            } else if (s.k0 < s.k1 || mbar_try_wait(bar(B_QF + qs), qpar)) {
+            } else if (s.k0 < s.k1 || mbar_test(bar(B_QF + qs), qpar)) {
               mma_commit(bar(B_QE + qs));  // this stream is done with the Q stage
               ls[w] = cs[w].advance(p, G);
               su[w] = ls[w] ? cs[w].it.s[w].k0 : 0;
@@ -271,8 +271,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const Params p) 
               const int v = (int)(np[w] & 1);
               const bool first = pu[w] == s.k0, last = pu[w] + 1 == s.k1;
               if (np[w] < ns[w] &&
-                  mbar_try_wait(bar(B_PF + 2 * w + v), (uint32_t)((np[w] >> 1) & 1)) &&
-                  (!first || mbar_try_wait(bar(B_OE + w), (uint32_t)((nsub[w] & 1) ^ 1)))) {
+                  mbar_test(bar(B_PF + 2 * w + v), (uint32_t)((np[w] >> 1) & 1)) &&
+                  (!first || mbar_test(bar(B_OE + w), (uint32_t)((nsub[w] & 1) ^ 1)))) {
                 tc_fence_after();
                 const uint32_t vv = sb + kOffKV + kv * kKV + 16384u;
                 const uint32_t tS = tmem + 256u * w + 64u * v, tO = tmem + 256u * w + 128u;
@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const Params p) 
                 ++pu[w];
                 progressed = true;
               }
-            } else if (mbar_try_wait(bar(B_KF + kv), (uint32_t)((rr / kKVStages) & 1))) {
+            } else if (mbar_test(bar(B_KF + kv), (uint32_t)((rr / kKVStages) & 1))) {
               mma_commit(bar(B_KE + kv));  // pass-by: tile not used by this sub-item
               ++pu[w];
               progressed = true;

@@ -34,7 +34,7 @@ struct Ring {
   }
   // consumer side, non-blocking: false if slot k is not filled yet
   __device__ bool try_consume(int k, int32_t& t) const {
-    if (!mbar_try_wait(full(k), (uint32_t)((k / kRingDepth) & 1))) return false;
+    if (!mbar_test(full(k), (uint32_t)((k / kRingDepth) & 1))) return false;
     t = slots[k & (kRingDepth - 1)];
     mbar_arrive(empty(k));
     return true;

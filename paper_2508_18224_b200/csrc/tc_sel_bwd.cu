@@ -45,21 +45,25 @@ constexpr uint32_t kOffDS = kOffP + 32768;  // dS[2] [128][128 B]
 constexpr uint32_t kStStride = 80;          // dq staging (inside the wg's P stage)
 constexpr uint32_t kOffBar = kOffDS + 32768;
 enum {
-  B_QDF = 0, B_QDE = 2, B_KVF = 4, B_KVE = 5, B_SDF = 6, B_SDE = 8, B_PDF = 10, B_DQF = 12,
-  B_KAF = 14, B_KAE = 15, B_RF = 16, B_RE = 20, kNumBars = 24
+  // smem stages (Q/dO, P/dS) by item parity; TMEM stages (S|dP, then dQ) by item mod 3
+  B_QDF = 0, B_QDE = 2, B_KVF = 4, B_KVE = 5, B_SDF = 6, B_SDE = 9, B_PDF = 12, B_DQF = 14,
+  B_KAF = 17, B_KAE = 18, B_RF = 19, B_RE = 23, kNumBars = 27
 };
 constexpr uint32_t kOffRing = kOffBar + kNumBars * 8;
 constexpr uint32_t kOffTmem = kOffRing + 16;
 constexpr uint32_t kSmemBytes = kOffTmem + 16 + 1024;
 
-// TMEM columns: stage s at 128 s (S | dP, later dQ), dK^T 256, dV^T 320
-constexpr uint32_t kColDK = 256, kColDV = 320;
+// TMEM columns: stage t (= item mod 3) at 128 t (S | dP, later dQ), dK^T 384, dV^T 448.
+// The third stage lets S/dP of item n+2 run while item n's dQ is read out.
+constexpr int kTStages = 3;
+constexpr uint32_t kColDK = 384, kColDV = 448;
 
 constexpr uint32_t kIdS = idesc_bf16(128, 64, false, false);  // S, dP
 constexpr uint32_t kIdKV = idesc_bf16(128, 64, true, true);   // dV^T, dK^T
 constexpr uint32_t kIdQ = idesc_bf16(128, 128, false, true);  // dQ
 
 struct Params {
+  long long* trace;  // debug timeline (CTA 0, first 256 items), null in production
   const __nv_bfloat16 *Q, *K, *V, *dO;
   const float *lse, *delta;
   const int32_t *offsets, *qlist;
@@ -73,6 +77,11 @@ struct Params {
   FastDiv fdT;
   float scale, scale_log2;
 };
+
+#define K8_TRACE(item, slot)                                                        \
+  do {                                                                              \
+    if (p.trace && blockIdx.x == 0 && (item) < 256) p.trace[(item) * 8 + (slot)] = clock64(); \
+  } while (0)
 
 // Rows of a task: the selected mode reads them from the inverse CSR; the
 // sliding mode uses the contiguous window of tokens [64 i, 64 i + 63 + W - 1].
@@ -126,9 +135,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
     for (int s = 0; s < 2; ++s) {
       mbar_init(bar(B_QDF + s), 128);
       mbar_init(bar(B_QDE + s), 1);
+      mbar_init(bar(B_PDF + s), 128);
+    }
+    for (int s = 0; s < kTStages; ++s) {
       mbar_init(bar(B_SDF + s), 1);
       mbar_init(bar(B_SDE + s), 128);
-      mbar_init(bar(B_PDF + s), 128);
       mbar_init(bar(B_DQF + s), 1);
     }
     mbar_init(bar(B_KVF), 128);
@@ -152,8 +163,20 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
     const int lr = threadIdx.x - 256;
     const int kt = lr / (int)p.g, hh = lr % (int)p.g;
     int64_t n = 0, kseq = 0;
-    int prev = -1;
+    // The newest gather stays in flight (unpublished) while the next one is
+    // issued; any wait that could block first publishes it.
+    uint32_t pend = 0;      // QDF barrier of the in-flight Q/dO gather
+    bool kv_pend = false;   // the task's K/V gather is not yet published
+    auto publish = [&]() {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      fence_proxy_async();
+      if (kv_pend) mbar_arrive(bar(B_KVF));
+      if (pend) mbar_arrive(pend);
+      kv_pend = false;
+      pend = 0;
+    };
     for (int k = 0;; ++k) {
+      publish();  // nothing in flight across the task ring
       if (lr == 0) ring.produce(k, p.counter, p.ntask);
       const int32_t task = ring.consume(k);
       if (task < 0) break;
@@ -167,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
         warp_gather_rows32(sb + (lw < 2 ? kOffK : kOffV), 8192u, row0, src, true, lane);
         asm volatile("cp.async.commit_group;" ::: "memory");
       }
-      bool kv_pending = true;
+      kv_pend = true;
       int32_t ent_next = kt < p.tpi ? entry_at(p, tr, kt) : 0;
       for (int c = 0; c < tr.nitems; ++c, ++n) {
         const int s = (int)(n & 1);
@@ -175,7 +198,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
         const bool ok = kt < p.tpi && pos < tr.ntok;
         const int32_t ent = ent_next;
         ent_next = kt < p.tpi ? entry_at(p, tr, pos + p.tpi) : 0;
-        mbar_wait(bar(B_QDE + s), (uint32_t)(((n >> 1) & 1) ^ 1));
+        const uint32_t par = (uint32_t)(((n >> 1) & 1) ^ 1);
+        if (!mbar_test(bar(B_QDE + s), par)) {
+          publish();
+          mbar_wait(bar(B_QDE + s), par);
+        }
         int64_t row = 0;
         if (ok) {
           int64_t t, slot;
@@ -184,20 +211,19 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
         }
         warp_gather_rows32(sb + kOffQ + s * kTile, 16384u, lr & ~31, p.Q + row * kD, ok, lane);
         warp_gather_rows32(sb + kOffDO + s * kTile, 16384u, lr & ~31, p.dO + row * kD, ok, lane);
-        // publish as soon as it lands: with two Q/dO stages an unpublished
-        // gather would block the MMA's look-ahead (it needs item n+1 before
-        // it can release item n's stage)
         asm volatile("cp.async.commit_group;" ::: "memory");
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        // everything but this gather has landed: publish the previous one
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
         fence_proxy_async();
-        if (kv_pending) {
-          mbar_arrive(bar(B_KVF));
-          kv_pending = false;
-        }
-        mbar_arrive(bar(B_QDF + s));
+        if (kv_pend) mbar_arrive(bar(B_KVF));
+        if (pend) mbar_arrive(pend);
+        kv_pend = false;
+        pend = bar(B_QDF + s);
+        if (lr == 0) K8_TRACE(n, 0);  // gather issued
       }
       ++kseq;
     }
+    publish();
   } else if (warp == 12) {
     // ================================================================ MMA issuer
     // Two independent in-order streams, polled without blocking:
@@ -239,12 +265,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
           }
           if (have) {
             const int s = (int)(ns & 1);
-            if (mbar_try_wait(bar(B_KVF), (uint32_t)(a_kseq & 1)) &&
-                mbar_try_wait(bar(B_QDF + s), (uint32_t)((ns >> 1) & 1)) &&
-                mbar_try_wait(bar(B_SDE + s), (uint32_t)(((ns >> 1) & 1) ^ 1))) {
+            if (mbar_test(bar(B_KVF), (uint32_t)(a_kseq & 1)) &&
+                mbar_test(bar(B_QDF + s), (uint32_t)((ns >> 1) & 1)) &&
+                mbar_test(bar(B_SDE + ns % kTStages), (uint32_t)(((ns / kTStages) & 1) ^ 1))) {
               tc_fence_after();
               const uint32_t q = sb + kOffQ + s * kTile, o = sb + kOffDO + s * kTile;
-              const uint32_t tS = tmem + 128u * s;
+              const uint32_t tS = tmem + 128u * (uint32_t)(ns % kTStages);
 #pragma unroll
               for (int k = 0; k < 8; ++k) {
                 const uint32_t ko = (k >> 2) * 16384u + (k & 3) * 32u, kk = (k >> 2) * 8192u + (k & 3) * 32u;
@@ -255,7 +281,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
                 const uint32_t ko = (k >> 2) * 16384u + (k & 3) * 32u, kk = (k >> 2) * 8192u + (k & 3) * 32u;
                 mma_bf16(tS + 64, desc_kmajor(o + ko), desc_kmajor(sb + kOffV + kk), kIdS, k > 0);
               }
-              mma_commit(bar(B_SDF + s));
+              mma_commit(bar(B_SDF + ns % kTStages));
+              K8_TRACE(ns, 1);  // S/dP issued
               ++a_c;
               ++ns;
               progressed = true;
@@ -266,8 +293,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
         if (np < ns) {
           const bool first = np == 0 || b_c + 1 >= b_tr.nitems;
           const int s = (int)(np & 1);
-          const bool ready = mbar_try_wait(bar(B_PDF + s), (uint32_t)((np >> 1) & 1)) &&
-                             (!first || mbar_try_wait(bar(B_KAE), (uint32_t)(((kseq_b + 1) & 1) ^ 1)));
+          const bool ready = mbar_test(bar(B_PDF + s), (uint32_t)((np >> 1) & 1)) &&
+                             (!first || mbar_test(bar(B_KAE), (uint32_t)(((kseq_b + 1) & 1) ^ 1)));
           if (ready) {
             if (first) {
               b_tr = rows_of(p, fifo.pop());
@@ -291,10 +318,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
             if (!p.no_dq) {
 #pragma unroll
               for (int k = 0; k < 4; ++k)
-                mma_bf16(tmem + 128u * s, desc_kmajor(ds + k * 32u),
+                mma_bf16(tmem + 128u * (uint32_t)(np % kTStages), desc_kmajor(ds + k * 32u),
                          desc_mnmajor(sb + kOffK + k * 2048u, 8192u), kIdQ, k > 0);
             }
-            mma_commit(bar(B_DQF + s));
+            mma_commit(bar(B_DQF + np % kTStages));
+            K8_TRACE(np, 4);  // products issued
             mma_commit(bar(B_QDE + s));
             if (last) {
               mma_commit(bar(B_KAF));
@@ -327,26 +355,24 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
       tc_fence_after();
       float* dk = p.dK + ((tr.i * kBK) * p.h_K + tr.kh) * kD + r;
       float* dv = p.dV + ((tr.i * kBK) * p.h_K + tr.kh) * kD + r;
+      const int64_t ks_ = p.h_K * kD;  // key stride
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        float v[32];
-        tmem_ld32(tmem + lb + kColDK + q * 32, v);
-        tmem_wait_ld();
-        if (p.accumulate) {
+      for (int q = 0; q < 4; ++q) {  // dK keys 0-31, 32-63, then dV
+        float* dst = (q < 2 ? dk : dv) + (int64_t)(q & 1) * 32 * ks_;
+        const float mul = q < 2 ? p.scale : 1.f;
+        float v[32], old[32];
+        if (p.accumulate) {  // batch the 32 loads: one memory latency per chunk
 #pragma unroll
-          for (int c = 0; c < 32; ++c) dk[(q * 32 + c) * p.h_K * kD] += v[c] * p.scale;
-        } else {
-#pragma unroll
-          for (int c = 0; c < 32; ++c) dk[(q * 32 + c) * p.h_K * kD] = v[c] * p.scale;
+          for (int c = 0; c < 32; ++c) old[c] = __ldcg(dst + c * ks_);
         }
-        tmem_ld32(tmem + lb + kColDV + q * 32, v);
+        tmem_ld32(tmem + lb + (q < 2 ? kColDK : kColDV) + (q & 1) * 32, v);
         tmem_wait_ld();
         if (p.accumulate) {
 #pragma unroll
-          for (int c = 0; c < 32; ++c) dv[(q * 32 + c) * p.h_K * kD] += v[c];
+          for (int c = 0; c < 32; ++c) dst[c * ks_] = old[c] + v[c] * mul;
         } else {
 #pragma unroll
-          for (int c = 0; c < 32; ++c) dv[(q * 32 + c) * p.h_K * kD] = v[c];
+          for (int c = 0; c < 32; ++c) dst[c * ks_] = v[c] * mul;
         }
       }
       tc_fence_before();
@@ -356,6 +382,17 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
       const int32_t task = ring.consume(k);
       if (task < 0) break;
       const TaskRows tr = rows_of(p, task);
+      if (p.accumulate && tr.nitems > 0) {
+        // the block's dK/dV rows are read back (+=) at the end of the task:
+        // pull them into L2 now (512 lines of 128 B over the 256 softmax threads)
+        const int x = threadIdx.x;  // 0..255
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int line = x + 256 * h2, key = (line >> 2) & 63, part = line & 3;
+          const float* base = (line < 256 ? p.dK : p.dV) + ((tr.i * kBK + key) * p.h_K + tr.kh) * kD;
+          prefetch_l2(base + part * 32);
+        }
+      }
       if (tr.nitems == 0) {  // no attending rows: the block's gradients are zero
         if (p.accumulate || wg != 0) continue;
         float* dk = p.dK + ((tr.i * kBK) * p.h_K + tr.kh) * kD + r;
@@ -394,15 +431,18 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
           dl = p.delta[j * p.N + t];
         }
         const bool full = __all_sync(0xffffffffu, klo == 0 && khi == kBK - 1);
-        mbar_wait(bar(B_SDF + s), (uint32_t)((n >> 1) & 1));
+        const int tm = (int)(n % kTStages);
+        const uint32_t tpar = (uint32_t)((n / kTStages) & 1);
+        mbar_wait(bar(B_SDF + tm), tpar);
+        if (r == 0) K8_TRACE(n, 2);  // S/dP landed
         tc_fence_after();
         unsigned char* prow = smem + kOffP + s * 16384u;
         unsigned char* drw = smem + kOffDS + s * 16384u;
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf) {  // 32 key columns at a time (register budget)
           float sv[32], dp[32];
-          tmem_ld32(tmem + lb + 128u * s + hf * 32, sv);
-          tmem_ld32(tmem + lb + 128u * s + 64 + hf * 32, dp);
+          tmem_ld32(tmem + lb + 128u * tm + hf * 32, sv);
+          tmem_ld32(tmem + lb + 128u * tm + 64 + hf * 32, dp);
           tmem_wait_ld();
           uint32_t pp[16], dd[16];
 #pragma unroll
@@ -428,13 +468,15 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
         }
         if (p.no_dq) {  // S/dP consumed: the TMEM stage is free right away
           tc_fence_before();
-          mbar_arrive(bar(B_SDE + s));
+          mbar_arrive(bar(B_SDE + tm));
         }
         fence_proxy_async();
         mbar_arrive(bar(B_PDF + s));
+        if (r == 0) K8_TRACE(n, 3);  // P/dS written
         // products of this item landed -> dQ partial out of TMEM; stage the
         // bf16 rows in this wg's (now consumed) P buffer for coalesced stores
-        mbar_wait(bar(B_DQF + s), (uint32_t)((n >> 1) & 1));
+        mbar_wait(bar(B_DQF + tm), tpar);
+        if (r == 0) K8_TRACE(n, 5);  // products landed
         tc_fence_after();
         if (p.no_dq) {
           if (c + 1 == tr.nitems) kv_epilogue(tr, kseq);
@@ -444,7 +486,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           float v[32];
-          tmem_ld32(tmem + lb + 128u * s + q * 32, v);
+          tmem_ld32(tmem + lb + 128u * tm + q * 32, v);
           tmem_wait_ld();
 #pragma unroll
           for (int c4 = 0; c4 < 4; ++c4) {
@@ -456,7 +498,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
           }
           if (q == 3) {
             tc_fence_before();
-            mbar_arrive(bar(B_SDE + s));  // stage s TMEM free for S/dP of item n+2
+            mbar_arrive(bar(B_SDE + tm));  // TMEM stage free for S/dP of item n+3
+            if (r == 0) K8_TRACE(n, 6);  // dQ read out of TMEM
           }
           __syncwarp();
 #pragma unroll
@@ -468,6 +511,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
           }
           __syncwarp();
         }
+        if (r == 0) K8_TRACE(n, 7);  // dQ rows stored
         if (c + 1 == tr.nitems) kv_epilogue(tr, kseq);
       }
       ++kseq;
@@ -487,10 +531,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
 bool tc_bwd_supported(const fsa_shape& s, int dtype) { return tc_fwd_supported(s, dtype); }
 
 namespace {
+long long* g_trace = nullptr;
 Params make_params(const fsa_shape* s, const void* Q, const void* K, const void* V,
                    const void* dOut, const void* lse, const void* delta, void* dq_buf, void* dK,
                    void* dV) {
   Params p{};
+  p.trace = g_trace;
   p.Q = (const __nv_bfloat16*)Q;
   p.K = (const __nv_bfloat16*)K;
   p.V = (const __nv_bfloat16*)V;
@@ -564,3 +610,6 @@ int tc_slide_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V
 }
 
 }  // namespace fsa
+
+// debug: record a per-item timeline of CTA 0 of the next tc_sel_bwd launches
+extern "C" void fsa_debug_bwd_trace(void* device_buf) { fsa::g_trace = (long long*)device_buf; }

@@ -192,9 +192,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const Params p)
           }
           if (have) {
             const int s = ns % kQStages, v = ns & 1, kvs = a_kseq & 1;
-            if (mbar_try_wait(bar(B_KVF + kvs), (uint32_t)((a_kseq >> 1) & 1)) &&
-                mbar_try_wait(bar(B_QF + s), (uint32_t)((ns / kQStages) & 1)) &&
-                mbar_try_wait(bar(B_SE + v), (uint32_t)(((ns >> 1) & 1) ^ 1))) {
+            if (mbar_test(bar(B_KVF + kvs), (uint32_t)((a_kseq >> 1) & 1)) &&
+                mbar_test(bar(B_QF + s), (uint32_t)((ns / kQStages) & 1)) &&
+                mbar_test(bar(B_SE + v), (uint32_t)(((ns >> 1) & 1) ^ 1))) {
               tc_fence_after();
               const uint32_t qa = sb + kOffQ + s * kQBytes;
               const uint32_t ka_ = sb + kOffKV + kvs * kKVBytes;
@@ -212,8 +212,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const Params p)
         }
         if (np < ns) {
           const int v = np & 1;
-          if (mbar_try_wait(bar(B_PF + v), (uint32_t)((np >> 1) & 1)) &&
-              mbar_try_wait(bar(B_OE + v), (uint32_t)(((np >> 1) & 1) ^ 1))) {
+          if (mbar_test(bar(B_PF + v), (uint32_t)((np >> 1) & 1)) &&
+              mbar_test(bar(B_OE + v), (uint32_t)(((np >> 1) & 1) ^ 1))) {
             if (np == 0 || b_c + 1 >= b_tr.nitems) {
               b_tr = task_rows(fifo.pop(), p.offsets, p.b, p.tpi);
               b_c = 0;

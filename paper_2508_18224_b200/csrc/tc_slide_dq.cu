@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const Params p
       pend = b;
     };
     auto wait_stage = [&](uint32_t b, uint32_t par) {
-      if (mbar_try_wait(b, par)) return;
+      if (mbar_test(b, par)) return;
       asm volatile("cp.async.wait_group 0;" ::: "memory");
       fence_proxy_async();
       if (pend) mbar_arrive(pend);
@@ -207,8 +207,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const Params p
             if (su[w] < s.k1) {
               const int rr = cs[w].rbase + (su[w] - cs[w].it.u0);
               const int kv = rr % kKVStages;
-              if (ns[w] == nd[w] && mbar_try_wait(bar(B_QF), qpar) &&
-                  mbar_try_wait(bar(B_KF + kv), (uint32_t)((rr / kKVStages) & 1))) {
+              if (ns[w] == nd[w] && mbar_test(bar(B_QF), qpar) &&
+                  mbar_test(bar(B_KF + kv), (uint32_t)((rr / kKVStages) & 1))) {
                 tc_fence_after();
                 const uint32_t q = sb + kOffQ + w * kT, o = sb + kOffQ + (2 + w) * kT;
                 const uint32_t k = sb + kOffKV + kv * kKV, vv = k + 16384u;
@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const Params p
                 ++su[w];
                 progressed = true;
               }
-            } else if (s.k0 < s.k1 || mbar_try_wait(bar(B_QF), qpar)) {
+            } else if (s.k0 < s.k1 || mbar_test(bar(B_QF), qpar)) {
               mma_commit(bar(B_QE));
               ls[w] = cs[w].advance(p, G);
               su[w] = ls[w] ? cs[w].it.s[w].k0 : 0;
@@ -239,8 +239,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const Params p
             const int kv = rr % kKVStages;
             if (du[w] >= s.k0 && du[w] < s.k1) {
               const bool first = du[w] == s.k0, last = du[w] + 1 == s.k1;
-              if (nd[w] < ns[w] && mbar_try_wait(bar(B_PF + w), (uint32_t)(nd[w] & 1)) &&
-                  (!first || mbar_try_wait(bar(B_OE + w), (uint32_t)((nsub[w] & 1) ^ 1)))) {
+              if (nd[w] < ns[w] && mbar_test(bar(B_PF + w), (uint32_t)(nd[w] & 1)) &&
+                  (!first || mbar_test(bar(B_OE + w), (uint32_t)((nsub[w] & 1) ^ 1)))) {
                 tc_fence_after();
                 const uint32_t k = sb + kOffKV + kv * kKV;
                 const uint32_t tS = tmem + 256u * w, tQ = tmem + 256u * w + 128u;
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const Params p
                 ++du[w];
                 progressed = true;
               }
-            } else if (mbar_try_wait(bar(B_KF + kv), (uint32_t)((rr / kKVStages) & 1))) {
+            } else if (mbar_test(bar(B_KF + kv), (uint32_t)((rr / kKVStages) & 1))) {
               mma_commit(bar(B_KE + kv));
               ++du[w];
               progressed = true;
@@ -296,6 +296,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const Params p
       const int khi = ok ? t : -1;
       const float lse_r = ok ? p.lse[j * p.N + t] * 1.4426950408889634f : 0.f;
       const float dl = ok ? p.delta[j * p.N + t] : 0.f;
+      if (ok && p.accumulate) {  // the row is read back (+=) by the epilogue
+        const float* row = p.dQ + ((int64_t)t * p.h + j) * kD;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) prefetch_l2(row + q * 32);
+      }
       for (int kt = s.k0; kt < s.k1; ++kt, ++u) {
         mbar_wait(bar(B_SF + w), (uint32_t)(u & 1));
         tc_fence_after();
@@ -331,23 +336,26 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const Params p
       float* orow = p.dQ + ((int64_t)t * p.h + j) * kD;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
+        float4 old[8];
+        if (ok && p.accumulate) {  // batched loads: one memory latency per chunk
+#pragma unroll
+          for (int cc = 0; cc < 8; ++cc) old[cc] = __ldcg(reinterpret_cast<const float4*>(orow + q * 32) + cc);
+        }
         float ov[32];
         tmem_ld32(tmem + lb + 128u + q * 32, ov);
         tmem_wait_ld();
         if (ok) {
 #pragma unroll
-          for (int cc = 0; cc < 32; cc += 4) {
-            float4 x = make_float4(ov[cc] * p.scale, ov[cc + 1] * p.scale, ov[cc + 2] * p.scale,
-                                   ov[cc + 3] * p.scale);
-            float4* dst = reinterpret_cast<float4*>(orow + q * 32 + cc);
+          for (int cc = 0; cc < 8; ++cc) {
+            float4 x = make_float4(ov[4 * cc] * p.scale, ov[4 * cc + 1] * p.scale,
+                                   ov[4 * cc + 2] * p.scale, ov[4 * cc + 3] * p.scale);
             if (p.accumulate) {
-              const float4 y = *dst;
-              x.x += y.x;
-              x.y += y.y;
-              x.z += y.z;
-              x.w += y.w;
+              x.x += old[cc].x;
+              x.y += old[cc].y;
+              x.z += old[cc].z;
+              x.w += old[cc].w;
             }
-            *dst = x;
+            reinterpret_cast<float4*>(orow + q * 32)[cc] = x;
           }
         }
       }

@@ -100,19 +100,28 @@ def _intake(cfg, Q, K, V=None, dOut=None):
     return dt, q, k, v, do
 
 
-def _fused_forward(cfg, dt, q, k, v, sel, inv):
-    """K5 (LOCAL) + K6 (LOCAL merge): returns out storage (N, h, d_V) and lse
-    (h, N), both in the accumulator dtype (f32 for bf16 inputs)."""
+def _sel_partials(cfg, dt, q, k, v, inv):
+    """K5 in LOCAL mode: slot-indexed partials O_i / l_i and (m_i, l_i)."""
     dev = q.device
     acc = _lib.acc_dtype(dt)
     (ob_code, ob_dtype), _ = _lib.buffer_dtypes(cfg, dt)
     obuf = torch.empty((cfg.h, cfg.N, cfg.T, cfg.d_V), dtype=ob_dtype, device=dev)
     ml = torch.empty((cfg.h, cfg.N, cfg.T, 2), dtype=acc, device=dev)
     s = _lib.shape_of(cfg)
-    st = _lib.stream()
     _lib.call("fsa_sel_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.FWD_LOCAL, _lib.ptr(q),
               _lib.ptr(k), _lib.ptr(v), _lib.ptr(inv.offsets), _lib.ptr(inv.qlist), _lib.ptr(inv.work),
-              None, _lib.ptr(obuf), ob_code, _lib.ptr(ml), st)
+              None, _lib.ptr(obuf), ob_code, _lib.ptr(ml), _lib.stream())
+    return obuf, ml, ob_code
+
+
+def _fused_forward(cfg, dt, q, k, v, sel, inv):
+    """K5 (LOCAL) + K6 (LOCAL merge): returns out storage (N, h, d_V) and lse
+    (h, N), both in the accumulator dtype (f32 for bf16 inputs)."""
+    dev = q.device
+    acc = _lib.acc_dtype(dt)
+    obuf, ml, ob_code = _sel_partials(cfg, dt, q, k, v, inv)
+    s = _lib.shape_of(cfg)
+    st = _lib.stream()
     out = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=acc, device=dev)
     lse = torch.empty((cfg.h, cfg.N), dtype=acc, device=dev)
     _lib.call("fsa_merge_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.MERGE_LOCAL,

@@ -27,7 +27,7 @@ import dataclasses
 import torch
 
 from . import _lib
-from .kv_major import _backward_core, _fused_forward
+from .kv_major import _backward_core, _sel_partials
 from .branches import _cmp_workspace, _slide_bwd_storage, _slide_fwd_storage
 from .selection import SelectionTensor, build_inverse_index
 
@@ -77,11 +77,17 @@ def nsa_forward(q, k, v, tau, cfg):
     sel = SelectionTensor(idx)
     sel._trusted = True
     inv = build_inverse_index(sel, cfg, validate=False)
-    out_sel, lse_sel = _fused_forward(cfg, dt, q, k, v, sel, inv)
+    # K5 writes the slot partials; the sliding branch runs before the merge so
+    # that K6 can apply the gated combine (K12) in the same pass
+    obuf, ml, ob_code = _sel_partials(cfg, dt, q, k, v, inv)
     out_slide, lse_slide = _slide_fwd_storage(cfg, dt, q, k, v)
+    out_sel = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=acc, device=dev)
+    lse_sel = torch.empty((cfg.h, cfg.N), dtype=acc, device=dev)
     out = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=dt, device=dev)
-    _lib.call("fsa_gated_combine", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(out_cmp),
-              _lib.ptr(out_sel), _lib.ptr(out_slide), _lib.ptr(tau), _lib.ptr(out), 0, st)
+    _lib.call("fsa_merge_combine_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(sel.idx),
+              _lib.ptr(obuf), ob_code, _lib.ptr(ml), _lib.ptr(out_cmp), _lib.ptr(out_slide),
+              _lib.ptr(tau), _lib.ptr(out_sel), _lib.ptr(lse_sel), _lib.ptr(out), st)
+    del obuf, ml
     ctx = NSAContext(cfg, dt, q, k, v, tau, sel, inv, out_sel, lse_sel, out_slide, lse_slide,
                      out_cmp, scores)
     return out, ctx
