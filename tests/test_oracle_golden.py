@@ -147,3 +147,38 @@ def test_acceptance_sweep():
         g = O.selected_backward(Q, K, V, idx, O.make_dout(c, seed), c)
         for got, key in zip(g, ("dQ", "dK", "dV")):
             assert np.abs(got - z[p + key]).max() <= 1e-9
+
+
+def test_sampled_row_restatement_matches_whole_array_oracle():
+    """oracle.nsa_rows / block_grads (used by the full-size GPU parity tests)
+    against the whole-array oracle pinned above, on a small problem."""
+    kw = dict(N=512, d_K=16, d_V=16, h=8, h_K=2, B_K=16, T=4, W=64)
+    c = O.cfg_of(**kw)
+    Q, K, V = O.make_qkv(c, 11)
+    dO = O.make_dout(c, 11)
+    tau = O.make_gates(c, 11)
+    cmp = O.compress_kv(K, V, c)
+    idx = O.select_topk(O.importance_scores(Q, cmp.K_cmp, c), c)
+    o_sel, l_sel = O.selected_forward(Q, K, V, idx, c)
+    o_sl, l_sl = O.sliding_forward(Q, K, V, c)
+    o_cmp, l_cmp = O.compressed_forward(Q, cmp, c)
+    out, _ = O.gated_combine((o_cmp, o_sel, o_sl), tau, c)
+    g_sel = O.selected_backward(Q, K, V, idx, dO * tau[:, 1][:, None, None], c)
+    g_sl = O.sliding_backward(Q, K, V, dO * tau[:, 2][:, None, None], c)
+    st = lambda x: np.ascontiguousarray(x.transpose(0, 2, 1))  # noqa: E731
+    Qs, Ks, Vs, dOs = st(Q), st(K), st(V), st(dO)
+    toks = np.array([0, 5, 14, 15, 16, 63, 64, 200, 511])
+    scores = O.importance_scores(Q, cmp.K_cmp, c)
+    np.testing.assert_array_equal(O.select_topk_rows(scores[:, toks], toks, c), idx[:, toks])
+    pooled = O.pooled_kv(Ks, Vs, c)
+    r = O.nsa_rows(Qs[toks], toks, Ks, Vs, idx[:, toks], tau[toks], pooled, c, dO_rows=dOs[toks])
+    for name, ref in (("out", out), ("out_sel", o_sel), ("out_slide", o_sl), ("out_cmp", o_cmp)):
+        np.testing.assert_allclose(r[name], st(ref)[toks], rtol=1e-10, atol=1e-12, err_msg=name)
+    for name, ref in (("lse_sel", l_sel), ("lse_slide", l_sl), ("lse_cmp", l_cmp)):
+        np.testing.assert_allclose(r[name], ref[:, toks], rtol=1e-10, atol=1e-12, err_msg=name)
+    np.testing.assert_allclose(r["dQ"], st(g_sel[0] + g_sl[0])[toks], rtol=1e-9, atol=1e-12)
+    for kh, i in ((0, 0), (1, 7), (1, 31)):
+        dK, dV = O.block_grads(i, kh, lambda ts: Qs[ts], Ks, Vs, lambda ts: dOs[ts], tau, idx[kh], c)
+        sl = slice(i * c.B_K, (i + 1) * c.B_K)
+        np.testing.assert_allclose(dK, (g_sel[1] + g_sl[1])[sl, :, kh], rtol=1e-9, atol=1e-12)
+        np.testing.assert_allclose(dV, (g_sel[2] + g_sl[2])[sl, :, kh], rtol=1e-9, atol=1e-12)
