@@ -206,9 +206,9 @@ int cmp_fwd_impl(const fsa_shape* s, const void* Q, const void* Kc, const void* 
         ntok);
   FSA_LAUNCH_CHECK("cmp_attn_fwd");
   if (tc) {
-    const bool fused = scores != nullptr && tc_cmp_scores_fused(*s);
-    int rc = tc_cmp_fwd(s, Q, Kc, Vc, out, lse, fused ? scores : nullptr, workspace, st);
-    if (rc || fused || scores == nullptr) return rc;
+    // scores for the formed blocks come from the tensor cores for every g:
+    // fused into this pass when g divides 32, else a group-summed-query pass
+    return tc_cmp_fwd(s, Q, Kc, Vc, out, lse, scores, workspace, st);
   }
   if (scores) {
     return fsa_importance_scores(s, dt, Q, Kc, scores, st);

@@ -103,102 +103,175 @@ __device__ __forceinline__ uint32_t score_key32(float f) {
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
-// f32 scores, b <= 32 * PER, T <= 32: one warp per (kh, t) row, the row's
-// causal candidates held in registers (candidate c = k * 32 + lane in
-// register k), and the T-th best key found by an exact 4-pass 8-bit radix
-// select over a per-warp shared-memory histogram.  Then
-//   selected = {key > kth} + the lowest-index (need) candidates with key == kth,
-// which is exactly the first T of the stable (score desc, index asc) order.
-// The ascending output falls out of a ballot compaction in index order.
-template <int PER>
-__global__ void __launch_bounds__(256) topk_radix_kernel(const float* __restrict__ scores,
-                                                         int32_t* __restrict__ idx, int64_t rows,
-                                                         int64_t N, int64_t B_K, int64_t b, int T) {
-  __shared__ uint32_t hist_all[8][256];
+// f32 scores, T <= 32, any b: one warp per (kh, t) row, streaming over the
+// row's causal candidates 32 at a time (few registers -> full occupancy):
+//   pass 1: count the selectable keys and take each lane's maximum; with
+//           <= T selectable the answer is all of them (index order);
+//   theta = the T-th largest lane maximum, a lower bound of the T-th best
+//           key (T lanes hold a key >= theta), so the answer lies among the
+//           keys >= theta;
+//   pass 2: collect those (typically ~T..2T) as (key, index) into shared
+//           memory and sort them exactly (warp bitonic, key desc / index
+//           asc): the first T are the selection -- exactly the first T of the
+//           reference's stable (score desc, index asc) order;
+//   fallback (> 64 candidates): an exact 4-pass 8-bit radix select of the
+//           T-th key, then an index-order compaction.
+// Output ascending, -1 padded (selection.py:78-102).
+__global__ void __launch_bounds__(256) topk_stream_kernel(const float* __restrict__ scores,
+                                                          int32_t* __restrict__ idx, int64_t rows,
+                                                          int64_t N, int64_t B_K, int64_t b, int T) {
+  __shared__ __align__(16) uint32_t smem_all[8][256];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t row = blockIdx.x * 8ll + wib;
   if (row >= rows) return;
-  uint32_t* hist = hist_all[wib];
+  uint32_t* hist = smem_all[wib];
   const int64_t t = row % N;
   const int own = (int)(t / B_K), ncand = own + 1;
   const float* sr = scores + row * b;
-  uint32_t key[PER];
-#pragma unroll
-  for (int k = 0; k < PER; ++k) {
-    const int c = k * 32 + lane;
-    key[k] = c < ncand ? (c == own ? 0xFF800000u : score_key32(__ldg(sr + c))) : 0u;
-  }
+  int32_t* dst = idx + row * T;
+  const unsigned lt = (1u << lane) - 1u;
+  auto keyat = [&](int c) -> uint32_t {
+    return c < ncand ? (c == own ? 0xFF800000u : score_key32(__ldg(sr + c))) : 0u;
+  };
+  // ---- pass 1
   int nsel = 0;
+  uint32_t lm = 0u;
+  for (int base = 0; base < ncand; base += 32) {
+    const uint32_t k = keyat(base + lane);
+    nsel += __popc(__ballot_sync(0xffffffffu, k != 0u));
+    lm = max(lm, k);
+  }
+  if (nsel <= T) {
+    int out = 0;
+    for (int base = 0; base < ncand; base += 32) {
+      const uint32_t k = keyat(base + lane);
+      const unsigned m = __ballot_sync(0xffffffffu, k != 0u);
+      if (k != 0u) dst[out + __popc(m & lt)] = base + lane;
+      out += __popc(m);
+    }
+    if (lane >= out && lane < T) dst[lane] = -1;
+    return;
+  }
+  // ---- theta: T-th largest lane maximum (warp bitonic, descending)
 #pragma unroll
-  for (int k = 0; k < PER; ++k) nsel += __popc(__ballot_sync(0xffffffffu, key[k] != 0u));
-  uint32_t kth = 1u;  // keys >= kth are candidates for selection
-  int need = 0;       // how many keys == kth to take (lowest index first)
-  if (nsel > T) {
-    uint32_t prefix = 0u, pmask = 0u;
-    need = T;
-#pragma unroll 1
-    for (int shift = 24; shift >= 0; shift -= 8) {
+  for (int kk = 2; kk <= 32; kk <<= 1) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) hist[lane * 8 + q] = 0u;
-      __syncwarp();
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      const uint32_t y = __shfl_xor_sync(0xffffffffu, lm, j);
+      const bool take_max = ((lane & j) == 0) == ((lane & kk) == 0);
+      lm = take_max ? max(lm, y) : min(lm, y);
+    }
+  }
+  const uint32_t theta = max(__shfl_sync(0xffffffffu, lm, T - 1), 1u);
+  // ---- pass 2: candidates >= theta, packed so that larger = better
+  unsigned long long* slots = reinterpret_cast<unsigned long long*>(hist);
+  int cand = 0;
+  for (int base = 0; base < ncand; base += 32) {
+    const uint32_t k = keyat(base + lane);
+    const bool c = k >= theta;
+    const unsigned m = __ballot_sync(0xffffffffu, c);
+    const int pos = cand + __popc(m & lt);
+    if (c && pos < 64)
+      slots[pos] = ((unsigned long long)k << 32) | (0xFFFFFFFFu - (uint32_t)(base + lane));
+    cand += __popc(m);
+  }
+  __syncwarp();
+  if (cand <= 64) {
+    unsigned long long x0 = lane < cand ? slots[lane] : 0ull;
+    unsigned long long x1 = lane + 32 < cand ? slots[lane + 32] : 0ull;
 #pragma unroll
-      for (int k = 0; k < PER; ++k)
-        if (key[k] != 0u && (key[k] & pmask) == prefix) atomicAdd(&hist[(key[k] >> shift) & 255u], 1u);
-      __syncwarp();
-      // lane L owns digits 255 - 8L .. 248 - 8L (descending); inclusive scan
-      uint32_t cnt[8], tot = 0;
+    for (int kk = 2; kk <= 64; kk <<= 1) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        cnt[q] = hist[255 - lane * 8 - q];
-        tot += cnt[q];
-      }
-      uint32_t incl = tot;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      const uint32_t excl = incl - tot;
-      const unsigned hit = __ballot_sync(0xffffffffu, excl < (uint32_t)need && incl >= (uint32_t)need);
-      const int src = __ffs(hit) - 1;
-      uint32_t digit = 0u, above = 0u;
-      if (lane == src) {
-        uint32_t run = excl;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          if (run + cnt[q] >= (uint32_t)need) {
-            digit = 255u - (uint32_t)(lane * 8 + q);
-            above = run;
-            break;
-          }
-          run += cnt[q];
+      for (int j = kk >> 1; j > 0; j >>= 1) {
+        if (j == 32) {  // partner in the same lane (only at kk = 64)
+          const unsigned long long hi = max(x0, x1), lo = min(x0, x1);
+          x0 = hi;
+          x1 = lo;
+        } else {
+          const unsigned long long y0 = __shfl_xor_sync(0xffffffffu, x0, j);
+          const unsigned long long y1 = __shfl_xor_sync(0xffffffffu, x1, j);
+          const bool lower = (lane & j) == 0;
+          const bool d0 = (lane & kk) == 0, d1 = ((lane + 32) & kk) == 0;
+          x0 = (lower == d0) ? max(x0, y0) : min(x0, y0);
+          x1 = (lower == d1) ? max(x1, y1) : min(x1, y1);
         }
       }
-      digit = __shfl_sync(0xffffffffu, digit, src);
-      above = __shfl_sync(0xffffffffu, above, src);
-      need -= (int)above;
-      prefix |= digit << shift;
-      pmask |= 0xFFu << shift;
-      __syncwarp();
     }
-    kth = prefix;
-  }
-  // compaction in ascending index order
-  int taken_eq = 0, out = 0;
-  const unsigned lt = (1u << lane) - 1u;
-  int32_t* dst = idx + row * T;
+    // the first T (T <= 32: lanes 0..T-1 of x0) are the selection; ascending index order
+    int v = lane < T ? (int)(0xFFFFFFFFu - (uint32_t)x0) : 0x7fffffff;
 #pragma unroll
-  for (int k = 0; k < PER; ++k) {
-    const bool eq = nsel > T && key[k] == kth;
+    for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+      for (int j = kk >> 1; j > 0; j >>= 1) {
+        const int y = __shfl_xor_sync(0xffffffffu, v, j);
+        const bool take_min = ((lane & j) == 0) == ((lane & kk) == 0);
+        v = take_min ? min(v, y) : max(v, y);
+      }
+    }
+    if (lane < T) dst[lane] = v;
+    return;
+  }
+  __syncwarp();
+  // ---- fallback: exact radix select of the T-th key (4 passes of 8 bits)
+  uint32_t prefix = 0u, pmask = 0u;
+  int need = T;
+#pragma unroll 1
+  for (int shift = 24; shift >= 0; shift -= 8) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) hist[lane * 8 + q] = 0u;
+    __syncwarp();
+    for (int base = 0; base < ncand; base += 32) {
+      const uint32_t k = keyat(base + lane);
+      if (k != 0u && (k & pmask) == prefix) atomicAdd(&hist[(k >> shift) & 255u], 1u);
+    }
+    __syncwarp();
+    uint32_t cnt[8], tot = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      cnt[q] = hist[255 - lane * 8 - q];
+      tot += cnt[q];
+    }
+    uint32_t incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const uint32_t excl = incl - tot;
+    const unsigned hit = __ballot_sync(0xffffffffu, excl < (uint32_t)need && incl >= (uint32_t)need);
+    const int src = __ffs(hit) - 1;
+    uint32_t digit = 0u, above = 0u;
+    if (lane == src) {
+      uint32_t run = excl;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (run + cnt[q] >= (uint32_t)need) {
+          digit = 255u - (uint32_t)(lane * 8 + q);
+          above = run;
+          break;
+        }
+        run += cnt[q];
+      }
+    }
+    digit = __shfl_sync(0xffffffffu, digit, src);
+    above = __shfl_sync(0xffffffffu, above, src);
+    need -= (int)above;
+    prefix |= digit << shift;
+    pmask |= 0xFFu << shift;
+    __syncwarp();
+  }
+  const uint32_t kth = prefix;
+  int taken_eq = 0, out = 0;
+  for (int base = 0; base < ncand; base += 32) {
+    const uint32_t k = keyat(base + lane);
+    const bool eq = k == kth;
     const unsigned me = __ballot_sync(0xffffffffu, eq);
-    const bool sel = key[k] != 0u && (key[k] > kth || (eq && taken_eq + __popc(me & lt) < need) ||
-                                      (nsel <= T));
+    const bool sel = k > kth || (eq && taken_eq + __popc(me & lt) < need);
     taken_eq += __popc(me);
     const unsigned ms = __ballot_sync(0xffffffffu, sel);
-    if (sel) dst[out + __popc(ms & lt)] = k * 32 + lane;
+    if (sel) dst[out + __popc(ms & lt)] = base + lane;
     out += __popc(ms);
   }
-  if (lane >= out && lane < T) dst[lane] = -1;
 }
 
 // One CTA per row for T > 32: bitonic sort of all causal candidates in smem.
@@ -297,15 +370,9 @@ int topk_impl(const fsa_shape* s, const void* scores, int32_t* idx, cudaStream_t
   const int64_t b = s->N / s->B_K, rows = s->h_K * s->N;
   const int T = (int)s->T;
   if (rows == 0) return FSA_OK;
-  if (sizeof(S) == 4 && T <= 32 && b <= 1024) {
-    const float* sc = (const float*)scores;
-    const unsigned grid = (unsigned)((rows + 7) / 8);
-    if (b <= 32) topk_radix_kernel<1><<<grid, 256, 0, st>>>(sc, idx, rows, s->N, s->B_K, b, T);
-    else if (b <= 64) topk_radix_kernel<2><<<grid, 256, 0, st>>>(sc, idx, rows, s->N, s->B_K, b, T);
-    else if (b <= 128) topk_radix_kernel<4><<<grid, 256, 0, st>>>(sc, idx, rows, s->N, s->B_K, b, T);
-    else if (b <= 256) topk_radix_kernel<8><<<grid, 256, 0, st>>>(sc, idx, rows, s->N, s->B_K, b, T);
-    else if (b <= 512) topk_radix_kernel<16><<<grid, 256, 0, st>>>(sc, idx, rows, s->N, s->B_K, b, T);
-    else topk_radix_kernel<32><<<grid, 256, 0, st>>>(sc, idx, rows, s->N, s->B_K, b, T);
+  if (sizeof(S) == 4 && T <= 32) {
+    topk_stream_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>((const float*)scores, idx, rows,
+                                                                  s->N, s->B_K, b, T);
   } else if (T <= 32) {
     const int warps = 8;
     topk_warp_kernel<S><<<(unsigned)((rows + warps - 1) / warps), warps * 32, 0, st>>>(

@@ -47,7 +47,10 @@ constexpr uint32_t kIdS = idesc_bf16(128, 64, false, false);
 constexpr uint32_t kIdPV = idesc_bf16(128, 128, false, true);
 constexpr float kRescale = 8.f;  // exp2 units
 
-enum Mode { SLIDE = 0, CMP = 1 };
+// SCORES: importance scores only (no softmax / PV), for group sizes that do not
+// divide 32: run on the group-summed queries Qsum (g = 1) so no cross-warp
+// head reduction is needed; scores = Qsum . K_cmp * score_mul.
+enum Mode { SLIDE = 0, CMP = 1, SCORES = 2 };
 
 struct Params {
   const __nv_bfloat16 *Q, *Kx, *Vx;  // keys/values: K,V [N][h_K][128] or pooled [b][h_K][128]
@@ -55,6 +58,7 @@ struct Params {
   int64_t N, h, h_K, g, W, B_K, b, n_keys, n_super;
   int tpi, mode;
   float scale, scale_log2;
+  float score_mul;  // scale / g of the real head group
 };
 
 struct Sub {
@@ -71,7 +75,7 @@ __device__ __forceinline__ bool super_of(const Params& p, int id, Super& it) {
   if (id >= p.h_K * p.n_super) return false;
   it.kh = id % (int)p.h_K;
   int st = id / (int)p.h_K;
-  if (p.mode == CMP) st = (int)p.n_super - 1 - st;  // heavy (late) tokens first
+  if (p.mode != SLIDE) st = (int)p.n_super - 1 - st;  // heavy (late) tokens first
   it.u0 = INT32_MAX;
   it.u1 = 0;
 #pragma unroll
@@ -195,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const Params p) 
         const int v = (int)(r % kKVStages);
         wait_stage(bar(B_KE + v), (uint32_t)(((r / kKVStages) & 1) ^ 1));
         // 4 gathers (K rows 0-31 / 32-63, V rows 0-31 / 32-63) over 3 warps
-        for (int cidx = warp - 8; cidx < 4; cidx += 3) {
+        for (int cidx = warp - 8; cidx < (p.mode == SCORES ? 2 : 4); cidx += 3) {
           const int row0 = (cidx & 1) * 32;
           const int key = u * 64 + row0 + lane;
           const bool ok = key < p.n_keys;
@@ -270,7 +274,14 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const Params p) 
             if (pu[w] >= s.k0 && pu[w] < s.k1) {
               const int v = (int)(np[w] & 1);
               const bool first = pu[w] == s.k0, last = pu[w] + 1 == s.k1;
-              if (np[w] < ns[w] &&
+              if (p.mode == SCORES) {  // no PV: release the K tile once S is consumed
+                if (np[w] < ns[w] && mbar_test(bar(B_PF + 2 * w + v), (uint32_t)((np[w] >> 1) & 1))) {
+                  mma_commit(bar(B_KE + kv));
+                  ++np[w];
+                  ++pu[w];
+                  progressed = true;
+                }
+              } else if (np[w] < ns[w] &&
                   mbar_test(bar(B_PF + 2 * w + v), (uint32_t)((np[w] >> 1) & 1)) &&
                   (!first || mbar_test(bar(B_OE + w), (uint32_t)((nsub[w] & 1) ^ 1)))) {
                 tc_fence_after();
@@ -345,10 +356,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const Params p) 
         tmem_ld32(tS + 32, sv + 32);
         tmem_wait_ld();
         const int kbase = kt * 64;
-        if (p.mode == CMP && p.scores != nullptr) {
+        if (p.mode != SLIDE && p.scores != nullptr) {
           // group mean over the g heads of this token (rows of a token are
           // adjacent lanes; g divides 32), written by the token's first row
-          const float gm = p.scale / (float)p.g;
+          const float gm = p.score_mul;
           float* dst = p.scores + ((int64_t)c.it.kh * p.N + t) * p.b + kbase;
           const bool wr = ok && hh == 0;
 #pragma unroll
@@ -361,15 +372,21 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const Params p) 
               x3 += __shfl_xor_sync(0xffffffffu, x3, o);
             }
             if (wr) {
-              if (kbase + cc + 3 < p.b) {
+              if (kbase + cc + 3 < p.b && (p.b & 3) == 0) {  // 16 B aligned rows
                 *reinterpret_cast<float4*>(dst + cc) = make_float4(x0 * gm, x1 * gm, x2 * gm, x3 * gm);
               } else {
                 if (kbase + cc < p.b) dst[cc] = x0 * gm;
                 if (kbase + cc + 1 < p.b) dst[cc + 1] = x1 * gm;
                 if (kbase + cc + 2 < p.b) dst[cc + 2] = x2 * gm;
+                if (kbase + cc + 3 < p.b) dst[cc + 3] = x3 * gm;
               }
             }
           }
+        }
+        if (p.mode == SCORES) {  // S consumed: hand the stage back
+          tc_fence_before();
+          mbar_arrive(bar(B_PF + 2 * w + v));
+          continue;
         }
         // rows whose visible range covers the whole tile skip the masking
         const bool full = __all_sync(0xffffffffu, klo <= kbase && kbase + 63 <= khi);
@@ -428,6 +445,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const Params p) 
         tc_fence_before();
         mbar_arrive(bar(B_PF + 2 * w + v));
       }
+      if (p.mode == SCORES) continue;
       // epilogue: out = O / l, lse = m + ln l
       mbar_wait(bar(B_OF + w), (uint32_t)(n_out & 1));
       tc_fence_after();
@@ -495,7 +513,29 @@ Params base_params(const fsa_shape* s) {
   p.n_super = (p.N + 2 * p.tpi - 1) / (2 * p.tpi);
   p.scale = (float)s->scale;
   p.scale_log2 = (float)(s->scale * 1.4426950408889634);
+  p.score_mul = (float)(s->scale / (double)p.g);
   return p;
+}
+
+// Qsum[t][kh][:] = sum of the g query rows of kv head kh (fp32 sum, bf16 out)
+__global__ void qsum_kernel(const __nv_bfloat16* __restrict__ Q, __nv_bfloat16* __restrict__ Qs,
+                            int64_t N, int64_t h_K, int64_t g) {
+  const int64_t row = blockIdx.x * 8ll + (threadIdx.x >> 5);  // (t, kh)
+  if (row >= N * h_K) return;
+  const int lane = threadIdx.x & 31;
+  const __nv_bfloat16* src = Q + row * g * kD + lane * 4;
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  for (int64_t j = 0; j < g; ++j) {
+    const uint2 u = *reinterpret_cast<const uint2*>(src + j * kD);
+    const float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+    const float2 y = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+    a0 += x.x; a1 += x.y; a2 += y.x; a3 += y.y;
+  }
+  const __nv_bfloat162 p0 = __floats2bfloat162_rn(a0, a1), p1 = __floats2bfloat162_rn(a2, a3);
+  uint2 o;
+  o.x = *reinterpret_cast<const uint32_t*>(&p0);
+  o.y = *reinterpret_cast<const uint32_t*>(&p1);
+  *reinterpret_cast<uint2*>(Qs + row * kD + lane * 4) = o;
 }
 
 }  // namespace
@@ -508,6 +548,7 @@ bool tc_cmp_scores_fused(const fsa_shape& s) {
   const int64_t g = s.h / s.h_K;
   return g <= 32 && (32 % g) == 0;
 }
+bool tc_cmp_scores_any_g() { return true; }
 
 int tc_slide_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V, void* out,
                  void* lse, cudaStream_t st) {
@@ -526,7 +567,9 @@ int tc_slide_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V
 }
 
 size_t tc_cmp_workspace_bytes(const fsa_shape* s) {
-  return (size_t)2 * (s->N / s->B_K) * s->h_K * kD * sizeof(__nv_bfloat16);
+  // bf16 pooled K/V, then (for group sizes not dividing 32) the group-summed queries
+  return (size_t)2 * (s->N / s->B_K) * s->h_K * kD * sizeof(__nv_bfloat16) +
+         (size_t)s->N * s->h_K * kD * sizeof(__nv_bfloat16);
 }
 
 int tc_cmp_fwd(const fsa_shape* s, const void* Q, const void* Kc, const void* Vc, void* out,
@@ -544,9 +587,29 @@ int tc_cmp_fwd(const fsa_shape* s, const void* Q, const void* Kc, const void* Vc
   p.n_keys = p.b;
   p.out = (float*)out;
   p.lse = (float*)lse;
-  p.scores = (float*)scores;
+  const bool fused = scores != nullptr && tc_cmp_scores_fused(*s);
+  p.scores = fused ? (float*)scores : nullptr;
   launch(p, st);
   FSA_LAUNCH_CHECK("tc_cmp_fwd");
+  if (scores != nullptr && !fused) {
+    // scores on the tensor cores for any g: the g query rows of a kv head are
+    // summed first, then a g = 1 problem over Qsum computes Qsum . K_cmp
+    __nv_bfloat16* qs = vb + n;
+    qsum_kernel<<<(unsigned)((p.N * p.h_K + 7) / 8), 256, 0, st>>>((const __nv_bfloat16*)Q, qs,
+                                                                    p.N, p.h_K, p.g);
+    Params q = p;
+    q.mode = SCORES;
+    q.Q = qs;
+    q.h = p.h_K;
+    q.g = 1;
+    q.tpi = kRows;
+    q.n_super = (q.N + 2 * q.tpi - 1) / (2 * q.tpi);
+    q.scores = (float*)scores;
+    q.out = nullptr;
+    q.lse = nullptr;
+    launch(q, st);
+    FSA_LAUNCH_CHECK("tc_cmp_scores");
+  }
   return FSA_OK;
 }
 

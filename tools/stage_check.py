@@ -17,18 +17,20 @@ from paper_2508_18224_b200 import kv_major  # noqa: E402
 
 def main():
     stage = sys.argv[1]
-    N = int(sys.argv[2]) if len(sys.argv) > 2 else 2048
+    N = int(sys.argv[2]) if len(sys.argv) > 2 and stage != "shape" else 2048
     g = torch.Generator(device="cuda").manual_seed(0)
     mk = lambda *s: torch.randn(*s, device="cuda", dtype=torch.bfloat16, generator=g)  # noqa: E731
-    if stage == "llama":  # the bench workload: 2 NSA fwd+bwd steps (profile the second)
-        cfg = fsa.make_config(N=32768, d_K=128, d_V=128, h=32, h_K=8, B_K=64, T=16, W=512)
-        q, k, v, do = mk(cfg.N, 32, 128), mk(cfg.N, 8, 128), mk(cfg.N, 8, 128), mk(cfg.N, 32, 128)
+    if stage in ("llama", "shape"):  # 2 NSA fwd+bwd steps (profile the second)
+        # shape: python tools/stage_check.py shape N h h_K
+        NN, hh, hk = (32768, 32, 8) if stage == "llama" else (int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4]))
+        cfg = fsa.make_config(N=NN, d_K=128, d_V=128, h=hh, h_K=hk, B_K=64, T=16, W=512)
+        q, k, v, do = mk(cfg.N, hh, 128), mk(cfg.N, hk, 128), mk(cfg.N, hk, 128), mk(cfg.N, hh, 128)
         tau = torch.rand(cfg.N, 3, device="cuda", generator=g)
         for _ in range(2):
             out, ctx = fsa.nsa_forward(q, k, v, tau, cfg)
             fsa.nsa_backward(ctx, do)
         torch.cuda.synchronize()
-        print("llama ok", flush=True)
+        print(stage, "ok", flush=True)
         return
     cfg = fsa.make_config(N=N, d_K=128, d_V=128, h=8, h_K=2, B_K=64, T=8, W=256)
     q, k, v, do = mk(N, 8, 128), mk(N, 2, 128), mk(N, 2, 128), mk(N, 8, 128)
