@@ -51,6 +51,24 @@ __device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// Warp-uniform probe for issuer warps that run their control flow on all 32
+// lanes (so descriptors stay in uniform registers): true only if every lane
+// saw the phase complete (a late lane just makes the warp retry).
+__device__ __forceinline__ bool mbar_test_warp(uint32_t bar, uint32_t parity) {
+  return __all_sync(0xffffffffu, mbar_test(bar, parity));
+}
+// One lane of a converged warp (elect.sync)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "elect.sync _|P, 0xffffffff;\n"
+      "selp.b32 %0, 1, 0, P;\n"
+      "}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
 // Blocking wait with a watchdog: a wait that has not completed after ~2^34
 // cycles (several seconds) reports the barrier and traps instead of hanging
 // the device (a pipeline bug must not take the GPU down with it).
@@ -147,6 +165,13 @@ __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, ui
       "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// Warp-wide issue helpers: the whole (converged) warp calls them with uniform
+// operands; one elected lane issues.
+__device__ __forceinline__ void mma_bf16_w(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                           uint32_t idesc, uint32_t accumulate);
+__device__ __forceinline__ void mma_bf16_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
+                                              uint32_t idesc, uint32_t accumulate);
+__device__ __forceinline__ void mma_commit_w(uint32_t bar);
 // 32 consecutive 32-bit columns of this thread's TMEM lane <- v
 __device__ __forceinline__ void tmem_st32u(uint32_t taddr, const uint32_t* v) {
   asm volatile(
@@ -168,6 +193,21 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    bar)
                : "memory");
+}
+__device__ __forceinline__ bool elect_one();
+__device__ __forceinline__ void mma_bf16_w(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                           uint32_t idesc, uint32_t accumulate) {
+  if (elect_one()) mma_bf16(d_tmem, adesc, bdesc, idesc, accumulate);
+  __syncwarp();
+}
+__device__ __forceinline__ void mma_bf16_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
+                                              uint32_t idesc, uint32_t accumulate) {
+  if (elect_one()) mma_bf16_ts(d_tmem, a_tmem, bdesc, idesc, accumulate);
+  __syncwarp();
+}
+__device__ __forceinline__ void mma_commit_w(uint32_t bar) {
+  if (elect_one()) mma_commit(bar);
+  __syncwarp();
 }
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");

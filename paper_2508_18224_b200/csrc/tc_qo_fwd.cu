@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const Params p) 
     if (pend) mbar_arrive(pend);
   } else if (warp == 11) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    {  // whole warp: uniform state; one elected lane issues
       // S stream w: for each super item, S tiles [k0_w, k1_w), then one QE
       // commit.  PV stream w: for each union tile r in [u0, u1): PV if r is in
       // the sub-item's range, else a pass-by KE commit (KE counts 2 arrivals).
@@ -245,22 +245,22 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const Params p) 
             if (su[w] < s.k1) {
               const int rr = cs[w].rbase + (su[w] - cs[w].it.u0);
               const int kv = (int)(rr % kKVStages), v = (int)(ns[w] & 1);
-              if (ns[w] < np[w] + 2 && mbar_test(bar(B_QF + qs), qpar) &&
-                  mbar_test(bar(B_KF + kv), (uint32_t)((rr / kKVStages) & 1))) {
+              if (ns[w] < np[w] + 2 && mbar_test_warp(bar(B_QF + qs), qpar) &&
+                  mbar_test_warp(bar(B_KF + kv), (uint32_t)((rr / kKVStages) & 1))) {
                 tc_fence_after();
                 const uint32_t q = sb + kOffQ + (qs * 2 + w) * kQ, k = sb + kOffKV + kv * kKV;
                 const uint32_t tS = tmem + 256u * w + 64u * v;
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk)
-                  mma_bf16(tS, desc_kmajor(q + (kk >> 2) * 16384u + (kk & 3) * 32u),
+                  mma_bf16_w(tS, desc_kmajor(q + (kk >> 2) * 16384u + (kk & 3) * 32u),
                            desc_kmajor(k + (kk >> 2) * 8192u + (kk & 3) * 32u), kIdS, kk > 0);
-                mma_commit(bar(B_SF + 2 * w + v));
+                mma_commit_w(bar(B_SF + 2 * w + v));
                 ++ns[w];
                 ++su[w];
                 progressed = true;
               }
-            } else if (s.k0 < s.k1 || mbar_test(bar(B_QF + qs), qpar)) {
-              mma_commit(bar(B_QE + qs));  // this stream is done with the Q stage
+            } else if (s.k0 < s.k1 || mbar_test_warp(bar(B_QF + qs), qpar)) {
+              mma_commit_w(bar(B_QE + qs));  // this stream is done with the Q stage
               ls[w] = cs[w].advance(p, G);
               su[w] = ls[w] ? cs[w].it.s[w].k0 : 0;
               progressed = true;
@@ -275,34 +275,34 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const Params p) 
               const int v = (int)(np[w] & 1);
               const bool first = pu[w] == s.k0, last = pu[w] + 1 == s.k1;
               if (p.mode == SCORES) {  // no PV: release the K tile once S is consumed
-                if (np[w] < ns[w] && mbar_test(bar(B_PF + 2 * w + v), (uint32_t)((np[w] >> 1) & 1))) {
-                  mma_commit(bar(B_KE + kv));
+                if (np[w] < ns[w] && mbar_test_warp(bar(B_PF + 2 * w + v), (uint32_t)((np[w] >> 1) & 1))) {
+                  mma_commit_w(bar(B_KE + kv));
                   ++np[w];
                   ++pu[w];
                   progressed = true;
                 }
               } else if (np[w] < ns[w] &&
-                  mbar_test(bar(B_PF + 2 * w + v), (uint32_t)((np[w] >> 1) & 1)) &&
-                  (!first || mbar_test(bar(B_OE + w), (uint32_t)((nsub[w] & 1) ^ 1)))) {
+                  mbar_test_warp(bar(B_PF + 2 * w + v), (uint32_t)((np[w] >> 1) & 1)) &&
+                  (!first || mbar_test_warp(bar(B_OE + w), (uint32_t)((nsub[w] & 1) ^ 1)))) {
                 tc_fence_after();
                 const uint32_t vv = sb + kOffKV + kv * kKV + 16384u;
                 const uint32_t tS = tmem + 256u * w + 64u * v, tO = tmem + 256u * w + 128u;
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk)
-                  mma_bf16_ts(tO, tS + kk * 8, desc_mnmajor(vv + kk * 2048u, 8192u), kIdPV,
+                  mma_bf16_ts_w(tO, tS + kk * 8, desc_mnmajor(vv + kk * 2048u, 8192u), kIdPV,
                               (first && kk == 0) ? 0u : 1u);
-                mma_commit(bar(B_KE + kv));
-                mma_commit(bar(B_PV + w));
+                mma_commit_w(bar(B_KE + kv));
+                mma_commit_w(bar(B_PV + w));
                 if (last) {
-                  mma_commit(bar(B_OF + w));
+                  mma_commit_w(bar(B_OF + w));
                   ++nsub[w];
                 }
                 ++np[w];
                 ++pu[w];
                 progressed = true;
               }
-            } else if (mbar_test(bar(B_KF + kv), (uint32_t)((rr / kKVStages) & 1))) {
-              mma_commit(bar(B_KE + kv));  // pass-by: tile not used by this sub-item
+            } else if (mbar_test_warp(bar(B_KF + kv), (uint32_t)((rr / kKVStages) & 1))) {
+              mma_commit_w(bar(B_KE + kv));  // pass-by: tile not used by this sub-item
               ++pu[w];
               progressed = true;
             }

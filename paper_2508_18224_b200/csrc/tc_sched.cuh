@@ -39,6 +39,14 @@ struct Ring {
     mbar_arrive(empty(k));
     return true;
   }
+  // warp-wide non-blocking consumer: all lanes read the slot, one arrives
+  __device__ bool try_consume_warp(int k, int32_t& t) const {
+    if (!mbar_test_warp(full(k), (uint32_t)((k / kRingDepth) & 1))) return false;
+    t = slots[k & (kRingDepth - 1)];
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(empty(k));
+    return true;
+  }
   // consumer side
   __device__ int32_t consume(int k) const {
     mbar_wait(full(k), (uint32_t)((k / kRingDepth) & 1));

@@ -80,7 +80,7 @@ struct Params {
 
 #define K8_TRACE(item, slot)                                                        \
   do {                                                                              \
-    if (p.trace && blockIdx.x == 0 && (item) < 256) p.trace[(item) * 8 + (slot)] = clock64(); \
+    if (p.trace && blockIdx.x == 0 && (item) < 256) p.trace[(item) * 16 + (slot)] = clock64(); \
   } while (0)
 
 // Rows of a task: the selected mode reads them from the inverse CSR; the
@@ -232,15 +232,17 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
     //   P stream : products of item m (needs the softmax's P/dS of item m).
     // Products never wait for the next item's gather, so a stage is released
     // (and its next gather started) as soon as the softmax is done with it.
-    if (lane == 0) {
+    // The whole warp runs the (warp-uniform) state machine so descriptors live
+    // in uniform registers; one elected lane issues each MMA / commit.
+    {
       const uint32_t tK = tmem + kColDK, tV = tmem + kColDV;
       TaskFifo fifo;
       int ka = 0, a_c = 0, a_n = 0;  // ring index, item in task, items in task
-      int64_t a_kseq = -1, ns = 0;   // K/V sequence of the S stream, next S item
+      int a_kseq = -1, ns = 0;       // K/V sequence of the S stream, next S item
       bool a_done = false;
       TaskRows b_tr{};
       int b_c = 0;
-      int64_t kseq_b = -1, np = 0;   // next products item
+      int kseq_b = -1, np = 0;       // next products item
       long long idle_since = 0;
       for (;;) {
         bool progressed = false;
@@ -249,7 +251,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
           bool have = a_c < a_n;
           while (!have) {
             int32_t t;
-            if (!ring.try_consume(ka, t)) break;
+            if (!ring.try_consume_warp(ka, t)) break;
             ++ka;
             if (t < 0) {
               a_done = true;
@@ -264,25 +266,28 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
             have = true;
           }
           if (have) {
-            const int s = (int)(ns & 1);
-            if (mbar_test(bar(B_KVF), (uint32_t)(a_kseq & 1)) &&
-                mbar_test(bar(B_QDF + s), (uint32_t)((ns >> 1) & 1)) &&
-                mbar_test(bar(B_SDE + ns % kTStages), (uint32_t)(((ns / kTStages) & 1) ^ 1))) {
+            const int s = ns & 1, tm = ns % kTStages;
+            if (mbar_test_warp(bar(B_KVF), (uint32_t)(a_kseq & 1)) &&
+                mbar_test_warp(bar(B_QDF + s), (uint32_t)((ns >> 1) & 1)) &&
+                mbar_test_warp(bar(B_SDE + tm), (uint32_t)(((ns / kTStages) & 1) ^ 1))) {
               tc_fence_after();
               const uint32_t q = sb + kOffQ + s * kTile, o = sb + kOffDO + s * kTile;
-              const uint32_t tS = tmem + 128u * (uint32_t)(ns % kTStages);
+              const uint32_t tS = tmem + 128u * (uint32_t)tm;
+              if (elect_one()) {
 #pragma unroll
-              for (int k = 0; k < 8; ++k) {
-                const uint32_t ko = (k >> 2) * 16384u + (k & 3) * 32u, kk = (k >> 2) * 8192u + (k & 3) * 32u;
-                mma_bf16(tS, desc_kmajor(q + ko), desc_kmajor(sb + kOffK + kk), kIdS, k > 0);
-              }
+                for (int k = 0; k < 8; ++k) {
+                  const uint32_t ko = (k >> 2) * 16384u + (k & 3) * 32u, kk = (k >> 2) * 8192u + (k & 3) * 32u;
+                  mma_bf16(tS, desc_kmajor(q + ko), desc_kmajor(sb + kOffK + kk), kIdS, k > 0);
+                }
 #pragma unroll
-              for (int k = 0; k < 8; ++k) {
-                const uint32_t ko = (k >> 2) * 16384u + (k & 3) * 32u, kk = (k >> 2) * 8192u + (k & 3) * 32u;
-                mma_bf16(tS + 64, desc_kmajor(o + ko), desc_kmajor(sb + kOffV + kk), kIdS, k > 0);
+                for (int k = 0; k < 8; ++k) {
+                  const uint32_t ko = (k >> 2) * 16384u + (k & 3) * 32u, kk = (k >> 2) * 8192u + (k & 3) * 32u;
+                  mma_bf16(tS + 64, desc_kmajor(o + ko), desc_kmajor(sb + kOffV + kk), kIdS, k > 0);
+                }
+                mma_commit(bar(B_SDF + tm));
+                K8_TRACE(ns, 1);  // S/dP issued
               }
-              mma_commit(bar(B_SDF + ns % kTStages));
-              K8_TRACE(ns, 1);  // S/dP issued
+              __syncwarp();
               ++a_c;
               ++ns;
               progressed = true;
@@ -292,9 +297,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
         // ---- P stream
         if (np < ns) {
           const bool first = np == 0 || b_c + 1 >= b_tr.nitems;
-          const int s = (int)(np & 1);
-          const bool ready = mbar_test(bar(B_PDF + s), (uint32_t)((np >> 1) & 1)) &&
-                             (!first || mbar_test(bar(B_KAE), (uint32_t)(((kseq_b + 1) & 1) ^ 1)));
+          const int s = np & 1, tm = np % kTStages;
+          const bool ready = mbar_test_warp(bar(B_PDF + s), (uint32_t)((np >> 1) & 1)) &&
+                             (!first || mbar_test_warp(bar(B_KAE), (uint32_t)(((kseq_b + 1) & 1) ^ 1)));
           if (ready) {
             if (first) {
               b_tr = rows_of(p, fifo.pop());
@@ -307,27 +312,31 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
             tc_fence_after();
             const uint32_t q = sb + kOffQ + s * kTile, o = sb + kOffDO + s * kTile;
             const uint32_t pp = sb + kOffP + s * 16384u, ds = sb + kOffDS + s * 16384u;
+            if (elect_one()) {
+              K8_TRACE(np, 8);  // products ready (seen by the MMA warp)
 #pragma unroll
-            for (int k = 0; k < 8; ++k)
-              mma_bf16(tV, desc_mnmajor(o + k * 2048u, 16384u), desc_mnmajor(pp + k * 2048u, 8192u),
-                       kIdKV, (first && k == 0) ? 0u : 1u);
+              for (int k = 0; k < 8; ++k)
+                mma_bf16(tV, desc_mnmajor(o + k * 2048u, 16384u), desc_mnmajor(pp + k * 2048u, 8192u),
+                         kIdKV, (first && k == 0) ? 0u : 1u);
 #pragma unroll
-            for (int k = 0; k < 8; ++k)
-              mma_bf16(tK, desc_mnmajor(q + k * 2048u, 16384u), desc_mnmajor(ds + k * 2048u, 8192u),
-                       kIdKV, (first && k == 0) ? 0u : 1u);
-            if (!p.no_dq) {
+              for (int k = 0; k < 8; ++k)
+                mma_bf16(tK, desc_mnmajor(q + k * 2048u, 16384u), desc_mnmajor(ds + k * 2048u, 8192u),
+                         kIdKV, (first && k == 0) ? 0u : 1u);
+              if (!p.no_dq) {
 #pragma unroll
-              for (int k = 0; k < 4; ++k)
-                mma_bf16(tmem + 128u * (uint32_t)(np % kTStages), desc_kmajor(ds + k * 32u),
-                         desc_mnmajor(sb + kOffK + k * 2048u, 8192u), kIdQ, k > 0);
+                for (int k = 0; k < 4; ++k)
+                  mma_bf16(tmem + 128u * (uint32_t)tm, desc_kmajor(ds + k * 32u),
+                           desc_mnmajor(sb + kOffK + k * 2048u, 8192u), kIdQ, k > 0);
+              }
+              mma_commit(bar(B_DQF + tm));
+              K8_TRACE(np, 4);  // products issued
+              mma_commit(bar(B_QDE + s));
+              if (last) {
+                mma_commit(bar(B_KAF));
+                mma_commit(bar(B_KVE));
+              }
             }
-            mma_commit(bar(B_DQF + np % kTStages));
-            K8_TRACE(np, 4);  // products issued
-            mma_commit(bar(B_QDE + s));
-            if (last) {
-              mma_commit(bar(B_KAF));
-              mma_commit(bar(B_KVE));
-            }
+            __syncwarp();
             ++np;
             progressed = true;
           }
@@ -472,6 +481,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
         }
         fence_proxy_async();
         mbar_arrive(bar(B_PDF + s));
+        if (lane == 0) K8_TRACE(n, 9 + (warp & 3));  // P/dS written by this warp
         if (r == 0) K8_TRACE(n, 3);  // P/dS written
         // products of this item landed -> dQ partial out of TMEM; stage the
         // bf16 rows in this wg's (now consumed) P buffer for coalesced stores

@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const Params p)
     // S = Q K^T of item m needs its gather, the task's K/V stage and a free S
     // TMEM stage; O = P V of item m needs the softmax's P.  PV never waits for
     // the next item's gather.
-    if (lane == 0) {
+    {  // whole warp: uniform state; one elected lane issues
       const uint32_t tS = tmem, tO = tmem + 128;
       TaskFifo fifo;
       int ka = 0, a_c = 0, a_n = 0, a_kseq = -1, ns = 0;
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const Params p)
           bool have = a_c < a_n;
           while (!have) {
             int32_t t;
-            if (!ring.try_consume(ka, t)) break;
+            if (!ring.try_consume_warp(ka, t)) break;
             ++ka;
             if (t < 0) {
               a_done = true;
@@ -192,18 +192,21 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const Params p)
           }
           if (have) {
             const int s = ns % kQStages, v = ns & 1, kvs = a_kseq & 1;
-            if (mbar_test(bar(B_KVF + kvs), (uint32_t)((a_kseq >> 1) & 1)) &&
-                mbar_test(bar(B_QF + s), (uint32_t)((ns / kQStages) & 1)) &&
-                mbar_test(bar(B_SE + v), (uint32_t)(((ns >> 1) & 1) ^ 1))) {
+            if (mbar_test_warp(bar(B_KVF + kvs), (uint32_t)((a_kseq >> 1) & 1)) &&
+                mbar_test_warp(bar(B_QF + s), (uint32_t)((ns / kQStages) & 1)) &&
+                mbar_test_warp(bar(B_SE + v), (uint32_t)(((ns >> 1) & 1) ^ 1))) {
               tc_fence_after();
               const uint32_t qa = sb + kOffQ + s * kQBytes;
               const uint32_t ka_ = sb + kOffKV + kvs * kKVBytes;
+              if (elect_one()) {
 #pragma unroll
-              for (int k = 0; k < 8; ++k)
-                mma_bf16(tS + v * 64, desc_kmajor(qa + (k >> 2) * 16384u + (k & 3) * 32u),
-                         desc_kmajor(ka_ + (k >> 2) * 8192u + (k & 3) * 32u), kIdescS, k > 0);
-              mma_commit(bar(B_SF + v));
-              mma_commit(bar(B_QE + s));
+                for (int k = 0; k < 8; ++k)
+                  mma_bf16(tS + v * 64, desc_kmajor(qa + (k >> 2) * 16384u + (k & 3) * 32u),
+                           desc_kmajor(ka_ + (k >> 2) * 8192u + (k & 3) * 32u), kIdescS, k > 0);
+                mma_commit(bar(B_SF + v));
+                mma_commit(bar(B_QE + s));
+              }
+              __syncwarp();
               ++a_c;
               ++ns;
               progressed = true;
@@ -212,8 +215,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const Params p)
         }
         if (np < ns) {
           const int v = np & 1;
-          if (mbar_test(bar(B_PF + v), (uint32_t)((np >> 1) & 1)) &&
-              mbar_test(bar(B_OE + v), (uint32_t)(((np >> 1) & 1) ^ 1))) {
+          if (mbar_test_warp(bar(B_PF + v), (uint32_t)((np >> 1) & 1)) &&
+              mbar_test_warp(bar(B_OE + v), (uint32_t)(((np >> 1) & 1) ^ 1))) {
             if (np == 0 || b_c + 1 >= b_tr.nitems) {
               b_tr = task_rows(fifo.pop(), p.offsets, p.b, p.tpi);
               b_c = 0;
@@ -225,13 +228,16 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const Params p)
             const int kvs = b_kseq & 1;
             tc_fence_after();
             const uint32_t va = sb + kOffKV + kvs * kKVBytes + 16384u;
+            if (elect_one()) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              mma_bf16_ts(tO + v * 128, tmem + kColP + v * 32 + k * 8,
-                          desc_mnmajor(va + k * 2048u, 8192u), kIdescPV, k > 0);
-            mma_commit(bar(B_OF + v));
-            mma_commit(bar(B_PE + v));
-            if (last) mma_commit(bar(B_KVE + kvs));
+              for (int k = 0; k < 4; ++k)
+                mma_bf16_ts(tO + v * 128, tmem + kColP + v * 32 + k * 8,
+                            desc_mnmajor(va + k * 2048u, 8192u), kIdescPV, k > 0);
+              mma_commit(bar(B_OF + v));
+              mma_commit(bar(B_PE + v));
+              if (last) mma_commit(bar(B_KVE + kvs));
+            }
+            __syncwarp();
             ++np;
             progressed = true;
           }

@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const Params p
     // S stream w: S/dP of each tile of sub-item w (single TMEM stage: the next
     // S/dP only after this wg's previous dQ product was issued), then a QE
     // commit.  D stream w: per union tile, dQ += dS K or a pass-by KE commit.
-    if (lane == 0) {
+    {  // whole warp: uniform state; one elected lane issues
       Cursor cs[2], cd[2];
       bool ls[2], ld[2];
       int su[2], du[2];
@@ -207,27 +207,27 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const Params p
             if (su[w] < s.k1) {
               const int rr = cs[w].rbase + (su[w] - cs[w].it.u0);
               const int kv = rr % kKVStages;
-              if (ns[w] == nd[w] && mbar_test(bar(B_QF), qpar) &&
-                  mbar_test(bar(B_KF + kv), (uint32_t)((rr / kKVStages) & 1))) {
+              if (ns[w] == nd[w] && mbar_test_warp(bar(B_QF), qpar) &&
+                  mbar_test_warp(bar(B_KF + kv), (uint32_t)((rr / kKVStages) & 1))) {
                 tc_fence_after();
                 const uint32_t q = sb + kOffQ + w * kT, o = sb + kOffQ + (2 + w) * kT;
                 const uint32_t k = sb + kOffKV + kv * kKV, vv = k + 16384u;
                 const uint32_t tS = tmem + 256u * w;
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk)
-                  mma_bf16(tS, desc_kmajor(q + (kk >> 2) * 16384u + (kk & 3) * 32u),
+                  mma_bf16_w(tS, desc_kmajor(q + (kk >> 2) * 16384u + (kk & 3) * 32u),
                            desc_kmajor(k + (kk >> 2) * 8192u + (kk & 3) * 32u), kIdS, kk > 0);
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk)
-                  mma_bf16(tS + 64, desc_kmajor(o + (kk >> 2) * 16384u + (kk & 3) * 32u),
+                  mma_bf16_w(tS + 64, desc_kmajor(o + (kk >> 2) * 16384u + (kk & 3) * 32u),
                            desc_kmajor(vv + (kk >> 2) * 8192u + (kk & 3) * 32u), kIdS, kk > 0);
-                mma_commit(bar(B_SF + w));
+                mma_commit_w(bar(B_SF + w));
                 ++ns[w];
                 ++su[w];
                 progressed = true;
               }
-            } else if (s.k0 < s.k1 || mbar_test(bar(B_QF), qpar)) {
-              mma_commit(bar(B_QE));
+            } else if (s.k0 < s.k1 || mbar_test_warp(bar(B_QF), qpar)) {
+              mma_commit_w(bar(B_QE));
               ls[w] = cs[w].advance(p, G);
               su[w] = ls[w] ? cs[w].it.s[w].k0 : 0;
               progressed = true;
@@ -239,26 +239,26 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const Params p
             const int kv = rr % kKVStages;
             if (du[w] >= s.k0 && du[w] < s.k1) {
               const bool first = du[w] == s.k0, last = du[w] + 1 == s.k1;
-              if (nd[w] < ns[w] && mbar_test(bar(B_PF + w), (uint32_t)(nd[w] & 1)) &&
-                  (!first || mbar_test(bar(B_OE + w), (uint32_t)((nsub[w] & 1) ^ 1)))) {
+              if (nd[w] < ns[w] && mbar_test_warp(bar(B_PF + w), (uint32_t)(nd[w] & 1)) &&
+                  (!first || mbar_test_warp(bar(B_OE + w), (uint32_t)((nsub[w] & 1) ^ 1)))) {
                 tc_fence_after();
                 const uint32_t k = sb + kOffKV + kv * kKV;
                 const uint32_t tS = tmem + 256u * w, tQ = tmem + 256u * w + 128u;
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk)
-                  mma_bf16_ts(tQ, tS + kk * 8, desc_mnmajor(k + kk * 2048u, 8192u), kIdQ,
+                  mma_bf16_ts_w(tQ, tS + kk * 8, desc_mnmajor(k + kk * 2048u, 8192u), kIdQ,
                               (first && kk == 0) ? 0u : 1u);
-                mma_commit(bar(B_KE + kv));
+                mma_commit_w(bar(B_KE + kv));
                 if (last) {
-                  mma_commit(bar(B_OF + w));
+                  mma_commit_w(bar(B_OF + w));
                   ++nsub[w];
                 }
                 ++nd[w];
                 ++du[w];
                 progressed = true;
               }
-            } else if (mbar_test(bar(B_KF + kv), (uint32_t)((rr / kKVStages) & 1))) {
-              mma_commit(bar(B_KE + kv));
+            } else if (mbar_test_warp(bar(B_KF + kv), (uint32_t)((rr / kKVStages) & 1))) {
+              mma_commit_w(bar(B_KE + kv));
               ++du[w];
               progressed = true;
             }

@@ -21,7 +21,7 @@ def main():
     out, ctx = nsa.nsa_forward(q, k, v, tau, cfg)
     nsa.nsa_backward(ctx, do)
     torch.cuda.synchronize()
-    buf = torch.zeros(256 * 8, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(256 * 16, dtype=torch.int64, device="cuda")
     lib = _lib.lib()
     lib.fsa_debug_bwd_trace(ctypes.c_void_p(buf.data_ptr()))
     if mode == "sel":
@@ -31,15 +31,15 @@ def main():
         nsa.nsa_backward(ctx, do)  # selected then sliding launch: the sliding one overwrites
     torch.cuda.synchronize()
     lib.fsa_debug_bwd_trace(None)
-    t = buf.view(256, 8).cpu()
+    t = buf.view(256, 16).cpu()
     if mode == "sel":
         pass
     t0 = int(t[0, 0])
-    names = ["gather", "sdp_iss", "sdp_land", "pds_done", "prod_iss", "prod_land", "dq_tmem", "dq_store"]
+    names = ["gather", "sdp_iss", "sdp_land", "pds_done", "prod_iss", "prod_land", "dq_tmem", "dq_store", "prod_rdy", "pds_w0", "pds_w1", "pds_w2", "pds_w3"]
     print("item " + " ".join(f"{n:>9}" for n in names) + "   (cycles from item 0 gather)")
     prev = None
     for i in range(0, 120):
-        row = [int(t[i, j]) - t0 if int(t[i, j]) else -1 for j in range(8)]
+        row = [int(t[i, j]) - t0 if int(t[i, j]) else -1 for j in range(13)]
         print(f"{i:4d} " + " ".join(f"{x:9d}" for x in row))
 
 
