@@ -124,8 +124,6 @@ def run_ours(args, rank, world, local_rank):
             dist.barrier()
 
     # per-step timing of the dominant kernel (K5) on the launching stream
-    orig_partials = nsa._sel_partials
-
     def step():
         out, ctx = nsa.nsa_forward(q, k, v, tau, cfg)
         grads = nsa.nsa_backward(ctx, dout)
@@ -153,31 +151,36 @@ def run_ours(args, rank, world, local_rank):
     except Exception as exc:  # pragma: no cover
         kernel_names = {"profiler_error": str(exc)[:120]}
 
-    # K5 is timed inside the same loop with CUDA events on the launching stream
+    # The tensor-core kernels are timed inside the same loop with CUDA events
+    # on the launching stream: the C-ABI entry points are wrapped so that each
+    # fsa_sel_fwd (K5) / fsa_sel_bwd (K8, selected branch) launch is bracketed.
     sampler = ClockSampler(local_rank)
     barrier()
     torch.cuda.synchronize()
     sampler.start()
     start = torch.cuda.Event(enable_timing=True)
     stop = torch.cuda.Event(enable_timing=True)
-    k5s = []
+    kev = {"fsa_sel_fwd": [], "fsa_sel_bwd": []}
+    orig_call = _lib.call
 
-    def timed_partials(cfg_, dt_, q_, k_, v_, inv_):
+    def timed_call(name, *a):
+        if name not in kev:
+            return orig_call(name, *a)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        res = orig_partials(cfg_, dt_, q_, k_, v_, inv_)
+        r = orig_call(name, *a)
         e1.record()
-        k5s.append((e0, e1, inv_))
-        return res
+        kev[name].append((e0, e1))
+        return r
 
-    nsa._sel_partials = timed_partials
+    _lib.call = timed_call
     start.record()
     for _ in range(args.steps):
-        step()
+        out_, grads_, ctx_ = step()
     stop.record()
     torch.cuda.synchronize()
-    nsa._sel_partials = orig_partials
+    _lib.call = orig_call
     clocks = sampler.stop()
     ms = start.elapsed_time(stop) / args.steps
     if world > 1:
@@ -185,11 +188,13 @@ def run_ours(args, rank, world, local_rank):
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    k5_ms = statistics.median(e0.elapsed_time(e1) for e0, e1, _ in k5s)
-    inv = k5s[-1][2]
+    k5_ms = statistics.median(e0.elapsed_time(e1) for e0, e1 in kev["fsa_sel_fwd"])
+    k8_ms = statistics.median(e0.elapsed_time(e1) for e0, e1 in kev["fsa_sel_bwd"])
+    inv = ctx_.inv
     nnz = int(inv.offsets[:, -1].to(torch.int64).sum())
     R = nnz * cfg.g
     k5_flops = 4.0 * cfg.d_K * cfg.B_K * R
+    k8_flops = 10.0 * cfg.d_K * cfg.B_K * R
 
     # ---- end to end through the public API: pinned host inputs in, out + grads
     # (bf16, the input dtype) back to pinned host memory, every step.  Copies
@@ -265,17 +270,24 @@ def run_ours(args, rank, world, local_rank):
     hbm, pk_burst, pk_sus, pk_src = _peaks()
     tokens = world * cfg.N
     value = tokens / (ms / 1e3)
-    sel_fwd_flops = k5_flops
     step_flops = (4.0 + 10.0) * cfg.d_K * cfg.B_K * R  # selected fwd + bwd
     slide_pairs = sum(min(t + 1, cfg.W) for t in range(cfg.N))
     step_flops += (4.0 + 10.0) * cfg.d_K * cfg.h * slide_pairs
     step_flops += 4.0 * cfg.d_K * cfg.h * sum((t + 1) // cfg.B_K for t in range(cfg.N))
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "k5_traffic.json")) as fh:
-            traffic = json.load(fh).get("dram_bytes_per_launch")
+    traffic = {}
+    try:  # dram__bytes_read.sum + dram__bytes_write.sum per launch, from the committed ncu capture
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            traffic = json.load(fh)
     except Exception:
         pass
+
+    def roof(kernel, flops, kms, algo, tkey):
+        ach = flops / (kms / 1e3) / 1e12
+        return {"kernel": kernel, "bound": "tensor", "achieved": round(ach, 2), "peak": pk_sus,
+                "unit": "TFLOP/s", "frac": round(ach / pk_sus, 4),
+                "traffic": traffic.get(tkey), "peak_source": f"{pk_src} sustained bf16",
+                "kernel_ms": round(kms, 4), "share_of_step": round(kms / ms, 4),
+                "algorithmic": algo}
     line = {
         "metric": "NSA fwd+bwd tokens/s (Llama-3-8B attention, 32K, GQA 4)",
         "value": round(value, 1),
@@ -294,13 +306,12 @@ def run_ours(args, rank, world, local_rank):
                    "window": cfg.W, "parallelism": f"batch{world}", "l2": "inputs exceed L2 "
                    "(Q 268 MB, K/V 67 MB each, partial buffer 4.2 GB); no flush"},
         "effective_tflops": round(step_flops / (ms / 1e3) / 1e12, 2),
-        "roofline": {"kernel": "sel_fwd (K5, tcgen05)", "bound": "tensor",
-                     "achieved": round(sel_fwd_flops / (k5_ms / 1e3) / 1e12, 2),
-                     "peak": pk_sus, "unit": "TFLOP/s",
-                     "frac": round(sel_fwd_flops / (k5_ms / 1e3) / 1e12 / pk_sus, 4),
-                     "traffic": traffic, "peak_source": f"{pk_src} sustained bf16",
-                     "k5_ms": round(k5_ms, 4), "k5_share": round(k5_ms / ms, 4),
-                     "algorithmic": "4*d*B_K*R FLOPs, R = (query head, token, block) rows = %d" % R},
+        # dominant kernel: the selected-attention backward (K8)
+        "roofline": roof("sel_bwd (K8, tcgen05, selected branch)", k8_flops, k8_ms,
+                         "10*d*B_K*R FLOPs, R = (query head, token, block) rows = %d" % R,
+                         "tc_sel_bwd_selected"),
+        "roofline_sel_fwd": roof("sel_fwd (K5, tcgen05)", k5_flops, k5_ms,
+                                 "4*d*B_K*R FLOPs, R = %d" % R, "tc_sel_fwd"),
         "e2e": {"value": round(tokens / (e2e_ms / 1e3), 1), "unit": "tokens/s",
                 "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
