@@ -58,6 +58,14 @@ def test_fullsize_nsa_step(name):
     if spec["bwd"]:
         dQ, dK, dV = nsa.nsa_backward(ctx, do)
     torch.cuda.synchronize()
+    # determinism: no floating-point atomics, fixed reduction orders -> a second
+    # run (different dynamic task-to-CTA assignment) is bit-identical
+    out2, ctx2 = nsa.nsa_forward(q, k, v, tau, cfg)
+    assert torch.equal(out2, out) and torch.equal(ctx2.sel.idx, ctx.sel.idx)
+    if spec["bwd"]:
+        for a_, b_ in zip(nsa.nsa_backward(ctx2, do), (dQ, dK, dV)):
+            assert torch.equal(a_, b_), "backward not bit-identical across runs"
+    del out2, ctx2
 
     # ---- selection structure on the whole result
     idx = ctx.sel.idx
