@@ -191,6 +191,13 @@ int fsa_gate_backward(const fsa_shape* s, int dtype, const void* dOut, const voi
                       const void* out_sel, const void* out_slide, void* d_sel, void* d_slide,
                       void* delta_sel, void* delta_slide, void* stream);
 
+/* NSA query-major selected forward (query_major.py:45-69, _core.pyx:134-181):
+ * one task per (kv head, token) over its selected blocks in ascending order,
+ * online softmax; the FSA-vs-NSA comparison baseline (CUDA cores; g <= 16,
+ * d_V <= 256).  out [N][h][d_V], lse [h][N] in acc dtype. */
+int fsa_qm_fwd(const fsa_shape* s, int dtype, const void* Q, const void* K, const void* V,
+               const int32_t* idx, void* out, void* lse, void* stream);
+
 /* Finiteness check for as_headed (config.py:146-155): *flag |= 1 on any non-finite. */
 int fsa_check_finite(int dtype, const void* x, int64_t n, int32_t* flag, void* stream);
 

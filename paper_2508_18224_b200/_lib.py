@@ -65,6 +65,7 @@ SIGNATURES = {
     "fsa_gated_combine": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp], _i),
     "fsa_gate_scale": ([_sp, _i, _vp, _vp, _i, _vp, _vp], _i),
     "fsa_gate_backward": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
+    "fsa_qm_fwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "fsa_check_finite": ([_i, _vp, _i64, _vp, _vp], _i),
 }
 

@@ -423,3 +423,31 @@ def test_tc_sliding_backward_vs_oracle(kw):
     want = O.sliding_backward(Q, K, V, dO, c)
     for g_, w_, name in zip(got, want, ("dQ", "dK", "dV")):
         assert_close(host(g_), w_, "bf16", name, grad=True)
+
+
+# ---------------------------------------------------------------------------
+# NSA query-major baseline (query_major.py:45-69): same outputs as the FSA
+# kv-major path / the oracle, reference meter closed form
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("kw,run_dt", [
+    (dict(N=512, d_K=32, d_V=48, h=8, h_K=2, B_K=16, T=4), "f64"),
+    (dict(N=1024, d_K=64, d_V=64, h=4, h_K=4, B_K=32, T=6), "f32"),
+    (dict(N=2048, d_K=128, d_V=128, h=16, h_K=2, B_K=64, T=8), "bf16"),
+    (dict(N=1024, d_K=128, d_V=128, h=7, h_K=1, B_K=64, T=5), "bf16"),
+])
+def test_query_major_forward_vs_oracle(kw, run_dt):
+    c = O.cfg_of(**kw)
+    cfg = _cfg(kw)
+    Q, K, V = (round_inputs(x, run_dt) for x in O.make_qkv(c, 31))
+    idx = O.select_topk(O.make_scores(c, 31), c)
+    tq, tk, tv = (dev(x, DT[run_dt]) for x in (Q, K, V))
+    res, meter = fsa.query_major.selected_forward(tq, tk, tv, fsa.SelectionTensor(idx), cfg)
+    want_o, want_l = O.selected_forward(Q, K, V, idx, c)
+    assert_close(host(res.out), want_o, run_dt, "qm out")
+    assert_close(host(res.lse), want_l, "f64" if run_dt == "f64" else "f32", "qm lse")
+    ph = meter.phases["query_major"]
+    steps = int((idx != -1).sum())
+    pad = max(c.g, c.min_tile)
+    assert ph.task_count == c.h_K * c.N and ph.inner_iterations == steps
+    assert ph.flops == steps * 2 * pad * c.B_K * (c.d_K + c.d_V)

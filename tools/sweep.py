@@ -54,6 +54,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--nsa", action="store_true",
+                    help="also time the selected branch alone: FSA (kv-major, tcgen05) vs the NSA "
+                         "query-major baseline (query_major.selected_forward)")
     a = ap.parse_args()
     rows = []
     for name, spec, bwd in CONFIGS:
@@ -80,6 +83,15 @@ def main():
             ms = time_it(step, a.steps, a.warmup)
             row.update({"fwd_bwd_ms": round(ms, 3), "fwd_bwd_tflops": round((f_fwd + f_bwd) / ms / 1e9, 1),
                         "fwd_bwd_tokens_s": round(cfg.N / ms * 1e3, 1)})
+        if a.nsa:
+            from paper_2508_18224_b200 import kv_major, query_major
+            L = lambda x: x.permute(0, 2, 1)  # noqa: E731  logical (N, d, h) views
+            sel = ctx.sel
+            row["sel_fwd_fsa_ms"] = round(time_it(
+                lambda: kv_major.selected_forward(L(q), L(k), L(v), sel, cfg), a.steps, a.warmup), 3)
+            row["sel_fwd_nsa_ms"] = round(time_it(
+                lambda: query_major.selected_forward(L(q), L(k), L(v), sel, cfg), a.steps, a.warmup), 3)
+            row["fsa_speedup"] = round(row["sel_fwd_nsa_ms"] / row["sel_fwd_fsa_ms"], 2)
         rows.append(row)
         print(json.dumps(row), flush=True)
         del q, k, v, do, tau, ctx
@@ -89,6 +101,11 @@ def main():
     for r in rows:
         print(f"| {r['config']} | {r['N']} | {r['g']} | {r['fwd_ms']} | {r['fwd_tflops']} | "
               f"{r.get('fwd_bwd_ms', '-')} | {r.get('fwd_bwd_tflops', '-')} | {r.get('fwd_bwd_tokens_s', '-')} |")
+    if a.nsa:
+        print("\n| config | g | selected fwd FSA ms | NSA query-major ms | FSA speed-up |")
+        print("|---|---|---|---|---|")
+        for r in rows:
+            print(f"| {r['config']} | {r['g']} | {r['sel_fwd_fsa_ms']} | {r['sel_fwd_nsa_ms']} | {r['fsa_speedup']}x |")
 
 
 if __name__ == "__main__":
