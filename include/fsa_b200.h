@@ -148,6 +148,12 @@ int fsa_sel_bwd(const fsa_shape* s, int dtype, const void* Q, const void* K, con
 int fsa_dq_reduce(const fsa_shape* s, int dtype, const int32_t* idx, const void* dq_buf,
                   int dqbuf_dtype, void* dQ, void* stream);
 
+/* fsa_dq_reduce plus addend [N][h][d_K] (acc dtype) added to every row in the
+ * same pass: dQ = (ascending-block sum of the dq partials) + addend.  bf16
+ * tensor-core configuration only (the NSA step: selected + sliding dQ). */
+int fsa_dq_reduce_add(const fsa_shape* s, int dtype, const int32_t* idx, const void* dq_buf,
+                      int dqbuf_dtype, const void* addend, void* dQ, void* stream);
+
 /* compressed_attention_forward (branches.py:47-78); scores (nullable) receives
  * importance_scores_from_compressed as a fused epilogue -- on the tensor-core
  * path only for the blocks a token's top-k can read (i < (t+1)//B_K, covered
@@ -167,7 +173,8 @@ int fsa_slide_fwd(const fsa_shape* s, int dtype, const void* Q, const void* K, c
  * The bf16 tensor-core path runs the FSA backward kernel over each KV block's
  * window of tokens and needs fsa_slide_bwd_workspace_bytes of workspace (the
  * per-window-slot dQ partials); accumulate != 0 adds into dQ/dK/dV (sums the
- * sliding branch onto the selected branch's gradients) -- tensor-core path only. */
+ * sliding branch onto the selected branch's gradients) -- tensor-core path only.
+ * accumulate == 2 adds into dK/dV but WRITES dQ (for fsa_dq_reduce_add). */
 size_t fsa_slide_bwd_workspace_bytes(const fsa_shape* s, int dtype);
 int fsa_slide_bwd(const fsa_shape* s, int dtype, const void* Q, const void* K, const void* V,
                   const void* dOut, const void* lse, const void* delta, void* dQ, void* dK,

@@ -57,6 +57,7 @@ SIGNATURES = {
     "fsa_bwd_delta": ([_sp, _i, _vp, _vp, _vp, _vp], _i),
     "fsa_sel_bwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp], _i),
     "fsa_dq_reduce": ([_sp, _i, _vp, _vp, _i, _vp, _vp], _i),
+    "fsa_dq_reduce_add": ([_sp, _i, _vp, _vp, _i, _vp, _vp, _vp], _i),
     "fsa_cmp_workspace_bytes": ([_sp], _sz),
     "fsa_cmp_attn_fwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "fsa_slide_fwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp], _i),

@@ -36,6 +36,7 @@ struct Combine {
   __nv_bfloat16* out;
 };
 
+template <int TMAX>  // >= T: partial rows held in registers
 __global__ void __launch_bounds__(256) merge_bf16_kernel(
     const int32_t* __restrict__ idx, const __nv_bfloat16* __restrict__ obuf,
     const float2* __restrict__ ml, float* __restrict__ out, float* __restrict__ lse,
@@ -51,9 +52,9 @@ __global__ void __launch_bounds__(256) merge_bf16_kernel(
   const __nv_bfloat16* src = obuf + rb * kD + lane * 4;
   // every partial row of this (head, token) is requested before the slot
   // statistics are reduced: one memory latency per warp, not two
-  uint2 raw[32];
+  uint2 raw[TMAX];
 #pragma unroll
-  for (int s = 0; s < 32; ++s)
+  for (int s = 0; s < TMAX; ++s)
     if (s < len) raw[s] = __ldcs(reinterpret_cast<const uint2*>(src + s * kD));
   float2 st = lane < len ? __ldg(ml + rb + lane) : make_float2(-INFINITY, 0.f);
   float cm[4], cs[4], tw[3];
@@ -75,7 +76,7 @@ __global__ void __launch_bounds__(256) merge_bf16_kernel(
   for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-  for (int s = 0; s < 32; ++s) {  // ascending block order
+  for (int s = 0; s < TMAX; ++s) {  // ascending block order
     if (s < len) {
       const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw[s].x));
       const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw[s].y));
@@ -111,7 +112,8 @@ __global__ void __launch_bounds__(256) merge_bf16_kernel(
 
 __global__ void dq_reduce_bf16_kernel(const int32_t* __restrict__ idx,
                                       const __nv_bfloat16* __restrict__ dq, float* __restrict__ dQ,
-                                      int64_t N, int64_t h, int64_t g, int T) {
+                                      int64_t N, int64_t h, int64_t g, int T,
+                                      const float* __restrict__ addend) {
   const int lane = threadIdx.x & 31;
   const int64_t wid = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (wid >= h * N) return;
@@ -132,6 +134,10 @@ __global__ void dq_reduce_bf16_kernel(const int32_t* __restrict__ idx,
     const float4 a = ld_bf16x4(src + s * kD);
     acc.x += a.x; acc.y += a.y; acc.z += a.z; acc.w += a.w;
   }
+  if (addend) {  // another branch's dQ rows (the sliding window), added once
+    const float4 a = __ldcs(reinterpret_cast<const float4*>(addend + (t * h + j) * kD + lane * 4));
+    acc.x += a.x; acc.y += a.y; acc.z += a.z; acc.w += a.w;
+  }
   *reinterpret_cast<float4*>(dQ + (t * h + j) * kD + lane * 4) = acc;
 }
 
@@ -143,7 +149,8 @@ int merge_bf16_fast(const fsa_shape* s, const int32_t* idx, const void* obuf, co
                     void* out, void* lse, void* m_out, void* l_out, cudaStream_t st) {
   const int64_t rows = s->h * s->N;
   if (rows == 0) return FSA_OK;
-  merge_bf16_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(
+  auto kern = s->T <= 16 ? merge_bf16_kernel<16> : merge_bf16_kernel<32>;
+  kern<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(
       idx, (const __nv_bfloat16*)obuf, (const float2*)ml, (float*)out, (float*)lse, (float*)m_out,
       (float*)l_out, s->N, s->h, s->h / s->h_K, (int)s->T, Combine{});
   FSA_LAUNCH_CHECK("merge_bf16");
@@ -156,7 +163,8 @@ int merge_combine_bf16_fast(const fsa_shape* s, const int32_t* idx, const void* 
   const int64_t rows = s->h * s->N;
   if (rows == 0) return FSA_OK;
   Combine c{(const float*)out_cmp, (const float*)out_slide, (const float*)tau, (__nv_bfloat16*)out};
-  merge_bf16_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(
+  auto kern = s->T <= 16 ? merge_bf16_kernel<16> : merge_bf16_kernel<32>;
+  kern<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(
       idx, (const __nv_bfloat16*)obuf, (const float2*)ml, (float*)out_sel, (float*)lse, nullptr,
       nullptr, s->N, s->h, s->h / s->h_K, (int)s->T, c);
   FSA_LAUNCH_CHECK("merge_combine_bf16");
@@ -164,11 +172,12 @@ int merge_combine_bf16_fast(const fsa_shape* s, const int32_t* idx, const void* 
 }
 
 int dq_reduce_bf16_fast(const fsa_shape* s, const int32_t* idx, const void* dq, void* dQ,
-                        cudaStream_t st) {
+                        cudaStream_t st, const void* addend) {
   const int64_t rows = s->h * s->N;
   if (rows == 0) return FSA_OK;
   dq_reduce_bf16_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(
-      idx, (const __nv_bfloat16*)dq, (float*)dQ, s->N, s->h, s->h / s->h_K, (int)s->T);
+      idx, (const __nv_bfloat16*)dq, (float*)dQ, s->N, s->h, s->h / s->h_K, (int)s->T,
+      (const float*)addend);
   FSA_LAUNCH_CHECK("dq_reduce_bf16");
   return FSA_OK;
 }

@@ -470,6 +470,15 @@ extern "C" int fsa_sel_bwd(const fsa_shape* s, int dtype, const void* Q, const v
               (cudaStream_t)stream);
 }
 
+extern "C" int fsa_dq_reduce_add(const fsa_shape* s, int dtype, const int32_t* idx,
+                                 const void* dq_buf, int dqbuf_dtype, const void* addend, void* dQ,
+                                 void* stream) {
+  if (dtype == FSA_DT_BF16 && dqbuf_dtype == FSA_DT_BF16 && fsa::fast_reduce_ok(*s))
+    return fsa::dq_reduce_bf16_fast(s, idx, dq_buf, dQ, (cudaStream_t)stream, addend);
+  fsa::set_error("dq_reduce_add: only the bf16 tensor-core configuration (d = 128, T <= 32)");
+  return FSA_ERR_UNSUPPORTED;
+}
+
 extern "C" int fsa_dq_reduce(const fsa_shape* s, int dtype, const int32_t* idx, const void* dq_buf,
                              int dqbuf_dtype, void* dQ, void* stream) {
   DISPATCH_DT(dtype, dq_reduce_impl, s, idx, dq_buf, dqbuf_dtype, dQ, (cudaStream_t)stream);

@@ -43,8 +43,15 @@ int merge_combine_bf16_fast(const fsa_shape* s, const int32_t* idx, const void* 
                             const void* ml, const void* out_cmp, const void* out_slide,
                             const void* tau, void* out_sel, void* lse, void* out, cudaStream_t st);
 int dq_reduce_bf16_fast(const fsa_shape* s, const int32_t* idx, const void* dq, void* dQ,
-                        cudaStream_t st);
+                        cudaStream_t st, const void* addend = nullptr);
 
 int num_sms();
+
+}  // namespace fsa
+#include <cuda.h>
+namespace fsa {
+// TMA descriptor of a token-major [N][heads][128] bf16 tensor, box (64, heads_box, tok_box)
+int make_tmap_tokens(CUtensorMap* map, const void* base, int64_t N, int64_t heads, int heads_box,
+                     int tok_box);
 
 }  // namespace fsa

@@ -609,14 +609,14 @@ int tc_slide_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V
   Params p = make_params(s, Q, K, V, dOut, lse, delta, nullptr, dK, dV);
   p.slide = 1;
   p.no_dq = 1;
-  p.accumulate = accumulate;
+  p.accumulate = accumulate != 0;  // dK/dV += (modes 1 and 2)
   p.W = s->W;
   p.T = S;
   p.fdT.init((uint32_t)S);
   p.counter = (int32_t*)workspace;
   int rc = launch_bwd(p, st);
   if (rc) return rc;
-  return tc_slide_dq(s, Q, K, V, dOut, lse, delta, dQ, accumulate, st);
+  return tc_slide_dq(s, Q, K, V, dOut, lse, delta, dQ, accumulate == 1, st);  // mode 2: dQ written
 }
 
 }  // namespace fsa

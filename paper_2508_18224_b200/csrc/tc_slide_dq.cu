@@ -13,7 +13,8 @@
 //   softmax: dS (bf16) written back over S in TMEM
 //   dQ_w += dS K                        (M128 N128 K64, A = dS from TMEM)
 // TMEM per wg (256 columns at 256 w): S +0, dP +64, dQ accumulator +128.
-// Roles: warps 0-3 / 4-7 softmax + epilogue, 8-10 loaders, 11 MMA issuer.
+// Roles: warps 0-3 / 4-7 softmax + epilogue, warp 8 the TMA loader (one lane;
+// 9-10 idle), 11 MMA issuer.
 #include "tc_plan.cuh"
 #include "tc_sched.cuh"
 
@@ -24,7 +25,6 @@ using namespace tc;
 
 constexpr int kD = 128, kRows = 128;
 constexpr int kThreads = 12 * 32;
-constexpr int kLoaders = 96;
 constexpr uint32_t kT = 32768;                          // one 128-row tile [2 halves][128][128 B]
 constexpr uint32_t kKV = 32768;                         // K | V tile of 64 keys
 constexpr int kKVStages = 3;
@@ -40,6 +40,8 @@ constexpr uint32_t kIdS = idesc_bf16(128, 64, false, false);
 constexpr uint32_t kIdQ = idesc_bf16(128, 128, false, true);
 
 struct Params {
+  CUtensorMap tmQ, tmO, tmK, tmV;  // TMA descriptors (tma_host.cu): Q/dO boxes (64, g, tpi), K/V (64, 1, 64)
+  long long* trace;  // debug timeline (CTA 0), null in production
   const __nv_bfloat16 *Q, *K, *V, *dO;
   const float *lse, *delta;
   float* dQ;  // [N][h][128]
@@ -47,6 +49,12 @@ struct Params {
   int tpi, accumulate;
   float scale, scale_log2;
 };
+
+#define DQ_TRACE(w, item, slot)                                                          \
+  do {                                                                                   \
+    if (p.trace && blockIdx.x == 0 && (item) < 128)                                      \
+      p.trace[((w) * 128 + (item)) * 8 + (slot)] = clock64();                            \
+  } while (0)
 
 struct Sub {
   int t0, tlast;  // tokens [t0, tlast]
@@ -97,7 +105,7 @@ struct Cursor {
   }
 };
 
-__global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const Params p) {
+__global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -106,7 +114,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const Params p
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffTmem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    mbar_init(bar(B_QF), kLoaders);
+    mbar_init(bar(B_QF), 1);  // TMA: one arrive.expect_tx + the transaction bytes
     mbar_init(bar(B_QE), 2);
     for (int w = 0; w < 2; ++w) {
       mbar_init(bar(B_SF + w), 1);
@@ -115,7 +123,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const Params p
       mbar_init(bar(B_OE + w), 128);
     }
     for (int s = 0; s < kKVStages; ++s) {
-      mbar_init(bar(B_KF + s), kLoaders);
+      mbar_init(bar(B_KF + s), 1);
       mbar_init(bar(B_KE + s), 2);
     }
     fence_mbar_init();
@@ -127,59 +135,42 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const Params p
   const uint32_t tmem = *tmem_slot;
   const int G = (int)gridDim.x;
 
-  if (warp >= 8 && warp < 11) {
-    // ------------------------------------------------------------ loaders
-    uint32_t pend = 0;
-    auto push_group = [&](uint32_t b) {
-      asm volatile("cp.async.commit_group;" ::: "memory");
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-      fence_proxy_async();
-      if (pend) mbar_arrive(pend);
-      pend = b;
-    };
-    auto wait_stage = [&](uint32_t b, uint32_t par) {
-      if (mbar_test(b, par)) return;
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-      fence_proxy_async();
-      if (pend) mbar_arrive(pend);
-      pend = 0;
-      mbar_wait(b, par);
-    };
-    Cursor c;
-    int r = 0;
-    while (c.advance(p, G)) {
-      wait_stage(bar(B_QE), (uint32_t)((c.seq & 1) ^ 1));
-      // 16 gathers of 32 rows: {Q, dO} x 2 sub-items x 128 rows, over 3 warps
-      for (int cidx = warp - 8; cidx < 16; cidx += 3) {
-        const int op = cidx >> 3, w = (cidx >> 2) & 1;
-        const Sub& s = c.it.s[w];
-        const int row = (cidx & 3) * 32 + lane;
-        const int kt = row / (int)p.g, hh = row % (int)p.g;
-        const int t = s.t0 + kt;
-        const bool ok = kt < p.tpi && t <= s.tlast;
-        const __nv_bfloat16* src =
-            (op ? p.dO : p.Q) + ((int64_t)(ok ? t : 0) * p.h + c.it.kh * p.g + hh) * kD;
-        warp_gather_rows32(sb + kOffQ + (op * 2 + w) * kT, 16384u, (cidx & 3) * 32, src, ok, lane);
-      }
-      push_group(bar(B_QF));
-      for (int u = c.it.u0; u < c.it.u1; ++u, ++r) {
-        const int v = r % kKVStages;
-        wait_stage(bar(B_KE + v), (uint32_t)(((r / kKVStages) & 1) ^ 1));
-        for (int cidx = warp - 8; cidx < 4; cidx += 3) {
-          const int row0 = (cidx & 1) * 32;
-          const int key = u * 64 + row0 + lane;
-          const bool ok = key < p.N;
-          const __nv_bfloat16* src =
-              (cidx < 2 ? p.K : p.V) + ((int64_t)(ok ? key : 0) * p.h_K + c.it.kh) * kD;
-          warp_gather_rows32(sb + kOffKV + v * kKV + (cidx < 2 ? 0u : 16384u), 8192u, row0, src,
-                             ok, lane);
+  if (warp == 8) {
+    // ------------------------------------------------------------ TMA loader (one lane)
+    // Q and dO of a sub-item are TPI consecutive tokens x the g heads of one kv
+    // head: one 3-D box per 64-feature half lands as the SW128 K-major tile.
+    if (lane == 0) {
+      const uint32_t qbox = 64u * (uint32_t)(p.g * p.tpi) * 2u;  // bytes per half tile
+      Cursor c;
+      int r = 0;
+      while (c.advance(p, G)) {
+        mbar_wait(bar(B_QE), (uint32_t)((c.seq & 1) ^ 1));
+        DQ_TRACE(0, c.seq, 4);  // loader: Q/dO stage free
+        mbar_arrive_expect_tx(bar(B_QF), 8u * qbox);
+#pragma unroll
+        for (int w = 0; w < 2; ++w)
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            tma_load_3d(sb + kOffQ + w * kT + hf * 16384u, &p.tmQ, hf * 64, c.it.kh * (int)p.g,
+                        c.it.s[w].t0, bar(B_QF));
+            tma_load_3d(sb + kOffQ + (2 + w) * kT + hf * 16384u, &p.tmO, hf * 64,
+                        c.it.kh * (int)p.g, c.it.s[w].t0, bar(B_QF));
+          }
+        DQ_TRACE(0, c.seq, 5);  // loader: Q/dO loads issued
+        for (int u = c.it.u0; u < c.it.u1; ++u, ++r) {
+          const int v = r % kKVStages;
+          mbar_wait(bar(B_KE + v), (uint32_t)(((r / kKVStages) & 1) ^ 1));
+          mbar_arrive_expect_tx(bar(B_KF + v), kKV);
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            tma_load_3d(sb + kOffKV + v * kKV + hf * 8192u, &p.tmK, hf * 64, c.it.kh, u * 64,
+                        bar(B_KF + v));
+            tma_load_3d(sb + kOffKV + v * kKV + 16384u + hf * 8192u, &p.tmV, hf * 64, c.it.kh,
+                        u * 64, bar(B_KF + v));
+          }
         }
-        push_group(bar(B_KF + v));
       }
     }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    fence_proxy_async();
-    if (pend) mbar_arrive(pend);
   } else if (warp == 11) {
     // ------------------------------------------------------------ MMA issuer
     // S stream w: S/dP of each tile of sub-item w (single TMEM stage: the next
@@ -222,6 +213,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const Params p
                   mma_bf16_w(tS + 64, desc_kmajor(o + (kk >> 2) * 16384u + (kk & 3) * 32u),
                            desc_kmajor(vv + (kk >> 2) * 8192u + (kk & 3) * 32u), kIdS, kk > 0);
                 mma_commit_w(bar(B_SF + w));
+                if (lane == 0) DQ_TRACE(w, ns[w], 0);  // S/dP issued
                 ++ns[w];
                 ++su[w];
                 progressed = true;
@@ -248,6 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const Params p
                 for (int kk = 0; kk < 4; ++kk)
                   mma_bf16_ts_w(tQ, tS + kk * 8, desc_mnmajor(k + kk * 2048u, 8192u), kIdQ,
                               (first && kk == 0) ? 0u : 1u);
+                if (lane == 0) DQ_TRACE(w, nd[w], 3);  // dQ issued
                 mma_commit_w(bar(B_KE + kv));
                 if (last) {
                   mma_commit_w(bar(B_OF + w));
@@ -278,7 +271,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const Params p
         }
       }
     }
-  } else {
+  } else if (warp < 8) {
     // ------------------------------------------------------------ softmax / epilogue
     const int w = warp >> 2;
     const int r = threadIdx.x & 127;
@@ -303,6 +296,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const Params p
       }
       for (int kt = s.k0; kt < s.k1; ++kt, ++u) {
         mbar_wait(bar(B_SF + w), (uint32_t)(u & 1));
+        if (r == 0) DQ_TRACE(w, u, 1);  // S/dP landed
         tc_fence_after();
         const int kbase = kt * 64;
         const bool full = __all_sync(0xffffffffu, klo <= kbase && kbase + 63 <= khi);
@@ -329,6 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const Params p
         tmem_wait_st_();
         tc_fence_before();
         mbar_arrive(bar(B_PF + w));
+        if (r == 0) DQ_TRACE(w, u, 2);  // dS written
       }
       // epilogue: dQ (+)= scale * accumulator
       mbar_wait(bar(B_OF + w), (uint32_t)(n_out & 1));
@@ -375,9 +370,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const Params p
 
 }  // namespace
 
+long long* g_dq_trace = nullptr;
 int tc_slide_dq(const fsa_shape* s, const void* Q, const void* K, const void* V, const void* dOut,
                 const void* lse, const void* delta, void* dQ, int accumulate, cudaStream_t st) {
   Params p{};
+  p.trace = g_dq_trace;
   p.Q = (const __nv_bfloat16*)Q;
   p.K = (const __nv_bfloat16*)K;
   p.V = (const __nv_bfloat16*)V;
@@ -395,6 +392,11 @@ int tc_slide_dq(const fsa_shape* s, const void* Q, const void* K, const void* V,
   p.accumulate = accumulate;
   p.scale = (float)s->scale;
   p.scale_log2 = (float)(s->scale * 1.4426950408889634);
+  int rc = make_tmap_tokens(&p.tmQ, Q, p.N, p.h, (int)p.g, p.tpi);
+  if (!rc) rc = make_tmap_tokens(&p.tmO, dOut, p.N, p.h, (int)p.g, p.tpi);
+  if (!rc) rc = make_tmap_tokens(&p.tmK, K, p.N, p.h_K, 1, 64);
+  if (!rc) rc = make_tmap_tokens(&p.tmV, V, p.N, p.h_K, 1, 64);
+  if (rc) return rc;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(tc_slide_dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -411,3 +413,5 @@ int tc_slide_dq(const fsa_shape* s, const void* Q, const void* K, const void* V,
 }
 
 }  // namespace fsa
+
+extern "C" void fsa_debug_dq_trace(void* device_buf) { fsa::g_dq_trace = (long long*)device_buf; }

@@ -107,10 +107,35 @@ def nsa_backward(ctx: NSAContext, dout):
     _lib.call("fsa_gate_backward", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(dout),
               _lib.ptr(ctx.tau), _lib.ptr(ctx.out_sel), _lib.ptr(ctx.out_slide), _lib.ptr(d_sel),
               _lib.ptr(d_slide), _lib.ptr(delta_sel), _lib.ptr(delta_slide), st)
-    dQ, dK, dV = _backward_core(cfg, dt, ctx.q, ctx.k, ctx.v, d_sel, ctx.sel, ctx.inv,
-                                ctx.out_sel, ctx.lse_sel, delta=delta_sel)
-    return _slide_bwd_storage(cfg, dt, ctx.q, ctx.k, ctx.v, d_slide, ctx.out_slide,
-                              ctx.lse_slide, accumulate_into=(dQ, dK, dV), delta=delta_slide)
+    _, (dq_code, dq_dtype) = _lib.buffer_dtypes(cfg, dt)
+    if dq_code != _lib.DT_BF16:  # generic (f32 / f64 / small shapes) path
+        dQ, dK, dV = _backward_core(cfg, dt, ctx.q, ctx.k, ctx.v, d_sel, ctx.sel, ctx.inv,
+                                    ctx.out_sel, ctx.lse_sel, delta=delta_sel)
+        return _slide_bwd_storage(cfg, dt, ctx.q, ctx.k, ctx.v, d_slide, ctx.out_slide,
+                                  ctx.lse_slide, accumulate_into=(dQ, dK, dV), delta=delta_slide)
+    # tensor-core path: K8 (selected) writes dK/dV and the dq partials; the
+    # sliding backward adds its dK/dV in-kernel and writes its dQ rows, which
+    # the dQ reduce (K9) adds while summing the partials -- every gradient
+    # element is written once, with no read-modify-write pass over dQ
+    dev = dout.device
+    inv = ctx.inv
+    dq_buf = torch.empty((cfg.h, cfg.N, cfg.T, cfg.d_K), dtype=dq_dtype, device=dev)
+    dK = torch.empty((cfg.N, cfg.h_K, cfg.d_K), dtype=acc, device=dev)
+    dV = torch.empty((cfg.N, cfg.h_K, cfg.d_V), dtype=acc, device=dev)
+    _lib.call("fsa_sel_bwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(ctx.q), _lib.ptr(ctx.k),
+              _lib.ptr(ctx.v), _lib.ptr(d_sel), _lib.ptr(ctx.lse_sel), _lib.ptr(delta_sel),
+              _lib.ptr(inv.offsets), _lib.ptr(inv.qlist), _lib.ptr(inv.work), _lib.ptr(dq_buf),
+              dq_code, _lib.ptr(dK), _lib.ptr(dV), st)
+    dQ_slide = torch.empty((cfg.N, cfg.h, cfg.d_K), dtype=acc, device=dev)
+    nws = _lib.lib().fsa_slide_bwd_workspace_bytes(ctypes.byref(s), _lib.dt_code(dt))
+    ws = torch.empty(max(nws, 1), dtype=torch.uint8, device=dev)
+    _lib.call("fsa_slide_bwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(ctx.q), _lib.ptr(ctx.k),
+              _lib.ptr(ctx.v), _lib.ptr(d_slide), _lib.ptr(ctx.lse_slide), _lib.ptr(delta_slide),
+              _lib.ptr(dQ_slide), _lib.ptr(dK), _lib.ptr(dV), _lib.ptr(ws), 2, st)
+    dQ = torch.empty((cfg.N, cfg.h, cfg.d_K), dtype=acc, device=dev)
+    _lib.call("fsa_dq_reduce_add", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(ctx.sel.idx),
+              _lib.ptr(dq_buf), dq_code, _lib.ptr(dQ_slide), _lib.ptr(dQ), st)
+    return dQ, dK, dV
 
 
 def nsa_forward_backward(q, k, v, tau, dout, cfg):
