@@ -20,7 +20,7 @@
 // without blocking, so neither warpgroup waits for the other.
 //
 // Roles: warps 0-3 / 4-7 softmax + epilogue of sub-item 0 / 1 (thread = TMEM
-// lane = MMA row), warps 8-10 cp.async loaders, warp 11 the MMA issuer.
+// lane = MMA row), warp 8 the TMA loader (one lane; 9-10 idle), warp 11 the MMA issuer.
 // TMEM: wg w owns columns [256 w, 256 w + 256): S/P stages at +0 / +64, O at +128.
 #include "tc_plan.cuh"
 #include "tc_sched.cuh"
@@ -32,7 +32,6 @@ using namespace tc;
 
 constexpr int kD = 128, kRows = 128;
 constexpr int kThreads = 12 * 32;  // 2 softmax warpgroups, 3 loader warps, 1 MMA warp
-constexpr int kLoaders = 96;
 constexpr uint32_t kQ = 32768, kKV = 32768;
 constexpr int kKVStages = 3;
 constexpr uint32_t kOffQ = 0;                           // [2 stages][2 subs] x kQ
@@ -53,6 +52,7 @@ constexpr float kRescale = 8.f;  // exp2 units
 enum Mode { SLIDE = 0, CMP = 1, SCORES = 2 };
 
 struct Params {
+  CUtensorMap tmQ, tmK, tmV;         // TMA: Q box (64, g, tpi), key/value boxes (64, 1, 64)
   const __nv_bfloat16 *Q, *Kx, *Vx;  // keys/values: K,V [N][h_K][128] or pooled [b][h_K][128]
   float *out, *lse, *scores;
   int64_t N, h, h_K, g, W, B_K, b, n_keys, n_super;
@@ -124,7 +124,7 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
   tmem_st32u(taddr, reinterpret_cast<const uint32_t*>(v));
 }
 
-__global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const Params p) {
+__global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const Params p) 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < 2; ++s) {
-      mbar_init(bar(B_QF + s), kLoaders);
+      mbar_init(bar(B_QF + s), 1);  // TMA: arrive.expect_tx + bytes
       mbar_init(bar(B_QE + s), 2);  // one commit per S stream
       mbar_init(bar(B_OF + s), 1);
       mbar_init(bar(B_OE + s), 128);
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const Params p) 
       mbar_init(bar(B_PF + s), 128);
     }
     for (int s = 0; s < kKVStages; ++s) {
-      mbar_init(bar(B_KF + s), kLoaders);
+      mbar_init(bar(B_KF + s), 1);
       mbar_init(bar(B_KE + s), 2);  // one commit per PV stream
     }
     fence_mbar_init();
@@ -157,63 +157,41 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const Params p) 
   const uint32_t tmem = *tmem_slot;
   const int G = (int)gridDim.x;
 
-  if (warp >= 8 && warp < 11) {
-    // ------------------------------------------------------------ loaders
-    // Each gather is its own cp.async group; the newest stays in flight while
-    // the previous one is published.
-    uint32_t pend = 0;
-    auto push_group = [&](uint32_t b) {
-      asm volatile("cp.async.commit_group;" ::: "memory");
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-      fence_proxy_async();
-      if (pend) mbar_arrive(pend);
-      pend = b;
-    };
-    // a stage wait that would block first publishes the in-flight gather
-    auto wait_stage = [&](uint32_t b, uint32_t par) {
-      if (mbar_test(b, par)) return;
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-      fence_proxy_async();
-      if (pend) mbar_arrive(pend);
-      pend = 0;
-      mbar_wait(b, par);
-    };
-    Cursor c;
-    int r = 0;
-    while (c.advance(p, G)) {
-      const int qs = (int)(c.seq & 1);
-      wait_stage(bar(B_QE + qs), (uint32_t)(((c.seq >> 1) & 1) ^ 1));
-      // 8 gathers of 32 rows (2 sub-items x 128 rows) over the 3 loader warps
-      for (int cidx = warp - 8; cidx < 8; cidx += 3) {
-        const Sub& s = c.it.s[cidx >> 2];
-        const int row = (cidx & 3) * 32 + lane;
-        const int kt = row / (int)p.g, hh = row % (int)p.g;
-        const int t = s.t0 + kt;
-        const bool ok = kt < p.tpi && t <= s.tlast;
-        const __nv_bfloat16* src = p.Q + ((int64_t)(ok ? t : 0) * p.h + c.it.kh * p.g + hh) * kD;
-        warp_gather_rows32(sb + kOffQ + (qs * 2 + (cidx >> 2)) * kQ, 16384u, (cidx & 3) * 32, src,
-                           ok, lane);
-      }
-      push_group(bar(B_QF + qs));
-      for (int u = c.it.u0; u < c.it.u1; ++u, ++r) {
-        const int v = (int)(r % kKVStages);
-        wait_stage(bar(B_KE + v), (uint32_t)(((r / kKVStages) & 1) ^ 1));
-        // 4 gathers (K rows 0-31 / 32-63, V rows 0-31 / 32-63) over 3 warps
-        for (int cidx = warp - 8; cidx < (p.mode == SCORES ? 2 : 4); cidx += 3) {
-          const int row0 = (cidx & 1) * 32;
-          const int key = u * 64 + row0 + lane;
-          const bool ok = key < p.n_keys;
-          const __nv_bfloat16* src =
-              (cidx < 2 ? p.Kx : p.Vx) + ((int64_t)(ok ? key : 0) * p.h_K + c.it.kh) * kD;
-          warp_gather_rows32(sb + kOffKV + v * kKV + (cidx < 2 ? 0u : 16384u), 8192u, row0, src,
-                             ok, lane);
+  if (warp == 8) {
+    // ------------------------------------------------------------ TMA loader (one lane)
+    // A sub-item's Q is TPI consecutive tokens x the g heads of one kv head:
+    // one 3-D box per 64-feature half lands as the SW128 K-major tile; key /
+    // value tiles are 64 consecutive rows of one kv head.
+    if (lane == 0) {
+      const uint32_t qbox = 64u * (uint32_t)(p.g * p.tpi) * 2u;
+      Cursor c;
+      int r = 0;
+      while (c.advance(p, G)) {
+        const int qs = (int)(c.seq & 1);
+        mbar_wait(bar(B_QE + qs), (uint32_t)(((c.seq >> 1) & 1) ^ 1));
+        mbar_arrive_expect_tx(bar(B_QF + qs), 4u * qbox);
+#pragma unroll
+        for (int w = 0; w < 2; ++w)
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf)
+            tma_load_3d(sb + kOffQ + (qs * 2 + w) * kQ + hf * 16384u, &p.tmQ, hf * 64,
+                        c.it.kh * (int)p.g, c.it.s[w].t0, bar(B_QF + qs));
+        const bool with_v = p.mode != SCORES;
+        for (int u = c.it.u0; u < c.it.u1; ++u, ++r) {
+          const int v = (int)(r % kKVStages);
+          mbar_wait(bar(B_KE + v), (uint32_t)(((r / kKVStages) & 1) ^ 1));
+          mbar_arrive_expect_tx(bar(B_KF + v), with_v ? kKV : kKV / 2);
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            tma_load_3d(sb + kOffKV + v * kKV + hf * 8192u, &p.tmK, hf * 64, c.it.kh, u * 64,
+                        bar(B_KF + v));
+            if (with_v)
+              tma_load_3d(sb + kOffKV + v * kKV + 16384u + hf * 8192u, &p.tmV, hf * 64, c.it.kh,
+                          u * 64, bar(B_KF + v));
+          }
         }
-        push_group(bar(B_KF + v));
       }
     }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    fence_proxy_async();
-    if (pend) mbar_arrive(pend);
   } else if (warp == 11) {
     // ------------------------------------------------------------ MMA issuer
     {  // whole warp: uniform state; one elected lane issues
@@ -322,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const Params p) 
         }
       }
     }
-  } else {
+  } else if (warp < 8) {
     // ------------------------------------------------------------ softmax / epilogue
     const int w = warp >> 2;
     const int r = threadIdx.x & 127;
@@ -485,7 +463,11 @@ __global__ void to_bf16_kernel(const float* __restrict__ x, __nv_bfloat16* __res
     y[e] = __float2bfloat16_rn(x[e]);
 }
 
-int launch(const Params& p, cudaStream_t st) {
+int launch(Params& p, cudaStream_t st) {
+  int rc = make_tmap_tokens(&p.tmQ, p.Q, p.N, p.h, (int)p.g, p.tpi);
+  if (!rc) rc = make_tmap_tokens(&p.tmK, p.Kx, p.n_keys, p.h_K, 1, 64);
+  if (!rc) rc = make_tmap_tokens(&p.tmV, p.Vx, p.n_keys, p.h_K, 1, 64);
+  if (rc) return rc;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(tc_qo_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -561,7 +543,7 @@ int tc_slide_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V
   p.out = (float*)out;
   p.lse = (float*)lse;
   p.scores = nullptr;
-  launch(p, st);
+  if (int rc = launch(p, st)) return rc;
   FSA_LAUNCH_CHECK("tc_slide_fwd");
   return FSA_OK;
 }
@@ -589,7 +571,7 @@ int tc_cmp_fwd(const fsa_shape* s, const void* Q, const void* Kc, const void* Vc
   p.lse = (float*)lse;
   const bool fused = scores != nullptr && tc_cmp_scores_fused(*s);
   p.scores = fused ? (float*)scores : nullptr;
-  launch(p, st);
+  if (int rc = launch(p, st)) return rc;
   FSA_LAUNCH_CHECK("tc_cmp_fwd");
   if (scores != nullptr && !fused) {
     // scores on the tensor cores for any g: the g query rows of a kv head are
@@ -607,7 +589,7 @@ int tc_cmp_fwd(const fsa_shape* s, const void* Q, const void* Kc, const void* Vc
     q.scores = (float*)scores;
     q.out = nullptr;
     q.lse = nullptr;
-    launch(q, st);
+    if (int rc = launch(q, st)) return rc;
     FSA_LAUNCH_CHECK("tc_cmp_scores");
   }
   return FSA_OK;
