@@ -63,6 +63,7 @@ constexpr uint32_t kIdKV = idesc_bf16(128, 64, true, true);   // dV^T, dK^T
 constexpr uint32_t kIdQ = idesc_bf16(128, 128, false, true);  // dQ
 
 struct Params {
+  CUtensorMap tmQ, tmO, tmK, tmV;  // sliding mode: TMA boxes (contiguous window rows)
   long long* trace;  // debug timeline (CTA 0, first 256 items), null in production
   const __nv_bfloat16 *Q, *K, *V, *dO;
   const float *lse, *delta;
@@ -121,7 +122,7 @@ struct TaskFifo {
   __device__ int32_t pop() { return task[head++ & 3]; }
 };
 
-__global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p) {
+__global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -175,6 +176,46 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const Params p)
       kv_pend = false;
       pend = 0;
     };
+    if (p.slide) {
+      // Sliding mode: an item's rows are TPI consecutive tokens x g heads and
+      // the task's keys 64 consecutive rows -> TMA boxes (one lane issues,
+      // the other loader threads just arrive).
+      const uint32_t box = 64u * (uint32_t)(p.g * p.tpi) * 2u;
+      for (int k = 0;; ++k) {
+        if (lr == 0) ring.produce(k, p.counter, p.ntask);
+        const int32_t task = ring.consume(k);
+        if (task < 0) break;
+        const TaskRows tr = rows_of(p, task);
+        if (tr.nitems == 0) continue;
+        mbar_wait(bar(B_KVE), (uint32_t)((kseq & 1) ^ 1));
+        if (lr == 0) {
+          mbar_arrive_expect_tx(bar(B_KVF), 32768u);
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            tma_load_3d(sb + kOffK + hf * 8192u, &p.tmK, hf * 64, (int)tr.kh, (int)(tr.i * kBK), bar(B_KVF));
+            tma_load_3d(sb + kOffV + hf * 8192u, &p.tmV, hf * 64, (int)tr.kh, (int)(tr.i * kBK), bar(B_KVF));
+          }
+        } else {
+          mbar_arrive(bar(B_KVF));
+        }
+        for (int c = 0; c < tr.nitems; ++c, ++n) {
+          const int s = (int)(n & 1);
+          mbar_wait(bar(B_QDE + s), (uint32_t)(((n >> 1) & 1) ^ 1));
+          if (lr == 0) {
+            const int t0 = (int)(tr.beg + (int64_t)c * p.tpi);
+            mbar_arrive_expect_tx(bar(B_QDF + s), 4u * box);
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+              tma_load_3d(sb + kOffQ + s * kTile + hf * 16384u, &p.tmQ, hf * 64, (int)(tr.kh * p.g), t0, bar(B_QDF + s));
+              tma_load_3d(sb + kOffDO + s * kTile + hf * 16384u, &p.tmO, hf * 64, (int)(tr.kh * p.g), t0, bar(B_QDF + s));
+            }
+          } else {
+            mbar_arrive(bar(B_QDF + s));
+          }
+        }
+        ++kseq;
+      }
+    } else
     for (int k = 0;; ++k) {
       publish();  // nothing in flight across the task ring
       if (lr == 0) ring.produce(k, p.counter, p.ntask);
@@ -614,7 +655,12 @@ int tc_slide_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V
   p.T = S;
   p.fdT.init((uint32_t)S);
   p.counter = (int32_t*)workspace;
-  int rc = launch_bwd(p, st);
+  int rc = make_tmap_tokens(&p.tmQ, Q, s->N, s->h, (int)p.g, p.tpi);
+  if (!rc) rc = make_tmap_tokens(&p.tmO, dOut, s->N, s->h, (int)p.g, p.tpi);
+  if (!rc) rc = make_tmap_tokens(&p.tmK, K, s->N, s->h_K, 1, 64);
+  if (!rc) rc = make_tmap_tokens(&p.tmV, V, s->N, s->h_K, 1, 64);
+  if (rc) return rc;
+  rc = launch_bwd(p, st);
   if (rc) return rc;
   return tc_slide_dq(s, Q, K, V, dOut, lse, delta, dQ, accumulate == 1, st);  // mode 2: dQ written
 }
