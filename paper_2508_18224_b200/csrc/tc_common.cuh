@@ -52,10 +52,13 @@ __device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
   return ok != 0;
 }
 // Warp-uniform probe for issuer warps that run their control flow on all 32
-// lanes (so descriptors stay in uniform registers): true only if every lane
-// saw the phase complete (a late lane just makes the warp retry).
+// lanes (so descriptors stay in uniform registers): lane 0 probes, the result
+// is broadcast.
 __device__ __forceinline__ bool mbar_test_warp(uint32_t bar, uint32_t parity) {
-  return __all_sync(0xffffffffu, mbar_test(bar, parity));
+  // one lane probes (a warp-wide probe would issue 32 barrier requests)
+  uint32_t ok = 0;
+  if ((threadIdx.x & 31) == 0) ok = mbar_test(bar, parity) ? 1u : 0u;
+  return __shfl_sync(0xffffffffu, ok, 0) != 0;
 }
 // One lane of a converged warp (elect.sync)
 __device__ __forceinline__ bool elect_one() {

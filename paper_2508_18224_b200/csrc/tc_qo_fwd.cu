@@ -51,8 +51,15 @@ constexpr float kRescale = 8.f;  // exp2 units
 // head reduction is needed; scores = Qsum . K_cmp * score_mul.
 enum Mode { SLIDE = 0, CMP = 1, SCORES = 2 };
 
+#define QO_TRACE(w, item, slot)                                                          \
+  do {                                                                                   \
+    if (p.trace && blockIdx.x == 0 && (item) < 128)                                      \
+      p.trace[((w) * 128 + (item)) * 8 + (slot)] = clock64();                            \
+  } while (0)
+
 struct Params {
-  CUtensorMap tmQ, tmK, tmV;         // TMA: Q box (64, g, tpi), key/value boxes (64, 1, 64)
+  CUtensorMap tmQ, tmK, tmV;
+  long long* trace;  // debug timeline (CTA 0), null in production         // TMA: Q box (64, g, tpi), key/value boxes (64, 1, 64)
   const __nv_bfloat16 *Q, *Kx, *Vx;  // keys/values: K,V [N][h_K][128] or pooled [b][h_K][128]
   float *out, *lse, *scores;
   int64_t N, h, h_K, g, W, B_K, b, n_keys, n_super;
@@ -211,8 +218,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
         pu[w] = lp[w] ? cp[w].it.u0 : 0;
       }
       long long idle_since = 0;
+      int iters = 0;
       for (;;) {
         bool progressed = false;
+        ++iters;
 #pragma unroll
         for (int w = 0; w < 2; ++w) {
           // ---- S stream w
@@ -226,13 +235,19 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
               if (ns[w] < np[w] + 2 && mbar_test_warp(bar(B_QF + qs), qpar) &&
                   mbar_test_warp(bar(B_KF + kv), (uint32_t)((rr / kKVStages) & 1))) {
                 tc_fence_after();
+                if (lane == 0) QO_TRACE(w + 2, ns[w], 0);  // before the S batch
                 const uint32_t q = sb + kOffQ + (qs * 2 + w) * kQ, k = sb + kOffKV + kv * kKV;
                 const uint32_t tS = tmem + 256u * w + 64u * v;
+                if (elect_one()) {  // one elected lane issues the whole batch
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk)
-                  mma_bf16_w(tS, desc_kmajor(q + (kk >> 2) * 16384u + (kk & 3) * 32u),
-                           desc_kmajor(k + (kk >> 2) * 8192u + (kk & 3) * 32u), kIdS, kk > 0);
-                mma_commit_w(bar(B_SF + 2 * w + v));
+                  for (int kk = 0; kk < 8; ++kk)
+                    mma_bf16(tS, desc_kmajor(q + (kk >> 2) * 16384u + (kk & 3) * 32u),
+                             desc_kmajor(k + (kk >> 2) * 8192u + (kk & 3) * 32u), kIdS, kk > 0);
+                  QO_TRACE(w + 2, ns[w], 1);  // after the S batch
+                  mma_commit(bar(B_SF + 2 * w + v));
+                }
+                __syncwarp();
+                if (lane == 0) QO_TRACE(w, ns[w], 0);  // S issued
                 ++ns[w];
                 ++su[w];
                 progressed = true;
@@ -265,16 +280,21 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
                 tc_fence_after();
                 const uint32_t vv = sb + kOffKV + kv * kKV + 16384u;
                 const uint32_t tS = tmem + 256u * w + 64u * v, tO = tmem + 256u * w + 128u;
+                if (elect_one()) {
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk)
-                  mma_bf16_ts_w(tO, tS + kk * 8, desc_mnmajor(vv + kk * 2048u, 8192u), kIdPV,
-                              (first && kk == 0) ? 0u : 1u);
-                mma_commit_w(bar(B_KE + kv));
-                mma_commit_w(bar(B_PV + w));
-                if (last) {
-                  mma_commit_w(bar(B_OF + w));
-                  ++nsub[w];
+                  for (int kk = 0; kk < 4; ++kk)
+                    mma_bf16_ts(tO, tS + kk * 8, desc_mnmajor(vv + kk * 2048u, 8192u), kIdPV,
+                                (first && kk == 0) ? 0u : 1u);
+                  mma_commit(bar(B_KE + kv));
+                  mma_commit(bar(B_PV + w));
+                  if (last) mma_commit(bar(B_OF + w));
                 }
+                __syncwarp();
+                if (lane == 0) QO_TRACE(w, np[w], 3);  // PV issued
+                if (lane == 0 && p.trace && blockIdx.x == 0 && np[w] < 128)
+                  p.trace[(w * 128 + np[w]) * 8 + 7] = iters;
+                iters = 0;
+                if (last) ++nsub[w];
                 ++np[w];
                 ++pu[w];
                 progressed = true;
@@ -328,6 +348,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
         const int v = (int)(u & 1);
         const uint32_t tS = tmem + lb + 64u * v;
         mbar_wait(bar(B_SF + 2 * w + v), (uint32_t)((u >> 1) & 1));
+        if (r == 0) QO_TRACE(w, u, 1);  // S landed
         tc_fence_after();
         float sv[64];
         tmem_ld32(tS, sv);
@@ -422,10 +443,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
         tmem_wait_st_();
         tc_fence_before();
         mbar_arrive(bar(B_PF + 2 * w + v));
+        if (r == 0) QO_TRACE(w, u, 2);  // P written
       }
       if (p.mode == SCORES) continue;
       // epilogue: out = O / l, lse = m + ln l
+      if (r == 0) QO_TRACE(w, u - 1, 4);  // epilogue: waiting for O
       mbar_wait(bar(B_OF + w), (uint32_t)(n_out & 1));
+      if (r == 0) QO_TRACE(w, u - 1, 5);  // O complete
       tc_fence_after();
       const bool write = ok && l > 0.f;
       const float inv = write ? 1.f / l : 0.f;
@@ -444,6 +468,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
       }
       tc_fence_before();
       mbar_arrive(bar(B_OE + w));
+      if (r == 0) QO_TRACE(w, u - 1, 6);  // epilogue done
       if (write) p.lse[j * p.N + t] = m_used * p.scale + __logf(l);
       ++n_out;
     }
@@ -463,7 +488,9 @@ __global__ void to_bf16_kernel(const float* __restrict__ x, __nv_bfloat16* __res
     y[e] = __float2bfloat16_rn(x[e]);
 }
 
+long long* g_qo_trace = nullptr;
 int launch(Params& p, cudaStream_t st) {
+  p.trace = (p.mode == SLIDE) ? g_qo_trace : nullptr;
   int rc = make_tmap_tokens(&p.tmQ, p.Q, p.N, p.h, (int)p.g, p.tpi);
   if (!rc) rc = make_tmap_tokens(&p.tmK, p.Kx, p.n_keys, p.h_K, 1, 64);
   if (!rc) rc = make_tmap_tokens(&p.tmV, p.Vx, p.n_keys, p.h_K, 1, 64);
@@ -596,3 +623,5 @@ int tc_cmp_fwd(const fsa_shape* s, const void* Q, const void* Kc, const void* Vc
 }
 
 }  // namespace fsa
+
+extern "C" void fsa_debug_qo_trace(void* device_buf) { fsa::g_qo_trace = (long long*)device_buf; }

@@ -236,16 +236,17 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const __grid_c
                 tc_fence_after();
                 const uint32_t k = sb + kOffKV + kv * kKV;
                 const uint32_t tS = tmem + 256u * w, tQ = tmem + 256u * w + 128u;
+                if (elect_one()) {
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk)
-                  mma_bf16_ts_w(tQ, tS + kk * 8, desc_mnmajor(k + kk * 2048u, 8192u), kIdQ,
-                              (first && kk == 0) ? 0u : 1u);
-                if (lane == 0) DQ_TRACE(w, nd[w], 3);  // dQ issued
-                mma_commit_w(bar(B_KE + kv));
-                if (last) {
-                  mma_commit_w(bar(B_OF + w));
-                  ++nsub[w];
+                  for (int kk = 0; kk < 4; ++kk)
+                    mma_bf16_ts(tQ, tS + kk * 8, desc_mnmajor(k + kk * 2048u, 8192u), kIdQ,
+                                (first && kk == 0) ? 0u : 1u);
+                  DQ_TRACE(w, nd[w], 3);  // dQ issued
+                  mma_commit(bar(B_KE + kv));
+                  if (last) mma_commit(bar(B_OF + w));
                 }
+                __syncwarp();
+                if (last) ++nsub[w];
                 ++nd[w];
                 ++du[w];
                 progressed = true;
