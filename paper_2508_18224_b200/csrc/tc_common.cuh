@@ -84,6 +84,13 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     if (clock64() - t0 > (1ll << 34)) mbar_stuck(bar, parity);
   }
 }
+// Whole-warp wait by one lane: the other 31 lanes do not poll the barrier
+// (hundreds of spinning threads congest the SM's barrier unit and slow down
+// every other probe, e.g. the MMA issuer's); __syncwarp publishes the result.
+__device__ __forceinline__ void mbar_wait_warp(uint32_t bar, uint32_t parity) {
+  if ((threadIdx.x & 31) == 0) mbar_wait(bar, parity);
+  __syncwarp();
+}
 static __device__ __noinline__ void mbar_stuck(uint32_t bar, uint32_t parity) {
   printf("fsa: mbarrier wait timed out: smem 0x%x parity %u block %d thread %d\n", bar, parity,
          (int)blockIdx.x, (int)threadIdx.x);

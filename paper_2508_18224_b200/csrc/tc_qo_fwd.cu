@@ -201,123 +201,92 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
     }
   } else if (warp == 11) {
     // ------------------------------------------------------------ MMA issuer
-    {  // whole warp: uniform state; one elected lane issues
-      // S stream w: for each super item, S tiles [k0_w, k1_w), then one QE
-      // commit.  PV stream w: for each union tile r in [u0, u1): PV if r is in
-      // the sub-item's range, else a pass-by KE commit (KE counts 2 arrivals).
-      Cursor cs[2], cp[2];
-      bool ls[2], lp[2];
-      int su[2], pu[2];      // next tile of each stream (su == k1: QE commit due)
-      int ns[2] = {0, 0};    // S tiles issued (stage / parity sequence)
-      int np[2] = {0, 0};    // PV tiles issued
-      int nsub[2] = {0, 0};  // non-empty sub-items started by the PV stream
-      for (int w = 0; w < 2; ++w) {
-        ls[w] = cs[w].advance(p, G);
-        su[w] = ls[w] ? cs[w].it.s[w].k0 : 0;
-        lp[w] = cp[w].advance(p, G);
-        pu[w] = lp[w] ? cp[w].it.u0 : 0;
-      }
-      long long idle_since = 0;
-      int iters = 0;
-      for (;;) {
-        bool progressed = false;
-        ++iters;
+    // Static order with blocking waits (one lane waits, the warp follows; one
+    // elected lane issues): per union tile u of a super item, S of both
+    // sub-items for tile u, then PV of both for tile u-1 (S runs one tile
+    // ahead so the softmax of u-1 overlaps the S MMAs of u).  Each PV stream
+    // commits KE once per union tile (pass-by when the tile is outside its
+    // range; KE counts 2), each S stream QE once per super item (QE counts 2).
+    {
+      Cursor c;
+      int ns[2] = {0, 0}, np[2] = {0, 0}, nsub[2] = {0, 0};
+      while (c.advance(p, G)) {
+        const Super& it = c.it;
+        const int qs = (int)(c.seq & 1);
+        bool q_ready = false;
+        for (int u = it.u0; u <= it.u1; ++u) {
+          if (u < it.u1) {  // ---- S of tile u
+            const int rr = c.rbase + (u - it.u0), kv = rr % kKVStages;
+            mbar_wait_warp(bar(B_KF + kv), (uint32_t)((rr / kKVStages) & 1));
 #pragma unroll
-        for (int w = 0; w < 2; ++w) {
-          // ---- S stream w
-          if (ls[w]) {
-            const Sub& s = cs[w].it.s[w];
-            const int qs = (int)(cs[w].seq & 1);
-            const uint32_t qpar = (uint32_t)((cs[w].seq >> 1) & 1);
-            if (su[w] < s.k1) {
-              const int rr = cs[w].rbase + (su[w] - cs[w].it.u0);
-              const int kv = (int)(rr % kKVStages), v = (int)(ns[w] & 1);
-              if (ns[w] < np[w] + 2 && mbar_test_warp(bar(B_QF + qs), qpar) &&
-                  mbar_test_warp(bar(B_KF + kv), (uint32_t)((rr / kKVStages) & 1))) {
-                tc_fence_after();
-                if (lane == 0) QO_TRACE(w + 2, ns[w], 0);  // before the S batch
-                const uint32_t q = sb + kOffQ + (qs * 2 + w) * kQ, k = sb + kOffKV + kv * kKV;
-                const uint32_t tS = tmem + 256u * w + 64u * v;
-                if (elect_one()) {  // one elected lane issues the whole batch
-#pragma unroll
-                  for (int kk = 0; kk < 8; ++kk)
-                    mma_bf16(tS, desc_kmajor(q + (kk >> 2) * 16384u + (kk & 3) * 32u),
-                             desc_kmajor(k + (kk >> 2) * 8192u + (kk & 3) * 32u), kIdS, kk > 0);
-                  QO_TRACE(w + 2, ns[w], 1);  // after the S batch
-                  mma_commit(bar(B_SF + 2 * w + v));
-                }
-                __syncwarp();
-                if (lane == 0) QO_TRACE(w, ns[w], 0);  // S issued
-                ++ns[w];
-                ++su[w];
-                progressed = true;
+            for (int w = 0; w < 2; ++w) {
+              if (u < it.s[w].k0 || u >= it.s[w].k1) continue;
+              if (!q_ready) {
+                mbar_wait_warp(bar(B_QF + qs), (uint32_t)((c.seq >> 1) & 1));
+                q_ready = true;
               }
-            } else if (s.k0 < s.k1 || mbar_test_warp(bar(B_QF + qs), qpar)) {
-              mma_commit_w(bar(B_QE + qs));  // this stream is done with the Q stage
-              ls[w] = cs[w].advance(p, G);
-              su[w] = ls[w] ? cs[w].it.s[w].k0 : 0;
-              progressed = true;
+              tc_fence_after();
+              const int v = ns[w] & 1;
+              const uint32_t q = sb + kOffQ + (qs * 2 + w) * kQ, k = sb + kOffKV + kv * kKV;
+              const uint32_t tS = tmem + 256u * w + 64u * v;
+              if (elect_one()) {
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                  mma_bf16(tS, desc_kmajor(q + (kk >> 2) * 16384u + (kk & 3) * 32u),
+                           desc_kmajor(k + (kk >> 2) * 8192u + (kk & 3) * 32u), kIdS, kk > 0);
+                mma_commit(bar(B_SF + 2 * w + v));
+                QO_TRACE(w, ns[w], 0);  // S issued
+              }
+              __syncwarp();
+              ++ns[w];
             }
           }
-          // ---- PV stream w
-          if (lp[w]) {
-            const Sub& s = cp[w].it.s[w];
-            const int rr = cp[w].rbase + (pu[w] - cp[w].it.u0);
-            const int kv = (int)(rr % kKVStages);
-            if (pu[w] >= s.k0 && pu[w] < s.k1) {
-              const int v = (int)(np[w] & 1);
-              const bool first = pu[w] == s.k0, last = pu[w] + 1 == s.k1;
+          if (u > it.u0) {  // ---- PV of tile u-1 (or pass-by KE commits)
+            const int up = u - 1;
+            const int rr = c.rbase + (up - it.u0), kv = rr % kKVStages;
+#pragma unroll
+            for (int w = 0; w < 2; ++w) {
+              const Sub& sw = it.s[w];
+              if (up < sw.k0 || up >= sw.k1) {
+                if (elect_one()) mma_commit(bar(B_KE + kv));  // pass-by
+                __syncwarp();
+                continue;
+              }
+              const int v = np[w] & 1;
+              const bool first = up == sw.k0, last = up + 1 == sw.k1;
+              mbar_wait_warp(bar(B_PF + 2 * w + v), (uint32_t)((np[w] >> 1) & 1));
               if (p.mode == SCORES) {  // no PV: release the K tile once S is consumed
-                if (np[w] < ns[w] && mbar_test_warp(bar(B_PF + 2 * w + v), (uint32_t)((np[w] >> 1) & 1))) {
-                  mma_commit_w(bar(B_KE + kv));
-                  ++np[w];
-                  ++pu[w];
-                  progressed = true;
-                }
-              } else if (np[w] < ns[w] &&
-                  mbar_test_warp(bar(B_PF + 2 * w + v), (uint32_t)((np[w] >> 1) & 1)) &&
-                  (!first || mbar_test_warp(bar(B_OE + w), (uint32_t)((nsub[w] & 1) ^ 1)))) {
-                tc_fence_after();
-                const uint32_t vv = sb + kOffKV + kv * kKV + 16384u;
-                const uint32_t tS = tmem + 256u * w + 64u * v, tO = tmem + 256u * w + 128u;
-                if (elect_one()) {
-#pragma unroll
-                  for (int kk = 0; kk < 4; ++kk)
-                    mma_bf16_ts(tO, tS + kk * 8, desc_mnmajor(vv + kk * 2048u, 8192u), kIdPV,
-                                (first && kk == 0) ? 0u : 1u);
-                  mma_commit(bar(B_KE + kv));
-                  mma_commit(bar(B_PV + w));
-                  if (last) mma_commit(bar(B_OF + w));
-                }
+                if (elect_one()) mma_commit(bar(B_KE + kv));
                 __syncwarp();
-                if (lane == 0) QO_TRACE(w, np[w], 3);  // PV issued
-                if (lane == 0 && p.trace && blockIdx.x == 0 && np[w] < 128)
-                  p.trace[(w * 128 + np[w]) * 8 + 7] = iters;
-                iters = 0;
-                if (last) ++nsub[w];
                 ++np[w];
-                ++pu[w];
-                progressed = true;
+                continue;
               }
-            } else if (mbar_test_warp(bar(B_KF + kv), (uint32_t)((rr / kKVStages) & 1))) {
-              mma_commit_w(bar(B_KE + kv));  // pass-by: tile not used by this sub-item
-              ++pu[w];
-              progressed = true;
-            }
-            if (pu[w] == cp[w].it.u1) {
-              lp[w] = cp[w].advance(p, G);
-              pu[w] = lp[w] ? cp[w].it.u0 : 0;
+              if (first) mbar_wait_warp(bar(B_OE + w), (uint32_t)((nsub[w] & 1) ^ 1));
+              tc_fence_after();
+              const uint32_t vv = sb + kOffKV + kv * kKV + 16384u;
+              const uint32_t tS = tmem + 256u * w + 64u * v, tO = tmem + 256u * w + 128u;
+              if (elect_one()) {
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+                  mma_bf16_ts(tO, tS + kk * 8, desc_mnmajor(vv + kk * 2048u, 8192u), kIdPV,
+                              (first && kk == 0) ? 0u : 1u);
+                mma_commit(bar(B_KE + kv));
+                mma_commit(bar(B_PV + w));
+                if (last) mma_commit(bar(B_OF + w));
+                QO_TRACE(w, np[w], 3);  // PV issued
+              }
+              __syncwarp();
+              if (last) ++nsub[w];
+              ++np[w];
             }
           }
         }
-        if (!ls[0] && !ls[1] && !lp[0] && !lp[1]) break;
-        if (progressed) {
-          idle_since = 0;
-        } else if (idle_since == 0) {
-          idle_since = clock64();
-        } else if (clock64() - idle_since > (1ll << 34)) {
-          mbar_stuck(bar(B_SF), 0);
+        // both S streams are done with this Q stage
+        if (elect_one()) {
+          mma_commit(bar(B_QE + qs));
+          mma_commit(bar(B_QE + qs));
         }
+        __syncwarp();
       }
     }
   } else if (warp < 8) {
@@ -347,7 +316,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
       for (int kt = s.k0; kt < s.k1; ++kt, ++u) {
         const int v = (int)(u & 1);
         const uint32_t tS = tmem + lb + 64u * v;
-        mbar_wait(bar(B_SF + 2 * w + v), (uint32_t)((u >> 1) & 1));
+        mbar_wait_warp(bar(B_SF + 2 * w + v), (uint32_t)((u >> 1) & 1));
         if (r == 0) QO_TRACE(w, u, 1);  // S landed
         tc_fence_after();
         float sv[64];
@@ -414,7 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
         }
         // rescale O in TMEM once PV(u-1) has landed (warp-collective)
         if (__any_sync(0xffffffffu, resc)) {
-          mbar_wait(bar(B_PV + w), (uint32_t)((u - 1) & 1));
+          mbar_wait_warp(bar(B_PV + w), (uint32_t)((u - 1) & 1));
           tc_fence_after();
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
@@ -444,11 +413,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
         tc_fence_before();
         mbar_arrive(bar(B_PF + 2 * w + v));
         if (r == 0) QO_TRACE(w, u, 2);  // P written
+        if (lane == 0) QO_TRACE(w + 2, u, 2 + (warp & 3));  // per-warp P arrival
       }
       if (p.mode == SCORES) continue;
       // epilogue: out = O / l, lse = m + ln l
       if (r == 0) QO_TRACE(w, u - 1, 4);  // epilogue: waiting for O
-      mbar_wait(bar(B_OF + w), (uint32_t)(n_out & 1));
+      mbar_wait_warp(bar(B_OF + w), (uint32_t)(n_out & 1));
       if (r == 0) QO_TRACE(w, u - 1, 5);  // O complete
       tc_fence_after();
       const bool write = ok && l > 0.f;

@@ -246,8 +246,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const Params p)
         if (progressed) {
           idle_since = 0;
         } else if (idle_since == 0) {
+          __nanosleep(64);  // yield issue slots to the softmax warps sharing this SMSP
           idle_since = clock64();
-        } else if (clock64() - idle_since > (1ll << 34)) {
+        } else if (__nanosleep(64), clock64() - idle_since > (1ll << 34)) {
           mbar_stuck(bar(B_SF), 0);
         }
       }

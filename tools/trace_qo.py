@@ -17,17 +17,25 @@ tau = torch.rand(cfg.N, 3, device="cuda", generator=g)
 out, ctx = nsa.nsa_forward(q, k, v, tau, cfg)
 nsa.nsa_backward(ctx, do)
 torch.cuda.synchronize()
-buf = torch.zeros(4 * 128 * 8, dtype=torch.int64, device="cuda")
+buf = torch.zeros(4 * 128 * 8 + 3072, dtype=torch.int64, device="cuda")
 lib = _lib.lib()
 lib.fsa_debug_qo_trace(ctypes.c_void_p(buf.data_ptr()))
 L = lambda x: x.permute(0, 2, 1)  # noqa: E731
 fsa.sliding_attention_forward(L(q), L(k), L(v), cfg)
 torch.cuda.synchronize()
 lib.fsa_debug_qo_trace(None)
-t = buf.view(4, 128, 8).cpu()
+tb = buf.cpu()
+t = tb[: 4 * 128 * 8].view(4, 128, 8)
+its = tb[4 * 128 * 8:]
 t0 = int(t[0, 0, 0])
 print("wg tile   S_iss  S_land  P_done  PV_iss  epi_wait  O_done  epi_done  iters")
 for u in range(40):
     for w in range(2):
         r = [int(t[w, u, j]) - t0 if int(t[w, u, j]) else -1 for j in range(7)] + [int(t[w, u, 7])]
-        print(f"{w:2d} {u:4d} " + " ".join(f"{x:8d}" for x in r) + f"   S batch {int(t[w + 2, u, 0]) - t0} -> {int(t[w + 2, u, 1]) - t0}")
+        print(f"{w:2d} {u:4d} " + " ".join(f"{x:8d}" for x in r) + f"   S batch {int(t[w + 2, u, 0]) - t0} -> {int(t[w + 2, u, 1]) - t0}  P by warp " + " ".join(str(int(t[w + 2, u, 2 + q]) - t0) for q in range(4)))
+
+print("MMA loop iteration start times (first 60):")
+print([int(x) - t0 for x in its[:60]])
+print("per iteration: [start, after PV streams, after S streams] (iterations 10..30)")
+for i in range(10, 30):
+    print(i, int(its[i]) - t0, int(its[1024 + i]) - int(its[i]), int(its[2048 + i]) - int(its[1024 + i]))
