@@ -173,68 +173,35 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const __grid_c
     }
   } else if (warp == 11) {
     // ------------------------------------------------------------ MMA issuer
-    // S stream w: S/dP of each tile of sub-item w (single TMEM stage: the next
-    // S/dP only after this wg's previous dQ product was issued), then a QE
-    // commit.  D stream w: per union tile, dQ += dS K or a pass-by KE commit.
-    {  // whole warp: uniform state; one elected lane issues
-      Cursor cs[2], cd[2];
-      bool ls[2], ld[2];
-      int su[2], du[2];
+    // Static order with blocking waits (one lane waits; one elected lane
+    // issues).  Per union tile u of a super item and per sub-item w: first
+    // dQ_w += dS K of tile u-1 (it frees wg w's single S/dP TMEM stage), then
+    // S/dP_w of tile u.  KE: one commit per stream per union tile (pass-by
+    // outside the sub-item's range; KE counts 2); QE: two per super item.
+    {
+      Cursor c;
       int ns[2] = {0, 0}, nd[2] = {0, 0}, nsub[2] = {0, 0};
-      for (int w = 0; w < 2; ++w) {
-        ls[w] = cs[w].advance(p, G);
-        su[w] = ls[w] ? cs[w].it.s[w].k0 : 0;
-        ld[w] = cd[w].advance(p, G);
-        du[w] = ld[w] ? cd[w].it.u0 : 0;
-      }
-      long long idle_since = 0;
-      for (;;) {
-        bool progressed = false;
+      while (c.advance(p, G)) {
+        const Super& it = c.it;
+        bool q_ready = false;
+        for (int u = it.u0; u <= it.u1; ++u) {
+          const bool s_step = u < it.u1;
+          const int rr = c.rbase + (u - it.u0), kv = rr % kKVStages;
+          if (s_step) mbar_wait_warp(bar(B_KF + kv), (uint32_t)((rr / kKVStages) & 1));
 #pragma unroll
-        for (int w = 0; w < 2; ++w) {
-          if (ls[w]) {
-            const Sub& s = cs[w].it.s[w];
-            const uint32_t qpar = (uint32_t)(cs[w].seq & 1);
-            if (su[w] < s.k1) {
-              const int rr = cs[w].rbase + (su[w] - cs[w].it.u0);
-              const int kv = rr % kKVStages;
-              if (ns[w] == nd[w] && mbar_test_warp(bar(B_QF), qpar) &&
-                  mbar_test_warp(bar(B_KF + kv), (uint32_t)((rr / kKVStages) & 1))) {
+          for (int w = 0; w < 2; ++w) {
+            const Sub& sw = it.s[w];
+            if (u > it.u0) {  // ---- dQ of tile u-1 (or a pass-by KE commit)
+              const int up = u - 1, rp = rr - 1, kvp = rp % kKVStages;
+              if (up < sw.k0 || up >= sw.k1) {
+                if (elect_one()) mma_commit(bar(B_KE + kvp));
+                __syncwarp();
+              } else {
+                const bool first = up == sw.k0, last = up + 1 == sw.k1;
+                mbar_wait_warp(bar(B_PF + w), (uint32_t)(nd[w] & 1));
+                if (first) mbar_wait_warp(bar(B_OE + w), (uint32_t)((nsub[w] & 1) ^ 1));
                 tc_fence_after();
-                const uint32_t q = sb + kOffQ + w * kT, o = sb + kOffQ + (2 + w) * kT;
-                const uint32_t k = sb + kOffKV + kv * kKV, vv = k + 16384u;
-                const uint32_t tS = tmem + 256u * w;
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk)
-                  mma_bf16_w(tS, desc_kmajor(q + (kk >> 2) * 16384u + (kk & 3) * 32u),
-                           desc_kmajor(k + (kk >> 2) * 8192u + (kk & 3) * 32u), kIdS, kk > 0);
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk)
-                  mma_bf16_w(tS + 64, desc_kmajor(o + (kk >> 2) * 16384u + (kk & 3) * 32u),
-                           desc_kmajor(vv + (kk >> 2) * 8192u + (kk & 3) * 32u), kIdS, kk > 0);
-                mma_commit_w(bar(B_SF + w));
-                if (lane == 0) DQ_TRACE(w, ns[w], 0);  // S/dP issued
-                ++ns[w];
-                ++su[w];
-                progressed = true;
-              }
-            } else if (s.k0 < s.k1 || mbar_test_warp(bar(B_QF), qpar)) {
-              mma_commit_w(bar(B_QE));
-              ls[w] = cs[w].advance(p, G);
-              su[w] = ls[w] ? cs[w].it.s[w].k0 : 0;
-              progressed = true;
-            }
-          }
-          if (ld[w]) {
-            const Sub& s = cd[w].it.s[w];
-            const int rr = cd[w].rbase + (du[w] - cd[w].it.u0);
-            const int kv = rr % kKVStages;
-            if (du[w] >= s.k0 && du[w] < s.k1) {
-              const bool first = du[w] == s.k0, last = du[w] + 1 == s.k1;
-              if (nd[w] < ns[w] && mbar_test_warp(bar(B_PF + w), (uint32_t)(nd[w] & 1)) &&
-                  (!first || mbar_test_warp(bar(B_OE + w), (uint32_t)((nsub[w] & 1) ^ 1)))) {
-                tc_fence_after();
-                const uint32_t k = sb + kOffKV + kv * kKV;
+                const uint32_t k = sb + kOffKV + kvp * kKV;
                 const uint32_t tS = tmem + 256u * w, tQ = tmem + 256u * w + 128u;
                 if (elect_one()) {
 #pragma unroll
@@ -242,35 +209,45 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const __grid_c
                     mma_bf16_ts(tQ, tS + kk * 8, desc_mnmajor(k + kk * 2048u, 8192u), kIdQ,
                                 (first && kk == 0) ? 0u : 1u);
                   DQ_TRACE(w, nd[w], 3);  // dQ issued
-                  mma_commit(bar(B_KE + kv));
+                  mma_commit(bar(B_KE + kvp));
                   if (last) mma_commit(bar(B_OF + w));
                 }
                 __syncwarp();
                 if (last) ++nsub[w];
                 ++nd[w];
-                ++du[w];
-                progressed = true;
               }
-            } else if (mbar_test_warp(bar(B_KF + kv), (uint32_t)((rr / kKVStages) & 1))) {
-              mma_commit_w(bar(B_KE + kv));
-              ++du[w];
-              progressed = true;
             }
-            if (du[w] == cd[w].it.u1) {
-              ld[w] = cd[w].advance(p, G);
-              du[w] = ld[w] ? cd[w].it.u0 : 0;
+            if (s_step && u >= sw.k0 && u < sw.k1) {  // ---- S/dP of tile u
+              if (!q_ready) {
+                mbar_wait_warp(bar(B_QF), (uint32_t)(c.seq & 1));
+                q_ready = true;
+              }
+              tc_fence_after();
+              const uint32_t q = sb + kOffQ + w * kT, o = sb + kOffQ + (2 + w) * kT;
+              const uint32_t k = sb + kOffKV + kv * kKV, vv = k + 16384u;
+              const uint32_t tS = tmem + 256u * w;
+              if (elect_one()) {
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                  mma_bf16(tS, desc_kmajor(q + (kk >> 2) * 16384u + (kk & 3) * 32u),
+                           desc_kmajor(k + (kk >> 2) * 8192u + (kk & 3) * 32u), kIdS, kk > 0);
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                  mma_bf16(tS + 64, desc_kmajor(o + (kk >> 2) * 16384u + (kk & 3) * 32u),
+                           desc_kmajor(vv + (kk >> 2) * 8192u + (kk & 3) * 32u), kIdS, kk > 0);
+                mma_commit(bar(B_SF + w));
+                DQ_TRACE(w, ns[w], 0);  // S/dP issued
+              }
+              __syncwarp();
+              ++ns[w];
             }
           }
         }
-        if (!ls[0] && !ls[1] && !ld[0] && !ld[1]) break;
-        if (progressed) {
-          idle_since = 0;
-        } else if (idle_since == 0) {
-          __nanosleep(64);  // yield issue slots to the softmax warps sharing this SMSP
-          idle_since = clock64();
-        } else if (__nanosleep(64), clock64() - idle_since > (1ll << 34)) {
-          mbar_stuck(bar(B_SF), 0);
+        if (elect_one()) {  // both S streams are done with this Q/dO stage
+          mma_commit(bar(B_QE));
+          mma_commit(bar(B_QE));
         }
+        __syncwarp();
       }
     }
   } else if (warp < 8) {
@@ -297,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const __grid_c
         for (int q = 0; q < 4; ++q) prefetch_l2(row + q * 32);
       }
       for (int kt = s.k0; kt < s.k1; ++kt, ++u) {
-        mbar_wait(bar(B_SF + w), (uint32_t)(u & 1));
+        mbar_wait_warp(bar(B_SF + w), (uint32_t)(u & 1));
         if (r == 0) DQ_TRACE(w, u, 1);  // S/dP landed
         tc_fence_after();
         const int kbase = kt * 64;
@@ -328,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const __grid_c
         if (r == 0) DQ_TRACE(w, u, 2);  // dS written
       }
       // epilogue: dQ (+)= scale * accumulator
-      mbar_wait(bar(B_OF + w), (uint32_t)(n_out & 1));
+      mbar_wait_warp(bar(B_OF + w), (uint32_t)(n_out & 1));
       tc_fence_after();
       float* orow = p.dQ + ((int64_t)t * p.h + j) * kD;
 #pragma unroll
