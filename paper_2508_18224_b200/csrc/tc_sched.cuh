@@ -47,6 +47,15 @@ struct Ring {
     if ((threadIdx.x & 31) == 0) mbar_arrive(empty(k));
     return true;
   }
+  // warp-wide blocking consumer: lane 0 waits, all lanes read, lane 0 arrives
+  __device__ int32_t consume_warp(int k) const {
+    if ((threadIdx.x & 31) == 0) mbar_wait(full(k), (uint32_t)((k / kRingDepth) & 1));
+    __syncwarp();
+    const int32_t t = slots[k & (kRingDepth - 1)];
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(empty(k));
+    return t;
+  }
   // consumer side
   __device__ int32_t consume(int k) const {
     mbar_wait(full(k), (uint32_t)((k / kRingDepth) & 1));
