@@ -67,6 +67,9 @@ SIGNATURES = {
     "fsa_gate_scale": ([_sp, _i, _vp, _vp, _i, _vp, _vp], _i),
     "fsa_gate_backward": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "fsa_qm_fwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
+    "fsa_debug_bwd_trace": ([_vp], None),
+    "fsa_debug_dq_trace": ([_vp], None),
+    "fsa_debug_qo_trace": ([_vp], None),
     "fsa_check_finite": ([_i, _vp, _i64, _vp, _vp], _i),
 }
 
