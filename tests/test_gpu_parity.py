@@ -451,3 +451,21 @@ def test_query_major_forward_vs_oracle(kw, run_dt):
     pad = max(c.g, c.min_tile)
     assert ph.task_count == c.h_K * c.N and ph.inner_iterations == steps
     assert ph.flops == steps * 2 * pad * c.B_K * (c.d_K + c.d_V)
+
+
+def test_cli_bench_csv(tmp_path):
+    """python -m paper_2508_18224_b200 bench: the reference's CSV columns, one row per phase."""
+    import csv as _csv
+
+    from paper_2508_18224_b200 import cli
+    cfgf = tmp_path / "tiny.cfg"
+    cfgf.write_text("N = 1024\nd_K = 64\nd_V = 64\nh = 4\nh_K = 1\nB_K = 64\nT = 8\n")
+    out = tmp_path / "bench.csv"
+    assert cli.main(["bench", "--config", str(cfgf), "--repeat", "2", "--dtype", "f32",
+                     "--csv", str(out)]) == 0
+    rows = list(_csv.DictReader(open(out)))
+    assert tuple(rows[0].keys()) == cli.BENCH_COLUMNS
+    phases = {(r["engine"], r["phase"]) for r in rows}
+    assert {("kv_major", "stats"), ("kv_major", "block_pass"), ("kv_major", "reduce"),
+            ("query_major", "forward")} <= phases
+    assert all(float(r["median_s"]) > 0 for r in rows)

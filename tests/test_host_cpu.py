@@ -119,3 +119,14 @@ def test_meter_merge_algebra():
     assert a.merged(b) == b.merged(a)
     assert a.merged(b).total_bytes == 8
     assert [n for n, _ in a.merged(b).as_rows()] == ["stats", "reduce"]
+
+
+# --- CLI (cli.py mirrors the reference's bench CSV, cli.py:149-242) ---------
+
+def test_cli_bad_config_exits_2(tmp_path, capsys):
+    from paper_2508_18224_b200 import cli
+    bad = tmp_path / "bad.cfg"
+    bad.write_text("N = 100\nd_K = 8\nd_V = 8\nh = 2\nh_K = 1\nB_K = 64\nT = 2\n")
+    assert cli.main(["bench", "--config", str(bad)]) == 2
+    assert "N not divisible by B_K" in capsys.readouterr().err
+    assert cli.BENCH_COLUMNS[:3] == ("engine", "phase", "backend")
