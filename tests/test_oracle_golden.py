@@ -182,3 +182,49 @@ def test_sampled_row_restatement_matches_whole_array_oracle():
         sl = slice(i * c.B_K, (i + 1) * c.B_K)
         np.testing.assert_allclose(dK, (g_sel[1] + g_sl[1])[sl, :, kh], rtol=1e-9, atol=1e-12)
         np.testing.assert_allclose(dV, (g_sel[2] + g_sl[2])[sl, :, kh], rtol=1e-9, atol=1e-12)
+
+
+def test_compressed_backward_and_gate_grad_vs_autograd():
+    """The compressed branch and the gate have no backward in the reference
+    (parity unpinned); the oracle's analytic gradients are pinned to float64
+    torch autograd of the same forward semantics (branches.py:34-104)."""
+    import torch
+    kw = dict(N=256, d_K=8, d_V=12, h=4, h_K=2, B_K=16, T=4, W=32)
+    c = O.cfg_of(**kw)
+    Q, K, V = O.make_qkv(c, 5)
+    dO = O.make_dout(c, 5)
+    tau = O.make_gates(c, 5)
+    tQ, tK, tV = (torch.from_numpy(x).requires_grad_(True) for x in (Q, K, V))
+    n_pref = min(c.B_K - 1, c.N)
+    Kc = tK.reshape(c.b, c.B_K, c.d_K, c.h_K).mean(1)
+    Vc = tV.reshape(c.b, c.B_K, c.d_V, c.h_K).mean(1)
+    Vp = torch.cumsum(tV[:n_pref], 0) / torch.arange(1, n_pref + 1, dtype=torch.float64)[:, None, None]
+    formed = (torch.arange(c.N) + 1) // c.B_K
+    outs = []
+    for j in range(c.h):
+        kh = j // c.g
+        z = (tQ[:, :, j] @ Kc[:, :, kh].T) * c.scale
+        z = z.masked_fill(torch.arange(c.b)[None, :] >= formed[:, None], float("-inf"))
+        ready = formed > 0
+        p = torch.softmax(z[ready], dim=1)
+        o = torch.zeros(c.N, c.d_V, dtype=torch.float64)
+        o = o.index_put((torch.nonzero(ready)[:, 0],), p @ Vc[:, :, kh])
+        o = o.index_put((torch.arange(n_pref),), Vp[:, :, kh])
+        outs.append(o)
+    out = torch.stack(outs, dim=2)
+    (out * torch.from_numpy(dO)).sum().backward()
+    dQ, dK, dV = O.compressed_backward(Q, K, V, dO, c)
+    np.testing.assert_allclose(dQ, tQ.grad.numpy(), rtol=1e-10, atol=1e-12)
+    np.testing.assert_allclose(dK, tK.grad.numpy(), rtol=1e-10, atol=1e-12)
+    np.testing.assert_allclose(dV, tV.grad.numpy(), rtol=1e-10, atol=1e-12)
+    # also equal to the forward restatement's output
+    o_cmp, _ = O.compressed_forward(Q, O.compress_kv(K, V, c), c)
+    np.testing.assert_allclose(out.detach().numpy(), o_cmp, rtol=1e-12, atol=1e-12)
+    # gate gradient vs autograd
+    o_sel, _ = O.selected_forward(Q, K, V, O.select_topk(O.make_scores(c, 5), c), c)
+    o_sl, _ = O.sliding_forward(Q, K, V, c)
+    tt = torch.from_numpy(tau).requires_grad_(True)
+    comb = sum(tt[:, i][:, None, None] * torch.from_numpy(x) for i, x in enumerate((o_cmp, o_sel, o_sl)))
+    (comb * torch.from_numpy(dO)).sum().backward()
+    np.testing.assert_allclose(O.gate_grad((o_cmp, o_sel, o_sl), dO, c), tt.grad.numpy(),
+                               rtol=1e-10, atol=1e-12)
