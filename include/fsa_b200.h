@@ -198,6 +198,25 @@ int fsa_gate_backward(const fsa_shape* s, int dtype, const void* dOut, const voi
                       const void* out_sel, const void* out_slide, void* d_sel, void* d_slide,
                       void* delta_sel, void* delta_slide, void* stream);
 
+/* Compressed-branch backward (the reference has none --
+ * parity vs the float64 oracle, pinned to autograd): gradients of
+ * sum(out_cmp * dOut) through the attention over the pooled rows and the
+ * pooling / prefix means (branches.py:34-78), ADDED into dQ [N][h][d_K] and
+ * dK, dV [N][h_K][d] (acc dtype).  K_cmp/V_cmp [b][h_K][d], lse [h][N],
+ * delta = sum_v out_cmp * dOut [h][N] in acc dtype; dOut in dtype. */
+size_t fsa_cmp_bwd_workspace_bytes(const fsa_shape* s, int dtype);
+int fsa_cmp_bwd(const fsa_shape* s, int dtype, const void* Q, const void* K_cmp, const void* V_cmp,
+                const void* dOut, const void* lse, const void* delta, void* dQ, void* dK, void* dV,
+                void* workspace, void* stream);
+
+/* Gate backward for all three branches (branches.py:95-104): d_c = tau[t][c]
+ * dOut (dtype), delta_c [h][N] = sum_v out_c * d_c, and the gate gradient
+ * dtau [N][3] = sum_{v,j} out_c * dOut (acc dtype).  One pass over dOut. */
+int fsa_gate_backward_full(const fsa_shape* s, int dtype, const void* dOut, const void* tau,
+                           const void* out_cmp, const void* out_sel, const void* out_slide,
+                           void* d_cmp, void* d_sel, void* d_slide, void* delta_cmp,
+                           void* delta_sel, void* delta_slide, void* dtau, void* stream);
+
 /* NSA query-major selected forward (query_major.py:45-69, _core.pyx:134-181):
  * one task per (kv head, token) over its selected blocks in ascending order,
  * online softmax; the FSA-vs-NSA comparison baseline (CUDA cores; g <= 16,

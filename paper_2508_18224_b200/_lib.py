@@ -66,6 +66,9 @@ SIGNATURES = {
     "fsa_gated_combine": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp], _i),
     "fsa_gate_scale": ([_sp, _i, _vp, _vp, _i, _vp, _vp], _i),
     "fsa_gate_backward": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
+    "fsa_cmp_bwd_workspace_bytes": ([_sp, _i], _sz),
+    "fsa_cmp_bwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
+    "fsa_gate_backward_full": ([_sp, _i] + [_vp] * 13, _i),
     "fsa_qm_fwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "fsa_debug_bwd_trace": ([_vp], None),
     "fsa_debug_dq_trace": ([_vp], None),

@@ -48,6 +48,10 @@ class NSAContext:
     lse_slide: torch.Tensor
     out_cmp: torch.Tensor
     scores: torch.Tensor
+    # compressed branch (for nsa_backward(..., full=True))
+    k_cmp: torch.Tensor = None
+    v_cmp: torch.Tensor = None
+    lse_cmp: torch.Tensor = None
 
 
 def nsa_forward(q, k, v, tau, cfg):
@@ -89,12 +93,17 @@ def nsa_forward(q, k, v, tau, cfg):
               _lib.ptr(tau), _lib.ptr(out_sel), _lib.ptr(lse_sel), _lib.ptr(out), st)
     del obuf, ml
     ctx = NSAContext(cfg, dt, q, k, v, tau, sel, inv, out_sel, lse_sel, out_slide, lse_slide,
-                     out_cmp, scores)
+                     out_cmp, scores, Kc, Vc, lse_cmp)
     return out, ctx
 
 
-def nsa_backward(ctx: NSAContext, dout):
-    """Returns (dQ, dK, dV) storage tensors in the accumulator dtype."""
+def nsa_backward(ctx: NSAContext, dout, *, full: bool = False):
+    """Returns (dQ, dK, dV) storage tensors in the accumulator dtype: the
+    gradients through the selected and sliding branches, the ones the
+    reference differentiates.  With ``full=True`` also through the compressed
+    branch (attention over the pooled rows, the pooling and the prefix means;
+    no reference backward -- SURVEY 8(f) rank 3) and returns
+    (dQ, dK, dV, dtau) with the gate gradient dtau (N, 3)."""
     cfg, dt = ctx.cfg, ctx.dtype
     s = _lib.shape_of(cfg)
     st = _lib.stream()
@@ -103,10 +112,35 @@ def nsa_backward(ctx: NSAContext, dout):
     d_slide = torch.empty_like(dout)
     delta_sel = torch.empty((cfg.h, cfg.N), dtype=acc, device=dout.device)
     delta_slide = torch.empty_like(delta_sel)
+    if full:
+        d_cmp = torch.empty_like(dout)
+        delta_cmp = torch.empty_like(delta_sel)
+        dtau = torch.empty((cfg.N, 3), dtype=acc, device=dout.device)
+        _lib.call("fsa_gate_backward_full", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(dout),
+                  _lib.ptr(ctx.tau), _lib.ptr(ctx.out_cmp), _lib.ptr(ctx.out_sel),
+                  _lib.ptr(ctx.out_slide), _lib.ptr(d_cmp), _lib.ptr(d_sel), _lib.ptr(d_slide),
+                  _lib.ptr(delta_cmp), _lib.ptr(delta_sel), _lib.ptr(delta_slide), _lib.ptr(dtau), st)
+        dQ, dK, dV = _sel_slide_backward(ctx, d_sel, d_slide, delta_sel, delta_slide)
+        nws = _lib.lib().fsa_cmp_bwd_workspace_bytes(ctypes.byref(s), _lib.dt_code(dt))
+        ws = torch.empty(nws, dtype=torch.uint8, device=dout.device)
+        _lib.call("fsa_cmp_bwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(ctx.q),
+                  _lib.ptr(ctx.k_cmp), _lib.ptr(ctx.v_cmp), _lib.ptr(d_cmp), _lib.ptr(ctx.lse_cmp),
+                  _lib.ptr(delta_cmp), _lib.ptr(dQ), _lib.ptr(dK), _lib.ptr(dV), _lib.ptr(ws), st)
+        return dQ, dK, dV, dtau
     # gate backward into both differentiated branches + their deltas, one pass
     _lib.call("fsa_gate_backward", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(dout),
               _lib.ptr(ctx.tau), _lib.ptr(ctx.out_sel), _lib.ptr(ctx.out_slide), _lib.ptr(d_sel),
               _lib.ptr(d_slide), _lib.ptr(delta_sel), _lib.ptr(delta_slide), st)
+    return _sel_slide_backward(ctx, d_sel, d_slide, delta_sel, delta_slide)
+
+
+def _sel_slide_backward(ctx: NSAContext, d_sel, d_slide, delta_sel, delta_slide):
+    """Selected + sliding backward from the gated cotangents and their deltas."""
+    cfg, dt = ctx.cfg, ctx.dtype
+    s = _lib.shape_of(cfg)
+    st = _lib.stream()
+    acc = _lib.acc_dtype(dt)
+    dout = d_sel
     _, (dq_code, dq_dtype) = _lib.buffer_dtypes(cfg, dt)
     if dq_code != _lib.DT_BF16:  # generic (f32 / f64 / small shapes) path
         dQ, dK, dV = _backward_core(cfg, dt, ctx.q, ctx.k, ctx.v, d_sel, ctx.sel, ctx.inv,
@@ -138,8 +172,7 @@ def nsa_backward(ctx: NSAContext, dout):
     return dQ, dK, dV
 
 
-def nsa_forward_backward(q, k, v, tau, dout, cfg):
-    """One full step: forward then backward; returns (out, dQ, dK, dV)."""
+def nsa_forward_backward(q, k, v, tau, dout, cfg, *, full: bool = False):
+    """One full step: forward then backward; returns (out, dQ, dK, dV[, dtau])."""
     out, ctx = nsa_forward(q, k, v, tau, cfg)
-    dQ, dK, dV = nsa_backward(ctx, dout)
-    return out, dQ, dK, dV
+    return (out,) + tuple(nsa_backward(ctx, dout, full=full))

@@ -363,6 +363,42 @@ def test_nsa_step_vs_oracle(run_dt):
     gl = O.sliding_backward(Q, K, V, dO * tau[:, 2][:, None, None], c)
     for got, a, b, name in zip((dQ, dK, dV), gs, gl, ("dQ", "dK", "dV")):
         assert_close(host(got.permute(0, 2, 1)), a + b, run_dt, name, grad=True)
+    # full NSA backward: + the compressed branch (no reference backward: the
+    # float64 oracle, pinned to autograd) and the gate gradient
+    fQ, fK, fV, dtau = fsa.nsa_backward(ctx, do, full=True)
+    gc = O.compressed_backward(Q, K, V, dO * tau[:, 0][:, None, None], c)
+    for got, a, b, cc, name in zip((fQ, fK, fV), gs, gl, gc, ("dQ", "dK", "dV")):
+        assert_close(host(got.permute(0, 2, 1)), a + b + cc, run_dt, name + " (full)", grad=True)
+    want_tau = O.gate_grad((o_cmp, o_sel, o_sl), dO, c)
+    assert_close(host(dtau), want_tau, run_dt, "dtau", grad=True)
+
+
+@pytest.mark.parametrize("kw,run_dt", [
+    (dict(N=512, d_K=16, d_V=24, h=4, h_K=2, B_K=16, T=4, W=64), "f64"),
+    (dict(N=1000, d_K=32, d_V=32, h=6, h_K=3, B_K=8, T=5, W=40), "f32"),
+])
+def test_compressed_backward_vs_oracle(kw, run_dt):
+    """fsa_cmp_bwd (generic kernels) at the reference's own tolerances for f64."""
+    c = O.cfg_of(**kw)
+    cfg = _cfg(kw)
+    Q, K, V = (round_inputs(x, run_dt) for x in O.make_qkv(c, 13))
+    dO = round_inputs(O.make_dout(c, 13), run_dt)
+    tau = O.make_gates(c, 13)
+    tdt = DT[run_dt]
+    q, k, v, do = (dev(x, tdt).permute(0, 2, 1).contiguous() for x in (Q, K, V, dO))
+    acc = torch.float64 if run_dt == "f64" else torch.float32
+    out, ctx = fsa.nsa_forward(q, k, v, torch.from_numpy(tau).to("cuda", acc), cfg)
+    fQ, fK, fV, dtau = fsa.nsa_backward(ctx, do, full=True)
+    idx = host(ctx.sel.idx)
+    gs = O.selected_backward(Q, K, V, idx, dO * tau[:, 1][:, None, None], c)
+    gl = O.sliding_backward(Q, K, V, dO * tau[:, 2][:, None, None], c)
+    gc = O.compressed_backward(Q, K, V, dO * tau[:, 0][:, None, None], c)
+    for got, a, b, cc, name in zip((fQ, fK, fV), gs, gl, gc, ("dQ", "dK", "dV")):
+        assert_close(host(got.permute(0, 2, 1)), a + b + cc, run_dt, name, grad=True)
+    cmp = O.compress_kv(K, V, c)
+    outs = (O.compressed_forward(Q, cmp, c)[0], O.selected_forward(Q, K, V, idx, c)[0],
+            O.sliding_forward(Q, K, V, c)[0])
+    assert_close(host(dtau), O.gate_grad(outs, dO, c), run_dt, "dtau", grad=True)
 
 
 # ---------------------------------------------------------------------------
