@@ -224,6 +224,14 @@ int fsa_gate_backward_full(const fsa_shape* s, int dtype, const void* dOut, cons
 int fsa_qm_fwd(const fsa_shape* s, int dtype, const void* Q, const void* K, const void* V,
                const int32_t* idx, void* out, void* lse, void* stream);
 
+/* NSA query-major selected backward (query_major.py:72-99, _core.pyx:184-241):
+ * per (KV head, token) task, P recomputed from lse, dQ rows written, dK / dV
+ * ([N][h_K][d], acc; zeroed here) scattered with atomics.  lse, delta [h][N]
+ * in acc dtype (fsa_qm_fwd + fsa_bwd_delta).  g <= 16. */
+int fsa_qm_bwd(const fsa_shape* s, int dtype, const void* Q, const void* K, const void* V,
+               const void* dOut, const int32_t* idx, const void* lse, const void* delta, void* dQ,
+               void* dK, void* dV, void* stream);
+
 /* Finiteness check for as_headed (config.py:146-155): *flag |= 1 on any non-finite. */
 int fsa_check_finite(int dtype, const void* x, int64_t n, int32_t* flag, void* stream);
 

@@ -70,6 +70,7 @@ SIGNATURES = {
     "fsa_cmp_bwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "fsa_gate_backward_full": ([_sp, _i] + [_vp] * 13, _i),
     "fsa_qm_fwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
+    "fsa_qm_bwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "fsa_debug_bwd_trace": ([_vp], None),
     "fsa_debug_dq_trace": ([_vp], None),
     "fsa_debug_qo_trace": ([_vp], None),

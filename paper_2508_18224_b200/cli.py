@@ -91,6 +91,8 @@ def cmd_bench(args) -> int:
     (res, med, best) = _time(lambda: kv_major.selected_backward(Q, K, V, sel, dOut, cfg), args.repeat)
     for name, counters in res[3].as_rows():
         record("kv_major", f"backward_{name}", counters, med, best)
+    (res, med, best) = _time(lambda: query_major.selected_backward(Q, K, V, sel, dOut, cfg), args.repeat)
+    record("query_major", "backward", res[3].phase("query_major"), med, best)
     out = open(args.csv, "w", newline="") if args.csv else sys.stdout
     try:
         w = csv.DictWriter(out, fieldnames=BENCH_COLUMNS)

@@ -9,8 +9,9 @@ rows a tcgen05 MMA needs, so this schedule runs on CUDA cores
 rank 1, ``tools/sweep.py --nsa``).  The traffic meter is the reference's
 closed form (query_major.py:32-42), including the min_tile padding.
 
-The query-major backward (query_major.py:72-115) is not built in this round:
-``kv_major.selected_backward`` computes the same gradients.
+The backward (query_major.py:72-115) recomputes the forward and scatters
+dK / dV with atomics (``fsa_qm_bwd``) -- the reduction FSA's KV-block-major
+backward replaces with single-writer tasks.
 """
 
 from __future__ import annotations
@@ -55,7 +56,47 @@ def selected_forward(Q, K, V, sel: SelectionTensor, cfg) -> tuple[AttentionOutpu
     return AttentionOutput(out=logical(out), lse=lse), meter
 
 
+def _meter_backward(sel: SelectionTensor, cfg, meter: TrafficMeter) -> None:
+    """query_major.py:101-114."""
+    ph = meter.phase("query_major")
+    bpe = cfg.bytes_per_elem
+    pad = max(cfg.g, cfg.min_tile)
+    steps = int(sel.row_lengths().sum())
+    ph.task_count += cfg.h_K * cfg.N
+    ph.inner_iterations += steps
+    ph.bytes_loaded += (cfg.h_K * cfg.N * (pad * cfg.d_K + cfg.g * cfg.d_V)
+                        + 2 * steps * cfg.B_K * (cfg.d_K + cfg.d_V)) * bpe
+    ph.bytes_stored += (cfg.h_K * cfg.N * cfg.g * cfg.d_K + steps * cfg.B_K * (cfg.d_K + cfg.d_V)) * bpe
+    ph.flops += steps * 2 * pad * cfg.B_K * (4 * cfg.d_K + 3 * cfg.d_V)
+
+
 def selected_backward(Q, K, V, sel: SelectionTensor, dOut, cfg):
-    """query_major.py:72-115 -- not built this round (same gradients as
-    kv_major.selected_backward)."""
-    raise NotImplementedError("query-major backward is not built; use kv_major.selected_backward")
+    """query_major.py:72-115 on the device: (dQ, dK, dV, TrafficMeter).
+
+    Recomputes the forward (``fsa_qm_fwd``) as the reference does
+    (_core.pyx:193), then ``fsa_bwd_delta`` and ``fsa_qm_bwd``: per (kv head,
+    token) task, dQ rows written once, dK / dV rows scattered with atomics
+    (the query-major schedule has no single writer per KV row; summation
+    order is therefore not fixed -- within tolerance, not bit-reproducible)."""
+    dt, q, k, v, do = _intake(cfg, Q, K, V, dOut)
+    validate_selection(sel, cfg)
+    acc = _lib.acc_dtype(dt)
+    dev = q.device
+    out = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=acc, device=dev)
+    lse = torch.empty((cfg.h, cfg.N), dtype=acc, device=dev)
+    delta = torch.empty((cfg.h, cfg.N), dtype=acc, device=dev)
+    dQ = torch.empty((cfg.N, cfg.h, cfg.d_K), dtype=acc, device=dev)
+    dK = torch.empty((cfg.N, cfg.h_K, cfg.d_K), dtype=acc, device=dev)
+    dV = torch.empty((cfg.N, cfg.h_K, cfg.d_V), dtype=acc, device=dev)
+    s = _lib.shape_of(cfg)
+    st = _lib.stream()
+    _lib.call("fsa_qm_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(q), _lib.ptr(k),
+              _lib.ptr(v), _lib.ptr(sel.idx), _lib.ptr(out), _lib.ptr(lse), st)
+    _lib.call("fsa_bwd_delta", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(out), _lib.ptr(do),
+              _lib.ptr(delta), st)
+    _lib.call("fsa_qm_bwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(q), _lib.ptr(k), _lib.ptr(v),
+              _lib.ptr(do), _lib.ptr(sel.idx), _lib.ptr(lse), _lib.ptr(delta), _lib.ptr(dQ),
+              _lib.ptr(dK), _lib.ptr(dV), st)
+    meter = TrafficMeter()
+    _meter_backward(sel, cfg, meter)
+    return logical(dQ), logical(dK), logical(dV), meter

@@ -489,6 +489,31 @@ def test_query_major_forward_vs_oracle(kw, run_dt):
     assert ph.flops == steps * 2 * pad * c.B_K * (c.d_K + c.d_V)
 
 
+@pytest.mark.parametrize("kw,run_dt", [
+    (dict(N=512, d_K=32, d_V=48, h=8, h_K=2, B_K=16, T=4), "f64"),
+    (dict(N=1056, d_K=64, d_V=64, h=4, h_K=4, B_K=32, T=6), "f32"),
+    (dict(N=2048, d_K=128, d_V=128, h=16, h_K=2, B_K=64, T=8), "bf16"),
+    (dict(N=1024, d_K=128, d_V=128, h=7, h_K=1, B_K=64, T=5), "bf16"),
+])
+def test_query_major_backward_vs_oracle(kw, run_dt):
+    """query_major.py:72-115: same gradients as the oracle, reference meter."""
+    c = O.cfg_of(**kw)
+    cfg = _cfg(kw)
+    Q, K, V = (round_inputs(x, run_dt) for x in O.make_qkv(c, 37))
+    dO = round_inputs(O.make_dout(c, 37), run_dt)
+    idx = O.select_topk(O.make_scores(c, 37), c)
+    tq, tk, tv, tdo = (dev(x, DT[run_dt]) for x in (Q, K, V, dO))
+    dQ, dK, dV, meter = fsa.query_major.selected_backward(tq, tk, tv, fsa.SelectionTensor(idx), tdo, cfg)
+    want = O.selected_backward(Q, K, V, idx, dO, c)
+    for g_, w_, name in zip((dQ, dK, dV), want, ("dQ", "dK", "dV")):
+        assert_close(host(g_), w_, run_dt, "qm " + name, grad=True)
+    ph = meter.phases["query_major"]
+    steps = int((idx != -1).sum())
+    pad = max(c.g, c.min_tile)
+    assert ph.task_count == c.h_K * c.N and ph.inner_iterations == steps
+    assert ph.flops == steps * 2 * pad * c.B_K * (4 * c.d_K + 3 * c.d_V)
+
+
 def test_cli_bench_csv(tmp_path):
     """python -m paper_2508_18224_b200 bench: the reference's CSV columns, one row per phase."""
     import csv as _csv
