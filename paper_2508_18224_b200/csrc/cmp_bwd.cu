@@ -12,7 +12,13 @@
 //   dK[s]   += dK_cmp[s // B_K] / B_K,  dV[s] += dV_cmp[s // B_K] / B_K
 //            + sum_{t=s}^{B_K-2} dOut[t] / (t+1)     (pending tokens' prefix means)
 // Deterministic: every output element has one writer and a fixed order.
-#include "common.cuh"
+//
+// bf16, d = 128: the tensor-core path.  dK_cmp / dV_cmp come from the FSA
+// backward kernel (K8) in its compressed mode -- 64 pooled rows per task held
+// in smem against a chunk of CH tokens, one partial slab per chunk, summed here
+// in chunk order -- and dQ from the query-outer dQ kernel over the formed pooled
+// rows (tc_slide_dq.cu).  Other dtypes / shapes use the generic kernels below.
+#include "tc_plan.cuh"
 
 namespace fsa {
 namespace {
@@ -189,11 +195,87 @@ __global__ void gate_backward_full_kernel(const T* __restrict__ dOut,
   }
 }
 
+// sum of a pooled row's per-chunk partial slabs, in chunk order (tensor-core path)
+__global__ void cmp_slab_reduce(const float* __restrict__ dKp, const float* __restrict__ dVp,
+                                float* __restrict__ dKc, float* __restrict__ dVc, int64_t b,
+                                int64_t h_K, int64_t B_K, int64_t CH, int64_t nch, int64_t cstride) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // (j, kh, c), c fastest
+  if (e >= b * h_K * 128) return;
+  const int64_t j = e / (h_K * 128);
+  const int64_t first = ((j / 64) * 64 + 1) * B_K - 1;  // first token of the tile's chunks
+  float ak = 0.f, av = 0.f;
+  for (int64_t q = first / CH; q < nch; ++q) {
+    ak += __ldcs(dKp + q * cstride + e);
+    av += __ldcs(dVp + q * cstride + e);
+  }
+  dKc[e] = ak;
+  dVc[e] = av;
+}
+
+__global__ void f32_to_bf16(const float* __restrict__ x, __nv_bfloat16* __restrict__ y, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = __float2bfloat16_rn(x[i]);
+}
+
+bool tc_cmp_bwd_ok(const fsa_shape& s) { return tc_qo_supported(s, FSA_DT_BF16) && s.N * s.h < (1ll << 31); }
+
+struct CmpWs {  // tensor-core path workspace
+  __nv_bfloat16 *kb, *vb;
+  float *dKp, *dVp, *dKc, *dVc;
+  int32_t* counter;
+  int64_t CH, nch, cstride;
+  size_t bytes;
+};
+CmpWs cmp_ws(const fsa_shape& s, void* base) {
+  CmpWs w{};
+  const int64_t b = s.N / s.B_K, n = b * s.h_K * 128;
+  w.CH = cmp_chunk_tokens(&s);
+  w.nch = (s.N + w.CH - 1) / w.CH;
+  w.cstride = ((b + 63) / 64) * 64 * s.h_K * 128;
+  char* p = (char*)base;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { char* r = p + off; off += (bytes + 255) & ~size_t(255); return r; };
+  w.kb = (__nv_bfloat16*)take(n * 2);
+  w.vb = (__nv_bfloat16*)take(n * 2);
+  w.dKp = (float*)take(w.nch * w.cstride * 4);
+  w.dVp = (float*)take(w.nch * w.cstride * 4);
+  w.dKc = (float*)take(n * 4);
+  w.dVc = (float*)take(n * 4);
+  w.counter = (int32_t*)take(256);
+  w.bytes = off + 256;
+  return w;
+}
+
+int cmp_bwd_tc(const fsa_shape* s, const void* Q, const void* Kc, const void* Vc, const void* dOut,
+               const void* lse, const void* delta, void* dQ, void* dK, void* dV, void* ws,
+               cudaStream_t st) {
+  const CmpWs w = cmp_ws(*s, ws);
+  const int64_t b = s->N / s->B_K, n = b * s->h_K * 128;
+  if (n > 0) {
+    f32_to_bf16<<<148, 256, 0, st>>>((const float*)Kc, w.kb, n);
+    f32_to_bf16<<<148, 256, 0, st>>>((const float*)Vc, w.vb, n);
+    FSA_LAUNCH_CHECK("cmp_bwd to_bf16");
+    if (int rc = tc_cmp_dq(s, Q, w.kb, w.vb, dOut, lse, delta, dQ, st)) return rc;
+    if (int rc = tc_cmp_bwd_kv(s, Q, w.kb, w.vb, dOut, lse, delta, w.dKp, w.dVp, w.counter, st)) return rc;
+    cmp_slab_reduce<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(w.dKp, w.dVp, w.dKc, w.dVc, b, s->h_K,
+                                                               s->B_K, w.CH, w.nch, w.cstride);
+    FSA_LAUNCH_CHECK("cmp_slab_reduce");
+  }
+  const int64_t pr = s->N * s->h_K;
+  if (pr > 0)
+    cmp_pool_bwd<__nv_bfloat16><<<(unsigned)((pr + 7) / 8), 256, 0, st>>>(
+        w.dKc, w.dVc, (const __nv_bfloat16*)dOut, (float*)dK, (float*)dV, *s);
+  FSA_LAUNCH_CHECK("cmp_pool_bwd");
+  return FSA_OK;
+}
+
 template <typename T>
 int cmp_bwd_impl(const fsa_shape* s, const void* Q, const void* Kc, const void* Vc, const void* dOut,
                  const void* lse, const void* delta, void* dQ, void* dK, void* dV, void* ws,
                  cudaStream_t st) {
   using A = typename Acc<T>::type;
+  if (sizeof(T) == 2 && tc_cmp_bwd_ok(*s))
+    return cmp_bwd_tc(s, Q, Kc, Vc, dOut, lse, delta, dQ, dK, dV, ws, st);
   const int64_t b = s->N / s->B_K;
   A* dKc = (A*)ws;
   A* dVc = dKc + b * s->h_K * s->d_K;
@@ -240,6 +322,7 @@ int gate_bwd_full_impl(const fsa_shape* s, const void* dOut, const void* tau, co
 
 extern "C" size_t fsa_cmp_bwd_workspace_bytes(const fsa_shape* s, int dtype) {
   const size_t acc = dtype == FSA_DT_F64 ? 8 : 4;
+  if (dtype == FSA_DT_BF16 && fsa::tc_cmp_bwd_ok(*s)) return fsa::cmp_ws(*s, nullptr).bytes;
   return (size_t)(s->N / s->B_K) * s->h_K * (s->d_K + s->d_V) * acc + 256;
 }
 

@@ -35,6 +35,15 @@ int tc_slide_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V
 int tc_slide_dq(const fsa_shape* s, const void* Q, const void* K, const void* V, const void* dOut,
                 const void* lse, const void* delta, void* dQ, int accumulate, cudaStream_t st);
 
+// compressed-branch backward on the same kernels (tc_sel_bwd.cu, tc_slide_dq.cu):
+// dK_cmp / dV_cmp partial slabs per token chunk, and dQ += over the pooled rows
+int64_t cmp_chunk_tokens(const fsa_shape* s);
+int tc_cmp_bwd_kv(const fsa_shape* s, const void* Q, const void* Kb, const void* Vb,
+                  const void* dOut, const void* lse, const void* delta, void* dKp, void* dVp,
+                  int32_t* counter, cudaStream_t st);
+int tc_cmp_dq(const fsa_shape* s, const void* Q, const void* Kb, const void* Vb, const void* dOut,
+              const void* lse, const void* delta, void* dQ, cudaStream_t st);
+
 // vectorised bf16 merge / dQ reduce for d = 128, T <= 32 (merge_fast.cu)
 bool fast_reduce_ok(const fsa_shape& s);
 int merge_bf16_fast(const fsa_shape* s, const int32_t* idx, const void* obuf, const void* ml,

@@ -73,6 +73,10 @@ struct Params {
   float *dK, *dV;     // [N][h_K][128]
   int64_t N, h, h_K, T, b, g, ntask;
   int64_t W;   // sliding mode: window; T is then the number of window slots
+  // compressed mode (slide == 2): keys = 64 pooled rows of K_cmp / V_cmp (bf16),
+  // rows = a chunk of CH consecutive tokens; dK/dV (the pooled rows' gradients)
+  // go to a per-chunk partial slab of cstride floats (tc_cmp_bwd sums them)
+  int64_t cmpBK, CH, nct, nch, cstride;
   int tpi, slide, accumulate;  // accumulate: dK/dV += (sliding branch onto the selected one)
   int no_dq;                   // sliding mode: dQ comes from the query-outer kernel (tc_slide_dq.cu)
   FastDiv fdT;
@@ -89,6 +93,17 @@ struct Params {
 __device__ __forceinline__ TaskRows rows_of(const Params& p, int32_t task) {
   if (!p.slide) return task_rows(task, p.offsets, p.b, p.tpi);
   TaskRows r;
+  if (p.slide == 2) {  // task = (kv head, pooled-row tile, token chunk), chunk fastest
+    const int64_t per = p.nct * p.nch;
+    r.kh = task / per;
+    r.i = (task % per) / p.nch;
+    const int64_t q = task % p.nch, first = (r.i * kBK + 1) * p.cmpBK - 1;
+    r.beg = q * p.CH > first ? q * p.CH : first;
+    const int64_t end = (q + 1) * p.CH < p.N ? (q + 1) * p.CH : p.N;
+    r.ntok = end > r.beg ? end - r.beg : 0;
+    r.nitems = (int)((r.ntok + p.tpi - 1) / p.tpi);
+    return r;
+  }
   r.kh = task / p.b;
   r.i = task % p.b;
   r.beg = r.i * kBK;
@@ -107,6 +122,9 @@ __device__ __forceinline__ void token_of(const Params& p, const TaskRows& tr, in
   if (!p.slide) {
     t = p.fdT.div((uint32_t)ent);
     slot = ent - t * p.T;
+  } else if (p.slide == 2) {
+    t = tr.beg + pos;
+    slot = 0;
   } else {
     t = tr.beg + pos;
     const int64_t first = (t - p.W + 1 > 0 ? t - p.W + 1 : 0) / kBK;
@@ -404,8 +422,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
     auto kv_epilogue = [&](const TaskRows& tr, int64_t ks) {
       mbar_wait(bar(B_KAF), (uint32_t)(ks & 1));
       tc_fence_after();
-      float* dk = p.dK + ((tr.i * kBK) * p.h_K + tr.kh) * kD + r;
-      float* dv = p.dV + ((tr.i * kBK) * p.h_K + tr.kh) * kD + r;
+      const int64_t slab = p.slide == 2 ? (tr.beg / p.CH) * p.cstride : 0;
+      float* dk = p.dK + slab + ((tr.i * kBK) * p.h_K + tr.kh) * kD + r;
+      float* dv = p.dV + slab + ((tr.i * kBK) * p.h_K + tr.kh) * kD + r;
       const int64_t ks_ = p.h_K * kD;  // key stride
 #pragma unroll
       for (int q = 0; q < 4; ++q) {  // dK keys 0-31, 32-63, then dV
@@ -445,7 +464,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
         }
       }
       if (tr.nitems == 0) {  // no attending rows: the block's gradients are zero
-        if (p.accumulate || wg != 0) continue;
+        if (p.accumulate || wg != 0 || p.slide == 2) continue;  // (compressed: slab not read)
         float* dk = p.dK + ((tr.i * kBK) * p.h_K + tr.kh) * kD + r;
         float* dv = p.dV + ((tr.i * kBK) * p.h_K + tr.kh) * kD + r;
         for (int key = 0; key < kBK; ++key) {
@@ -472,9 +491,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
           token_of(p, tr, pos, ent, t, slot);
           const int64_t j = tr.kh * p.g + hh;
           drow = (j * p.N + t) * p.T + slot;
-          const int64_t hi = t - tr.i * kBK;
+          // compressed mode: pooled row j is formed for t iff j < (t + 1) / B_K
+          const int64_t hi = (p.slide == 2 ? (t + 1) / p.cmpBK - 1 : t) - tr.i * kBK;
           khi = hi < kBK - 1 ? (int)hi : kBK - 1;
-          if (p.slide) {
+          if (p.slide == 1) {
             const int64_t lo = t - p.W + 1 - tr.i * kBK;
             klo = lo > 0 ? (int)lo : 0;
           }
@@ -664,6 +684,40 @@ int tc_slide_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V
   rc = launch_bwd(p, st);
   if (rc) return rc;
   return tc_slide_dq(s, Q, K, V, dOut, lse, delta, dQ, accumulate == 1, st);  // mode 2: dQ written
+}
+
+// Compressed-branch dK_cmp / dV_cmp: the same kernel with
+// 64 pooled rows as a task's keys and a chunk of CH tokens as its rows; each
+// (kv head, pooled tile, chunk) task writes its own partial slab.  Kb / Vb are
+// bf16 [b][h_K][128]; dKp / dVp hold nch slabs of nct * 64 * h_K * 128 floats.
+int64_t cmp_chunk_tokens(const fsa_shape* s) {
+  int64_t ch = 2048;
+  while (s->N > 32 * ch) ch *= 2;  // at most 32 slabs
+  return ch;
+}
+
+int tc_cmp_bwd_kv(const fsa_shape* s, const void* Q, const void* Kb, const void* Vb,
+                  const void* dOut, const void* lse, const void* delta, void* dKp, void* dVp,
+                  int32_t* counter, cudaStream_t st) {
+  Params p = make_params(s, Q, Kb, Vb, dOut, lse, delta, nullptr, dKp, dVp);
+  p.slide = 2;
+  p.no_dq = 1;
+  p.accumulate = 0;
+  p.cmpBK = s->B_K;
+  p.CH = cmp_chunk_tokens(s);
+  p.nct = (p.b + kBK - 1) / kBK;
+  p.nch = (p.N + p.CH - 1) / p.CH;
+  p.cstride = p.nct * kBK * p.h_K * kD;
+  p.ntask = p.h_K * p.nct * p.nch;
+  p.T = 1;
+  p.fdT.init(1u);
+  p.counter = counter;
+  int rc = make_tmap_tokens(&p.tmQ, Q, s->N, s->h, (int)p.g, p.tpi);
+  if (!rc) rc = make_tmap_tokens(&p.tmO, dOut, s->N, s->h, (int)p.g, p.tpi);
+  if (!rc) rc = make_tmap_tokens(&p.tmK, Kb, p.b, s->h_K, 1, 64);
+  if (!rc) rc = make_tmap_tokens(&p.tmV, Vb, p.b, s->h_K, 1, 64);
+  if (rc) return rc;
+  return launch_bwd(p, st);
 }
 
 }  // namespace fsa

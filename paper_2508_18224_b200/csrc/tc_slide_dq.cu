@@ -47,6 +47,8 @@ struct Params {
   float* dQ;  // [N][h][128]
   int64_t N, h, h_K, g, W, n_super;
   int tpi, accumulate;
+  int cmp;         // compressed mode: keys = pooled rows of K_cmp / V_cmp (bf16), row j
+  int64_t cmpBK;   // visible to token t iff j < (t + 1) / B_K (branches.py:47-78)
   float scale, scale_log2;
 };
 
@@ -69,7 +71,7 @@ struct Super {
 __device__ __forceinline__ bool super_of(const Params& p, int id, Super& it) {
   if (id >= p.h_K * p.n_super) return false;
   it.kh = id % (int)p.h_K;
-  const int st = id / (int)p.h_K;
+  const int st = p.cmp ? (int)p.n_super - 1 - id / (int)p.h_K : id / (int)p.h_K;  // cmp: late (heavy) tokens first
   it.u0 = INT32_MAX;
   it.u1 = 0;
 #pragma unroll
@@ -78,7 +80,13 @@ __device__ __forceinline__ bool super_of(const Params& p, int id, Super& it) {
     s.t0 = (2 * st + w) * p.tpi;
     s.tlast = min(s.t0 + p.tpi, (int)p.N) - 1;
     s.k0 = s.k1 = 0;
-    if (s.tlast >= s.t0) {
+    if (s.tlast >= s.t0 && p.cmp) {
+      s.k1 = (int)(((s.tlast + 1) / p.cmpBK + 63) / 64);  // tiles of the formed pooled rows
+      if (s.k1 > 0) {
+        it.u0 = 0;
+        it.u1 = max(it.u1, s.k1);
+      }
+    } else if (s.tlast >= s.t0) {
       s.k0 = (s.t0 - (int)p.W + 1 > 0 ? s.t0 - (int)p.W + 1 : 0) / 64;
       s.k1 = s.tlast / 64 + 1;
       it.u0 = min(it.u0, s.k0);
@@ -264,8 +272,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const __grid_c
       const int t = s.t0 + kt_row;
       const bool ok = kt_row < p.tpi && t <= s.tlast;
       const int64_t j = (int64_t)c.it.kh * p.g + hh;
-      const int klo = t - (int)p.W + 1 > 0 ? t - (int)p.W + 1 : 0;
-      const int khi = ok ? t : -1;
+      const int klo = p.cmp ? 0 : (t - (int)p.W + 1 > 0 ? t - (int)p.W + 1 : 0);
+      const int khi = !ok ? -1 : p.cmp ? (int)((t + 1) / p.cmpBK) - 1 : t;
       const float lse_r = ok ? p.lse[j * p.N + t] * 1.4426950408889634f : 0.f;
       const float dl = ok ? p.delta[j * p.N + t] : 0.f;
       if (ok && p.accumulate) {  // the row is read back (+=) by the epilogue
@@ -388,6 +396,46 @@ int tc_slide_dq(const fsa_shape* s, const void* Q, const void* K, const void* V,
   if (grid < 1) return FSA_OK;
   tc_slide_dq_kernel<<<grid, kThreads, kSmemBytes, st>>>(p);
   FSA_LAUNCH_CHECK("tc_slide_dq");
+  return FSA_OK;
+}
+
+// Compressed-branch dQ += scale * dS K_cmp: the same
+// query-outer kernel over the formed pooled rows (Kb / Vb bf16 [b][h_K][128]).
+int tc_cmp_dq(const fsa_shape* s, const void* Q, const void* Kb, const void* Vb, const void* dOut,
+              const void* lse, const void* delta, void* dQ, cudaStream_t st) {
+  Params p{};
+  p.Q = (const __nv_bfloat16*)Q;
+  p.K = (const __nv_bfloat16*)Kb;
+  p.V = (const __nv_bfloat16*)Vb;
+  p.dO = (const __nv_bfloat16*)dOut;
+  p.lse = (const float*)lse;
+  p.delta = (const float*)delta;
+  p.dQ = (float*)dQ;
+  p.N = s->N;
+  p.h = s->h;
+  p.h_K = s->h_K;
+  p.g = s->h / s->h_K;
+  p.W = s->W;
+  p.cmp = 1;
+  p.cmpBK = s->B_K;
+  p.tpi = (int)(kRows / p.g);
+  p.n_super = (p.N + 2 * p.tpi - 1) / (2 * p.tpi);
+  p.accumulate = 1;
+  p.scale = (float)s->scale;
+  p.scale_log2 = (float)(s->scale * 1.4426950408889634);
+  const int64_t b = s->N / s->B_K;
+  int rc = make_tmap_tokens(&p.tmQ, Q, p.N, p.h, (int)p.g, p.tpi);
+  if (!rc) rc = make_tmap_tokens(&p.tmO, dOut, p.N, p.h, (int)p.g, p.tpi);
+  if (!rc) rc = make_tmap_tokens(&p.tmK, Kb, b, p.h_K, 1, 64);
+  if (!rc) rc = make_tmap_tokens(&p.tmV, Vb, b, p.h_K, 1, 64);
+  if (rc) return rc;
+  cudaFuncSetAttribute(tc_slide_dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+  int64_t items = p.h_K * p.n_super;
+  int grid = num_sms();
+  if (items < grid) grid = (int)items;
+  if (grid < 1) return FSA_OK;
+  tc_slide_dq_kernel<<<grid, kThreads, kSmemBytes, st>>>(p);
+  FSA_LAUNCH_CHECK("tc_cmp_dq");
   return FSA_OK;
 }
 

@@ -376,6 +376,10 @@ def test_nsa_step_vs_oracle(run_dt):
 @pytest.mark.parametrize("kw,run_dt", [
     (dict(N=512, d_K=16, d_V=24, h=4, h_K=2, B_K=16, T=4, W=64), "f64"),
     (dict(N=1000, d_K=32, d_V=32, h=6, h_K=3, B_K=8, T=5, W=40), "f32"),
+    # tensor-core path (bf16, d = 128): K8 compressed mode + query-outer dQ
+    (dict(N=4096, d_K=128, d_V=128, h=8, h_K=2, B_K=32, T=8, W=256), "bf16"),
+    (dict(N=2048, d_K=128, d_V=128, h=7, h_K=1, B_K=32, T=6, W=128), "bf16"),
+    (dict(N=4800, d_K=128, d_V=128, h=4, h_K=4, B_K=16, T=8, W=64), "bf16"),
 ])
 def test_compressed_backward_vs_oracle(kw, run_dt):
     """fsa_cmp_bwd (generic kernels) at the reference's own tolerances for f64."""

@@ -57,6 +57,8 @@ def main():
     ap.add_argument("--nsa", action="store_true",
                     help="also time the selected branch alone: FSA (kv-major, tcgen05) vs the NSA "
                          "query-major baseline (query_major.selected_forward)")
+    ap.add_argument("--full", action="store_true",
+                    help="also time the step with the compressed-branch + gate backward (full=True)")
     a = ap.parse_args()
     rows = []
     for name, spec, bwd in CONFIGS:
@@ -92,6 +94,17 @@ def main():
             row["sel_fwd_nsa_ms"] = round(time_it(
                 lambda: query_major.selected_forward(L(q), L(k), L(v), sel, cfg), a.steps, a.warmup), 3)
             row["fsa_speedup"] = round(row["sel_fwd_nsa_ms"] / row["sel_fwd_fsa_ms"], 2)
+            if bwd:
+                row["sel_bwd_fsa_ms"] = round(time_it(
+                    lambda: kv_major.selected_backward(L(q), L(k), L(v), sel, L(do), cfg), 2, 1), 3)
+                row["sel_bwd_nsa_ms"] = round(time_it(
+                    lambda: query_major.selected_backward(L(q), L(k), L(v), sel, L(do), cfg), 2, 1), 3)
+                row["fsa_bwd_speedup"] = round(row["sel_bwd_nsa_ms"] / row["sel_bwd_fsa_ms"], 2)
+        if a.full and bwd:
+            def full_step():
+                _, c_ = nsa.nsa_forward(q, k, v, tau, cfg)
+                nsa.nsa_backward(c_, do, full=True)
+            row["fwd_bwd_full_ms"] = round(time_it(full_step, 2, 1), 3)
         rows.append(row)
         print(json.dumps(row), flush=True)
         del q, k, v, do, tau, ctx
@@ -102,10 +115,12 @@ def main():
         print(f"| {r['config']} | {r['N']} | {r['g']} | {r['fwd_ms']} | {r['fwd_tflops']} | "
               f"{r.get('fwd_bwd_ms', '-')} | {r.get('fwd_bwd_tflops', '-')} | {r.get('fwd_bwd_tokens_s', '-')} |")
     if a.nsa:
-        print("\n| config | g | selected fwd FSA ms | NSA query-major ms | FSA speed-up |")
-        print("|---|---|---|---|---|")
+        print("\n| config | g | selected fwd FSA ms | NSA query-major ms | FSA speed-up | "
+              "selected bwd FSA ms | NSA query-major bwd ms | FSA bwd speed-up |")
+        print("|---|---|---|---|---|---|---|---|")
         for r in rows:
-            print(f"| {r['config']} | {r['g']} | {r['sel_fwd_fsa_ms']} | {r['sel_fwd_nsa_ms']} | {r['fsa_speedup']}x |")
+            print(f"| {r['config']} | {r['g']} | {r['sel_fwd_fsa_ms']} | {r['sel_fwd_nsa_ms']} | {r['fsa_speedup']}x | "
+                  f"{r.get('sel_bwd_fsa_ms', '-')} | {r.get('sel_bwd_nsa_ms', '-')} | {r.get('fsa_bwd_speedup', '-')}x |")
 
 
 if __name__ == "__main__":
