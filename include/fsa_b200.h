@@ -242,6 +242,9 @@ int fsa_check_finite(int dtype, const void* x, int64_t n, int32_t* flag, void* s
 void fsa_debug_bwd_trace(void* device_buf);
 void fsa_debug_dq_trace(void* device_buf);
 void fsa_debug_qo_trace(void* device_buf);
+/* Debugging: TMA tile::gather4 / tile::scatter4 round trip of n rows (tools/gather4_test.py). */
+int fsa_debug_gather4_test(const void* src, int64_t rows, const int32_t* idx, const int32_t* idx2,
+                           int n, int box_rows, void* out, void* out2, int64_t rows2, void* stream);
 
 #ifdef __cplusplus
 }

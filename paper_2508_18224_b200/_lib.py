@@ -74,6 +74,7 @@ SIGNATURES = {
     "fsa_debug_bwd_trace": ([_vp], None),
     "fsa_debug_dq_trace": ([_vp], None),
     "fsa_debug_qo_trace": ([_vp], None),
+    "fsa_debug_gather4_test": ([_vp, ctypes.c_int64, _vp, _vp, _i, _i, _vp, _vp, ctypes.c_int64, _vp], _i),
     "fsa_check_finite": ([_i, _vp, _i64, _vp, _vp], _i),
 }
 

@@ -84,6 +84,24 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     if (clock64() - t0 > (1ll << 34)) mbar_stuck(bar, parity);
   }
 }
+// Spin on test_wait (never suspends): try_wait may park the thread for
+// thousands of cycles past a tcgen05.commit-driven phase flip (measured in the
+// K8 timeline: ~4k cycles), so latency-critical consumers poll instead.
+// A short __nanosleep between probes hands the issue slots to the warps that
+// share the SM sub-partition (a hot spin measurably slows their softmax).
+__device__ __forceinline__ void mbar_spin(uint32_t bar, uint32_t parity) {
+  if (mbar_test(bar, parity)) return;
+  const long long t0 = clock64();
+  for (;;) {
+    __nanosleep(20);
+    if (mbar_test(bar, parity)) return;
+    if (clock64() - t0 > (1ll << 34)) mbar_stuck(bar, parity);
+  }
+}
+__device__ __forceinline__ void mbar_spin_warp(uint32_t bar, uint32_t parity) {
+  if ((threadIdx.x & 31) == 0) mbar_spin(bar, parity);
+  __syncwarp();
+}
 // Whole-warp wait by one lane: the other 31 lanes do not poll the barrier
 // (hundreds of spinning threads congest the SM's barrier unit and slow down
 // every other probe, e.g. the MMA issuer's); __syncwarp publishes the result.
@@ -118,6 +136,31 @@ __device__ __forceinline__ void prefetch_l2(const void* ptr) {
 }
 
 // ---------------------------------------------------------------- TMA
+// 4 arbitrary rows (r[0..3]) x 64 features from column col of a 2-D row map
+// (box (64, 1)) -> 4 x 128 B at dst (SW128 rows), completing on bar.
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const void* map, int col, const int32_t* r,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+      "l"(map), "r"(col), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// this thread's bulk stores have finished reading shared memory
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// the reverse: 4 x 128 B from src (SW128 rows) to rows r[0..3] (bulk group);
+// rows outside the map are dropped
+__device__ __forceinline__ void tma_scatter4(const void* map, int col, const int32_t* r, uint32_t src) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.tile::scatter4.bulk_group"
+      " [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(map),
+      "r"(col), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(src)
+      : "memory");
+}
 // arrive + announce tx_bytes the TMA loads of this phase will complete
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t tx_bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tx_bytes)
@@ -253,6 +296,19 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
       : "r"(taddr));
 #pragma unroll
   for (int k = 0; k < 32; ++k) v[k] = __uint_as_float(r[k]);
+}
+// 16 consecutive fp32 columns of this thread's TMEM lane
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+#pragma unroll
+  for (int k = 0; k < 16; ++k) v[k] = __uint_as_float(r[k]);
 }
 
 // ---------------------------------------------------------------- descriptors

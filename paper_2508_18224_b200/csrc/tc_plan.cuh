@@ -62,5 +62,7 @@ namespace fsa {
 // TMA descriptor of a token-major [N][heads][128] bf16 tensor, box (64, heads_box, tok_box)
 int make_tmap_tokens(CUtensorMap* map, const void* base, int64_t N, int64_t heads, int heads_box,
                      int tok_box);
+// 2-D [rows][128] bf16 view, box (64, box_rows): the tile::gather4 / scatter4 operand
+int make_tmap_rows(CUtensorMap* map, const void* base, int64_t rows, int box_rows);
 
 }  // namespace fsa

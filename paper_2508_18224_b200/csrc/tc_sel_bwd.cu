@@ -19,8 +19,10 @@
 // Roles: warps 0-7 two softmax warpgroups that ping-pong over items (wg owns
 // items n with n % 2 == wg and its own Q/dO, S/dP and P/dS stages; after its
 // item's products land it stages the dQ epilogue in its now-free P/dS smem),
-// warps 8-11 cp.async gather loaders (one item's gather kept in flight), warp
-// 12 MMA issuer (S/dP of item n+1 issued ahead of the products of item n).
+// warps 8-11 cp.async gather loaders (one item's gather kept in flight; TMA
+// tile::gather4 measured ~70 cycles per 512 B request -- too slow for 64 KB
+// items), warp 12 the MMA issuer (S/dP of item n+1 issued ahead of the
+// products of item n).
 // Tasks are claimed dynamically, head-major (tc_sched.cuh).  The sliding
 // branch's backward runs the same kernel with each block's contiguous token
 // window as its rows and a band mask (oracle.py:102-131).
@@ -42,7 +44,6 @@ constexpr uint32_t kOffK = 4 * kTile;       // K [2 halves][64][128 B] = 16384
 constexpr uint32_t kOffV = kOffK + 16384;
 constexpr uint32_t kOffP = kOffV + 16384;   // P[2]  [128][128 B]
 constexpr uint32_t kOffDS = kOffP + 32768;  // dS[2] [128][128 B]
-constexpr uint32_t kStStride = 80;          // dq staging (inside the wg's P stage)
 constexpr uint32_t kOffBar = kOffDS + 32768;
 enum {
   // smem stages (Q/dO, P/dS) by item parity; TMEM stages (S|dP, then dQ) by item mod 3
@@ -63,7 +64,8 @@ constexpr uint32_t kIdKV = idesc_bf16(128, 64, true, true);   // dV^T, dK^T
 constexpr uint32_t kIdQ = idesc_bf16(128, 128, false, true);  // dQ
 
 struct Params {
-  CUtensorMap tmQ, tmO, tmK, tmV;  // sliding mode: TMA boxes (contiguous window rows)
+  CUtensorMap tmQ, tmO, tmK, tmV;  // sliding / compressed modes: TMA token boxes
+  CUtensorMap tmDQ;                 // dq partial rows [h N T][128] (scatter4 stores)
   long long* trace;  // debug timeline (CTA 0, first 256 items), null in production
   const __nv_bfloat16 *Q, *K, *V, *dO;
   const float *lse, *delta;
@@ -167,7 +169,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
     mbar_init(bar(B_KAE), 128);
     for (int k = 0; k < kRingDepth; ++k) {
       mbar_init(bar(B_RF + k), 1);
-      mbar_init(bar(B_RE + k), 385);  // 256 softmax + 128 loader + 1 MMA
+      mbar_init(bar(B_RE + k), 137);  // 8 softmax warps + 128 loader threads + MMA warp
     }
     fence_mbar_init();
   }
@@ -205,7 +207,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
         if (task < 0) break;
         const TaskRows tr = rows_of(p, task);
         if (tr.nitems == 0) continue;
-        mbar_wait(bar(B_KVE), (uint32_t)((kseq & 1) ^ 1));
+        mbar_spin(bar(B_KVE), (uint32_t)((kseq & 1) ^ 1));
         if (lr == 0) {
           mbar_arrive_expect_tx(bar(B_KVF), 32768u);
 #pragma unroll
@@ -218,7 +220,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
         }
         for (int c = 0; c < tr.nitems; ++c, ++n) {
           const int s = (int)(n & 1);
-          mbar_wait(bar(B_QDE + s), (uint32_t)(((n >> 1) & 1) ^ 1));
+          mbar_spin(bar(B_QDE + s), (uint32_t)(((n >> 1) & 1) ^ 1));
           if (lr == 0) {
             const int t0 = (int)(tr.beg + (int64_t)c * p.tpi);
             mbar_arrive_expect_tx(bar(B_QDF + s), 4u * box);
@@ -241,7 +243,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
       if (task < 0) break;
       const TaskRows tr = rows_of(p, task);
       if (tr.nitems == 0) continue;
-      mbar_wait(bar(B_KVE), (uint32_t)((kseq & 1) ^ 1));
+      mbar_spin(bar(B_KVE), (uint32_t)((kseq & 1) ^ 1));
       {  // warps 8,9: K rows 0-31, 32-63; warps 10,11: V rows 0-31, 32-63
         const int lw = warp - 8, row0 = (lw & 1) * 32;
         const __nv_bfloat16* src =
@@ -260,7 +262,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
         const uint32_t par = (uint32_t)(((n >> 1) & 1) ^ 1);
         if (!mbar_test(bar(B_QDE + s), par)) {
           publish();
-          mbar_wait(bar(B_QDE + s), par);
+          mbar_spin(bar(B_QDE + s), par);
         }
         int64_t row = 0;
         if (ok) {
@@ -347,6 +349,14 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
                 K8_TRACE(ns, 1);  // S/dP issued
               }
               __syncwarp();
+              if (p.trace && blockIdx.x == 0 && ns < 256 && (p.trace[255 * 16 + 15] & 1)) {
+                // debug probe: raw S/dP completion latency (serialises the issuer)
+                if (lane == 0) {
+                  while (!mbar_test(bar(B_SDF + tm), (uint32_t)((ns / kTStages) & 1))) {}
+                  K8_TRACE(ns, 13);
+                }
+                __syncwarp();
+              }
               ++a_c;
               ++ns;
               progressed = true;
@@ -420,36 +430,36 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
     const int kt = r / (int)p.g, hh = r % (int)p.g;
     int64_t n = 0, kseq = 0;
     auto kv_epilogue = [&](const TaskRows& tr, int64_t ks) {
-      mbar_wait(bar(B_KAF), (uint32_t)(ks & 1));
+      mbar_spin_warp(bar(B_KAF), (uint32_t)(ks & 1));
       tc_fence_after();
       const int64_t slab = p.slide == 2 ? (tr.beg / p.CH) * p.cstride : 0;
       float* dk = p.dK + slab + ((tr.i * kBK) * p.h_K + tr.kh) * kD + r;
       float* dv = p.dV + slab + ((tr.i * kBK) * p.h_K + tr.kh) * kD + r;
       const int64_t ks_ = p.h_K * kD;  // key stride
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {  // dK keys 0-31, 32-63, then dV
-        float* dst = (q < 2 ? dk : dv) + (int64_t)(q & 1) * 32 * ks_;
-        const float mul = q < 2 ? p.scale : 1.f;
-        float v[32], old[32];
-        if (p.accumulate) {  // batch the 32 loads: one memory latency per chunk
+      for (int q = 0; q < 8; ++q) {  // dK keys 16 at a time, then dV (register budget)
+        float* dst = (q < 4 ? dk : dv) + (int64_t)(q & 3) * 16 * ks_;
+        const float mul = q < 4 ? p.scale : 1.f;
+        float v[16], old[16];
+        if (p.accumulate) {  // batch the 16 loads: one memory latency per chunk
 #pragma unroll
-          for (int c = 0; c < 32; ++c) old[c] = __ldcg(dst + c * ks_);
+          for (int c = 0; c < 16; ++c) old[c] = __ldcg(dst + c * ks_);
         }
-        tmem_ld32(tmem + lb + (q < 2 ? kColDK : kColDV) + (q & 1) * 32, v);
+        tmem_ld16(tmem + lb + (q < 4 ? kColDK : kColDV) + (q & 3) * 16, v);
         tmem_wait_ld();
         if (p.accumulate) {
 #pragma unroll
-          for (int c = 0; c < 32; ++c) dst[c * ks_] = old[c] + v[c] * mul;
+          for (int c = 0; c < 16; ++c) dst[c * ks_] = old[c] + v[c] * mul;
         } else {
 #pragma unroll
-          for (int c = 0; c < 32; ++c) dst[c * ks_] = v[c] * mul;
+          for (int c = 0; c < 16; ++c) dst[c * ks_] = v[c] * mul;
         }
       }
       tc_fence_before();
       mbar_arrive(bar(B_KAE));
     };
     for (int k = 0;; ++k) {
-      const int32_t task = ring.consume(k);
+      const int32_t task = ring.consume_warp(k);
       if (task < 0) break;
       const TaskRows tr = rows_of(p, task);
       if (p.accumulate && tr.nitems > 0) {
@@ -473,22 +483,40 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
         }
         continue;
       }
-      // entries of this warpgroup's items (every other item), one own item ahead
+      // Per-row inputs of this warpgroup's items (every other item), loaded
+      // ahead: the list entry two own items ahead, the token's lse / delta
+      // (scattered [h][N] reads, mostly HBM misses) one own item ahead -- the
+      // loads would otherwise sit between the S/dP landing and the softmax.
       const int c0 = (int)((wg - n) & 1);
-      int32_t ent_next = kt < p.tpi ? entry_at(p, tr, (int64_t)c0 * p.tpi + kt) : 0;
+      auto row_t = [&](int64_t pos, int32_t ent, int64_t& t, int64_t& slot) -> bool {
+        if (kt >= p.tpi || pos >= tr.ntok) return false;
+        token_of(p, tr, pos, ent, t, slot);
+        return true;
+      };
+      auto stats_of = [&](int64_t pos, int32_t ent, float& lz, float& dz) {
+        int64_t t, slot;
+        lz = dz = 0.f;
+        if (row_t(pos, ent, t, slot)) {
+          const int64_t j = tr.kh * p.g + hh;
+          lz = __ldg(p.lse + j * p.N + t);
+          dz = __ldg(p.delta + j * p.N + t);
+        }
+      };
+      int32_t ent_a = kt < p.tpi ? entry_at(p, tr, (int64_t)c0 * p.tpi + kt) : 0;        // item c
+      int32_t ent_b = kt < p.tpi ? entry_at(p, tr, (int64_t)(c0 + 2) * p.tpi + kt) : 0;  // item c + 2
+      float lse_a, dl_a;
+      stats_of((int64_t)c0 * p.tpi + kt, ent_a, lse_a, dl_a);
       for (int c = 0; c < tr.nitems; ++c, ++n) {
         if ((int)(n & 1) != wg) continue;
         const int s = (int)(n & 1);
         const int64_t pos = (int64_t)c * p.tpi + kt;
-        const bool ok = kt < p.tpi && pos < tr.ntok;
-        const int32_t ent = ent_next;
-        ent_next = kt < p.tpi ? entry_at(p, tr, pos + 2 * p.tpi) : 0;
+        const int32_t ent = ent_a;
+        const float lse_raw = lse_a, dl = dl_a;
         int klo = 0, khi = -1;  // visible keys of the block: [klo, khi]
         int64_t drow = -1;
-        float lse_r = 0.f, dl = 0.f;
+        int64_t t, slot;
+        const bool ok = row_t(pos, ent, t, slot);
         if (ok) {
-          int64_t t, slot;
-          token_of(p, tr, pos, ent, t, slot);
           const int64_t j = tr.kh * p.g + hh;
           drow = (j * p.N + t) * p.T + slot;
           // compressed mode: pooled row j is formed for t iff j < (t + 1) / B_K
@@ -498,27 +526,35 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
             const int64_t lo = t - p.W + 1 - tr.i * kBK;
             klo = lo > 0 ? (int)lo : 0;
           }
-          lse_r = p.lse[j * p.N + t] * 1.4426950408889634f;
-          dl = p.delta[j * p.N + t];
         }
+        const float lse_r = lse_raw * 1.4426950408889634f;
         const bool full = __all_sync(0xffffffffu, klo == 0 && khi == kBK - 1);
         const int tm = (int)(n % kTStages);
         const uint32_t tpar = (uint32_t)((n / kTStages) & 1);
-        mbar_wait(bar(B_SDF + tm), tpar);
+        mbar_spin_warp(bar(B_SDF + tm), tpar);
         if (r == 0) K8_TRACE(n, 2);  // S/dP landed
+        // next own item's loads go out now, ahead of this item's dq stores (a
+        // load issued behind 32 KB of stores waits for the LSU queue to drain)
+        stats_of(pos + 2 * p.tpi, ent_b, lse_a, dl_a);
+        ent_a = ent_b;
+        ent_b = kt < p.tpi ? entry_at(p, tr, pos + 4 * p.tpi) : 0;
         tc_fence_after();
         unsigned char* prow = smem + kOffP + s * 16384u;
         unsigned char* drw = smem + kOffDS + s * 16384u;
+        if (!p.no_dq) {  // the previous own item's dq scatter has read these buffers
+          if (lane < 16) bulk_wait_read();
+          __syncwarp();
+        }
 #pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {  // 32 key columns at a time (register budget)
-          float sv[32], dp[32];
-          tmem_ld32(tmem + lb + 128u * tm + hf * 32, sv);
-          tmem_ld32(tmem + lb + 128u * tm + 64 + hf * 32, dp);
+        for (int hf = 0; hf < 4; ++hf) {  // 16 key columns at a time (register budget: 13 warps -> 128)
+          float sv[16], dp[16];
+          tmem_ld16(tmem + lb + 128u * tm + hf * 16, sv);
+          tmem_ld16(tmem + lb + 128u * tm + 64 + hf * 16, dp);
           tmem_wait_ld();
-          uint32_t pp[16], dd[16];
+          uint32_t pp[8], dd[8];
 #pragma unroll
-          for (int c2 = 0; c2 < 32; c2 += 2) {
-            const int key = hf * 32 + c2;
+          for (int c2 = 0; c2 < 16; c2 += 2) {
+            const int key = hf * 16 + c2;
             float p0 = ex2(fmaf(sv[c2], p.scale_log2, -lse_r));
             float p1 = ex2(fmaf(sv[c2 + 1], p.scale_log2, -lse_r));
             if (!full) {
@@ -530,10 +566,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
             dd[c2 >> 1] = pack_bf16(p0 * (dp[c2] - dl), p1 * (dp[c2 + 1] - dl));
           }
 #pragma unroll
-          for (int c4 = 0; c4 < 4; ++c4) {
-            *reinterpret_cast<uint4*>(prow + sw128_off(r, hf * 4 + c4)) =
+          for (int c4 = 0; c4 < 2; ++c4) {
+            *reinterpret_cast<uint4*>(prow + sw128_off(r, hf * 2 + c4)) =
                 make_uint4(pp[4 * c4], pp[4 * c4 + 1], pp[4 * c4 + 2], pp[4 * c4 + 3]);
-            *reinterpret_cast<uint4*>(drw + sw128_off(r, hf * 4 + c4)) =
+            *reinterpret_cast<uint4*>(drw + sw128_off(r, hf * 2 + c4)) =
                 make_uint4(dd[4 * c4], dd[4 * c4 + 1], dd[4 * c4 + 2], dd[4 * c4 + 3]);
           }
         }
@@ -547,41 +583,50 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
         if (r == 0) K8_TRACE(n, 3);  // P/dS written
         // products of this item landed -> dQ partial out of TMEM; stage the
         // bf16 rows in this wg's (now consumed) P buffer for coalesced stores
-        mbar_wait(bar(B_DQF + tm), tpar);
+        mbar_spin_warp(bar(B_DQF + tm), tpar);
         if (r == 0) K8_TRACE(n, 5);  // products landed
         tc_fence_after();
         if (p.no_dq) {
           if (c + 1 == tr.nitems) kv_epilogue(tr, kseq);
           continue;
         }
-        unsigned char* st = prow + (warp & 3) * 32 * kStStride;
+        // rows -> SW128 staging tile [2 halves][128 rows][128 B] in this wg's
+        // consumed P (half 0) and dS (half 1) buffers, then 4-row tile::scatter4
+        // stores to the rows' dq partial slots (TMA: no LSU queue, so the next
+        // item's loads are not stuck behind 32 KB of stores)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           float v[32];
           tmem_ld32(tmem + lb + 128u * tm + q * 32, v);
           tmem_wait_ld();
+          unsigned char* half = q < 2 ? prow : drw;
 #pragma unroll
           for (int c4 = 0; c4 < 4; ++c4) {
             const uint4 u = make_uint4(pack_bf16(v[8 * c4] * p.scale, v[8 * c4 + 1] * p.scale),
                                        pack_bf16(v[8 * c4 + 2] * p.scale, v[8 * c4 + 3] * p.scale),
                                        pack_bf16(v[8 * c4 + 4] * p.scale, v[8 * c4 + 5] * p.scale),
                                        pack_bf16(v[8 * c4 + 6] * p.scale, v[8 * c4 + 7] * p.scale));
-            *reinterpret_cast<uint4*>(st + lane * kStStride + c4 * 16) = u;
+            *reinterpret_cast<uint4*>(half + sw128_off(r, (q & 1) * 4 + c4)) = u;
           }
-          if (q == 3) {
-            tc_fence_before();
-            mbar_arrive(bar(B_SDE + tm));  // TMEM stage free for S/dP of item n+3
-            if (r == 0) K8_TRACE(n, 6);  // dQ read out of TMEM
-          }
-          __syncwarp();
+        }
+        tc_fence_before();
+        mbar_arrive(bar(B_SDE + tm));  // TMEM stage free for S/dP of item n+3
+        if (r == 0) K8_TRACE(n, 6);  // dQ read out of TMEM
+        fence_proxy_async();
+        __syncwarp();
+        {
+          const int grp = lane & 7, hf = lane >> 3;  // lanes 0-15: 8 row groups x 2 halves
+          int32_t rows[4];
 #pragma unroll
-          for (int it = 0; it < 4; ++it) {
-            const int rr = it * 8 + (lane >> 2), ch = lane & 3;
-            const int64_t d = __shfl_sync(0xffffffffu, drow, rr);
-            const uint4 u = *reinterpret_cast<const uint4*>(st + rr * kStStride + ch * 16);
-            if (d >= 0) __stcs(reinterpret_cast<uint4*>(p.dq + d * kD + q * 32 + ch * 8), u);  // streaming: keep Q/dO in L2
+          for (int i = 0; i < 4; ++i) {
+            const int64_t d = __shfl_sync(0xffffffffu, drow, 4 * grp + i);
+            rows[i] = d >= 0 ? (int32_t)d : INT32_MAX;  // out of the map: dropped
           }
-          __syncwarp();
+          if (lane < 16) {
+            tma_scatter4(&p.tmDQ, hf * 64, rows,
+                         smem_u32(hf ? drw : prow) + (uint32_t)(32 * (warp & 3) + 4 * grp) * 128u);
+            bulk_commit();
+          }
         }
         if (r == 0) K8_TRACE(n, 7);  // dQ rows stored
         if (c + 1 == tr.nitems) kv_epilogue(tr, kseq);
@@ -590,6 +635,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
     }
   }
 
+  if (warp < 8 && lane < 16) bulk_wait_all();  // dq scatters complete before exit
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {
@@ -657,6 +703,8 @@ int tc_sel_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V, 
   p.offsets = offsets;
   p.qlist = qlist;
   p.counter = const_cast<int32_t*>(work) + p.ntask + 1;
+  int rc = make_tmap_rows(&p.tmDQ, dq_buf, s->h * s->N * s->T, 1);  // scatter4 dq rows
+  if (rc) return rc;
   return launch_bwd(p, st);
 }
 

@@ -22,6 +22,8 @@ def main():
     nsa.nsa_backward(ctx, do)
     torch.cuda.synchronize()
     buf = torch.zeros(256 * 16, dtype=torch.int64, device="cuda")
+    if os.environ.get("K8_PROBE"):
+        buf[255 * 16 + 15] = 1  # raw S/dP completion probe (slot 13)
     lib = _lib.lib()
     lib.fsa_debug_bwd_trace(ctypes.c_void_p(buf.data_ptr()))
     if mode == "sel":
@@ -35,11 +37,11 @@ def main():
     if mode == "sel":
         pass
     t0 = int(t[0, 0])
-    names = ["gather", "sdp_iss", "sdp_land", "pds_done", "prod_iss", "prod_land", "dq_tmem", "dq_store", "prod_rdy", "pds_w0", "pds_w1", "pds_w2", "pds_w3"]
+    names = ["gather", "sdp_iss", "sdp_land", "pds_done", "prod_iss", "prod_land", "dq_tmem", "dq_store", "prod_rdy", "pds_w0", "pds_w1", "pds_w2", "pds_w3", "sdp_raw", "ld_wait", "ld_free"]
     print("item " + " ".join(f"{n:>9}" for n in names) + "   (cycles from item 0 gather)")
     prev = None
     for i in range(0, 120):
-        row = [int(t[i, j]) - t0 if int(t[i, j]) else -1 for j in range(13)]
+        row = [int(t[i, j]) - t0 if int(t[i, j]) else -1 for j in range(16)]
         print(f"{i:4d} " + " ".join(f"{x:9d}" for x in row))
 
 
