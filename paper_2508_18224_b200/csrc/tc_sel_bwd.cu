@@ -92,10 +92,11 @@ struct Params {
 
 // Rows of a task: the selected mode reads them from the inverse CSR; the
 // sliding mode uses the contiguous window of tokens [64 i, 64 i + 63 + W - 1].
+template <int SL>
 __device__ __forceinline__ TaskRows rows_of(const Params& p, int32_t task) {
-  if (!p.slide) return task_rows(task, p.offsets, p.b, p.tpi);
+  if (SL == 0) return task_rows(task, p.offsets, p.b, p.tpi);
   TaskRows r;
-  if (p.slide == 2) {  // task = (kv head, pooled-row tile, token chunk), chunk fastest
+  if (SL == 2) {  // task = (kv head, pooled-row tile, token chunk), chunk fastest
     const int64_t per = p.nct * p.nch;
     r.kh = task / per;
     r.i = (task % per) / p.nch;
@@ -115,16 +116,18 @@ __device__ __forceinline__ TaskRows rows_of(const Params& p, int32_t task) {
   return r;
 }
 // query-list entry at position pos of a task (selected mode; loaded ahead of use)
+template <int SL>
 __device__ __forceinline__ int32_t entry_at(const Params& p, const TaskRows& tr, int64_t pos) {
-  return (p.slide || pos >= tr.ntok) ? 0 : __ldg(p.qlist + tr.kh * p.N * p.T + tr.beg + pos);
+  return (SL != 0 || pos >= tr.ntok) ? 0 : __ldg(p.qlist + tr.kh * p.N * p.T + tr.beg + pos);
 }
 // token and slot of list position pos of a task (ent = entry_at(pos))
+template <int SL>
 __device__ __forceinline__ void token_of(const Params& p, const TaskRows& tr, int64_t pos,
                                          int32_t ent, int64_t& t, int64_t& slot) {
-  if (!p.slide) {
+  if (SL == 0) {
     t = p.fdT.div((uint32_t)ent);
     slot = ent - t * p.T;
-  } else if (p.slide == 2) {
+  } else if (SL == 2) {
     t = tr.beg + pos;
     slot = 0;
   } else {
@@ -142,6 +145,9 @@ struct TaskFifo {
   __device__ int32_t pop() { return task[head++ & 3]; }
 };
 
+// kMode: 0 selected (gathered rows, dq partials), 1 sliding window, 2 compressed
+// (compile-time: each mode carries only its own code -- instruction-cache footprint)
+template <int SL>
 __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -151,6 +157,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
   Ring ring{bar(B_RF), bar(B_RE), reinterpret_cast<volatile int32_t*>(smem + kOffRing)};
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffTmem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool ACC = SL == 1 && p.accumulate;  // dK/dV += (only the sliding mode reads them back)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < 2; ++s) {
@@ -196,7 +203,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
       kv_pend = false;
       pend = 0;
     };
-    if (p.slide) {
+    if (SL != 0) {
       // Sliding mode: an item's rows are TPI consecutive tokens x g heads and
       // the task's keys 64 consecutive rows -> TMA boxes (one lane issues,
       // the other loader threads just arrive).
@@ -205,7 +212,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
         if (lr == 0) ring.produce(k, p.counter, p.ntask);
         const int32_t task = ring.consume(k);
         if (task < 0) break;
-        const TaskRows tr = rows_of(p, task);
+        const TaskRows tr = rows_of<SL>(p, task);
         if (tr.nitems == 0) continue;
         mbar_spin(bar(B_KVE), (uint32_t)((kseq & 1) ^ 1));
         if (lr == 0) {
@@ -241,7 +248,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
       if (lr == 0) ring.produce(k, p.counter, p.ntask);
       const int32_t task = ring.consume(k);
       if (task < 0) break;
-      const TaskRows tr = rows_of(p, task);
+      const TaskRows tr = rows_of<SL>(p, task);
       if (tr.nitems == 0) continue;
       mbar_spin(bar(B_KVE), (uint32_t)((kseq & 1) ^ 1));
       {  // warps 8,9: K rows 0-31, 32-63; warps 10,11: V rows 0-31, 32-63
@@ -252,13 +259,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
         asm volatile("cp.async.commit_group;" ::: "memory");
       }
       kv_pend = true;
-      int32_t ent_next = kt < p.tpi ? entry_at(p, tr, kt) : 0;
+      int32_t ent_next = kt < p.tpi ? entry_at<SL>(p, tr, kt) : 0;
       for (int c = 0; c < tr.nitems; ++c, ++n) {
         const int s = (int)(n & 1);
         const int64_t pos = (int64_t)c * p.tpi + kt;
         const bool ok = kt < p.tpi && pos < tr.ntok;
         const int32_t ent = ent_next;
-        ent_next = kt < p.tpi ? entry_at(p, tr, pos + p.tpi) : 0;
+        ent_next = kt < p.tpi ? entry_at<SL>(p, tr, pos + p.tpi) : 0;
         const uint32_t par = (uint32_t)(((n >> 1) & 1) ^ 1);
         if (!mbar_test(bar(B_QDE + s), par)) {
           publish();
@@ -267,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
         int64_t row = 0;
         if (ok) {
           int64_t t, slot;
-          token_of(p, tr, pos, ent, t, slot);
+          token_of<SL>(p, tr, pos, ent, t, slot);
           row = t * p.h + tr.kh * p.g + hh;
         }
         warp_gather_rows32(sb + kOffQ + s * kTile, 16384u, lr & ~31, p.Q + row * kD, ok, lane);
@@ -318,7 +325,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
               a_done = true;
               break;
             }
-            const TaskRows tr = rows_of(p, t);
+            const TaskRows tr = rows_of<SL>(p, t);
             if (tr.nitems == 0) continue;
             a_c = 0;
             a_n = tr.nitems;
@@ -371,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
                              (!first || mbar_test_warp(bar(B_KAE), (uint32_t)(((kseq_b + 1) & 1) ^ 1)));
           if (ready) {
             if (first) {
-              b_tr = rows_of(p, fifo.pop());
+              b_tr = rows_of<SL>(p, fifo.pop());
               b_c = 0;
               ++kseq_b;
             } else {
@@ -391,7 +398,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
               for (int k = 0; k < 8; ++k)
                 mma_bf16(tK, desc_mnmajor(q + k * 2048u, 16384u), desc_mnmajor(ds + k * 2048u, 8192u),
                          kIdKV, (first && k == 0) ? 0u : 1u);
-              if (!p.no_dq) {
+              if (SL == 0) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
                   mma_bf16(tmem + 128u * (uint32_t)tm, desc_kmajor(ds + k * 32u),
@@ -432,7 +439,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
     auto kv_epilogue = [&](const TaskRows& tr, int64_t ks) {
       mbar_spin_warp(bar(B_KAF), (uint32_t)(ks & 1));
       tc_fence_after();
-      const int64_t slab = p.slide == 2 ? (tr.beg / p.CH) * p.cstride : 0;
+      const int64_t slab = SL == 2 ? (tr.beg / p.CH) * p.cstride : 0;
       float* dk = p.dK + slab + ((tr.i * kBK) * p.h_K + tr.kh) * kD + r;
       float* dv = p.dV + slab + ((tr.i * kBK) * p.h_K + tr.kh) * kD + r;
       const int64_t ks_ = p.h_K * kD;  // key stride
@@ -441,13 +448,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
         float* dst = (q < 4 ? dk : dv) + (int64_t)(q & 3) * 16 * ks_;
         const float mul = q < 4 ? p.scale : 1.f;
         float v[16], old[16];
-        if (p.accumulate) {  // batch the 16 loads: one memory latency per chunk
+        if (ACC) {  // batch the 16 loads: one memory latency per chunk
 #pragma unroll
           for (int c = 0; c < 16; ++c) old[c] = __ldcg(dst + c * ks_);
         }
         tmem_ld16(tmem + lb + (q < 4 ? kColDK : kColDV) + (q & 3) * 16, v);
         tmem_wait_ld();
-        if (p.accumulate) {
+        if (ACC) {
 #pragma unroll
           for (int c = 0; c < 16; ++c) dst[c * ks_] = old[c] + v[c] * mul;
         } else {
@@ -461,8 +468,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
     for (int k = 0;; ++k) {
       const int32_t task = ring.consume_warp(k);
       if (task < 0) break;
-      const TaskRows tr = rows_of(p, task);
-      if (p.accumulate && tr.nitems > 0) {
+      const TaskRows tr = rows_of<SL>(p, task);
+      if (ACC && tr.nitems > 0) {
         // the block's dK/dV rows are read back (+=) at the end of the task:
         // pull them into L2 now (512 lines of 128 B over the 256 softmax threads)
         const int x = threadIdx.x;  // 0..255
@@ -474,7 +481,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
         }
       }
       if (tr.nitems == 0) {  // no attending rows: the block's gradients are zero
-        if (p.accumulate || wg != 0 || p.slide == 2) continue;  // (compressed: slab not read)
+        if (ACC || wg != 0 || SL == 2) continue;  // (compressed: slab not read)
         float* dk = p.dK + ((tr.i * kBK) * p.h_K + tr.kh) * kD + r;
         float* dv = p.dV + ((tr.i * kBK) * p.h_K + tr.kh) * kD + r;
         for (int key = 0; key < kBK; ++key) {
@@ -490,7 +497,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
       const int c0 = (int)((wg - n) & 1);
       auto row_t = [&](int64_t pos, int32_t ent, int64_t& t, int64_t& slot) -> bool {
         if (kt >= p.tpi || pos >= tr.ntok) return false;
-        token_of(p, tr, pos, ent, t, slot);
+        token_of<SL>(p, tr, pos, ent, t, slot);
         return true;
       };
       auto stats_of = [&](int64_t pos, int32_t ent, float& lz, float& dz) {
@@ -502,8 +509,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
           dz = __ldg(p.delta + j * p.N + t);
         }
       };
-      int32_t ent_a = kt < p.tpi ? entry_at(p, tr, (int64_t)c0 * p.tpi + kt) : 0;        // item c
-      int32_t ent_b = kt < p.tpi ? entry_at(p, tr, (int64_t)(c0 + 2) * p.tpi + kt) : 0;  // item c + 2
+      int32_t ent_a = kt < p.tpi ? entry_at<SL>(p, tr, (int64_t)c0 * p.tpi + kt) : 0;        // item c
+      int32_t ent_b = kt < p.tpi ? entry_at<SL>(p, tr, (int64_t)(c0 + 2) * p.tpi + kt) : 0;  // item c + 2
       float lse_a, dl_a;
       stats_of((int64_t)c0 * p.tpi + kt, ent_a, lse_a, dl_a);
       for (int c = 0; c < tr.nitems; ++c, ++n) {
@@ -520,9 +527,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
           const int64_t j = tr.kh * p.g + hh;
           drow = (j * p.N + t) * p.T + slot;
           // compressed mode: pooled row j is formed for t iff j < (t + 1) / B_K
-          const int64_t hi = (p.slide == 2 ? (t + 1) / p.cmpBK - 1 : t) - tr.i * kBK;
+          const int64_t hi = (SL == 2 ? (t + 1) / p.cmpBK - 1 : t) - tr.i * kBK;
           khi = hi < kBK - 1 ? (int)hi : kBK - 1;
-          if (p.slide == 1) {
+          if (SL == 1) {
             const int64_t lo = t - p.W + 1 - tr.i * kBK;
             klo = lo > 0 ? (int)lo : 0;
           }
@@ -537,11 +544,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
         // load issued behind 32 KB of stores waits for the LSU queue to drain)
         stats_of(pos + 2 * p.tpi, ent_b, lse_a, dl_a);
         ent_a = ent_b;
-        ent_b = kt < p.tpi ? entry_at(p, tr, pos + 4 * p.tpi) : 0;
+        ent_b = kt < p.tpi ? entry_at<SL>(p, tr, pos + 4 * p.tpi) : 0;
         tc_fence_after();
         unsigned char* prow = smem + kOffP + s * 16384u;
         unsigned char* drw = smem + kOffDS + s * 16384u;
-        if (!p.no_dq) {  // the previous own item's dq scatter has read these buffers
+        if (SL == 0) {  // the previous own item's dq scatter has read these buffers
           if (lane < 16) bulk_wait_read();
           __syncwarp();
         }
@@ -573,7 +580,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
                 make_uint4(dd[4 * c4], dd[4 * c4 + 1], dd[4 * c4 + 2], dd[4 * c4 + 3]);
           }
         }
-        if (p.no_dq) {  // S/dP consumed: the TMEM stage is free right away
+        if (SL != 0) {  // S/dP consumed: the TMEM stage is free right away
           tc_fence_before();
           mbar_arrive(bar(B_SDE + tm));
         }
@@ -586,7 +593,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
         mbar_spin_warp(bar(B_DQF + tm), tpar);
         if (r == 0) K8_TRACE(n, 5);  // products landed
         tc_fence_after();
-        if (p.no_dq) {
+        if (SL != 0) {
           if (c + 1 == tr.nitems) kv_epilogue(tr, kseq);
           continue;
         }
@@ -682,11 +689,17 @@ int launch_bwd(Params& p, cudaStream_t st) {
   cudaMemsetAsync(p.counter, 0, sizeof(int32_t), st);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(tc_sel_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kSmemBytes);
+    cudaFuncSetAttribute(tc_sel_bwd_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+    cudaFuncSetAttribute(tc_sel_bwd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+    cudaFuncSetAttribute(tc_sel_bwd_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
     attr = true;
   }
-  tc_sel_bwd_kernel<<<num_sms(), kThreads, kSmemBytes, st>>>(p);
+  if (p.slide == 1)
+    tc_sel_bwd_kernel<1><<<num_sms(), kThreads, kSmemBytes, st>>>(p);
+  else if (p.slide == 2)
+    tc_sel_bwd_kernel<2><<<num_sms(), kThreads, kSmemBytes, st>>>(p);
+  else
+    tc_sel_bwd_kernel<0><<<num_sms(), kThreads, kSmemBytes, st>>>(p);
   FSA_LAUNCH_CHECK("tc_sel_bwd");
   return FSA_OK;
 }
