@@ -78,11 +78,12 @@ struct Super {
   int u0, u1;  // union of the key-tile ranges
 };
 
+template <int M>
 __device__ __forceinline__ bool super_of(const Params& p, int id, Super& it) {
   if (id >= p.h_K * p.n_super) return false;
   it.kh = id % (int)p.h_K;
   int st = id / (int)p.h_K;
-  if (p.mode != SLIDE) st = (int)p.n_super - 1 - st;  // heavy (late) tokens first
+  if (M != SLIDE) st = (int)p.n_super - 1 - st;  // heavy (late) tokens first
   it.u0 = INT32_MAX;
   it.u1 = 0;
 #pragma unroll
@@ -92,7 +93,7 @@ __device__ __forceinline__ bool super_of(const Params& p, int id, Super& it) {
     s.tlast = min(s.t0 + p.tpi, (int)p.N) - 1;
     s.k0 = s.k1 = 0;
     if (s.tlast >= s.t0) {
-      if (p.mode == SLIDE) {
+      if (M == SLIDE) {
         s.k0 = (s.t0 - (int)p.W + 1 > 0 ? s.t0 - (int)p.W + 1 : 0) / 64;
         s.k1 = s.tlast / 64 + 1;
       } else {
@@ -109,6 +110,7 @@ __device__ __forceinline__ bool super_of(const Params& p, int id, Super& it) {
 }
 
 // Position of one stream in the CTA's sequence of non-empty super items.
+template <int M>
 struct Cursor {
   int n = -1;    // enumeration index
   int seq = -1;  // index among non-empty super items (Q stage sequence)
@@ -117,7 +119,7 @@ struct Cursor {
   __device__ bool advance(const Params& p, int G) {
     for (;;) {
       ++n;
-      if (!super_of(p, (int)blockIdx.x + n * G, it)) return false;
+      if (!super_of<M>(p, (int)blockIdx.x + n * G, it)) return false;
       if (it.u0 == it.u1) continue;
       ++seq;
       rbase = rnext;
@@ -131,6 +133,8 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
   tmem_st32u(taddr, reinterpret_cast<const uint32_t*>(v));
 }
 
+// M: SLIDE / CMP / SCORES at compile time (per-mode code only: instruction-cache footprint)
+template <int M>
 __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -171,7 +175,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
     // value tiles are 64 consecutive rows of one kv head.
     if (lane == 0) {
       const uint32_t qbox = 64u * (uint32_t)(p.g * p.tpi) * 2u;
-      Cursor c;
+      Cursor<M> c;
       int r = 0;
       while (c.advance(p, G)) {
         const int qs = (int)(c.seq & 1);
@@ -183,7 +187,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
           for (int hf = 0; hf < 2; ++hf)
             tma_load_3d(sb + kOffQ + (qs * 2 + w) * kQ + hf * 16384u, &p.tmQ, hf * 64,
                         c.it.kh * (int)p.g, c.it.s[w].t0, bar(B_QF + qs));
-        const bool with_v = p.mode != SCORES;
+        const bool with_v = M != SCORES;
         for (int u = c.it.u0; u < c.it.u1; ++u, ++r) {
           const int v = (int)(r % kKVStages);
           mbar_wait(bar(B_KE + v), (uint32_t)(((r / kKVStages) & 1) ^ 1));
@@ -208,7 +212,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
     // commits KE once per union tile (pass-by when the tile is outside its
     // range; KE counts 2), each S stream QE once per super item (QE counts 2).
     {
-      Cursor c;
+      Cursor<M> c;
       int ns[2] = {0, 0}, np[2] = {0, 0}, nsub[2] = {0, 0};
       while (c.advance(p, G)) {
         const Super& it = c.it;
@@ -255,7 +259,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
               const int v = np[w] & 1;
               const bool first = up == sw.k0, last = up + 1 == sw.k1;
               mbar_wait_warp(bar(B_PF + 2 * w + v), (uint32_t)((np[w] >> 1) & 1));
-              if (p.mode == SCORES) {  // no PV: release the K tile once S is consumed
+              if (M == SCORES) {  // no PV: release the K tile once S is consumed
                 if (elect_one()) mma_commit(bar(B_KE + kv));
                 __syncwarp();
                 ++np[w];
@@ -296,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
     const uint32_t lb = ((uint32_t)((warp & 3) * 32) << 16) + 256u * w;
     const int kt_row = r / (int)p.g, hh = r % (int)p.g;
     int u = 0, n_out = 0;  // tiles processed / sub-items finished by this wg
-    Cursor c;
+    Cursor<M> c;
     while (c.advance(p, G)) {
       const Sub& s = c.it.s[w];
       if (s.k0 >= s.k1) continue;
@@ -304,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
       const bool ok = kt_row < p.tpi && t <= s.tlast;
       const int64_t j = (int64_t)c.it.kh * p.g + hh;
       int klo, khi;  // visible keys [klo, khi]
-      if (p.mode == SLIDE) {
+      if (M == SLIDE) {
         klo = t - (int)p.W + 1 > 0 ? t - (int)p.W + 1 : 0;
         khi = t;
       } else {
@@ -324,7 +328,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
         tmem_ld32(tS + 32, sv + 32);
         tmem_wait_ld();
         const int kbase = kt * 64;
-        if (p.mode != SLIDE && p.scores != nullptr) {
+        if (M != SLIDE && p.scores != nullptr) {
           // group mean over the g heads of this token (rows of a token are
           // adjacent lanes; g divides 32), written by the token's first row
           const float gm = p.score_mul;
@@ -351,7 +355,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
             }
           }
         }
-        if (p.mode == SCORES) {  // S consumed: hand the stage back
+        if (M == SCORES) {  // S consumed: hand the stage back
           tc_fence_before();
           mbar_arrive(bar(B_PF + 2 * w + v));
           continue;
@@ -415,7 +419,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
         if (r == 0) QO_TRACE(w, u, 2);  // P written
         if (lane == 0) QO_TRACE(w + 2, u, 2 + (warp & 3));  // per-warp P arrival
       }
-      if (p.mode == SCORES) continue;
+      if (M == SCORES) continue;
       // epilogue: out = O / l, lse = m + ln l
       if (r == 0) QO_TRACE(w, u - 1, 4);  // epilogue: waiting for O
       mbar_wait_warp(bar(B_OF + w), (uint32_t)(n_out & 1));
@@ -467,15 +471,21 @@ int launch(Params& p, cudaStream_t st) {
   if (rc) return rc;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(tc_qo_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kSmemBytes);
+    cudaFuncSetAttribute(tc_qo_fwd_kernel<SLIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+    cudaFuncSetAttribute(tc_qo_fwd_kernel<CMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+    cudaFuncSetAttribute(tc_qo_fwd_kernel<SCORES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
     attr = true;
   }
   int64_t items = p.h_K * p.n_super;
   int grid = num_sms();
   if (items < grid) grid = (int)items;
   if (grid < 1) return FSA_OK;
-  tc_qo_fwd_kernel<<<grid, kThreads, kSmemBytes, st>>>(p);
+  if (p.mode == SLIDE)
+    tc_qo_fwd_kernel<SLIDE><<<grid, kThreads, kSmemBytes, st>>>(p);
+  else if (p.mode == CMP)
+    tc_qo_fwd_kernel<CMP><<<grid, kThreads, kSmemBytes, st>>>(p);
+  else
+    tc_qo_fwd_kernel<SCORES><<<grid, kThreads, kSmemBytes, st>>>(p);
   return FSA_OK;
 }
 

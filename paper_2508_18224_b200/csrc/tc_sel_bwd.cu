@@ -180,6 +180,18 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
     }
     fence_mbar_init();
   }
+  if (SL != 0) {
+    // TMA boxes fill g * tpi rows of a Q / dO tile; zero the rest once (they
+    // carry P = dS = 0, but stale shared memory may hold NaN patterns and
+    // 0 * NaN would poison the dK / dV row sums)
+    const int used = (int)(p.g * p.tpi);
+    for (int e = threadIdx.x; e < 2 * 2 * 2 * (kRows - used) * 8; e += kThreads) {
+      const int c = e & 7, rr = used + (e >> 3) % (kRows - used), t = (e >> 3) / (kRows - used);
+      const uint32_t base = (t & 4 ? kOffDO : kOffQ) + (uint32_t)((t >> 1) & 1) * kTile + (uint32_t)(t & 1) * 16384u;
+      *reinterpret_cast<uint4*>(smem + base + rr * 128u + c * 16u) = make_uint4(0u, 0u, 0u, 0u);
+    }
+    fence_proxy_async();
+  }
   if (warp == 0) tmem_alloc<512>(smem_u32(tmem_slot));
   tc_fence_before();
   __syncthreads();

@@ -68,10 +68,11 @@ struct Super {
   int u0, u1;
 };
 
+template <int CM>
 __device__ __forceinline__ bool super_of(const Params& p, int id, Super& it) {
   if (id >= p.h_K * p.n_super) return false;
   it.kh = id % (int)p.h_K;
-  const int st = p.cmp ? (int)p.n_super - 1 - id / (int)p.h_K : id / (int)p.h_K;  // cmp: late (heavy) tokens first
+  const int st = CM ? (int)p.n_super - 1 - id / (int)p.h_K : id / (int)p.h_K;  // cmp: late (heavy) tokens first
   it.u0 = INT32_MAX;
   it.u1 = 0;
 #pragma unroll
@@ -80,7 +81,7 @@ __device__ __forceinline__ bool super_of(const Params& p, int id, Super& it) {
     s.t0 = (2 * st + w) * p.tpi;
     s.tlast = min(s.t0 + p.tpi, (int)p.N) - 1;
     s.k0 = s.k1 = 0;
-    if (s.tlast >= s.t0 && p.cmp) {
+    if (s.tlast >= s.t0 && CM) {
       s.k1 = (int)(((s.tlast + 1) / p.cmpBK + 63) / 64);  // tiles of the formed pooled rows
       if (s.k1 > 0) {
         it.u0 = 0;
@@ -97,13 +98,14 @@ __device__ __forceinline__ bool super_of(const Params& p, int id, Super& it) {
   return true;
 }
 
+template <int CM>
 struct Cursor {
   int n = -1, seq = -1, rbase = 0, rnext = 0;
   Super it;
   __device__ bool advance(const Params& p, int G) {
     for (;;) {
       ++n;
-      if (!super_of(p, (int)blockIdx.x + n * G, it)) return false;
+      if (!super_of<CM>(p, (int)blockIdx.x + n * G, it)) return false;
       if (it.u0 == it.u1) continue;
       ++seq;
       rbase = rnext;
@@ -113,6 +115,8 @@ struct Cursor {
   }
 };
 
+// CM: compressed mode at compile time (per-mode code only)
+template <int CM>
 __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -149,7 +153,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const __grid_c
     // head: one 3-D box per 64-feature half lands as the SW128 K-major tile.
     if (lane == 0) {
       const uint32_t qbox = 64u * (uint32_t)(p.g * p.tpi) * 2u;  // bytes per half tile
-      Cursor c;
+      Cursor<CM> c;
       int r = 0;
       while (c.advance(p, G)) {
         mbar_wait(bar(B_QE), (uint32_t)((c.seq & 1) ^ 1));
@@ -187,7 +191,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const __grid_c
     // S/dP_w of tile u.  KE: one commit per stream per union tile (pass-by
     // outside the sub-item's range; KE counts 2); QE: two per super item.
     {
-      Cursor c;
+      Cursor<CM> c;
       int ns[2] = {0, 0}, nd[2] = {0, 0}, nsub[2] = {0, 0};
       while (c.advance(p, G)) {
         const Super& it = c.it;
@@ -265,15 +269,15 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const __grid_c
     const uint32_t lb = ((uint32_t)((warp & 3) * 32) << 16) + 256u * w;
     const int kt_row = r / (int)p.g, hh = r % (int)p.g;
     int u = 0, n_out = 0;
-    Cursor c;
+    Cursor<CM> c;
     while (c.advance(p, G)) {
       const Sub& s = c.it.s[w];
       if (s.k0 >= s.k1) continue;
       const int t = s.t0 + kt_row;
       const bool ok = kt_row < p.tpi && t <= s.tlast;
       const int64_t j = (int64_t)c.it.kh * p.g + hh;
-      const int klo = p.cmp ? 0 : (t - (int)p.W + 1 > 0 ? t - (int)p.W + 1 : 0);
-      const int khi = !ok ? -1 : p.cmp ? (int)((t + 1) / p.cmpBK) - 1 : t;
+      const int klo = CM ? 0 : (t - (int)p.W + 1 > 0 ? t - (int)p.W + 1 : 0);
+      const int khi = !ok ? -1 : CM ? (int)((t + 1) / p.cmpBK) - 1 : t;
       const float lse_r = ok ? p.lse[j * p.N + t] * 1.4426950408889634f : 0.f;
       const float dl = ok ? p.delta[j * p.N + t] : 0.f;
       if (ok && p.accumulate) {  // the row is read back (+=) by the epilogue
@@ -386,7 +390,7 @@ int tc_slide_dq(const fsa_shape* s, const void* Q, const void* K, const void* V,
   if (rc) return rc;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(tc_slide_dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(tc_slide_dq_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kSmemBytes);
     attr = true;
   }
@@ -394,7 +398,7 @@ int tc_slide_dq(const fsa_shape* s, const void* Q, const void* K, const void* V,
   int grid = num_sms();
   if (items < grid) grid = (int)items;
   if (grid < 1) return FSA_OK;
-  tc_slide_dq_kernel<<<grid, kThreads, kSmemBytes, st>>>(p);
+  tc_slide_dq_kernel<0><<<grid, kThreads, kSmemBytes, st>>>(p);
   FSA_LAUNCH_CHECK("tc_slide_dq");
   return FSA_OK;
 }
@@ -429,12 +433,12 @@ int tc_cmp_dq(const fsa_shape* s, const void* Q, const void* Kb, const void* Vb,
   if (!rc) rc = make_tmap_tokens(&p.tmK, Kb, b, p.h_K, 1, 64);
   if (!rc) rc = make_tmap_tokens(&p.tmV, Vb, b, p.h_K, 1, 64);
   if (rc) return rc;
-  cudaFuncSetAttribute(tc_slide_dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+  cudaFuncSetAttribute(tc_slide_dq_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
   int64_t items = p.h_K * p.n_super;
   int grid = num_sms();
   if (items < grid) grid = (int)items;
   if (grid < 1) return FSA_OK;
-  tc_slide_dq_kernel<<<grid, kThreads, kSmemBytes, st>>>(p);
+  tc_slide_dq_kernel<1><<<grid, kThreads, kSmemBytes, st>>>(p);
   FSA_LAUNCH_CHECK("tc_cmp_dq");
   return FSA_OK;
 }
