@@ -309,10 +309,7 @@ def run_ours(args, rank, world, local_rank):
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic N(0,1) Q/K/V/dOut, U[0,1) gates, random init",
-        "config": {"workload": w["name"], "seq_len": cfg.N, "batch_per_gpu": 1, "q_heads": cfg.h,
-                   "kv_heads": cfg.h_K, "head_dim": cfg.d_K, "block": cfg.B_K, "top_k": cfg.T,
-                   "window": cfg.W, "parallelism": f"batch{world}", "l2": "inputs exceed L2 "
-                   "(Q 268 MB, K/V 67 MB each, partial buffer 4.2 GB); no flush"},
+        "config": arm_config(world),
         "effective_tflops": round(step_flops / (ms / 1e3) / 1e12, 2),
         # dominant kernel: the selected-attention backward (K8)
         "roofline": roof("sel_bwd (K8, tcgen05, selected branch)", k8_flops, k8_ms,
@@ -376,6 +373,16 @@ def cpu_baseline(args, sample_n=CPU_SAMPLE_N, steps=1):
                       f"{cores} processes; {wall:.1f} s wall"}
 
 
+def arm_config(world):
+    """The workload both arms report (the reference arm measures a bounded
+    sample of it; cpu_baseline.sample says which)."""
+    w = WORKLOAD
+    return {"workload": w["name"], "seq_len": w["N"], "batch_per_gpu": 1, "q_heads": w["h"],
+            "kv_heads": w["h_K"], "head_dim": w["d"], "block": w["B_K"], "top_k": w["T"],
+            "window": w["W"], "parallelism": f"batch{world}", "l2": "inputs exceed L2 "
+            "(Q 268 MB, K/V 67 MB each, partial buffer 4.2 GB); no flush"}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return None
@@ -386,8 +393,7 @@ def run_reference(args, rank, world):
         "metric": "NSA fwd+bwd tokens/s (Llama-3-8B attention, 32K, GQA 4)",
         "value": cb["value"], "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic", "config": {"workload": WORKLOAD["name"],
-                                                        "seq_len": n, "sample": cb["sample"]},
+        "dtype": "f64", "data": "synthetic", "config": arm_config(world),
         "cpu_baseline": cb,
         "e2e": {"value": cb["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
