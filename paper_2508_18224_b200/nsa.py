@@ -29,6 +29,7 @@ import torch
 from . import _lib
 from .kv_major import _backward_core, _sel_partials
 from .branches import _cmp_workspace, _slide_bwd_storage, _slide_fwd_storage
+from .config import make_config
 from .selection import SelectionTensor, build_inverse_index
 
 
@@ -54,8 +55,15 @@ class NSAContext:
     lse_cmp: torch.Tensor = None
 
 
-def nsa_forward(q, k, v, tau, cfg):
-    """Returns (combined out (N, h, d_V), ctx)."""
+def nsa_forward(q, k, v, tau, cfg, *, heads=None):
+    """Returns (combined out (N, h, d_V), ctx).
+
+    ``heads=(lo, hi)``: compute only query heads lo..hi-1 of every kv group
+    (the query-head split of parallel.shard_plan).  The compressed branch and
+    the block selection still see the whole group -- the importance scores
+    sum over all g heads of a group (selection.py:105-120) -- then the
+    selected and sliding branches and the combine run on the sub-group only.
+    Out and ctx describe the sub-problem (h = h_K * (hi - lo))."""
     dt = q.dtype
     acc = _lib.acc_dtype(dt)
     dev = q.device
@@ -80,6 +88,23 @@ def nsa_forward(q, k, v, tau, cfg):
               _lib.ptr(idx), st)
     sel = SelectionTensor(idx)
     sel._trusted = True
+    if heads is not None:
+        lo, hi = heads
+        if not 0 <= lo < hi <= cfg.g:
+            raise ValueError(f"heads {heads} outside the group of {cfg.g} query heads")
+        sub = make_config(N=cfg.N, d_K=cfg.d_K, d_V=cfg.d_V, h=cfg.h_K * (hi - lo), h_K=cfg.h_K,
+                          B_K=cfg.B_K, T=cfg.T, B_Q=cfg.B_Q, W=cfg.W,
+                          bytes_per_elem=cfg.bytes_per_elem, min_tile=cfg.min_tile)
+
+        def take(x, axis):  # heads axis of a storage tensor -> the sub-group's heads
+            shp = list(x.shape)
+            y = x.reshape(shp[:axis] + [cfg.h_K, cfg.g] + shp[axis + 1:])
+            y = y.narrow(axis + 1, lo, hi - lo)
+            return y.reshape(shp[:axis] + [sub.h] + shp[axis + 1:]).contiguous()
+
+        q, out_cmp, lse_cmp = take(q, 1), take(out_cmp, 1), take(lse_cmp, 0)
+        cfg = sub
+        s = _lib.shape_of(cfg)
     inv = build_inverse_index(sel, cfg, validate=False)
     # K5 writes the slot partials; the sliding branch runs before the merge so
     # that K6 can apply the gated combine (K12) in the same pass

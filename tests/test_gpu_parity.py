@@ -557,3 +557,30 @@ def test_window_backward_partial_tile_repeatable(full):
             ref = got
         else:
             assert all(torch.equal(a, b) for a, b in zip(got, ref))
+
+
+def test_query_head_split_matches_unsharded():
+    """parallel.QueryShard on the device: the two ranks of a kv head (simulated
+    in one process) reproduce the unsharded step; dK / dV are the sum of the
+    ranks' partials (the all_reduce of the multi-GPU run)."""
+    from paper_2508_18224_b200 import parallel
+
+    cfg = fsa.make_config(N=4096, d_K=128, d_V=128, h=7, h_K=1, B_K=64, T=8, W=256)
+    g = torch.Generator(device="cuda").manual_seed(11)
+    mk = lambda *s: torch.randn(*s, device="cuda", dtype=torch.bfloat16, generator=g)  # noqa: E731
+    q, k, v, do = mk(cfg.N, 7, 128), mk(cfg.N, 1, 128), mk(cfg.N, 1, 128), mk(cfg.N, 7, 128)
+    tau = torch.rand(cfg.N, 3, device="cuda", generator=g)
+    out, ctx = fsa.nsa.nsa_forward(q, k, v, tau, cfg)
+    dQ, dK, dV = fsa.nsa.nsa_backward(ctx, do)
+    parts = []
+    for rank in range(2):
+        sh = parallel.shard_plan(cfg, rank, 2)
+        qg, kk, vv, dd = parallel.query_shard_inputs(sh, q, k, v, do)
+        parts.append(parallel.query_shard_step(sh, qg, kk, vv, tau, dd))
+    o2 = torch.cat([p[0] for p in parts], 1)
+    dq2 = torch.cat([p[1] for p in parts], 1)
+    dk2, dv2 = parts[0][2] + parts[1][2], parts[0][3] + parts[1][3]
+    assert torch.allclose(o2.float(), out.float(), rtol=1e-2, atol=1e-2)
+    for got, ref in ((dq2, dQ), (dk2, dK), (dv2, dV)):
+        err = (got - ref).abs().max().item()
+        assert err <= 1e-3 * ref.abs().max().item(), err
