@@ -35,7 +35,11 @@ namespace {
 using namespace tc;
 
 constexpr int kD = 128, kBK = 64, kRows = 128;
-constexpr int kThreads = 13 * 32;
+// 8 softmax warps + loader warps + 1 MMA warp.  The selected mode gathers with
+// 4 cp.async loader warps (13 warps: 128 registers); the window / compressed
+// modes load by TMA from one lane, so one loader warp (10 warps: 168 registers)
+template <int SL> constexpr int loader_warps() { return SL == 0 ? 4 : 1; }
+template <int SL> constexpr int threads_of() { return (9 + loader_warps<SL>()) * 32; }
 
 constexpr uint32_t kTile = kRows * kD * 2;  // 32768: [2 halves][128][128 B]
 constexpr uint32_t kOffQ = 0;               // Q[2]
@@ -148,7 +152,8 @@ struct TaskFifo {
 // kMode: 0 selected (gathered rows, dq partials), 1 sliding window, 2 compressed
 // (compile-time: each mode carries only its own code -- instruction-cache footprint)
 template <int SL>
-__global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const __grid_constant__ Params p) {
+  constexpr int kLoaders = 32 * loader_warps<SL>();  // loader threads
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -161,7 +166,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < 2; ++s) {
-      mbar_init(bar(B_QDF + s), 128);
+      mbar_init(bar(B_QDF + s), kLoaders);
       mbar_init(bar(B_QDE + s), 1);
       mbar_init(bar(B_PDF + s), 128);
     }
@@ -170,13 +175,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
       mbar_init(bar(B_SDE + s), 128);
       mbar_init(bar(B_DQF + s), 1);
     }
-    mbar_init(bar(B_KVF), 128);
+    mbar_init(bar(B_KVF), kLoaders);
     mbar_init(bar(B_KVE), 1);
     mbar_init(bar(B_KAF), 1);
     mbar_init(bar(B_KAE), 128);
     for (int k = 0; k < kRingDepth; ++k) {
       mbar_init(bar(B_RF + k), 1);
-      mbar_init(bar(B_RE + k), 137);  // 8 softmax warps + 128 loader threads + MMA warp
+      mbar_init(bar(B_RE + k), 8 + kLoaders + 1);  // 8 softmax warps + loader threads + MMA warp
     }
     fence_mbar_init();
   }
@@ -185,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
     // carry P = dS = 0, but stale shared memory may hold NaN patterns and
     // 0 * NaN would poison the dK / dV row sums)
     const int used = (int)(p.g * p.tpi);
-    for (int e = threadIdx.x; e < 2 * 2 * 2 * (kRows - used) * 8; e += kThreads) {
+    for (int e = threadIdx.x; e < 2 * 2 * 2 * (kRows - used) * 8; e += (int)blockDim.x) {
       const int c = e & 7, rr = used + (e >> 3) % (kRows - used), t = (e >> 3) / (kRows - used);
       const uint32_t base = (t & 4 ? kOffDO : kOffQ) + (uint32_t)((t >> 1) & 1) * kTile + (uint32_t)(t & 1) * 16384u;
       *reinterpret_cast<uint4*>(smem + base + rr * 128u + c * 16u) = make_uint4(0u, 0u, 0u, 0u);
@@ -198,7 +203,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp >= 8 && warp < 12) {
+  if (warp >= 8 && warp < 8 + loader_warps<SL>()) {
     // ================================================================ loaders
     const int lr = threadIdx.x - 256;
     const int kt = lr / (int)p.g, hh = lr % (int)p.g;
@@ -304,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
       ++kseq;
     }
     publish();
-  } else if (warp == 12) {
+  } else if (warp == 8 + loader_warps<SL>()) {
     // ================================================================ MMA issuer
     // Two independent in-order streams, polled without blocking:
     //   S stream : S/dP of item m (needs its Q/dO gather, the task's K/V, and
@@ -564,16 +569,24 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
           if (lane < 16) bulk_wait_read();
           __syncwarp();
         }
+        // P / dS in chunks of CW key columns: 16 in the selected mode (13 warps,
+        // 128 registers), 32 in the window / compressed modes (10 warps)
+        constexpr int CW = SL == 0 ? 16 : 32;
 #pragma unroll
-        for (int hf = 0; hf < 4; ++hf) {  // 16 key columns at a time (register budget: 13 warps -> 128)
-          float sv[16], dp[16];
-          tmem_ld16(tmem + lb + 128u * tm + hf * 16, sv);
-          tmem_ld16(tmem + lb + 128u * tm + 64 + hf * 16, dp);
+        for (int hf = 0; hf < 64 / CW; ++hf) {
+          float sv[CW], dp[CW];
+          if constexpr (CW == 16) {
+            tmem_ld16(tmem + lb + 128u * tm + hf * 16, sv);
+            tmem_ld16(tmem + lb + 128u * tm + 64 + hf * 16, dp);
+          } else {
+            tmem_ld32(tmem + lb + 128u * tm + hf * 32, sv);
+            tmem_ld32(tmem + lb + 128u * tm + 64 + hf * 32, dp);
+          }
           tmem_wait_ld();
-          uint32_t pp[8], dd[8];
+          uint32_t pp[CW / 2], dd[CW / 2];
 #pragma unroll
-          for (int c2 = 0; c2 < 16; c2 += 2) {
-            const int key = hf * 16 + c2;
+          for (int c2 = 0; c2 < CW; c2 += 2) {
+            const int key = hf * CW + c2;
             float p0 = ex2(fmaf(sv[c2], p.scale_log2, -lse_r));
             float p1 = ex2(fmaf(sv[c2 + 1], p.scale_log2, -lse_r));
             if (!full) {
@@ -585,10 +598,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_bwd_kernel(const __grid_co
             dd[c2 >> 1] = pack_bf16(p0 * (dp[c2] - dl), p1 * (dp[c2 + 1] - dl));
           }
 #pragma unroll
-          for (int c4 = 0; c4 < 2; ++c4) {
-            *reinterpret_cast<uint4*>(prow + sw128_off(r, hf * 2 + c4)) =
+          for (int c4 = 0; c4 < CW / 8; ++c4) {
+            *reinterpret_cast<uint4*>(prow + sw128_off(r, hf * (CW / 8) + c4)) =
                 make_uint4(pp[4 * c4], pp[4 * c4 + 1], pp[4 * c4 + 2], pp[4 * c4 + 3]);
-            *reinterpret_cast<uint4*>(drw + sw128_off(r, hf * 2 + c4)) =
+            *reinterpret_cast<uint4*>(drw + sw128_off(r, hf * (CW / 8) + c4)) =
                 make_uint4(dd[4 * c4], dd[4 * c4 + 1], dd[4 * c4 + 2], dd[4 * c4 + 3]);
           }
         }
@@ -707,11 +720,11 @@ int launch_bwd(Params& p, cudaStream_t st) {
     attr = true;
   }
   if (p.slide == 1)
-    tc_sel_bwd_kernel<1><<<num_sms(), kThreads, kSmemBytes, st>>>(p);
+    tc_sel_bwd_kernel<1><<<num_sms(), threads_of<1>(), kSmemBytes, st>>>(p);
   else if (p.slide == 2)
-    tc_sel_bwd_kernel<2><<<num_sms(), kThreads, kSmemBytes, st>>>(p);
+    tc_sel_bwd_kernel<2><<<num_sms(), threads_of<2>(), kSmemBytes, st>>>(p);
   else
-    tc_sel_bwd_kernel<0><<<num_sms(), kThreads, kSmemBytes, st>>>(p);
+    tc_sel_bwd_kernel<0><<<num_sms(), threads_of<0>(), kSmemBytes, st>>>(p);
   FSA_LAUNCH_CHECK("tc_sel_bwd");
   return FSA_OK;
 }
