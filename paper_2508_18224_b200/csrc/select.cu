@@ -136,6 +136,7 @@ __global__ void __launch_bounds__(256) topk_stream_kernel(const float* __restric
   // ---- pass 1
   int nsel = 0;
   uint32_t lm = 0u;
+#pragma unroll 4
   for (int base = 0; base < ncand; base += 32) {
     const uint32_t k = keyat(base + lane);
     nsel += __popc(__ballot_sync(0xffffffffu, k != 0u));
@@ -143,6 +144,7 @@ __global__ void __launch_bounds__(256) topk_stream_kernel(const float* __restric
   }
   if (nsel <= T) {
     int out = 0;
+#pragma unroll 4
     for (int base = 0; base < ncand; base += 32) {
       const uint32_t k = keyat(base + lane);
       const unsigned m = __ballot_sync(0xffffffffu, k != 0u);
@@ -166,6 +168,7 @@ __global__ void __launch_bounds__(256) topk_stream_kernel(const float* __restric
   // ---- pass 2: candidates >= theta, packed so that larger = better
   unsigned long long* slots = reinterpret_cast<unsigned long long*>(hist);
   int cand = 0;
+#pragma unroll 4
   for (int base = 0; base < ncand; base += 32) {
     const uint32_t k = keyat(base + lane);
     const bool c = k >= theta;
@@ -220,6 +223,7 @@ __global__ void __launch_bounds__(256) topk_stream_kernel(const float* __restric
 #pragma unroll
     for (int q = 0; q < 8; ++q) hist[lane * 8 + q] = 0u;
     __syncwarp();
+#pragma unroll 4
     for (int base = 0; base < ncand; base += 32) {
       const uint32_t k = keyat(base + lane);
       if (k != 0u && (k & pmask) == prefix) atomicAdd(&hist[(k >> shift) & 255u], 1u);
@@ -273,6 +277,223 @@ __global__ void __launch_bounds__(256) topk_stream_kernel(const float* __restric
     out += __popc(ms);
   }
 }
+
+__global__ void __launch_bounds__(256) topk_stream4_kernel(const float* __restrict__ scores,
+                                                          int32_t* __restrict__ idx, int64_t rows,
+                                                          int64_t N, int64_t B_K, int64_t b, int T) {
+  __shared__ __align__(16) uint32_t smem_all[8][256];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t row = blockIdx.x * 8ll + wib;
+  if (row >= rows) return;
+  uint32_t* hist = smem_all[wib];
+  const int64_t t = row % N;
+  const int own = (int)(t / B_K), ncand = own + 1;
+  const float* sr = scores + row * b;
+  int32_t* dst = idx + row * T;
+  const unsigned lt = (1u << lane) - 1u;
+  auto keyat = [&](int c) -> uint32_t {
+    return c < ncand ? (c == own ? 0xFF800000u : score_key32(__ldg(sr + c))) : 0u;
+  };
+  // ---- pass 1 (4 consecutive candidates per lane: one 16-byte load)
+  const float4* sr4 = reinterpret_cast<const float4*>(sr);
+  auto keys4 = [&](int base, uint32_t (&k4)[4]) {
+    const int c0 = base + 4 * lane;
+    const float4 f = c0 < ncand ? __ldg(sr4 + (c0 >> 2)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float fv[4] = {f.x, f.y, f.z, f.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      k4[e] = c0 + e < ncand ? (c0 + e == own ? 0xFF800000u : score_key32(fv[e])) : 0u;
+  };
+  auto excl_scan = [&](int v, int& total) {  // warp exclusive prefix sum
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    total = __shfl_sync(0xffffffffu, incl, 31);
+    return incl - v;
+  };
+  int nsel_l = 0;
+  uint32_t lm = 0u;
+#pragma unroll 2
+  for (int base = 0; base < ncand; base += 128) {
+    uint32_t k4[4];
+    keys4(base, k4);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      nsel_l += k4[e] != 0u;
+      lm = max(lm, k4[e]);
+    }
+  }
+  int nsel = nsel_l;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nsel += __shfl_xor_sync(0xffffffffu, nsel, o);
+  if (nsel <= T) {
+    int out = 0;
+    for (int base = 0; base < ncand; base += 128) {
+      uint32_t k4[4];
+      keys4(base, k4);
+      int cnt = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) cnt += k4[e] != 0u;
+      int tot;
+      int pos = out + excl_scan(cnt, tot);
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (k4[e] != 0u) dst[pos++] = base + 4 * lane + e;
+      out += tot;
+    }
+    if (lane >= out && lane < T) dst[lane] = -1;
+    return;
+  }
+  // ---- theta: T-th largest lane maximum (warp bitonic, descending)
+#pragma unroll
+  for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      const uint32_t y = __shfl_xor_sync(0xffffffffu, lm, j);
+      const bool take_max = ((lane & j) == 0) == ((lane & kk) == 0);
+      lm = take_max ? max(lm, y) : min(lm, y);
+    }
+  }
+  const uint32_t theta = max(__shfl_sync(0xffffffffu, lm, T - 1), 1u);
+  // ---- pass 2: candidates >= theta, packed so that larger = better
+  unsigned long long* slots = reinterpret_cast<unsigned long long*>(hist);
+  int cand = 0;
+  for (int base = 0; base < ncand; base += 128) {
+    uint32_t k4[4];
+    keys4(base, k4);
+    int cnt = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) cnt += k4[e] >= theta;
+    int tot;
+    int pos = cand + excl_scan(cnt, tot);
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (k4[e] >= theta) {
+        if (pos < 64)
+          slots[pos] = ((unsigned long long)k4[e] << 32) | (0xFFFFFFFFu - (uint32_t)(base + 4 * lane + e));
+        ++pos;
+      }
+    cand += tot;
+  }
+  __syncwarp();
+  if (cand <= 32) {
+    // typical case (~T..2T candidates): lane L holds candidate L, and the
+    // candidates sit in ascending index order.  Rank each by counting the
+    // better ones (key desc, index asc -- the packed value is larger); the
+    // T best, read in lane order, are the ascending selection.
+    const unsigned long long x = lane < cand ? slots[lane] : 0ull;
+    int rank = 0;
+#pragma unroll 8
+    for (int j = 0; j < 32; ++j) rank += __shfl_sync(0xffffffffu, x, j) > x;
+    const bool sel = lane < cand && rank < T;
+    const unsigned ms = __ballot_sync(0xffffffffu, sel);
+    if (sel) dst[__popc(ms & lt)] = (int)(0xFFFFFFFFu - (uint32_t)x);
+    const int got = __popc(ms);
+    if (lane >= got && lane < T) dst[lane] = -1;
+    return;
+  }
+  if (cand <= 64) {
+    unsigned long long x0 = lane < cand ? slots[lane] : 0ull;
+    unsigned long long x1 = lane + 32 < cand ? slots[lane + 32] : 0ull;
+#pragma unroll
+    for (int kk = 2; kk <= 64; kk <<= 1) {
+#pragma unroll
+      for (int j = kk >> 1; j > 0; j >>= 1) {
+        if (j == 32) {  // partner in the same lane (only at kk = 64)
+          const unsigned long long hi = max(x0, x1), lo = min(x0, x1);
+          x0 = hi;
+          x1 = lo;
+        } else {
+          const unsigned long long y0 = __shfl_xor_sync(0xffffffffu, x0, j);
+          const unsigned long long y1 = __shfl_xor_sync(0xffffffffu, x1, j);
+          const bool lower = (lane & j) == 0;
+          const bool d0 = (lane & kk) == 0, d1 = ((lane + 32) & kk) == 0;
+          x0 = (lower == d0) ? max(x0, y0) : min(x0, y0);
+          x1 = (lower == d1) ? max(x1, y1) : min(x1, y1);
+        }
+      }
+    }
+    // the first T (T <= 32: lanes 0..T-1 of x0) are the selection; ascending index order
+    int v = lane < T ? (int)(0xFFFFFFFFu - (uint32_t)x0) : 0x7fffffff;
+#pragma unroll
+    for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+      for (int j = kk >> 1; j > 0; j >>= 1) {
+        const int y = __shfl_xor_sync(0xffffffffu, v, j);
+        const bool take_min = ((lane & j) == 0) == ((lane & kk) == 0);
+        v = take_min ? min(v, y) : max(v, y);
+      }
+    }
+    if (lane < T) dst[lane] = v;
+    return;
+  }
+  __syncwarp();
+  // ---- fallback: exact radix select of the T-th key (4 passes of 8 bits)
+  uint32_t prefix = 0u, pmask = 0u;
+  int need = T;
+#pragma unroll 1
+  for (int shift = 24; shift >= 0; shift -= 8) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) hist[lane * 8 + q] = 0u;
+    __syncwarp();
+#pragma unroll 4
+    for (int base = 0; base < ncand; base += 32) {
+      const uint32_t k = keyat(base + lane);
+      if (k != 0u && (k & pmask) == prefix) atomicAdd(&hist[(k >> shift) & 255u], 1u);
+    }
+    __syncwarp();
+    uint32_t cnt[8], tot = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      cnt[q] = hist[255 - lane * 8 - q];
+      tot += cnt[q];
+    }
+    uint32_t incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const uint32_t excl = incl - tot;
+    const unsigned hit = __ballot_sync(0xffffffffu, excl < (uint32_t)need && incl >= (uint32_t)need);
+    const int src = __ffs(hit) - 1;
+    uint32_t digit = 0u, above = 0u;
+    if (lane == src) {
+      uint32_t run = excl;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (run + cnt[q] >= (uint32_t)need) {
+          digit = 255u - (uint32_t)(lane * 8 + q);
+          above = run;
+          break;
+        }
+        run += cnt[q];
+      }
+    }
+    digit = __shfl_sync(0xffffffffu, digit, src);
+    above = __shfl_sync(0xffffffffu, above, src);
+    need -= (int)above;
+    prefix |= digit << shift;
+    pmask |= 0xFFu << shift;
+    __syncwarp();
+  }
+  const uint32_t kth = prefix;
+  int taken_eq = 0, out = 0;
+  for (int base = 0; base < ncand; base += 32) {
+    const uint32_t k = keyat(base + lane);
+    const bool eq = k == kth;
+    const unsigned me = __ballot_sync(0xffffffffu, eq);
+    const bool sel = k > kth || (eq && taken_eq + __popc(me & lt) < need);
+    taken_eq += __popc(me);
+    const unsigned ms = __ballot_sync(0xffffffffu, sel);
+    if (sel) dst[out + __popc(ms & lt)] = base + lane;
+    out += __popc(ms);
+  }
+}
+
 
 // One CTA per row for T > 32: bitonic sort of all causal candidates in smem.
 template <typename S>
@@ -370,7 +591,10 @@ int topk_impl(const fsa_shape* s, const void* scores, int32_t* idx, cudaStream_t
   const int64_t b = s->N / s->B_K, rows = s->h_K * s->N;
   const int T = (int)s->T;
   if (rows == 0) return FSA_OK;
-  if (sizeof(S) == 4 && T <= 32) {
+  if (sizeof(S) == 4 && T <= 32 && b % 4 == 0) {
+    topk_stream4_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>((const float*)scores, idx, rows,
+                                                                   s->N, s->B_K, b, T);
+  } else if (sizeof(S) == 4 && T <= 32) {
     topk_stream_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>((const float*)scores, idx, rows,
                                                                   s->N, s->B_K, b, T);
   } else if (T <= 32) {
