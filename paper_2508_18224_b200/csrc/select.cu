@@ -125,8 +125,10 @@ __global__ void __launch_bounds__(256) topk_stream_kernel(const float* __restric
   const int64_t row = blockIdx.x * 8ll + wib;
   if (row >= rows) return;
   uint32_t* hist = smem_all[wib];
-  const int64_t t = row % N;
-  const int own = (int)(t / B_K), ncand = own + 1;
+  // 32-bit index math (rows = h_K N < 2^31): a 64-bit divide is a long
+  // emulated sequence, paid once per row
+  const int64_t t = (int64_t)((uint32_t)row % (uint32_t)N);
+  const int own = (int)((uint32_t)t / (uint32_t)B_K), ncand = own + 1;
   const float* sr = scores + row * b;
   int32_t* dst = idx + row * T;
   const unsigned lt = (1u << lane) - 1u;
@@ -286,23 +288,30 @@ __global__ void __launch_bounds__(256) topk_stream4_kernel(const float* __restri
   const int64_t row = blockIdx.x * 8ll + wib;
   if (row >= rows) return;
   uint32_t* hist = smem_all[wib];
-  const int64_t t = row % N;
-  const int own = (int)(t / B_K), ncand = own + 1;
+  // 32-bit index math (rows = h_K N < 2^31): a 64-bit divide is a long
+  // emulated sequence, paid once per row
+  const int64_t t = (int64_t)((uint32_t)row % (uint32_t)N);
+  const int own = (int)((uint32_t)t / (uint32_t)B_K), ncand = own + 1;
   const float* sr = scores + row * b;
   int32_t* dst = idx + row * T;
   const unsigned lt = (1u << lane) - 1u;
   auto keyat = [&](int c) -> uint32_t {
     return c < ncand ? (c == own ? 0xFF800000u : score_key32(__ldg(sr + c))) : 0u;
   };
-  // ---- pass 1 (4 consecutive candidates per lane: one 16-byte load)
+  // ---- pass 1 (4 consecutive candidates per lane: one 16-byte load).
+  // The passes compare floats directly -- the own block as +inf, NaN / -inf
+  // unselectable (v > -inf is false for both), fmaxf ignores NaN, -0.0 == 0.0
+  // -- and only the candidates get the 32-bit order key.
   const float4* sr4 = reinterpret_cast<const float4*>(sr);
-  auto keys4 = [&](int base, uint32_t (&k4)[4]) {
+  auto vals4 = [&](int base, float (&v4)[4]) {
     const int c0 = base + 4 * lane;
-    const float4 f = c0 < ncand ? __ldg(sr4 + (c0 >> 2)) : make_float4(0.f, 0.f, 0.f, 0.f);
-    const float fv[4] = {f.x, f.y, f.z, f.w};
+    const float4 f = c0 < ncand ? __ldg(sr4 + (c0 >> 2)) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+    v4[0] = f.x; v4[1] = f.y; v4[2] = f.z; v4[3] = f.w;
 #pragma unroll
-    for (int e = 0; e < 4; ++e)
-      k4[e] = c0 + e < ncand ? (c0 + e == own ? 0xFF800000u : score_key32(fv[e])) : 0u;
+    for (int e = 0; e < 4; ++e) {
+      if (c0 + e >= ncand) v4[e] = -INFINITY;
+      if (c0 + e == own) v4[e] = INFINITY;
+    }
   };
   auto excl_scan = [&](int v, int& total) {  // warp exclusive prefix sum
     int incl = v;
@@ -315,15 +324,15 @@ __global__ void __launch_bounds__(256) topk_stream4_kernel(const float* __restri
     return incl - v;
   };
   int nsel_l = 0;
-  uint32_t lm = 0u;
+  float lmf = -INFINITY;
 #pragma unroll 2
   for (int base = 0; base < ncand; base += 128) {
-    uint32_t k4[4];
-    keys4(base, k4);
+    float v4[4];
+    vals4(base, v4);
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      nsel_l += k4[e] != 0u;
-      lm = max(lm, k4[e]);
+      nsel_l += v4[e] > -INFINITY;
+      lmf = fmaxf(lmf, v4[e]);
     }
   }
   int nsel = nsel_l;
@@ -332,22 +341,23 @@ __global__ void __launch_bounds__(256) topk_stream4_kernel(const float* __restri
   if (nsel <= T) {
     int out = 0;
     for (int base = 0; base < ncand; base += 128) {
-      uint32_t k4[4];
-      keys4(base, k4);
+      float v4[4];
+      vals4(base, v4);
       int cnt = 0;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) cnt += k4[e] != 0u;
+      for (int e = 0; e < 4; ++e) cnt += v4[e] > -INFINITY;
       int tot;
       int pos = out + excl_scan(cnt, tot);
 #pragma unroll
       for (int e = 0; e < 4; ++e)
-        if (k4[e] != 0u) dst[pos++] = base + 4 * lane + e;
+        if (v4[e] > -INFINITY) dst[pos++] = base + 4 * lane + e;
       out += tot;
     }
     if (lane >= out && lane < T) dst[lane] = -1;
     return;
   }
   // ---- theta: T-th largest lane maximum (warp bitonic, descending)
+  uint32_t lm = score_key32(lmf);  // 0 for an all-unselectable lane
 #pragma unroll
   for (int kk = 2; kk <= 32; kk <<= 1) {
 #pragma unroll
@@ -358,22 +368,30 @@ __global__ void __launch_bounds__(256) topk_stream4_kernel(const float* __restri
     }
   }
   const uint32_t theta = max(__shfl_sync(0xffffffffu, lm, T - 1), 1u);
+  // the float threshold with the same meaning (keys are monotone in the value)
+  const float thf = theta == 1u ? -INFINITY
+                                : __uint_as_float((theta & 0x80000000u) ? (theta & 0x7FFFFFFFu) : ~theta);
   // ---- pass 2: candidates >= theta, packed so that larger = better
   unsigned long long* slots = reinterpret_cast<unsigned long long*>(hist);
   int cand = 0;
   for (int base = 0; base < ncand; base += 128) {
-    uint32_t k4[4];
-    keys4(base, k4);
+    float v4[4];
+    vals4(base, v4);
+    bool c[4];
     int cnt = 0;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) cnt += k4[e] >= theta;
+    for (int e = 0; e < 4; ++e) {
+      c[e] = v4[e] > -INFINITY && v4[e] >= thf;
+      cnt += c[e];
+    }
     int tot;
     int pos = cand + excl_scan(cnt, tot);
 #pragma unroll
     for (int e = 0; e < 4; ++e)
-      if (k4[e] >= theta) {
+      if (c[e]) {
         if (pos < 64)
-          slots[pos] = ((unsigned long long)k4[e] << 32) | (0xFFFFFFFFu - (uint32_t)(base + 4 * lane + e));
+          slots[pos] = ((unsigned long long)score_key32(v4[e]) << 32) |
+                       (0xFFFFFFFFu - (uint32_t)(base + 4 * lane + e));
         ++pos;
       }
     cand += tot;
