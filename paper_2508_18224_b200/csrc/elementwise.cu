@@ -9,30 +9,47 @@ namespace fsa {
 // over features.  Block means in the accumulator type.
 // ---------------------------------------------------------------------------
 template <typename T>
-__global__ void compress_kernel(const T* __restrict__ X, typename Acc<T>::type* __restrict__ Xc,
-                                int64_t B_K, int64_t h_K, int64_t d) {
+__global__ void compress_kernel(const T* __restrict__ K, const T* __restrict__ V,
+                                typename Acc<T>::type* __restrict__ Kc,
+                                typename Acc<T>::type* __restrict__ Vc, int64_t B_K, int64_t h_K,
+                                int64_t dK, int64_t dV) {
+  // blockIdx.z: 0 = K, 1 = V (one launch); 8 independent row accumulators per
+  // column keep 8 loads in flight (the block's 64 rows are 64 strided reads)
   using A = typename Acc<T>::type;
-  const int64_t i = blockIdx.x, kh = blockIdx.y;
+  const T* X = blockIdx.z ? V : K;
+  A* Xc = blockIdx.z ? Vc : Kc;
+  const int64_t d = blockIdx.z ? dV : dK;
+  const int64_t i = blockIdx.x, kh = blockIdx.y, stride = h_K * d;
   const A inv = A(1) / A(B_K);
   for (int64_t c = threadIdx.x; c < d; c += blockDim.x) {
-    A acc = 0;
     const T* p = X + ((i * B_K) * h_K + kh) * d + c;
-    for (int64_t r = 0; r < B_K; ++r) acc += to_acc(p[r * h_K * d]);
+    A a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int64_t r = 0;
+    for (; r + 8 <= B_K; r += 8) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) a[j] += to_acc(p[(r + j) * stride]);
+    }
+    for (; r < B_K; ++r) a[0] += to_acc(p[r * stride]);
+    const A acc = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
     Xc[(i * h_K + kh) * d + c] = acc * inv;
   }
 }
 
-// running prefix means of rows 0..t, t < n_pref (branches.py:40-43)
+// running prefix means of rows 0..t, t < n_pref (branches.py:40-43): one block
+// per (t, tensor), rows summed in order (the reference's cumsum order)
 template <typename T>
-__global__ void prefix_kernel(const T* __restrict__ X, typename Acc<T>::type* __restrict__ Xp,
-                              int64_t n_pref, int64_t h_K, int64_t d) {
+__global__ void prefix_kernel(const T* __restrict__ K, const T* __restrict__ V,
+                              typename Acc<T>::type* __restrict__ Kp,
+                              typename Acc<T>::type* __restrict__ Vp, int64_t h_K, int64_t dK,
+                              int64_t dV) {
   using A = typename Acc<T>::type;
-  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (idx >= h_K * d) return;
-  A acc = 0;
-  for (int64_t t = 0; t < n_pref; ++t) {
-    acc += to_acc(X[t * h_K * d + idx]);
-    Xp[t * h_K * d + idx] = acc / A(t + 1);
+  const T* X = blockIdx.y ? V : K;
+  A* Xp = blockIdx.y ? Vp : Kp;
+  const int64_t w = h_K * (blockIdx.y ? dV : dK), t = blockIdx.x;
+  for (int64_t idx = threadIdx.x; idx < w; idx += blockDim.x) {
+    A acc = 0;
+    for (int64_t r = 0; r <= t; ++r) acc += to_acc(X[r * w + idx]);
+    Xp[t * w + idx] = acc / A(t + 1);
   }
 }
 
@@ -196,14 +213,15 @@ int compress_impl(const fsa_shape* s, const void* K, const void* V, void* Kc, vo
                   void* Vp, cudaStream_t st) {
   using A = typename Acc<T>::type;
   const int64_t b = s->N / s->B_K, n_pref = s->B_K - 1 < s->N ? s->B_K - 1 : s->N;
-  dim3 grid((unsigned)b, (unsigned)s->h_K);
-  compress_kernel<T><<<grid, 128, 0, st>>>((const T*)K, (A*)Kc, s->B_K, s->h_K, s->d_K);
-  compress_kernel<T><<<grid, 128, 0, st>>>((const T*)V, (A*)Vc, s->B_K, s->h_K, s->d_V);
+  if (b > 0) {
+    dim3 grid((unsigned)b, (unsigned)s->h_K, 2);
+    compress_kernel<T><<<grid, 128, 0, st>>>((const T*)K, (const T*)V, (A*)Kc, (A*)Vc, s->B_K,
+                                             s->h_K, s->d_K, s->d_V);
+  }
   if (n_pref > 0) {
-    prefix_kernel<T><<<(unsigned)((s->h_K * s->d_K + 127) / 128), 128, 0, st>>>(
-        (const T*)K, (A*)Kp, n_pref, s->h_K, s->d_K);
-    prefix_kernel<T><<<(unsigned)((s->h_K * s->d_V + 127) / 128), 128, 0, st>>>(
-        (const T*)V, (A*)Vp, n_pref, s->h_K, s->d_V);
+    dim3 grid((unsigned)n_pref, 2);
+    prefix_kernel<T><<<grid, 256, 0, st>>>((const T*)K, (const T*)V, (A*)Kp, (A*)Vp, s->h_K,
+                                           s->d_K, s->d_V);
   }
   FSA_LAUNCH_CHECK("compress_kv");
   return FSA_OK;
