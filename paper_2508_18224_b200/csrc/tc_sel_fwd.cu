@@ -29,11 +29,12 @@ constexpr int kQStages = 4;
 constexpr uint32_t kQBytes = kRows * kD * 2;     // 32768: [2 halves][128 rows][128 B]
 constexpr uint32_t kKVBytes = 2 * kBK * kD * 2;  // 32768: K [2][64][128 B], V [2][64][128 B]
 constexpr uint32_t kPBytes = kRows * kBK * 2;    // 16384: [128 rows][128 B]
-constexpr uint32_t kStStride = 80;               // epilogue staging: 32 rows x (64 + 16) B per warp
 constexpr uint32_t kOffQ = 0;
 constexpr uint32_t kOffKV = kOffQ + kQStages * kQBytes;
 constexpr uint32_t kOffSt = kOffKV + 2 * kKVBytes;  // P lives in TMEM (A operand of PV)
-constexpr uint32_t kOffBar = kOffSt + 8 * 32 * kStStride;
+// epilogue staging: per softmax warp one SW128 half tile (32 rows x 128 B), the
+// source of its tile::scatter4 stores
+constexpr uint32_t kOffBar = kOffSt + 8 * 4096;
 enum { B_QF = 0, B_QE = 4, B_KVF = 8, B_KVE = 10, B_SF = 12, B_SE = 14, B_PF = 16, B_PE = 18,
        B_OF = 20, B_OE = 22, B_RF = 24, B_RE = 28, kNumBars = 32 };
 constexpr uint32_t kOffRing = kOffBar + kNumBars * 8;
@@ -45,6 +46,7 @@ constexpr uint32_t kIdescS = idesc_bf16(128, 64, false, false);
 constexpr uint32_t kIdescPV = idesc_bf16(128, 128, false, true);
 
 struct Params {
+  CUtensorMap tmO;  // obuf rows [h N T][128] bf16 (tile::scatter4 stores)
   const __nv_bfloat16 *Q, *K, *V;
   const int32_t *offsets, *qlist;
   int32_t* counter;
@@ -62,7 +64,7 @@ struct TaskFifo {
   __device__ int32_t pop() { return task[head++ & 3]; }
 };
 
-__global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const Params p) {
+__global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -261,7 +263,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const Params p)
     const int wg = warp >> 2;
     const int r = threadIdx.x & 127;  // MMA row == TMEM lane
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-    unsigned char* st = smem + kOffSt + warp * 32 * kStStride;
+    unsigned char* st = smem + kOffSt + warp * 4096u;
     const int kt_row = r / p.g, hh = r % p.g;
     int64_t prow = -1;  // obuf row of this thread's row in the pending item
     float pm = 0.f, pl = 1.f;
@@ -273,33 +275,44 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const Params p)
       mbar_wait(bar(B_OF + s1), (uint32_t)((m1 >> 1) & 1));
       tc_fence_after();
       const float inv = 1.f / pl;
+      int32_t rows[4];  // lanes 0-7: the obuf rows of row group `lane`
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        float ov[32];
-        tmem_ld32(tmem + lane_base + 128 + s1 * 128 + q * 32, ov);
-        tmem_wait_ld();
+      for (int i = 0; i < 4; ++i) {
+        const int64_t d = __shfl_sync(0xffffffffu, prow, (4 * lane + i) & 31);
+        rows[i] = d >= 0 ? (int32_t)d : INT32_MAX;  // out of the map: dropped
+      }
+      // Partial rows leave by TMA tile::scatter4 (4 rows x 128 B per request)
+      // from an SW128 half tile per warp: off the LSU, which the loaders'
+      // gathers and the next item's entry loads share.
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const uint4 v4 = make_uint4(pack_bf16(ov[8 * c] * inv, ov[8 * c + 1] * inv),
-                                      pack_bf16(ov[8 * c + 2] * inv, ov[8 * c + 3] * inv),
-                                      pack_bf16(ov[8 * c + 4] * inv, ov[8 * c + 5] * inv),
-                                      pack_bf16(ov[8 * c + 6] * inv, ov[8 * c + 7] * inv));
-          *reinterpret_cast<uint4*>(st + lane * kStStride + c * 16) = v4;
+      for (int hf = 0; hf < 2; ++hf) {
+        if (lane < 8) bulk_wait_read();  // the previous half's scatter has read the staging
+        __syncwarp();
+#pragma unroll
+        for (int qq = 0; qq < 2; ++qq) {
+          const int q = 2 * hf + qq;
+          float ov[32];
+          tmem_ld32(tmem + lane_base + 128 + s1 * 128 + q * 32, ov);
+          tmem_wait_ld();
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const uint4 v4 = make_uint4(pack_bf16(ov[8 * c] * inv, ov[8 * c + 1] * inv),
+                                        pack_bf16(ov[8 * c + 2] * inv, ov[8 * c + 3] * inv),
+                                        pack_bf16(ov[8 * c + 4] * inv, ov[8 * c + 5] * inv),
+                                        pack_bf16(ov[8 * c + 6] * inv, ov[8 * c + 7] * inv));
+            *reinterpret_cast<uint4*>(st + sw128_off(lane, qq * 4 + c)) = v4;
+          }
         }
-        if (q == 3) {
+        if (hf == 1) {
           tc_fence_before();
           mbar_arrive(bar(B_OE + s1));
         }
+        fence_proxy_async();
         __syncwarp();
-        // 32 rows x 64 B of this column chunk: 8 rows per instruction
-#pragma unroll
-        for (int it = 0; it < 4; ++it) {
-          const int rr = it * 8 + (lane >> 2), ch = lane & 3;
-          const int64_t drow = __shfl_sync(0xffffffffu, prow, rr);
-          const uint4 v4 = *reinterpret_cast<const uint4*>(st + rr * kStStride + ch * 16);
-          if (drow >= 0) __stcs(reinterpret_cast<uint4*>(p.obuf + drow * kD + q * 32 + ch * 8), v4);  // streaming: keep Q in L2
+        if (lane < 8) {
+          tma_scatter4(&p.tmO, hf * 64, rows, smem_u32(st) + (uint32_t)lane * 512u);
+          bulk_commit();
         }
-        __syncwarp();
       }
       if (prow >= 0) __stcs(reinterpret_cast<float2*>(p.ml + 2 * prow), make_float2(pm, pl));
     };
@@ -388,6 +401,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const Params p)
     if (pend) epilogue(pend_n);
   }
 
+  if (warp < 8 && lane < 8) bulk_wait_all();  // partial-row scatters complete before exit
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {
@@ -438,6 +452,7 @@ int tc_sel_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V,
   p.scale = (float)s->scale;
   p.scale_log2 = (float)(s->scale * 1.4426950408889634);
   p.counter = const_cast<int32_t*>(work) + p.ntask + 1;
+  if (int rc = make_tmap_rows(&p.tmO, obuf, s->h * s->N * s->T, 1)) return rc;
   cudaMemsetAsync(p.counter, 0, sizeof(int32_t), st);
   static bool attr = false;
   if (!attr) {
