@@ -207,7 +207,7 @@ int cmp_fwd_impl(const fsa_shape* s, const void* Q, const void* Kc, const void* 
   FSA_LAUNCH_CHECK("cmp_attn_fwd");
   if (tc) {
     // scores for the formed blocks come from the tensor cores for every g:
-    // fused into this pass when g divides 32, else a group-summed-query pass
+    // fused into this pass for g <= 2, else a group-summed-query pass
     return tc_cmp_fwd(s, Q, Kc, Vc, out, lse, scores, workspace, st);
   }
   if (scores) {

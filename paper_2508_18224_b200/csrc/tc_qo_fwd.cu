@@ -533,9 +533,13 @@ bool tc_qo_supported(const fsa_shape& s, int dtype) {
   return dtype == FSA_DT_BF16 && s.d_K == kD && s.d_V == kD && s.h_K > 0 && s.h % s.h_K == 0 &&
          s.h / s.h_K <= kRows && s.N < (1ll << 30);
 }
+// Fused scores epilogue only for g <= 2: it sums the g rows of a token with
+// warp shuffles (64 values per thread per step) and stores through the LSU;
+// for larger groups the group-summed-query pass on the tensor cores is faster
+// (measured: g = 4 at 32K 0.72 -> 0.65 ms; g = 1 at 64K fused 1.62 vs 2.11 ms).
 bool tc_cmp_scores_fused(const fsa_shape& s) {
   const int64_t g = s.h / s.h_K;
-  return g <= 32 && (32 % g) == 0;
+  return g <= 2;
 }
 bool tc_cmp_scores_any_g() { return true; }
 
