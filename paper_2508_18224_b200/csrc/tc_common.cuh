@@ -136,6 +136,24 @@ __device__ __forceinline__ void prefetch_l2(const void* ptr) {
 }
 
 // ---------------------------------------------------------------- TMA
+// 3-D tile store (or fp32 reduce-add) from shared memory (bulk group)
+__device__ __forceinline__ void tma_store_3d(const void* tmap, int c0, int c1, int c2, uint32_t src) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                   reinterpret_cast<uint64_t>(tmap)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(src)
+               : "memory");
+}
+__device__ __forceinline__ void tma_reduce_add_3d(const void* tmap, int c0, int c1, int c2, uint32_t src) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+          reinterpret_cast<uint64_t>(tmap)),
+      "r"(c0), "r"(c1), "r"(c2), "r"(src)
+      : "memory");
+}
+// named barrier over `count` threads (a warpgroup: count 128)
+__device__ __forceinline__ void named_bar(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
 // 4 arbitrary rows (r[0..3]) x 64 features from column col of a 2-D row map
 // (box (64, 1)) -> 4 x 128 B at dst (SW128 rows), completing on bar.
 __device__ __forceinline__ void tma_gather4(uint32_t dst, const void* map, int col, const int32_t* r,

@@ -62,6 +62,9 @@ namespace fsa {
 // TMA descriptor of a token-major [N][heads][128] bf16 tensor, box (64, heads_box, tok_box)
 int make_tmap_tokens(CUtensorMap* map, const void* base, int64_t N, int64_t heads, int heads_box,
                      int tok_box);
+// fp32 [N][heads][128], box (32, heads_box, tok_box), SW128 (accumulator-tile stores)
+int make_tmap_tokens_f32(CUtensorMap* map, const void* base, int64_t N, int64_t heads, int heads_box,
+                         int tok_box);
 // 2-D [rows][128] bf16 view, box (64, box_rows): the tile::gather4 / scatter4 operand
 int make_tmap_rows(CUtensorMap* map, const void* base, int64_t rows, int box_rows);
 

@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
       int r = 0;
       while (c.advance(p, G)) {
         const int qs = (int)(c.seq & 1);
-        mbar_wait(bar(B_QE + qs), (uint32_t)(((c.seq >> 1) & 1) ^ 1));
+        mbar_spin(bar(B_QE + qs), (uint32_t)(((c.seq >> 1) & 1) ^ 1));
         mbar_arrive_expect_tx(bar(B_QF + qs), 4u * qbox);
 #pragma unroll
         for (int w = 0; w < 2; ++w)
@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
         const bool with_v = M != SCORES;
         for (int u = c.it.u0; u < c.it.u1; ++u, ++r) {
           const int v = (int)(r % kKVStages);
-          mbar_wait(bar(B_KE + v), (uint32_t)(((r / kKVStages) & 1) ^ 1));
+          mbar_spin(bar(B_KE + v), (uint32_t)(((r / kKVStages) & 1) ^ 1));
           mbar_arrive_expect_tx(bar(B_KF + v), with_v ? kKV : kKV / 2);
 #pragma unroll
           for (int hf = 0; hf < 2; ++hf) {

@@ -41,6 +41,7 @@ constexpr uint32_t kIdQ = idesc_bf16(128, 128, false, true);
 
 struct Params {
   CUtensorMap tmQ, tmO, tmK, tmV;  // TMA descriptors (tma_host.cu): Q/dO boxes (64, g, tpi), K/V (64, 1, 64)
+  CUtensorMap tmDQ;                 // dQ fp32 boxes (32, g, tpi): the epilogue's store / reduce-add
   long long* trace;  // debug timeline (CTA 0), null in production
   const __nv_bfloat16 *Q, *K, *V, *dO;
   const float *lse, *delta;
@@ -127,7 +128,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const __grid_c
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     mbar_init(bar(B_QF), 1);  // TMA: one arrive.expect_tx + the transaction bytes
-    mbar_init(bar(B_QE), 2);
+    mbar_init(bar(B_QE), 2);  // one arrival per softmax warpgroup (epilogue staging read)
     for (int w = 0; w < 2; ++w) {
       mbar_init(bar(B_SF + w), 1);
       mbar_init(bar(B_PF + w), 128);
@@ -156,7 +157,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const __grid_c
       Cursor<CM> c;
       int r = 0;
       while (c.advance(p, G)) {
-        mbar_wait(bar(B_QE), (uint32_t)((c.seq & 1) ^ 1));
+        mbar_spin(bar(B_QE), (uint32_t)((c.seq & 1) ^ 1));
         DQ_TRACE(0, c.seq, 4);  // loader: Q/dO stage free
         mbar_arrive_expect_tx(bar(B_QF), 8u * qbox);
 #pragma unroll
@@ -171,7 +172,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const __grid_c
         DQ_TRACE(0, c.seq, 5);  // loader: Q/dO loads issued
         for (int u = c.it.u0; u < c.it.u1; ++u, ++r) {
           const int v = r % kKVStages;
-          mbar_wait(bar(B_KE + v), (uint32_t)(((r / kKVStages) & 1) ^ 1));
+          mbar_spin(bar(B_KE + v), (uint32_t)(((r / kKVStages) & 1) ^ 1));
           mbar_arrive_expect_tx(bar(B_KF + v), kKV);
 #pragma unroll
           for (int hf = 0; hf < 2; ++hf) {
@@ -255,11 +256,6 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const __grid_c
             }
           }
         }
-        if (elect_one()) {  // both S streams are done with this Q/dO stage
-          mma_commit(bar(B_QE));
-          mma_commit(bar(B_QE));
-        }
-        __syncwarp();
       }
     }
   } else if (warp < 8) {
@@ -272,7 +268,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const __grid_c
     Cursor<CM> c;
     while (c.advance(p, G)) {
       const Sub& s = c.it.s[w];
-      if (s.k0 >= s.k1) continue;
+      if (s.k0 >= s.k1) {  // empty sub-item: nothing staged in this Q/dO stage
+        if (r == 0) mbar_arrive(bar(B_QE));
+        continue;
+      }
       const int t = s.t0 + kt_row;
       const bool ok = kt_row < p.tpi && t <= s.tlast;
       const int64_t j = (int64_t)c.it.kh * p.g + hh;
@@ -280,11 +279,6 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const __grid_c
       const int khi = !ok ? -1 : CM ? (int)((t + 1) / p.cmpBK) - 1 : t;
       const float lse_r = ok ? p.lse[j * p.N + t] * 1.4426950408889634f : 0.f;
       const float dl = ok ? p.delta[j * p.N + t] : 0.f;
-      if (ok && p.accumulate) {  // the row is read back (+=) by the epilogue
-        const float* row = p.dQ + ((int64_t)t * p.h + j) * kD;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) prefetch_l2(row + q * 32);
-      }
       for (int kt = s.k0; kt < s.k1; ++kt, ++u) {
         mbar_wait_warp(bar(B_SF + w), (uint32_t)(u & 1));
         if (r == 0) DQ_TRACE(w, u, 1);  // S/dP landed
@@ -316,34 +310,39 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const __grid_c
         mbar_arrive(bar(B_PF + w));
         if (r == 0) DQ_TRACE(w, u, 2);  // dS written
       }
-      // epilogue: dQ (+)= scale * accumulator
+      // epilogue: dQ (+)= scale * accumulator.  The rows are staged in this
+      // warpgroup's (consumed) Q / dO sub-tiles as four SW128 boxes of 32
+      // fp32 columns x (g heads x tpi tokens) and leave by TMA store -- or
+      // TMA reduce-add when accumulating -- instead of 16-byte scattered
+      // per-thread stores; then the Q / dO stage is released to the loader.
       mbar_wait_warp(bar(B_OF + w), (uint32_t)(n_out & 1));
       tc_fence_after();
-      float* orow = p.dQ + ((int64_t)t * p.h + j) * kD;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        float4 old[8];
-        if (ok && p.accumulate) {  // batched loads: one memory latency per chunk
-#pragma unroll
-          for (int cc = 0; cc < 8; ++cc) old[cc] = __ldcg(reinterpret_cast<const float4*>(orow + q * 32) + cc);
-        }
         float ov[32];
         tmem_ld32(tmem + lb + 128u + q * 32, ov);
         tmem_wait_ld();
-        if (ok) {
+        unsigned char* box = smem + kOffQ + (q < 2 ? w : 2 + w) * kT + (q & 1) * 16384u;
 #pragma unroll
-          for (int cc = 0; cc < 8; ++cc) {
-            float4 x = make_float4(ov[4 * cc] * p.scale, ov[4 * cc + 1] * p.scale,
-                                   ov[4 * cc + 2] * p.scale, ov[4 * cc + 3] * p.scale);
-            if (p.accumulate) {
-              x.x += old[cc].x;
-              x.y += old[cc].y;
-              x.z += old[cc].z;
-              x.w += old[cc].w;
-            }
-            reinterpret_cast<float4*>(orow + q * 32)[cc] = x;
-          }
+        for (int cc = 0; cc < 8; ++cc)
+          *reinterpret_cast<float4*>(box + sw128_off(r, cc)) =
+              make_float4(ov[4 * cc] * p.scale, ov[4 * cc + 1] * p.scale, ov[4 * cc + 2] * p.scale,
+                          ov[4 * cc + 3] * p.scale);
+      }
+      fence_proxy_async();
+      named_bar(1 + w, 128);
+      if (r == 0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t box = sb + kOffQ + (q < 2 ? w : 2 + w) * kT + (q & 1) * 16384u;
+          if (p.accumulate)
+            tma_reduce_add_3d(&p.tmDQ, q * 32, c.it.kh * (int)p.g, s.t0, box);
+          else
+            tma_store_3d(&p.tmDQ, q * 32, c.it.kh * (int)p.g, s.t0, box);
         }
+        bulk_commit();
+        bulk_wait_read();
+        mbar_arrive(bar(B_QE));
       }
       tc_fence_before();
       mbar_arrive(bar(B_OE + w));
@@ -351,6 +350,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const __grid_c
     }
   }
 
+  if (threadIdx.x == 0 || threadIdx.x == 128) bulk_wait_all();  // dQ stores complete before exit
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {
@@ -387,6 +387,7 @@ int tc_slide_dq(const fsa_shape* s, const void* Q, const void* K, const void* V,
   if (!rc) rc = make_tmap_tokens(&p.tmO, dOut, p.N, p.h, (int)p.g, p.tpi);
   if (!rc) rc = make_tmap_tokens(&p.tmK, K, p.N, p.h_K, 1, 64);
   if (!rc) rc = make_tmap_tokens(&p.tmV, V, p.N, p.h_K, 1, 64);
+  if (!rc) rc = make_tmap_tokens_f32(&p.tmDQ, dQ, p.N, p.h, (int)p.g, p.tpi);
   if (rc) return rc;
   static bool attr = false;
   if (!attr) {
@@ -432,6 +433,7 @@ int tc_cmp_dq(const fsa_shape* s, const void* Q, const void* Kb, const void* Vb,
   if (!rc) rc = make_tmap_tokens(&p.tmO, dOut, p.N, p.h, (int)p.g, p.tpi);
   if (!rc) rc = make_tmap_tokens(&p.tmK, Kb, b, p.h_K, 1, 64);
   if (!rc) rc = make_tmap_tokens(&p.tmV, Vb, b, p.h_K, 1, 64);
+  if (!rc) rc = make_tmap_tokens_f32(&p.tmDQ, dQ, p.N, p.h, (int)p.g, p.tpi);
   if (rc) return rc;
   cudaFuncSetAttribute(tc_slide_dq_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
   int64_t items = p.h_K * p.n_super;

@@ -53,6 +53,29 @@ int make_tmap_tokens(CUtensorMap* map, const void* base, int64_t N, int64_t head
   return FSA_OK;
 }
 
+// fp32 token-major [N][heads][128], box (32 floats = 128 B, heads_box, tok_box), SW128:
+// the TMA store / reduce-add target of a 128-row accumulator tile, 4 column quarters
+int make_tmap_tokens_f32(CUtensorMap* map, const void* base, int64_t N, int64_t heads, int heads_box,
+                         int tok_box) {
+  const cuuint64_t dims[3] = {128, (cuuint64_t)heads, (cuuint64_t)N};
+  const cuuint64_t strides[2] = {(cuuint64_t)(128 * 4), (cuuint64_t)(heads * 128 * 4)};
+  const cuuint32_t box[3] = {32, (cuuint32_t)heads_box, (cuuint32_t)tok_box};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  EncodeTiled enc = encode_fn();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled is not available from the driver");
+    return FSA_ERR_CUDA;
+  }
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (f32 tokens) failed (%d)", (int)r);
+    return FSA_ERR_CUDA;
+  }
+  return FSA_OK;
+}
+
 // 2-D view [rows][128] bf16 of a row-major tensor, box (64, box_rows), SW128:
 // the tile::gather4 / tile::scatter4 operand (4 arbitrary rows per instruction).
 int make_tmap_rows(CUtensorMap* map, const void* base, int64_t rows, int box_rows) {
