@@ -197,20 +197,21 @@ int cmp_fwd_impl(const fsa_shape* s, const void* Q, const void* Kc, const void* 
   using A = typename Acc<T>::type;
   const int dt = sizeof(T) == 8 ? FSA_DT_F64 : (sizeof(T) == 4 ? FSA_DT_F32 : FSA_DT_BF16);
   const bool tc = tc_qo_supported(*s, dt) && workspace != nullptr;
-  // tensor-core path: formed tokens on tcgen05, the < B_K - 1 pending ones here
+  // tensor-core path: formed tokens on tcgen05 (its tile stores write the
+  // pending rows as 0), then the < B_K - 1 pending ones here
   const int64_t ntok = tc ? (s->B_K - 1 < s->N ? s->B_K - 1 : s->N) : s->N;
+  if (tc) {
+    // scores for the formed blocks come from the tensor cores for every g:
+    // fused into this pass for g <= 2, else a group-summed-query pass
+    if (int rc = tc_cmp_fwd(s, Q, Kc, Vc, out, lse, scores, workspace, st)) return rc;
+  }
   const int64_t rows = s->h * ntok;
   if (rows > 0)
     cmp_fwd_generic<T><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(
         (const T*)Q, (const A*)Kc, (const A*)Vc, (const A*)Kp, (const A*)Vp, (A*)out, (A*)lse, *s,
         ntok);
   FSA_LAUNCH_CHECK("cmp_attn_fwd");
-  if (tc) {
-    // scores for the formed blocks come from the tensor cores for every g:
-    // fused into this pass for g <= 2, else a group-summed-query pass
-    return tc_cmp_fwd(s, Q, Kc, Vc, out, lse, scores, workspace, st);
-  }
-  if (scores) {
+  if (!tc && scores) {
     return fsa_importance_scores(s, dt, Q, Kc, scores, st);
   }
   return FSA_OK;

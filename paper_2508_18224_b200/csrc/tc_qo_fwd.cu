@@ -58,6 +58,7 @@ enum Mode { SLIDE = 0, CMP = 1, SCORES = 2 };
   } while (0)
 
 struct Params {
+  CUtensorMap tmOut;  // out fp32 boxes (32, g, tpi): the epilogue TMA store
   CUtensorMap tmQ, tmK, tmV;
   long long* trace;  // debug timeline (CTA 0), null in production         // TMA: Q box (64, g, tpi), key/value boxes (64, 1, 64)
   const __nv_bfloat16 *Q, *Kx, *Vx;  // keys/values: K,V [N][h_K][128] or pooled [b][h_K][128]
@@ -285,12 +286,16 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
             }
           }
         }
-        // both S streams are done with this Q stage
-        if (elect_one()) {
-          mma_commit(bar(B_QE + qs));
-          mma_commit(bar(B_QE + qs));
+        // SCORES: both S streams are done with this Q stage.  (SLIDE / CMP: the
+        // softmax warpgroups release it after their epilogue has staged the
+        // output rows in it and the TMA store has read them.)
+        if constexpr (M == SCORES) {
+          if (elect_one()) {
+            mma_commit(bar(B_QE + qs));
+            mma_commit(bar(B_QE + qs));
+          }
+          __syncwarp();
         }
-        __syncwarp();
       }
     }
   } else if (warp < 8) {
@@ -303,7 +308,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
     Cursor<M> c;
     while (c.advance(p, G)) {
       const Sub& s = c.it.s[w];
-      if (s.k0 >= s.k1) continue;
+      if (s.k0 >= s.k1) {  // empty sub-item: nothing staged in this Q stage
+        if (M != SCORES && r == 0) mbar_arrive(bar(B_QE + (c.seq & 1)));
+        continue;
+      }
       const int t = s.t0 + kt_row;
       const bool ok = kt_row < p.tpi && t <= s.tlast;
       const int64_t j = (int64_t)c.it.kh * p.g + hh;
@@ -427,18 +435,44 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
       tc_fence_after();
       const bool write = ok && l > 0.f;
       const float inv = write ? 1.f / l : 0.f;
-      float* orow = p.out + ((int64_t)t * p.h + j) * kD;
+      // Rows leave by TMA store: staged in this warpgroup's consumed Q
+      // sub-tile (32 KB) as two SW128 boxes of 32 fp32 columns x (g heads x
+      // tpi tokens) at a time -- instead of 16-byte scattered per-thread
+      // stores.  Rows without a visible key are stored as 0 (the compressed
+      // branch's pending tokens are written after this kernel).
+      unsigned char* qsub = smem + kOffQ + ((c.seq & 1) * 2 + w) * kQ;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        float ov[32];
-        tmem_ld32(tmem + lb + 128u + q * 32, ov);
-        tmem_wait_ld();
-        if (write) {
-#pragma unroll
-          for (int cc = 0; cc < 32; cc += 4)
-            *reinterpret_cast<float4*>(orow + q * 32 + cc) =
-                make_float4(ov[cc] * inv, ov[cc + 1] * inv, ov[cc + 2] * inv, ov[cc + 3] * inv);
+      for (int pass = 0; pass < 2; ++pass) {
+        if (pass == 1) {
+          if (r == 0) bulk_wait_read();
+          named_bar(1 + w, 128);
         }
+#pragma unroll
+        for (int qq = 0; qq < 2; ++qq) {
+          const int q = 2 * pass + qq;
+          float ov[32];
+          tmem_ld32(tmem + lb + 128u + q * 32, ov);
+          tmem_wait_ld();
+          unsigned char* box = qsub + qq * 16384u;
+#pragma unroll
+          for (int cc = 0; cc < 8; ++cc)
+            *reinterpret_cast<float4*>(box + sw128_off(r, cc)) =
+                make_float4(ov[4 * cc] * inv, ov[4 * cc + 1] * inv, ov[4 * cc + 2] * inv,
+                            ov[4 * cc + 3] * inv);
+        }
+        fence_proxy_async();
+        named_bar(1 + w, 128);
+        if (r == 0) {
+#pragma unroll
+          for (int qq = 0; qq < 2; ++qq)
+            tma_store_3d(&p.tmOut, (2 * pass + qq) * 32, c.it.kh * (int)p.g, s.t0,
+                         smem_u32(qsub) + qq * 16384u);
+          bulk_commit();
+        }
+      }
+      if (r == 0) {
+        bulk_wait_read();
+        mbar_arrive(bar(B_QE + (c.seq & 1)));
       }
       tc_fence_before();
       mbar_arrive(bar(B_OE + w));
@@ -448,6 +482,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
     }
   }
 
+  if (threadIdx.x == 0 || threadIdx.x == 128) bulk_wait_all();  // out stores complete before exit
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {
@@ -468,6 +503,7 @@ int launch(Params& p, cudaStream_t st) {
   int rc = make_tmap_tokens(&p.tmQ, p.Q, p.N, p.h, (int)p.g, p.tpi);
   if (!rc) rc = make_tmap_tokens(&p.tmK, p.Kx, p.n_keys, p.h_K, 1, 64);
   if (!rc) rc = make_tmap_tokens(&p.tmV, p.Vx, p.n_keys, p.h_K, 1, 64);
+  if (!rc && p.out) rc = make_tmap_tokens_f32(&p.tmOut, p.out, p.N, p.h, (int)p.g, p.tpi);
   if (rc) return rc;
   static bool attr = false;
   if (!attr) {
