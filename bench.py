@@ -324,7 +324,7 @@ def run_ours(args, rank, world, local_rank):
         "kernels_per_step": kernel_names,
         "clocks": clocks,
     }
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:  # rank 0 at N = 1 only
         line["cpu_baseline"] = cpu_baseline(args, sample_n=CPU_SAMPLE_N, steps=1)
     if world > 1:
         import torch.distributed as dist
