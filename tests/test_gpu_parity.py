@@ -584,3 +584,38 @@ def test_query_head_split_matches_unsharded():
     for got, ref in ((dq2, dQ), (dk2, dK), (dv2, dV)):
         err = (got - ref).abs().max().item()
         assert err <= 1e-3 * ref.abs().max().item(), err
+
+
+# NSA step on the tensor-core path over group sizes / windows / budgets the
+# BASELINE shapes do not reach (partial items, windows not a multiple of 64,
+# T = 1, g = 3, 6, 16, several kv heads): out, dQ, dK, dV, dtau vs the oracle.
+@pytest.mark.parametrize("kw", [
+    dict(N=1536, d_K=128, d_V=128, h=6, h_K=2, B_K=64, T=1, W=100),
+    dict(N=1024, d_K=128, d_V=128, h=16, h_K=1, B_K=64, T=16, W=700),
+    dict(N=3072, d_K=128, d_V=128, h=9, h_K=3, B_K=64, T=5, W=64),
+    dict(N=1088, d_K=128, d_V=128, h=6, h_K=1, B_K=64, T=3, W=1),
+    dict(N=1088, d_K=128, d_V=128, h=2, h_K=2, B_K=64, T=4, W=333),
+    dict(N=512, d_K=128, d_V=128, h=128, h_K=1, B_K=64, T=4, W=128),
+])
+def test_nsa_step_shapes_vs_oracle(kw):
+    c = O.cfg_of(**kw)
+    cfg = _cfg(kw)
+    Q, K, V = (round_inputs(x, "bf16") for x in O.make_qkv(c, 21))
+    dO = round_inputs(O.make_dout(c, 21), "bf16")
+    tau = O.make_gates(c, 21)
+    q, k, v, do = (dev(x, torch.bfloat16).permute(0, 2, 1).contiguous() for x in (Q, K, V, dO))
+    out, ctx = fsa.nsa_forward(q, k, v, torch.from_numpy(tau).to("cuda", torch.float32), cfg)
+    idx = O.select_topk(host(ctx.scores).astype(np.float64), c)
+    np.testing.assert_array_equal(host(ctx.sel.idx), idx)
+    cmp = O.compress_kv(K, V, c)
+    outs = (O.compressed_forward(Q, cmp, c)[0], O.selected_forward(Q, K, V, idx, c)[0],
+            O.sliding_forward(Q, K, V, c)[0])
+    want, _ = O.gated_combine(outs, tau, c)
+    assert_close(host(out.permute(0, 2, 1)), want, "bf16", "combined")
+    fQ, fK, fV, dtau = fsa.nsa_backward(ctx, do, full=True)
+    gs = O.selected_backward(Q, K, V, idx, dO * tau[:, 1][:, None, None], c)
+    gl = O.sliding_backward(Q, K, V, dO * tau[:, 2][:, None, None], c)
+    gc = O.compressed_backward(Q, K, V, dO * tau[:, 0][:, None, None], c)
+    for got, a, b, cc, name in zip((fQ, fK, fV), gs, gl, gc, ("dQ", "dK", "dV")):
+        assert_close(host(got.permute(0, 2, 1)), a + b + cc, "bf16", name, grad=True)
+    assert_close(host(dtau), O.gate_grad(outs, dO, c), "bf16", "dtau", grad=True)
