@@ -198,6 +198,15 @@ int fsa_gate_backward(const fsa_shape* s, int dtype, const void* dOut, const voi
                       const void* out_sel, const void* out_slide, void* d_sel, void* d_slide,
                       void* delta_sel, void* delta_slide, void* stream);
 
+/* The gate backward folded into the branch statistics (tensor-core path, used by
+ * the NSA step): delta_c = sum_v out_c * dOut and lse_c_adj = lse_c - ln tau_c[t]
+ * for c = selected, sliding ([h][N], acc).  The branch backward kernels then take
+ * the raw dOut: tau * exp(z - lse) = exp(z - lse_adj) (branches.py:103). */
+int fsa_gate_backward_fold(const fsa_shape* s, int dtype, const void* dOut, const void* tau,
+                           const void* out_sel, const void* out_slide, const void* lse_sel,
+                           const void* lse_slide, void* delta_sel, void* delta_slide,
+                           void* lse_sel_adj, void* lse_slide_adj, void* stream);
+
 /* Compressed-branch backward (the reference has none --
  * parity vs the float64 oracle, pinned to autograd): gradients of
  * sum(out_cmp * dOut) through the attention over the pooled rows and the

@@ -284,6 +284,61 @@ int gate_backward_impl(const fsa_shape* s, const void* dOut, const void* tau, co
   return FSA_OK;
 }
 
+// Gate backward folded into the branches' softmax statistics (tensor-core
+// path): with d_c = tau_c[t] * dOut, every backward quantity of branch c is
+// tau_c[t] times its value for the raw dOut (dP, dS, the dV product), and
+// tau * exp(z - lse) = exp(z - (lse - ln tau)).  So the branch kernels take the
+// raw dOut with lse_c - ln tau_c and delta_c = sum_v out_c * dOut -- no gated
+// copies of dOut are written (nor rounded to bf16).  Warp per (token, head).
+template <typename T>
+__global__ void gate_fold_kernel(const T* __restrict__ dOut, const typename Acc<T>::type* __restrict__ tau,
+                                 const typename Acc<T>::type* __restrict__ out_sel,
+                                 const typename Acc<T>::type* __restrict__ out_slide,
+                                 const typename Acc<T>::type* __restrict__ lse_sel,
+                                 const typename Acc<T>::type* __restrict__ lse_slide,
+                                 typename Acc<T>::type* __restrict__ delta_sel,
+                                 typename Acc<T>::type* __restrict__ delta_slide,
+                                 typename Acc<T>::type* __restrict__ lse_sel_adj,
+                                 typename Acc<T>::type* __restrict__ lse_slide_adj, int64_t N, int64_t h,
+                                 int64_t dv) {
+  using A = typename Acc<T>::type;
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (wid >= N * h) return;
+  const int64_t t = wid / h, j = wid - t * h;
+  const int64_t base = wid * dv;
+  A s1 = 0, s2 = 0;
+  for (int64_t c = lane; c < dv; c += 32) {
+    const A x = to_acc(dOut[base + c]);
+    s1 += out_sel[base + c] * x;
+    s2 += out_slide[base + c] * x;
+  }
+  s1 = warp_sum(s1);
+  s2 = warp_sum(s2);
+  if (lane == 0) {
+    const int64_t r = j * N + t;
+    delta_sel[r] = s1;
+    delta_slide[r] = s2;
+    lse_sel_adj[r] = lse_sel[r] - log_acc(tau[t * 3 + 1]);  // tau = 0: +inf, P = 0
+    lse_slide_adj[r] = lse_slide[r] - log_acc(tau[t * 3 + 2]);
+  }
+}
+
+template <typename T>
+int gate_fold_impl(const fsa_shape* s, const void* dOut, const void* tau, const void* out_sel,
+                   const void* out_slide, const void* lse_sel, const void* lse_slide, void* delta_sel,
+                   void* delta_slide, void* lse_sel_adj, void* lse_slide_adj, cudaStream_t st) {
+  using A = typename Acc<T>::type;
+  const int64_t rows = s->N * s->h;
+  if (rows == 0) return FSA_OK;
+  gate_fold_kernel<T><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(
+      (const T*)dOut, (const A*)tau, (const A*)out_sel, (const A*)out_slide, (const A*)lse_sel,
+      (const A*)lse_slide, (A*)delta_sel, (A*)delta_slide, (A*)lse_sel_adj, (A*)lse_slide_adj, s->N,
+      s->h, s->d_V);
+  FSA_LAUNCH_CHECK("gate_backward_fold");
+  return FSA_OK;
+}
+
 template <typename T>
 int finite_impl(const void* x, int64_t n, int32_t* flag, cudaStream_t st) {
   int64_t blocks = (n + 255) / 256;
@@ -332,6 +387,14 @@ extern "C" int fsa_gate_backward(const fsa_shape* s, int dtype, const void* dOut
                                  void* d_slide, void* delta_sel, void* delta_slide, void* stream) {
   DISPATCH_DT(dtype, gate_backward_impl, s, dOut, tau, out_sel, out_slide, d_sel, d_slide, delta_sel,
               delta_slide, (cudaStream_t)stream);
+}
+
+extern "C" int fsa_gate_backward_fold(const fsa_shape* s, int dtype, const void* dOut, const void* tau,
+                                      const void* out_sel, const void* out_slide, const void* lse_sel,
+                                      const void* lse_slide, void* delta_sel, void* delta_slide,
+                                      void* lse_sel_adj, void* lse_slide_adj, void* stream) {
+  DISPATCH_DT(dtype, gate_fold_impl, s, dOut, tau, out_sel, out_slide, lse_sel, lse_slide, delta_sel,
+              delta_slide, lse_sel_adj, lse_slide_adj, (cudaStream_t)stream);
 }
 
 extern "C" int fsa_check_finite(int dtype, const void* x, int64_t n, int32_t* flag, void* stream) {

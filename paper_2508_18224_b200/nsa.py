@@ -133,11 +133,10 @@ def nsa_backward(ctx: NSAContext, dout, *, full: bool = False):
     s = _lib.shape_of(cfg)
     st = _lib.stream()
     acc = _lib.acc_dtype(dt)
-    d_sel = torch.empty_like(dout)
-    d_slide = torch.empty_like(dout)
     delta_sel = torch.empty((cfg.h, cfg.N), dtype=acc, device=dout.device)
     delta_slide = torch.empty_like(delta_sel)
     if full:
+        d_sel, d_slide = torch.empty_like(dout), torch.empty_like(dout)
         d_cmp = torch.empty_like(dout)
         delta_cmp = torch.empty_like(delta_sel)
         dtau = torch.empty((cfg.N, 3), dtype=acc, device=dout.device)
@@ -152,16 +151,32 @@ def nsa_backward(ctx: NSAContext, dout, *, full: bool = False):
                   _lib.ptr(ctx.k_cmp), _lib.ptr(ctx.v_cmp), _lib.ptr(d_cmp), _lib.ptr(ctx.lse_cmp),
                   _lib.ptr(delta_cmp), _lib.ptr(dQ), _lib.ptr(dK), _lib.ptr(dV), _lib.ptr(ws), st)
         return dQ, dK, dV, dtau
+    _, (dq_code, _) = _lib.buffer_dtypes(cfg, dt)
+    if dq_code == _lib.DT_BF16:
+        # tensor-core path: the gate folds into the branch statistics (raw
+        # dOut, lse - ln tau, delta = sum out * dOut) -- no gated dOut copies
+        lse_sel = torch.empty_like(delta_sel)
+        lse_slide = torch.empty_like(delta_sel)
+        _lib.call("fsa_gate_backward_fold", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(dout),
+                  _lib.ptr(ctx.tau), _lib.ptr(ctx.out_sel), _lib.ptr(ctx.out_slide),
+                  _lib.ptr(ctx.lse_sel), _lib.ptr(ctx.lse_slide), _lib.ptr(delta_sel),
+                  _lib.ptr(delta_slide), _lib.ptr(lse_sel), _lib.ptr(lse_slide), st)
+        return _sel_slide_backward(ctx, dout, dout, delta_sel, delta_slide, lse_sel, lse_slide)
     # gate backward into both differentiated branches + their deltas, one pass
+    d_sel, d_slide = torch.empty_like(dout), torch.empty_like(dout)
     _lib.call("fsa_gate_backward", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(dout),
               _lib.ptr(ctx.tau), _lib.ptr(ctx.out_sel), _lib.ptr(ctx.out_slide), _lib.ptr(d_sel),
               _lib.ptr(d_slide), _lib.ptr(delta_sel), _lib.ptr(delta_slide), st)
     return _sel_slide_backward(ctx, d_sel, d_slide, delta_sel, delta_slide)
 
 
-def _sel_slide_backward(ctx: NSAContext, d_sel, d_slide, delta_sel, delta_slide):
-    """Selected + sliding backward from the gated cotangents and their deltas."""
+def _sel_slide_backward(ctx: NSAContext, d_sel, d_slide, delta_sel, delta_slide, lse_sel=None,
+                        lse_slide=None):
+    """Selected + sliding backward from the gated cotangents and their deltas
+    (or, folded: the raw dOut with gate-adjusted lse -- fsa_gate_backward_fold)."""
     cfg, dt = ctx.cfg, ctx.dtype
+    lse_sel = ctx.lse_sel if lse_sel is None else lse_sel
+    lse_slide = ctx.lse_slide if lse_slide is None else lse_slide
     s = _lib.shape_of(cfg)
     st = _lib.stream()
     acc = _lib.acc_dtype(dt)
@@ -169,9 +184,9 @@ def _sel_slide_backward(ctx: NSAContext, d_sel, d_slide, delta_sel, delta_slide)
     _, (dq_code, dq_dtype) = _lib.buffer_dtypes(cfg, dt)
     if dq_code != _lib.DT_BF16:  # generic (f32 / f64 / small shapes) path
         dQ, dK, dV = _backward_core(cfg, dt, ctx.q, ctx.k, ctx.v, d_sel, ctx.sel, ctx.inv,
-                                    ctx.out_sel, ctx.lse_sel, delta=delta_sel)
+                                    ctx.out_sel, lse_sel, delta=delta_sel)
         return _slide_bwd_storage(cfg, dt, ctx.q, ctx.k, ctx.v, d_slide, ctx.out_slide,
-                                  ctx.lse_slide, accumulate_into=(dQ, dK, dV), delta=delta_slide)
+                                  lse_slide, accumulate_into=(dQ, dK, dV), delta=delta_slide)
     # tensor-core path: K8 (selected) writes dK/dV and the dq partials; the
     # sliding backward adds its dK/dV in-kernel and writes its dQ rows, which
     # the dQ reduce (K9) adds while summing the partials -- every gradient
@@ -182,14 +197,14 @@ def _sel_slide_backward(ctx: NSAContext, d_sel, d_slide, delta_sel, delta_slide)
     dK = torch.empty((cfg.N, cfg.h_K, cfg.d_K), dtype=acc, device=dev)
     dV = torch.empty((cfg.N, cfg.h_K, cfg.d_V), dtype=acc, device=dev)
     _lib.call("fsa_sel_bwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(ctx.q), _lib.ptr(ctx.k),
-              _lib.ptr(ctx.v), _lib.ptr(d_sel), _lib.ptr(ctx.lse_sel), _lib.ptr(delta_sel),
+              _lib.ptr(ctx.v), _lib.ptr(d_sel), _lib.ptr(lse_sel), _lib.ptr(delta_sel),
               _lib.ptr(inv.offsets), _lib.ptr(inv.qlist), _lib.ptr(inv.work), _lib.ptr(dq_buf),
               dq_code, _lib.ptr(dK), _lib.ptr(dV), st)
     dQ_slide = torch.empty((cfg.N, cfg.h, cfg.d_K), dtype=acc, device=dev)
     nws = _lib.lib().fsa_slide_bwd_workspace_bytes(ctypes.byref(s), _lib.dt_code(dt))
     ws = torch.empty(max(nws, 1), dtype=torch.uint8, device=dev)
     _lib.call("fsa_slide_bwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(ctx.q), _lib.ptr(ctx.k),
-              _lib.ptr(ctx.v), _lib.ptr(d_slide), _lib.ptr(ctx.lse_slide), _lib.ptr(delta_slide),
+              _lib.ptr(ctx.v), _lib.ptr(d_slide), _lib.ptr(lse_slide), _lib.ptr(delta_slide),
               _lib.ptr(dQ_slide), _lib.ptr(dK), _lib.ptr(dV), _lib.ptr(ws), 2, st)
     dQ = torch.empty((cfg.N, cfg.h, cfg.d_K), dtype=acc, device=dev)
     _lib.call("fsa_dq_reduce_add", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(ctx.sel.idx),
