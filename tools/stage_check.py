@@ -1,7 +1,7 @@
 """Run one kernel stage on a small bf16 problem (hang isolation / quick timing).
 
     python tools/stage_check.py <stage> [N]
-stages: slide_fwd cmp_fwd sel_fwd sel_bwd slide_bwd nsa
+stages: slide_fwd cmp_fwd sel_fwd sel_bwd slide_bwd nsa nsa_full
 """
 
 import os
@@ -52,6 +52,9 @@ def main():
     elif stage == "nsa":
         out, ctx = fsa.nsa_forward(q, k, v, torch.rand(N, 3, device="cuda", generator=g), cfg)
         r = fsa.nsa_backward(ctx, do)
+    elif stage == "nsa_full":  # + the compressed-branch backward (K8 compressed mode)
+        out, ctx = fsa.nsa_forward(q, k, v, torch.rand(N, 3, device="cuda", generator=g), cfg)
+        r = fsa.nsa_backward(ctx, do, full=True)
     torch.cuda.synchronize()
     print(f"{stage} N={N} ok {time.time() - t0:.3f}s", flush=True)
 
