@@ -7,7 +7,7 @@
  * selected through `_kernels/__init__.py:13-56`.  That granularity is one task
  * per call, far too fine for a GPU launch, so this ABI sits one level up: one
  * entry point per reference *operator* (cited per function below).  The Python
- * host layer (paper_2508_18224_b200/*.py) binds these with ctypes and mirrors
+ * host layer (the paper_2508_18224_b200 package) binds these with ctypes and mirrors
  * the reference's names, argument order and exceptions.
  *
  * Conventions

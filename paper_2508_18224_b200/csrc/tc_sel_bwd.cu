@@ -618,7 +618,7 @@ __global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const _
         mbar_spin_warp(bar(B_DQF + tm), tpar);
         if (r == 0) K8_TRACE(n, 5);  // products landed
         tc_fence_after();
-        if (SL != 0) {
+        if constexpr (SL != 0) {
           if (c + 1 == tr.nitems) kv_epilogue(tr, kseq);
           continue;
         }

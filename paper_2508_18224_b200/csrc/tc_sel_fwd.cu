@@ -28,7 +28,6 @@ constexpr int kQStages = 4;
 
 constexpr uint32_t kQBytes = kRows * kD * 2;     // 32768: [2 halves][128 rows][128 B]
 constexpr uint32_t kKVBytes = 2 * kBK * kD * 2;  // 32768: K [2][64][128 B], V [2][64][128 B]
-constexpr uint32_t kPBytes = kRows * kBK * 2;    // 16384: [128 rows][128 B]
 constexpr uint32_t kOffQ = 0;
 constexpr uint32_t kOffKV = kOffQ + kQStages * kQBytes;
 constexpr uint32_t kOffSt = kOffKV + 2 * kKVBytes;  // P lives in TMEM (A operand of PV)
