@@ -202,7 +202,7 @@ int cmp_fwd_impl(const fsa_shape* s, const void* Q, const void* Kc, const void* 
   const int64_t ntok = tc ? (s->B_K - 1 < s->N ? s->B_K - 1 : s->N) : s->N;
   if (tc) {
     // scores for the formed blocks come from the tensor cores for every g:
-    // fused into this pass for g <= 2, else a group-summed-query pass
+    // a separate group-summed-query pass (bf16 hi/lo pairs, ~fp32 accurate)
     if (int rc = tc_cmp_fwd(s, Q, Kc, Vc, out, lse, scores, workspace, st)) return rc;
   }
   const int64_t rows = s->h * ntok;

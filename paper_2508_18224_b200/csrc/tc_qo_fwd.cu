@@ -46,9 +46,10 @@ constexpr uint32_t kIdS = idesc_bf16(128, 64, false, false);
 constexpr uint32_t kIdPV = idesc_bf16(128, 128, false, true);
 constexpr float kRescale = 8.f;  // exp2 units
 
-// SCORES: importance scores only (no softmax / PV), for group sizes that do not
-// divide 32: run on the group-summed queries Qsum (g = 1) so no cross-warp
-// head reduction is needed; scores = Qsum . K_cmp * score_mul.
+// SCORES: importance scores only (no softmax / PV), on the group-summed
+// queries as bf16 hi/lo pairs (a g = 2 problem: the epilogue adds a token's
+// two rows) against K_cmp hi (K slot) + lo (V slot): scores = Qsum . K_cmp *
+// score_mul at ~fp32 accuracy.
 enum Mode { SLIDE = 0, CMP = 1, SCORES = 2 };
 
 #define QO_TRACE(w, item, slot)                                                          \
@@ -188,7 +189,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
           for (int hf = 0; hf < 2; ++hf)
             tma_load_3d(sb + kOffQ + (qs * 2 + w) * kQ + hf * 16384u, &p.tmQ, hf * 64,
                         c.it.kh * (int)p.g, c.it.s[w].t0, bar(B_QF + qs));
-        const bool with_v = M != SCORES;
+        const bool with_v = true;  // SCORES: the V slot carries K_cmp's low part
         for (int u = c.it.u0; u < c.it.u1; ++u, ++r) {
           const int v = (int)(r % kKVStages);
           mbar_spin(bar(B_KE + v), (uint32_t)(((r / kKVStages) & 1) ^ 1));
@@ -239,6 +240,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
                 for (int kk = 0; kk < 8; ++kk)
                   mma_bf16(tS, desc_kmajor(q + (kk >> 2) * 16384u + (kk & 3) * 32u),
                            desc_kmajor(k + (kk >> 2) * 8192u + (kk & 3) * 32u), kIdS, kk > 0);
+                if constexpr (M == SCORES) {  // + Q . K_lo^T (the V slot holds K_cmp's low part)
+#pragma unroll
+                  for (int kk = 0; kk < 8; ++kk)
+                    mma_bf16(tS, desc_kmajor(q + (kk >> 2) * 16384u + (kk & 3) * 32u),
+                             desc_kmajor(k + 16384u + (kk >> 2) * 8192u + (kk & 3) * 32u), kIdS, 1u);
+                }
                 mma_commit(bar(B_SF + 2 * w + v));
                 QO_TRACE(w, ns[w], 0);  // S issued
               }
@@ -542,25 +549,40 @@ Params base_params(const fsa_shape* s) {
   return p;
 }
 
-// Qsum[t][kh][:] = sum of the g query rows of kv head kh (fp32 sum, bf16 out)
+// Qsum[t][kh] = sum of the g query rows of kv head kh, as a bf16 hi/lo pair
+// Qs[t][kh][0] = bf16(sum), Qs[t][kh][1] = bf16(sum - hi): the scores pass runs
+// it as a g = 2 problem whose two rows per token are added in the epilogue, so
+// (hi + lo) . (K_hi + K_lo) keeps the scores at ~fp32 accuracy -- bf16 operands
+// alone flip ~2 % of the top-k selections against the float64 reference.
 __global__ void qsum_kernel(const __nv_bfloat16* __restrict__ Q, __nv_bfloat16* __restrict__ Qs,
                             int64_t N, int64_t h_K, int64_t g) {
   const int64_t row = blockIdx.x * 8ll + (threadIdx.x >> 5);  // (t, kh)
   if (row >= N * h_K) return;
   const int lane = threadIdx.x & 31;
   const __nv_bfloat16* src = Q + row * g * kD + lane * 4;
-  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  float a[4] = {0.f, 0.f, 0.f, 0.f};
   for (int64_t j = 0; j < g; ++j) {
     const uint2 u = *reinterpret_cast<const uint2*>(src + j * kD);
     const float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
     const float2 y = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
-    a0 += x.x; a1 += x.y; a2 += y.x; a3 += y.y;
+    a[0] += x.x; a[1] += x.y; a[2] += y.x; a[3] += y.y;
   }
-  const __nv_bfloat162 p0 = __floats2bfloat162_rn(a0, a1), p1 = __floats2bfloat162_rn(a2, a3);
-  uint2 o;
-  o.x = *reinterpret_cast<const uint32_t*>(&p0);
-  o.y = *reinterpret_cast<const uint32_t*>(&p1);
-  *reinterpret_cast<uint2*>(Qs + row * kD + lane * 4) = o;
+  __nv_bfloat16 hi[4], lo[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    hi[e] = __float2bfloat16_rn(a[e]);
+    lo[e] = __float2bfloat16_rn(a[e] - __bfloat162float(hi[e]));
+  }
+  *reinterpret_cast<uint2*>(Qs + (row * 2) * kD + lane * 4) = *reinterpret_cast<const uint2*>(hi);
+  *reinterpret_cast<uint2*>(Qs + (row * 2 + 1) * kD + lane * 4) = *reinterpret_cast<const uint2*>(lo);
+}
+
+// K_lo = bf16(K_cmp - bf16(K_cmp))
+__global__ void lo_part_kernel(const float* __restrict__ x, const __nv_bfloat16* __restrict__ hi,
+                               __nv_bfloat16* __restrict__ lo, int64_t n) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    lo[e] = __float2bfloat16_rn(x[e] - __bfloat162float(hi[e]));
 }
 
 }  // namespace
@@ -574,8 +596,8 @@ bool tc_qo_supported(const fsa_shape& s, int dtype) {
 // for larger groups the group-summed-query pass on the tensor cores is faster
 // (measured: g = 4 at 32K 0.72 -> 0.65 ms; g = 1 at 64K fused 1.62 vs 2.11 ms).
 bool tc_cmp_scores_fused(const fsa_shape& s) {
-  const int64_t g = s.h / s.h_K;
-  return g <= 2;
+  (void)s;
+  return false;  // every g: the hi/lo scores pass (selection parity with the fp64 reference)
 }
 bool tc_cmp_scores_any_g() { return true; }
 
@@ -596,9 +618,9 @@ int tc_slide_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V
 }
 
 size_t tc_cmp_workspace_bytes(const fsa_shape* s) {
-  // bf16 pooled K/V, then (for group sizes not dividing 32) the group-summed queries
+  // bf16 pooled K/V, then the group-summed queries as bf16 hi/lo pairs
   return (size_t)2 * (s->N / s->B_K) * s->h_K * kD * sizeof(__nv_bfloat16) +
-         (size_t)s->N * s->h_K * kD * sizeof(__nv_bfloat16);
+         (size_t)2 * s->N * s->h_K * kD * sizeof(__nv_bfloat16);
 }
 
 int tc_cmp_fwd(const fsa_shape* s, const void* Q, const void* Kc, const void* Vc, void* out,
@@ -622,16 +644,19 @@ int tc_cmp_fwd(const fsa_shape* s, const void* Q, const void* Kc, const void* Vc
   FSA_LAUNCH_CHECK("tc_cmp_fwd");
   if (scores != nullptr && !fused) {
     // scores on the tensor cores for any g: the g query rows of a kv head are
-    // summed first, then a g = 1 problem over Qsum computes Qsum . K_cmp
+    // summed first (hi/lo), then a g = 2 problem over (Qsum_hi, Qsum_lo) against
+    // K_cmp hi (the K slot) + lo (the V slot, overwriting the pooled V copy the
+    // compressed pass above has finished with) computes Qsum . K_cmp
     __nv_bfloat16* qs = vb + n;
+    lo_part_kernel<<<148, 256, 0, st>>>((const float*)Kc, kb, vb, n);
     qsum_kernel<<<(unsigned)((p.N * p.h_K + 7) / 8), 256, 0, st>>>((const __nv_bfloat16*)Q, qs,
                                                                     p.N, p.h_K, p.g);
     Params q = p;
     q.mode = SCORES;
     q.Q = qs;
-    q.h = p.h_K;
-    q.g = 1;
-    q.tpi = kRows;
+    q.h = 2 * p.h_K;
+    q.g = 2;
+    q.tpi = kRows / 2;
     q.n_super = (q.N + 2 * q.tpi - 1) / (2 * q.tpi);
     q.scores = (float*)scores;
     q.out = nullptr;

@@ -639,6 +639,8 @@ def test_selection_vs_oracle_fp64_scores_near_ties():
     want = O.select_topk(s64, c)
     rows = np.argwhere((got != want).any(-1))
     print(f"rows selecting differently under fp64 oracle scores: {len(rows)} of {c.h_K * c.N}")
+    # hi/lo bf16 scores keep ~fp32 accuracy: 1 row of 16,384 measured (bf16 operands: 293)
+    assert len(rows) <= 1e-3 * c.h_K * c.N
     for kh, t in rows:
         own = t // c.B_K
         cand = np.arange(own + 1)
