@@ -343,9 +343,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
         tmem_ld32(tS + 32, sv + 32);
         tmem_wait_ld();
         const int kbase = kt * 64;
-        if (M != SLIDE && p.scores != nullptr) {
-          // group mean over the g heads of this token (rows of a token are
-          // adjacent lanes; g divides 32), written by the token's first row
+        if (M == SCORES) {
+          // the token's rows (hi, lo) are adjacent lanes: summed, written by the first
           const float gm = p.score_mul;
           float* dst = p.scores + ((int64_t)c.it.kh * p.N + t) * p.b + kbase;
           const bool wr = ok && hh == 0;
