@@ -49,6 +49,13 @@ extern "C" {
 
 typedef enum { FSA_DT_F32 = 0, FSA_DT_F64 = 1, FSA_DT_BF16 = 2, FSA_DT_I32 = 3 } fsa_dtype;
 
+/* OR-ed into the dtype argument of fsa_slide_fwd, fsa_cmp_attn_fwd,
+ * fsa_merge_combine_fwd, fsa_gate_backward_fold and fsa_gate_backward_full: the
+ * branch outputs (out_cmp, out_slide, out_sel) are bf16 instead of the
+ * accumulator dtype -- bf16 tensor-core path only (the NSA step uses it: the
+ * branch outputs are intermediates of the bf16 combined output). */
+#define FSA_OUT_NARROW 0x100
+
 /* Resolved AttentionConfig (config.py:30-104); scale = 1/sqrt(d_K). */
 typedef struct fsa_shape {
   int64_t N, d_K, d_V, h, h_K, B_K, T, W;

@@ -19,6 +19,7 @@ FSA_OK, FSA_ERR_INVALID, FSA_ERR_CUDA, FSA_ERR_UNSUPPORTED = 0, 1, 2, 3
 DT_F32, DT_F64, DT_BF16, DT_I32 = 0, 1, 2, 3
 FWD_LOCAL, FWD_STATS, FWD_GLOBAL = 0, 1, 2
 MERGE_LOCAL, MERGE_STATS, MERGE_REDUCE = 0, 1, 2
+OUT_NARROW = 0x100  # FSA_OUT_NARROW: branch outputs in bf16 (include/fsa_b200.h)
 
 SEL_FLAGS = (  # bit, message -- in the reference's check order (selection.py:59-75)
     (1, "malformed selection: empty row"),

@@ -19,11 +19,11 @@ __device__ __forceinline__ typename Acc<T>::type dot_row(const T* q, const KT* k
 // compressed attention: token t attends the (t+1)//B_K formed pooled rows;
 // pending tokens copy their prefix row (branches.py:72-77).
 // ---------------------------------------------------------------------------
-template <typename T>
+template <typename T, typename O = typename Acc<T>::type>  // O: out element type
 __global__ void cmp_fwd_generic(const T* __restrict__ Q, const typename Acc<T>::type* __restrict__ Kc,
                                 const typename Acc<T>::type* __restrict__ Vc,
                                 const typename Acc<T>::type* __restrict__ Kp,
-                                const typename Acc<T>::type* __restrict__ Vp, typename Acc<T>::type* __restrict__ out,
+                                const typename Acc<T>::type* __restrict__ Vp, O* __restrict__ out,
                                 typename Acc<T>::type* __restrict__ lse, fsa_shape s,
                                 int64_t ntok) {
   // ntok < N: only the first ntok tokens (the pending ones on the tensor-core path)
@@ -34,7 +34,7 @@ __global__ void cmp_fwd_generic(const T* __restrict__ Q, const typename Acc<T>::
   const int64_t j = wid / ntok, t = wid % ntok, g = s.h / s.h_K, kh = j / g;
   const int64_t dK = s.d_K, dV = s.d_V;
   const T* q = Q + (t * s.h + j) * dK;
-  A* o = out + (t * s.h + j) * dV;
+  O* o = out + (t * s.h + j) * dV;
   const int64_t nf = (t + 1) / s.B_K;
   const A scale = A(s.scale);
   if (nf == 0) {
@@ -42,7 +42,7 @@ __global__ void cmp_fwd_generic(const T* __restrict__ Q, const typename Acc<T>::
     A acc = 0;
     for (int64_t c = lane; c < dK; c += 32) acc += to_acc(q[c]) * kp[c];
     acc = warp_sum(acc);
-    for (int64_t c = lane; c < dV; c += 32) o[c] = Vp[(t * s.h_K + kh) * dV + c];
+    for (int64_t c = lane; c < dV; c += 32) o[c] = from_acc<O>(Vp[(t * s.h_K + kh) * dV + c]);
     if (lane == 0) lse[j * s.N + t] = acc * scale;
     return;
   }
@@ -64,7 +64,7 @@ __global__ void cmp_fwd_generic(const T* __restrict__ Q, const typename Acc<T>::
       }
     }
     if (c0 == 0) l = warp_sum(l);
-    if (c0 + lane < dV) o[c0 + lane] = acc / l;
+    if (c0 + lane < dV) o[c0 + lane] = from_acc<O>(acc / l);
   }
   if (lane == 0) lse[j * s.N + t] = m + log_acc(l);
 }
@@ -193,7 +193,7 @@ __global__ void slide_bwd_dkdv_generic(const T* __restrict__ Q, const T* __restr
 template <typename T>
 int cmp_fwd_impl(const fsa_shape* s, const void* Q, const void* Kc, const void* Vc, const void* Kp,
                  const void* Vp, void* out, void* lse, void* scores, void* workspace,
-                 cudaStream_t st) {
+                 cudaStream_t st, int narrow) {
   using A = typename Acc<T>::type;
   const int dt = sizeof(T) == 8 ? FSA_DT_F64 : (sizeof(T) == 4 ? FSA_DT_F32 : FSA_DT_BF16);
   const bool tc = tc_qo_supported(*s, dt) && workspace != nullptr;
@@ -203,10 +203,15 @@ int cmp_fwd_impl(const fsa_shape* s, const void* Q, const void* Kc, const void* 
   if (tc) {
     // scores for the formed blocks come from the tensor cores for every g:
     // a separate group-summed-query pass (bf16 hi/lo pairs, ~fp32 accurate)
-    if (int rc = tc_cmp_fwd(s, Q, Kc, Vc, out, lse, scores, workspace, st)) return rc;
+    if (int rc = tc_cmp_fwd(s, Q, Kc, Vc, out, lse, scores, workspace, st, narrow)) return rc;
   }
+  FSA_REQUIRE(!narrow || (tc && sizeof(T) == 2), "cmp_attn_fwd: narrow output needs the bf16 tensor-core path");
   const int64_t rows = s->h * ntok;
-  if (rows > 0)
+  if (rows > 0 && narrow)
+    cmp_fwd_generic<T, __nv_bfloat16><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(
+        (const T*)Q, (const A*)Kc, (const A*)Vc, (const A*)Kp, (const A*)Vp, (__nv_bfloat16*)out,
+        (A*)lse, *s, ntok);
+  else if (rows > 0)
     cmp_fwd_generic<T><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(
         (const T*)Q, (const A*)Kc, (const A*)Vc, (const A*)Kp, (const A*)Vp, (A*)out, (A*)lse, *s,
         ntok);
@@ -260,8 +265,10 @@ extern "C" int fsa_cmp_attn_fwd(const fsa_shape* s, int dtype, const void* Q, co
                                 const void* V_cmp, const void* K_prefix, const void* V_prefix,
                                 void* out, void* lse, void* scores, void* workspace,
                                 void* stream) {
+  const int narrow = (dtype & FSA_OUT_NARROW) != 0;
+  dtype &= ~FSA_OUT_NARROW;
   DISPATCH_DT(dtype, cmp_fwd_impl, s, Q, K_cmp, V_cmp, K_prefix, V_prefix, out, lse, scores,
-              workspace, (cudaStream_t)stream);
+              workspace, (cudaStream_t)stream, narrow);
 }
 
 extern "C" size_t fsa_cmp_workspace_bytes(const fsa_shape* s) {
@@ -270,8 +277,11 @@ extern "C" size_t fsa_cmp_workspace_bytes(const fsa_shape* s) {
 
 extern "C" int fsa_slide_fwd(const fsa_shape* s, int dtype, const void* Q, const void* K,
                              const void* V, void* out, void* lse, void* stream) {
+  const int narrow = (dtype & FSA_OUT_NARROW) != 0;
+  dtype &= ~FSA_OUT_NARROW;
   if (fsa::tc_qo_supported(*s, dtype))
-    return fsa::tc_slide_fwd(s, Q, K, V, out, lse, (cudaStream_t)stream);
+    return fsa::tc_slide_fwd(s, Q, K, V, out, lse, (cudaStream_t)stream, narrow);
+  FSA_REQUIRE(!narrow, "slide_fwd: narrow output needs the bf16 tensor-core path");
   DISPATCH_DT(dtype, slide_fwd_impl, s, Q, K, V, out, lse, (cudaStream_t)stream);
 }
 

@@ -141,12 +141,11 @@ __global__ void cmp_pool_bwd(const typename Acc<T>::type* __restrict__ dKc,
 // Gate backward for all three branches + their deltas + dtau: warp per token.
 //   d_c = tau[t,c] dOut (rounded to T), delta_c[j,t] = sum_v out_c * d_c,
 //   dtau[t,c] = sum_{j,v} out_c * dOut            (branches.py:103)
-template <typename T>
+template <typename T, typename B = typename Acc<T>::type>  // B: branch-output element type
 __global__ void gate_backward_full_kernel(const T* __restrict__ dOut,
                                           const typename Acc<T>::type* __restrict__ tau,
-                                          const typename Acc<T>::type* __restrict__ o0,
-                                          const typename Acc<T>::type* __restrict__ o1,
-                                          const typename Acc<T>::type* __restrict__ o2,
+                                          const B* __restrict__ o0, const B* __restrict__ o1,
+                                          const B* __restrict__ o2,
                                           T* __restrict__ d0, T* __restrict__ d1, T* __restrict__ d2,
                                           typename Acc<T>::type* __restrict__ del0,
                                           typename Acc<T>::type* __restrict__ del1,
@@ -164,7 +163,7 @@ __global__ void gate_backward_full_kernel(const T* __restrict__ dOut,
     A s0 = 0, s1 = 0, s2 = 0;
     for (int64_t c = lane; c < dv; c += 32) {
       const A x = to_acc(dOut[base + c]);
-      const A a0 = o0[base + c], a1 = o1[base + c], a2 = o2[base + c];
+      const A a0 = to_acc(o0[base + c]), a1 = to_acc(o1[base + c]), a2 = to_acc(o2[base + c]);
       const T r0 = from_acc<T>(w0 * x), r1 = from_acc<T>(w1 * x), r2 = from_acc<T>(w2 * x);
       d0[base + c] = r0;
       d1[base + c] = r1;
@@ -299,12 +298,19 @@ int cmp_bwd_impl(const fsa_shape* s, const void* Q, const void* Kc, const void* 
 template <typename T>
 int gate_bwd_full_impl(const fsa_shape* s, const void* dOut, const void* tau, const void* o0,
                        const void* o1, const void* o2, void* d0, void* d1, void* d2, void* del0,
-                       void* del1, void* del2, void* dtau, cudaStream_t st) {
+                       void* del1, void* del2, void* dtau, cudaStream_t st, int narrow) {
   using A = typename Acc<T>::type;
   if (s->N == 0) return FSA_OK;
-  gate_backward_full_kernel<T><<<(unsigned)((s->N + 7) / 8), 256, 0, st>>>(
-      (const T*)dOut, (const A*)tau, (const A*)o0, (const A*)o1, (const A*)o2, (T*)d0, (T*)d1,
-      (T*)d2, (A*)del0, (A*)del1, (A*)del2, (A*)dtau, s->N, s->h, s->d_V);
+  FSA_REQUIRE(!narrow || sizeof(T) == 2, "gate_backward_full: narrow outputs need bf16");
+  if (narrow)
+    gate_backward_full_kernel<T, __nv_bfloat16><<<(unsigned)((s->N + 7) / 8), 256, 0, st>>>(
+        (const T*)dOut, (const A*)tau, (const __nv_bfloat16*)o0, (const __nv_bfloat16*)o1,
+        (const __nv_bfloat16*)o2, (T*)d0, (T*)d1, (T*)d2, (A*)del0, (A*)del1, (A*)del2, (A*)dtau,
+        s->N, s->h, s->d_V);
+  else
+    gate_backward_full_kernel<T><<<(unsigned)((s->N + 7) / 8), 256, 0, st>>>(
+        (const T*)dOut, (const A*)tau, (const A*)o0, (const A*)o1, (const A*)o2, (T*)d0, (T*)d1,
+        (T*)d2, (A*)del0, (A*)del1, (A*)del2, (A*)dtau, s->N, s->h, s->d_V);
   FSA_LAUNCH_CHECK("gate_backward_full");
   return FSA_OK;
 }
@@ -339,6 +345,8 @@ extern "C" int fsa_gate_backward_full(const fsa_shape* s, int dtype, const void*
                                       const void* out_slide, void* d_cmp, void* d_sel,
                                       void* d_slide, void* delta_cmp, void* delta_sel,
                                       void* delta_slide, void* dtau, void* stream) {
+  const int narrow = (dtype & FSA_OUT_NARROW) != 0;
+  dtype &= ~FSA_OUT_NARROW;
   DISPATCH_DT(dtype, gate_bwd_full_impl, s, dOut, tau, out_cmp, out_sel, out_slide, d_cmp, d_sel,
-              d_slide, delta_cmp, delta_sel, delta_slide, dtau, (cudaStream_t)stream);
+              d_slide, delta_cmp, delta_sel, delta_slide, dtau, (cudaStream_t)stream, narrow);
 }

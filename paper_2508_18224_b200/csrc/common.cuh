@@ -25,6 +25,7 @@ template <> __device__ __forceinline__ float from_acc<float>(float x) { return x
 template <> __device__ __forceinline__ __nv_bfloat16 from_acc<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
 template <typename T> __device__ __forceinline__ T from_acc(double x);
 template <> __device__ __forceinline__ double from_acc<double>(double x) { return x; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_acc<__nv_bfloat16>(double x) { return __double2bfloat16(x); }
 
 __device__ __forceinline__ float exp_acc(float x) { return expf(x); }
 __device__ __forceinline__ double exp_acc(double x) { return exp(x); }

@@ -29,17 +29,28 @@ __device__ __forceinline__ int row_len(const int32_t* row, int T, int lane) {
 
 // Gated-combine epilogue (branches.py:95-104): with cmb.out != null the warp
 // also writes out = ((0 + tau0 out_cmp) + tau1 out_sel) + tau2 out_slide (bf16).
+// kNarrow: out_cmp / out_slide are read and out (out_sel) written as bf16.
 struct Combine {
-  const float* out_cmp;
-  const float* out_slide;
+  const void* out_cmp;
+  const void* out_slide;
   const float* tau;
   __nv_bfloat16* out;
 };
 
-template <int TMAX>  // >= T: partial rows held in registers
+__device__ __forceinline__ void ld4(const void* p, int64_t e, bool narrow, float (&v)[4]) {
+  if (narrow) {
+    const float4 x = ld_bf16x4(reinterpret_cast<const __nv_bfloat16*>(p) + e);
+    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+  } else {
+    const float4 x = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p) + e);
+    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+  }
+}
+
+template <int TMAX, bool kNarrow>  // TMAX >= T: partial rows held in registers
 __global__ void __launch_bounds__(256) merge_bf16_kernel(
     const int32_t* __restrict__ idx, const __nv_bfloat16* __restrict__ obuf,
-    const float2* __restrict__ ml, float* __restrict__ out, float* __restrict__ lse,
+    const float2* __restrict__ ml, void* __restrict__ out, float* __restrict__ lse,
     float* __restrict__ m_out, float* __restrict__ l_out, int64_t N, int64_t h, int64_t g, int T,
     Combine cmb) {
   const int lane = threadIdx.x & 31;
@@ -59,10 +70,8 @@ __global__ void __launch_bounds__(256) merge_bf16_kernel(
   float2 st = lane < len ? __ldg(ml + rb + lane) : make_float2(-INFINITY, 0.f);
   float cm[4], cs[4], tw[3];
   if (cmb.out) {
-    const float4 a = *reinterpret_cast<const float4*>(cmb.out_cmp + (t * h + j) * kD + lane * 4);
-    const float4 b = *reinterpret_cast<const float4*>(cmb.out_slide + (t * h + j) * kD + lane * 4);
-    cm[0] = a.x; cm[1] = a.y; cm[2] = a.z; cm[3] = a.w;
-    cs[0] = b.x; cs[1] = b.y; cs[2] = b.z; cs[3] = b.w;
+    ld4(cmb.out_cmp, (t * h + j) * kD + lane * 4, kNarrow, cm);
+    ld4(cmb.out_slide, (t * h + j) * kD + lane * 4, kNarrow, cs);
     tw[0] = __ldg(cmb.tau + t * 3);
     tw[1] = __ldg(cmb.tau + t * 3 + 1);
     tw[2] = __ldg(cmb.tau + t * 3 + 2);
@@ -86,7 +95,15 @@ __global__ void __launch_bounds__(256) merge_bf16_kernel(
   }
   const float inv = 1.f / L;
   const float4 o = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
-  *reinterpret_cast<float4*>(out + (t * h + j) * kD + lane * 4) = o;
+  if (kNarrow) {
+    const __nv_bfloat162 p0 = __floats2bfloat162_rn(o.x, o.y), p1 = __floats2bfloat162_rn(o.z, o.w);
+    uint2 u;
+    u.x = *reinterpret_cast<const uint32_t*>(&p0);
+    u.y = *reinterpret_cast<const uint32_t*>(&p1);
+    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(out) + (t * h + j) * kD + lane * 4) = u;
+  } else {
+    *reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + (t * h + j) * kD + lane * 4) = o;
+  }
   if (cmb.out) {
     const float ov[4] = {o.x, o.y, o.z, o.w};
     float r[4];
@@ -149,9 +166,9 @@ int merge_bf16_fast(const fsa_shape* s, const int32_t* idx, const void* obuf, co
                     void* out, void* lse, void* m_out, void* l_out, cudaStream_t st) {
   const int64_t rows = s->h * s->N;
   if (rows == 0) return FSA_OK;
-  auto kern = s->T <= 16 ? merge_bf16_kernel<16> : merge_bf16_kernel<32>;
+  auto kern = s->T <= 16 ? merge_bf16_kernel<16, false> : merge_bf16_kernel<32, false>;
   kern<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(
-      idx, (const __nv_bfloat16*)obuf, (const float2*)ml, (float*)out, (float*)lse, (float*)m_out,
+      idx, (const __nv_bfloat16*)obuf, (const float2*)ml, out, (float*)lse, (float*)m_out,
       (float*)l_out, s->N, s->h, s->h / s->h_K, (int)s->T, Combine{});
   FSA_LAUNCH_CHECK("merge_bf16");
   return FSA_OK;
@@ -159,13 +176,15 @@ int merge_bf16_fast(const fsa_shape* s, const int32_t* idx, const void* obuf, co
 
 int merge_combine_bf16_fast(const fsa_shape* s, const int32_t* idx, const void* obuf,
                             const void* ml, const void* out_cmp, const void* out_slide,
-                            const void* tau, void* out_sel, void* lse, void* out, cudaStream_t st) {
+                            const void* tau, void* out_sel, void* lse, void* out, cudaStream_t st,
+                            int narrow) {
   const int64_t rows = s->h * s->N;
   if (rows == 0) return FSA_OK;
-  Combine c{(const float*)out_cmp, (const float*)out_slide, (const float*)tau, (__nv_bfloat16*)out};
-  auto kern = s->T <= 16 ? merge_bf16_kernel<16> : merge_bf16_kernel<32>;
+  Combine c{out_cmp, out_slide, (const float*)tau, (__nv_bfloat16*)out};
+  auto kern = narrow ? (s->T <= 16 ? merge_bf16_kernel<16, true> : merge_bf16_kernel<32, true>)
+                     : (s->T <= 16 ? merge_bf16_kernel<16, false> : merge_bf16_kernel<32, false>);
   kern<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(
-      idx, (const __nv_bfloat16*)obuf, (const float2*)ml, (float*)out_sel, (float*)lse, nullptr,
+      idx, (const __nv_bfloat16*)obuf, (const float2*)ml, out_sel, (float*)lse, nullptr,
       nullptr, s->N, s->h, s->h / s->h_K, (int)s->T, c);
   FSA_LAUNCH_CHECK("merge_combine_bf16");
   return FSA_OK;

@@ -443,9 +443,12 @@ extern "C" int fsa_merge_combine_fwd(const fsa_shape* s, int dtype, const int32_
                                      const void* out_cmp, const void* out_slide, const void* tau,
                                      void* out_sel, void* lse, void* out, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
+  const int narrow = (dtype & FSA_OUT_NARROW) != 0;
+  dtype &= ~FSA_OUT_NARROW;
   if (dtype == FSA_DT_BF16 && obuf_dtype == FSA_DT_BF16 && fsa::fast_reduce_ok(*s))
     return fsa::merge_combine_bf16_fast(s, idx, obuf, ml, out_cmp, out_slide, tau, out_sel, lse,
-                                        out, st);
+                                        out, st, narrow);
+  FSA_REQUIRE(!narrow, "merge_combine_fwd: narrow branch outputs need the bf16 fast path");
   int rc = fsa_merge_fwd(s, dtype, FSA_MERGE_LOCAL, idx, obuf, obuf_dtype, ml, nullptr, nullptr,
                          out_sel, lse, nullptr, nullptr, 0, stream);
   if (rc) return rc;

@@ -20,10 +20,10 @@ int tc_sel_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V, 
 bool tc_qo_supported(const fsa_shape& s, int dtype);
 bool tc_cmp_scores_fused(const fsa_shape& s);
 int tc_slide_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V, void* out,
-                 void* lse, cudaStream_t st);
+                 void* lse, cudaStream_t st, int out_bf16 = 0);
 size_t tc_cmp_workspace_bytes(const fsa_shape* s);
 int tc_cmp_fwd(const fsa_shape* s, const void* Q, const void* Kc, const void* Vc, void* out,
-               void* lse, void* scores, void* workspace, cudaStream_t st);
+               void* lse, void* scores, void* workspace, cudaStream_t st, int out_bf16 = 0);
 
 // sliding-window backward on the FSA backward kernel (tc_sel_bwd.cu)
 size_t tc_slide_bwd_workspace_bytes(const fsa_shape* s);
@@ -50,7 +50,8 @@ int merge_bf16_fast(const fsa_shape* s, const int32_t* idx, const void* obuf, co
                     void* out, void* lse, void* m_out, void* l_out, cudaStream_t st);
 int merge_combine_bf16_fast(const fsa_shape* s, const int32_t* idx, const void* obuf,
                             const void* ml, const void* out_cmp, const void* out_slide,
-                            const void* tau, void* out_sel, void* lse, void* out, cudaStream_t st);
+                            const void* tau, void* out_sel, void* lse, void* out, cudaStream_t st,
+                            int narrow = 0);
 int dq_reduce_bf16_fast(const fsa_shape* s, const int32_t* idx, const void* dq, void* dQ,
                         cudaStream_t st, const void* addend = nullptr);
 

@@ -59,11 +59,12 @@ enum Mode { SLIDE = 0, CMP = 1, SCORES = 2 };
   } while (0)
 
 struct Params {
-  CUtensorMap tmOut;  // out fp32 boxes (32, g, tpi): the epilogue TMA store
+  CUtensorMap tmOut;  // out boxes (fp32: 32 or bf16: 64 columns, g, tpi): the epilogue TMA store
   CUtensorMap tmQ, tmK, tmV;
   long long* trace;  // debug timeline (CTA 0), null in production         // TMA: Q box (64, g, tpi), key/value boxes (64, 1, 64)
   const __nv_bfloat16 *Q, *Kx, *Vx;  // keys/values: K,V [N][h_K][128] or pooled [b][h_K][128]
-  float *out, *lse, *scores;
+  float *out, *lse, *scores;  // out: fp32, or bf16 when out_bf16
+  int out_bf16;
   int64_t N, h, h_K, g, W, B_K, b, n_keys, n_super;
   int tpi, mode;
   float scale, scale_log2;
@@ -447,6 +448,30 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
       // stores.  Rows without a visible key are stored as 0 (the compressed
       // branch's pending tokens are written after this kernel).
       unsigned char* qsub = smem + kOffQ + ((c.seq & 1) * 2 + w) * kQ;
+      if (p.out_bf16) {  // bf16 rows: both 64-column boxes fit the Q sub-tile at once
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float ov[32];
+          tmem_ld32(tmem + lb + 128u + q * 32, ov);
+          tmem_wait_ld();
+          unsigned char* box = qsub + (q >> 1) * 16384u;
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc)
+            *reinterpret_cast<uint4*>(box + sw128_off(r, (q & 1) * 4 + cc)) =
+                make_uint4(pack_bf16(ov[8 * cc] * inv, ov[8 * cc + 1] * inv),
+                           pack_bf16(ov[8 * cc + 2] * inv, ov[8 * cc + 3] * inv),
+                           pack_bf16(ov[8 * cc + 4] * inv, ov[8 * cc + 5] * inv),
+                           pack_bf16(ov[8 * cc + 6] * inv, ov[8 * cc + 7] * inv));
+        }
+        fence_proxy_async();
+        named_bar(1 + w, 128);
+        if (r == 0) {
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf)
+            tma_store_3d(&p.tmOut, hf * 64, c.it.kh * (int)p.g, s.t0, smem_u32(qsub) + hf * 16384u);
+          bulk_commit();
+        }
+      } else {
 #pragma unroll
       for (int pass = 0; pass < 2; ++pass) {
         if (pass == 1) {
@@ -475,6 +500,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
                          smem_u32(qsub) + qq * 16384u);
           bulk_commit();
         }
+      }
       }
       if (r == 0) {
         bulk_wait_read();
@@ -509,7 +535,9 @@ int launch(Params& p, cudaStream_t st) {
   int rc = make_tmap_tokens(&p.tmQ, p.Q, p.N, p.h, (int)p.g, p.tpi);
   if (!rc) rc = make_tmap_tokens(&p.tmK, p.Kx, p.n_keys, p.h_K, 1, 64);
   if (!rc) rc = make_tmap_tokens(&p.tmV, p.Vx, p.n_keys, p.h_K, 1, 64);
-  if (!rc && p.out) rc = make_tmap_tokens_f32(&p.tmOut, p.out, p.N, p.h, (int)p.g, p.tpi);
+  if (!rc && p.out)
+    rc = p.out_bf16 ? make_tmap_tokens(&p.tmOut, p.out, p.N, p.h, (int)p.g, p.tpi)
+                    : make_tmap_tokens_f32(&p.tmOut, p.out, p.N, p.h, (int)p.g, p.tpi);
   if (rc) return rc;
   static bool attr = false;
   if (!attr) {
@@ -601,9 +629,10 @@ bool tc_cmp_scores_fused(const fsa_shape& s) {
 bool tc_cmp_scores_any_g() { return true; }
 
 int tc_slide_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V, void* out,
-                 void* lse, cudaStream_t st) {
+                 void* lse, cudaStream_t st, int out_bf16) {
   Params p = base_params(s);
   p.mode = SLIDE;
+  p.out_bf16 = out_bf16;
   p.Q = (const __nv_bfloat16*)Q;
   p.Kx = (const __nv_bfloat16*)K;
   p.Vx = (const __nv_bfloat16*)V;
@@ -623,9 +652,10 @@ size_t tc_cmp_workspace_bytes(const fsa_shape* s) {
 }
 
 int tc_cmp_fwd(const fsa_shape* s, const void* Q, const void* Kc, const void* Vc, void* out,
-               void* lse, void* scores, void* workspace, cudaStream_t st) {
+               void* lse, void* scores, void* workspace, cudaStream_t st, int out_bf16) {
   Params p = base_params(s);
   p.mode = CMP;
+  p.out_bf16 = out_bf16;
   const int64_t n = p.b * p.h_K * kD;
   __nv_bfloat16* kb = (__nv_bfloat16*)workspace;
   __nv_bfloat16* vb = kb + n;

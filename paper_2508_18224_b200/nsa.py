@@ -53,6 +53,7 @@ class NSAContext:
     k_cmp: torch.Tensor = None
     v_cmp: torch.Tensor = None
     lse_cmp: torch.Tensor = None
+    narrow: bool = False  # out_cmp / out_slide / out_sel in bf16 (FSA_OUT_NARROW)
 
 
 def nsa_forward(q, k, v, tau, cfg, *, heads=None):
@@ -69,6 +70,14 @@ def nsa_forward(q, k, v, tau, cfg, *, heads=None):
     dev = q.device
     s = _lib.shape_of(cfg)
     st = _lib.stream()
+    # bf16 tensor-core path: the three branch outputs are bf16 intermediates of
+    # the bf16 combined output (half the HBM traffic in the window forward, the
+    # merge + combine and the gate backward)
+    (ob0, _), _ = _lib.buffer_dtypes(cfg, dt)
+    narrow = (dt == torch.bfloat16 and ob0 == _lib.DT_BF16 and cfg.d_K == 128 and cfg.d_V == 128
+              and cfg.T <= 32)
+    branch_dt = torch.bfloat16 if narrow else acc
+    nflag = _lib.OUT_NARROW if narrow else 0
     n_pref = min(cfg.B_K - 1, cfg.N)
     Kc = torch.empty((cfg.b, cfg.h_K, cfg.d_K), dtype=acc, device=dev)
     Vc = torch.empty((cfg.b, cfg.h_K, cfg.d_V), dtype=acc, device=dev)
@@ -76,11 +85,11 @@ def nsa_forward(q, k, v, tau, cfg, *, heads=None):
     Vp = torch.empty((max(n_pref, 1), cfg.h_K, cfg.d_V), dtype=acc, device=dev)
     _lib.call("fsa_compress_kv", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(k), _lib.ptr(v),
               _lib.ptr(Kc), _lib.ptr(Vc), _lib.ptr(Kp), _lib.ptr(Vp), st)
-    out_cmp = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=acc, device=dev)
+    out_cmp = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=branch_dt, device=dev)
     lse_cmp = torch.empty((cfg.h, cfg.N), dtype=acc, device=dev)
     scores = torch.empty((cfg.h_K, cfg.N, cfg.b), dtype=acc, device=dev)
     ws = _cmp_workspace(cfg, dev)
-    _lib.call("fsa_cmp_attn_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(q), _lib.ptr(Kc),
+    _lib.call("fsa_cmp_attn_fwd", ctypes.byref(s), _lib.dt_code(dt) | nflag, _lib.ptr(q), _lib.ptr(Kc),
               _lib.ptr(Vc), _lib.ptr(Kp), _lib.ptr(Vp), _lib.ptr(out_cmp), _lib.ptr(lse_cmp),
               _lib.ptr(scores), _lib.ptr(ws), st)
     idx = torch.empty((cfg.h_K, cfg.N, cfg.T), dtype=torch.int32, device=dev)
@@ -109,16 +118,16 @@ def nsa_forward(q, k, v, tau, cfg, *, heads=None):
     # K5 writes the slot partials; the sliding branch runs before the merge so
     # that K6 can apply the gated combine (K12) in the same pass
     obuf, ml, ob_code = _sel_partials(cfg, dt, q, k, v, inv)
-    out_slide, lse_slide = _slide_fwd_storage(cfg, dt, q, k, v)
-    out_sel = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=acc, device=dev)
+    out_slide, lse_slide = _slide_fwd_storage(cfg, dt, q, k, v, narrow=narrow)
+    out_sel = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=branch_dt, device=dev)
     lse_sel = torch.empty((cfg.h, cfg.N), dtype=acc, device=dev)
     out = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=dt, device=dev)
-    _lib.call("fsa_merge_combine_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(sel.idx),
+    _lib.call("fsa_merge_combine_fwd", ctypes.byref(s), _lib.dt_code(dt) | nflag, _lib.ptr(sel.idx),
               _lib.ptr(obuf), ob_code, _lib.ptr(ml), _lib.ptr(out_cmp), _lib.ptr(out_slide),
               _lib.ptr(tau), _lib.ptr(out_sel), _lib.ptr(lse_sel), _lib.ptr(out), st)
     del obuf, ml
     ctx = NSAContext(cfg, dt, q, k, v, tau, sel, inv, out_sel, lse_sel, out_slide, lse_slide,
-                     out_cmp, scores, Kc, Vc, lse_cmp)
+                     out_cmp, scores, Kc, Vc, lse_cmp, narrow)
     return out, ctx
 
 
@@ -140,7 +149,8 @@ def nsa_backward(ctx: NSAContext, dout, *, full: bool = False):
         d_cmp = torch.empty_like(dout)
         delta_cmp = torch.empty_like(delta_sel)
         dtau = torch.empty((cfg.N, 3), dtype=acc, device=dout.device)
-        _lib.call("fsa_gate_backward_full", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(dout),
+        nflag = _lib.OUT_NARROW if ctx.narrow else 0
+        _lib.call("fsa_gate_backward_full", ctypes.byref(s), _lib.dt_code(dt) | nflag, _lib.ptr(dout),
                   _lib.ptr(ctx.tau), _lib.ptr(ctx.out_cmp), _lib.ptr(ctx.out_sel),
                   _lib.ptr(ctx.out_slide), _lib.ptr(d_cmp), _lib.ptr(d_sel), _lib.ptr(d_slide),
                   _lib.ptr(delta_cmp), _lib.ptr(delta_sel), _lib.ptr(delta_slide), _lib.ptr(dtau), st)
@@ -157,7 +167,8 @@ def nsa_backward(ctx: NSAContext, dout, *, full: bool = False):
         # dOut, lse - ln tau, delta = sum out * dOut) -- no gated dOut copies
         lse_sel = torch.empty_like(delta_sel)
         lse_slide = torch.empty_like(delta_sel)
-        _lib.call("fsa_gate_backward_fold", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(dout),
+        nflag = _lib.OUT_NARROW if ctx.narrow else 0
+        _lib.call("fsa_gate_backward_fold", ctypes.byref(s), _lib.dt_code(dt) | nflag, _lib.ptr(dout),
                   _lib.ptr(ctx.tau), _lib.ptr(ctx.out_sel), _lib.ptr(ctx.out_slide),
                   _lib.ptr(ctx.lse_sel), _lib.ptr(ctx.lse_slide), _lib.ptr(delta_sel),
                   _lib.ptr(delta_slide), _lib.ptr(lse_sel), _lib.ptr(lse_slide), st)
