@@ -50,7 +50,8 @@ extern "C" {
 typedef enum { FSA_DT_F32 = 0, FSA_DT_F64 = 1, FSA_DT_BF16 = 2, FSA_DT_I32 = 3 } fsa_dtype;
 
 /* OR-ed into the dtype argument of fsa_slide_fwd, fsa_cmp_attn_fwd,
- * fsa_merge_combine_fwd, fsa_gate_backward_fold and fsa_gate_backward_full: the
+ * fsa_merge_combine_fwd, fsa_gate_backward_fold, fsa_gate_backward_full (and of
+ * fsa_dq_reduce_add, for its addend): the
  * branch outputs (out_cmp, out_slide, out_sel) are bf16 instead of the
  * accumulator dtype -- bf16 tensor-core path only (the NSA step uses it: the
  * branch outputs are intermediates of the bf16 combined output). */
@@ -155,9 +156,10 @@ int fsa_sel_bwd(const fsa_shape* s, int dtype, const void* Q, const void* K, con
 int fsa_dq_reduce(const fsa_shape* s, int dtype, const int32_t* idx, const void* dq_buf,
                   int dqbuf_dtype, void* dQ, void* stream);
 
-/* fsa_dq_reduce plus addend [N][h][d_K] (acc dtype) added to every row in the
- * same pass: dQ = (ascending-block sum of the dq partials) + addend.  bf16
- * tensor-core configuration only (the NSA step: selected + sliding dQ). */
+/* fsa_dq_reduce plus addend [N][h][d_K] (acc dtype; bf16 with dtype |
+ * FSA_OUT_NARROW) added to every row in the same pass: dQ = (ascending-block sum
+ * of the dq partials) + addend.  bf16 tensor-core configuration only (the NSA
+ * step: selected + sliding dQ). */
 int fsa_dq_reduce_add(const fsa_shape* s, int dtype, const int32_t* idx, const void* dq_buf,
                       int dqbuf_dtype, const void* addend, void* dQ, void* stream);
 
@@ -181,7 +183,8 @@ int fsa_slide_fwd(const fsa_shape* s, int dtype, const void* Q, const void* K, c
  * window of tokens and needs fsa_slide_bwd_workspace_bytes of workspace (the
  * per-window-slot dQ partials); accumulate != 0 adds into dQ/dK/dV (sums the
  * sliding branch onto the selected branch's gradients) -- tensor-core path only.
- * accumulate == 2 adds into dK/dV but WRITES dQ (for fsa_dq_reduce_add). */
+ * accumulate == 2 adds into dK/dV but WRITES dQ (for fsa_dq_reduce_add);
+ * accumulate == 3 likewise, with dQ written as bf16 (the NSA step's hand-off). */
 size_t fsa_slide_bwd_workspace_bytes(const fsa_shape* s, int dtype);
 int fsa_slide_bwd(const fsa_shape* s, int dtype, const void* Q, const void* K, const void* V,
                   const void* dOut, const void* lse, const void* delta, void* dQ, void* dK,

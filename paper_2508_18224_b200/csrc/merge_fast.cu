@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(256) merge_bf16_kernel(
 __global__ void dq_reduce_bf16_kernel(const int32_t* __restrict__ idx,
                                       const __nv_bfloat16* __restrict__ dq, float* __restrict__ dQ,
                                       int64_t N, int64_t h, int64_t g, int T,
-                                      const float* __restrict__ addend) {
+                                      const void* __restrict__ addend, int addend_bf16) {
   const int lane = threadIdx.x & 31;
   const int64_t wid = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (wid >= h * N) return;
@@ -152,7 +152,9 @@ __global__ void dq_reduce_bf16_kernel(const int32_t* __restrict__ idx,
     acc.x += a.x; acc.y += a.y; acc.z += a.z; acc.w += a.w;
   }
   if (addend) {  // another branch's dQ rows (the sliding window), added once
-    const float4 a = __ldcs(reinterpret_cast<const float4*>(addend + (t * h + j) * kD + lane * 4));
+    const int64_t e = (t * h + j) * kD + lane * 4;
+    const float4 a = addend_bf16 ? ld_bf16x4(reinterpret_cast<const __nv_bfloat16*>(addend) + e)
+                                 : __ldcs(reinterpret_cast<const float4*>(addend) + e / 4);
     acc.x += a.x; acc.y += a.y; acc.z += a.z; acc.w += a.w;
   }
   *reinterpret_cast<float4*>(dQ + (t * h + j) * kD + lane * 4) = acc;
@@ -191,12 +193,12 @@ int merge_combine_bf16_fast(const fsa_shape* s, const int32_t* idx, const void* 
 }
 
 int dq_reduce_bf16_fast(const fsa_shape* s, const int32_t* idx, const void* dq, void* dQ,
-                        cudaStream_t st, const void* addend) {
+                        cudaStream_t st, const void* addend, int addend_bf16) {
   const int64_t rows = s->h * s->N;
   if (rows == 0) return FSA_OK;
   dq_reduce_bf16_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(
-      idx, (const __nv_bfloat16*)dq, (float*)dQ, s->N, s->h, s->h / s->h_K, (int)s->T,
-      (const float*)addend);
+      idx, (const __nv_bfloat16*)dq, (float*)dQ, s->N, s->h, s->h / s->h_K, (int)s->T, addend,
+      addend_bf16);
   FSA_LAUNCH_CHECK("dq_reduce_bf16");
   return FSA_OK;
 }

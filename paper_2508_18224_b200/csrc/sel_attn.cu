@@ -476,8 +476,10 @@ extern "C" int fsa_sel_bwd(const fsa_shape* s, int dtype, const void* Q, const v
 extern "C" int fsa_dq_reduce_add(const fsa_shape* s, int dtype, const int32_t* idx,
                                  const void* dq_buf, int dqbuf_dtype, const void* addend, void* dQ,
                                  void* stream) {
+  const int narrow = (dtype & FSA_OUT_NARROW) != 0;  // the addend is bf16
+  dtype &= ~FSA_OUT_NARROW;
   if (dtype == FSA_DT_BF16 && dqbuf_dtype == FSA_DT_BF16 && fsa::fast_reduce_ok(*s))
-    return fsa::dq_reduce_bf16_fast(s, idx, dq_buf, dQ, (cudaStream_t)stream, addend);
+    return fsa::dq_reduce_bf16_fast(s, idx, dq_buf, dQ, (cudaStream_t)stream, addend, narrow);
   fsa::set_error("dq_reduce_add: only the bf16 tensor-core configuration (d = 128, T <= 32)");
   return FSA_ERR_UNSUPPORTED;
 }

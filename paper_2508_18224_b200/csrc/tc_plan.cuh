@@ -33,7 +33,8 @@ int tc_slide_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V
 
 // query-outer sliding-window dQ (tc_slide_dq.cu); accumulate: dQ += (fp32)
 int tc_slide_dq(const fsa_shape* s, const void* Q, const void* K, const void* V, const void* dOut,
-                const void* lse, const void* delta, void* dQ, int accumulate, cudaStream_t st);
+                const void* lse, const void* delta, void* dQ, int accumulate, cudaStream_t st,
+                int out_bf16 = 0);
 
 // compressed-branch backward on the same kernels (tc_sel_bwd.cu, tc_slide_dq.cu):
 // dK_cmp / dV_cmp partial slabs per token chunk, and dQ += over the pooled rows
@@ -53,7 +54,7 @@ int merge_combine_bf16_fast(const fsa_shape* s, const int32_t* idx, const void* 
                             const void* tau, void* out_sel, void* lse, void* out, cudaStream_t st,
                             int narrow = 0);
 int dq_reduce_bf16_fast(const fsa_shape* s, const int32_t* idx, const void* dq, void* dQ,
-                        cudaStream_t st, const void* addend = nullptr);
+                        cudaStream_t st, const void* addend = nullptr, int addend_bf16 = 0);
 
 int num_sms();
 

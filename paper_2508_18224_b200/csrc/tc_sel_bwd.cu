@@ -769,7 +769,8 @@ int tc_slide_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V
   if (rc) return rc;
   rc = launch_bwd(p, st);
   if (rc) return rc;
-  return tc_slide_dq(s, Q, K, V, dOut, lse, delta, dQ, accumulate == 1, st);  // mode 2: dQ written
+  // mode 1: dQ +=; mode 2: dQ written (fp32); mode 3: dQ written as bf16
+  return tc_slide_dq(s, Q, K, V, dOut, lse, delta, dQ, accumulate == 1, st, accumulate == 3);
 }
 
 // Compressed-branch dK_cmp / dV_cmp: the same kernel with

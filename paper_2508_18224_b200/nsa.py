@@ -211,14 +211,18 @@ def _sel_slide_backward(ctx: NSAContext, d_sel, d_slide, delta_sel, delta_slide,
               _lib.ptr(ctx.v), _lib.ptr(d_sel), _lib.ptr(lse_sel), _lib.ptr(delta_sel),
               _lib.ptr(inv.offsets), _lib.ptr(inv.qlist), _lib.ptr(inv.work), _lib.ptr(dq_buf),
               dq_code, _lib.ptr(dK), _lib.ptr(dV), st)
-    dQ_slide = torch.empty((cfg.N, cfg.h, cfg.d_K), dtype=acc, device=dev)
+    # the sliding dQ rows are handed to the reduce in bf16 with the narrow
+    # branch outputs (mode 3), else fp32 (mode 2)
+    dQ_slide = torch.empty((cfg.N, cfg.h, cfg.d_K), dtype=torch.bfloat16 if ctx.narrow else acc,
+                           device=dev)
     nws = _lib.lib().fsa_slide_bwd_workspace_bytes(ctypes.byref(s), _lib.dt_code(dt))
     ws = torch.empty(max(nws, 1), dtype=torch.uint8, device=dev)
     _lib.call("fsa_slide_bwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(ctx.q), _lib.ptr(ctx.k),
               _lib.ptr(ctx.v), _lib.ptr(d_slide), _lib.ptr(lse_slide), _lib.ptr(delta_slide),
-              _lib.ptr(dQ_slide), _lib.ptr(dK), _lib.ptr(dV), _lib.ptr(ws), 2, st)
+              _lib.ptr(dQ_slide), _lib.ptr(dK), _lib.ptr(dV), _lib.ptr(ws), 3 if ctx.narrow else 2, st)
     dQ = torch.empty((cfg.N, cfg.h, cfg.d_K), dtype=acc, device=dev)
-    _lib.call("fsa_dq_reduce_add", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(ctx.sel.idx),
+    _lib.call("fsa_dq_reduce_add", ctypes.byref(s),
+              _lib.dt_code(dt) | (_lib.OUT_NARROW if ctx.narrow else 0), _lib.ptr(ctx.sel.idx),
               _lib.ptr(dq_buf), dq_code, _lib.ptr(dQ_slide), _lib.ptr(dQ), st)
     return dQ, dK, dV
 
