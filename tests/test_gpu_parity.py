@@ -650,3 +650,20 @@ def test_selection_vs_oracle_fp64_scores_near_ties():
         err = np.abs(s_gpu[kh, t, :own] - s64[kh, t, :own]).max()
         diff = np.setxor1d(got[kh, t][got[kh, t] >= 0], want[kh, t][want[kh, t] >= 0])
         assert np.all(np.abs(s64[kh, t, diff] - s_T) <= 2 * err + 1e-12), (kh, t, diff)
+
+
+def test_narrow_flag_rejected_off_the_tensor_core_path():
+    """FSA_OUT_NARROW (bf16 branch outputs) exists only on the bf16 tensor-core
+    path: the generic f32 path refuses it with the library's error."""
+    import ctypes
+
+    from paper_2508_18224_b200 import _lib
+    cfg = fsa.make_config(N=256, d_K=32, d_V=32, h=4, h_K=2, B_K=16, T=4, W=32)
+    s = _lib.shape_of(cfg)
+    q = torch.zeros(cfg.N, cfg.h, 32, device="cuda")
+    k = torch.zeros(cfg.N, cfg.h_K, 32, device="cuda")
+    out = torch.empty(cfg.N, cfg.h, 32, device="cuda")
+    lse = torch.empty(cfg.h, cfg.N, device="cuda")
+    rc = _lib.lib().fsa_slide_fwd(ctypes.byref(s), _lib.DT_F32 | _lib.OUT_NARROW, _lib.ptr(q),
+                                  _lib.ptr(k), _lib.ptr(k), _lib.ptr(out), _lib.ptr(lse), None)
+    assert rc != 0 and b"narrow" in _lib.lib().fsa_last_error()
