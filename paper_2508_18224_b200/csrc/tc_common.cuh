@@ -170,6 +170,22 @@ __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// L2 policy for streamed-out data (the 4.2 GB partial buffers): evict first,
+// so the stores do not push the gathered Q / dO rows out of L2
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+// tile::scatter4 with an L2 cache-policy hint
+__device__ __forceinline__ void tma_scatter4_hint(const void* map, int col, const int32_t* r,
+                                                  uint32_t src, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.tile::scatter4.bulk_group.L2::cache_hint"
+      " [%0, {%1, %2, %3, %4, %5}], [%6], %7;" ::"l"(map),
+      "r"(col), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(src), "l"(pol)
+      : "memory");
+}
 // the reverse: 4 x 128 B from src (SW128 rows) to rows r[0..3] (bulk group);
 // rows outside the map are dropped
 __device__ __forceinline__ void tma_scatter4(const void* map, int col, const int32_t* r, uint32_t src) {

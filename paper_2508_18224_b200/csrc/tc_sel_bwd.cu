@@ -655,8 +655,9 @@ __global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const _
             rows[i] = d >= 0 ? (int32_t)d : INT32_MAX;  // out of the map: dropped
           }
           if (lane < 16) {
-            tma_scatter4(&p.tmDQ, hf * 64, rows,
-                         smem_u32(hf ? drw : prow) + (uint32_t)(32 * (warp & 3) + 4 * grp) * 128u);
+            tma_scatter4_hint(&p.tmDQ, hf * 64, rows,
+                              smem_u32(hf ? drw : prow) + (uint32_t)(32 * (warp & 3) + 4 * grp) * 128u,
+                              l2_evict_first());
             bulk_commit();
           }
         }

@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
         fence_proxy_async();
         __syncwarp();
         if (lane < 8) {
-          tma_scatter4(&p.tmO, hf * 64, rows, smem_u32(st) + (uint32_t)lane * 512u);
+          tma_scatter4_hint(&p.tmO, hf * 64, rows, smem_u32(st) + (uint32_t)lane * 512u, l2_evict_first());
           bulk_commit();
         }
       }
