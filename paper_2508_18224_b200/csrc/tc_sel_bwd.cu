@@ -52,7 +52,9 @@ constexpr uint32_t kOffBar = kOffDS + 32768;
 enum {
   // smem stages (Q/dO, P/dS) by item parity; TMEM stages (S|dP, then dQ) by item mod 3
   B_QDF = 0, B_QDE = 2, B_KVF = 4, B_KVE = 5, B_SDF = 6, B_SDE = 9, B_PDF = 12, B_DQF = 14,
-  B_KAF = 17, B_KAE = 18, B_RF = 19, B_RE = 23, kNumBars = 27
+  B_KAF = 17, B_KAE = 18, B_RF = 19, B_RE = 23,
+  B_DE = 27,  // selected mode: dO stage free (after the dV product), ahead of Q (QDE)
+  kNumBars = 29
 };
 constexpr uint32_t kOffRing = kOffBar + kNumBars * 8;
 constexpr uint32_t kOffTmem = kOffRing + 16;
@@ -168,6 +170,7 @@ __global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const _
     for (int s = 0; s < 2; ++s) {
       mbar_init(bar(B_QDF + s), kLoaders);
       mbar_init(bar(B_QDE + s), 1);
+      mbar_init(bar(B_DE + s), 1);
       mbar_init(bar(B_PDF + s), 128);
     }
     for (int s = 0; s < kTStages; ++s) {
@@ -284,18 +287,24 @@ __global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const _
         const int32_t ent = ent_next;
         ent_next = kt < p.tpi ? entry_at<SL>(p, tr, pos + p.tpi) : 0;
         const uint32_t par = (uint32_t)(((n >> 1) & 1) ^ 1);
-        if (!mbar_test(bar(B_QDE + s), par)) {
-          publish();
-          mbar_spin(bar(B_QDE + s), par);
-        }
         int64_t row = 0;
         if (ok) {
           int64_t t, slot;
           token_of<SL>(p, tr, pos, ent, t, slot);
           row = t * p.h + tr.kh * p.g + hh;
         }
-        warp_gather_rows32(sb + kOffQ + s * kTile, 16384u, lr & ~31, p.Q + row * kD, ok, lane);
+        // the dO half of the stage frees first (after the dV product): gather it
+        // while the dK / dQ products still read Q
+        if (!mbar_test(bar(B_DE + s), par)) {
+          publish();
+          mbar_spin(bar(B_DE + s), par);
+        }
         warp_gather_rows32(sb + kOffDO + s * kTile, 16384u, lr & ~31, p.dO + row * kD, ok, lane);
+        if (!mbar_test(bar(B_QDE + s), par)) {
+          publish();
+          mbar_spin(bar(B_QDE + s), par);
+        }
+        warp_gather_rows32(sb + kOffQ + s * kTile, 16384u, lr & ~31, p.Q + row * kD, ok, lane);
         asm volatile("cp.async.commit_group;" ::: "memory");
         // everything but this gather has landed: publish the previous one
         asm volatile("cp.async.wait_group 1;" ::: "memory");
@@ -411,6 +420,7 @@ __global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const _
               for (int k = 0; k < 8; ++k)
                 mma_bf16(tV, desc_mnmajor(o + k * 2048u, 16384u), desc_mnmajor(pp + k * 2048u, 8192u),
                          kIdKV, (first && k == 0) ? 0u : 1u);
+              if constexpr (SL == 0) mma_commit(bar(B_DE + s));  // dO read: its half of the stage is free
 #pragma unroll
               for (int k = 0; k < 8; ++k)
                 mma_bf16(tK, desc_mnmajor(q + k * 2048u, 16384u), desc_mnmajor(ds + k * 2048u, 8192u),
