@@ -228,6 +228,14 @@ int fsa_cmp_bwd(const fsa_shape* s, int dtype, const void* Q, const void* K_cmp,
                 const void* dOut, const void* lse, const void* delta, void* dQ, void* dK, void* dV,
                 void* workspace, void* stream);
 
+/* fsa_cmp_bwd with the gate folded in (after fsa_gate_backward_full_fold): dOut
+ * is the raw cotangent, lse_adj = lse_cmp - ln tau[t, 0], delta = sum out_cmp *
+ * dOut, and tau (N, 3) gates the pending tokens' prefix-mean gradients.  bf16
+ * tensor-core configuration only. */
+int fsa_cmp_bwd_fold(const fsa_shape* s, int dtype, const void* Q, const void* K_cmp,
+                     const void* V_cmp, const void* dOut, const void* tau, const void* lse_adj,
+                     const void* delta, void* dQ, void* dK, void* dV, void* workspace, void* stream);
+
 /* Gate backward for all three branches (branches.py:95-104): d_c = tau[t][c]
  * dOut (dtype), delta_c [h][N] = sum_v out_c * d_c, and the gate gradient
  * dtau [N][3] = sum_{v,j} out_c * dOut (acc dtype).  One pass over dOut. */
@@ -235,6 +243,17 @@ int fsa_gate_backward_full(const fsa_shape* s, int dtype, const void* dOut, cons
                            const void* out_cmp, const void* out_sel, const void* out_slide,
                            void* d_cmp, void* d_sel, void* d_slide, void* delta_cmp,
                            void* delta_sel, void* delta_slide, void* dtau, void* stream);
+
+/* fsa_gate_backward_full folded into the branch statistics (the tensor-core NSA
+ * step with full=True): delta_c = sum_v out_c * dOut, lse_c_adj = lse_c - ln
+ * tau_c[t] for c = compressed, selected, sliding ([h][N], acc), and dtau (N, 3);
+ * the branch backward kernels then take the raw dOut (no gated copies). */
+int fsa_gate_backward_full_fold(const fsa_shape* s, int dtype, const void* dOut, const void* tau,
+                                const void* out_cmp, const void* out_sel, const void* out_slide,
+                                const void* lse_cmp, const void* lse_sel, const void* lse_slide,
+                                void* delta_cmp, void* delta_sel, void* delta_slide,
+                                void* lse_cmp_adj, void* lse_sel_adj, void* lse_slide_adj,
+                                void* dtau, void* stream);
 
 /* NSA query-major selected forward (query_major.py:45-69, _core.pyx:134-181):
  * one task per (kv head, token) over its selected blocks in ascending order,

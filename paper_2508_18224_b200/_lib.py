@@ -68,6 +68,8 @@ SIGNATURES = {
     "fsa_gate_scale": ([_sp, _i, _vp, _vp, _i, _vp, _vp], _i),
     "fsa_gate_backward": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "fsa_gate_backward_fold": ([_sp, _i] + [_vp] * 10 + [_vp], _i),
+    "fsa_gate_backward_full_fold": ([_sp, _i] + [_vp] * 15 + [_vp], _i),
+    "fsa_cmp_bwd_fold": ([_sp, _i] + [_vp] * 11 + [_vp], _i),
     "fsa_cmp_bwd_workspace_bytes": ([_sp, _i], _sz),
     "fsa_cmp_bwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "fsa_gate_backward_full": ([_sp, _i] + [_vp] * 13, _i),

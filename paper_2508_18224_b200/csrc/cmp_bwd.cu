@@ -117,7 +117,9 @@ template <typename T>
 __global__ void cmp_pool_bwd(const typename Acc<T>::type* __restrict__ dKc,
                              const typename Acc<T>::type* __restrict__ dVc,
                              const T* __restrict__ dOut, typename Acc<T>::type* __restrict__ dK,
-                             typename Acc<T>::type* __restrict__ dV, fsa_shape s) {
+                             typename Acc<T>::type* __restrict__ dV, fsa_shape s,
+                             const typename Acc<T>::type* __restrict__ tau = nullptr) {
+  // tau != null: dOut is the raw cotangent and the gate (tau[t, 0]) applies here
   using A = typename Acc<T>::type;
   const int lane = threadIdx.x & 31;
   const int64_t wid = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -132,6 +134,7 @@ __global__ void cmp_pool_bwd(const typename Acc<T>::type* __restrict__ dKc,
     for (int64_t t = sk; t < n_pref; ++t) {
       A sum = 0;
       for (int64_t hh = 0; hh < g; ++hh) sum += to_acc(dOut[(t * s.h + kh * g + hh) * s.d_V + c]);
+      if (tau) sum *= tau[t * 3];
       acc += sum / A(t + 1);
     }
     dV[(sk * s.h_K + kh) * s.d_V + c] += acc;
@@ -246,6 +249,7 @@ CmpWs cmp_ws(const fsa_shape& s, void* base) {
 }
 
 int cmp_bwd_tc(const fsa_shape* s, const void* Q, const void* Kc, const void* Vc, const void* dOut,
+               const void* tau,
                const void* lse, const void* delta, void* dQ, void* dK, void* dV, void* ws,
                cudaStream_t st) {
   const CmpWs w = cmp_ws(*s, ws);
@@ -263,7 +267,7 @@ int cmp_bwd_tc(const fsa_shape* s, const void* Q, const void* Kc, const void* Vc
   const int64_t pr = s->N * s->h_K;
   if (pr > 0)
     cmp_pool_bwd<__nv_bfloat16><<<(unsigned)((pr + 7) / 8), 256, 0, st>>>(
-        w.dKc, w.dVc, (const __nv_bfloat16*)dOut, (float*)dK, (float*)dV, *s);
+        w.dKc, w.dVc, (const __nv_bfloat16*)dOut, (float*)dK, (float*)dV, *s, (const float*)tau);
   FSA_LAUNCH_CHECK("cmp_pool_bwd");
   return FSA_OK;
 }
@@ -274,7 +278,7 @@ int cmp_bwd_impl(const fsa_shape* s, const void* Q, const void* Kc, const void* 
                  cudaStream_t st) {
   using A = typename Acc<T>::type;
   if (sizeof(T) == 2 && tc_cmp_bwd_ok(*s))
-    return cmp_bwd_tc(s, Q, Kc, Vc, dOut, lse, delta, dQ, dK, dV, ws, st);
+    return cmp_bwd_tc(s, Q, Kc, Vc, dOut, nullptr, lse, delta, dQ, dK, dV, ws, st);
   const int64_t b = s->N / s->B_K;
   A* dKc = (A*)ws;
   A* dVc = dKc + b * s->h_K * s->d_K;
@@ -292,6 +296,86 @@ int cmp_bwd_impl(const fsa_shape* s, const void* Q, const void* Kc, const void* 
   cmp_pool_bwd<T><<<(unsigned)((pr + 7) / 8), 256, 0, st>>>(dKc, dVc, (const T*)dOut, (A*)dK,
                                                            (A*)dV, *s);
   FSA_LAUNCH_CHECK("cmp_bwd");
+  return FSA_OK;
+}
+
+// The full gate backward folded into the three branches' statistics (the
+// tensor-core NSA step with full=True): delta_c = sum_v out_c * dOut, lse_c_adj
+// = lse_c - ln tau_c[t] -- the branch kernels then take the raw dOut -- and
+// dtau[t, c] = sum_{j,v} out_c * dOut.  Warp per token (deterministic dtau).
+template <typename T, typename B>
+__global__ void gate_fold3_kernel(const T* __restrict__ dOut, const typename Acc<T>::type* __restrict__ tau,
+                                  const B* __restrict__ o0, const B* __restrict__ o1,
+                                  const B* __restrict__ o2, const typename Acc<T>::type* __restrict__ l0,
+                                  const typename Acc<T>::type* __restrict__ l1,
+                                  const typename Acc<T>::type* __restrict__ l2,
+                                  typename Acc<T>::type* __restrict__ del0,
+                                  typename Acc<T>::type* __restrict__ del1,
+                                  typename Acc<T>::type* __restrict__ del2,
+                                  typename Acc<T>::type* __restrict__ la0,
+                                  typename Acc<T>::type* __restrict__ la1,
+                                  typename Acc<T>::type* __restrict__ la2,
+                                  typename Acc<T>::type* __restrict__ dtau, int64_t N, int64_t h,
+                                  int64_t dv) {
+  using A = typename Acc<T>::type;
+  const int lane = threadIdx.x & 31;
+  const int64_t t = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= N) return;
+  const A w0 = tau[t * 3], w1 = tau[t * 3 + 1], w2 = tau[t * 3 + 2];
+  const A lw0 = log_acc(w0), lw1 = log_acc(w1), lw2 = log_acc(w2);
+  A g0 = 0, g1 = 0, g2 = 0;
+  for (int64_t j = 0; j < h; ++j) {
+    const int64_t base = (t * h + j) * dv;
+    A s0 = 0, s1 = 0, s2 = 0;
+    for (int64_t c = lane; c < dv; c += 32) {
+      const A x = to_acc(dOut[base + c]);
+      s0 += A(to_acc(o0[base + c])) * x;
+      s1 += A(to_acc(o1[base + c])) * x;
+      s2 += A(to_acc(o2[base + c])) * x;
+    }
+    s0 = warp_sum(s0);
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    g0 += s0;
+    g1 += s1;
+    g2 += s2;
+    if (lane == 0) {
+      const int64_t r = j * N + t;
+      del0[r] = s0;
+      del1[r] = s1;
+      del2[r] = s2;
+      la0[r] = l0[r] - lw0;  // tau = 0: +inf, the branch's P = 0
+      la1[r] = l1[r] - lw1;
+      la2[r] = l2[r] - lw2;
+    }
+  }
+  if (lane == 0) {
+    dtau[t * 3] = g0;
+    dtau[t * 3 + 1] = g1;
+    dtau[t * 3 + 2] = g2;
+  }
+}
+
+template <typename T>
+int gate_fold3_impl(const fsa_shape* s, const void* dOut, const void* tau, const void* o0,
+                    const void* o1, const void* o2, const void* l0, const void* l1, const void* l2,
+                    void* del0, void* del1, void* del2, void* la0, void* la1, void* la2, void* dtau,
+                    cudaStream_t st, int narrow) {
+  using A = typename Acc<T>::type;
+  if (s->N == 0) return FSA_OK;
+  FSA_REQUIRE(!narrow || sizeof(T) == 2, "gate_backward_full_fold: narrow outputs need bf16");
+  const unsigned grid = (unsigned)((s->N + 7) / 8);
+  if (narrow)
+    gate_fold3_kernel<T, __nv_bfloat16><<<grid, 256, 0, st>>>(
+        (const T*)dOut, (const A*)tau, (const __nv_bfloat16*)o0, (const __nv_bfloat16*)o1,
+        (const __nv_bfloat16*)o2, (const A*)l0, (const A*)l1, (const A*)l2, (A*)del0, (A*)del1,
+        (A*)del2, (A*)la0, (A*)la1, (A*)la2, (A*)dtau, s->N, s->h, s->d_V);
+  else
+    gate_fold3_kernel<T, A><<<grid, 256, 0, st>>>(
+        (const T*)dOut, (const A*)tau, (const A*)o0, (const A*)o1, (const A*)o2, (const A*)l0,
+        (const A*)l1, (const A*)l2, (A*)del0, (A*)del1, (A*)del2, (A*)la0, (A*)la1, (A*)la2,
+        (A*)dtau, s->N, s->h, s->d_V);
+  FSA_LAUNCH_CHECK("gate_backward_full_fold");
   return FSA_OK;
 }
 
@@ -340,6 +424,17 @@ extern "C" int fsa_cmp_bwd(const fsa_shape* s, int dtype, const void* Q, const v
               (cudaStream_t)stream);
 }
 
+extern "C" int fsa_cmp_bwd_fold(const fsa_shape* s, int dtype, const void* Q, const void* K_cmp,
+                                const void* V_cmp, const void* dOut, const void* tau,
+                                const void* lse_adj, const void* delta, void* dQ, void* dK, void* dV,
+                                void* workspace, void* stream) {
+  FSA_REQUIRE(workspace != nullptr, "cmp_bwd: workspace required");
+  FSA_REQUIRE(dtype == FSA_DT_BF16 && fsa::tc_cmp_bwd_ok(*s),
+              "cmp_bwd_fold: the bf16 tensor-core configuration only");
+  return fsa::cmp_bwd_tc(s, Q, K_cmp, V_cmp, dOut, tau, lse_adj, delta, dQ, dK, dV, workspace,
+                         (cudaStream_t)stream);
+}
+
 extern "C" int fsa_gate_backward_full(const fsa_shape* s, int dtype, const void* dOut,
                                       const void* tau, const void* out_cmp, const void* out_sel,
                                       const void* out_slide, void* d_cmp, void* d_sel,
@@ -349,4 +444,18 @@ extern "C" int fsa_gate_backward_full(const fsa_shape* s, int dtype, const void*
   dtype &= ~FSA_OUT_NARROW;
   DISPATCH_DT(dtype, gate_bwd_full_impl, s, dOut, tau, out_cmp, out_sel, out_slide, d_cmp, d_sel,
               d_slide, delta_cmp, delta_sel, delta_slide, dtau, (cudaStream_t)stream, narrow);
+}
+
+extern "C" int fsa_gate_backward_full_fold(const fsa_shape* s, int dtype, const void* dOut,
+                                           const void* tau, const void* out_cmp, const void* out_sel,
+                                           const void* out_slide, const void* lse_cmp,
+                                           const void* lse_sel, const void* lse_slide,
+                                           void* delta_cmp, void* delta_sel, void* delta_slide,
+                                           void* lse_cmp_adj, void* lse_sel_adj, void* lse_slide_adj,
+                                           void* dtau, void* stream) {
+  const int narrow = (dtype & FSA_OUT_NARROW) != 0;
+  dtype &= ~FSA_OUT_NARROW;
+  DISPATCH_DT(dtype, gate_fold3_impl, s, dOut, tau, out_cmp, out_sel, out_slide, lse_cmp, lse_sel,
+              lse_slide, delta_cmp, delta_sel, delta_slide, lse_cmp_adj, lse_sel_adj, lse_slide_adj,
+              dtau, (cudaStream_t)stream, narrow);
 }

@@ -144,6 +144,27 @@ def nsa_backward(ctx: NSAContext, dout, *, full: bool = False):
     acc = _lib.acc_dtype(dt)
     delta_sel = torch.empty((cfg.h, cfg.N), dtype=acc, device=dout.device)
     delta_slide = torch.empty_like(delta_sel)
+    _, (dq_code, _) = _lib.buffer_dtypes(cfg, dt)
+    if full and dq_code == _lib.DT_BF16:
+        # tensor-core path: the gate folds into all three branches' statistics
+        delta_cmp = torch.empty_like(delta_sel)
+        lse_cmp, lse_sel, lse_slide = (torch.empty_like(delta_sel) for _ in range(3))
+        dtau = torch.empty((cfg.N, 3), dtype=acc, device=dout.device)
+        nflag = _lib.OUT_NARROW if ctx.narrow else 0
+        _lib.call("fsa_gate_backward_full_fold", ctypes.byref(s), _lib.dt_code(dt) | nflag,
+                  _lib.ptr(dout), _lib.ptr(ctx.tau), _lib.ptr(ctx.out_cmp), _lib.ptr(ctx.out_sel),
+                  _lib.ptr(ctx.out_slide), _lib.ptr(ctx.lse_cmp), _lib.ptr(ctx.lse_sel),
+                  _lib.ptr(ctx.lse_slide), _lib.ptr(delta_cmp), _lib.ptr(delta_sel),
+                  _lib.ptr(delta_slide), _lib.ptr(lse_cmp), _lib.ptr(lse_sel), _lib.ptr(lse_slide),
+                  _lib.ptr(dtau), st)
+        dQ, dK, dV = _sel_slide_backward(ctx, dout, dout, delta_sel, delta_slide, lse_sel, lse_slide)
+        nws = _lib.lib().fsa_cmp_bwd_workspace_bytes(ctypes.byref(s), _lib.dt_code(dt))
+        ws = torch.empty(nws, dtype=torch.uint8, device=dout.device)
+        _lib.call("fsa_cmp_bwd_fold", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(ctx.q),
+                  _lib.ptr(ctx.k_cmp), _lib.ptr(ctx.v_cmp), _lib.ptr(dout), _lib.ptr(ctx.tau),
+                  _lib.ptr(lse_cmp), _lib.ptr(delta_cmp), _lib.ptr(dQ), _lib.ptr(dK), _lib.ptr(dV),
+                  _lib.ptr(ws), st)
+        return dQ, dK, dV, dtau
     if full:
         d_sel, d_slide = torch.empty_like(dout), torch.empty_like(dout)
         d_cmp = torch.empty_like(dout)
@@ -161,7 +182,6 @@ def nsa_backward(ctx: NSAContext, dout, *, full: bool = False):
                   _lib.ptr(ctx.k_cmp), _lib.ptr(ctx.v_cmp), _lib.ptr(d_cmp), _lib.ptr(ctx.lse_cmp),
                   _lib.ptr(delta_cmp), _lib.ptr(dQ), _lib.ptr(dK), _lib.ptr(dV), _lib.ptr(ws), st)
         return dQ, dK, dV, dtau
-    _, (dq_code, _) = _lib.buffer_dtypes(cfg, dt)
     if dq_code == _lib.DT_BF16:
         # tensor-core path: the gate folds into the branch statistics (raw
         # dOut, lse - ln tau, delta = sum out * dOut) -- no gated dOut copies
