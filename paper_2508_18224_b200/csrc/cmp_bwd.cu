@@ -327,11 +327,40 @@ __global__ void gate_fold3_kernel(const T* __restrict__ dOut, const typename Acc
   for (int64_t j = 0; j < h; ++j) {
     const int64_t base = (t * h + j) * dv;
     A s0 = 0, s1 = 0, s2 = 0;
-    for (int64_t c = lane; c < dv; c += 32) {
-      const A x = to_acc(dOut[base + c]);
-      s0 += A(to_acc(o0[base + c])) * x;
-      s1 += A(to_acc(o1[base + c])) * x;
-      s2 += A(to_acc(o2[base + c])) * x;
+    if constexpr (sizeof(T) == 2 && sizeof(B) == 2) {
+      if (dv == 128) {  // 4 features per lane: 8-byte loads of dOut and the three outputs
+        const int64_t e = base + lane * 4;
+        const uint2 ux = *reinterpret_cast<const uint2*>(dOut + e);
+        const uint2 u0 = *reinterpret_cast<const uint2*>(o0 + e);
+        const uint2 u1 = *reinterpret_cast<const uint2*>(o1 + e);
+        const uint2 u2 = *reinterpret_cast<const uint2*>(o2 + e);
+        const __nv_bfloat162* px = reinterpret_cast<const __nv_bfloat162*>(&ux);
+        const __nv_bfloat162* p0 = reinterpret_cast<const __nv_bfloat162*>(&u0);
+        const __nv_bfloat162* p1 = reinterpret_cast<const __nv_bfloat162*>(&u1);
+        const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&u2);
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const float2 x = __bfloat1622float2(px[k]), a = __bfloat1622float2(p0[k]),
+                       b = __bfloat1622float2(p1[k]), c2 = __bfloat1622float2(p2[k]);
+          s0 += a.x * x.x + a.y * x.y;
+          s1 += b.x * x.x + b.y * x.y;
+          s2 += c2.x * x.x + c2.y * x.y;
+        }
+      } else {
+        for (int64_t c = lane; c < dv; c += 32) {
+          const A x = to_acc(dOut[base + c]);
+          s0 += A(to_acc(o0[base + c])) * x;
+          s1 += A(to_acc(o1[base + c])) * x;
+          s2 += A(to_acc(o2[base + c])) * x;
+        }
+      }
+    } else {
+      for (int64_t c = lane; c < dv; c += 32) {
+        const A x = to_acc(dOut[base + c]);
+        s0 += A(to_acc(o0[base + c])) * x;
+        s1 += A(to_acc(o1[base + c])) * x;
+        s2 += A(to_acc(o2[base + c])) * x;
+      }
     }
     s0 = warp_sum(s0);
     s1 = warp_sum(s1);
