@@ -323,38 +323,15 @@ __global__ void __launch_bounds__(256) topk_stream4_kernel(const float* __restri
     total = __shfl_sync(0xffffffffu, incl, 31);
     return incl - v;
   };
-  int nsel_l = 0;
+  // (no separate "<= T selectable" pass: then theta = 1 and every selectable
+  // key is a candidate, which the rank path below returns in index order)
   float lmf = -INFINITY;
 #pragma unroll 2
   for (int base = 0; base < ncand; base += 128) {
     float v4[4];
     vals4(base, v4);
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      nsel_l += v4[e] > -INFINITY;
-      lmf = fmaxf(lmf, v4[e]);
-    }
-  }
-  int nsel = nsel_l;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) nsel += __shfl_xor_sync(0xffffffffu, nsel, o);
-  if (nsel <= T) {
-    int out = 0;
-    for (int base = 0; base < ncand; base += 128) {
-      float v4[4];
-      vals4(base, v4);
-      int cnt = 0;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) cnt += v4[e] > -INFINITY;
-      int tot;
-      int pos = out + excl_scan(cnt, tot);
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (v4[e] > -INFINITY) dst[pos++] = base + 4 * lane + e;
-      out += tot;
-    }
-    if (lane >= out && lane < T) dst[lane] = -1;
-    return;
+    for (int e = 0; e < 4; ++e) lmf = fmaxf(lmf, v4[e]);
   }
   // ---- theta: T-th largest lane maximum (warp bitonic, descending)
   uint32_t lm = score_key32(lmf);  // 0 for an all-unselectable lane
