@@ -54,7 +54,10 @@ class ClockSampler:
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index):
-        self.index = index
+        # nvidia-smi numbers the physical GPUs: map the CUDA device through
+        # CUDA_VISIBLE_DEVICES when it is set
+        vis = [x for x in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if x.strip()]
+        self.index = vis[index].strip() if index < len(vis) else index
         self.rows = []
         self.proc = None
 
