@@ -5,11 +5,13 @@
 // the slot-indexed partial buffer that the merge kernel (K6) combines.
 //
 // Persistent, warp-specialised, one CTA per SM:
-//   warps 0-3  softmax + epilogue, one TMEM lane (= MMA row) per thread
-//   warps 4-7  loaders: cp.async gather of an item's 128 query rows (TPI
+//   warps 0-7  two softmax + epilogue warpgroups ping-ponging over items, one
+//              TMEM lane (= MMA row) per thread; P goes back to TMEM (the PV A
+//              operand) and the partial rows leave by TMA tile::scatter4
+//   warps 8-11 loaders: cp.async gather of an item's 128 query rows (TPI
 //              tokens x g group heads); one item's gather stays in flight while
-//              the next is issued (3 Q stages); K_i/V_i per task (2 stages)
-//   warp  8    MMA issuer (one thread): S = Q K^T (M128 N64 K128) and
+//              the next is issued (4 Q stages); K_i/V_i per task (2 stages)
+//   warp  12   MMA issuer (one elected lane): S = Q K^T (M128 N64 K128) and
 //              O = P V (M128 N128 K64) into TMEM, tcgen05.commit -> mbarriers;
 //              S of item n+1 is issued before PV of item n
 // Tasks (kv head, block) are claimed dynamically in head-major order
