@@ -33,7 +33,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOAD = dict(name="llama3-8b-attn-32k", N=32768, d=128, h=32, h_K=8, B_K=64, T=16, W=512)
-CPU_SAMPLE_N = 8192
+CPU_SAMPLE_N = int(os.environ.get("FSA_BENCH_CPU_SAMPLE", 8192))  # smaller only in the CPU tests
 
 
 def _peaks():

@@ -130,3 +130,28 @@ def test_cli_bad_config_exits_2(tmp_path, capsys):
     assert cli.main(["bench", "--config", str(bad)]) == 2
     assert "N not divisible by B_K" in capsys.readouterr().err
     assert cli.BENCH_COLUMNS[:3] == ("engine", "phase", "backend")
+
+
+def test_bench_reference_arm_json_contract():
+    """bench.py --impl reference (the CPU oracle port) prints one JSON line with
+    the arm contract: impl, our arm's metric / unit / config, a cpu_baseline
+    describing the run and a zero-copy e2e."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FSA_BENCH_CPU_SAMPLE="2048")  # b = 32 >= T = 16
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference",
+                          "--steps", "1", "--warmup", "3"], capture_output=True, text=True,
+                         env=env, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    assert d["impl"] == "reference" and d["unit"] == "tokens/s" and d["value"] > 0
+    assert d["metric"].startswith("NSA fwd+bwd tokens/s") and d["higher_is_better"] is True
+    assert d["config"]["workload"] == "llama3-8b-attn-32k" and d["config"]["seq_len"] == 32768
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
+    assert d["e2e"] == {"value": d["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}
