@@ -43,7 +43,10 @@ def main():
             if i is None:
                 vals.append(f"{'-':>10}")
                 continue
-            v = float(r[i].replace(",", "")) if r[i] else 0.0
+            try:
+                v = float(r[i].replace(",", "")) if r[i] else 0.0
+            except ValueError:  # "no data" (metric not collected for this launch)
+                v = float("nan")
             u = units[i]
             if key.startswith("gpu__time"):
                 v *= {"ns": 1, "nsecond": 1, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6}.get(u, 1)
