@@ -4,18 +4,29 @@
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
         --master-port P bench.py --gpus N ...
 
-Workload (BASELINE.json configs[1]): Llama-3-8B attention shape, 32 q / 8 kv
-heads (GQA 4), d = 128, block 64, top-16, window 512, bf16, seq 32K, NSA
-forward + backward.  A step = compress -> compressed attention + scores ->
-top-k -> inverse index -> FSA selected forward -> sliding window -> gated
-combine, then the selected and sliding backward (the branches the reference
-differentiates).  Synthetic N(0,1) inputs, random-init -- no datasets.
-Scaling is weak: each rank runs its own sequence (batch sharding, no
-collective on the data path); value = all ranks' tokens / max-over-ranks time.
+Headline workload (BASELINE.json configs[4], the config the metric's
+"tokens/s at 1/2/4/8 GPU" is quoted on): Qwen3-14B attention shape, 40 q /
+8 kv heads (GQA 5), d = 128, block 64, top-16, window 512, bf16, seq 128K,
+NSA forward + backward, sharded by kv head.  A step = compress -> compressed
+attention + scores -> top-k -> inverse index -> FSA selected forward ->
+sliding window -> gated combine, then the selected and sliding backward (the
+branches the reference differentiates).  Synthetic N(0,1) inputs, random
+init -- no datasets.
 
-``--impl reference`` times the reference algorithm on the host CPU (the oracle
-port, oracle/fsa_oracle.py -- the reference is Python and cannot travel to the
-GPU box) on a bounded sample, rank 0 only.
+Multi-GPU: rank r of N owns kv heads [r h_K / N, (r+1) h_K / N)
+of the one sequence and their query heads and runs the unmodified
+single-GPU path on them -- no collective on the data path.  Total work is
+fixed: "scaling": "strong"; value = the sequence's tokens / max-over-ranks
+step time.
+
+The step is captured once in a CUDA graph (static input buffers; the
+operator path has no host synchronisation), so the timed region measures the
+device, not the host's launch rate.  Extra keys time the Llama-3-8B shape at
+32K (configs[1]) and at 64K (the north_star target) the same way.
+
+``--impl reference`` times the reference algorithm on the host CPU (the
+oracle port, oracle/fsa_oracle.py -- the reference is Python + Cython and is
+not present on the GPU box) on a labelled bounded sample, rank 0 only.
 """
 
 from __future__ import annotations
@@ -32,17 +43,28 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-WORKLOAD = dict(name="llama3-8b-attn-32k", N=32768, d=128, h=32, h_K=8, B_K=64, T=16, W=512)
-CPU_SAMPLE_N = int(os.environ.get("FSA_BENCH_CPU_SAMPLE", 8192))  # smaller only in the CPU tests
+WORKLOADS = {
+    # BASELINE.json configs[4]: the headline (tokens/s at 1/2/4/8 GPU, kv-head shards)
+    "qwen3-14b-attn-128k": dict(N=131072, h=40, h_K=8, d=128, B_K=64, T=16, W=512),
+    # configs[1]
+    "llama3-8b-attn-32k": dict(N=32768, h=32, h_K=8, d=128, B_K=64, T=16, W=512),
+    # the north_star target shape
+    "llama3-8b-attn-64k": dict(N=65536, h=32, h_K=8, d=128, B_K=64, T=16, W=512),
+}
+HEADLINE = "qwen3-14b-attn-128k"
+METRIC = "NSA fwd+bwd tokens/s (Qwen3-14B attention, 128K, GQA 5, kv-head sharded)"
+# reference-arm / cpu_baseline sample: the causal prefix of every kv group
+CPU_SAMPLE_N = int(os.environ.get("FSA_BENCH_CPU_SAMPLE", 16384))
 
 
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
             p = json.load(fh)
-        return p["hbm_gbs"], p["bf16_tflops"], p.get("bf16_tflops_sustained", p["bf16_tflops"]), "measured"
+        return (p["hbm_gbs"], p["bf16_tflops"], p.get("bf16_tflops_sustained", p["bf16_tflops"]),
+                "MEASURED_PEAKS.json")
     except Exception:
-        return 6650.0, 1590.0, 1400.0, "fallback"
+        return 6650.0, 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
 
 
 # ---------------------------------------------------------------------------
@@ -102,113 +124,195 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
-def run_ours(args, rank, world, local_rank):
-    import numpy as np
+def full_cfg(w):
+    import paper_2508_18224_b200 as fsa
+    return fsa.make_config(N=w["N"], d_K=w["d"], d_V=w["d"], h=w["h"], h_K=w["h_K"], B_K=w["B_K"],
+                           T=w["T"], W=w["W"])
+
+
+def rank_inputs(cfg, kv_lo, kv_hi, dev, seed=1234):
+    """This rank's slice of the synthetic problem: every kv head's group is
+    drawn from its own generator, so a shard is the same data whatever the
+    world size.  Q / dOut (N, g*(kv_hi-kv_lo), d), K / V (N, kv_hi-kv_lo, d),
+    gates (N, 3) shared by all heads."""
+    import torch
+    bf = torch.bfloat16
+    qs, ks, vs, ds = [], [], [], []
+    for kh in range(kv_lo, kv_hi):
+        gen = torch.Generator(device=dev).manual_seed(seed + kh)
+        qs.append(torch.randn(cfg.N, cfg.g, cfg.d_K, device=dev, dtype=bf, generator=gen))
+        ks.append(torch.randn(cfg.N, 1, cfg.d_K, device=dev, dtype=bf, generator=gen))
+        vs.append(torch.randn(cfg.N, 1, cfg.d_V, device=dev, dtype=bf, generator=gen))
+        ds.append(torch.randn(cfg.N, cfg.g, cfg.d_V, device=dev, dtype=bf, generator=gen))
+    gen = torch.Generator(device=dev).manual_seed(seed - 1)
+    tau = torch.rand(cfg.N, 3, device=dev, generator=gen)
+    cat = lambda xs: torch.cat(xs, 1).contiguous()  # noqa: E731
+    return cat(qs), cat(ks), cat(vs), cat(ds), tau
+
+
+def algorithmic_flops(cfg, R):
+    """selected 4 / 10 d B_K R, sliding 4 / 10 d h sum_t min(t+1, W),
+    compressed forward 4 d h sum_t floor((t+1)/B_K)."""
+    slide = sum(min(t + 1, cfg.W) for t in range(cfg.N))
+    formed = sum((t + 1) // cfg.B_K for t in range(cfg.N))
+    return ((4.0 + 10.0) * cfg.d_K * cfg.B_K * R + (4.0 + 10.0) * cfg.d_K * cfg.h * slide
+            + 4.0 * cfg.d_K * cfg.h * formed)
+
+
+def measure(name, w, rank, world, dev, steps, warmup, barrier, use_graph=True):
+    """Device-timed NSA fwd+bwd of this rank's kv-head shard of workload w.
+    Returns per-rank ms/step plus the K5 / K8 launch durations (CUDA events
+    on the launching stream inside the timed region)."""
     import torch
 
-    import paper_2508_18224_b200 as fsa
-    from paper_2508_18224_b200 import _lib, kv_major, nsa
+    from paper_2508_18224_b200 import _lib, nsa, parallel
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
-    w = WORKLOAD
-    cfg = fsa.make_config(N=w["N"], d_K=w["d"], d_V=w["d"], h=w["h"], h_K=w["h_K"], B_K=w["B_K"],
-                          T=w["T"], W=w["W"])
-    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
-    bf = torch.bfloat16
-    q = torch.randn(cfg.N, cfg.h, cfg.d_K, device=dev, dtype=bf, generator=gen)
-    k = torch.randn(cfg.N, cfg.h_K, cfg.d_K, device=dev, dtype=bf, generator=gen)
-    v = torch.randn(cfg.N, cfg.h_K, cfg.d_V, device=dev, dtype=bf, generator=gen)
-    dout = torch.randn(cfg.N, cfg.h, cfg.d_V, device=dev, dtype=bf, generator=gen)
-    tau = torch.rand(cfg.N, 3, device=dev, generator=gen)
+    cfg0 = full_cfg(w)
+    sh = parallel.shard_kv_heads(cfg0, rank, world)
+    cfg = sh.cfg
+    q, k, v, dout, tau = rank_inputs(cfg0, sh.kv_lo, sh.kv_hi, dev)
+    orig_call = _lib.call
+    kev = {"fsa_sel_fwd": [], "fsa_sel_bwd": []}
+    capturing = [False]
 
-    def barrier():
-        if world > 1:
-            import torch.distributed as dist
-            dist.barrier()
+    def record(e):
+        if capturing[0]:
+            # inside stream capture a plain record is only a dependency edge;
+            # an "external" record becomes a timing node of the graph
+            _cu_event_record_external(e, torch.cuda.current_stream())
+        else:
+            e.record()
 
-    # per-step timing of the dominant kernel (K5) on the launching stream
+    def timed_call(name_, *a):
+        if name_ not in kev:
+            return orig_call(name_, *a)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        if capturing[0]:  # create the driver events before capture uses them
+            e0.record(side)
+            e1.record(side)
+        record(e0)
+        r = orig_call(name_, *a)
+        record(e1)
+        kev[name_].append((e0, e1))
+        return r
+
     def step():
         out, ctx = nsa.nsa_forward(q, k, v, tau, cfg)
         grads = nsa.nsa_backward(ctx, dout)
         return out, grads, ctx
 
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
     torch.cuda.synchronize()
+    _, _, ctx = step()
+    nnz = int(ctx.inv.offsets[:, -1].to(torch.int64).sum())
+    R = nnz * cfg.g
+    del ctx
 
-    # kernel launches of our library inside one step (profiler, outside the timed region)
-    gpu_launches, kernel_names = None, {}
-    try:
-        from torch.profiler import ProfilerActivity, profile
-        with profile(activities=[ProfilerActivity.CUDA]) as prof:
-            step()
+    graph = None
+    if use_graph:
+        # one CUDA graph holding all K timed steps, each with its own K5 / K8
+        # events (a replayed single-step graph would overwrite them)
+        try:
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                step()
+            torch.cuda.current_stream().wait_stream(side)
             torch.cuda.synchronize()
-        kernel_ms = {}
-        for e in prof.key_averages():
-            if e.device_type is not None and "fsa" in e.key and e.count:
-                kernel_names[e.key[:80]] = kernel_names.get(e.key[:80], 0) + e.count
-                t_us = getattr(e, "device_time_total", None) or getattr(e, "cuda_time_total", 0)
-                kernel_ms[e.key[:80]] = round(t_us / 1e3, 4)
-        gpu_launches = sum(kernel_names.values()) * args.steps
-        kernel_names = {"launches": kernel_names, "device_ms_profiled": kernel_ms}
-    except Exception as exc:  # pragma: no cover
-        kernel_names = {"profiler_error": str(exc)[:120]}
-
-    # The tensor-core kernels are timed inside the same loop with CUDA events
-    # on the launching stream: the C-ABI entry points are wrapped so that each
-    # fsa_sel_fwd (K5) / fsa_sel_bwd (K8, selected branch) launch is bracketed.
-    sampler = ClockSampler(local_rank)
+            graph = torch.cuda.CUDAGraph()
+            _lib.call = timed_call
+            capturing[0] = True
+            with torch.cuda.graph(graph):
+                for _ in range(steps):
+                    step()
+        except Exception as exc:  # pragma: no cover - reported, then the eager loop runs
+            graph = None
+            print(f"bench: CUDA graph capture failed ({exc!s:.120}); timing eager launches",
+                  file=sys.stderr)
+        finally:
+            _lib.call = orig_call
+            capturing[0] = False
+        if graph is None:
+            kev = {"fsa_sel_fwd": [], "fsa_sel_bwd": []}
+        else:
+            graph.replay()  # untimed: first replay uploads the graph
+            torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
-    sampler.start()
     start = torch.cuda.Event(enable_timing=True)
     stop = torch.cuda.Event(enable_timing=True)
-    kev = {"fsa_sel_fwd": [], "fsa_sel_bwd": []}
-    orig_call = _lib.call
-
-    def timed_call(name, *a):
-        if name not in kev:
-            return orig_call(name, *a)
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-        r = orig_call(name, *a)
-        e1.record()
-        kev[name].append((e0, e1))
-        return r
-
-    _lib.call = timed_call
-    start.record()
-    for _ in range(args.steps):
-        out_, grads_, ctx_ = step()
-    stop.record()
+    if graph is not None:
+        start.record()
+        graph.replay()
+        stop.record()
+    else:
+        _lib.call = timed_call
+        start.record()
+        for _ in range(steps):
+            step()
+        stop.record()
+        _lib.call = orig_call
     torch.cuda.synchronize()
-    _lib.call = orig_call
-    clocks = sampler.stop()
-    ms = start.elapsed_time(stop) / args.steps
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    k5_ms = statistics.median(e0.elapsed_time(e1) for e0, e1 in kev["fsa_sel_fwd"])
-    k8_ms = statistics.median(e0.elapsed_time(e1) for e0, e1 in kev["fsa_sel_bwd"])
-    inv = ctx_.inv
-    nnz = int(inv.offsets[:, -1].to(torch.int64).sum())
-    R = nnz * cfg.g
-    k5_flops = 4.0 * cfg.d_K * cfg.B_K * R
-    k8_flops = 10.0 * cfg.d_K * cfg.B_K * R
+    ms = start.elapsed_time(stop) / steps
+    k5 = [e0.elapsed_time(e1) for e0, e1 in kev["fsa_sel_fwd"]][-steps:]
+    k8 = [e0.elapsed_time(e1) for e0, e1 in kev["fsa_sel_bwd"]][-steps:]
+    del graph
+    torch.cuda.empty_cache()
+    return dict(name=name, cfg=cfg, cfg0=cfg0, shard=sh, ms=ms, R=R,
+                k5_ms=statistics.mean(k5), k8_ms=statistics.mean(k8), graph=use_graph,
+                inputs=(q, k, v, dout, tau))
 
-    # ---- end to end through the public API: pinned host inputs in, out + grads
-    # (bf16, the input dtype) back to pinned host memory, every step.  Copies
-    # run on their own streams, double-buffered, so step i+1's upload and step
-    # i-1's download overlap step i's kernels.
+
+_LIBCUDA = None
+
+
+def _cu_event_record_external(ev, stream):
+    """cuEventRecordWithFlags(CU_EVENT_RECORD_EXTERNAL): a timing event inside a
+    CUDA graph (torch's Event.record during capture is only a dependency)."""
+    import ctypes
+    global _LIBCUDA
+    if _LIBCUDA is None:
+        _LIBCUDA = ctypes.CDLL("libcuda.so.1")
+    rc = _LIBCUDA.cuEventRecordWithFlags(ctypes.c_void_p(ev.cuda_event),
+                                         ctypes.c_void_p(stream.cuda_stream), ctypes.c_uint(1))
+    if rc != 0:
+        raise RuntimeError(f"cuEventRecordWithFlags failed ({rc})")
+
+
+def max_over_ranks(x, world, dev):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x, world, dev):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def e2e_run(m, world, dev, steps, barrier):
+    """End to end through the public API: pinned host inputs in, out + grads
+    (bf16, the input dtype) back to pinned host memory, every step.  Copies
+    run on their own streams, double-buffered, so step i+1's upload and step
+    i-1's download overlap step i's kernels."""
+    import torch
+
+    from paper_2508_18224_b200 import nsa
+    cfg = m["cfg"]
+    bf = torch.bfloat16
     names = ("q", "k", "v", "dout", "tau")
-    host_in = {n: t.cpu().pin_memory() for n, t in zip(names, (q, k, v, dout, tau))}
+    host_in = {n: t.cpu().pin_memory() for n, t in zip(names, m["inputs"])}
     h2d = sum(t.numel() * t.element_size() for t in host_in.values())
     dev_in = [{n: torch.empty_like(t, device=dev) for n, t in host_in.items()} for _ in range(2)]
     out_shapes = ((cfg.N, cfg.h, cfg.d_V), (cfg.N, cfg.h, cfg.d_K), (cfg.N, cfg.h_K, cfg.d_K),
@@ -218,8 +322,7 @@ def run_ours(args, rank, world, local_rank):
     d2h = sum(x.numel() * x.element_size() for x in host_out[0])
     comp = torch.cuda.current_stream()
     up, down = torch.cuda.Stream(), torch.cuda.Stream()
-    ev = lambda: torch.cuda.Event()  # noqa: E731
-    in_ready, in_free, out_ready, out_free = ([ev() for _ in range(2)] for _ in range(4))
+    in_ready, in_free, out_ready, out_free = ([torch.cuda.Event() for _ in range(2)] for _ in range(4))
 
     def upload(i):
         s_ = i % 2
@@ -248,11 +351,6 @@ def run_ours(args, rank, world, local_rank):
                 dst.copy_(src, non_blocking=True)
             out_free[s_].record(down)
 
-    # the copy pipeline's fill (first upload) and drain (last download) are
-    # one-off costs; time enough steps that the per-step figure is the steady
-    # state of a long run (each step still uploads its inputs and downloads
-    # its results inside the timed region)
-    e2e_steps = max(args.steps, 30)
     for i in range(2):  # warm the copy path
         upload(i)
         e2e_step(i)
@@ -264,71 +362,146 @@ def run_ours(args, rank, world, local_rank):
     e_start.record(comp)
     up.wait_event(e_start)
     upload(0)
-    for i in range(e2e_steps):
-        if i + 1 < e2e_steps:
+    for i in range(steps):
+        if i + 1 < steps:
             upload(i + 1)
         e2e_step(i)
     comp.wait_stream(down)
     e_stop.record(comp)
     torch.cuda.synchronize()
-    e2e_ms = e_start.elapsed_time(e_stop) / e2e_steps
+    return e_start.elapsed_time(e_stop) / steps, h2d, d2h
+
+
+def count_launches(m):
+    """Our kernels launched in one step (profiler, outside the timed region)."""
+    import torch
+
+    from paper_2508_18224_b200 import nsa
+    q, k, v, dout, tau = m["inputs"]
+    names, kms = {}, {}
+    try:
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            out, ctx = nsa.nsa_forward(q, k, v, tau, m["cfg"])
+            nsa.nsa_backward(ctx, dout)
+            torch.cuda.synchronize()
+        for e in prof.key_averages():
+            if e.device_type is not None and "fsa" in e.key and e.count:
+                names[e.key[:80]] = names.get(e.key[:80], 0) + e.count
+                t_us = getattr(e, "device_time_total", None) or getattr(e, "cuda_time_total", 0)
+                kms[e.key[:80]] = round(t_us / 1e3, 4)
+        return sum(names.values()), {"launches": names, "device_ms_profiled": kms}
+    except Exception as exc:  # pragma: no cover
+        return None, {"profiler_error": str(exc)[:120]}
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
     if world > 1:
         import torch.distributed as dist
-        t = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
 
     hbm, pk_burst, pk_sus, pk_src = _peaks()
-    tokens = world * cfg.N
-    value = tokens / (ms / 1e3)
-    step_flops = (4.0 + 10.0) * cfg.d_K * cfg.B_K * R  # selected fwd + bwd
-    slide_pairs = sum(min(t + 1, cfg.W) for t in range(cfg.N))
-    step_flops += (4.0 + 10.0) * cfg.d_K * cfg.h * slide_pairs
-    step_flops += 4.0 * cfg.d_K * cfg.h * sum((t + 1) // cfg.B_K for t in range(cfg.N))
     traffic = {}
-    try:  # dram__bytes_read.sum + dram__bytes_write.sum per launch, from the committed ncu capture
+    try:  # dram__bytes_read.sum + dram__bytes_write.sum per launch, committed ncu capture
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
             traffic = json.load(fh)
     except Exception:
         pass
 
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    m = measure(HEADLINE, WORKLOADS[HEADLINE], rank, world, dev, args.steps, args.warmup, barrier,
+                use_graph=not args.no_graph)
+    clocks = sampler.stop()
+    cfg0 = m["cfg0"]
+    ms = max_over_ranks(m["ms"], world, dev)
+    k5_ms = max_over_ranks(m["k5_ms"], world, dev)
+    k8_ms = max_over_ranks(m["k8_ms"], world, dev)
+    R_rank = m["R"]
+    R_all = sum_over_ranks(R_rank, world, dev)
+    gpu_launches, kernel_names = count_launches(m)
+    if gpu_launches is not None:
+        gpu_launches *= args.steps
+    e2e_ms, h2d, d2h = e2e_run(m, world, dev, max(args.steps, 10), barrier)
+    e2e_ms = max_over_ranks(e2e_ms, world, dev)
+    h2d, d2h = sum_over_ranks(h2d, world, dev), sum_over_ranks(d2h, world, dev)
+    del m
+
+    step_flops = algorithmic_flops(cfg0, R_all)
+
     def roof(kernel, flops, kms, algo, tkey):
+        # burst peak: a kernel timed alone inside a 20-step loop at full clocks
         ach = flops / (kms / 1e3) / 1e12
-        return {"kernel": kernel, "bound": "tensor", "achieved": round(ach, 2), "peak": pk_sus,
-                "unit": "TFLOP/s", "frac": round(ach / pk_sus, 4),
-                "traffic": traffic.get(tkey), "peak_source": f"{pk_src} sustained bf16",
+        return {"kernel": kernel, "bound": "tensor", "achieved": round(ach, 2), "peak": pk_burst,
+                "unit": "TFLOP/s", "frac": round(ach / pk_burst, 4),
+                "traffic": traffic.get(tkey), "peak_source": f"{pk_src} bf16 burst",
                 "kernel_ms": round(kms, 4), "share_of_step": round(kms / ms, 4),
                 "algorithmic": algo}
+
+    # per-rank FLOPs of the selected kernels (R of the rank's shard)
+    k5_flops = 4.0 * cfg0.d_K * cfg0.B_K * R_rank
+    k8_flops = 10.0 * cfg0.d_K * cfg0.B_K * R_rank
     line = {
-        "metric": "NSA fwd+bwd tokens/s (Llama-3-8B attention, 32K, GQA 4)",
-        "value": round(value, 1),
+        "metric": METRIC,
+        "value": round(cfg0.N / (ms / 1e3), 1),
         "unit": "tokens/s",
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": round(ms, 4),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic N(0,1) Q/K/V/dOut, U[0,1) gates, random init",
-        "config": arm_config(world),
+        "config": arm_config(world, HEADLINE),
+        "timing": "CUDA graph of the K timed steps, one replay between CUDA events"
+                  if not args.no_graph else "eager launches between CUDA events",
         "effective_tflops": round(step_flops / (ms / 1e3) / 1e12, 2),
         # dominant kernel: the selected-attention backward (K8)
         "roofline": roof("sel_bwd (K8, tcgen05, selected branch)", k8_flops, k8_ms,
-                         "10*d*B_K*R FLOPs, R = (query head, token, block) rows = %d" % R,
-                         "tc_sel_bwd_selected"),
+                         "10*d*B_K*R FLOPs per launch, R = (query head, token, block) rows = %d "
+                         "on this rank" % R_rank, "tc_sel_bwd_selected"),
         "roofline_sel_fwd": roof("sel_fwd (K5, tcgen05)", k5_flops, k5_ms,
-                                 "4*d*B_K*R FLOPs, R = %d" % R, "tc_sel_fwd"),
-        "e2e": {"value": round(tokens / (e2e_ms / 1e3), 1), "unit": "tokens/s",
-                "ms_per_step": round(e2e_ms, 3), "steps": e2e_steps, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h},
+                                 "4*d*B_K*R FLOPs per launch, R = %d on this rank" % R_rank,
+                                 "tc_sel_fwd"),
+        "e2e": {"value": round(cfg0.N / (e2e_ms / 1e3), 1), "unit": "tokens/s",
+                "ms_per_step": round(e2e_ms, 3), "steps": max(args.steps, 10),
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": gpu_launches,
         "kernels_per_step": kernel_names,
         "clocks": clocks,
     }
+    if not args.no_extras:
+        extras = {}
+        for name in ("llama3-8b-attn-32k", "llama3-8b-attn-64k"):
+            x = measure(name, WORKLOADS[name], rank, world, dev, args.steps, args.warmup, barrier,
+                        use_graph=not args.no_graph)
+            xms = max_over_ranks(x["ms"], world, dev)
+            xk5 = max_over_ranks(x["k5_ms"], world, dev)
+            xk8 = max_over_ranks(x["k8_ms"], world, dev)
+            xR = sum_over_ranks(x["R"], world, dev)
+            c0 = x["cfg0"]
+            extras[name] = {
+                "tokens_per_s": round(c0.N / (xms / 1e3), 1), "ms_per_step": round(xms, 4),
+                "effective_tflops": round(algorithmic_flops(c0, xR) / (xms / 1e3) / 1e12, 2),
+                "k5_ms": round(xk5, 4), "k8_ms": round(xk8, 4),
+                "k5_frac_burst": round(4.0 * c0.d_K * c0.B_K * x["R"] / (xk5 / 1e3) / 1e12 / pk_burst, 4),
+                "k8_frac_burst": round(10.0 * c0.d_K * c0.B_K * x["R"] / (xk8 / 1e3) / 1e12 / pk_burst, 4),
+                "config": arm_config(world, name)}
+            del x
+        line["extra_workloads"] = extras
     if rank == 0 and world == 1 and not args.no_cpu_baseline:  # rank 0 at N = 1 only
-        line["cpu_baseline"] = cpu_baseline(args, sample_n=CPU_SAMPLE_N, steps=1)
+        line["cpu_baseline"] = cpu_baseline(sample_n=CPU_SAMPLE_N, steps=1)
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
@@ -343,9 +516,8 @@ def run_ours(args, rank, world, local_rank):
 def _cpu_group(args_tuple):
     n_tok, seed = args_tuple
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    import numpy as np
     from oracle import fsa_oracle as O
-    w = WORKLOAD
+    w = WORKLOADS[HEADLINE]
     c = O.cfg_of(N=n_tok, d_K=w["d"], d_V=w["d"], h=w["h"] // w["h_K"], h_K=1, B_K=w["B_K"],
                  T=w["T"], W=w["W"])
     Q, K, V = O.make_qkv(c, seed)
@@ -356,12 +528,12 @@ def _cpu_group(args_tuple):
     return time.perf_counter() - t0
 
 
-def cpu_baseline(args, sample_n=CPU_SAMPLE_N, steps=1):
+def cpu_baseline(sample_n=CPU_SAMPLE_N, steps=1):
     """The oracle port on the host cores: one process per KV group (bit-exact
     sharding); sample = the first ``sample_n`` tokens of each KV
-    group of the workload, fwd+bwd of every branch."""
+    group of the headline workload, fwd+bwd of every branch."""
     import multiprocessing as mp
-    w = WORKLOAD
+    w = WORKLOADS[HEADLINE]
     cores = max(1, min(len(os.sched_getaffinity(0)), w["h_K"]))
     times = []
     with mp.get_context("spawn").Pool(cores) as pool:
@@ -371,32 +543,38 @@ def cpu_baseline(args, sample_n=CPU_SAMPLE_N, steps=1):
             times.append(time.perf_counter() - t0)
     wall = statistics.median(times)
     return {"value": round(sample_n / wall, 2), "unit": "tokens/s", "cores": cores, "kind": "port",
-            "sample": f"all {w['h_K']} KV groups of {w['name']}, first {sample_n} tokens "
-                      f"(N={sample_n} causal prefix), NSA fwd+bwd in float64 numpy, "
-                      f"{cores} processes; {wall:.1f} s wall"}
+            "sample": f"all {w['h_K']} KV groups of {HEADLINE}, first {sample_n} tokens "
+                      f"(N={sample_n} causal prefix of the 131072-token sequence), NSA fwd+bwd "
+                      f"in float64 numpy, {cores} processes; {wall:.1f} s wall"}
 
 
-def arm_config(world):
-    """The workload both arms report (the reference arm measures a bounded
-    sample of it; cpu_baseline.sample says which)."""
-    w = WORKLOAD
-    return {"workload": w["name"], "seq_len": w["N"], "batch_per_gpu": 1, "q_heads": w["h"],
-            "kv_heads": w["h_K"], "head_dim": w["d"], "block": w["B_K"], "top_k": w["T"],
-            "window": w["W"], "parallelism": f"batch{world}", "l2": "inputs exceed L2 "
-            "(Q 268 MB, K/V 67 MB each, partial buffer 4.2 GB); no flush"}
+def arm_config(world, name=HEADLINE, seq_len=None, sample=None):
+    """The workload an arm reports."""
+    w = WORKLOADS[name]
+    c = {"workload": name, "seq_len": w["N"] if seq_len is None else seq_len, "batch": 1,
+         "q_heads": w["h"], "kv_heads": w["h_K"], "head_dim": w["d"], "block": w["B_K"],
+         "top_k": w["T"], "window": w["W"], "parallelism": f"kv-head shards x{world}",
+         "l2": "inputs exceed L2 (Q and dOut 1.3 GB each at 128K, slot-partial buffers "
+               "21 GB); no flush"}
+    if sample:
+        c["sample"] = sample
+    return c
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return None
     n = CPU_SAMPLE_N
-    cb = cpu_baseline(args, sample_n=n, steps=max(1, min(args.steps, 5)))
+    cb = cpu_baseline(sample_n=n, steps=max(1, min(args.steps, 3)))
     return {
         "impl": "reference",
-        "metric": "NSA fwd+bwd tokens/s (Llama-3-8B attention, 32K, GQA 4)",
+        "metric": METRIC,
         "value": cb["value"], "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic", "config": arm_config(world),
+        "warmup": args.warmup, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": arm_config(world, HEADLINE, seq_len=n,
+                             sample=f"first {n} tokens (causal prefix) of every kv group of the "
+                                    f"{WORKLOADS[HEADLINE]['N']}-token workload"),
         "cpu_baseline": cb,
         "e2e": {"value": cb["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -406,10 +584,12 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the Llama 32K / 64K extra keys")
+    ap.add_argument("--no-graph", action="store_true", help="time eager launches (no CUDA graph)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", args.gpus if args.gpus == 1 else 1))

@@ -2,6 +2,9 @@
 
 from __future__ import annotations
 
+import json
+import os
+
 import numpy as np
 import torch
 
@@ -26,17 +29,24 @@ def rms(a):
     return float(np.sqrt(np.mean(a * a))) if a.size else 0.0
 
 
-def assert_close(got, ref, dtype, what="", grad=False):
-    """Tolerance per north_star: fp32 rtol 1e-4, bf16 rtol 2e-2, each with an
-    RMS-scaled absolute floor; f64 at the reference's own 1e-10.
+def _report(rec):
+    """FSA_PARITY_REPORT=<file>: append one JSON line per comparison (violation
+    counts, max normalised error) -- the evidence behind profiles/*parity*."""
+    path = os.environ.get("FSA_PARITY_REPORT")
+    if path:
+        with open(path, "a") as fh:
+            fh.write(json.dumps(rec) + "\n")
 
-    bf16 results are compared normwise -- max|err| <= 2e-2 * max|ref| and
-    ||err||_2 <= 2e-2 * ||ref||_2 -- because the tensor-core path rounds P,
-    dS and the per-block partial outputs to bf16 (as every bf16 flash
-    attention does): over 10^7 elements a handful land a few RMS-atol away
-    from the float64 oracle, and gradients additionally inherit the rounding
-    of delta = rowsum(out * dOut) where dP - delta cancels.  (``grad`` is
-    kept for call-site documentation.)"""
+
+def assert_close(got, ref, dtype, what="", grad=False):
+    """Tolerance per north_star and SURVEY 8(d), elementwise for every dtype:
+
+        |got - ref| <= rtol * |ref| + rtol * RMS(ref)
+
+    rtol = 1e-4 (f32), 2e-2 (bf16); f64 at the reference's own 1e-9 scale.
+    ``ref`` is the float64 oracle run on the dtype-rounded inputs.  The
+    normwise error ||err|| / ||ref|| is reported alongside as a diagnostic
+    only.  ``grad`` is kept for call-site documentation."""
     got = np.asarray(got, dtype=np.float64)
     ref = np.asarray(ref, dtype=np.float64)
     assert got.shape == ref.shape, (what, got.shape, ref.shape)
@@ -46,13 +56,15 @@ def assert_close(got, ref, dtype, what="", grad=False):
         assert err <= tol, f"{what}: max abs err {err:.3e} > {tol:.1e}"
         return
     rtol = 1e-4 if dtype == "f32" else 2e-2
-    if dtype == "bf16":
-        err = np.abs(got - ref)
-        assert err.max() <= rtol * np.abs(ref).max(), f"{what}: max err {err.max():.3e}"
-        assert np.linalg.norm(err) <= rtol * np.linalg.norm(ref), (
-            f"{what}: normwise err {np.linalg.norm(err) / np.linalg.norm(ref):.3e}")
-        return
     atol = rtol * max(rms(ref), 1e-30)
-    bad = np.abs(got - ref) > atol + rtol * np.abs(ref)
-    assert not bad.any(), (f"{what}: {int(bad.sum())}/{bad.size} outside rtol={rtol} atol={atol:.2e}; "
-                           f"max abs err {float(np.abs(got - ref).max()):.3e}")
+    err = np.abs(got - ref)
+    bound = atol + rtol * np.abs(ref)
+    bad = ~(err <= bound)  # NaN counts as a violation
+    nbad = int(bad.sum())
+    worst = float((err / bound).max()) if ref.size else 0.0
+    normwise = float(np.linalg.norm(err) / max(np.linalg.norm(ref), 1e-300)) if ref.size else 0.0
+    _report(dict(what=what, dtype=dtype, n=int(ref.size), violations=nbad,
+                 worst_err_over_bound=worst, normwise=normwise))
+    assert nbad == 0, (f"{what}: {nbad}/{bad.size} elements outside |err| <= {rtol}*|ref| + "
+                       f"{rtol}*RMS(ref) (atol {atol:.2e}); worst err/bound {worst:.2f}, "
+                       f"normwise {normwise:.2e}")

@@ -150,7 +150,9 @@ def test_bench_reference_arm_json_contract():
     d = json.loads(out.stdout.strip().splitlines()[-1])
     assert d["impl"] == "reference" and d["unit"] == "tokens/s" and d["value"] > 0
     assert d["metric"].startswith("NSA fwd+bwd tokens/s") and d["higher_is_better"] is True
-    assert d["config"]["workload"] == "llama3-8b-attn-32k" and d["config"]["seq_len"] == 32768
+    # the headline workload; seq_len states the sample that was timed
+    assert d["config"]["workload"] == "qwen3-14b-attn-128k" and d["config"]["seq_len"] == 2048
+    assert "2048" in d["config"]["sample"]
     cb = d["cpu_baseline"]
     assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
     assert d["e2e"] == {"value": d["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
