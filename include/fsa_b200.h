@@ -45,17 +45,18 @@ extern "C" {
 #define FSA_ERR_CUDA 2
 #define FSA_ERR_UNSUPPORTED 3
 
-#define FSA_ABI_VERSION 1
+#define FSA_ABI_VERSION 2
 
-typedef enum { FSA_DT_F32 = 0, FSA_DT_F64 = 1, FSA_DT_BF16 = 2, FSA_DT_I32 = 3 } fsa_dtype;
-
-/* OR-ed into the dtype argument of fsa_slide_fwd, fsa_cmp_attn_fwd,
- * fsa_merge_combine_fwd, fsa_gate_backward_fold, fsa_gate_backward_full (and of
- * fsa_dq_reduce_add, for its addend): the
- * branch outputs (out_cmp, out_slide, out_sel) are bf16 instead of the
- * accumulator dtype -- bf16 tensor-core path only (the NSA step uses it: the
- * branch outputs are intermediates of the bf16 combined output). */
-#define FSA_OUT_NARROW 0x100
+/* Element types.  FSA_DT_F16 and FSA_DT_F16R are buffer formats of the bf16
+ * tensor-core path, never input dtypes:
+ *   F16  obuf [h][N][T][128] fp16 partials O_i / l_i in the power-of-two scale
+ *        s_kh of the fsa_v_to_f16 copy of V (the merge divides by vscale[kh]);
+ *   F16R dq_buf = fp16 rows [h][N][T][128] followed by one int8 exponent e per
+ *        row [h][N][T]: row value = fp16 * 2^-e (per-row scale, row max in
+ *        [2^14, 2^15)) -- bytes h*N*T*(2*128 + 1). */
+typedef enum {
+  FSA_DT_F32 = 0, FSA_DT_F64 = 1, FSA_DT_BF16 = 2, FSA_DT_I32 = 3, FSA_DT_F16 = 4, FSA_DT_F16R = 5
+} fsa_dtype;
 
 /* Resolved AttentionConfig (config.py:30-104); scale = 1/sqrt(d_K). */
 typedef struct fsa_shape {
@@ -87,8 +88,15 @@ int fsa_abi_version(void);
 int fsa_device_check(void);
 
 /* Buffer dtypes the library will read/write for a given problem: obuf (LOCAL
- * mode) and dq_buf.  bf16 problems on the tensor-core path use bf16 obuf. */
+ * mode) and dq_buf.  bf16 problems on the tensor-core path (d = 128, B_K = 64)
+ * use FSA_DT_F16 obuf and FSA_DT_F16R dq_buf. */
 int fsa_buffer_dtypes(const fsa_shape* s, int dtype, int* obuf_dtype, int* dqbuf_dtype);
+
+/* fp16 staging of V for the tensor-core P.V products (bf16 path): V16 [N][h_K][d_V]
+ * = fp16(V * s_kh), s_kh = 2^(15 - k) for max|V[:, kh, :]| = f 2^k, f in [0.5, 1).
+ * vscale [2 h_K] floats: s_kh in [0, h_K), scratch after.  dtype BF16 or F32. */
+int fsa_v_to_f16(const fsa_shape* s, int dtype, const void* V, void* V16, float* vscale,
+                 void* stream);
 
 /* compress_kv (branches.py:34-44): block means K_cmp/V_cmp [b][h_K][d] and the
  * running prefix means of the first min(B_K-1, N) rows [n_pref][h_K][d]; acc dtype. */
@@ -119,26 +127,30 @@ int fsa_build_inverse(const fsa_shape* s, const int32_t* idx, void* workspace, i
 
 /* FSA block pass (kv_major.py:105-204, _core.pyx:49-94): one task per
  * (KV head, block) loads K_i/V_i once and serves all g query heads of the
- * gathered rows.  m_global ([h][N], acc) only for FSA_FWD_GLOBAL. */
+ * gathered rows.  m_global ([h][N], acc) only for FSA_FWD_GLOBAL.
+ * obuf_dtype FSA_DT_F16 selects the tcgen05 kernel (LOCAL mode; V must then be
+ * the fsa_v_to_f16 copy). */
 int fsa_sel_fwd(const fsa_shape* s, int dtype, int mode, const void* Q, const void* K,
                 const void* V, const int32_t* offsets, const int32_t* qlist, const int32_t* work,
                 const void* m_global, void* obuf, int obuf_dtype, void* ml, void* stream);
 
 /* Merge of per-slot partials in ascending block order (kv_major.py:207-242;
  * stats merge kv_major.py:137-149, shared max :141-146).  out, lse, m_out,
- * l_out in acc dtype; m_out/l_out/lse nullable. */
+ * l_out in acc dtype; m_out/l_out/lse nullable.  vscale: the V16 scales
+ * (required with FSA_DT_F16 obuf, else ignored). */
 int fsa_merge_fwd(const fsa_shape* s, int dtype, int mode, const int32_t* idx, const void* obuf,
                   int obuf_dtype, const void* ml, const void* m_global, const void* l_global,
-                  void* out, void* lse, void* m_out, void* l_out, int shared_max, void* stream);
+                  void* out, void* lse, void* m_out, void* l_out, int shared_max,
+                  const float* vscale, void* stream);
 
 /* K6 + K12 fused for the NSA step: the LOCAL merge (as fsa_merge_fwd) writes the
  * selected branch's out_sel / lse (acc dtype) and, in the same pass, the gated
  * combine (branches.py:95-104) out = tau0 out_cmp + tau1 out_sel + tau2 out_slide
  * in dtype.  out_cmp / out_slide / tau in acc dtype. */
 int fsa_merge_combine_fwd(const fsa_shape* s, int dtype, const int32_t* idx, const void* obuf,
-                          int obuf_dtype, const void* ml, const void* out_cmp,
-                          const void* out_slide, const void* tau, void* out_sel, void* lse,
-                          void* out, void* stream);
+                          int obuf_dtype, const void* ml, const float* vscale,
+                          const void* out_cmp, const void* out_slide, const void* tau,
+                          void* out_sel, void* lse, void* out, void* stream);
 
 /* delta = sum_v out * dOut (kv_major.py:284); [h][N] acc. */
 int fsa_bwd_delta(const fsa_shape* s, int dtype, const void* out, const void* dOut, void* delta,
@@ -156,10 +168,10 @@ int fsa_sel_bwd(const fsa_shape* s, int dtype, const void* Q, const void* K, con
 int fsa_dq_reduce(const fsa_shape* s, int dtype, const int32_t* idx, const void* dq_buf,
                   int dqbuf_dtype, void* dQ, void* stream);
 
-/* fsa_dq_reduce plus addend [N][h][d_K] (acc dtype; bf16 with dtype |
- * FSA_OUT_NARROW) added to every row in the same pass: dQ = (ascending-block sum
- * of the dq partials) + addend.  bf16 tensor-core configuration only (the NSA
- * step: selected + sliding dQ). */
+/* fsa_dq_reduce plus addend [N][h][d_K] (fp32) added to every row in the same
+ * pass: dQ = (ascending-block sum of the dq partials) + addend.  bf16
+ * tensor-core configuration only (FSA_DT_F16R partials; the NSA step:
+ * selected + sliding dQ). */
 int fsa_dq_reduce_add(const fsa_shape* s, int dtype, const int32_t* idx, const void* dq_buf,
                       int dqbuf_dtype, const void* addend, void* dQ, void* stream);
 
@@ -174,17 +186,19 @@ int fsa_cmp_attn_fwd(const fsa_shape* s, int dtype, const void* Q, const void* K
                      const void* V_cmp, const void* K_prefix, const void* V_prefix, void* out,
                      void* lse, void* scores, void* workspace, void* stream);
 
-/* sliding_attention_forward (branches.py:81-83 -> oracle.py:39-44, :64-74). */
+/* sliding_attention_forward (branches.py:81-83 -> oracle.py:39-44, :64-74).
+ * bf16 tensor-core path: V is the fsa_v_to_f16 copy and vscale its scales
+ * (required); f32 / f64: vscale ignored. */
 int fsa_slide_fwd(const fsa_shape* s, int dtype, const void* Q, const void* K, const void* V,
-                  void* out, void* lse, void* stream);
+                  const float* vscale, void* out, void* lse, void* stream);
 
 /* Band-mask dense_backward (oracle.py:102-131 with band_mask); grads acc dtype.
  * The bf16 tensor-core path runs the FSA backward kernel over each KV block's
- * window of tokens and needs fsa_slide_bwd_workspace_bytes of workspace (the
- * per-window-slot dQ partials); accumulate != 0 adds into dQ/dK/dV (sums the
- * sliding branch onto the selected branch's gradients) -- tensor-core path only.
- * accumulate == 2 adds into dK/dV but WRITES dQ (for fsa_dq_reduce_add);
- * accumulate == 3 likewise, with dQ written as bf16 (the NSA step's hand-off). */
+ * window of tokens (dK / dV) and a query-outer kernel for dQ, and needs
+ * fsa_slide_bwd_workspace_bytes of workspace (its scheduler counter);
+ * accumulate == 1 adds into dQ/dK/dV (sums the sliding branch onto the selected
+ * branch's gradients), accumulate == 2 adds into dK/dV but WRITES dQ (fp32, for
+ * fsa_dq_reduce_add) -- tensor-core path only. */
 size_t fsa_slide_bwd_workspace_bytes(const fsa_shape* s, int dtype);
 int fsa_slide_bwd(const fsa_shape* s, int dtype, const void* Q, const void* K, const void* V,
                   const void* dOut, const void* lse, const void* delta, void* dQ, void* dK,

@@ -16,10 +16,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libfsa_b200.so")
 
 FSA_OK, FSA_ERR_INVALID, FSA_ERR_CUDA, FSA_ERR_UNSUPPORTED = 0, 1, 2, 3
-DT_F32, DT_F64, DT_BF16, DT_I32 = 0, 1, 2, 3
+DT_F32, DT_F64, DT_BF16, DT_I32, DT_F16, DT_F16R = 0, 1, 2, 3, 4, 5
 FWD_LOCAL, FWD_STATS, FWD_GLOBAL = 0, 1, 2
 MERGE_LOCAL, MERGE_STATS, MERGE_REDUCE = 0, 1, 2
-OUT_NARROW = 0x100  # FSA_OUT_NARROW: branch outputs in bf16 (include/fsa_b200.h)
 
 SEL_FLAGS = (  # bit, message -- in the reference's check order (selection.py:59-75)
     (1, "malformed selection: empty row"),
@@ -46,6 +45,7 @@ SIGNATURES = {
     "fsa_abi_version": ([], _i),
     "fsa_device_check": ([], _i),
     "fsa_buffer_dtypes": ([_sp, _i, _ip, _ip], _i),
+    "fsa_v_to_f16": ([_sp, _i, _vp, _vp, _vp, _vp], _i),
     "fsa_compress_kv": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "fsa_importance_scores": ([_sp, _i, _vp, _vp, _vp, _vp], _i),
     "fsa_select_topk": ([_sp, _i, _vp, _vp, _vp], _i),
@@ -53,15 +53,15 @@ SIGNATURES = {
     "fsa_inverse_workspace_bytes": ([_sp], _sz),
     "fsa_build_inverse": ([_sp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "fsa_sel_fwd": ([_sp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp], _i),
-    "fsa_merge_fwd": ([_sp, _i, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp], _i),
-    "fsa_merge_combine_fwd": ([_sp, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
+    "fsa_merge_fwd": ([_sp, _i, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp], _i),
+    "fsa_merge_combine_fwd": ([_sp, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "fsa_bwd_delta": ([_sp, _i, _vp, _vp, _vp, _vp], _i),
     "fsa_sel_bwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp], _i),
     "fsa_dq_reduce": ([_sp, _i, _vp, _vp, _i, _vp, _vp], _i),
     "fsa_dq_reduce_add": ([_sp, _i, _vp, _vp, _i, _vp, _vp, _vp], _i),
     "fsa_cmp_workspace_bytes": ([_sp], _sz),
     "fsa_cmp_attn_fwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
-    "fsa_slide_fwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp], _i),
+    "fsa_slide_fwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "fsa_slide_bwd_workspace_bytes": ([_sp, _i], _sz),
     "fsa_slide_bwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp], _i),
     "fsa_gated_combine": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp], _i),
@@ -161,11 +161,33 @@ def acc_dtype(dtype):
     return torch.float64 if dtype == torch.float64 else torch.float32
 
 
-_TORCH_OF = {DT_F32: torch.float32, DT_F64: torch.float64, DT_BF16: torch.bfloat16}
+_TORCH_OF = {DT_F32: torch.float32, DT_F64: torch.float64, DT_BF16: torch.bfloat16,
+             DT_F16: torch.float16, DT_F16R: torch.uint8}
 
 
 def buffer_dtypes(cfg, dtype):
+    """((obuf code, torch dtype), (dq_buf code, torch dtype)) for a problem; the
+    tensor-core path uses fp16 obuf and FSA_DT_F16R dq_buf (bytes)."""
     s = shape_of(cfg)
     ob, dq = ctypes.c_int(), ctypes.c_int()
     call("fsa_buffer_dtypes", ctypes.byref(s), dt_code(dtype), ctypes.byref(ob), ctypes.byref(dq))
     return (ob.value, _TORCH_OF[ob.value]), (dq.value, _TORCH_OF[dq.value])
+
+
+def dq_buffer(cfg, code, dtype, dev):
+    """The dq partial buffer: [h][N][T][d_K] of dtype, or for FSA_DT_F16R the
+    fp16 rows followed by one int8 exponent per row (include/fsa_b200.h)."""
+    if code == DT_F16R:
+        rows = cfg.h * cfg.N * cfg.T
+        return torch.empty(rows * (2 * cfg.d_K + 1), dtype=torch.uint8, device=dev)
+    return torch.empty((cfg.h, cfg.N, cfg.T, cfg.d_K), dtype=dtype, device=dev)
+
+
+def v_to_f16(cfg, v):
+    """fsa_v_to_f16: the power-of-two scaled fp16 copy of V (N, h_K, d_V) and
+    its per-kv-head scales -- the value operand of the tensor-core P.V products."""
+    v16 = torch.empty(v.shape, dtype=torch.float16, device=v.device)
+    vscale = torch.empty(2 * cfg.h_K, dtype=torch.float32, device=v.device)
+    s = shape_of(cfg)
+    call("fsa_v_to_f16", ctypes.byref(s), dt_code(v.dtype), ptr(v), ptr(v16), ptr(vscale), stream())
+    return v16, vscale

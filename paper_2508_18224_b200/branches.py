@@ -96,15 +96,18 @@ def sliding_attention_forward(Q, K, V, cfg) -> AttentionOutput:
     return AttentionOutput(out=logical(out), lse=lse)
 
 
-def _slide_fwd_storage(cfg, dt, q, k, v, narrow=False):
-    """narrow: out in bf16 (FSA_OUT_NARROW; the NSA step's intermediate)."""
+def _slide_fwd_storage(cfg, dt, q, k, v, v16=None):
+    """K10 on storage tensors.  The bf16 tensor-core path reads V as its
+    scaled fp16 copy ``v16 = (V16, vscale)`` (made here when not given)."""
     dev, acc = q.device, _lib.acc_dtype(dt)
-    out = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=torch.bfloat16 if narrow else acc, device=dev)
+    out = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=acc, device=dev)
     lse = torch.empty((cfg.h, cfg.N), dtype=acc, device=dev)
     s = _lib.shape_of(cfg)
-    code = _lib.dt_code(dt) | (_lib.OUT_NARROW if narrow else 0)
-    _lib.call("fsa_slide_fwd", ctypes.byref(s), code, _lib.ptr(q), _lib.ptr(k),
-              _lib.ptr(v), _lib.ptr(out), _lib.ptr(lse), _lib.stream())
+    vscale = None
+    if dt == torch.bfloat16 and cfg.d_K == 128 and cfg.d_V == 128 and cfg.g <= 128:
+        v, vscale = v16 if v16 is not None else _lib.v_to_f16(cfg, v)
+    _lib.call("fsa_slide_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(q), _lib.ptr(k),
+              _lib.ptr(v), _lib.ptr(vscale), _lib.ptr(out), _lib.ptr(lse), _lib.stream())
     return out, lse
 
 

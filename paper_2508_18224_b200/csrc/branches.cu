@@ -193,7 +193,7 @@ __global__ void slide_bwd_dkdv_generic(const T* __restrict__ Q, const T* __restr
 template <typename T>
 int cmp_fwd_impl(const fsa_shape* s, const void* Q, const void* Kc, const void* Vc, const void* Kp,
                  const void* Vp, void* out, void* lse, void* scores, void* workspace,
-                 cudaStream_t st, int narrow) {
+                 cudaStream_t st) {
   using A = typename Acc<T>::type;
   const int dt = sizeof(T) == 8 ? FSA_DT_F64 : (sizeof(T) == 4 ? FSA_DT_F32 : FSA_DT_BF16);
   const bool tc = tc_qo_supported(*s, dt) && workspace != nullptr;
@@ -203,15 +203,10 @@ int cmp_fwd_impl(const fsa_shape* s, const void* Q, const void* Kc, const void* 
   if (tc) {
     // scores for the formed blocks come from the tensor cores for every g:
     // a separate group-summed-query pass (bf16 hi/lo pairs, ~fp32 accurate)
-    if (int rc = tc_cmp_fwd(s, Q, Kc, Vc, out, lse, scores, workspace, st, narrow)) return rc;
+    if (int rc = tc_cmp_fwd(s, Q, Kc, Vc, out, lse, scores, workspace, st)) return rc;
   }
-  FSA_REQUIRE(!narrow || (tc && sizeof(T) == 2), "cmp_attn_fwd: narrow output needs the bf16 tensor-core path");
   const int64_t rows = s->h * ntok;
-  if (rows > 0 && narrow)
-    cmp_fwd_generic<T, __nv_bfloat16><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(
-        (const T*)Q, (const A*)Kc, (const A*)Vc, (const A*)Kp, (const A*)Vp, (__nv_bfloat16*)out,
-        (A*)lse, *s, ntok);
-  else if (rows > 0)
+  if (rows > 0)
     cmp_fwd_generic<T><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(
         (const T*)Q, (const A*)Kc, (const A*)Vc, (const A*)Kp, (const A*)Vp, (A*)out, (A*)lse, *s,
         ntok);
@@ -265,10 +260,8 @@ extern "C" int fsa_cmp_attn_fwd(const fsa_shape* s, int dtype, const void* Q, co
                                 const void* V_cmp, const void* K_prefix, const void* V_prefix,
                                 void* out, void* lse, void* scores, void* workspace,
                                 void* stream) {
-  const int narrow = (dtype & FSA_OUT_NARROW) != 0;
-  dtype &= ~FSA_OUT_NARROW;
   DISPATCH_DT(dtype, cmp_fwd_impl, s, Q, K_cmp, V_cmp, K_prefix, V_prefix, out, lse, scores,
-              workspace, (cudaStream_t)stream, narrow);
+              workspace, (cudaStream_t)stream);
 }
 
 extern "C" size_t fsa_cmp_workspace_bytes(const fsa_shape* s) {
@@ -276,12 +269,10 @@ extern "C" size_t fsa_cmp_workspace_bytes(const fsa_shape* s) {
 }
 
 extern "C" int fsa_slide_fwd(const fsa_shape* s, int dtype, const void* Q, const void* K,
-                             const void* V, void* out, void* lse, void* stream) {
-  const int narrow = (dtype & FSA_OUT_NARROW) != 0;
-  dtype &= ~FSA_OUT_NARROW;
-  if (fsa::tc_qo_supported(*s, dtype))
-    return fsa::tc_slide_fwd(s, Q, K, V, out, lse, (cudaStream_t)stream, narrow);
-  FSA_REQUIRE(!narrow, "slide_fwd: narrow output needs the bf16 tensor-core path");
+                             const void* V, const float* vscale, void* out, void* lse,
+                             void* stream) {
+  if (fsa::tc_qo_supported(*s, dtype))  // V: the fsa_v_to_f16 copy, vscale its scales
+    return fsa::tc_slide_fwd(s, Q, K, V, vscale, out, lse, (cudaStream_t)stream);
   DISPATCH_DT(dtype, slide_fwd_impl, s, Q, K, V, out, lse, (cudaStream_t)stream);
 }
 

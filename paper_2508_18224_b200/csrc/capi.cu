@@ -50,8 +50,8 @@ extern "C" int fsa_device_check(void) {
 
 extern "C" int fsa_buffer_dtypes(const fsa_shape* s, int dtype, int* obuf_dtype, int* dqbuf_dtype) {
   const bool tc = fsa::tc_fwd_supported(*s, dtype);
-  if (obuf_dtype) *obuf_dtype = tc ? FSA_DT_BF16 : (dtype == FSA_DT_F64 ? FSA_DT_F64 : FSA_DT_F32);
+  if (obuf_dtype) *obuf_dtype = tc ? FSA_DT_F16 : (dtype == FSA_DT_F64 ? FSA_DT_F64 : FSA_DT_F32);
   const bool tcb = fsa::tc_bwd_supported(*s, dtype);
-  if (dqbuf_dtype) *dqbuf_dtype = tcb ? FSA_DT_BF16 : (dtype == FSA_DT_F64 ? FSA_DT_F64 : FSA_DT_F32);
+  if (dqbuf_dtype) *dqbuf_dtype = tcb ? FSA_DT_F16R : (dtype == FSA_DT_F64 ? FSA_DT_F64 : FSA_DT_F32);
   return FSA_OK;
 }

@@ -389,18 +389,11 @@ template <typename T>
 int gate_fold3_impl(const fsa_shape* s, const void* dOut, const void* tau, const void* o0,
                     const void* o1, const void* o2, const void* l0, const void* l1, const void* l2,
                     void* del0, void* del1, void* del2, void* la0, void* la1, void* la2, void* dtau,
-                    cudaStream_t st, int narrow) {
+                    cudaStream_t st) {
   using A = typename Acc<T>::type;
   if (s->N == 0) return FSA_OK;
-  FSA_REQUIRE(!narrow || sizeof(T) == 2, "gate_backward_full_fold: narrow outputs need bf16");
   const unsigned grid = (unsigned)((s->N + 7) / 8);
-  if (narrow)
-    gate_fold3_kernel<T, __nv_bfloat16><<<grid, 256, 0, st>>>(
-        (const T*)dOut, (const A*)tau, (const __nv_bfloat16*)o0, (const __nv_bfloat16*)o1,
-        (const __nv_bfloat16*)o2, (const A*)l0, (const A*)l1, (const A*)l2, (A*)del0, (A*)del1,
-        (A*)del2, (A*)la0, (A*)la1, (A*)la2, (A*)dtau, s->N, s->h, s->d_V);
-  else
-    gate_fold3_kernel<T, A><<<grid, 256, 0, st>>>(
+  gate_fold3_kernel<T, A><<<grid, 256, 0, st>>>(
         (const T*)dOut, (const A*)tau, (const A*)o0, (const A*)o1, (const A*)o2, (const A*)l0,
         (const A*)l1, (const A*)l2, (A*)del0, (A*)del1, (A*)del2, (A*)la0, (A*)la1, (A*)la2,
         (A*)dtau, s->N, s->h, s->d_V);
@@ -411,17 +404,10 @@ int gate_fold3_impl(const fsa_shape* s, const void* dOut, const void* tau, const
 template <typename T>
 int gate_bwd_full_impl(const fsa_shape* s, const void* dOut, const void* tau, const void* o0,
                        const void* o1, const void* o2, void* d0, void* d1, void* d2, void* del0,
-                       void* del1, void* del2, void* dtau, cudaStream_t st, int narrow) {
+                       void* del1, void* del2, void* dtau, cudaStream_t st) {
   using A = typename Acc<T>::type;
   if (s->N == 0) return FSA_OK;
-  FSA_REQUIRE(!narrow || sizeof(T) == 2, "gate_backward_full: narrow outputs need bf16");
-  if (narrow)
-    gate_backward_full_kernel<T, __nv_bfloat16><<<(unsigned)((s->N + 7) / 8), 256, 0, st>>>(
-        (const T*)dOut, (const A*)tau, (const __nv_bfloat16*)o0, (const __nv_bfloat16*)o1,
-        (const __nv_bfloat16*)o2, (T*)d0, (T*)d1, (T*)d2, (A*)del0, (A*)del1, (A*)del2, (A*)dtau,
-        s->N, s->h, s->d_V);
-  else
-    gate_backward_full_kernel<T><<<(unsigned)((s->N + 7) / 8), 256, 0, st>>>(
+  gate_backward_full_kernel<T><<<(unsigned)((s->N + 7) / 8), 256, 0, st>>>(
         (const T*)dOut, (const A*)tau, (const A*)o0, (const A*)o1, (const A*)o2, (T*)d0, (T*)d1,
         (T*)d2, (A*)del0, (A*)del1, (A*)del2, (A*)dtau, s->N, s->h, s->d_V);
   FSA_LAUNCH_CHECK("gate_backward_full");
@@ -469,10 +455,8 @@ extern "C" int fsa_gate_backward_full(const fsa_shape* s, int dtype, const void*
                                       const void* out_slide, void* d_cmp, void* d_sel,
                                       void* d_slide, void* delta_cmp, void* delta_sel,
                                       void* delta_slide, void* dtau, void* stream) {
-  const int narrow = (dtype & FSA_OUT_NARROW) != 0;
-  dtype &= ~FSA_OUT_NARROW;
   DISPATCH_DT(dtype, gate_bwd_full_impl, s, dOut, tau, out_cmp, out_sel, out_slide, d_cmp, d_sel,
-              d_slide, delta_cmp, delta_sel, delta_slide, dtau, (cudaStream_t)stream, narrow);
+              d_slide, delta_cmp, delta_sel, delta_slide, dtau, (cudaStream_t)stream);
 }
 
 extern "C" int fsa_gate_backward_full_fold(const fsa_shape* s, int dtype, const void* dOut,
@@ -482,9 +466,7 @@ extern "C" int fsa_gate_backward_full_fold(const fsa_shape* s, int dtype, const 
                                            void* delta_cmp, void* delta_sel, void* delta_slide,
                                            void* lse_cmp_adj, void* lse_sel_adj, void* lse_slide_adj,
                                            void* dtau, void* stream) {
-  const int narrow = (dtype & FSA_OUT_NARROW) != 0;
-  dtype &= ~FSA_OUT_NARROW;
   DISPATCH_DT(dtype, gate_fold3_impl, s, dOut, tau, out_cmp, out_sel, out_slide, lse_cmp, lse_sel,
               lse_slide, delta_cmp, delta_sel, delta_slide, lse_cmp_adj, lse_sel_adj, lse_slide_adj,
-              dtau, (cudaStream_t)stream, narrow);
+              dtau, (cudaStream_t)stream);
 }

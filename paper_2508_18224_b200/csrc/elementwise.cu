@@ -323,40 +323,31 @@ __global__ void gate_fold_kernel(const T* __restrict__ dOut, const typename Acc<
   }
 }
 
-// bf16 everything, d_V = 128: a half warp per (token, head) row, 16-byte loads
-__global__ void gate_fold_bf16x8_kernel(const __nv_bfloat16* __restrict__ dOut, const float* __restrict__ tau,
-                                        const __nv_bfloat16* __restrict__ out_sel,
-                                        const __nv_bfloat16* __restrict__ out_slide,
-                                        const float* __restrict__ lse_sel, const float* __restrict__ lse_slide,
-                                        float* __restrict__ delta_sel, float* __restrict__ delta_slide,
-                                        float* __restrict__ lse_sel_adj, float* __restrict__ lse_slide_adj,
-                                        int64_t N, int64_t h) {
-  const int lane = threadIdx.x & 31, hl = lane & 15;
-  const int64_t row = (blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5)) * 2 + (lane >> 4);
-  const bool live = row < N * h;
-  float s1 = 0.f, s2 = 0.f;
-  if (live) {
-    const int64_t e = row * 128 + hl * 8;
-    const uint4 x = *reinterpret_cast<const uint4*>(dOut + e);
-    const uint4 a = *reinterpret_cast<const uint4*>(out_sel + e);
-    const uint4 b = *reinterpret_cast<const uint4*>(out_slide + e);
-    const __nv_bfloat162* xp = reinterpret_cast<const __nv_bfloat162*>(&x);
-    const __nv_bfloat162* ap = reinterpret_cast<const __nv_bfloat162*>(&a);
-    const __nv_bfloat162* bp = reinterpret_cast<const __nv_bfloat162*>(&b);
+// bf16 dOut, fp32 branch outputs, d_V = 128: a warp per (token, head) row,
+// 16-byte branch-output loads and 8-byte dOut loads
+__global__ void __launch_bounds__(256) gate_fold_d128_kernel(
+    const __nv_bfloat16* __restrict__ dOut, const float* __restrict__ tau,
+    const float* __restrict__ out_sel, const float* __restrict__ out_slide,
+    const float* __restrict__ lse_sel, const float* __restrict__ lse_slide,
+    float* __restrict__ delta_sel, float* __restrict__ delta_slide,
+    float* __restrict__ lse_sel_adj, float* __restrict__ lse_slide_adj, int64_t N, int64_t h) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= N * h) return;
+  const int64_t e = row * 128 + lane * 4;
+  const uint2 x = __ldg(reinterpret_cast<const uint2*>(dOut + e));
+  const float4 a = __ldcs(reinterpret_cast<const float4*>(out_sel + e));
+  const float4 b = __ldcs(reinterpret_cast<const float4*>(out_slide + e));
+  const float2 x0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&x.x));
+  const float2 x1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&x.y));
+  float s1 = a.x * x0.x + a.y * x0.y + a.z * x1.x + a.w * x1.y;
+  float s2 = b.x * x0.x + b.y * x0.y + b.z * x1.x + b.w * x1.y;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float2 xf = __bfloat1622float2(xp[k]), af = __bfloat1622float2(ap[k]),
-                   bf = __bfloat1622float2(bp[k]);
-      s1 += af.x * xf.x + af.y * xf.y;
-      s2 += bf.x * xf.x + bf.y * xf.y;
-    }
-  }
-#pragma unroll
-  for (int o = 8; o > 0; o >>= 1) {
+  for (int o = 16; o > 0; o >>= 1) {
     s1 += __shfl_xor_sync(0xffffffffu, s1, o);
     s2 += __shfl_xor_sync(0xffffffffu, s2, o);
   }
-  if (live && hl == 0) {
+  if (lane == 0) {
     const int64_t t = row / h, j = row - t * h, r = j * N + t;
     delta_sel[r] = s1;
     delta_slide[r] = s2;
@@ -368,22 +359,15 @@ __global__ void gate_fold_bf16x8_kernel(const __nv_bfloat16* __restrict__ dOut, 
 template <typename T>
 int gate_fold_impl(const fsa_shape* s, const void* dOut, const void* tau, const void* out_sel,
                    const void* out_slide, const void* lse_sel, const void* lse_slide, void* delta_sel,
-                   void* delta_slide, void* lse_sel_adj, void* lse_slide_adj, cudaStream_t st,
-                   int narrow) {
+                   void* delta_slide, void* lse_sel_adj, void* lse_slide_adj, cudaStream_t st) {
   using A = typename Acc<T>::type;
   const int64_t rows = s->N * s->h;
   if (rows == 0) return FSA_OK;
-  FSA_REQUIRE(!narrow || sizeof(T) == 2, "gate_backward_fold: narrow outputs need bf16");
-  if (narrow && sizeof(T) == 2 && s->d_V == 128)
-    gate_fold_bf16x8_kernel<<<(unsigned)((rows + 15) / 16), 256, 0, st>>>(
-        (const __nv_bfloat16*)dOut, (const float*)tau, (const __nv_bfloat16*)out_sel,
-        (const __nv_bfloat16*)out_slide, (const float*)lse_sel, (const float*)lse_slide,
+  if (sizeof(T) == 2 && s->d_V == 128)
+    gate_fold_d128_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(
+        (const __nv_bfloat16*)dOut, (const float*)tau, (const float*)out_sel,
+        (const float*)out_slide, (const float*)lse_sel, (const float*)lse_slide,
         (float*)delta_sel, (float*)delta_slide, (float*)lse_sel_adj, (float*)lse_slide_adj, s->N, s->h);
-  else if (narrow)
-    gate_fold_kernel<T, __nv_bfloat16><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(
-        (const T*)dOut, (const A*)tau, (const __nv_bfloat16*)out_sel, (const __nv_bfloat16*)out_slide,
-        (const A*)lse_sel, (const A*)lse_slide, (A*)delta_sel, (A*)delta_slide, (A*)lse_sel_adj,
-        (A*)lse_slide_adj, s->N, s->h, s->d_V);
   else
     gate_fold_kernel<T><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(
         (const T*)dOut, (const A*)tau, (const A*)out_sel, (const A*)out_slide, (const A*)lse_sel,
@@ -447,10 +431,8 @@ extern "C" int fsa_gate_backward_fold(const fsa_shape* s, int dtype, const void*
                                       const void* out_sel, const void* out_slide, const void* lse_sel,
                                       const void* lse_slide, void* delta_sel, void* delta_slide,
                                       void* lse_sel_adj, void* lse_slide_adj, void* stream) {
-  const int narrow = (dtype & FSA_OUT_NARROW) != 0;
-  dtype &= ~FSA_OUT_NARROW;
   DISPATCH_DT(dtype, gate_fold_impl, s, dOut, tau, out_sel, out_slide, lse_sel, lse_slide, delta_sel,
-              delta_slide, lse_sel_adj, lse_slide_adj, (cudaStream_t)stream, narrow);
+              delta_slide, lse_sel_adj, lse_slide_adj, (cudaStream_t)stream);
 }
 
 extern "C" int fsa_check_finite(int dtype, const void* x, int64_t n, int32_t* flag, void* stream) {

@@ -326,18 +326,17 @@ int sel_fwd_impl(const fsa_shape* s, int mode, const void* Q, const void* K, con
 template <typename T>
 int merge_impl(const fsa_shape* s, int mode, const int32_t* idx, const void* obuf, int obuf_dtype,
                const void* ml, const void* mg, const void* lg, void* out, void* lse, void* m_out,
-               void* l_out, int shared_max, cudaStream_t st) {
+               void* l_out, int shared_max, const float* vscale, cudaStream_t st) {
   using A = typename Acc<T>::type;
   const int64_t rows = s->h_K * s->N;
   if (rows == 0) return FSA_OK;
   const unsigned grid = (unsigned)((rows + 7) / 8);
-  if (obuf_dtype == FSA_DT_BF16 && mode == FSA_MERGE_LOCAL && fast_reduce_ok(*s))
-    return merge_bf16_fast(s, idx, obuf, ml, out, lse, m_out, l_out, st);
-  if (obuf_dtype == FSA_DT_BF16) {
-    merge_generic<T, __nv_bfloat16><<<grid, 256, 0, st>>>(
-        mode, idx, (const __nv_bfloat16*)obuf, (const A*)ml, (const A*)mg, (const A*)lg, (A*)out,
-        (A*)lse, (A*)m_out, (A*)l_out, shared_max, *s);
-  } else {
+  if (obuf_dtype == FSA_DT_F16) {  // the tensor-core path's fp16 partials (LOCAL mode only)
+    FSA_REQUIRE(mode == FSA_MERGE_LOCAL && fast_reduce_ok(*s) && sizeof(A) == 4,
+                "merge_fwd: fp16 partials only in LOCAL mode with d = 128");
+    return merge_f16_fast(s, idx, obuf, ml, vscale, out, lse, m_out, l_out, st);
+  }
+  {
     merge_generic<T, A><<<grid, 256, 0, st>>>(mode, idx, (const A*)obuf, (const A*)ml, (const A*)mg,
                                               (const A*)lg, (A*)out, (A*)lse, (A*)m_out, (A*)l_out,
                                               shared_max, *s);
@@ -386,13 +385,11 @@ int dq_reduce_impl(const fsa_shape* s, const int32_t* idx, const void* dq_buf, i
   const int64_t rows = s->h * s->N;
   if (rows == 0) return FSA_OK;
   const unsigned grid = (unsigned)((rows + 7) / 8);
-  if (dqbuf_dtype == FSA_DT_BF16 && fast_reduce_ok(*s))
-    return dq_reduce_bf16_fast(s, idx, dq_buf, dQ, st);
-  if (dqbuf_dtype == FSA_DT_BF16)
-    dq_reduce_kernel<T, __nv_bfloat16><<<grid, 256, 0, st>>>(idx, (const __nv_bfloat16*)dq_buf,
-                                                             (A*)dQ, *s);
-  else
-    dq_reduce_kernel<T, A><<<grid, 256, 0, st>>>(idx, (const A*)dq_buf, (A*)dQ, *s);
+  if (dqbuf_dtype == FSA_DT_F16R) {
+    FSA_REQUIRE(fast_reduce_ok(*s) && sizeof(A) == 4, "dq_reduce: fp16 partials need d = 128");
+    return dq_reduce_f16r(s, idx, dq_buf, dQ, st);
+  }
+  dq_reduce_kernel<T, A><<<grid, 256, 0, st>>>(idx, (const A*)dq_buf, (A*)dQ, *s);
   FSA_LAUNCH_CHECK("dq_reduce");
   return FSA_OK;
 }
@@ -415,9 +412,9 @@ extern "C" int fsa_sel_fwd(const fsa_shape* s, int dtype, int mode, const void* 
     fsa::set_error("sel_fwd: bad mode %d", mode);
     return FSA_ERR_INVALID;
   }
-  if (obuf_dtype == FSA_DT_BF16) {
+  if (obuf_dtype == FSA_DT_F16) {  // V is the fsa_v_to_f16 copy
     if (mode != FSA_FWD_LOCAL || !fsa::tc_fwd_supported(*s, dtype)) {
-      fsa::set_error("sel_fwd: bf16 partial buffer only on the tensor-core LOCAL path");
+      fsa::set_error("sel_fwd: fp16 partial buffer only on the tensor-core LOCAL path");
       return FSA_ERR_INVALID;
     }
     return fsa::tc_sel_fwd(s, Q, K, V, offsets, qlist, work, obuf, ml, (cudaStream_t)stream);
@@ -429,28 +426,26 @@ extern "C" int fsa_sel_fwd(const fsa_shape* s, int dtype, int mode, const void* 
 extern "C" int fsa_merge_fwd(const fsa_shape* s, int dtype, int mode, const int32_t* idx,
                              const void* obuf, int obuf_dtype, const void* ml, const void* m_global,
                              const void* l_global, void* out, void* lse, void* m_out, void* l_out,
-                             int shared_max, void* stream) {
+                             int shared_max, const float* vscale, void* stream) {
   if (mode == FSA_MERGE_STATS && (!m_out || !l_out)) {
     fsa::set_error("merge_fwd: STATS mode needs m_out and l_out");
     return FSA_ERR_INVALID;
   }
   DISPATCH_DT(dtype, merge_impl, s, mode, idx, obuf, obuf_dtype, ml, m_global, l_global, out, lse,
-              m_out, l_out, shared_max, (cudaStream_t)stream);
+              m_out, l_out, shared_max, vscale, (cudaStream_t)stream);
 }
 
 extern "C" int fsa_merge_combine_fwd(const fsa_shape* s, int dtype, const int32_t* idx,
                                      const void* obuf, int obuf_dtype, const void* ml,
-                                     const void* out_cmp, const void* out_slide, const void* tau,
-                                     void* out_sel, void* lse, void* out, void* stream) {
+                                     const float* vscale, const void* out_cmp,
+                                     const void* out_slide, const void* tau, void* out_sel,
+                                     void* lse, void* out, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  const int narrow = (dtype & FSA_OUT_NARROW) != 0;
-  dtype &= ~FSA_OUT_NARROW;
-  if (dtype == FSA_DT_BF16 && obuf_dtype == FSA_DT_BF16 && fsa::fast_reduce_ok(*s))
-    return fsa::merge_combine_bf16_fast(s, idx, obuf, ml, out_cmp, out_slide, tau, out_sel, lse,
-                                        out, st, narrow);
-  FSA_REQUIRE(!narrow, "merge_combine_fwd: narrow branch outputs need the bf16 fast path");
+  if (dtype == FSA_DT_BF16 && obuf_dtype == FSA_DT_F16 && fsa::fast_reduce_ok(*s))
+    return fsa::merge_f16_fast(s, idx, obuf, ml, vscale, out_sel, lse, nullptr, nullptr, st,
+                               out_cmp, out_slide, tau, out);
   int rc = fsa_merge_fwd(s, dtype, FSA_MERGE_LOCAL, idx, obuf, obuf_dtype, ml, nullptr, nullptr,
-                         out_sel, lse, nullptr, nullptr, 0, stream);
+                         out_sel, lse, nullptr, nullptr, 0, vscale, stream);
   if (rc) return rc;
   return fsa_gated_combine(s, dtype, out_cmp, out_sel, out_slide, tau, out, 0, stream);
 }
@@ -464,7 +459,7 @@ extern "C" int fsa_sel_bwd(const fsa_shape* s, int dtype, const void* Q, const v
                            const void* V, const void* dOut, const void* lse, const void* delta,
                            const int32_t* offsets, const int32_t* qlist, const int32_t* work,
                            void* dq_buf, int dqbuf_dtype, void* dK, void* dV, void* stream) {
-  if (fsa::tc_bwd_supported(*s, dtype))
+  if (fsa::tc_bwd_supported(*s, dtype))  // dq_buf: FSA_DT_F16R rows + exponents
     return fsa::tc_sel_bwd(s, Q, K, V, dOut, lse, delta, offsets, qlist, work, dq_buf, dqbuf_dtype,
                            dK, dV, (cudaStream_t)stream);
   FSA_REQUIRE(dqbuf_dtype == (dtype == FSA_DT_F64 ? FSA_DT_F64 : FSA_DT_F32),
@@ -476,11 +471,9 @@ extern "C" int fsa_sel_bwd(const fsa_shape* s, int dtype, const void* Q, const v
 extern "C" int fsa_dq_reduce_add(const fsa_shape* s, int dtype, const int32_t* idx,
                                  const void* dq_buf, int dqbuf_dtype, const void* addend, void* dQ,
                                  void* stream) {
-  const int narrow = (dtype & FSA_OUT_NARROW) != 0;  // the addend is bf16
-  dtype &= ~FSA_OUT_NARROW;
-  if (dtype == FSA_DT_BF16 && dqbuf_dtype == FSA_DT_BF16 && fsa::fast_reduce_ok(*s))
-    return fsa::dq_reduce_bf16_fast(s, idx, dq_buf, dQ, (cudaStream_t)stream, addend, narrow);
-  fsa::set_error("dq_reduce_add: only the bf16 tensor-core configuration (d = 128, T <= 32)");
+  if (dtype == FSA_DT_BF16 && dqbuf_dtype == FSA_DT_F16R && fsa::fast_reduce_ok(*s))
+    return fsa::dq_reduce_f16r(s, idx, dq_buf, dQ, (cudaStream_t)stream, addend);
+  fsa::set_error("dq_reduce_add: only the bf16 tensor-core configuration (fp16 partials, d = 128)");
   return FSA_ERR_UNSUPPORTED;
 }
 

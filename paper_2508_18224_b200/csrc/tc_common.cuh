@@ -4,6 +4,7 @@
 #pragma once
 #include <stdint.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <stdio.h>
 
 namespace fsa {
@@ -401,6 +402,15 @@ __host__ __device__ constexpr uint32_t idesc_bf16(uint32_t M, uint32_t N, bool a
          ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
+// kind::f16 instruction descriptor: fp16 x fp16 -> f32 (a/b format 0 = F16).
+// The P.V products run in fp16: P <= 2^8 and the power-of-two scaled V copy
+// (fsa_v_to_f16) fit its range, and its 10-bit mantissa rounds P 8x finer
+// than bf16 -- the rounding that otherwise drives out / delta / dQ errors.
+__host__ __device__ constexpr uint32_t idesc_f16(uint32_t M, uint32_t N, bool a_mn, bool b_mn) {
+  return (1u << 4) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) | ((N >> 3) << 17) |
+         ((M >> 4) << 24);
+}
+
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -409,6 +419,19 @@ __device__ __forceinline__ float ex2(float x) {
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ uint32_t pack_f16(float a, float b) {
+  __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+// Power-of-two exponent e with max_abs * 2^e in [2^14, 2^15) (0 for 0 / non-finite):
+// the per-row scale of the fp16 dq partials.
+__device__ __forceinline__ int f16_row_exp(float max_abs) {
+  if (!(max_abs > 0.f) || !isfinite(max_abs)) return 0;
+  int k;
+  frexpf(max_abs, &k);  // max_abs = f 2^k, f in [0.5, 1)
+  const int e = 15 - k;
+  return e < -120 ? -120 : (e > 120 ? 120 : e);
 }
 
 }  // namespace tc

@@ -8,7 +8,8 @@ namespace fsa {
 bool tc_fwd_supported(const fsa_shape& s, int dtype);
 bool tc_bwd_supported(const fsa_shape& s, int dtype);
 
-int tc_sel_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V,
+// V: the fp16 staged copy (stage_f16); obuf fp16 [h][N][T][128] in its scale
+int tc_sel_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V16,
                const int32_t* offsets, const int32_t* qlist, const int32_t* work, void* obuf,
                void* ml, cudaStream_t st);
 int tc_sel_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V, const void* dOut,
@@ -16,14 +17,18 @@ int tc_sel_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V, 
                const int32_t* work, void* dq_buf, int dqbuf_dtype, void* dK, void* dV,
                cudaStream_t st);
 
+// fp16 staging of a [rows][heads][d] bf16 / f32 tensor with a power-of-two
+// scale per head (f16_stage.cu); vscale [2 heads]: scales, then scratch
+int stage_f16(int src_dtype, const void* x, int64_t rows, int64_t heads, int64_t d, void* y,
+              float* vscale, cudaStream_t st);
+
 // query-outer forward (tc_qo_fwd.cu): sliding window and compressed attention
 bool tc_qo_supported(const fsa_shape& s, int dtype);
-bool tc_cmp_scores_fused(const fsa_shape& s);
-int tc_slide_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V, void* out,
-                 void* lse, cudaStream_t st, int out_bf16 = 0);
+int tc_slide_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V16,
+                 const float* vscale, void* out, void* lse, cudaStream_t st);
 size_t tc_cmp_workspace_bytes(const fsa_shape* s);
 int tc_cmp_fwd(const fsa_shape* s, const void* Q, const void* Kc, const void* Vc, void* out,
-               void* lse, void* scores, void* workspace, cudaStream_t st, int out_bf16 = 0);
+               void* lse, void* scores, void* workspace, cudaStream_t st);
 
 // sliding-window backward on the FSA backward kernel (tc_sel_bwd.cu)
 size_t tc_slide_bwd_workspace_bytes(const fsa_shape* s);
@@ -33,8 +38,7 @@ int tc_slide_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V
 
 // query-outer sliding-window dQ (tc_slide_dq.cu); accumulate: dQ += (fp32)
 int tc_slide_dq(const fsa_shape* s, const void* Q, const void* K, const void* V, const void* dOut,
-                const void* lse, const void* delta, void* dQ, int accumulate, cudaStream_t st,
-                int out_bf16 = 0);
+                const void* lse, const void* delta, void* dQ, int accumulate, cudaStream_t st);
 
 // compressed-branch backward on the same kernels (tc_sel_bwd.cu, tc_slide_dq.cu):
 // dK_cmp / dV_cmp partial slabs per token chunk, and dQ += over the pooled rows
@@ -45,18 +49,30 @@ int tc_cmp_bwd_kv(const fsa_shape* s, const void* Q, const void* Kb, const void*
 int tc_cmp_dq(const fsa_shape* s, const void* Q, const void* Kb, const void* Vb, const void* dOut,
               const void* lse, const void* delta, void* dQ, cudaStream_t st);
 
-// vectorised bf16 merge / dQ reduce for d = 128, T <= 32 (merge_fast.cu)
+// vectorised merge of the fp16 slot partials / reduce of the fp16 dq partials
+// for d = 128, any T (merge_fast.cu); out / lse / m / l / dQ / addend fp32.
+// out_cmp / out_slide / tau / out_comb non-null: the gated combine in the same pass.
 bool fast_reduce_ok(const fsa_shape& s);
-int merge_bf16_fast(const fsa_shape* s, const int32_t* idx, const void* obuf, const void* ml,
-                    void* out, void* lse, void* m_out, void* l_out, cudaStream_t st);
-int merge_combine_bf16_fast(const fsa_shape* s, const int32_t* idx, const void* obuf,
-                            const void* ml, const void* out_cmp, const void* out_slide,
-                            const void* tau, void* out_sel, void* lse, void* out, cudaStream_t st,
-                            int narrow = 0);
-int dq_reduce_bf16_fast(const fsa_shape* s, const int32_t* idx, const void* dq, void* dQ,
-                        cudaStream_t st, const void* addend = nullptr, int addend_bf16 = 0);
+int merge_f16_fast(const fsa_shape* s, const int32_t* idx, const void* obuf, const void* ml,
+                   const float* vscale, void* out, void* lse, void* m_out, void* l_out,
+                   cudaStream_t st, const void* out_cmp = nullptr, const void* out_slide = nullptr,
+                   const void* tau = nullptr, void* out_comb = nullptr);
+int dq_reduce_f16r(const fsa_shape* s, const int32_t* idx, const void* dq, void* dQ,
+                   cudaStream_t st, const void* addend = nullptr);
 
 int num_sms();
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) holds per device: set it the
+// first time a kernel launches on each device (one bit per device in `done`).
+template <typename K>
+inline void ensure_smem_attr(K kern, int bytes, unsigned long long& done) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (__atomic_load_n(&done, __ATOMIC_ACQUIRE) & bit) return;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  __atomic_fetch_or(&done, bit, __ATOMIC_RELEASE);
+}
 
 }  // namespace fsa
 #include <cuda.h>

@@ -13,9 +13,11 @@
 // sub-item w:
 //   S_w = Q_w K^T  (M128 N64 K128) -> TMEM stage v of wg w
 //   softmax: mask, lazy running max (moved only on a > 2^8 increase, so the
-//            O accumulator is rescaled almost never), P = exp2(...) packed
-//            bf16 written back over S in TMEM (tcgen05.st)
-//   O_w += P V     (M128 N128 K64, A operand = P read from TMEM)
+//            O accumulator is rescaled almost never), P = exp2(...) <= 2^8
+//            packed fp16 written back over S in TMEM (tcgen05.st)
+//   O_w += P V     (M128 N128 K64, fp16: A operand = P read from TMEM, V the
+//                   power-of-two scaled fp16 copy of f16_stage.cu; the
+//                   epilogue divides by the head's scale)
 // The MMA thread runs four in-order streams (S_0, S_1, PV_0, PV_1) polled
 // without blocking, so neither warpgroup waits for the other.
 //
@@ -43,7 +45,7 @@ constexpr uint32_t kOffTmem = kOffBar + kNumBars * 8;
 constexpr uint32_t kSmemBytes = kOffTmem + 16 + 1024;
 static_assert(kSmemBytes <= 232448, "shared memory budget");
 constexpr uint32_t kIdS = idesc_bf16(128, 64, false, false);
-constexpr uint32_t kIdPV = idesc_bf16(128, 128, false, true);
+constexpr uint32_t kIdPV = idesc_f16(128, 128, false, true);  // P, V16 in fp16
 constexpr float kRescale = 8.f;  // exp2 units
 
 // SCORES: importance scores only (no softmax / PV), on the group-summed
@@ -59,12 +61,15 @@ enum Mode { SLIDE = 0, CMP = 1, SCORES = 2 };
   } while (0)
 
 struct Params {
-  CUtensorMap tmOut;  // out boxes (fp32: 32 or bf16: 64 columns, g, tpi): the epilogue TMA store
-  CUtensorMap tmQ, tmK, tmV;
-  long long* trace;  // debug timeline (CTA 0), null in production         // TMA: Q box (64, g, tpi), key/value boxes (64, 1, 64)
-  const __nv_bfloat16 *Q, *Kx, *Vx;  // keys/values: K,V [N][h_K][128] or pooled [b][h_K][128]
-  float *out, *lse, *scores;  // out: fp32, or bf16 when out_bf16
-  int out_bf16;
+  CUtensorMap tmOut;  // out boxes (fp32, 32 columns x g x tpi): the epilogue TMA store
+  CUtensorMap tmQ, tmK, tmV;  // TMA: Q box (64, g, tpi), key/value boxes (64, 1, 64)
+  long long* trace;  // debug timeline (CTA 0), null in production
+  // keys bf16, values the fp16 staged copy (SCORES: the V slot holds K_cmp's
+  // bf16 low part): K,V [N][h_K][128] or pooled [b][h_K][128]
+  const __nv_bfloat16 *Q, *Kx;
+  const void* Vx;
+  const float* vscale;  // [h_K] power-of-two scale of the fp16 values
+  float *out, *lse, *scores;
   int64_t N, h, h_K, g, W, B_K, b, n_keys, n_super;
   int tpi, mode;
   float scale, scale_log2;
@@ -424,10 +429,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
           const float e1 = ex2(fmaf(sv[cc + 1], p.scale_log2, -mb));
           l0 += e0;
           l1 += e1;
-          pk[cc >> 1] = pack_bf16(e0, e1);
+          pk[cc >> 1] = pack_f16(e0, e1);
         }
         l += l0 + l1;
-        tmem_st32u(tS, pk);  // P over S: bf16 pairs, K-packed
+        tmem_st32u(tS, pk);  // P over S: fp16 pairs, K-packed
         tmem_wait_st_();
         tc_fence_before();
         mbar_arrive(bar(B_PF + 2 * w + v));
@@ -441,37 +446,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
       if (r == 0) QO_TRACE(w, u - 1, 5);  // O complete
       tc_fence_after();
       const bool write = ok && l > 0.f;
-      const float inv = write ? 1.f / l : 0.f;
+      const float inv = write ? 1.f / (l * __ldg(p.vscale + c.it.kh)) : 0.f;
       // Rows leave by TMA store: staged in this warpgroup's consumed Q
       // sub-tile (32 KB) as two SW128 boxes of 32 fp32 columns x (g heads x
       // tpi tokens) at a time -- instead of 16-byte scattered per-thread
       // stores.  Rows without a visible key are stored as 0 (the compressed
       // branch's pending tokens are written after this kernel).
       unsigned char* qsub = smem + kOffQ + ((c.seq & 1) * 2 + w) * kQ;
-      if (p.out_bf16) {  // bf16 rows: both 64-column boxes fit the Q sub-tile at once
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          float ov[32];
-          tmem_ld32(tmem + lb + 128u + q * 32, ov);
-          tmem_wait_ld();
-          unsigned char* box = qsub + (q >> 1) * 16384u;
-#pragma unroll
-          for (int cc = 0; cc < 4; ++cc)
-            *reinterpret_cast<uint4*>(box + sw128_off(r, (q & 1) * 4 + cc)) =
-                make_uint4(pack_bf16(ov[8 * cc] * inv, ov[8 * cc + 1] * inv),
-                           pack_bf16(ov[8 * cc + 2] * inv, ov[8 * cc + 3] * inv),
-                           pack_bf16(ov[8 * cc + 4] * inv, ov[8 * cc + 5] * inv),
-                           pack_bf16(ov[8 * cc + 6] * inv, ov[8 * cc + 7] * inv));
-        }
-        fence_proxy_async();
-        named_bar(1 + w, 128);
-        if (r == 0) {
-#pragma unroll
-          for (int hf = 0; hf < 2; ++hf)
-            tma_store_3d(&p.tmOut, hf * 64, c.it.kh * (int)p.g, s.t0, smem_u32(qsub) + hf * 16384u);
-          bulk_commit();
-        }
-      } else {
 #pragma unroll
       for (int pass = 0; pass < 2; ++pass) {
         if (pass == 1) {
@@ -500,7 +481,6 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
                          smem_u32(qsub) + qq * 16384u);
           bulk_commit();
         }
-      }
       }
       if (r == 0) {
         bulk_wait_read();
@@ -535,17 +515,12 @@ int launch(Params& p, cudaStream_t st) {
   int rc = make_tmap_tokens(&p.tmQ, p.Q, p.N, p.h, (int)p.g, p.tpi);
   if (!rc) rc = make_tmap_tokens(&p.tmK, p.Kx, p.n_keys, p.h_K, 1, 64);
   if (!rc) rc = make_tmap_tokens(&p.tmV, p.Vx, p.n_keys, p.h_K, 1, 64);
-  if (!rc && p.out)
-    rc = p.out_bf16 ? make_tmap_tokens(&p.tmOut, p.out, p.N, p.h, (int)p.g, p.tpi)
-                    : make_tmap_tokens_f32(&p.tmOut, p.out, p.N, p.h, (int)p.g, p.tpi);
+  if (!rc && p.out) rc = make_tmap_tokens_f32(&p.tmOut, p.out, p.N, p.h, (int)p.g, p.tpi);
   if (rc) return rc;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(tc_qo_fwd_kernel<SLIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-    cudaFuncSetAttribute(tc_qo_fwd_kernel<CMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-    cudaFuncSetAttribute(tc_qo_fwd_kernel<SCORES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-    attr = true;
-  }
+  static unsigned long long done[3] = {0, 0, 0};
+  ensure_smem_attr(tc_qo_fwd_kernel<SLIDE>, (int)kSmemBytes, done[0]);
+  ensure_smem_attr(tc_qo_fwd_kernel<CMP>, (int)kSmemBytes, done[1]);
+  ensure_smem_attr(tc_qo_fwd_kernel<SCORES>, (int)kSmemBytes, done[2]);
   int64_t items = p.h_K * p.n_super;
   int grid = num_sms();
   if (items < grid) grid = (int)items;
@@ -628,14 +603,16 @@ bool tc_cmp_scores_fused(const fsa_shape& s) {
 }
 bool tc_cmp_scores_any_g() { return true; }
 
-int tc_slide_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V, void* out,
-                 void* lse, cudaStream_t st, int out_bf16) {
+int tc_slide_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V16,
+                 const float* vscale, void* out, void* lse, cudaStream_t st) {
+  FSA_REQUIRE(vscale != nullptr, "slide_fwd: the tensor-core path takes the fp16 V copy and its "
+              "scales (fsa_v_to_f16)");
   Params p = base_params(s);
   p.mode = SLIDE;
-  p.out_bf16 = out_bf16;
   p.Q = (const __nv_bfloat16*)Q;
   p.Kx = (const __nv_bfloat16*)K;
-  p.Vx = (const __nv_bfloat16*)V;
+  p.Vx = V16;
+  p.vscale = vscale;
   p.n_keys = s->N;
   p.out = (float*)out;
   p.lse = (float*)lse;
@@ -646,24 +623,26 @@ int tc_slide_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V
 }
 
 size_t tc_cmp_workspace_bytes(const fsa_shape* s) {
-  // bf16 pooled K/V, then the group-summed queries as bf16 hi/lo pairs
+  // bf16 pooled K, fp16 (scaled) pooled V, the group-summed queries as bf16
+  // hi/lo pairs, then the pooled V's per-head scales (+ scratch)
   return (size_t)2 * (s->N / s->B_K) * s->h_K * kD * sizeof(__nv_bfloat16) +
-         (size_t)2 * s->N * s->h_K * kD * sizeof(__nv_bfloat16);
+         (size_t)2 * s->N * s->h_K * kD * sizeof(__nv_bfloat16) + 2 * s->h_K * sizeof(float);
 }
 
 int tc_cmp_fwd(const fsa_shape* s, const void* Q, const void* Kc, const void* Vc, void* out,
-               void* lse, void* scores, void* workspace, cudaStream_t st, int out_bf16) {
+               void* lse, void* scores, void* workspace, cudaStream_t st) {
   Params p = base_params(s);
   p.mode = CMP;
-  p.out_bf16 = out_bf16;
   const int64_t n = p.b * p.h_K * kD;
   __nv_bfloat16* kb = (__nv_bfloat16*)workspace;
   __nv_bfloat16* vb = kb + n;
+  float* vsc = reinterpret_cast<float*>(vb + n + 2 * p.N * p.h_K * kD);
   to_bf16_kernel<<<148, 256, 0, st>>>((const float*)Kc, kb, n);
-  to_bf16_kernel<<<148, 256, 0, st>>>((const float*)Vc, vb, n);
+  if (int rc = stage_f16(FSA_DT_F32, Vc, p.b, p.h_K, kD, vb, vsc, st)) return rc;
   p.Q = (const __nv_bfloat16*)Q;
   p.Kx = kb;
   p.Vx = vb;
+  p.vscale = vsc;
   p.n_keys = p.b;
   p.out = (float*)out;
   p.lse = (float*)lse;

@@ -12,7 +12,8 @@
 //   dV^T += dO^T P       M128(d) N64 K128(rows)  TMEM accumulator
 //   dK^T += Q^T dS       M128(d) N64 K128(rows)  TMEM accumulator
 //   dQ_i  = dS K         M128 N128 K64  -> TMEM stage s (over the consumed S/dP)
-//                                        -> bf16 partial row of dq_buf
+//                                        -> fp16 partial row of dq_buf with a
+//                                           per-row power-of-two exponent
 // dQ partials are summed over the token's selected blocks in ascending block
 // order by the dq_reduce kernel (kv_major.py:326-340).
 //
@@ -71,13 +72,14 @@ constexpr uint32_t kIdQ = idesc_bf16(128, 128, false, true);  // dQ
 
 struct Params {
   CUtensorMap tmQ, tmO, tmK, tmV;  // sliding / compressed modes: TMA token boxes
-  CUtensorMap tmDQ;                 // dq partial rows [h N T][128] (scatter4 stores)
+  CUtensorMap tmDQ;                 // dq partial rows [h N T][128] fp16 (scatter4 stores)
   long long* trace;  // debug timeline (CTA 0, first 256 items), null in production
   const __nv_bfloat16 *Q, *K, *V, *dO;
   const float *lse, *delta;
   const int32_t *offsets, *qlist;
   int32_t* counter;
-  __nv_bfloat16* dq;  // [h][N][T][128]
+  __half* dq;         // [h][N][T][128] fp16 rows (FSA_DT_F16R) ...
+  int8_t* dqe;        // ... and their exponents [h][N][T]: value = row * 2^-e
   float *dK, *dV;     // [N][h_K][128]
   int64_t N, h, h_K, T, b, g, ntask;
   int64_t W;   // sliding mode: window; T is then the number of window slots
@@ -635,7 +637,20 @@ __global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const _
         // rows -> SW128 staging tile [2 halves][128 rows][128 B] in this wg's
         // consumed P (half 0) and dS (half 1) buffers, then 4-row tile::scatter4
         // stores to the rows' dq partial slots (TMA: no LSU queue, so the next
-        // item's loads are not stuck behind 32 KB of stores)
+        // item's loads are not stuck behind 32 KB of stores).  fp16 with a
+        // per-row power-of-two scale (row max -> [2^14, 2^15)): 11-bit rows at
+        // the bf16 rows' traffic; the first pass over TMEM finds the row max.
+        float amax = 0.f;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float v[32];
+          tmem_ld32(tmem + lb + 128u * tm + q * 32, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int c = 0; c < 32; ++c) amax = fmaxf(amax, fabsf(v[c]));
+        }
+        const int ex = f16_row_exp(amax * p.scale);
+        const float mul = ldexpf(p.scale, ex);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           float v[32];
@@ -644,13 +659,14 @@ __global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const _
           unsigned char* half = q < 2 ? prow : drw;
 #pragma unroll
           for (int c4 = 0; c4 < 4; ++c4) {
-            const uint4 u = make_uint4(pack_bf16(v[8 * c4] * p.scale, v[8 * c4 + 1] * p.scale),
-                                       pack_bf16(v[8 * c4 + 2] * p.scale, v[8 * c4 + 3] * p.scale),
-                                       pack_bf16(v[8 * c4 + 4] * p.scale, v[8 * c4 + 5] * p.scale),
-                                       pack_bf16(v[8 * c4 + 6] * p.scale, v[8 * c4 + 7] * p.scale));
+            const uint4 u = make_uint4(pack_f16(v[8 * c4] * mul, v[8 * c4 + 1] * mul),
+                                       pack_f16(v[8 * c4 + 2] * mul, v[8 * c4 + 3] * mul),
+                                       pack_f16(v[8 * c4 + 4] * mul, v[8 * c4 + 5] * mul),
+                                       pack_f16(v[8 * c4 + 6] * mul, v[8 * c4 + 7] * mul));
             *reinterpret_cast<uint4*>(half + sw128_off(r, (q & 1) * 4 + c4)) = u;
           }
         }
+        if (drow >= 0) p.dqe[drow] = (int8_t)ex;
         tc_fence_before();
         mbar_arrive(bar(B_SDE + tm));  // TMEM stage free for S/dP of item n+3
         if (r == 0) K8_TRACE(n, 6);  // dQ read out of TMEM
@@ -704,7 +720,8 @@ Params make_params(const fsa_shape* s, const void* Q, const void* K, const void*
   p.dO = (const __nv_bfloat16*)dOut;
   p.lse = (const float*)lse;
   p.delta = (const float*)delta;
-  p.dq = (__nv_bfloat16*)dq_buf;
+  p.dq = (__half*)dq_buf;
+  p.dqe = dq_buf ? reinterpret_cast<int8_t*>(p.dq + s->h * s->N * s->T * kD) : nullptr;
   p.dK = (float*)dK;
   p.dV = (float*)dV;
   p.N = s->N;
@@ -723,13 +740,10 @@ Params make_params(const fsa_shape* s, const void* Q, const void* K, const void*
 
 int launch_bwd(Params& p, cudaStream_t st) {
   cudaMemsetAsync(p.counter, 0, sizeof(int32_t), st);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(tc_sel_bwd_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-    cudaFuncSetAttribute(tc_sel_bwd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-    cudaFuncSetAttribute(tc_sel_bwd_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-    attr = true;
-  }
+  static unsigned long long done[3] = {0, 0, 0};
+  ensure_smem_attr(tc_sel_bwd_kernel<0>, (int)kSmemBytes, done[0]);
+  ensure_smem_attr(tc_sel_bwd_kernel<1>, (int)kSmemBytes, done[1]);
+  ensure_smem_attr(tc_sel_bwd_kernel<2>, (int)kSmemBytes, done[2]);
   if (p.slide == 1)
     tc_sel_bwd_kernel<1><<<num_sms(), threads_of<1>(), kSmemBytes, st>>>(p);
   else if (p.slide == 2)
@@ -747,7 +761,8 @@ int tc_sel_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V, 
                const int32_t* work, void* dq_buf, int dqbuf_dtype, void* dK, void* dV,
                cudaStream_t st) {
   FSA_REQUIRE(work != nullptr, "tensor-core backward needs the inverse work buffer");
-  FSA_REQUIRE(dqbuf_dtype == FSA_DT_BF16, "tensor-core backward writes bf16 dq partials");
+  FSA_REQUIRE(dqbuf_dtype == FSA_DT_F16R,
+              "tensor-core backward writes fp16 dq partials with row exponents (FSA_DT_F16R)");
   Params p = make_params(s, Q, K, V, dOut, lse, delta, dq_buf, dK, dV);
   p.offsets = offsets;
   p.qlist = qlist;
@@ -780,8 +795,8 @@ int tc_slide_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V
   if (rc) return rc;
   rc = launch_bwd(p, st);
   if (rc) return rc;
-  // mode 1: dQ +=; mode 2: dQ written (fp32); mode 3: dQ written as bf16
-  return tc_slide_dq(s, Q, K, V, dOut, lse, delta, dQ, accumulate == 1, st, accumulate == 3);
+  // mode 1: dQ +=; mode 2: dQ written (fp32)
+  return tc_slide_dq(s, Q, K, V, dOut, lse, delta, dQ, accumulate == 1, st);
 }
 
 // Compressed-branch dK_cmp / dV_cmp: the same kernel with

@@ -1,8 +1,10 @@
 // FSA selected-attention forward on tcgen05 tensor cores (K5), bf16, d = 128,
 // B_K = 64.  Replaces kv_major.py:152-204 / _core.pyx:49-94 for the
 // BASELINE.json shapes, in the fused LOCAL mode: per gathered
-// (token, head) row it writes O_i / l_i (bf16) and (m_i, l_i) for block i into
-// the slot-indexed partial buffer that the merge kernel (K6) combines.
+// (token, head) row it writes O_i / l_i (fp16, in the V16 scale) and (m_i, l_i)
+// for block i into the slot-indexed partial buffer that the merge kernel (K6)
+// combines.  S = Q K^T runs in bf16; O = P V in fp16 against the scaled fp16
+// copy of V (f16_stage.cu), so P is rounded to 11 bits instead of 8.
 //
 // Persistent, warp-specialised, one CTA per SM:
 //   warps 0-7  two softmax + epilogue warpgroups ping-ponging over items, one
@@ -11,8 +13,8 @@
 //   warps 8-11 loaders: cp.async gather of an item's 128 query rows (TPI
 //              tokens x g group heads); one item's gather stays in flight while
 //              the next is issued (4 Q stages); K_i/V_i per task (2 stages)
-//   warp  12   MMA issuer (one elected lane): S = Q K^T (M128 N64 K128) and
-//              O = P V (M128 N128 K64) into TMEM, tcgen05.commit -> mbarriers;
+//   warp  12   MMA issuer (one elected lane): S = Q K^T (M128 N64 K128, bf16)
+//              and O = P V (M128 N128 K64, fp16) into TMEM, tcgen05.commit;
 //              S of item n+1 is issued before PV of item n
 // Tasks (kv head, block) are claimed dynamically in head-major order
 // (tc_sched.cuh), so the gathered Q rows of the current kv group stay in L2.
@@ -44,14 +46,15 @@ constexpr uint32_t kSmemBytes = kOffTmem + 16 + 1024;
 
 constexpr uint32_t kColP = 384;  // TMEM: S[2] 0..127, O[2] 128..383, P[2] 384..447
 constexpr uint32_t kIdescS = idesc_bf16(128, 64, false, false);
-constexpr uint32_t kIdescPV = idesc_bf16(128, 128, false, true);
+constexpr uint32_t kIdescPV = idesc_f16(128, 128, false, true);  // P, V16 in fp16
 
 struct Params {
-  CUtensorMap tmO;  // obuf rows [h N T][128] bf16 (tile::scatter4 stores)
-  const __nv_bfloat16 *Q, *K, *V;
+  CUtensorMap tmO;  // obuf rows [h N T][128] fp16 (tile::scatter4 stores)
+  const __nv_bfloat16 *Q, *K;
+  const __half* V;  // the scaled fp16 copy (fsa_v_to_f16)
   const int32_t *offsets, *qlist;
   int32_t* counter;
-  __nv_bfloat16* obuf;
+  __half* obuf;
   float* ml;
   int N, h, h_K, T, b, g, ntask, tpi;
   FastDiv fdT;  // entry -> token (entries are t * T + slot)
@@ -118,8 +121,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
       mbar_wait(bar(B_KVE + kvs), (uint32_t)(((kseq >> 1) & 1) ^ 1));
       {  // warps 4,5: K rows 0-31, 32-63; warps 6,7: V rows 0-31, 32-63
         const int lw = warp - 8, row0 = (lw & 1) * 32;
-        const __nv_bfloat16* src =
-            (lw < 2 ? p.K : p.V) + ((int)(tr.i * kBK + row0 + lane) * p.h_K + (int)tr.kh) * kD;
+        const int64_t off = ((int64_t)(tr.i * kBK + row0 + lane) * p.h_K + tr.kh) * kD;
+        const void* src = lw < 2 ? (const void*)(p.K + off) : (const void*)(p.V + off);
         warp_gather_rows32(sb + kOffKV + kvs * kKVBytes + (lw < 2 ? 0u : 16384u), 8192u, row0, src,
                            true, lane);
         asm volatile("cp.async.commit_group;" ::: "memory");
@@ -297,10 +300,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
           tmem_wait_ld();
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            const uint4 v4 = make_uint4(pack_bf16(ov[8 * c] * inv, ov[8 * c + 1] * inv),
-                                        pack_bf16(ov[8 * c + 2] * inv, ov[8 * c + 3] * inv),
-                                        pack_bf16(ov[8 * c + 4] * inv, ov[8 * c + 5] * inv),
-                                        pack_bf16(ov[8 * c + 6] * inv, ov[8 * c + 7] * inv));
+            const uint4 v4 = make_uint4(pack_f16(ov[8 * c] * inv, ov[8 * c + 1] * inv),
+                                        pack_f16(ov[8 * c + 2] * inv, ov[8 * c + 3] * inv),
+                                        pack_f16(ov[8 * c + 4] * inv, ov[8 * c + 5] * inv),
+                                        pack_f16(ov[8 * c + 6] * inv, ov[8 * c + 7] * inv));
             *reinterpret_cast<uint4*>(st + sw128_off(lane, qq * 4 + c)) = v4;
           }
         }
@@ -369,7 +372,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
             const float e1 = ex2(fmaf(sv[c2 + 1], p.scale_log2, -mb));
             sum += e0;
             s2 += e1;
-            pk[c2 >> 1] = pack_bf16(e0, e1);
+            pk[c2 >> 1] = pack_f16(e0, e1);
           }
         } else {
 #pragma unroll
@@ -382,12 +385,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
             const float e1 = c2 + 1 < vis ? ex2(fmaf(sv[c2 + 1], p.scale_log2, -mb)) : 0.f;
             sum += e0;
             s2 += e1;
-            pk[c2 >> 1] = pack_bf16(e0, e1);
+            pk[c2 >> 1] = pack_f16(e0, e1);
           }
         }
         sum += s2;
         mbar_wait(bar(B_PE + s), (uint32_t)(((n >> 1) & 1) ^ 1));
-        tmem_st32u(tmem + lane_base + kColP + s * 32, pk);  // bf16 pairs, K-packed
+        tmem_st32u(tmem + lane_base + kColP + s * 32, pk);  // fp16 pairs, K-packed
         tmem_wait_st_();
         tc_fence_before();
         mbar_arrive(bar(B_PF + s));
@@ -413,15 +416,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
 
 }  // namespace
 
-int num_sms() {
-  static int cached = 0;
-  if (!cached) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
-    if (cached <= 0) cached = 148;
-  }
-  return cached;
+int num_sms() {  // of the current device (a process may drive several)
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
 }
 
 bool tc_fwd_supported(const fsa_shape& s, int dtype) {
@@ -436,10 +435,10 @@ int tc_sel_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V,
   Params p{};
   p.Q = (const __nv_bfloat16*)Q;
   p.K = (const __nv_bfloat16*)K;
-  p.V = (const __nv_bfloat16*)V;
+  p.V = (const __half*)V;
   p.offsets = offsets;
   p.qlist = qlist;
-  p.obuf = (__nv_bfloat16*)obuf;
+  p.obuf = (__half*)obuf;
   p.ml = (float*)ml;
   p.N = (int)s->N;
   p.h = (int)s->h;
@@ -455,12 +454,8 @@ int tc_sel_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V,
   p.counter = const_cast<int32_t*>(work) + p.ntask + 1;
   if (int rc = make_tmap_rows(&p.tmO, obuf, s->h * s->N * s->T, 1)) return rc;
   cudaMemsetAsync(p.counter, 0, sizeof(int32_t), st);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(tc_sel_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kSmemBytes);
-    attr = true;
-  }
+  static unsigned long long done = 0;
+  ensure_smem_attr(tc_sel_fwd_kernel, (int)kSmemBytes, done);
   tc_sel_fwd_kernel<<<num_sms(), kThreads, kSmemBytes, st>>>(p);
   FSA_LAUNCH_CHECK("tc_sel_fwd");
   return FSA_OK;

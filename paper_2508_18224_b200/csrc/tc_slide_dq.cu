@@ -48,7 +48,6 @@ struct Params {
   float* dQ;  // [N][h][128]
   int64_t N, h, h_K, g, W, n_super;
   int tpi, accumulate;
-  int out_bf16;    // dQ written as bf16 (the NSA step's hand-off to the dQ reduce)
   int cmp;         // compressed mode: keys = pooled rows of K_cmp / V_cmp (bf16), row j
   int64_t cmpBK;   // visible to token t iff j < (t + 1) / B_K (branches.py:47-78)
   float scale, scale_log2;
@@ -323,41 +322,23 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const __grid_c
         float ov[32];
         tmem_ld32(tmem + lb + 128u + q * 32, ov);
         tmem_wait_ld();
-        if (p.out_bf16) {  // bf16: two 64-column boxes in the Q sub-tile
-          unsigned char* box = smem + kOffQ + w * kT + (q >> 1) * 16384u;
+        unsigned char* box = smem + kOffQ + (q < 2 ? w : 2 + w) * kT + (q & 1) * 16384u;
 #pragma unroll
-          for (int cc = 0; cc < 4; ++cc)
-            *reinterpret_cast<uint4*>(box + sw128_off(r, (q & 1) * 4 + cc)) =
-                make_uint4(pack_bf16(ov[8 * cc] * p.scale, ov[8 * cc + 1] * p.scale),
-                           pack_bf16(ov[8 * cc + 2] * p.scale, ov[8 * cc + 3] * p.scale),
-                           pack_bf16(ov[8 * cc + 4] * p.scale, ov[8 * cc + 5] * p.scale),
-                           pack_bf16(ov[8 * cc + 6] * p.scale, ov[8 * cc + 7] * p.scale));
-        } else {
-          unsigned char* box = smem + kOffQ + (q < 2 ? w : 2 + w) * kT + (q & 1) * 16384u;
-#pragma unroll
-          for (int cc = 0; cc < 8; ++cc)
-            *reinterpret_cast<float4*>(box + sw128_off(r, cc)) =
-                make_float4(ov[4 * cc] * p.scale, ov[4 * cc + 1] * p.scale, ov[4 * cc + 2] * p.scale,
-                            ov[4 * cc + 3] * p.scale);
-        }
+        for (int cc = 0; cc < 8; ++cc)
+          *reinterpret_cast<float4*>(box + sw128_off(r, cc)) =
+              make_float4(ov[4 * cc] * p.scale, ov[4 * cc + 1] * p.scale, ov[4 * cc + 2] * p.scale,
+                          ov[4 * cc + 3] * p.scale);
       }
       fence_proxy_async();
       named_bar(1 + w, 128);
       if (r == 0) {
-        if (p.out_bf16) {
 #pragma unroll
-          for (int hf = 0; hf < 2; ++hf)
-            tma_store_3d(&p.tmDQ, hf * 64, c.it.kh * (int)p.g, s.t0,
-                         sb + kOffQ + w * kT + hf * 16384u);
-        } else {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const uint32_t box = sb + kOffQ + (q < 2 ? w : 2 + w) * kT + (q & 1) * 16384u;
-            if (p.accumulate)
-              tma_reduce_add_3d(&p.tmDQ, q * 32, c.it.kh * (int)p.g, s.t0, box);
-            else
-              tma_store_3d(&p.tmDQ, q * 32, c.it.kh * (int)p.g, s.t0, box);
-          }
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t box = sb + kOffQ + (q < 2 ? w : 2 + w) * kT + (q & 1) * 16384u;
+          if (p.accumulate)
+            tma_reduce_add_3d(&p.tmDQ, q * 32, c.it.kh * (int)p.g, s.t0, box);
+          else
+            tma_store_3d(&p.tmDQ, q * 32, c.it.kh * (int)p.g, s.t0, box);
         }
         bulk_commit();
         bulk_wait_read();
@@ -382,10 +363,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const __grid_c
 
 long long* g_dq_trace = nullptr;
 int tc_slide_dq(const fsa_shape* s, const void* Q, const void* K, const void* V, const void* dOut,
-                const void* lse, const void* delta, void* dQ, int accumulate, cudaStream_t st,
-                int out_bf16) {
+                const void* lse, const void* delta, void* dQ, int accumulate, cudaStream_t st) {
   Params p{};
-  p.out_bf16 = out_bf16;
   p.trace = g_dq_trace;
   p.Q = (const __nv_bfloat16*)Q;
   p.K = (const __nv_bfloat16*)K;
@@ -408,16 +387,10 @@ int tc_slide_dq(const fsa_shape* s, const void* Q, const void* K, const void* V,
   if (!rc) rc = make_tmap_tokens(&p.tmO, dOut, p.N, p.h, (int)p.g, p.tpi);
   if (!rc) rc = make_tmap_tokens(&p.tmK, K, p.N, p.h_K, 1, 64);
   if (!rc) rc = make_tmap_tokens(&p.tmV, V, p.N, p.h_K, 1, 64);
-  if (!rc)
-    rc = out_bf16 ? make_tmap_tokens(&p.tmDQ, dQ, p.N, p.h, (int)p.g, p.tpi)
-                  : make_tmap_tokens_f32(&p.tmDQ, dQ, p.N, p.h, (int)p.g, p.tpi);
+  if (!rc) rc = make_tmap_tokens_f32(&p.tmDQ, dQ, p.N, p.h, (int)p.g, p.tpi);
   if (rc) return rc;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(tc_slide_dq_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kSmemBytes);
-    attr = true;
-  }
+  static unsigned long long done = 0;
+  ensure_smem_attr(tc_slide_dq_kernel<0>, (int)kSmemBytes, done);
   int64_t items = p.h_K * p.n_super;
   int grid = num_sms();
   if (items < grid) grid = (int)items;
@@ -458,7 +431,8 @@ int tc_cmp_dq(const fsa_shape* s, const void* Q, const void* Kb, const void* Vb,
   if (!rc) rc = make_tmap_tokens(&p.tmV, Vb, b, p.h_K, 1, 64);
   if (!rc) rc = make_tmap_tokens_f32(&p.tmDQ, dQ, p.N, p.h, (int)p.g, p.tpi);
   if (rc) return rc;
-  cudaFuncSetAttribute(tc_slide_dq_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+  static unsigned long long done = 0;
+  ensure_smem_attr(tc_slide_dq_kernel<1>, (int)kSmemBytes, done);
   int64_t items = p.h_K * p.n_super;
   int grid = num_sms();
   if (items < grid) grid = (int)items;

@@ -100,18 +100,24 @@ def _intake(cfg, Q, K, V=None, dOut=None):
     return dt, q, k, v, do
 
 
-def _sel_partials(cfg, dt, q, k, v, inv):
-    """K5 in LOCAL mode: slot-indexed partials O_i / l_i and (m_i, l_i)."""
+def _sel_partials(cfg, dt, q, k, v, inv, v16=None):
+    """K5 in LOCAL mode: slot-indexed partials O_i / l_i and (m_i, l_i).
+    On the tensor-core path (fp16 obuf) V is read as its scaled fp16 copy
+    (``v16 = (V16, vscale)`` from fsa_v_to_f16, made here when not given).
+    Returns (obuf, ml, obuf code, vscale or None)."""
     dev = q.device
     acc = _lib.acc_dtype(dt)
     (ob_code, ob_dtype), _ = _lib.buffer_dtypes(cfg, dt)
+    vscale = None
+    if ob_code == _lib.DT_F16:
+        v, vscale = v16 if v16 is not None else _lib.v_to_f16(cfg, v)
     obuf = torch.empty((cfg.h, cfg.N, cfg.T, cfg.d_V), dtype=ob_dtype, device=dev)
     ml = torch.empty((cfg.h, cfg.N, cfg.T, 2), dtype=acc, device=dev)
     s = _lib.shape_of(cfg)
     _lib.call("fsa_sel_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.FWD_LOCAL, _lib.ptr(q),
               _lib.ptr(k), _lib.ptr(v), _lib.ptr(inv.offsets), _lib.ptr(inv.qlist), _lib.ptr(inv.work),
               None, _lib.ptr(obuf), ob_code, _lib.ptr(ml), _lib.stream())
-    return obuf, ml, ob_code
+    return obuf, ml, ob_code, vscale
 
 
 def _fused_forward(cfg, dt, q, k, v, sel, inv):
@@ -119,14 +125,14 @@ def _fused_forward(cfg, dt, q, k, v, sel, inv):
     (h, N), both in the accumulator dtype (f32 for bf16 inputs)."""
     dev = q.device
     acc = _lib.acc_dtype(dt)
-    obuf, ml, ob_code = _sel_partials(cfg, dt, q, k, v, inv)
+    obuf, ml, ob_code, vscale = _sel_partials(cfg, dt, q, k, v, inv)
     s = _lib.shape_of(cfg)
     st = _lib.stream()
     out = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=acc, device=dev)
     lse = torch.empty((cfg.h, cfg.N), dtype=acc, device=dev)
     _lib.call("fsa_merge_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.MERGE_LOCAL,
               _lib.ptr(sel.idx), _lib.ptr(obuf), ob_code, _lib.ptr(ml), None, None, _lib.ptr(out),
-              _lib.ptr(lse), None, None, 0, st)
+              _lib.ptr(lse), None, None, 0, _lib.ptr(vscale), st)
     return out, lse
 
 
@@ -152,7 +158,7 @@ def compute_softmax_stats(Q, K, sel: SelectionTensor, cfg, *, shared_max: bool =
     l = torch.empty_like(m)
     _lib.call("fsa_merge_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.MERGE_STATS,
               _lib.ptr(sel.idx), None, acc_code, _lib.ptr(ml), None, None, None, None, _lib.ptr(m),
-              _lib.ptr(l), int(bool(shared_max)), st)
+              _lib.ptr(l), int(bool(shared_max)), None, st)
     if meter is not None:
         meter_stats(meter, inv.n_valid, cfg)
     return SoftmaxStats(m=m, l=l)
@@ -203,7 +209,7 @@ def reduce_forward(buf: OutputBuffer, inv: InverseIndex, stats: SoftmaxStats, cf
     s = _lib.shape_of(cfg)
     _lib.call("fsa_merge_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.MERGE_REDUCE,
               _lib.ptr(sel_idx), _lib.ptr(data), _lib.dt_code(acc), None, _lib.ptr(mg),
-              _lib.ptr(lg), _lib.ptr(out), _lib.ptr(lse), None, None, 0, _lib.stream())
+              _lib.ptr(lg), _lib.ptr(out), _lib.ptr(lse), None, None, 0, None, _lib.stream())
     if meter is not None:
         meter_reduce(meter, nv, cfg)
     return AttentionOutput(out=logical(out), lse=lse)
@@ -243,7 +249,7 @@ def _backward_core(cfg, dt, q, k, v, do, sel, inv, out, lse, delta=None):
         _lib.call("fsa_bwd_delta", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(out), _lib.ptr(do),
                   _lib.ptr(delta), st)
     _, (dq_code, dq_dtype) = _lib.buffer_dtypes(cfg, dt)
-    dq_buf = torch.empty((cfg.h, cfg.N, cfg.T, cfg.d_K), dtype=dq_dtype, device=dev)
+    dq_buf = _lib.dq_buffer(cfg, dq_code, dq_dtype, dev)
     dK = torch.empty((cfg.N, cfg.h_K, cfg.d_K), dtype=acc, device=dev)
     dV = torch.empty((cfg.N, cfg.h_K, cfg.d_V), dtype=acc, device=dev)
     _lib.call("fsa_sel_bwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(q), _lib.ptr(k),

@@ -53,11 +53,40 @@ class NSAContext:
     k_cmp: torch.Tensor = None
     v_cmp: torch.Tensor = None
     lse_cmp: torch.Tensor = None
-    narrow: bool = False  # out_cmp / out_slide / out_sel in bf16 (FSA_OUT_NARROW)
+
+
+def _check(x, name, shape, dtype, dev):
+    """Storage-layout intake of the step (the device path reads raw pointers):
+    the reference's shape message (config.py:149-154), one dtype, one device,
+    contiguous storage.  No host synchronisation."""
+    if not isinstance(x, torch.Tensor):
+        raise TypeError(f"{name} must be a torch tensor on the device")
+    if tuple(x.shape) != tuple(shape):
+        raise ValueError(f"shape mismatch for {name}: expected {tuple(shape)}, got {tuple(x.shape)}")
+    if x.dtype != dtype:
+        raise ValueError(f"{name} has dtype {x.dtype}; the step runs in {dtype} (all of Q, K, V, dOut)")
+    if x.device != dev:
+        raise ValueError(f"{name} is on {x.device}, Q on {dev}")
+    if not x.is_contiguous():
+        raise ValueError(f"{name} must be contiguous storage ({', '.join(map(str, shape))}); "
+                         "use the operator API for logical (N, d, h) views")
+
+
+def _gates(tau, cfg, acc, dev):
+    """tau (N, 3) in the accumulator dtype, contiguous (a bf16 tau is cast)."""
+    if not isinstance(tau, torch.Tensor) or tuple(tau.shape) != (cfg.N, 3):
+        shp = tuple(tau.shape) if hasattr(tau, "shape") else type(tau).__name__
+        raise ValueError(f"shape mismatch for gates: expected {(cfg.N, 3)}, got {shp}")
+    if tau.device != dev:
+        raise ValueError(f"gates are on {tau.device}, Q on {dev}")
+    return tau.to(acc).contiguous()
 
 
 def nsa_forward(q, k, v, tau, cfg, *, heads=None):
     """Returns (combined out (N, h, d_V), ctx).
+
+    Storage-layout inputs: q (N, h, d_K), k (N, h_K, d_K), v (N, h_K, d_V), one
+    dtype, contiguous, on the device; tau (N, 3) (cast to the accumulator dtype).
 
     ``heads=(lo, hi)``: compute only query heads lo..hi-1 of every kv group
     (the query-head split of parallel.shard_plan).  The compressed branch and
@@ -68,16 +97,15 @@ def nsa_forward(q, k, v, tau, cfg, *, heads=None):
     dt = q.dtype
     acc = _lib.acc_dtype(dt)
     dev = q.device
+    _check(q, "Q", (cfg.N, cfg.h, cfg.d_K), dt, dev)
+    _check(k, "K", (cfg.N, cfg.h_K, cfg.d_K), dt, dev)
+    _check(v, "V", (cfg.N, cfg.h_K, cfg.d_V), dt, dev)
+    tau = _gates(tau, cfg, acc, dev)
     s = _lib.shape_of(cfg)
     st = _lib.stream()
-    # bf16 tensor-core path: the three branch outputs are bf16 intermediates of
-    # the bf16 combined output (half the HBM traffic in the window forward, the
-    # merge + combine and the gate backward)
-    (ob0, _), _ = _lib.buffer_dtypes(cfg, dt)
-    narrow = (dt == torch.bfloat16 and ob0 == _lib.DT_BF16 and cfg.d_K == 128 and cfg.d_V == 128
-              and cfg.T <= 32)
-    branch_dt = torch.bfloat16 if narrow else acc
-    nflag = _lib.OUT_NARROW if narrow else 0
+    (ob_code, _), _ = _lib.buffer_dtypes(cfg, dt)
+    # the tensor-core P.V products read V as its power-of-two scaled fp16 copy
+    v16 = _lib.v_to_f16(cfg, v) if ob_code == _lib.DT_F16 else None
     n_pref = min(cfg.B_K - 1, cfg.N)
     Kc = torch.empty((cfg.b, cfg.h_K, cfg.d_K), dtype=acc, device=dev)
     Vc = torch.empty((cfg.b, cfg.h_K, cfg.d_V), dtype=acc, device=dev)
@@ -85,11 +113,11 @@ def nsa_forward(q, k, v, tau, cfg, *, heads=None):
     Vp = torch.empty((max(n_pref, 1), cfg.h_K, cfg.d_V), dtype=acc, device=dev)
     _lib.call("fsa_compress_kv", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(k), _lib.ptr(v),
               _lib.ptr(Kc), _lib.ptr(Vc), _lib.ptr(Kp), _lib.ptr(Vp), st)
-    out_cmp = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=branch_dt, device=dev)
+    out_cmp = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=acc, device=dev)
     lse_cmp = torch.empty((cfg.h, cfg.N), dtype=acc, device=dev)
     scores = torch.empty((cfg.h_K, cfg.N, cfg.b), dtype=acc, device=dev)
     ws = _cmp_workspace(cfg, dev)
-    _lib.call("fsa_cmp_attn_fwd", ctypes.byref(s), _lib.dt_code(dt) | nflag, _lib.ptr(q), _lib.ptr(Kc),
+    _lib.call("fsa_cmp_attn_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(q), _lib.ptr(Kc),
               _lib.ptr(Vc), _lib.ptr(Kp), _lib.ptr(Vp), _lib.ptr(out_cmp), _lib.ptr(lse_cmp),
               _lib.ptr(scores), _lib.ptr(ws), st)
     idx = torch.empty((cfg.h_K, cfg.N, cfg.T), dtype=torch.int32, device=dev)
@@ -117,17 +145,18 @@ def nsa_forward(q, k, v, tau, cfg, *, heads=None):
     inv = build_inverse_index(sel, cfg, validate=False)
     # K5 writes the slot partials; the sliding branch runs before the merge so
     # that K6 can apply the gated combine (K12) in the same pass
-    obuf, ml, ob_code = _sel_partials(cfg, dt, q, k, v, inv)
-    out_slide, lse_slide = _slide_fwd_storage(cfg, dt, q, k, v, narrow=narrow)
-    out_sel = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=branch_dt, device=dev)
+    obuf, ml, ob_code, vscale = _sel_partials(cfg, dt, q, k, v, inv, v16=v16)
+    out_slide, lse_slide = _slide_fwd_storage(cfg, dt, q, k, v, v16=v16)
+    out_sel = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=acc, device=dev)
     lse_sel = torch.empty((cfg.h, cfg.N), dtype=acc, device=dev)
     out = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=dt, device=dev)
-    _lib.call("fsa_merge_combine_fwd", ctypes.byref(s), _lib.dt_code(dt) | nflag, _lib.ptr(sel.idx),
-              _lib.ptr(obuf), ob_code, _lib.ptr(ml), _lib.ptr(out_cmp), _lib.ptr(out_slide),
-              _lib.ptr(tau), _lib.ptr(out_sel), _lib.ptr(lse_sel), _lib.ptr(out), st)
+    _lib.call("fsa_merge_combine_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(sel.idx),
+              _lib.ptr(obuf), ob_code, _lib.ptr(ml), _lib.ptr(vscale), _lib.ptr(out_cmp),
+              _lib.ptr(out_slide), _lib.ptr(tau), _lib.ptr(out_sel), _lib.ptr(lse_sel), _lib.ptr(out),
+              st)
     del obuf, ml
     ctx = NSAContext(cfg, dt, q, k, v, tau, sel, inv, out_sel, lse_sel, out_slide, lse_slide,
-                     out_cmp, scores, Kc, Vc, lse_cmp, narrow)
+                     out_cmp, scores, Kc, Vc, lse_cmp)
     return out, ctx
 
 
@@ -137,21 +166,23 @@ def nsa_backward(ctx: NSAContext, dout, *, full: bool = False):
     reference differentiates.  With ``full=True`` also through the compressed
     branch (attention over the pooled rows, the pooling and the prefix means;
     no reference backward -- SURVEY 8(f) rank 3) and returns
-    (dQ, dK, dV, dtau) with the gate gradient dtau (N, 3)."""
+    (dQ, dK, dV, dtau) with the gate gradient dtau (N, 3).
+    dout: (N, h, d_V) storage in the step's dtype, contiguous, on the device."""
     cfg, dt = ctx.cfg, ctx.dtype
+    _check(dout, "dOut", (cfg.N, cfg.h, cfg.d_V), dt, ctx.q.device)
     s = _lib.shape_of(cfg)
     st = _lib.stream()
     acc = _lib.acc_dtype(dt)
     delta_sel = torch.empty((cfg.h, cfg.N), dtype=acc, device=dout.device)
     delta_slide = torch.empty_like(delta_sel)
     _, (dq_code, _) = _lib.buffer_dtypes(cfg, dt)
-    if full and dq_code == _lib.DT_BF16:
+    tc = dq_code == _lib.DT_F16R
+    if full and tc:
         # tensor-core path: the gate folds into all three branches' statistics
         delta_cmp = torch.empty_like(delta_sel)
         lse_cmp, lse_sel, lse_slide = (torch.empty_like(delta_sel) for _ in range(3))
         dtau = torch.empty((cfg.N, 3), dtype=acc, device=dout.device)
-        nflag = _lib.OUT_NARROW if ctx.narrow else 0
-        _lib.call("fsa_gate_backward_full_fold", ctypes.byref(s), _lib.dt_code(dt) | nflag,
+        _lib.call("fsa_gate_backward_full_fold", ctypes.byref(s), _lib.dt_code(dt),
                   _lib.ptr(dout), _lib.ptr(ctx.tau), _lib.ptr(ctx.out_cmp), _lib.ptr(ctx.out_sel),
                   _lib.ptr(ctx.out_slide), _lib.ptr(ctx.lse_cmp), _lib.ptr(ctx.lse_sel),
                   _lib.ptr(ctx.lse_slide), _lib.ptr(delta_cmp), _lib.ptr(delta_sel),
@@ -170,8 +201,7 @@ def nsa_backward(ctx: NSAContext, dout, *, full: bool = False):
         d_cmp = torch.empty_like(dout)
         delta_cmp = torch.empty_like(delta_sel)
         dtau = torch.empty((cfg.N, 3), dtype=acc, device=dout.device)
-        nflag = _lib.OUT_NARROW if ctx.narrow else 0
-        _lib.call("fsa_gate_backward_full", ctypes.byref(s), _lib.dt_code(dt) | nflag, _lib.ptr(dout),
+        _lib.call("fsa_gate_backward_full", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(dout),
                   _lib.ptr(ctx.tau), _lib.ptr(ctx.out_cmp), _lib.ptr(ctx.out_sel),
                   _lib.ptr(ctx.out_slide), _lib.ptr(d_cmp), _lib.ptr(d_sel), _lib.ptr(d_slide),
                   _lib.ptr(delta_cmp), _lib.ptr(delta_sel), _lib.ptr(delta_slide), _lib.ptr(dtau), st)
@@ -182,13 +212,12 @@ def nsa_backward(ctx: NSAContext, dout, *, full: bool = False):
                   _lib.ptr(ctx.k_cmp), _lib.ptr(ctx.v_cmp), _lib.ptr(d_cmp), _lib.ptr(ctx.lse_cmp),
                   _lib.ptr(delta_cmp), _lib.ptr(dQ), _lib.ptr(dK), _lib.ptr(dV), _lib.ptr(ws), st)
         return dQ, dK, dV, dtau
-    if dq_code == _lib.DT_BF16:
+    if tc:
         # tensor-core path: the gate folds into the branch statistics (raw
         # dOut, lse - ln tau, delta = sum out * dOut) -- no gated dOut copies
         lse_sel = torch.empty_like(delta_sel)
         lse_slide = torch.empty_like(delta_sel)
-        nflag = _lib.OUT_NARROW if ctx.narrow else 0
-        _lib.call("fsa_gate_backward_fold", ctypes.byref(s), _lib.dt_code(dt) | nflag, _lib.ptr(dout),
+        _lib.call("fsa_gate_backward_fold", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(dout),
                   _lib.ptr(ctx.tau), _lib.ptr(ctx.out_sel), _lib.ptr(ctx.out_slide),
                   _lib.ptr(ctx.lse_sel), _lib.ptr(ctx.lse_slide), _lib.ptr(delta_sel),
                   _lib.ptr(delta_slide), _lib.ptr(lse_sel), _lib.ptr(lse_slide), st)
@@ -213,36 +242,32 @@ def _sel_slide_backward(ctx: NSAContext, d_sel, d_slide, delta_sel, delta_slide,
     acc = _lib.acc_dtype(dt)
     dout = d_sel
     _, (dq_code, dq_dtype) = _lib.buffer_dtypes(cfg, dt)
-    if dq_code != _lib.DT_BF16:  # generic (f32 / f64 / small shapes) path
+    if dq_code != _lib.DT_F16R:  # generic (f32 / f64 / small shapes) path
         dQ, dK, dV = _backward_core(cfg, dt, ctx.q, ctx.k, ctx.v, d_sel, ctx.sel, ctx.inv,
                                     ctx.out_sel, lse_sel, delta=delta_sel)
         return _slide_bwd_storage(cfg, dt, ctx.q, ctx.k, ctx.v, d_slide, ctx.out_slide,
                                   lse_slide, accumulate_into=(dQ, dK, dV), delta=delta_slide)
-    # tensor-core path: K8 (selected) writes dK/dV and the dq partials; the
-    # sliding backward adds its dK/dV in-kernel and writes its dQ rows, which
-    # the dQ reduce (K9) adds while summing the partials -- every gradient
-    # element is written once, with no read-modify-write pass over dQ
+    # tensor-core path: K8 (selected) writes dK/dV and the fp16 dq partials;
+    # the sliding backward adds its dK/dV in-kernel and writes its fp32 dQ
+    # rows, which the dQ reduce (K9) adds while summing the partials -- every
+    # gradient element is written once, with no read-modify-write pass over dQ
     dev = dout.device
     inv = ctx.inv
-    dq_buf = torch.empty((cfg.h, cfg.N, cfg.T, cfg.d_K), dtype=dq_dtype, device=dev)
+    dq_buf = _lib.dq_buffer(cfg, dq_code, dq_dtype, dev)
     dK = torch.empty((cfg.N, cfg.h_K, cfg.d_K), dtype=acc, device=dev)
     dV = torch.empty((cfg.N, cfg.h_K, cfg.d_V), dtype=acc, device=dev)
     _lib.call("fsa_sel_bwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(ctx.q), _lib.ptr(ctx.k),
               _lib.ptr(ctx.v), _lib.ptr(d_sel), _lib.ptr(lse_sel), _lib.ptr(delta_sel),
               _lib.ptr(inv.offsets), _lib.ptr(inv.qlist), _lib.ptr(inv.work), _lib.ptr(dq_buf),
               dq_code, _lib.ptr(dK), _lib.ptr(dV), st)
-    # the sliding dQ rows are handed to the reduce in bf16 with the narrow
-    # branch outputs (mode 3), else fp32 (mode 2)
-    dQ_slide = torch.empty((cfg.N, cfg.h, cfg.d_K), dtype=torch.bfloat16 if ctx.narrow else acc,
-                           device=dev)
+    dQ_slide = torch.empty((cfg.N, cfg.h, cfg.d_K), dtype=acc, device=dev)
     nws = _lib.lib().fsa_slide_bwd_workspace_bytes(ctypes.byref(s), _lib.dt_code(dt))
     ws = torch.empty(max(nws, 1), dtype=torch.uint8, device=dev)
     _lib.call("fsa_slide_bwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(ctx.q), _lib.ptr(ctx.k),
               _lib.ptr(ctx.v), _lib.ptr(d_slide), _lib.ptr(lse_slide), _lib.ptr(delta_slide),
-              _lib.ptr(dQ_slide), _lib.ptr(dK), _lib.ptr(dV), _lib.ptr(ws), 3 if ctx.narrow else 2, st)
+              _lib.ptr(dQ_slide), _lib.ptr(dK), _lib.ptr(dV), _lib.ptr(ws), 2, st)
     dQ = torch.empty((cfg.N, cfg.h, cfg.d_K), dtype=acc, device=dev)
-    _lib.call("fsa_dq_reduce_add", ctypes.byref(s),
-              _lib.dt_code(dt) | (_lib.OUT_NARROW if ctx.narrow else 0), _lib.ptr(ctx.sel.idx),
+    _lib.call("fsa_dq_reduce_add", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(ctx.sel.idx),
               _lib.ptr(dq_buf), dq_code, _lib.ptr(dQ_slide), _lib.ptr(dQ), st)
     return dQ, dK, dV
 

@@ -13,7 +13,7 @@ and KV blocks:
 * backward: dQ rows on sampled tokens, dK/dV rows of sampled KV blocks, and
   for every kv head the identity sum_s dV[s] = sum_t sum_{j in group}
   (tau1 + tau2)[t] dOut[t, j] (softmax rows sum to one).
-Tolerances as tests/gpu_util.assert_close (bf16: 2e-2, normwise).
+Tolerances as tests/gpu_util.assert_close (bf16: elementwise 2e-2 |ref| + 2e-2 RMS(ref)).
 """
 
 import numpy as np

@@ -652,18 +652,43 @@ def test_selection_vs_oracle_fp64_scores_near_ties():
         assert np.all(np.abs(s64[kh, t, diff] - s_T) <= 2 * err + 1e-12), (kh, t, diff)
 
 
-def test_narrow_flag_rejected_off_the_tensor_core_path():
-    """FSA_OUT_NARROW (bf16 branch outputs) exists only on the bf16 tensor-core
-    path: the generic f32 path refuses it with the library's error."""
+def test_tc_window_forward_requires_the_f16_value_copy():
+    """The bf16 tensor-core window forward multiplies P by the scaled fp16 copy
+    of V (fsa_v_to_f16): called without its scales it refuses with the
+    library's error instead of reading bf16 V as fp16."""
     import ctypes
 
     from paper_2508_18224_b200 import _lib
-    cfg = fsa.make_config(N=256, d_K=32, d_V=32, h=4, h_K=2, B_K=16, T=4, W=32)
+    cfg = fsa.make_config(N=256, d_K=128, d_V=128, h=4, h_K=2, B_K=64, T=2, W=64)
     s = _lib.shape_of(cfg)
-    q = torch.zeros(cfg.N, cfg.h, 32, device="cuda")
-    k = torch.zeros(cfg.N, cfg.h_K, 32, device="cuda")
-    out = torch.empty(cfg.N, cfg.h, 32, device="cuda")
+    q = torch.zeros(cfg.N, cfg.h, 128, device="cuda", dtype=torch.bfloat16)
+    k = torch.zeros(cfg.N, cfg.h_K, 128, device="cuda", dtype=torch.bfloat16)
+    out = torch.empty(cfg.N, cfg.h, 128, device="cuda")
     lse = torch.empty(cfg.h, cfg.N, device="cuda")
-    rc = _lib.lib().fsa_slide_fwd(ctypes.byref(s), _lib.DT_F32 | _lib.OUT_NARROW, _lib.ptr(q),
-                                  _lib.ptr(k), _lib.ptr(k), _lib.ptr(out), _lib.ptr(lse), None)
-    assert rc != 0 and b"narrow" in _lib.lib().fsa_last_error()
+    rc = _lib.lib().fsa_slide_fwd(ctypes.byref(s), _lib.DT_BF16, _lib.ptr(q), _lib.ptr(k),
+                                  _lib.ptr(k), None, _lib.ptr(out), _lib.ptr(lse), None)
+    assert rc != 0 and b"fsa_v_to_f16" in _lib.lib().fsa_last_error()
+
+
+def test_v_to_f16_scales_per_kv_head():
+    """fsa_v_to_f16: V16 = fp16(V * s_kh) with s_kh = 2^(15 - k), max|V_kh| = f 2^k,
+    f in [0.5, 1): every head's maximum lands in [2^14, 2^15), exactly (a bf16
+    value times a power of two is representable in fp16 in that range), also
+    for values far outside fp16's range."""
+    from paper_2508_18224_b200 import _lib
+    cfg = fsa.make_config(N=512, d_K=128, d_V=128, h=3, h_K=3, B_K=64, T=2, W=64)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    v = torch.randn(cfg.N, 3, 128, device="cuda", generator=g)
+    v[:, 1] *= 1e6     # above fp16's 65504
+    v[:, 2] *= 1e-7    # below fp16's normal range
+    v = v.to(torch.bfloat16)
+    v16, vscale = _lib.v_to_f16(cfg, v)
+    vd = v.double()
+    for kh in range(3):
+        m = float(vd[:, kh].abs().max())
+        s = float(vscale[kh])
+        assert 2.0 ** 14 <= m * s < 2.0 ** 15
+        assert s == 2.0 ** round(np.log2(s))
+        big = vd[:, kh].abs() * s >= 2.0 ** -14  # fp16 normal range: exact
+        got = v16[:, kh].double()
+        assert torch.equal(got[big], (vd[:, kh] * s)[big])

@@ -40,7 +40,7 @@ def test_library_exports_every_declared_symbol(built):
     missing = [s for s in syms if s not in exported]
     assert not missing, missing
     assert sorted(_lib.SIGNATURES) == syms
-    assert built.fsa_abi_version() == 1
+    assert built.fsa_abi_version() == 2
 
 
 def test_library_is_sm100a_only(built):

@@ -46,11 +46,12 @@ def main():
     obuf = torch.empty((cfg.h, cfg.N, cfg.T, 128), dtype=ob_dt, device="cuda")
     ml = torch.empty((cfg.h, cfg.N, cfg.T, 2), dtype=torch.float32, device="cuda")
     s = _lib.shape_of(cfg)
+    v16, vscale = _lib.v_to_f16(cfg, v)
     t5, t6 = [], []
     for it in range(a.iters + 2):
         ev[0].record()
         _lib.call("fsa_sel_fwd", ctypes.byref(s), _lib.DT_BF16, _lib.FWD_LOCAL, _lib.ptr(q), _lib.ptr(k),
-                  _lib.ptr(v), _lib.ptr(inv.offsets), _lib.ptr(inv.qlist), _lib.ptr(inv.work), None,
+                  _lib.ptr(v16), _lib.ptr(inv.offsets), _lib.ptr(inv.qlist), _lib.ptr(inv.work), None,
                   _lib.ptr(obuf), ob_code, _lib.ptr(ml), _lib.stream())
         ev[1].record()
         o2 = torch.empty((cfg.N, cfg.h, 128), dtype=torch.float32, device="cuda")
@@ -58,7 +59,7 @@ def main():
         ev[2].record()
         _lib.call("fsa_merge_fwd", ctypes.byref(s), _lib.DT_BF16, _lib.MERGE_LOCAL, _lib.ptr(sel.idx),
                   _lib.ptr(obuf), ob_code, _lib.ptr(ml), None, None, _lib.ptr(o2), _lib.ptr(l2), None,
-                  None, 0, _lib.stream())
+                  None, 0, _lib.ptr(vscale), _lib.stream())
         ev[3].record()
         torch.cuda.synchronize()
         if it >= 2:
