@@ -45,7 +45,7 @@ extern "C" {
 #define FSA_ERR_CUDA 2
 #define FSA_ERR_UNSUPPORTED 3
 
-#define FSA_ABI_VERSION 2
+#define FSA_ABI_VERSION 3
 
 /* Element types.  FSA_DT_F16 and FSA_DT_F16R are buffer formats of the bf16
  * tensor-core path, never input dtypes:
@@ -97,6 +97,20 @@ int fsa_buffer_dtypes(const fsa_shape* s, int dtype, int* obuf_dtype, int* dqbuf
  * vscale [2 h_K] floats: s_kh in [0, h_K), scratch after.  dtype BF16 or F32. */
 int fsa_v_to_f16(const fsa_shape* s, int dtype, const void* V, void* V16, float* vscale,
                  void* stream);
+
+/* fp16 operands of the bf16 tensor-core BACKWARD (all of its products run
+ * fp16 x fp16 -> fp32: P and dS keep 11 mantissa bits where bf16 keeps 8, the
+ * rounding that otherwise drives elementwise dQ / dK / dV errors -- see
+ * tools/emulate_bf16.py).  Q16 [N][h][d_K], K16 [N][h_K][d_K], V16 [N][h_K][d_V],
+ * dO16 [N][h][d_V] = fp16(x * s) with one power-of-two scale s per kv head (for
+ * Q and dOut: per kv group, over its g heads), max |x s| in [2^14, 2^15): exact
+ * for every bf16 value above 2^-24 of the maximum.  scales [4][2 h_K] floats:
+ * s_Q, s_K, s_V, s_dO at offsets 0, 2 h_K, 4 h_K, 6 h_K (the upper half of each
+ * block is scratch).  A NULL source skips that operand (its scale block is left
+ * untouched: V16 and its scale can be the forward's fsa_v_to_f16 copy). */
+int fsa_stage_f16_ops(const fsa_shape* s, int dtype, const void* Q, const void* K, const void* V,
+                      const void* dOut, void* Q16, void* K16, void* V16, void* dO16, float* scales,
+                      void* stream);
 
 /* compress_kv (branches.py:34-44): block means K_cmp/V_cmp [b][h_K][d] and the
  * running prefix means of the first min(B_K-1, N) rows [n_pref][h_K][d]; acc dtype. */
@@ -158,11 +172,13 @@ int fsa_bwd_delta(const fsa_shape* s, int dtype, const void* out, const void* dO
 
 /* Selected backward tasks (kv_major.py:297-324, _core.pyx:97-131), one per
  * (KV head, block): dq partial rows into dq_buf, dK/dV ([N][h_K][d], acc) as
- * the single writer of the block (replaces the head sum at kv_major.py:342-354). */
+ * the single writer of the block (replaces the head sum at kv_major.py:342-354).
+ * bf16 tensor-core path: Q, K, V, dOut are the fsa_stage_f16_ops copies and
+ * scales their scale blocks (required there; ignored -- may be NULL -- else). */
 int fsa_sel_bwd(const fsa_shape* s, int dtype, const void* Q, const void* K, const void* V,
                 const void* dOut, const void* lse, const void* delta, const int32_t* offsets,
                 const int32_t* qlist, const int32_t* work, void* dq_buf, int dqbuf_dtype,
-                void* dK, void* dV, void* stream);
+                void* dK, void* dV, const float* scales, void* stream);
 
 /* dQ = ascending-block sum of dq partials (kv_major.py:326-340); [N][h][d_K] acc. */
 int fsa_dq_reduce(const fsa_shape* s, int dtype, const int32_t* idx, const void* dq_buf,
@@ -179,12 +195,15 @@ int fsa_dq_reduce_add(const fsa_shape* s, int dtype, const int32_t* idx, const v
  * importance_scores_from_compressed as a fused epilogue -- on the tensor-core
  * path only for the blocks a token's top-k can read (i < (t+1)//B_K, covered
  * by the formed key tiles); call fsa_importance_scores for every block.
- * workspace (fsa_cmp_workspace_bytes, nullable = SIMT path) holds bf16 copies
- * of the pooled K/V for the tcgen05 kernel. */
+ * workspace (fsa_cmp_workspace_bytes, nullable = SIMT path) holds the staged
+ * pooled K/V for the tcgen05 kernel, whose S runs in fp16: Q16 / qscale are the
+ * fsa_stage_f16_ops copy of Q and its scale block (required on that path,
+ * ignored otherwise) -- the operands the compressed backward recomputes S from. */
 size_t fsa_cmp_workspace_bytes(const fsa_shape* s);
 int fsa_cmp_attn_fwd(const fsa_shape* s, int dtype, const void* Q, const void* K_cmp,
                      const void* V_cmp, const void* K_prefix, const void* V_prefix, void* out,
-                     void* lse, void* scores, void* workspace, void* stream);
+                     void* lse, void* scores, void* workspace, const void* Q16,
+                     const float* qscale, void* stream);
 
 /* sliding_attention_forward (branches.py:81-83 -> oracle.py:39-44, :64-74).
  * bf16 tensor-core path: V is the fsa_v_to_f16 copy and vscale its scales
@@ -202,7 +221,7 @@ int fsa_slide_fwd(const fsa_shape* s, int dtype, const void* Q, const void* K, c
 size_t fsa_slide_bwd_workspace_bytes(const fsa_shape* s, int dtype);
 int fsa_slide_bwd(const fsa_shape* s, int dtype, const void* Q, const void* K, const void* V,
                   const void* dOut, const void* lse, const void* delta, void* dQ, void* dK,
-                  void* dV, void* workspace, int accumulate, void* stream);
+                  void* dV, void* workspace, int accumulate, const float* scales, void* stream);
 
 /* gated_combine (branches.py:95-104): out = sum_c tau[t][c] * out_c; branch
  * outputs and tau [N][3] in acc dtype; out in acc dtype if out_acc else dtype. */
@@ -244,11 +263,15 @@ int fsa_cmp_bwd(const fsa_shape* s, int dtype, const void* Q, const void* K_cmp,
 
 /* fsa_cmp_bwd with the gate folded in (after fsa_gate_backward_full_fold): dOut
  * is the raw cotangent, lse_adj = lse_cmp - ln tau[t, 0], delta = sum out_cmp *
- * dOut, and tau (N, 3) gates the pending tokens' prefix-mean gradients.  bf16
- * tensor-core configuration only. */
+ * dOut, and tau (N, 3) gates the pending tokens' prefix-mean gradients.  On the
+ * bf16 tensor-core path (d = 128) Q16 / dO16 / scales are the fsa_stage_f16_ops
+ * copies of Q and dOut (required there; ignored elsewhere).  workspace:
+ * fsa_cmp_bwd_fold_workspace_bytes. */
+size_t fsa_cmp_bwd_fold_workspace_bytes(const fsa_shape* s, int dtype);
 int fsa_cmp_bwd_fold(const fsa_shape* s, int dtype, const void* Q, const void* K_cmp,
                      const void* V_cmp, const void* dOut, const void* tau, const void* lse_adj,
-                     const void* delta, void* dQ, void* dK, void* dV, void* workspace, void* stream);
+                     const void* delta, void* dQ, void* dK, void* dV, const void* Q16,
+                     const void* dO16, const float* scales, void* workspace, void* stream);
 
 /* Gate backward for all three branches (branches.py:95-104): d_c = tau[t][c]
  * dOut (dtype), delta_c [h][N] = sum_v out_c * d_c, and the gate gradient

@@ -46,6 +46,7 @@ SIGNATURES = {
     "fsa_device_check": ([], _i),
     "fsa_buffer_dtypes": ([_sp, _i, _ip, _ip], _i),
     "fsa_v_to_f16": ([_sp, _i, _vp, _vp, _vp, _vp], _i),
+    "fsa_stage_f16_ops": ([_sp, _i] + [_vp] * 9 + [_vp], _i),
     "fsa_compress_kv": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "fsa_importance_scores": ([_sp, _i, _vp, _vp, _vp, _vp], _i),
     "fsa_select_topk": ([_sp, _i, _vp, _vp, _vp], _i),
@@ -56,20 +57,21 @@ SIGNATURES = {
     "fsa_merge_fwd": ([_sp, _i, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp], _i),
     "fsa_merge_combine_fwd": ([_sp, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "fsa_bwd_delta": ([_sp, _i, _vp, _vp, _vp, _vp], _i),
-    "fsa_sel_bwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp], _i),
+    "fsa_sel_bwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp], _i),
     "fsa_dq_reduce": ([_sp, _i, _vp, _vp, _i, _vp, _vp], _i),
     "fsa_dq_reduce_add": ([_sp, _i, _vp, _vp, _i, _vp, _vp, _vp], _i),
     "fsa_cmp_workspace_bytes": ([_sp], _sz),
-    "fsa_cmp_attn_fwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
+    "fsa_cmp_attn_fwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "fsa_slide_fwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "fsa_slide_bwd_workspace_bytes": ([_sp, _i], _sz),
-    "fsa_slide_bwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp], _i),
+    "fsa_slide_bwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp], _i),
     "fsa_gated_combine": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp], _i),
     "fsa_gate_scale": ([_sp, _i, _vp, _vp, _i, _vp, _vp], _i),
     "fsa_gate_backward": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "fsa_gate_backward_fold": ([_sp, _i] + [_vp] * 10 + [_vp], _i),
     "fsa_gate_backward_full_fold": ([_sp, _i] + [_vp] * 15 + [_vp], _i),
-    "fsa_cmp_bwd_fold": ([_sp, _i] + [_vp] * 11 + [_vp], _i),
+    "fsa_cmp_bwd_fold_workspace_bytes": ([_sp, _i], _sz),
+    "fsa_cmp_bwd_fold": ([_sp, _i] + [_vp] * 14 + [_vp], _i),
     "fsa_cmp_bwd_workspace_bytes": ([_sp, _i], _sz),
     "fsa_cmp_bwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "fsa_gate_backward_full": ([_sp, _i] + [_vp] * 13, _i),
@@ -191,3 +193,38 @@ def v_to_f16(cfg, v):
     s = shape_of(cfg)
     call("fsa_v_to_f16", ctypes.byref(s), dt_code(v.dtype), ptr(v), ptr(v16), ptr(vscale), stream())
     return v16, vscale
+
+
+class F16Ops:
+    """fsa_stage_f16_ops: the fp16 operands of the bf16 tensor-core path
+    (Q16, K16, V16, dO16, power-of-two scaled per kv head / kv group) and their
+    scale blocks ``scales`` ([4][2 h_K] floats: s_Q, s_K, s_V, s_dO).  The
+    forward stages Q (compressed-attention S) and V (every P.V product); the
+    backward adds K and dOut."""
+
+    def __init__(self, cfg, dev):
+        self.cfg = cfg
+        self.scales = torch.empty(8 * cfg.h_K, dtype=torch.float32, device=dev)
+        self.q = self.k = self.v = self.dout = None
+
+    def block(self, i):
+        """scale block i (0 Q, 1 K, 2 V, 3 dOut): [2 h_K] floats, scales first."""
+        hk = self.cfg.h_K
+        return self.scales[2 * hk * i:2 * hk * (i + 1)]
+
+    def stage(self, q=None, k=None, v=None, dout=None):
+        src = (q, k, v, dout)
+        dst = [None if x is None else torch.empty(x.shape, dtype=torch.float16, device=x.device)
+               for x in src]
+        s = shape_of(self.cfg)
+        dt = next(x.dtype for x in src if x is not None)
+        call("fsa_stage_f16_ops", ctypes.byref(s), dt_code(dt), *(ptr(x) for x in src),
+             *(ptr(x) for x in dst), ptr(self.scales), stream())
+        for name, x in zip(("q", "k", "v", "dout"), dst):
+            if x is not None:
+                setattr(self, name, x)
+        return self
+
+    @classmethod
+    def of(cls, cfg, q, k, v, dout):
+        return cls(cfg, q.device).stage(q, k, v, dout)

@@ -47,6 +47,12 @@ def compress_kv(K, V, cfg) -> CompressedKV:
     return CompressedKV(logical(Kc), logical(Vc), logical(Kp), logical(Vp))
 
 
+def _tc_qo(cfg, dt) -> bool:
+    """The query-outer tensor-core forward's configuration (tc_qo_supported)."""
+    return (dt == torch.bfloat16 and cfg.d_K == 128 and cfg.d_V == 128 and cfg.h % cfg.h_K == 0
+            and cfg.g <= 128 and cfg.N < (1 << 30))
+
+
 def _cmp_workspace(cfg, dev):
     s = _lib.shape_of(cfg)
     n = _lib.lib().fsa_cmp_workspace_bytes(ctypes.byref(s))
@@ -73,9 +79,11 @@ def compressed_attention_forward(Q, cmp: CompressedKV, cfg, *, scores_out: bool 
     lse = torch.empty((cfg.h, cfg.N), dtype=acc, device=dev)
     s = _lib.shape_of(cfg)
     ws = _cmp_workspace(cfg, dev)
+    ops = _lib.F16Ops(cfg, dev).stage(q=q) if _tc_qo(cfg, dt) else None
     _lib.call("fsa_cmp_attn_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(q), _lib.ptr(Kc),
               _lib.ptr(Vc), _lib.ptr(Kp), _lib.ptr(Vp), _lib.ptr(out), _lib.ptr(lse), None,
-              _lib.ptr(ws), _lib.stream())
+              _lib.ptr(ws), None if ops is None else _lib.ptr(ops.q),
+              None if ops is None else _lib.ptr(ops.scales), _lib.stream())
     scores = None
     if scores_out:  # every block, causal or not (selection.py:105-120)
         scores = torch.empty((cfg.h_K, cfg.N, cfg.b), dtype=acc, device=dev)
@@ -104,17 +112,18 @@ def _slide_fwd_storage(cfg, dt, q, k, v, v16=None):
     lse = torch.empty((cfg.h, cfg.N), dtype=acc, device=dev)
     s = _lib.shape_of(cfg)
     vscale = None
-    if dt == torch.bfloat16 and cfg.d_K == 128 and cfg.d_V == 128 and cfg.g <= 128:
+    if _tc_qo(cfg, dt):
         v, vscale = v16 if v16 is not None else _lib.v_to_f16(cfg, v)
     _lib.call("fsa_slide_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(q), _lib.ptr(k),
               _lib.ptr(v), _lib.ptr(vscale), _lib.ptr(out), _lib.ptr(lse), _lib.stream())
     return out, lse
 
 
-def _slide_bwd_storage(cfg, dt, q, k, v, do, out, lse, accumulate_into=None, delta=None):
+def _slide_bwd_storage(cfg, dt, q, k, v, do, out, lse, accumulate_into=None, delta=None, ops=None):
     """K11.  With ``accumulate_into=(dQ, dK, dV)`` the sliding gradients are
     added onto those tensors in-kernel (tensor-core path) and they are returned.
-    ``delta`` (h, N) may be passed precomputed (fsa_gate_backward)."""
+    ``delta`` (h, N) may be passed precomputed (fsa_gate_backward); ``ops``:
+    staged fp16 operands (_lib.F16Ops holding K16 and dO16 of this do)."""
     dev, acc = q.device, _lib.acc_dtype(dt)
     s = _lib.shape_of(cfg)
     st = _lib.stream()
@@ -132,9 +141,15 @@ def _slide_bwd_storage(cfg, dt, q, k, v, do, out, lse, accumulate_into=None, del
         dK = torch.empty((cfg.N, cfg.h_K, cfg.d_K), dtype=acc, device=dev)
         dV = torch.empty((cfg.N, cfg.h_K, cfg.d_V), dtype=acc, device=dev)
         accumulate = 0
-    _lib.call("fsa_slide_bwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(q), _lib.ptr(k),
-              _lib.ptr(v), _lib.ptr(do), _lib.ptr(lse), _lib.ptr(delta), _lib.ptr(dQ), _lib.ptr(dK),
-              _lib.ptr(dV), _lib.ptr(ws), accumulate, st)
+    if ws is not None and ops is None:  # tensor-core path: fp16 operands
+        ops = _lib.F16Ops.of(cfg, q, k, v, do)
+    elif ws is None:
+        ops = None
+    qq, kk, vv, dd = (q, k, v, do) if ops is None else (ops.q, ops.k, ops.v, ops.dout)
+    _lib.call("fsa_slide_bwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(qq), _lib.ptr(kk),
+              _lib.ptr(vv), _lib.ptr(dd), _lib.ptr(lse), _lib.ptr(delta), _lib.ptr(dQ), _lib.ptr(dK),
+              _lib.ptr(dV), _lib.ptr(ws), accumulate, None if ops is None else _lib.ptr(ops.scales),
+              st)
     if accumulate_into is not None and not accumulate:
         aQ, aK, aV = accumulate_into
         aQ += dQ

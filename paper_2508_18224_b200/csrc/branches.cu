@@ -193,7 +193,7 @@ __global__ void slide_bwd_dkdv_generic(const T* __restrict__ Q, const T* __restr
 template <typename T>
 int cmp_fwd_impl(const fsa_shape* s, const void* Q, const void* Kc, const void* Vc, const void* Kp,
                  const void* Vp, void* out, void* lse, void* scores, void* workspace,
-                 cudaStream_t st) {
+                 const void* Q16, const float* qscale, cudaStream_t st) {
   using A = typename Acc<T>::type;
   const int dt = sizeof(T) == 8 ? FSA_DT_F64 : (sizeof(T) == 4 ? FSA_DT_F32 : FSA_DT_BF16);
   const bool tc = tc_qo_supported(*s, dt) && workspace != nullptr;
@@ -203,7 +203,7 @@ int cmp_fwd_impl(const fsa_shape* s, const void* Q, const void* Kc, const void* 
   if (tc) {
     // scores for the formed blocks come from the tensor cores for every g:
     // a separate group-summed-query pass (bf16 hi/lo pairs, ~fp32 accurate)
-    if (int rc = tc_cmp_fwd(s, Q, Kc, Vc, out, lse, scores, workspace, st)) return rc;
+    if (int rc = tc_cmp_fwd(s, Q, Q16, qscale, Kc, Vc, out, lse, scores, workspace, st)) return rc;
   }
   const int64_t rows = s->h * ntok;
   if (rows > 0)
@@ -259,9 +259,9 @@ int slide_bwd_impl(const fsa_shape* s, const void* Q, const void* K, const void*
 extern "C" int fsa_cmp_attn_fwd(const fsa_shape* s, int dtype, const void* Q, const void* K_cmp,
                                 const void* V_cmp, const void* K_prefix, const void* V_prefix,
                                 void* out, void* lse, void* scores, void* workspace,
-                                void* stream) {
+                                const void* Q16, const float* qscale, void* stream) {
   DISPATCH_DT(dtype, cmp_fwd_impl, s, Q, K_cmp, V_cmp, K_prefix, V_prefix, out, lse, scores,
-              workspace, (cudaStream_t)stream);
+              workspace, Q16, qscale, (cudaStream_t)stream);
 }
 
 extern "C" size_t fsa_cmp_workspace_bytes(const fsa_shape* s) {
@@ -283,11 +283,13 @@ extern "C" size_t fsa_slide_bwd_workspace_bytes(const fsa_shape* s, int dtype) {
 extern "C" int fsa_slide_bwd(const fsa_shape* s, int dtype, const void* Q, const void* K,
                              const void* V, const void* dOut, const void* lse, const void* delta,
                              void* dQ, void* dK, void* dV, void* workspace, int accumulate,
-                             void* stream) {
+                             const float* scales, void* stream) {
   if (fsa::tc_bwd_supported(*s, dtype)) {
     FSA_REQUIRE(workspace != nullptr, "slide_bwd: tensor-core path needs its workspace");
+    FSA_REQUIRE(scales != nullptr,
+                "slide_bwd: the tensor-core path reads the fsa_stage_f16_ops copies and their scales");
     return fsa::tc_slide_bwd(s, Q, K, V, dOut, lse, delta, dQ, dK, dV, workspace, accumulate,
-                             (cudaStream_t)stream);
+                             fsa::f16_scales_of(scales, s->h_K), (cudaStream_t)stream);
   }
   FSA_REQUIRE(!accumulate, "slide_bwd: accumulate only on the tensor-core path");
   DISPATCH_DT(dtype, slide_bwd_impl, s, Q, K, V, dOut, lse, delta, dQ, dK, dV, (cudaStream_t)stream);

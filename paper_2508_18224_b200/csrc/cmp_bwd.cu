@@ -222,13 +222,16 @@ __global__ void f32_to_bf16(const float* __restrict__ x, __nv_bfloat16* __restri
 bool tc_cmp_bwd_ok(const fsa_shape& s) { return tc_qo_supported(s, FSA_DT_BF16) && s.N * s.h < (1ll << 31); }
 
 struct CmpWs {  // tensor-core path workspace
-  __nv_bfloat16 *kb, *vb;
+  __half *kc16, *vc16;   // fp16 staged K_cmp / V_cmp (their own per-kv-head scales)
+  float *kcs, *vcs;      // [2 h_K] each: scales, scratch
+  __half *q16, *o16;     // staged Q / dOut (fsa_cmp_bwd only; the fold entry gets them)
+  float* qos;            // [8 h_K]: the fsa_stage_f16_ops scale blocks (s_Q, s_dO used)
   float *dKp, *dVp, *dKc, *dVc;
   int32_t* counter;
   int64_t CH, nch, cstride;
   size_t bytes;
 };
-CmpWs cmp_ws(const fsa_shape& s, void* base) {
+CmpWs cmp_ws(const fsa_shape& s, void* base, bool stage_qo) {
   CmpWs w{};
   const int64_t b = s.N / s.B_K, n = b * s.h_K * 128;
   w.CH = cmp_chunk_tokens(&s);
@@ -237,8 +240,15 @@ CmpWs cmp_ws(const fsa_shape& s, void* base) {
   char* p = (char*)base;
   size_t off = 0;
   auto take = [&](size_t bytes) { char* r = p + off; off += (bytes + 255) & ~size_t(255); return r; };
-  w.kb = (__nv_bfloat16*)take(n * 2);
-  w.vb = (__nv_bfloat16*)take(n * 2);
+  w.kc16 = (__half*)take(n * 2);
+  w.vc16 = (__half*)take(n * 2);
+  w.kcs = (float*)take(2 * s.h_K * 4);
+  w.vcs = (float*)take(2 * s.h_K * 4);
+  if (stage_qo) {
+    w.q16 = (__half*)take(s.N * s.h * s.d_K * 2);
+    w.o16 = (__half*)take(s.N * s.h * s.d_V * 2);
+    w.qos = (float*)take(8 * s.h_K * 4);  // fsa_stage_f16_ops scale blocks
+  }
   w.dKp = (float*)take(w.nch * w.cstride * 4);
   w.dVp = (float*)take(w.nch * w.cstride * 4);
   w.dKc = (float*)take(n * 4);
@@ -248,18 +258,22 @@ CmpWs cmp_ws(const fsa_shape& s, void* base) {
   return w;
 }
 
-int cmp_bwd_tc(const fsa_shape* s, const void* Q, const void* Kc, const void* Vc, const void* dOut,
-               const void* tau,
-               const void* lse, const void* delta, void* dQ, void* dK, void* dV, void* ws,
-               cudaStream_t st) {
-  const CmpWs w = cmp_ws(*s, ws);
+// Q16 / dO16 / qos: the fsa_stage_f16_ops copies of Q and dOut and their scales
+// (sq, so: per kv head); dOut: the raw bf16 cotangent (the
+// pending tokens' prefix-mean gradients read it)
+int cmp_bwd_tc(const fsa_shape* s, const void* Q16, const void* Kc, const void* Vc,
+               const void* dOut, const void* dO16, const float* sq, const float* so,
+               const void* tau, const void* lse, const void* delta, void* dQ, void* dK, void* dV,
+               const CmpWs& w, cudaStream_t st) {
   const int64_t b = s->N / s->B_K, n = b * s->h_K * 128;
   if (n > 0) {
-    f32_to_bf16<<<148, 256, 0, st>>>((const float*)Kc, w.kb, n);
-    f32_to_bf16<<<148, 256, 0, st>>>((const float*)Vc, w.vb, n);
-    FSA_LAUNCH_CHECK("cmp_bwd to_bf16");
-    if (int rc = tc_cmp_dq(s, Q, w.kb, w.vb, dOut, lse, delta, dQ, st)) return rc;
-    if (int rc = tc_cmp_bwd_kv(s, Q, w.kb, w.vb, dOut, lse, delta, w.dKp, w.dVp, w.counter, st)) return rc;
+    if (int rc = stage_f16(FSA_DT_F32, Kc, b, s->h_K, 128, w.kc16, w.kcs, st)) return rc;
+    if (int rc = stage_f16(FSA_DT_F32, Vc, b, s->h_K, 128, w.vc16, w.vcs, st)) return rc;
+    const F16Scales sc{sq, w.kcs, w.vcs, so};
+    if (int rc = tc_cmp_dq(s, Q16, w.kc16, w.vc16, dO16, lse, delta, dQ, sc, st)) return rc;
+    if (int rc = tc_cmp_bwd_kv(s, Q16, w.kc16, w.vc16, dO16, lse, delta, w.dKp, w.dVp, w.counter,
+                               sc, st))
+      return rc;
     cmp_slab_reduce<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(w.dKp, w.dVp, w.dKc, w.dVc, b, s->h_K,
                                                                s->B_K, w.CH, w.nch, w.cstride);
     FSA_LAUNCH_CHECK("cmp_slab_reduce");
@@ -272,13 +286,35 @@ int cmp_bwd_tc(const fsa_shape* s, const void* Q, const void* Kc, const void* Vc
   return FSA_OK;
 }
 
+// tau non-null: the gate is folded in (lse = lse_adj, dOut raw; tau gates the
+// pending tokens' prefix-mean gradients).  Q16 / dO16 / scales: the
+// fsa_stage_f16_ops copies for the tensor-core path (null: staged here, into
+// a workspace sized for it).
 template <typename T>
 int cmp_bwd_impl(const fsa_shape* s, const void* Q, const void* Kc, const void* Vc, const void* dOut,
-                 const void* lse, const void* delta, void* dQ, void* dK, void* dV, void* ws,
-                 cudaStream_t st) {
+                 const void* tau, const void* lse, const void* delta, void* dQ, void* dK, void* dV,
+                 void* ws, const void* Q16, const void* dO16, const float* scales, cudaStream_t st) {
   using A = typename Acc<T>::type;
-  if (sizeof(T) == 2 && tc_cmp_bwd_ok(*s))
-    return cmp_bwd_tc(s, Q, Kc, Vc, dOut, nullptr, lse, delta, dQ, dK, dV, ws, st);
+  if (sizeof(T) == 2 && tc_cmp_bwd_ok(*s)) {
+    const bool stage = Q16 == nullptr;
+    const CmpWs w = cmp_ws(*s, ws, stage);
+    const float *sq, *so;
+    if (stage) {
+      if (int rc = fsa_stage_f16_ops(s, FSA_DT_BF16, Q, nullptr, nullptr, dOut, w.q16, nullptr,
+                                     nullptr, w.o16, w.qos, st))
+        return rc;
+      Q16 = w.q16;
+      dO16 = w.o16;
+      sq = w.qos;
+      so = w.qos + 6 * s->h_K;
+    } else {
+      FSA_REQUIRE(dO16 != nullptr && scales != nullptr, "cmp_bwd: Q16 given without dO16 / scales");
+      const F16Scales sc = f16_scales_of(scales, s->h_K);
+      sq = sc.q;
+      so = sc.o;
+    }
+    return cmp_bwd_tc(s, Q16, Kc, Vc, dOut, dO16, sq, so, tau, lse, delta, dQ, dK, dV, w, st);
+  }
   const int64_t b = s->N / s->B_K;
   A* dKc = (A*)ws;
   A* dVc = dKc + b * s->h_K * s->d_K;
@@ -294,7 +330,7 @@ int cmp_bwd_impl(const fsa_shape* s, const void* Q, const void* Kc, const void* 
         dKc, dVc, *s);
   const int64_t pr = s->N * s->h_K;
   cmp_pool_bwd<T><<<(unsigned)((pr + 7) / 8), 256, 0, st>>>(dKc, dVc, (const T*)dOut, (A*)dK,
-                                                           (A*)dV, *s);
+                                                           (A*)dV, *s, (const A*)tau);
   FSA_LAUNCH_CHECK("cmp_bwd");
   return FSA_OK;
 }
@@ -427,7 +463,7 @@ int gate_bwd_full_impl(const fsa_shape* s, const void* dOut, const void* tau, co
 
 extern "C" size_t fsa_cmp_bwd_workspace_bytes(const fsa_shape* s, int dtype) {
   const size_t acc = dtype == FSA_DT_F64 ? 8 : 4;
-  if (dtype == FSA_DT_BF16 && fsa::tc_cmp_bwd_ok(*s)) return fsa::cmp_ws(*s, nullptr).bytes;
+  if (dtype == FSA_DT_BF16 && fsa::tc_cmp_bwd_ok(*s)) return fsa::cmp_ws(*s, nullptr, true).bytes;
   return (size_t)(s->N / s->B_K) * s->h_K * (s->d_K + s->d_V) * acc + 256;
 }
 
@@ -435,19 +471,27 @@ extern "C" int fsa_cmp_bwd(const fsa_shape* s, int dtype, const void* Q, const v
                            const void* V_cmp, const void* dOut, const void* lse, const void* delta,
                            void* dQ, void* dK, void* dV, void* workspace, void* stream) {
   FSA_REQUIRE(workspace != nullptr, "cmp_bwd: workspace required");
-  DISPATCH_DT(dtype, cmp_bwd_impl, s, Q, K_cmp, V_cmp, dOut, lse, delta, dQ, dK, dV, workspace,
-              (cudaStream_t)stream);
+  DISPATCH_DT(dtype, cmp_bwd_impl, s, Q, K_cmp, V_cmp, dOut, nullptr, lse, delta, dQ, dK, dV,
+              workspace, nullptr, nullptr, nullptr, (cudaStream_t)stream);
+}
+
+extern "C" size_t fsa_cmp_bwd_fold_workspace_bytes(const fsa_shape* s, int dtype) {
+  if (dtype == FSA_DT_BF16 && fsa::tc_cmp_bwd_ok(*s)) return fsa::cmp_ws(*s, nullptr, false).bytes;
+  return fsa_cmp_bwd_workspace_bytes(s, dtype);
 }
 
 extern "C" int fsa_cmp_bwd_fold(const fsa_shape* s, int dtype, const void* Q, const void* K_cmp,
                                 const void* V_cmp, const void* dOut, const void* tau,
                                 const void* lse_adj, const void* delta, void* dQ, void* dK, void* dV,
+                                const void* Q16, const void* dO16, const float* scales,
                                 void* workspace, void* stream) {
   FSA_REQUIRE(workspace != nullptr, "cmp_bwd: workspace required");
-  FSA_REQUIRE(dtype == FSA_DT_BF16 && fsa::tc_cmp_bwd_ok(*s),
-              "cmp_bwd_fold: the bf16 tensor-core configuration only");
-  return fsa::cmp_bwd_tc(s, Q, K_cmp, V_cmp, dOut, tau, lse_adj, delta, dQ, dK, dV, workspace,
-                         (cudaStream_t)stream);
+  FSA_REQUIRE(tau != nullptr, "cmp_bwd_fold: tau required");
+  if (dtype == FSA_DT_BF16 && fsa::tc_cmp_bwd_ok(*s))
+    FSA_REQUIRE(Q16 != nullptr && dO16 != nullptr && scales != nullptr,
+                "cmp_bwd_fold: the tensor-core path reads the fsa_stage_f16_ops copies of Q and dOut");
+  DISPATCH_DT(dtype, cmp_bwd_impl, s, Q, K_cmp, V_cmp, dOut, tau, lse_adj, delta, dQ, dK, dV,
+              workspace, Q16, dO16, scales, (cudaStream_t)stream);
 }
 
 extern "C" int fsa_gate_backward_full(const fsa_shape* s, int dtype, const void* dOut,

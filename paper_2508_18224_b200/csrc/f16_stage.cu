@@ -124,6 +124,27 @@ int stage_f16(int src_dtype, const void* x, int64_t rows, int64_t heads, int64_t
 
 }  // namespace fsa
 
+extern "C" int fsa_stage_f16_ops(const fsa_shape* s, int dtype, const void* Q, const void* K,
+                                 const void* V, const void* dOut, void* Q16, void* K16, void* V16,
+                                 void* dO16, float* scales, void* stream) {
+  // Q / dOut [N][h][d] are [N][h_K][g d]: one scale per kv group (the rows of
+  // one backward item mix the group's heads, and dK^T / dV^T contract over them)
+  FSA_REQUIRE(scales != nullptr, "stage_f16_ops: scales is required");
+  FSA_REQUIRE(s->h_K > 0 && s->h % s->h_K == 0, "stage_f16_ops: h %% h_K != 0");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t g = s->h / s->h_K, hk = s->h_K;
+  const void* src[4] = {Q, K, V, dOut};
+  void* dst[4] = {Q16, K16, V16, dO16};
+  const int64_t d[4] = {g * s->d_K, s->d_K, s->d_V, g * s->d_V};
+  for (int i = 0; i < 4; ++i) {
+    if (!src[i]) continue;
+    FSA_REQUIRE(dst[i] != nullptr, "stage_f16_ops: operand %d has no destination", i);
+    if (int rc = fsa::stage_f16(dtype, src[i], s->N, hk, d[i], dst[i], scales + 2 * hk * i, st))
+      return rc;
+  }
+  return FSA_OK;
+}
+
 extern "C" int fsa_v_to_f16(const fsa_shape* s, int dtype, const void* V, void* V16, float* vscale,
                             void* stream) {
   return fsa::stage_f16(dtype, V, s->N, s->h_K, s->d_V, V16, vscale, (cudaStream_t)stream);

@@ -458,10 +458,14 @@ extern "C" int fsa_bwd_delta(const fsa_shape* s, int dtype, const void* out, con
 extern "C" int fsa_sel_bwd(const fsa_shape* s, int dtype, const void* Q, const void* K,
                            const void* V, const void* dOut, const void* lse, const void* delta,
                            const int32_t* offsets, const int32_t* qlist, const int32_t* work,
-                           void* dq_buf, int dqbuf_dtype, void* dK, void* dV, void* stream) {
-  if (fsa::tc_bwd_supported(*s, dtype))  // dq_buf: FSA_DT_F16R rows + exponents
+                           void* dq_buf, int dqbuf_dtype, void* dK, void* dV,
+                           const float* scales, void* stream) {
+  if (fsa::tc_bwd_supported(*s, dtype)) {  // dq_buf: FSA_DT_F16R rows + exponents
+    FSA_REQUIRE(scales != nullptr,
+                "sel_bwd: the tensor-core path reads the fsa_stage_f16_ops copies and their scales");
     return fsa::tc_sel_bwd(s, Q, K, V, dOut, lse, delta, offsets, qlist, work, dq_buf, dqbuf_dtype,
-                           dK, dV, (cudaStream_t)stream);
+                           dK, dV, fsa::f16_scales_of(scales, s->h_K), (cudaStream_t)stream);
+  }
   FSA_REQUIRE(dqbuf_dtype == (dtype == FSA_DT_F64 ? FSA_DT_F64 : FSA_DT_F32),
               "sel_bwd: dq buffer dtype mismatch");
   DISPATCH_DT(dtype, sel_bwd_impl, s, Q, K, V, dOut, lse, delta, offsets, qlist, dq_buf, dK, dV,

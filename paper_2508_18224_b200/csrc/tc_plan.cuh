@@ -8,14 +8,25 @@ namespace fsa {
 bool tc_fwd_supported(const fsa_shape& s, int dtype);
 bool tc_bwd_supported(const fsa_shape& s, int dtype);
 
+// Per-kv-head power-of-two scales of the fp16 backward operands
+// (fsa_stage_f16_ops): x16 = x * s.  q: Q (per kv group), k: K, v: V, o: dOut.
+struct F16Scales {
+  const float *q, *k, *v, *o;
+};
+// the scale blocks of an fsa_stage_f16_ops `scales` buffer ([4][2 h_K])
+inline F16Scales f16_scales_of(const float* scales, int64_t h_K) {
+  return F16Scales{scales, scales + 2 * h_K, scales + 4 * h_K, scales + 6 * h_K};
+}
+
 // V: the fp16 staged copy (stage_f16); obuf fp16 [h][N][T][128] in its scale
 int tc_sel_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V16,
                const int32_t* offsets, const int32_t* qlist, const int32_t* work, void* obuf,
                void* ml, cudaStream_t st);
+// Q, K, V, dOut: the fp16 staged copies, sc their scales
 int tc_sel_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V, const void* dOut,
                const void* lse, const void* delta, const int32_t* offsets, const int32_t* qlist,
                const int32_t* work, void* dq_buf, int dqbuf_dtype, void* dK, void* dV,
-               cudaStream_t st);
+               F16Scales sc, cudaStream_t st);
 
 // fp16 staging of a [rows][heads][d] bf16 / f32 tensor with a power-of-two
 // scale per head (f16_stage.cu); vscale [2 heads]: scales, then scratch
@@ -27,27 +38,31 @@ bool tc_qo_supported(const fsa_shape& s, int dtype);
 int tc_slide_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V16,
                  const float* vscale, void* out, void* lse, cudaStream_t st);
 size_t tc_cmp_workspace_bytes(const fsa_shape* s);
-int tc_cmp_fwd(const fsa_shape* s, const void* Q, const void* Kc, const void* Vc, void* out,
-               void* lse, void* scores, void* workspace, cudaStream_t st);
+// Q16 / qscale: the fsa_stage_f16_ops copy of Q and its scale block (the
+// compressed attention's S runs in fp16, as its backward recomputes it)
+int tc_cmp_fwd(const fsa_shape* s, const void* Q, const void* Q16, const float* qscale,
+               const void* Kc, const void* Vc, void* out, void* lse, void* scores, void* workspace,
+               cudaStream_t st);
 
 // sliding-window backward on the FSA backward kernel (tc_sel_bwd.cu)
 size_t tc_slide_bwd_workspace_bytes(const fsa_shape* s);
 int tc_slide_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V,
                  const void* dOut, const void* lse, const void* delta, void* dQ, void* dK,
-                 void* dV, void* workspace, int accumulate, cudaStream_t st);
+                 void* dV, void* workspace, int accumulate, F16Scales sc, cudaStream_t st);
 
 // query-outer sliding-window dQ (tc_slide_dq.cu); accumulate: dQ += (fp32)
 int tc_slide_dq(const fsa_shape* s, const void* Q, const void* K, const void* V, const void* dOut,
-                const void* lse, const void* delta, void* dQ, int accumulate, cudaStream_t st);
+                const void* lse, const void* delta, void* dQ, int accumulate, F16Scales sc,
+                cudaStream_t st);
 
 // compressed-branch backward on the same kernels (tc_sel_bwd.cu, tc_slide_dq.cu):
 // dK_cmp / dV_cmp partial slabs per token chunk, and dQ += over the pooled rows
 int64_t cmp_chunk_tokens(const fsa_shape* s);
 int tc_cmp_bwd_kv(const fsa_shape* s, const void* Q, const void* Kb, const void* Vb,
                   const void* dOut, const void* lse, const void* delta, void* dKp, void* dVp,
-                  int32_t* counter, cudaStream_t st);
+                  int32_t* counter, F16Scales sc, cudaStream_t st);
 int tc_cmp_dq(const fsa_shape* s, const void* Q, const void* Kb, const void* Vb, const void* dOut,
-              const void* lse, const void* delta, void* dQ, cudaStream_t st);
+              const void* lse, const void* delta, void* dQ, F16Scales sc, cudaStream_t st);
 
 // vectorised merge of the fp16 slot partials / reduce of the fp16 dq partials
 // for d = 128, any T (merge_fast.cu); out / lse / m / l / dQ / addend fp32.

@@ -44,7 +44,14 @@ enum { B_QF = 0, B_QE = 2, B_KF = 4, B_KE = 7, B_SF = 10, B_PF = 14, B_OF = 18, 
 constexpr uint32_t kOffTmem = kOffBar + kNumBars * 8;
 constexpr uint32_t kSmemBytes = kOffTmem + 16 + 1024;
 static_assert(kSmemBytes <= 232448, "shared memory budget");
-constexpr uint32_t kIdS = idesc_bf16(128, 64, false, false);
+// S operands: bf16 Q / K (SLIDE; SCORES: the hi/lo pairs), fp16 in CMP mode --
+// the fsa_stage_f16_ops copy of Q against the fp16 staged pooled K, exactly
+// the operands the compressed backward recomputes S from (tc_sel_bwd.cu /
+// tc_slide_dq.cu compressed modes), so its P = exp(S - lse) is consistent
+template <int M>
+__host__ __device__ constexpr uint32_t ids_of() {
+  return M == 1 ? idesc_f16(128, 64, false, false) : idesc_bf16(128, 64, false, false);
+}
 constexpr uint32_t kIdPV = idesc_f16(128, 128, false, true);  // P, V16 in fp16
 constexpr float kRescale = 8.f;  // exp2 units
 
@@ -66,7 +73,8 @@ struct Params {
   long long* trace;  // debug timeline (CTA 0), null in production
   // keys bf16, values the fp16 staged copy (SCORES: the V slot holds K_cmp's
   // bf16 low part): K,V [N][h_K][128] or pooled [b][h_K][128]
-  const __nv_bfloat16 *Q, *Kx;
+  const void *Q, *Kx;      // 16-bit: bf16, or fp16 (CMP: Q16, pooled K16)
+  const float *qscale, *kscale;  // CMP: the fp16 operands' per-kv-head scales
   const void* Vx;
   const float* vscale;  // [h_K] power-of-two scale of the fp16 values
   float *out, *lse, *scores;
@@ -245,12 +253,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk)
                   mma_bf16(tS, desc_kmajor(q + (kk >> 2) * 16384u + (kk & 3) * 32u),
-                           desc_kmajor(k + (kk >> 2) * 8192u + (kk & 3) * 32u), kIdS, kk > 0);
+                           desc_kmajor(k + (kk >> 2) * 8192u + (kk & 3) * 32u), ids_of<M>(), kk > 0);
                 if constexpr (M == SCORES) {  // + Q . K_lo^T (the V slot holds K_cmp's low part)
 #pragma unroll
                   for (int kk = 0; kk < 8; ++kk)
                     mma_bf16(tS, desc_kmajor(q + (kk >> 2) * 16384u + (kk & 3) * 32u),
-                             desc_kmajor(k + 16384u + (kk >> 2) * 8192u + (kk & 3) * 32u), kIdS, 1u);
+                             desc_kmajor(k + 16384u + (kk >> 2) * 8192u + (kk & 3) * 32u), ids_of<M>(), 1u);
                 }
                 mma_commit(bar(B_SF + 2 * w + v));
                 QO_TRACE(w, ns[w], 0);  // S issued
@@ -338,6 +346,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
       }
       if (!ok) khi = -1;
       float m_used = -INFINITY, l = 0.f;
+      float sl2 = p.scale_log2, scl = p.scale;  // per unit of S as computed
+      if (M == CMP) {  // S16 = S s_Q s_Kc
+        const float f = 1.f / (__ldg(p.qscale + c.it.kh) * __ldg(p.kscale + c.it.kh));
+        sl2 *= f;
+        scl *= f;
+      }
       for (int kt = s.k0; kt < s.k1; ++kt, ++u) {
         const int v = (int)(u & 1);
         const uint32_t tS = tmem + lb + 64u * v;
@@ -397,9 +411,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
         // move the reference max only on a large increase (or the first finite max)
         float f = 1.f;
         bool resc = false;
-        if (mx > -INFINITY && (m_used == -INFINITY || (mx - m_used) * p.scale_log2 > kRescale)) {
+        if (mx > -INFINITY && (m_used == -INFINITY || (mx - m_used) * sl2 > kRescale)) {
           if (m_used != -INFINITY) {
-            f = ex2((m_used - mx) * p.scale_log2);
+            f = ex2((m_used - mx) * sl2);
             l *= f;
             resc = true;
           }
@@ -420,13 +434,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
           }
           tmem_wait_st_();
         }
-        const float mb = m_used == -INFINITY ? 0.f : m_used * p.scale_log2;
+        const float mb = m_used == -INFINITY ? 0.f : m_used * sl2;
         uint32_t pk[32];
         float l0 = 0.f, l1 = 0.f;
 #pragma unroll
         for (int cc = 0; cc < 64; cc += 2) {
-          const float e0 = ex2(fmaf(sv[cc], p.scale_log2, -mb));  // -inf -> 0
-          const float e1 = ex2(fmaf(sv[cc + 1], p.scale_log2, -mb));
+          const float e0 = ex2(fmaf(sv[cc], sl2, -mb));  // -inf -> 0
+          const float e1 = ex2(fmaf(sv[cc + 1], sl2, -mb));
           l0 += e0;
           l1 += e1;
           pk[cc >> 1] = pack_f16(e0, e1);
@@ -489,7 +503,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
       tc_fence_before();
       mbar_arrive(bar(B_OE + w));
       if (r == 0) QO_TRACE(w, u - 1, 6);  // epilogue done
-      if (write) p.lse[j * p.N + t] = m_used * p.scale + __logf(l);
+      if (write) p.lse[j * p.N + t] = m_used * scl + __logf(l);
       ++n_out;
     }
   }
@@ -609,8 +623,8 @@ int tc_slide_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V
               "scales (fsa_v_to_f16)");
   Params p = base_params(s);
   p.mode = SLIDE;
-  p.Q = (const __nv_bfloat16*)Q;
-  p.Kx = (const __nv_bfloat16*)K;
+  p.Q = Q;
+  p.Kx = K;
   p.Vx = V16;
   p.vscale = vscale;
   p.n_keys = s->N;
@@ -624,23 +638,34 @@ int tc_slide_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V
 
 size_t tc_cmp_workspace_bytes(const fsa_shape* s) {
   // bf16 pooled K, fp16 (scaled) pooled V, the group-summed queries as bf16
-  // hi/lo pairs, then the pooled V's per-head scales (+ scratch)
-  return (size_t)2 * (s->N / s->B_K) * s->h_K * kD * sizeof(__nv_bfloat16) +
-         (size_t)2 * s->N * s->h_K * kD * sizeof(__nv_bfloat16) + 2 * s->h_K * sizeof(float);
+  // hi/lo pairs, the pooled V's per-head scales (+ scratch), the fp16 (scaled)
+  // pooled K and its scales (+ scratch)
+  const size_t n = (size_t)(s->N / s->B_K) * s->h_K * kD;
+  return 2 * n * 2 + (size_t)2 * s->N * s->h_K * kD * 2 + 2 * s->h_K * sizeof(float) + 256 +
+         n * 2 + 256 + 2 * s->h_K * sizeof(float);
 }
 
-int tc_cmp_fwd(const fsa_shape* s, const void* Q, const void* Kc, const void* Vc, void* out,
-               void* lse, void* scores, void* workspace, cudaStream_t st) {
+int tc_cmp_fwd(const fsa_shape* s, const void* Q, const void* Q16, const float* qscale,
+               const void* Kc, const void* Vc, void* out, void* lse, void* scores, void* workspace,
+               cudaStream_t st) {
+  FSA_REQUIRE(Q16 != nullptr && qscale != nullptr,
+              "cmp_attn_fwd: the tensor-core path reads the fsa_stage_f16_ops copy of Q and its scales");
   Params p = base_params(s);
   p.mode = CMP;
   const int64_t n = p.b * p.h_K * kD;
   __nv_bfloat16* kb = (__nv_bfloat16*)workspace;
   __nv_bfloat16* vb = kb + n;
   float* vsc = reinterpret_cast<float*>(vb + n + 2 * p.N * p.h_K * kD);
-  to_bf16_kernel<<<148, 256, 0, st>>>((const float*)Kc, kb, n);
+  // 256-byte aligned (TMA base addresses need 16)
+  auto align = [](void* x) { return (void*)(((uintptr_t)x + 255) & ~(uintptr_t)255); };
+  __half* k16 = (__half*)align(vsc + 2 * p.h_K);
+  float* ksc = (float*)align(k16 + n);
+  if (int rc = stage_f16(FSA_DT_F32, Kc, p.b, p.h_K, kD, k16, ksc, st)) return rc;
   if (int rc = stage_f16(FSA_DT_F32, Vc, p.b, p.h_K, kD, vb, vsc, st)) return rc;
-  p.Q = (const __nv_bfloat16*)Q;
-  p.Kx = kb;
+  p.Q = Q16;
+  p.qscale = qscale;
+  p.Kx = k16;
+  p.kscale = ksc;
   p.Vx = vb;
   p.vscale = vsc;
   p.n_keys = p.b;
@@ -656,12 +681,14 @@ int tc_cmp_fwd(const fsa_shape* s, const void* Q, const void* Kc, const void* Vc
     // K_cmp hi (the K slot) + lo (the V slot, overwriting the pooled V copy the
     // compressed pass above has finished with) computes Qsum . K_cmp
     __nv_bfloat16* qs = vb + n;
+    to_bf16_kernel<<<148, 256, 0, st>>>((const float*)Kc, kb, n);
     lo_part_kernel<<<148, 256, 0, st>>>((const float*)Kc, kb, vb, n);
     qsum_kernel<<<(unsigned)((p.N * p.h_K + 7) / 8), 256, 0, st>>>((const __nv_bfloat16*)Q, qs,
                                                                     p.N, p.h_K, p.g);
     Params q = p;
     q.mode = SCORES;
     q.Q = qs;
+    q.Kx = kb;  // K_cmp hi; lo in the V slot (vb)
     q.h = 2 * p.h_K;
     q.g = 2;
     q.tpi = kRows / 2;

@@ -8,7 +8,7 @@
 // Per 128-row item (TPI tokens x g heads), rows = gathered (token, slot):
 //   S   = Q K^T          M128 N64  K128   TMEM stage s, cols [0, 64)
 //   dP  = dO V^T         M128 N64  K128   TMEM stage s, cols [64, 128)
-//   P   = exp(S*scale - lse),  dS = P * (dP - delta)      (softmax warps, bf16 -> smem)
+//   P   = exp(S*scale - lse),  dS = P * (dP - delta)      (softmax warps, fp16 -> smem)
 //   dV^T += dO^T P       M128(d) N64 K128(rows)  TMEM accumulator
 //   dK^T += Q^T dS       M128(d) N64 K128(rows)  TMEM accumulator
 //   dQ_i  = dS K         M128 N128 K64  -> TMEM stage s (over the consumed S/dP)
@@ -16,6 +16,15 @@
 //                                           per-row power-of-two exponent
 // dQ partials are summed over the token's selected blocks in ascending block
 // order by the dq_reduce kernel (kv_major.py:326-340).
+//
+// Every product runs fp16 x fp16 -> fp32 on the fsa_stage_f16_ops copies
+// Q16 = Q s_Q, K16 = K s_K, V16 = V s_V, dO16 = dO s_dO (power-of-two scales
+// per kv head, max |x s| in [2^14, 2^15)): S and dP come out exact as with
+// bf16 operands, while P and dS are rounded to 11 bits instead of 8 -- the
+// rounding behind elementwise dQ / dK / dV errors (tools/emulate_bf16.py).
+// Stored operands:  P16 = P 2^15 (P <= 1),  dS16 = P (dP16 - delta s_V s_dO) 2^-23,
+// where |dP16|, |delta s_V s_dO| <= 128 2^15 2^15 (|out| <= max|V|), so
+// |dS16| <= 2^15 < 65504 for any input scale; the epilogues divide the scales out.
 //
 // Roles: warps 0-7 two softmax warpgroups that ping-pong over items (wg owns
 // items n with n % 2 == wg and its own Q/dO, S/dP and P/dS stages; after its
@@ -66,15 +75,18 @@ constexpr uint32_t kSmemBytes = kOffTmem + 16 + 1024;
 constexpr int kTStages = 3;
 constexpr uint32_t kColDK = 384, kColDV = 448;
 
-constexpr uint32_t kIdS = idesc_bf16(128, 64, false, false);  // S, dP
-constexpr uint32_t kIdKV = idesc_bf16(128, 64, true, true);   // dV^T, dK^T
-constexpr uint32_t kIdQ = idesc_bf16(128, 128, false, true);  // dQ
+constexpr uint32_t kIdS = idesc_f16(128, 64, false, false);  // S, dP
+constexpr uint32_t kIdKV = idesc_f16(128, 64, true, true);   // dV^T, dK^T
+constexpr uint32_t kIdQ = idesc_f16(128, 128, false, true);  // dQ
+constexpr float kP16 = 32768.f;             // P16 = P 2^15
+constexpr float kDS16 = 1.f / 8388608.f;    // dS16 = P (dP16 - delta16) 2^-23
 
 struct Params {
   CUtensorMap tmQ, tmO, tmK, tmV;  // sliding / compressed modes: TMA token boxes
   CUtensorMap tmDQ;                 // dq partial rows [h N T][128] fp16 (scatter4 stores)
   long long* trace;  // debug timeline (CTA 0, first 256 items), null in production
-  const __nv_bfloat16 *Q, *K, *V, *dO;
+  const __half *Q, *K, *V, *dO;  // the fp16 staged copies (fsa_stage_f16_ops)
+  F16Scales sc;                   // their per-kv-head scales
   const float *lse, *delta;
   const int32_t *offsets, *qlist;
   int32_t* counter;
@@ -275,7 +287,7 @@ __global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const _
       mbar_spin(bar(B_KVE), (uint32_t)((kseq & 1) ^ 1));
       {  // warps 8,9: K rows 0-31, 32-63; warps 10,11: V rows 0-31, 32-63
         const int lw = warp - 8, row0 = (lw & 1) * 32;
-        const __nv_bfloat16* src =
+        const __half* src =
             (lw < 2 ? p.K : p.V) + ((tr.i * kBK + row0 + lane) * p.h_K + tr.kh) * kD;
         warp_gather_rows32(sb + (lw < 2 ? kOffK : kOffV), 8192u, row0, src, true, lane);
         asm volatile("cp.async.commit_group;" ::: "memory");
@@ -472,10 +484,12 @@ __global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const _
       float* dk = p.dK + slab + ((tr.i * kBK) * p.h_K + tr.kh) * kD + r;
       float* dv = p.dV + slab + ((tr.i * kBK) * p.h_K + tr.kh) * kD + r;
       const int64_t ks_ = p.h_K * kD;  // key stride
+      const float sv = p.sc.v[tr.kh], so = p.sc.o[tr.kh];
+      const float mul_k = p.scale / (kDS16 * p.sc.q[tr.kh] * sv * so), mul_v = 1.f / (kP16 * so);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {  // dK keys 16 at a time, then dV (register budget)
         float* dst = (q < 4 ? dk : dv) + (int64_t)(q & 3) * 16 * ks_;
-        const float mul = q < 4 ? p.scale : 1.f;
+        const float mul = q < 4 ? mul_k : mul_v;
         float v[16], old[16];
         if (ACC) {  // batch the 16 loads: one memory latency per chunk
 #pragma unroll
@@ -538,6 +552,10 @@ __global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const _
           dz = __ldg(p.delta + j * p.N + t);
         }
       };
+      // fp16 operand scales of this kv head: S16 = S s_Q s_K, dP16 = dP s_V s_dO
+      const float sl2 = p.scale_log2 / (p.sc.q[tr.kh] * p.sc.k[tr.kh]);
+      const float d16 = p.sc.v[tr.kh] * p.sc.o[tr.kh];
+      const float mul_q = p.scale / (kDS16 * p.sc.k[tr.kh] * d16);  // dQ = scale dS K
       int32_t ent_a = kt < p.tpi ? entry_at<SL>(p, tr, (int64_t)c0 * p.tpi + kt) : 0;        // item c
       int32_t ent_b = kt < p.tpi ? entry_at<SL>(p, tr, (int64_t)(c0 + 2) * p.tpi + kt) : 0;  // item c + 2
       float lse_a, dl_a;
@@ -564,6 +582,7 @@ __global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const _
           }
         }
         const float lse_r = lse_raw * 1.4426950408889634f;
+        const float dl16 = dl * d16;
         const bool full = __all_sync(0xffffffffu, klo == 0 && khi == kBK - 1);
         const int tm = (int)(n % kTStages);
         const uint32_t tpar = (uint32_t)((n / kTStages) & 1);
@@ -599,15 +618,15 @@ __global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const _
 #pragma unroll
           for (int c2 = 0; c2 < CW; c2 += 2) {
             const int key = hf * CW + c2;
-            float p0 = ex2(fmaf(sv[c2], p.scale_log2, -lse_r));
-            float p1 = ex2(fmaf(sv[c2 + 1], p.scale_log2, -lse_r));
+            float p0 = ex2(fmaf(sv[c2], sl2, -lse_r));
+            float p1 = ex2(fmaf(sv[c2 + 1], sl2, -lse_r));
             if (!full) {
               p0 = (key >= klo && key <= khi) ? p0 : 0.f;
               p1 = (key + 1 >= klo && key + 1 <= khi) ? p1 : 0.f;
             }
             if (!ok) p0 = p1 = 0.f;
-            pp[c2 >> 1] = pack_bf16(p0, p1);
-            dd[c2 >> 1] = pack_bf16(p0 * (dp[c2] - dl), p1 * (dp[c2 + 1] - dl));
+            pp[c2 >> 1] = pack_f16(p0 * kP16, p1 * kP16);
+            dd[c2 >> 1] = pack_f16(p0 * ((dp[c2] - dl16) * kDS16), p1 * ((dp[c2 + 1] - dl16) * kDS16));
           }
 #pragma unroll
           for (int c4 = 0; c4 < CW / 8; ++c4) {
@@ -649,8 +668,8 @@ __global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const _
 #pragma unroll
           for (int c = 0; c < 32; ++c) amax = fmaxf(amax, fabsf(v[c]));
         }
-        const int ex = f16_row_exp(amax * p.scale);
-        const float mul = ldexpf(p.scale, ex);
+        const int ex = f16_row_exp(amax * mul_q);
+        const float mul = ldexpf(mul_q, ex);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           float v[32];
@@ -711,13 +730,14 @@ namespace {
 long long* g_trace = nullptr;
 Params make_params(const fsa_shape* s, const void* Q, const void* K, const void* V,
                    const void* dOut, const void* lse, const void* delta, void* dq_buf, void* dK,
-                   void* dV) {
+                   void* dV, F16Scales sc) {
   Params p{};
+  p.sc = sc;
   p.trace = g_trace;
-  p.Q = (const __nv_bfloat16*)Q;
-  p.K = (const __nv_bfloat16*)K;
-  p.V = (const __nv_bfloat16*)V;
-  p.dO = (const __nv_bfloat16*)dOut;
+  p.Q = (const __half*)Q;
+  p.K = (const __half*)K;
+  p.V = (const __half*)V;
+  p.dO = (const __half*)dOut;
   p.lse = (const float*)lse;
   p.delta = (const float*)delta;
   p.dq = (__half*)dq_buf;
@@ -759,11 +779,11 @@ int launch_bwd(Params& p, cudaStream_t st) {
 int tc_sel_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V, const void* dOut,
                const void* lse, const void* delta, const int32_t* offsets, const int32_t* qlist,
                const int32_t* work, void* dq_buf, int dqbuf_dtype, void* dK, void* dV,
-               cudaStream_t st) {
+               F16Scales sc, cudaStream_t st) {
   FSA_REQUIRE(work != nullptr, "tensor-core backward needs the inverse work buffer");
   FSA_REQUIRE(dqbuf_dtype == FSA_DT_F16R,
               "tensor-core backward writes fp16 dq partials with row exponents (FSA_DT_F16R)");
-  Params p = make_params(s, Q, K, V, dOut, lse, delta, dq_buf, dK, dV);
+  Params p = make_params(s, Q, K, V, dOut, lse, delta, dq_buf, dK, dV, sc);
   p.offsets = offsets;
   p.qlist = qlist;
   p.counter = const_cast<int32_t*>(work) + p.ntask + 1;
@@ -778,9 +798,9 @@ size_t tc_slide_bwd_workspace_bytes(const fsa_shape* s) { return 256; }  // sche
 // window of tokens (no dQ there), then dQ query-outer (tc_slide_dq.cu).
 int tc_slide_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V,
                  const void* dOut, const void* lse, const void* delta, void* dQ, void* dK,
-                 void* dV, void* workspace, int accumulate, cudaStream_t st) {
+                 void* dV, void* workspace, int accumulate, F16Scales sc, cudaStream_t st) {
   const int64_t S = (s->W - 1) / kBK + 2;  // window slots of a token (for the row bookkeeping)
-  Params p = make_params(s, Q, K, V, dOut, lse, delta, nullptr, dK, dV);
+  Params p = make_params(s, Q, K, V, dOut, lse, delta, nullptr, dK, dV, sc);
   p.slide = 1;
   p.no_dq = 1;
   p.accumulate = accumulate != 0;  // dK/dV += (modes 1 and 2)
@@ -796,7 +816,7 @@ int tc_slide_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V
   rc = launch_bwd(p, st);
   if (rc) return rc;
   // mode 1: dQ +=; mode 2: dQ written (fp32)
-  return tc_slide_dq(s, Q, K, V, dOut, lse, delta, dQ, accumulate == 1, st);
+  return tc_slide_dq(s, Q, K, V, dOut, lse, delta, dQ, accumulate == 1, sc, st);
 }
 
 // Compressed-branch dK_cmp / dV_cmp: the same kernel with
@@ -811,8 +831,8 @@ int64_t cmp_chunk_tokens(const fsa_shape* s) {
 
 int tc_cmp_bwd_kv(const fsa_shape* s, const void* Q, const void* Kb, const void* Vb,
                   const void* dOut, const void* lse, const void* delta, void* dKp, void* dVp,
-                  int32_t* counter, cudaStream_t st) {
-  Params p = make_params(s, Q, Kb, Vb, dOut, lse, delta, nullptr, dKp, dVp);
+                  int32_t* counter, F16Scales sc, cudaStream_t st) {
+  Params p = make_params(s, Q, Kb, Vb, dOut, lse, delta, nullptr, dKp, dVp, sc);
   p.slide = 2;
   p.no_dq = 1;
   p.accumulate = 0;

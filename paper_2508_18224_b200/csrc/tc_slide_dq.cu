@@ -10,11 +10,14 @@
 // of TPI = 128/g tokens x g heads of one kv head sharing one stream of 64-key
 // K/V tiles; softmax warpgroup w owns sub-item w.  Per tile:
 //   S_w = Q_w K^T, dP_w = dO_w V^T      (2 x M128 N64 K128) -> TMEM of wg w
-//   softmax: dS (bf16) written back over S in TMEM
+//   softmax: dS (fp16) written back over S in TMEM
 //   dQ_w += dS K                        (M128 N128 K64, A = dS from TMEM)
 // TMEM per wg (256 columns at 256 w): S +0, dP +64, dQ accumulator +128.
 // Roles: warps 0-3 / 4-7 softmax + epilogue, warp 8 the TMA loader (one lane;
 // 9-10 idle), 11 MMA issuer.
+// fp16 operands (fsa_stage_f16_ops copies, as tc_sel_bwd.cu): S16 = S s_Q s_K,
+// dP16 = dP s_V s_dO, dS16 = P (dP16 - delta s_V s_dO) 2^-23 (|dS16| <= 2^15),
+// dQ = scale acc / (2^-23 s_K s_V s_dO).
 #include "tc_plan.cuh"
 #include "tc_sched.cuh"
 
@@ -36,14 +39,16 @@ enum { B_QF = 0, B_QE = 1, B_KF = 2, B_KE = 5, B_SF = 8, B_PF = 10, B_OF = 12, B
 constexpr uint32_t kOffTmem = kOffBar + kNumBars * 8;
 constexpr uint32_t kSmemBytes = kOffTmem + 16 + 1024;
 static_assert(kSmemBytes <= 232448, "shared memory budget");
-constexpr uint32_t kIdS = idesc_bf16(128, 64, false, false);
-constexpr uint32_t kIdQ = idesc_bf16(128, 128, false, true);
+constexpr uint32_t kIdS = idesc_f16(128, 64, false, false);
+constexpr uint32_t kIdQ = idesc_f16(128, 128, false, true);
+constexpr float kDS16 = 1.f / 8388608.f;  // dS16 = P (dP16 - delta16) 2^-23
 
 struct Params {
   CUtensorMap tmQ, tmO, tmK, tmV;  // TMA descriptors (tma_host.cu): Q/dO boxes (64, g, tpi), K/V (64, 1, 64)
   CUtensorMap tmDQ;                 // dQ fp32 boxes (32, g, tpi): the epilogue's store / reduce-add
   long long* trace;  // debug timeline (CTA 0), null in production
-  const __nv_bfloat16 *Q, *K, *V, *dO;
+  const __half *Q, *K, *V, *dO;  // fp16 staged copies
+  F16Scales sc;
   const float *lse, *delta;
   float* dQ;  // [N][h][128]
   int64_t N, h, h_K, g, W, n_super;
@@ -278,7 +283,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const __grid_c
       const int klo = CM ? 0 : (t - (int)p.W + 1 > 0 ? t - (int)p.W + 1 : 0);
       const int khi = !ok ? -1 : CM ? (int)((t + 1) / p.cmpBK) - 1 : t;
       const float lse_r = ok ? p.lse[j * p.N + t] * 1.4426950408889634f : 0.f;
-      const float dl = ok ? p.delta[j * p.N + t] : 0.f;
+      const float d16 = p.sc.v[c.it.kh] * p.sc.o[c.it.kh];
+      const float sl2 = p.scale_log2 / (p.sc.q[c.it.kh] * p.sc.k[c.it.kh]);
+      const float mul_q = p.scale / (kDS16 * p.sc.k[c.it.kh] * d16);
+      const float dl = ok ? p.delta[j * p.N + t] * d16 : 0.f;
       for (int kt = s.k0; kt < s.k1; ++kt, ++u) {
         mbar_wait_warp(bar(B_SF + w), (uint32_t)(u & 1));
         if (r == 0) DQ_TRACE(w, u, 1);  // S/dP landed
@@ -295,16 +303,17 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const __grid_c
 #pragma unroll
           for (int cc = 0; cc < 32; cc += 2) {
             const int key = kbase + hf * 32 + cc;
-            float p0 = ex2(fmaf(sv[cc], p.scale_log2, -lse_r));
-            float p1 = ex2(fmaf(sv[cc + 1], p.scale_log2, -lse_r));
+            float p0 = ex2(fmaf(sv[cc], sl2, -lse_r));
+            float p1 = ex2(fmaf(sv[cc + 1], sl2, -lse_r));
             if (!full) {
               p0 = (key >= klo && key <= khi) ? p0 : 0.f;
               p1 = (key + 1 >= klo && key + 1 <= khi) ? p1 : 0.f;
             }
-            dd[hf * 16 + (cc >> 1)] = pack_bf16(p0 * (dp[cc] - dl), p1 * (dp[cc + 1] - dl));
+            dd[hf * 16 + (cc >> 1)] =
+                pack_f16(p0 * ((dp[cc] - dl) * kDS16), p1 * ((dp[cc + 1] - dl) * kDS16));
           }
         }
-        tmem_st32u(tmem + lb, dd);  // dS over S: bf16 pairs, K-packed
+        tmem_st32u(tmem + lb, dd);  // dS over S: fp16 pairs, K-packed
         tmem_wait_st_();
         tc_fence_before();
         mbar_arrive(bar(B_PF + w));
@@ -326,8 +335,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const __grid_c
 #pragma unroll
         for (int cc = 0; cc < 8; ++cc)
           *reinterpret_cast<float4*>(box + sw128_off(r, cc)) =
-              make_float4(ov[4 * cc] * p.scale, ov[4 * cc + 1] * p.scale, ov[4 * cc + 2] * p.scale,
-                          ov[4 * cc + 3] * p.scale);
+              make_float4(ov[4 * cc] * mul_q, ov[4 * cc + 1] * mul_q, ov[4 * cc + 2] * mul_q,
+                          ov[4 * cc + 3] * mul_q);
       }
       fence_proxy_async();
       named_bar(1 + w, 128);
@@ -363,13 +372,15 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const __grid_c
 
 long long* g_dq_trace = nullptr;
 int tc_slide_dq(const fsa_shape* s, const void* Q, const void* K, const void* V, const void* dOut,
-                const void* lse, const void* delta, void* dQ, int accumulate, cudaStream_t st) {
+                const void* lse, const void* delta, void* dQ, int accumulate, F16Scales sc,
+                cudaStream_t st) {
   Params p{};
+  p.sc = sc;
   p.trace = g_dq_trace;
-  p.Q = (const __nv_bfloat16*)Q;
-  p.K = (const __nv_bfloat16*)K;
-  p.V = (const __nv_bfloat16*)V;
-  p.dO = (const __nv_bfloat16*)dOut;
+  p.Q = (const __half*)Q;
+  p.K = (const __half*)K;
+  p.V = (const __half*)V;
+  p.dO = (const __half*)dOut;
   p.lse = (const float*)lse;
   p.delta = (const float*)delta;
   p.dQ = (float*)dQ;
@@ -403,12 +414,13 @@ int tc_slide_dq(const fsa_shape* s, const void* Q, const void* K, const void* V,
 // Compressed-branch dQ += scale * dS K_cmp: the same
 // query-outer kernel over the formed pooled rows (Kb / Vb bf16 [b][h_K][128]).
 int tc_cmp_dq(const fsa_shape* s, const void* Q, const void* Kb, const void* Vb, const void* dOut,
-              const void* lse, const void* delta, void* dQ, cudaStream_t st) {
+              const void* lse, const void* delta, void* dQ, F16Scales sc, cudaStream_t st) {
   Params p{};
-  p.Q = (const __nv_bfloat16*)Q;
-  p.K = (const __nv_bfloat16*)Kb;
-  p.V = (const __nv_bfloat16*)Vb;
-  p.dO = (const __nv_bfloat16*)dOut;
+  p.sc = sc;
+  p.Q = (const __half*)Q;
+  p.K = (const __half*)Kb;
+  p.V = (const __half*)Vb;
+  p.dO = (const __half*)dOut;
   p.lse = (const float*)lse;
   p.delta = (const float*)delta;
   p.dQ = (float*)dQ;

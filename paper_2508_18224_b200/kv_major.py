@@ -252,9 +252,12 @@ def _backward_core(cfg, dt, q, k, v, do, sel, inv, out, lse, delta=None):
     dq_buf = _lib.dq_buffer(cfg, dq_code, dq_dtype, dev)
     dK = torch.empty((cfg.N, cfg.h_K, cfg.d_K), dtype=acc, device=dev)
     dV = torch.empty((cfg.N, cfg.h_K, cfg.d_V), dtype=acc, device=dev)
-    _lib.call("fsa_sel_bwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(q), _lib.ptr(k),
-              _lib.ptr(v), _lib.ptr(do), _lib.ptr(lse), _lib.ptr(delta), _lib.ptr(inv.offsets),
-              _lib.ptr(inv.qlist), _lib.ptr(inv.work), _lib.ptr(dq_buf), dq_code, _lib.ptr(dK), _lib.ptr(dV), st)
+    ops = _lib.F16Ops.of(cfg, q, k, v, do) if dq_code == _lib.DT_F16R else None  # tensor-core path
+    qq, kk, vv, dd = (q, k, v, do) if ops is None else (ops.q, ops.k, ops.v, ops.dout)
+    _lib.call("fsa_sel_bwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(qq), _lib.ptr(kk),
+              _lib.ptr(vv), _lib.ptr(dd), _lib.ptr(lse), _lib.ptr(delta), _lib.ptr(inv.offsets),
+              _lib.ptr(inv.qlist), _lib.ptr(inv.work), _lib.ptr(dq_buf), dq_code, _lib.ptr(dK),
+              _lib.ptr(dV), None if ops is None else _lib.ptr(ops.scales), st)
     dQ = torch.empty((cfg.N, cfg.h, cfg.d_K), dtype=acc, device=dev)
     _lib.call("fsa_dq_reduce", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(sel.idx),
               _lib.ptr(dq_buf), dq_code, _lib.ptr(dQ), st)

@@ -28,7 +28,7 @@ import torch
 
 from . import _lib
 from .kv_major import _backward_core, _sel_partials
-from .branches import _cmp_workspace, _slide_bwd_storage, _slide_fwd_storage
+from .branches import _cmp_workspace, _slide_bwd_storage, _slide_fwd_storage, _tc_qo
 from .config import make_config
 from .selection import SelectionTensor, build_inverse_index
 
@@ -53,6 +53,9 @@ class NSAContext:
     k_cmp: torch.Tensor = None
     v_cmp: torch.Tensor = None
     lse_cmp: torch.Tensor = None
+    # tensor-core path: the fp16 operands staged by the forward (Q16, V16 and
+    # their scales, _lib.F16Ops); the backward adds K16 and dO16
+    ops: object = None
 
 
 def _check(x, name, shape, dtype, dev):
@@ -104,8 +107,11 @@ def nsa_forward(q, k, v, tau, cfg, *, heads=None):
     s = _lib.shape_of(cfg)
     st = _lib.stream()
     (ob_code, _), _ = _lib.buffer_dtypes(cfg, dt)
-    # the tensor-core P.V products read V as its power-of-two scaled fp16 copy
-    v16 = _lib.v_to_f16(cfg, v) if ob_code == _lib.DT_F16 else None
+    # tensor-core path: the P.V products read V as its power-of-two scaled fp16
+    # copy and the compressed attention's S runs on the fp16 copy of Q (the
+    # operands its backward recomputes S from)
+    ops = _lib.F16Ops(cfg, dev).stage(q=q, v=v) if _tc_qo(cfg, dt) else None
+    v16 = None if ops is None else (ops.v, ops.block(2))
     n_pref = min(cfg.B_K - 1, cfg.N)
     Kc = torch.empty((cfg.b, cfg.h_K, cfg.d_K), dtype=acc, device=dev)
     Vc = torch.empty((cfg.b, cfg.h_K, cfg.d_V), dtype=acc, device=dev)
@@ -119,7 +125,8 @@ def nsa_forward(q, k, v, tau, cfg, *, heads=None):
     ws = _cmp_workspace(cfg, dev)
     _lib.call("fsa_cmp_attn_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(q), _lib.ptr(Kc),
               _lib.ptr(Vc), _lib.ptr(Kp), _lib.ptr(Vp), _lib.ptr(out_cmp), _lib.ptr(lse_cmp),
-              _lib.ptr(scores), _lib.ptr(ws), st)
+              _lib.ptr(scores), _lib.ptr(ws), None if ops is None else _lib.ptr(ops.q),
+              None if ops is None else _lib.ptr(ops.scales), st)
     idx = torch.empty((cfg.h_K, cfg.N, cfg.T), dtype=torch.int32, device=dev)
     _lib.call("fsa_select_topk", ctypes.byref(s), _lib.dt_code(acc), _lib.ptr(scores),
               _lib.ptr(idx), st)
@@ -142,6 +149,11 @@ def nsa_forward(q, k, v, tau, cfg, *, heads=None):
         q, out_cmp, lse_cmp = take(q, 1), take(out_cmp, 1), take(lse_cmp, 0)
         cfg = sub
         s = _lib.shape_of(cfg)
+        if ops is not None:  # the sub-group's Q16 (its own scale); V16 carries over
+            sops = _lib.F16Ops(cfg, dev).stage(q=q)
+            sops.v = ops.v
+            sops.block(2).copy_(ops.block(2))
+            ops = sops
     inv = build_inverse_index(sel, cfg, validate=False)
     # K5 writes the slot partials; the sliding branch runs before the merge so
     # that K6 can apply the gated combine (K12) in the same pass
@@ -156,7 +168,7 @@ def nsa_forward(q, k, v, tau, cfg, *, heads=None):
               st)
     del obuf, ml
     ctx = NSAContext(cfg, dt, q, k, v, tau, sel, inv, out_sel, lse_sel, out_slide, lse_slide,
-                     out_cmp, scores, Kc, Vc, lse_cmp)
+                     out_cmp, scores, Kc, Vc, lse_cmp, ops)
     return out, ctx
 
 
@@ -167,86 +179,64 @@ def nsa_backward(ctx: NSAContext, dout, *, full: bool = False):
     branch (attention over the pooled rows, the pooling and the prefix means;
     no reference backward -- SURVEY 8(f) rank 3) and returns
     (dQ, dK, dV, dtau) with the gate gradient dtau (N, 3).
-    dout: (N, h, d_V) storage in the step's dtype, contiguous, on the device."""
+    dout: (N, h, d_V) storage in the step's dtype, contiguous, on the device.
+
+    The gate (branches.py:103, d_c = tau_c dOut) folds into each branch's
+    statistics: tau exp(z - lse) = exp(z - (lse - ln tau)) and delta_c =
+    sum out_c * dOut, so every branch backward reads the raw dOut -- no gated
+    (and, in bf16, rounded) cotangent copies."""
     cfg, dt = ctx.cfg, ctx.dtype
     _check(dout, "dOut", (cfg.N, cfg.h, cfg.d_V), dt, ctx.q.device)
     s = _lib.shape_of(cfg)
     st = _lib.stream()
     acc = _lib.acc_dtype(dt)
-    delta_sel = torch.empty((cfg.h, cfg.N), dtype=acc, device=dout.device)
+    dev = dout.device
+    delta_sel = torch.empty((cfg.h, cfg.N), dtype=acc, device=dev)
     delta_slide = torch.empty_like(delta_sel)
-    _, (dq_code, _) = _lib.buffer_dtypes(cfg, dt)
-    tc = dq_code == _lib.DT_F16R
-    if full and tc:
-        # tensor-core path: the gate folds into all three branches' statistics
-        delta_cmp = torch.empty_like(delta_sel)
-        lse_cmp, lse_sel, lse_slide = (torch.empty_like(delta_sel) for _ in range(3))
-        dtau = torch.empty((cfg.N, 3), dtype=acc, device=dout.device)
+    lse_sel, lse_slide = torch.empty_like(delta_sel), torch.empty_like(delta_sel)
+    if full:
+        delta_cmp, lse_cmp = torch.empty_like(delta_sel), torch.empty_like(delta_sel)
+        dtau = torch.empty((cfg.N, 3), dtype=acc, device=dev)
         _lib.call("fsa_gate_backward_full_fold", ctypes.byref(s), _lib.dt_code(dt),
                   _lib.ptr(dout), _lib.ptr(ctx.tau), _lib.ptr(ctx.out_cmp), _lib.ptr(ctx.out_sel),
                   _lib.ptr(ctx.out_slide), _lib.ptr(ctx.lse_cmp), _lib.ptr(ctx.lse_sel),
                   _lib.ptr(ctx.lse_slide), _lib.ptr(delta_cmp), _lib.ptr(delta_sel),
                   _lib.ptr(delta_slide), _lib.ptr(lse_cmp), _lib.ptr(lse_sel), _lib.ptr(lse_slide),
                   _lib.ptr(dtau), st)
-        dQ, dK, dV = _sel_slide_backward(ctx, dout, dout, delta_sel, delta_slide, lse_sel, lse_slide)
-        nws = _lib.lib().fsa_cmp_bwd_workspace_bytes(ctypes.byref(s), _lib.dt_code(dt))
-        ws = torch.empty(nws, dtype=torch.uint8, device=dout.device)
-        _lib.call("fsa_cmp_bwd_fold", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(ctx.q),
-                  _lib.ptr(ctx.k_cmp), _lib.ptr(ctx.v_cmp), _lib.ptr(dout), _lib.ptr(ctx.tau),
-                  _lib.ptr(lse_cmp), _lib.ptr(delta_cmp), _lib.ptr(dQ), _lib.ptr(dK), _lib.ptr(dV),
-                  _lib.ptr(ws), st)
-        return dQ, dK, dV, dtau
-    if full:
-        d_sel, d_slide = torch.empty_like(dout), torch.empty_like(dout)
-        d_cmp = torch.empty_like(dout)
-        delta_cmp = torch.empty_like(delta_sel)
-        dtau = torch.empty((cfg.N, 3), dtype=acc, device=dout.device)
-        _lib.call("fsa_gate_backward_full", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(dout),
-                  _lib.ptr(ctx.tau), _lib.ptr(ctx.out_cmp), _lib.ptr(ctx.out_sel),
-                  _lib.ptr(ctx.out_slide), _lib.ptr(d_cmp), _lib.ptr(d_sel), _lib.ptr(d_slide),
-                  _lib.ptr(delta_cmp), _lib.ptr(delta_sel), _lib.ptr(delta_slide), _lib.ptr(dtau), st)
-        dQ, dK, dV = _sel_slide_backward(ctx, d_sel, d_slide, delta_sel, delta_slide)
-        nws = _lib.lib().fsa_cmp_bwd_workspace_bytes(ctypes.byref(s), _lib.dt_code(dt))
-        ws = torch.empty(nws, dtype=torch.uint8, device=dout.device)
-        _lib.call("fsa_cmp_bwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(ctx.q),
-                  _lib.ptr(ctx.k_cmp), _lib.ptr(ctx.v_cmp), _lib.ptr(d_cmp), _lib.ptr(ctx.lse_cmp),
-                  _lib.ptr(delta_cmp), _lib.ptr(dQ), _lib.ptr(dK), _lib.ptr(dV), _lib.ptr(ws), st)
-        return dQ, dK, dV, dtau
-    if tc:
-        # tensor-core path: the gate folds into the branch statistics (raw
-        # dOut, lse - ln tau, delta = sum out * dOut) -- no gated dOut copies
-        lse_sel = torch.empty_like(delta_sel)
-        lse_slide = torch.empty_like(delta_sel)
+    else:
         _lib.call("fsa_gate_backward_fold", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(dout),
                   _lib.ptr(ctx.tau), _lib.ptr(ctx.out_sel), _lib.ptr(ctx.out_slide),
                   _lib.ptr(ctx.lse_sel), _lib.ptr(ctx.lse_slide), _lib.ptr(delta_sel),
                   _lib.ptr(delta_slide), _lib.ptr(lse_sel), _lib.ptr(lse_slide), st)
-        return _sel_slide_backward(ctx, dout, dout, delta_sel, delta_slide, lse_sel, lse_slide)
-    # gate backward into both differentiated branches + their deltas, one pass
-    d_sel, d_slide = torch.empty_like(dout), torch.empty_like(dout)
-    _lib.call("fsa_gate_backward", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(dout),
-              _lib.ptr(ctx.tau), _lib.ptr(ctx.out_sel), _lib.ptr(ctx.out_slide), _lib.ptr(d_sel),
-              _lib.ptr(d_slide), _lib.ptr(delta_sel), _lib.ptr(delta_slide), st)
-    return _sel_slide_backward(ctx, d_sel, d_slide, delta_sel, delta_slide)
+    # tensor-core operands: the forward staged Q16 / V16, the backward adds K16 / dO16
+    ops = ctx.ops.stage(k=ctx.k, dout=dout) if ctx.ops is not None else None
+    dQ, dK, dV = _sel_slide_backward(ctx, dout, delta_sel, delta_slide, lse_sel, lse_slide, ops)
+    if not full:
+        return dQ, dK, dV
+    nws = _lib.lib().fsa_cmp_bwd_fold_workspace_bytes(ctypes.byref(s), _lib.dt_code(dt))
+    ws = torch.empty(max(nws, 1), dtype=torch.uint8, device=dev)
+    _lib.call("fsa_cmp_bwd_fold", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(ctx.q),
+              _lib.ptr(ctx.k_cmp), _lib.ptr(ctx.v_cmp), _lib.ptr(dout), _lib.ptr(ctx.tau),
+              _lib.ptr(lse_cmp), _lib.ptr(delta_cmp), _lib.ptr(dQ), _lib.ptr(dK), _lib.ptr(dV),
+              None if ops is None else _lib.ptr(ops.q), None if ops is None else _lib.ptr(ops.dout),
+              None if ops is None else _lib.ptr(ops.scales), _lib.ptr(ws), st)
+    return dQ, dK, dV, dtau
 
 
-def _sel_slide_backward(ctx: NSAContext, d_sel, d_slide, delta_sel, delta_slide, lse_sel=None,
-                        lse_slide=None):
-    """Selected + sliding backward from the gated cotangents and their deltas
-    (or, folded: the raw dOut with gate-adjusted lse -- fsa_gate_backward_fold)."""
+def _sel_slide_backward(ctx: NSAContext, dout, delta_sel, delta_slide, lse_sel, lse_slide, ops):
+    """Selected + sliding backward from the raw dOut with the gate folded into
+    each branch's statistics (lse - ln tau, delta = sum out * dOut).  ``ops``:
+    the fp16 operands (_lib.F16Ops) of the tensor-core path."""
     cfg, dt = ctx.cfg, ctx.dtype
-    lse_sel = ctx.lse_sel if lse_sel is None else lse_sel
-    lse_slide = ctx.lse_slide if lse_slide is None else lse_slide
     s = _lib.shape_of(cfg)
     st = _lib.stream()
     acc = _lib.acc_dtype(dt)
-    dout = d_sel
     _, (dq_code, dq_dtype) = _lib.buffer_dtypes(cfg, dt)
     if dq_code != _lib.DT_F16R:  # generic (f32 / f64 / small shapes) path
-        dQ, dK, dV = _backward_core(cfg, dt, ctx.q, ctx.k, ctx.v, d_sel, ctx.sel, ctx.inv,
+        dQ, dK, dV = _backward_core(cfg, dt, ctx.q, ctx.k, ctx.v, dout, ctx.sel, ctx.inv,
                                     ctx.out_sel, lse_sel, delta=delta_sel)
-        return _slide_bwd_storage(cfg, dt, ctx.q, ctx.k, ctx.v, d_slide, ctx.out_slide,
-                                  lse_slide, accumulate_into=(dQ, dK, dV), delta=delta_slide)
+        return _slide_bwd_storage(cfg, dt, ctx.q, ctx.k, ctx.v, dout, ctx.out_slide, lse_slide,
+                                  accumulate_into=(dQ, dK, dV), delta=delta_slide, ops=ops)
     # tensor-core path: K8 (selected) writes dK/dV and the fp16 dq partials;
     # the sliding backward adds its dK/dV in-kernel and writes its fp32 dQ
     # rows, which the dQ reduce (K9) adds while summing the partials -- every
@@ -256,16 +246,17 @@ def _sel_slide_backward(ctx: NSAContext, d_sel, d_slide, delta_sel, delta_slide,
     dq_buf = _lib.dq_buffer(cfg, dq_code, dq_dtype, dev)
     dK = torch.empty((cfg.N, cfg.h_K, cfg.d_K), dtype=acc, device=dev)
     dV = torch.empty((cfg.N, cfg.h_K, cfg.d_V), dtype=acc, device=dev)
-    _lib.call("fsa_sel_bwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(ctx.q), _lib.ptr(ctx.k),
-              _lib.ptr(ctx.v), _lib.ptr(d_sel), _lib.ptr(lse_sel), _lib.ptr(delta_sel),
+    _lib.call("fsa_sel_bwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(ops.q), _lib.ptr(ops.k),
+              _lib.ptr(ops.v), _lib.ptr(ops.dout), _lib.ptr(lse_sel), _lib.ptr(delta_sel),
               _lib.ptr(inv.offsets), _lib.ptr(inv.qlist), _lib.ptr(inv.work), _lib.ptr(dq_buf),
-              dq_code, _lib.ptr(dK), _lib.ptr(dV), st)
+              dq_code, _lib.ptr(dK), _lib.ptr(dV), _lib.ptr(ops.scales), st)
     dQ_slide = torch.empty((cfg.N, cfg.h, cfg.d_K), dtype=acc, device=dev)
     nws = _lib.lib().fsa_slide_bwd_workspace_bytes(ctypes.byref(s), _lib.dt_code(dt))
     ws = torch.empty(max(nws, 1), dtype=torch.uint8, device=dev)
-    _lib.call("fsa_slide_bwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(ctx.q), _lib.ptr(ctx.k),
-              _lib.ptr(ctx.v), _lib.ptr(d_slide), _lib.ptr(lse_slide), _lib.ptr(delta_slide),
-              _lib.ptr(dQ_slide), _lib.ptr(dK), _lib.ptr(dV), _lib.ptr(ws), 2, st)
+    _lib.call("fsa_slide_bwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(ops.q), _lib.ptr(ops.k),
+              _lib.ptr(ops.v), _lib.ptr(ops.dout), _lib.ptr(lse_slide), _lib.ptr(delta_slide),
+              _lib.ptr(dQ_slide), _lib.ptr(dK), _lib.ptr(dV), _lib.ptr(ws), 2, _lib.ptr(ops.scales),
+              st)
     dQ = torch.empty((cfg.N, cfg.h, cfg.d_K), dtype=acc, device=dev)
     _lib.call("fsa_dq_reduce_add", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(ctx.sel.idx),
               _lib.ptr(dq_buf), dq_code, _lib.ptr(dQ_slide), _lib.ptr(dQ), st)

@@ -40,7 +40,27 @@ def test_library_exports_every_declared_symbol(built):
     missing = [s for s in syms if s not in exported]
     assert not missing, missing
     assert sorted(_lib.SIGNATURES) == syms
-    assert built.fsa_abi_version() == 2
+    assert built.fsa_abi_version() == 3
+
+
+def _header_prototypes():
+    """name -> parameter count of every fsa_* prototype in include/fsa_b200.h."""
+    text = re.sub(r"/\*.*?\*/", "", open(HEADER).read(), flags=re.S)
+    protos = {}
+    for m in re.finditer(r"\b(?:int|size_t|void|const char\*)\s+(fsa_[a-z0-9_]+)\s*\(([^)]*)\)\s*;",
+                         text):
+        args = m.group(2).strip()
+        protos[m.group(1)] = 0 if args in ("", "void") else args.count(",") + 1
+    return protos
+
+
+def test_ctypes_signatures_match_header_arity():
+    """Every _lib.SIGNATURES entry passes as many arguments as the C prototype
+    declares (a short ctypes argtypes list silently misreads the stack)."""
+    protos = _header_prototypes()
+    assert sorted(protos) == sorted(_lib.SIGNATURES)
+    bad = {n: (len(a), protos[n]) for n, (a, _) in _lib.SIGNATURES.items() if len(a) != protos[n]}
+    assert not bad, bad
 
 
 def test_library_is_sm100a_only(built):
