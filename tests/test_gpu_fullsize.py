@@ -1,10 +1,14 @@
-"""Full-size parity of the NSA step at every BASELINE.json GPU shape.
+"""Full-size parity of the NSA step at every BASELINE.json GPU shape and at
+north_star's target (Llama-3-8B attention, 64K tokens).
 
-The whole-array oracle cannot run at 32K-128K tokens, so parity here rests on
-(1) size-independent structure checked on the whole device result and
-(2) the oracle's sampled-row restatement (oracle.nsa_rows / block_grads,
-pinned to the whole-array oracle by test_oracle_golden.py) on sampled tokens
-and KV blocks:
+Whole-array parity: for one complete KV group of every configuration the
+float64 oracle (oracle.selected_forward_backward, sliding_forward/backward,
+compressed_forward, select_topk -- pinned to the reference by
+test_oracle_golden.py) runs on the group's whole sequence, in worker
+processes (one per query head for the selected branch, one each for the
+sliding branch, the compressed branch and the top-k), and every element of
+out / out_sel / out_slide / out_cmp / lse / dQ / dK / dV of that group and
+its (N, T) selection are compared.  In addition, on the whole device result:
 
 * selection: ascending, causal, own block present, row length min(own+1, T),
   and bit-exact against the oracle's top-k on the GPU's own scores;
@@ -31,6 +35,7 @@ pytestmark = pytest.mark.gpu
 # BASELINE.json configs[1..4]; B_K = 64, T = 16, W = 512
 CONFIGS = {
     "llama3_8b_32k": dict(N=32768, h=32, h_K=8, bwd=True),
+    "llama3_8b_64k": dict(N=65536, h=32, h_K=8, bwd=True),  # north_star's target
     "qwen25_7b_64k_fwd": dict(N=65536, h=28, h_K=4, bwd=False),
     "gqa1_64k": dict(N=65536, h=16, h_K=16, bwd=True),
     "qwen3_14b_128k": dict(N=131072, h=40, h_K=8, bwd=True),
@@ -122,3 +127,122 @@ def test_fullsize_nsa_step(name):
     lhs = dV.double().sum(0)
     err = (lhs - rhs).norm() / rhs.norm()
     assert float(err) < 1e-2, f"{name}: dV column-sum identity off by {float(err):.2e}"
+
+
+# ---------------------------------------------------------------------------
+# whole-array parity of one complete KV group (every element, every branch)
+# ---------------------------------------------------------------------------
+
+_G = {}  # the group's float64 inputs, shared copy-on-write with the forked workers
+
+
+def _oracle_part(task):
+    """One piece of the float64 oracle for the group in _G, run in a worker;
+    arrays come back as float32 (8e-8 relative, far below the bf16 bound)."""
+    from threadpoolctl import threadpool_limits
+
+    kind, j = task
+    g, c1, cg, bwd = _G["g"], _G["c1"], _G["cg"], _G["bwd"]
+    Q, K, V, dO, tau = _G["Q"], _G["K"], _G["V"], _G["dO"], _G["tau"]
+    f32 = lambda x: np.asarray(x, dtype=np.float32)  # noqa: E731
+    with threadpool_limits(1):
+        if kind == "sel":  # query head j of the group (its dK/dV share: summed in head order)
+            q = Q[:, :, j:j + 1]
+            if bwd:
+                d = dO[:, :, j:j + 1] * tau[:, 1][:, None, None]
+                out, lse, dq, dk, dv = O.selected_forward_backward(q, K, V, _G["idx"], d, c1)
+                return kind, j, dict(out=f32(out), lse=lse, dQ=f32(dq), dK=dk, dV=dv)
+            out, lse = O.selected_forward(q, K, V, _G["idx"], c1)
+            return kind, j, dict(out=f32(out), lse=lse)
+        if kind == "slide":
+            out, lse = O.sliding_forward(Q, K, V, cg)
+            res = dict(out=f32(out), lse=lse)
+            if bwd:
+                dq, dk, dv = O.sliding_backward(Q, K, V, dO * tau[:, 2][:, None, None], cg)
+                res.update(dQ=f32(dq), dK=dk, dV=dv)
+            return kind, j, res
+        if kind == "cmp":
+            cmp = O.compress_kv(K, V, cg)
+            out, lse = O.compressed_forward(Q, cmp, cg)
+            scores = O.importance_scores(Q, cmp.K_cmp, cg)
+            return kind, j, dict(out=f32(out), lse=lse, scores=scores)
+        if kind == "topk":  # on the GPU's own scores (fp32 -> f64 exact)
+            return kind, j, dict(idx=O.select_topk(_G["scores"], cg))
+    raise ValueError(kind)
+
+
+def _whole_group(name, spec, q, k, v, do, tau, out, ctx, grads, kh):
+    import multiprocessing as mp
+
+    N, g = spec["N"], spec["h"] // spec["h_K"]
+    kw = dict(N=N, d_K=128, d_V=128, h=g, h_K=1, B_K=64, T=16, W=512)
+    js = slice(kh * g, (kh + 1) * g)
+    lg = lambda x: np.ascontiguousarray(_np(x).transpose(0, 2, 1)).astype(np.float64)  # noqa: E731
+    _G.clear()
+    _G.update(g=g, bwd=spec["bwd"], cg=O.cfg_of(**kw), c1=O.cfg_of(**dict(kw, h=1)),
+              Q=lg(q[:, js]), K=lg(k[:, kh:kh + 1]), V=lg(v[:, kh:kh + 1]),
+              dO=lg(do[:, js]) if spec["bwd"] else None, tau=tau.double().cpu().numpy(),
+              idx=ctx.sel.idx[kh:kh + 1].cpu().numpy(),
+              scores=ctx.scores[kh:kh + 1].double().cpu().numpy())
+    tasks = [("topk", 0), ("slide", 0), ("cmp", 0)] + [("sel", j) for j in range(g)]
+    import os
+    with mp.get_context("fork").Pool(max(1, min(len(tasks), os.cpu_count() or 1))) as pool:
+        parts = {}
+        for kind, j, res in pool.imap_unordered(_oracle_part, tasks):
+            parts[(kind, j)] = res
+    # selection of the whole group: bit-exact on the GPU's own scores
+    np.testing.assert_array_equal(parts[("topk", 0)]["idx"], _G["idx"])
+    lay = lambda x: x.transpose(0, 2, 1)  # noqa: E731  oracle (N, d, h) -> storage (N, h, d)
+    sel_out = np.concatenate([parts[("sel", j)]["out"] for j in range(g)], axis=2)
+    sel_lse = np.concatenate([parts[("sel", j)]["lse"] for j in range(g)], axis=0)
+    sl, cm = parts[("slide", 0)], parts[("cmp", 0)]
+    t = _G["tau"]
+    want = (t[:, 0][:, None, None] * cm["out"].astype(np.float64)
+            + t[:, 1][:, None, None] * sel_out + t[:, 2][:, None, None] * sl["out"])
+    tag = f"{name} kv{kh} (whole group)"
+    assert_close(_np(out[:, js]), lay(want), "bf16", f"{tag} out")
+    assert_close(_np(ctx.out_sel[:, js]), lay(sel_out), "bf16", f"{tag} out_sel")
+    assert_close(_np(ctx.out_slide[:, js]), lay(sl["out"]), "bf16", f"{tag} out_slide")
+    assert_close(_np(ctx.out_cmp[:, js]), lay(cm["out"]), "bf16", f"{tag} out_cmp")
+    for br, ref in (("sel", sel_lse), ("slide", sl["lse"]), ("cmp", cm["lse"])):
+        got = getattr(ctx, "lse_" + br)[js].double().cpu().numpy()
+        err = float(np.abs(got - ref).max())
+        assert err < 2e-2, f"{tag} lse_{br}: max abs err {err:.2e}"
+    # importance scores of the causal blocks (the ones top-k reads)
+    rows = np.arange(0, N, 4)  # every 4th token (the scores are N x b)
+    causal = np.arange(N // 64)[None, :] <= (rows // 64)[:, None]
+    assert_close(_G["scores"][0][rows][causal], cm["scores"][0][rows][causal], "bf16",
+                 f"{tag} scores")
+    if not spec["bwd"]:
+        return
+    dQ, dK, dV = grads
+    sel_dq = np.concatenate([parts[("sel", j)]["dQ"] for j in range(g)], axis=2)
+    want_dq = sel_dq.astype(np.float64) + sl["dQ"]
+    want_dk = sl["dK"].copy()
+    want_dv = sl["dV"].copy()
+    sk = sum(parts[("sel", j)]["dK"] for j in range(g))  # ascending head order
+    sv = sum(parts[("sel", j)]["dV"] for j in range(g))
+    want_dk, want_dv = sk + want_dk, sv + want_dv
+    assert_close(_np(dQ[:, js]), lay(want_dq), "bf16", f"{tag} dQ", grad=True)
+    assert_close(_np(dK[:, kh:kh + 1]), lay(want_dk), "bf16", f"{tag} dK", grad=True)
+    assert_close(_np(dV[:, kh:kh + 1]), lay(want_dv), "bf16", f"{tag} dV", grad=True)
+
+
+@pytest.mark.parametrize("name", list(CONFIGS))
+def test_fullsize_whole_group(name):
+    """Every element of one whole KV group (the last) against the float64 oracle."""
+    spec = CONFIGS[name]
+    kw = dict(N=spec["N"], d_K=128, d_V=128, h=spec["h"], h_K=spec["h_K"], B_K=64, T=16, W=512)
+    cfg = fsa.make_config(**kw)
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    bf = torch.bfloat16
+    N, h, hk = spec["N"], spec["h"], spec["h_K"]
+    q = torch.randn(N, h, 128, device="cuda", dtype=bf, generator=gen)
+    k = torch.randn(N, hk, 128, device="cuda", dtype=bf, generator=gen)
+    v = torch.randn(N, hk, 128, device="cuda", dtype=bf, generator=gen)
+    do = torch.randn(N, h, 128, device="cuda", dtype=bf, generator=gen)
+    tau = torch.rand(N, 3, device="cuda", generator=gen)
+    out, ctx = nsa.nsa_forward(q, k, v, tau, cfg)
+    grads = nsa.nsa_backward(ctx, do) if spec["bwd"] else None
+    torch.cuda.synchronize()
+    _whole_group(name, spec, q, k, v, do, tau, out, ctx, grads, hk - 1)
