@@ -45,15 +45,21 @@ extern "C" {
 #define FSA_ERR_CUDA 2
 #define FSA_ERR_UNSUPPORTED 3
 
-#define FSA_ABI_VERSION 3
+#define FSA_ABI_VERSION 4
 
 /* Element types.  FSA_DT_F16 and FSA_DT_F16R are buffer formats of the bf16
  * tensor-core path, never input dtypes:
- *   F16  obuf [h][N][T][128] fp16 partials O_i / l_i in the power-of-two scale
- *        s_kh of the fsa_v_to_f16 copy of V (the merge divides by vscale[kh]);
- *   F16R dq_buf = fp16 rows [h][N][T][128] followed by one int8 exponent e per
- *        row [h][N][T]: row value = fp16 * 2^-e (per-row scale, row max in
- *        [2^14, 2^15)) -- bytes h*N*T*(2*128 + 1). */
+ *   F16  obuf [R][128] fp16 partials O_i / l_i in the power-of-two scale s_kh
+ *        of the fsa_v_to_f16 copy of V (the merge divides by vscale[kh]), ml
+ *        [R] (m_i, l_i) fp32 pairs, R = fsa_partial_rows().  ITEM-MAJOR rows:
+ *        item n of the work plan (fsa_build_inverse) owns rows [128 n, 128 n +
+ *        128), row 128 n + (p % tpi) g + hh holding list position p of the
+ *        item's task for group head hh (tpi = 128 / g tokens per item);
+ *   F16R dq_buf = fp16 rows [h][N][T][128] (slot-indexed) followed by 4 int8
+ *        exponents per row [h][N][T] (one per 32 columns, int32-packed, low
+ *        byte first): value = fp16 * 2^-e (chunk max in [2^14, 2^15)) --
+ *        bytes h N T (2 * 128 + 4).
+ * Every other obuf / ml / dq_buf is slot-indexed [h][N][T][d] (R = h N T). */
 typedef enum {
   FSA_DT_F32 = 0, FSA_DT_F64 = 1, FSA_DT_BF16 = 2, FSA_DT_I32 = 3, FSA_DT_F16 = 4, FSA_DT_F16R = 5
 } fsa_dtype;
@@ -131,10 +137,16 @@ int fsa_select_topk(const fsa_shape* s, int score_dtype, const void* scores, int
 int fsa_validate_selection(const fsa_shape* s, const int32_t* idx, int32_t* flags, void* stream);
 
 /* build_inverse_index (selection.py:146-169) as CSR; flags as above (nullable).
- * work (nullable, [h_K*b + 1] int32) receives the tensor-core work plan: tasks
- * ordered block-major (task = i*h_K + kh, heavy early blocks first), each cut
- * into ceil(n_valid / (128/g)) items of <= 128 (token, head) rows; work[task]
- * is the exclusive prefix of item counts. */
+ * work (nullable; fsa_work_plan_bytes, int32) receives the tensor-core work
+ * plan: tasks task = kh * b + i (head-major), each cut into ceil(n_valid /
+ * (128/g)) items of <= 128 (token, head) rows; work[task] is the exclusive
+ * prefix of item counts (work[h_K b] the total), work[h_K b + 1] a scheduler
+ * counter, and from int32 offset ceil((h_K b + 2) / 32) * 32 the list position
+ * of every live selection entry [h_K][N][T] (the item-major buffer address). */
+size_t fsa_work_plan_bytes(const fsa_shape* s);
+/* Rows of the obuf / ml partial buffers for dtype's path (item-major on the
+ * tensor-core path: 128 x an upper bound of the item count; else h N T). */
+int64_t fsa_partial_rows(const fsa_shape* s, int dtype);
 size_t fsa_inverse_workspace_bytes(const fsa_shape* s);
 int fsa_build_inverse(const fsa_shape* s, const int32_t* idx, void* workspace, int32_t* offsets,
                       int32_t* qlist, int32_t* work, int32_t* flags, void* stream);
@@ -151,18 +163,19 @@ int fsa_sel_fwd(const fsa_shape* s, int dtype, int mode, const void* Q, const vo
 /* Merge of per-slot partials in ascending block order (kv_major.py:207-242;
  * stats merge kv_major.py:137-149, shared max :141-146).  out, lse, m_out,
  * l_out in acc dtype; m_out/l_out/lse nullable.  vscale: the V16 scales
- * (required with FSA_DT_F16 obuf, else ignored). */
-int fsa_merge_fwd(const fsa_shape* s, int dtype, int mode, const int32_t* idx, const void* obuf,
-                  int obuf_dtype, const void* ml, const void* m_global, const void* l_global,
-                  void* out, void* lse, void* m_out, void* l_out, int shared_max,
-                  const float* vscale, void* stream);
+ * (required with FSA_DT_F16 obuf, else ignored); work: the work plan of the
+ * item-major FSA_DT_F16 / FSA_DT_F16R buffers (ignored for the others). */
+int fsa_merge_fwd(const fsa_shape* s, int dtype, int mode, const int32_t* idx,
+                  const int32_t* work, const void* obuf, int obuf_dtype, const void* ml,
+                  const void* m_global, const void* l_global, void* out, void* lse, void* m_out,
+                  void* l_out, int shared_max, const float* vscale, void* stream);
 
 /* K6 + K12 fused for the NSA step: the LOCAL merge (as fsa_merge_fwd) writes the
  * selected branch's out_sel / lse (acc dtype) and, in the same pass, the gated
  * combine (branches.py:95-104) out = tau0 out_cmp + tau1 out_sel + tau2 out_slide
  * in dtype.  out_cmp / out_slide / tau in acc dtype. */
-int fsa_merge_combine_fwd(const fsa_shape* s, int dtype, const int32_t* idx, const void* obuf,
-                          int obuf_dtype, const void* ml, const float* vscale,
+int fsa_merge_combine_fwd(const fsa_shape* s, int dtype, const int32_t* idx, const int32_t* work,
+                          const void* obuf, int obuf_dtype, const void* ml, const float* vscale,
                           const void* out_cmp, const void* out_slide, const void* tau,
                           void* out_sel, void* lse, void* out, void* stream);
 

@@ -52,10 +52,12 @@ SIGNATURES = {
     "fsa_select_topk": ([_sp, _i, _vp, _vp, _vp], _i),
     "fsa_validate_selection": ([_sp, _vp, _vp, _vp], _i),
     "fsa_inverse_workspace_bytes": ([_sp], _sz),
+    "fsa_work_plan_bytes": ([_sp], _sz),
+    "fsa_partial_rows": ([_sp, _i], _i64),
     "fsa_build_inverse": ([_sp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "fsa_sel_fwd": ([_sp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp], _i),
-    "fsa_merge_fwd": ([_sp, _i, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp], _i),
-    "fsa_merge_combine_fwd": ([_sp, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
+    "fsa_merge_fwd": ([_sp, _i, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp], _i),
+    "fsa_merge_combine_fwd": ([_sp, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "fsa_bwd_delta": ([_sp, _i, _vp, _vp, _vp, _vp], _i),
     "fsa_sel_bwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp], _i),
     "fsa_dq_reduce": ([_sp, _i, _vp, _vp, _i, _vp, _vp], _i),
@@ -176,13 +178,21 @@ def buffer_dtypes(cfg, dtype):
     return (ob.value, _TORCH_OF[ob.value]), (dq.value, _TORCH_OF[dq.value])
 
 
+def partial_rows(cfg, dtype) -> int:
+    """Rows of the obuf / ml partial buffers (item-major tiles on the
+    tensor-core path, slot-indexed h N T otherwise; include/fsa_b200.h)."""
+    s = shape_of(cfg)
+    return int(lib().fsa_partial_rows(ctypes.byref(s), dt_code(dtype)))
+
+
 def dq_buffer(cfg, code, dtype, dev):
-    """The dq partial buffer: [h][N][T][d_K] of dtype, or for FSA_DT_F16R the
-    fp16 rows followed by one int8 exponent per row (include/fsa_b200.h)."""
+    """The dq partial buffer: slot-indexed rows [h N T][d_K] of dtype, or for
+    FSA_DT_F16R the fp16 rows followed by 4 int8 exponents per row
+    (include/fsa_b200.h)."""
+    rows = cfg.h * cfg.N * cfg.T
     if code == DT_F16R:
-        rows = cfg.h * cfg.N * cfg.T
-        return torch.empty(rows * (2 * cfg.d_K + 1), dtype=torch.uint8, device=dev)
-    return torch.empty((cfg.h, cfg.N, cfg.T, cfg.d_K), dtype=dtype, device=dev)
+        return torch.empty(rows * (2 * cfg.d_K + 4), dtype=torch.uint8, device=dev)
+    return torch.empty((rows, cfg.d_K), dtype=dtype, device=dev)
 
 
 def v_to_f16(cfg, v):

@@ -48,6 +48,13 @@ extern "C" int fsa_device_check(void) {
   return FSA_OK;
 }
 
+extern "C" int64_t fsa_partial_rows(const fsa_shape* s, int dtype) {
+  // tensor-core path: item-major tiles of 128 rows (common.cuh, work plan);
+  // otherwise slot-indexed rows [h][N][T]
+  if (fsa::tc_fwd_supported(*s, dtype)) return fsa::plan_max_items(*s) * 128;
+  return s->h * s->N * s->T;
+}
+
 extern "C" int fsa_buffer_dtypes(const fsa_shape* s, int dtype, int* obuf_dtype, int* dqbuf_dtype) {
   const bool tc = fsa::tc_fwd_supported(*s, dtype);
   if (obuf_dtype) *obuf_dtype = tc ? FSA_DT_F16 : (dtype == FSA_DT_F64 ? FSA_DT_F64 : FSA_DT_F32);

@@ -66,6 +66,33 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 void set_error(const char* fmt, ...);
 int check_launch(const char* what);
 
+// ---------------------------------------------------------------------------
+// Work plan of the tensor-core selected branch (fsa_build_inverse's `work`,
+// int32): [0, ntask] the item prefix over head-major tasks (task = kh * b + i;
+// an item is <= 128 rows = tpi tokens x g heads), [ntask + 1] the persistent
+// kernels' scheduler counter, then from plan_pos_offset the position of every
+// live selection entry (kh, t, slot) in its task's query list.  Item n owns
+// rows [128 n, 128 n + 128) of the partial buffers (obuf / ml / dq partials):
+// row 128 n + (p % tpi) g + hh for list position p and group head hh.
+// ---------------------------------------------------------------------------
+__host__ __device__ inline int64_t plan_ntask(const fsa_shape& s) { return s.h_K * (s.N / s.B_K); }
+__host__ __device__ inline int64_t plan_pos_offset(const fsa_shape& s) {
+  return ((plan_ntask(s) + 2 + 31) / 32) * 32;
+}
+__host__ __device__ inline int64_t plan_tpi(const fsa_shape& s) {
+  const int64_t g = s.h / s.h_K;
+  return g >= 128 ? 1 : 128 / g;
+}
+// item count bound: a valid selection has <= min(t / B_K + 1, T) entries per
+// token, so nnz <= B_K * sum_j min(j + 1, T) per kv head, and every task adds
+// at most one partial item
+inline int64_t plan_max_items(const fsa_shape& s) {
+  const int64_t b = s.N / s.B_K, T = s.T;
+  const int64_t cols = b <= T ? b * (b + 1) / 2 : T * (T + 1) / 2 + (b - T) * T;
+  const int64_t nnz = s.B_K * cols, tpi = plan_tpi(s);
+  return s.h_K * ((nnz + tpi - 1) / tpi + b);
+}
+
 }  // namespace fsa
 
 #define FSA_REQUIRE(cond, ...)            \

@@ -47,7 +47,7 @@ template <bool kScatter>
 __global__ void __launch_bounds__(kInvTile)
 inverse_tile_kernel(const int32_t* __restrict__ idx, int64_t N, int64_t B_K, int64_t b, int T,
                     int32_t* __restrict__ hist, const int32_t* __restrict__ offsets,
-                    int32_t* __restrict__ qlist, int32_t* flags) {
+                    int32_t* __restrict__ qlist, int32_t* flags, int32_t* __restrict__ pos) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint32_t* mask = reinterpret_cast<uint32_t*>(smem_raw);  // [b]
   int32_t* cnt = reinterpret_cast<int32_t*>(mask + b);     // [b]
@@ -88,6 +88,7 @@ inverse_tile_kernel(const int32_t* __restrict__ idx, int64_t N, int64_t B_K, int
         if (!live_entry(e, own)) continue;
         const int rank = cnt[e] + __popc(mask[e] & lt);
         ql[off[e] + base[e] + rank] = (int32_t)(t * T + s);
+        if (pos) pos[(kh * N + t) * T + s] = base[e] + rank;
       }
     }
     __syncwarp();
@@ -122,7 +123,7 @@ template <bool kScatter>
 __global__ void __launch_bounds__(kInvTile)
 inverse_tile_bits_kernel(const int32_t* __restrict__ idx, int64_t N, int64_t B_K, int64_t b, int T,
                          int32_t* __restrict__ hist, const int32_t* __restrict__ offsets,
-                         int32_t* __restrict__ qlist, int32_t* flags) {
+                         int32_t* __restrict__ qlist, int32_t* flags, int32_t* __restrict__ pos) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint32_t* mask = reinterpret_cast<uint32_t*>(smem_raw);  // [b][8]
   const int kh = blockIdx.y, tile = blockIdx.x, n_tiles = gridDim.x;
@@ -167,6 +168,7 @@ inverse_tile_bits_kernel(const int32_t* __restrict__ idx, int64_t N, int64_t B_K
       int rank = __popc(m[warp] & lt);
       for (int w = 0; w < warp; ++w) rank += __popc(m[w]);
       ql[off[e] + base[e] + rank] = (int32_t)(t * T + s);
+      if (pos) pos[((int64_t)kh * N + t) * T + s] = base[e] + rank;
     }
   }
 }
@@ -236,10 +238,11 @@ __global__ void inverse_scan_blocks_kernel(int32_t* __restrict__ offsets, int64_
   }
 }
 
-// Work plan for the persistent tensor-core kernels: tasks in heavy-first
-// order (task = block * h_K + kv head; early blocks attract the most rows),
-// each split into ceil(n_valid / tpi) items of tpi tokens x g heads <= 128 rows.
-// work[task] = exclusive prefix of the item counts; work[h_K * b] = total.
+// Work plan of the persistent tensor-core kernels (tc_plan.cuh: WorkPlan):
+// each task (kv head, block), task = kh * b + i (head-major, the order the
+// kernels claim them), is cut into ceil(n_valid / tpi) items of tpi tokens x
+// g heads <= 128 rows; work[task] = exclusive prefix of the item counts (the
+// item's 128-row tile in the partial buffers), work[h_K * b] = total.
 __global__ void work_plan_kernel(const int32_t* __restrict__ offsets, int64_t h_K, int64_t b,
                                  int tpi, int32_t* __restrict__ work) {
   __shared__ int32_t warp_tot[32];
@@ -252,7 +255,7 @@ __global__ void work_plan_kernel(const int32_t* __restrict__ offsets, int64_t h_
     const int64_t task = c0 + threadIdx.x;
     int32_t v = 0;
     if (task < ntask) {
-      const int64_t i = task / h_K, kh = task % h_K;
+      const int64_t kh = task / b, i = task % b;
       const int32_t n = offsets[kh * (b + 1) + i + 1] - offsets[kh * (b + 1) + i];
       v = (n + tpi - 1) / tpi;
     }
@@ -287,6 +290,10 @@ __global__ void work_plan_kernel(const int32_t* __restrict__ offsets, int64_t h_
 
 static int64_t n_tiles_of(const fsa_shape* s) { return (s->N + fsa::kInvTile - 1) / fsa::kInvTile; }
 
+extern "C" size_t fsa_work_plan_bytes(const fsa_shape* s) {
+  return (size_t)(fsa::plan_pos_offset(*s) + s->h_K * s->N * s->T) * sizeof(int32_t);
+}
+
 extern "C" size_t fsa_inverse_workspace_bytes(const fsa_shape* s) {
   const int64_t b = s->N / s->B_K;
   return (size_t)(s->h_K * n_tiles_of(s) * b) * sizeof(int32_t);
@@ -310,24 +317,25 @@ extern "C" int fsa_build_inverse(const fsa_shape* s, const int32_t* idx, void* w
     cudaFuncSetAttribute(fsa::inverse_tile_bits_kernel<true>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     fsa::inverse_tile_bits_kernel<false><<<grid, fsa::kInvTile, smem, st>>>(
-        idx, s->N, s->B_K, b, (int)s->T, hist, nullptr, nullptr, flags);
+        idx, s->N, s->B_K, b, (int)s->T, hist, nullptr, nullptr, flags, nullptr);
   } else {
     cudaFuncSetAttribute(fsa::inverse_tile_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     cudaFuncSetAttribute(fsa::inverse_tile_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     fsa::inverse_tile_kernel<false><<<grid, fsa::kInvTile, smem, st>>>(
-        idx, s->N, s->B_K, b, (int)s->T, hist, nullptr, nullptr, flags);
+        idx, s->N, s->B_K, b, (int)s->T, hist, nullptr, nullptr, flags, nullptr);
   }
   fsa::inverse_scan_tiles_kernel<<<(unsigned)((s->h_K * b + 255) / 256), 256, 0, st>>>(
       hist, offsets, s->h_K, nt, b);
   fsa::inverse_scan_blocks_kernel<<<(unsigned)s->h_K, 1024, 0, st>>>(offsets, b);
+  int32_t* pos = work ? work + fsa::plan_pos_offset(*s) : nullptr;
   if (bits)
     fsa::inverse_tile_bits_kernel<true><<<grid, fsa::kInvTile, smem, st>>>(
-        idx, s->N, s->B_K, b, (int)s->T, hist, offsets, qlist, nullptr);
+        idx, s->N, s->B_K, b, (int)s->T, hist, offsets, qlist, nullptr, pos);
   else
     fsa::inverse_tile_kernel<true><<<grid, fsa::kInvTile, smem, st>>>(
-        idx, s->N, s->B_K, b, (int)s->T, hist, offsets, qlist, nullptr);
+        idx, s->N, s->B_K, b, (int)s->T, hist, offsets, qlist, nullptr, pos);
   if (work) {
     const int64_t g = s->h / s->h_K;
     const int tpi = g >= 128 ? 1 : (int)(128 / g);

@@ -9,6 +9,9 @@
 // One warp per (j, t): lane k owns dims 4k..4k+3 (8-byte fp16 loads, 16-byte
 // fp32 stores -> every partial row is one coalesced 256 B request); the slot
 // statistics live one per lane and are reduced with shuffles.
+// The partial rows are item-major (common.cuh, work plan): slot s of (kh, t)
+// names block i = idx[kh][t][s] at list position p = pos[kh][t][s], i.e. row
+// 128 (item[kh b + i] + p / tpi) + (p % tpi) g + hh of the buffers.
 #include "common.cuh"
 #include <cuda_fp16.h>
 
@@ -44,27 +47,43 @@ struct Combine {
   __nv_bfloat16* out;
 };
 
+// item-major partial rows (common.cuh, work plan)
+struct ItemRows {
+  const int32_t* item;  // item prefix per task [h_K b + 1]
+  const int32_t* pos;   // list position per (kh, t, slot) [h_K][N][T]
+  int64_t b, N;
+  int tpi, g;
+  // row of slot s of (kh, t) -- its block blk -- for group head hh
+  __device__ __forceinline__ int64_t row(int64_t kh, int64_t t, int T, int s, int blk, int hh) const {
+    const int p = __ldg(pos + (kh * N + t) * T + s);
+    const int it = __ldg(item + kh * b + blk) + p / tpi;
+    return (int64_t)it * 128 + (int64_t)(p % tpi) * g + hh;
+  }
+};
+
 template <int TMAX>  // TMAX >= T: partial rows held in registers
 __global__ void __launch_bounds__(256) merge_f16_kernel(
     const int32_t* __restrict__ idx, const __half* __restrict__ obuf,
     const float2* __restrict__ ml, const float* __restrict__ vscale, float* __restrict__ out,
     float* __restrict__ lse, float* __restrict__ m_out, float* __restrict__ l_out, int64_t N,
-    int64_t h, int64_t g, int T, Combine cmb) {
+    int64_t h, int64_t g, int T, Combine cmb, ItemRows ir) {
   const int lane = threadIdx.x & 31;
   const int64_t wid = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (wid >= h * N) return;
   // consecutive warps take the g heads of one token (shared idx row)
   const int64_t t = wid / h, j = wid % h, kh = j / g;
-  const int len = row_len(idx + (kh * N + t) * T, T, lane);
-  const int64_t rb = (j * N + t) * (int64_t)T;
-  const __half* src = obuf + rb * kD + lane * 4;
+  const int32_t* irow = idx + (kh * N + t) * T;
+  const int len = row_len(irow, T, lane);
+  const int64_t my = lane < len ? ir.row(kh, t, T, lane, __ldg(irow + lane), (int)(j - kh * g)) : 0;
   // every partial row of this (head, token) is requested before the slot
   // statistics are reduced: one memory latency per warp, not two
   uint2 raw[TMAX];
 #pragma unroll
-  for (int s = 0; s < TMAX; ++s)
-    if (s < len) raw[s] = __ldcs(reinterpret_cast<const uint2*>(src + s * kD));
-  float2 st = lane < len ? __ldg(ml + rb + lane) : make_float2(-INFINITY, 0.f);
+  for (int s = 0; s < TMAX; ++s) {
+    const int64_t rs = __shfl_sync(0xffffffffu, my, s & 31);
+    if (s < len) raw[s] = __ldcs(reinterpret_cast<const uint2*>(obuf + rs * kD + lane * 4));
+  }
+  float2 st = lane < len ? __ldg(ml + my) : make_float2(-INFINITY, 0.f);
   float4 cm = make_float4(0.f, 0.f, 0.f, 0.f), cs = cm;
   float tw[3];
   if (cmb.out) {
@@ -122,26 +141,29 @@ __global__ void __launch_bounds__(256) merge_f16_long_kernel(
     const int32_t* __restrict__ idx, const __half* __restrict__ obuf,
     const float2* __restrict__ ml, const float* __restrict__ vscale, float* __restrict__ out,
     float* __restrict__ lse, float* __restrict__ m_out, float* __restrict__ l_out, int64_t N,
-    int64_t h, int64_t g, int T, Combine cmb) {
+    int64_t h, int64_t g, int T, Combine cmb, ItemRows ir) {
   const int lane = threadIdx.x & 31;
   const int64_t wid = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (wid >= h * N) return;
   const int64_t t = wid / h, j = wid % h, kh = j / g;
-  const int len = row_len(idx + (kh * N + t) * T, T, lane);
-  const int64_t rb = (j * N + t) * (int64_t)T;
+  const int32_t* irow = idx + (kh * N + t) * T;
+  const int len = row_len(irow, T, lane);
+  const int hh = (int)(j - kh * g);
   float M = -INFINITY;
-  for (int s = lane; s < len; s += 32) M = fmaxf(M, __ldg(ml + rb + s).x);
+  for (int s = lane; s < len; s += 32) M = fmaxf(M, __ldg(ml + ir.row(kh, t, T, s, __ldg(irow + s), hh)).x);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
   float L = 0.f;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int c = 0; c < len; c += 32) {
-    const float2 st = c + lane < len ? __ldg(ml + rb + c + lane) : make_float2(-INFINITY, 0.f);
+    const int64_t my = c + lane < len ? ir.row(kh, t, T, c + lane, __ldg(irow + c + lane), hh) : 0;
+    const float2 st = c + lane < len ? __ldg(ml + my) : make_float2(-INFINITY, 0.f);
     const float w = c + lane < len ? st.y * __expf(st.x - M) : 0.f;
     const int n = len - c < 32 ? len - c : 32;
     for (int s = 0; s < n; ++s) {  // ascending block order
       const float ws = __shfl_sync(0xffffffffu, w, s);
-      const float4 a = h4(__ldcs(reinterpret_cast<const uint2*>(obuf + (rb + c + s) * kD + lane * 4)));
+      const int64_t rs = __shfl_sync(0xffffffffu, my, s);
+      const float4 a = h4(__ldcs(reinterpret_cast<const uint2*>(obuf + rs * kD + lane * 4)));
       acc.x += ws * a.x; acc.y += ws * a.y; acc.z += ws * a.z; acc.w += ws * a.w;
       L += ws;
     }
@@ -177,10 +199,10 @@ __global__ void __launch_bounds__(256) merge_f16_long_kernel(
   }
 }
 
-// dq partial buffer (FSA_DT_F16R): fp16 rows [h][N][T][128] then one int8
-// exponent per row [h][N][T]; row value = fp16 * 2^-e.
+// dq partial buffer (FSA_DT_F16R): fp16 rows [h][N][T][128] then 4 int8
+// exponents per row (one per 32 columns) [h][N][T]; value = fp16 * 2^-e.
 __global__ void __launch_bounds__(256) dq_reduce_f16r_kernel(
-    const int32_t* __restrict__ idx, const __half* __restrict__ dq, const int8_t* __restrict__ dqe,
+    const int32_t* __restrict__ idx, const __half* __restrict__ dq, const int32_t* __restrict__ dqe,
     float* __restrict__ dQ, int64_t N, int64_t h, int64_t g, int T, const float* __restrict__ addend) {
   const int lane = threadIdx.x & 31;
   const int64_t wid = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -189,9 +211,10 @@ __global__ void __launch_bounds__(256) dq_reduce_f16r_kernel(
   const int len = row_len(idx + (kh * N + t) * T, T, lane);
   const int64_t rb = (j * N + t) * (int64_t)T;
   const __half* src = dq + rb * kD + lane * 4;
+  const int sh = 8 * (lane >> 3);  // this lane's 32-column chunk: exponent byte
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int c = 0; c < len; c += 32) {
-    const float sc = c + lane < len ? ldexpf(1.f, -(int)__ldg(dqe + rb + c + lane)) : 0.f;
+    const int32_t e4 = c + lane < len ? __ldg(dqe + rb + c + lane) : 0;
     const int n = len - c < 32 ? len - c : 32;
     int s = 0;
     for (; s + 4 <= n; s += 4) {  // four rows in flight per step
@@ -200,13 +223,15 @@ __global__ void __launch_bounds__(256) dq_reduce_f16r_kernel(
       for (int k = 0; k < 4; ++k) r[k] = __ldcs(reinterpret_cast<const uint2*>(src + (c + s + k) * kD));
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const float m = __shfl_sync(0xffffffffu, sc, s + k);
+        const int32_t e = __shfl_sync(0xffffffffu, e4, s + k);
+        const float m = ldexpf(1.f, -(int)(int8_t)(e >> sh));
         const float4 a = h4(r[k]);
         acc.x += a.x * m; acc.y += a.y * m; acc.z += a.z * m; acc.w += a.w * m;
       }
     }
     for (; s < n; ++s) {
-      const float m = __shfl_sync(0xffffffffu, sc, s);
+      const int32_t e = __shfl_sync(0xffffffffu, e4, s);
+      const float m = ldexpf(1.f, -(int)(int8_t)(e >> sh));
       const float4 a = h4(__ldcs(reinterpret_cast<const uint2*>(src + (c + s) * kD)));
       acc.x += a.x * m; acc.y += a.y * m; acc.z += a.z * m; acc.w += a.w * m;
     }
@@ -222,11 +247,23 @@ __global__ void __launch_bounds__(256) dq_reduce_f16r_kernel(
 
 bool fast_reduce_ok(const fsa_shape& s) { return s.d_V == kD && s.d_K == kD; }
 
-int merge_f16_fast(const fsa_shape* s, const int32_t* idx, const void* obuf, const void* ml,
-                   const float* vscale, void* out, void* lse, void* m_out, void* l_out,
-                   cudaStream_t st, const void* out_cmp, const void* out_slide, const void* tau,
-                   void* out_comb) {
+ItemRows item_rows(const fsa_shape* s, const int32_t* work) {
+  ItemRows ir;
+  ir.item = work;
+  ir.pos = work + plan_pos_offset(*s);
+  ir.b = s->N / s->B_K;
+  ir.N = s->N;
+  ir.tpi = (int)plan_tpi(*s);
+  ir.g = (int)(s->h / s->h_K);
+  return ir;
+}
+
+int merge_f16_fast(const fsa_shape* s, const int32_t* idx, const int32_t* work, const void* obuf,
+                   const void* ml, const float* vscale, void* out, void* lse, void* m_out,
+                   void* l_out, cudaStream_t st, const void* out_cmp, const void* out_slide,
+                   const void* tau, void* out_comb) {
   FSA_REQUIRE(vscale != nullptr, "merge: fp16 partials need the V16 scales (vscale)");
+  FSA_REQUIRE(work != nullptr, "merge: item-major fp16 partials need the work plan");
   const int64_t rows = s->h * s->N;
   if (rows == 0) return FSA_OK;
   Combine c{(const float*)out_cmp, (const float*)out_slide, (const float*)tau,
@@ -234,7 +271,7 @@ int merge_f16_fast(const fsa_shape* s, const int32_t* idx, const void* obuf, con
   auto kern = s->T <= 16 ? merge_f16_kernel<16> : s->T <= 32 ? merge_f16_kernel<32> : merge_f16_long_kernel;
   kern<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(
       idx, (const __half*)obuf, (const float2*)ml, vscale, (float*)out, (float*)lse,
-      (float*)m_out, (float*)l_out, s->N, s->h, s->h / s->h_K, (int)s->T, c);
+      (float*)m_out, (float*)l_out, s->N, s->h, s->h / s->h_K, (int)s->T, c, item_rows(s, work));
   FSA_LAUNCH_CHECK("merge_f16");
   return FSA_OK;
 }
@@ -244,7 +281,7 @@ int dq_reduce_f16r(const fsa_shape* s, const int32_t* idx, const void* dq, void*
   const int64_t rows = s->h * s->N;
   if (rows == 0) return FSA_OK;
   const __half* rows16 = (const __half*)dq;
-  const int8_t* ex = (const int8_t*)(rows16 + rows * s->T * kD);
+  const int32_t* ex = (const int32_t*)(rows16 + rows * s->T * kD);
   dq_reduce_f16r_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(
       idx, rows16, ex, (float*)dQ, s->N, s->h, s->h / s->h_K, (int)s->T, (const float*)addend);
   FSA_LAUNCH_CHECK("dq_reduce_f16r");

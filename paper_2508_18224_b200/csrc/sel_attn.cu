@@ -324,9 +324,10 @@ int sel_fwd_impl(const fsa_shape* s, int mode, const void* Q, const void* K, con
 }
 
 template <typename T>
-int merge_impl(const fsa_shape* s, int mode, const int32_t* idx, const void* obuf, int obuf_dtype,
-               const void* ml, const void* mg, const void* lg, void* out, void* lse, void* m_out,
-               void* l_out, int shared_max, const float* vscale, cudaStream_t st) {
+int merge_impl(const fsa_shape* s, int mode, const int32_t* idx, const int32_t* work,
+               const void* obuf, int obuf_dtype, const void* ml, const void* mg, const void* lg,
+               void* out, void* lse, void* m_out, void* l_out, int shared_max, const float* vscale,
+               cudaStream_t st) {
   using A = typename Acc<T>::type;
   const int64_t rows = s->h_K * s->N;
   if (rows == 0) return FSA_OK;
@@ -334,7 +335,7 @@ int merge_impl(const fsa_shape* s, int mode, const int32_t* idx, const void* obu
   if (obuf_dtype == FSA_DT_F16) {  // the tensor-core path's fp16 partials (LOCAL mode only)
     FSA_REQUIRE(mode == FSA_MERGE_LOCAL && fast_reduce_ok(*s) && sizeof(A) == 4,
                 "merge_fwd: fp16 partials only in LOCAL mode with d = 128");
-    return merge_f16_fast(s, idx, obuf, ml, vscale, out, lse, m_out, l_out, st);
+    return merge_f16_fast(s, idx, work, obuf, ml, vscale, out, lse, m_out, l_out, st);
   }
   {
     merge_generic<T, A><<<grid, 256, 0, st>>>(mode, idx, (const A*)obuf, (const A*)ml, (const A*)mg,
@@ -424,28 +425,30 @@ extern "C" int fsa_sel_fwd(const fsa_shape* s, int dtype, int mode, const void* 
 }
 
 extern "C" int fsa_merge_fwd(const fsa_shape* s, int dtype, int mode, const int32_t* idx,
-                             const void* obuf, int obuf_dtype, const void* ml, const void* m_global,
-                             const void* l_global, void* out, void* lse, void* m_out, void* l_out,
-                             int shared_max, const float* vscale, void* stream) {
+                             const int32_t* work, const void* obuf, int obuf_dtype, const void* ml,
+                             const void* m_global, const void* l_global, void* out, void* lse,
+                             void* m_out, void* l_out, int shared_max, const float* vscale,
+                             void* stream) {
   if (mode == FSA_MERGE_STATS && (!m_out || !l_out)) {
     fsa::set_error("merge_fwd: STATS mode needs m_out and l_out");
     return FSA_ERR_INVALID;
   }
-  DISPATCH_DT(dtype, merge_impl, s, mode, idx, obuf, obuf_dtype, ml, m_global, l_global, out, lse,
-              m_out, l_out, shared_max, vscale, (cudaStream_t)stream);
+  DISPATCH_DT(dtype, merge_impl, s, mode, idx, work, obuf, obuf_dtype, ml, m_global, l_global, out,
+              lse, m_out, l_out, shared_max, vscale, (cudaStream_t)stream);
 }
 
 extern "C" int fsa_merge_combine_fwd(const fsa_shape* s, int dtype, const int32_t* idx,
-                                     const void* obuf, int obuf_dtype, const void* ml,
+                                     const int32_t* work, const void* obuf, int obuf_dtype,
+                                     const void* ml,
                                      const float* vscale, const void* out_cmp,
                                      const void* out_slide, const void* tau, void* out_sel,
                                      void* lse, void* out, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (dtype == FSA_DT_BF16 && obuf_dtype == FSA_DT_F16 && fsa::fast_reduce_ok(*s))
-    return fsa::merge_f16_fast(s, idx, obuf, ml, vscale, out_sel, lse, nullptr, nullptr, st,
+    return fsa::merge_f16_fast(s, idx, work, obuf, ml, vscale, out_sel, lse, nullptr, nullptr, st,
                                out_cmp, out_slide, tau, out);
-  int rc = fsa_merge_fwd(s, dtype, FSA_MERGE_LOCAL, idx, obuf, obuf_dtype, ml, nullptr, nullptr,
-                         out_sel, lse, nullptr, nullptr, 0, vscale, stream);
+  int rc = fsa_merge_fwd(s, dtype, FSA_MERGE_LOCAL, idx, work, obuf, obuf_dtype, ml, nullptr,
+                         nullptr, out_sel, lse, nullptr, nullptr, 0, vscale, stream);
   if (rc) return rc;
   return fsa_gated_combine(s, dtype, out_cmp, out_sel, out_slide, tau, out, 0, stream);
 }

@@ -187,6 +187,16 @@ __device__ __forceinline__ void tma_scatter4_hint(const void* map, int col, cons
       "r"(col), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(src), "l"(pol)
       : "memory");
 }
+// 2-D tile store (bulk group) with an L2 cache-policy hint: the box of the
+// map at (col, row) from an SW128 shared tile
+__device__ __forceinline__ void tma_store_2d_hint(const void* map, int col, int row, uint32_t src,
+                                                  uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint"
+      " [%0, {%1, %2}], [%3], %4;" ::"l"(map),
+      "r"(col), "r"(row), "r"(src), "l"(pol)
+      : "memory");
+}
 // the reverse: 4 x 128 B from src (SW128 rows) to rows r[0..3] (bulk group);
 // rows outside the map are dropped
 __device__ __forceinline__ void tma_scatter4(const void* map, int col, const int32_t* r, uint32_t src) {

@@ -68,10 +68,11 @@ int tc_cmp_dq(const fsa_shape* s, const void* Q, const void* Kb, const void* Vb,
 // for d = 128, any T (merge_fast.cu); out / lse / m / l / dQ / addend fp32.
 // out_cmp / out_slide / tau / out_comb non-null: the gated combine in the same pass.
 bool fast_reduce_ok(const fsa_shape& s);
-int merge_f16_fast(const fsa_shape* s, const int32_t* idx, const void* obuf, const void* ml,
-                   const float* vscale, void* out, void* lse, void* m_out, void* l_out,
-                   cudaStream_t st, const void* out_cmp = nullptr, const void* out_slide = nullptr,
-                   const void* tau = nullptr, void* out_comb = nullptr);
+int merge_f16_fast(const fsa_shape* s, const int32_t* idx, const int32_t* work, const void* obuf,
+                   const void* ml, const float* vscale, void* out, void* lse, void* m_out,
+                   void* l_out, cudaStream_t st, const void* out_cmp = nullptr,
+                   const void* out_slide = nullptr, const void* tau = nullptr,
+                   void* out_comb = nullptr);
 int dq_reduce_f16r(const fsa_shape* s, const int32_t* idx, const void* dq, void* dQ,
                    cudaStream_t st, const void* addend = nullptr);
 

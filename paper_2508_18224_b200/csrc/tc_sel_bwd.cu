@@ -13,7 +13,10 @@
 //   dK^T += Q^T dS       M128(d) N64 K128(rows)  TMEM accumulator
 //   dQ_i  = dS K         M128 N128 K64  -> TMEM stage s (over the consumed S/dP)
 //                                        -> fp16 partial row of dq_buf with a
-//                                           per-row power-of-two exponent
+//                                           power-of-two exponent per 32 columns
+// dq partial rows are slot-indexed [h][N][T] (the dQ reduce then reads each
+// token's rows contiguously; item-major tiles measured no faster here and a
+// 1.6x slower reduce).
 // dQ partials are summed over the token's selected blocks in ascending block
 // order by the dq_reduce kernel (kv_major.py:326-340).
 //
@@ -91,7 +94,7 @@ struct Params {
   const int32_t *offsets, *qlist;
   int32_t* counter;
   __half* dq;         // [h][N][T][128] fp16 rows (FSA_DT_F16R) ...
-  int8_t* dqe;        // ... and their exponents [h][N][T]: value = row * 2^-e
+  int32_t* dqe;       // ... and 4 int8 exponents per row (one per 32 columns): value = x * 2^-e
   float *dK, *dV;     // [N][h_K][128]
   int64_t N, h, h_K, T, b, g, ntask;
   int64_t W;   // sliding mode: window; T is then the number of window slots
@@ -571,8 +574,7 @@ __global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const _
         int64_t t, slot;
         const bool ok = row_t(pos, ent, t, slot);
         if (ok) {
-          const int64_t j = tr.kh * p.g + hh;
-          drow = (j * p.N + t) * p.T + slot;
+          drow = ((tr.kh * p.g + hh) * p.N + t) * p.T + slot;
           // compressed mode: pooled row j is formed for t iff j < (t + 1) / B_K
           const int64_t hi = (SL == 2 ? (t + 1) / p.cmpBK - 1 : t) - tr.i * kBK;
           khi = hi < kBK - 1 ? (int)hi : kBK - 1;
@@ -596,7 +598,7 @@ __global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const _
         tc_fence_after();
         unsigned char* prow = smem + kOffP + s * 16384u;
         unsigned char* drw = smem + kOffDS + s * 16384u;
-        if (SL == 0) {  // the previous own item's dq scatter has read these buffers
+        if (SL == 0) {  // the previous own item's dq scatters have read these buffers
           if (lane < 16) bulk_wait_read();
           __syncwarp();
         }
@@ -654,27 +656,24 @@ __global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const _
           continue;
         }
         // rows -> SW128 staging tile [2 halves][128 rows][128 B] in this wg's
-        // consumed P (half 0) and dS (half 1) buffers, then 4-row tile::scatter4
-        // stores to the rows' dq partial slots (TMA: no LSU queue, so the next
-        // item's loads are not stuck behind 32 KB of stores).  fp16 with a
-        // per-row power-of-two scale (row max -> [2^14, 2^15)): 11-bit rows at
-        // the bf16 rows' traffic; the first pass over TMEM finds the row max.
-        float amax = 0.f;
+        // consumed P (half 0) and dS (half 1) buffers, then 4-row
+        // tile::scatter4 stores to the rows' dq partial slots (TMA: no LSU
+        // queue, so the next item's loads are not stuck behind 32 KB of
+        // stores).  fp16 with a
+        // power-of-two scale per 32 columns (chunk max -> [2^14, 2^15)):
+        // 11-bit rows at the bf16 rows' traffic, one pass over TMEM.
+        uint32_t ex4 = 0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           float v[32];
           tmem_ld32(tmem + lb + 128u * tm + q * 32, v);
           tmem_wait_ld();
+          float amax = 0.f;
 #pragma unroll
           for (int c = 0; c < 32; ++c) amax = fmaxf(amax, fabsf(v[c]));
-        }
-        const int ex = f16_row_exp(amax * mul_q);
-        const float mul = ldexpf(mul_q, ex);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          float v[32];
-          tmem_ld32(tmem + lb + 128u * tm + q * 32, v);
-          tmem_wait_ld();
+          const int ex = f16_row_exp(amax * mul_q);
+          const float mul = ldexpf(mul_q, ex);
+          ex4 |= (uint32_t)(ex & 0xff) << (8 * q);
           unsigned char* half = q < 2 ? prow : drw;
 #pragma unroll
           for (int c4 = 0; c4 < 4; ++c4) {
@@ -685,7 +684,7 @@ __global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const _
             *reinterpret_cast<uint4*>(half + sw128_off(r, (q & 1) * 4 + c4)) = u;
           }
         }
-        if (drow >= 0) p.dqe[drow] = (int8_t)ex;
+        if (drow >= 0) __stcs(p.dqe + drow, (int32_t)ex4);
         tc_fence_before();
         mbar_arrive(bar(B_SDE + tm));  // TMEM stage free for S/dP of item n+3
         if (r == 0) K8_TRACE(n, 6);  // dQ read out of TMEM
@@ -741,7 +740,7 @@ Params make_params(const fsa_shape* s, const void* Q, const void* K, const void*
   p.lse = (const float*)lse;
   p.delta = (const float*)delta;
   p.dq = (__half*)dq_buf;
-  p.dqe = dq_buf ? reinterpret_cast<int8_t*>(p.dq + s->h * s->N * s->T * kD) : nullptr;
+  p.dqe = dq_buf ? reinterpret_cast<int32_t*>(p.dq + s->h * s->N * s->T * kD) : nullptr;
   p.dK = (float*)dK;
   p.dV = (float*)dV;
   p.N = s->N;

@@ -5,6 +5,9 @@
 // for block i into the slot-indexed partial buffer that the merge kernel (K6)
 // combines.  S = Q K^T runs in bf16; O = P V in fp16 against the scaled fp16
 // copy of V (f16_stage.cu), so P is rounded to 11 bits instead of 8.
+// Partial rows are item-major (common.cuh, work plan): item n of the plan owns
+// rows [128 n, 128 n + 128), so each warp's 32 rows leave as two TMA tile
+// stores of 32 x 128 B instead of 16 four-row scatters.
 //
 // Persistent, warp-specialised, one CTA per SM:
 //   warps 0-7  two softmax + epilogue warpgroups ping-ponging over items, one
@@ -53,6 +56,7 @@ struct Params {
   const __nv_bfloat16 *Q, *K;
   const __half* V;  // the scaled fp16 copy (fsa_v_to_f16)
   const int32_t *offsets, *qlist;
+  const int32_t* work;  // item prefix per task (the item's row tile in obuf / ml)
   int32_t* counter;
   __half* obuf;
   float* ml;
@@ -270,6 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
     unsigned char* st = smem + kOffSt + warp * 4096u;
     const int kt_row = r / p.g, hh = r % p.g;
     int64_t prow = -1;  // obuf row of this thread's row in the pending item
+    int pitem = 0;      // the pending item's index in the plan
     float pm = 0.f, pl = 1.f;
     bool pend = false;
     int pend_n = 0;
@@ -279,18 +284,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
       mbar_wait(bar(B_OF + s1), (uint32_t)((m1 >> 1) & 1));
       tc_fence_after();
       const float inv = 1.f / pl;
-      int32_t rows[4];  // lanes 0-7: the obuf rows of row group `lane`
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int64_t d = __shfl_sync(0xffffffffu, prow, (4 * lane + i) & 31);
-        rows[i] = d >= 0 ? (int32_t)d : INT32_MAX;  // out of the map: dropped
-      }
-      // Partial rows leave by TMA tile::scatter4 (4 rows x 128 B per request)
-      // from an SW128 half tile per warp: off the LSU, which the loaders'
-      // gathers and the next item's entry loads share.
+      // The item's rows are contiguous: each warp's 32 rows leave by one TMA
+      // tile store per 64-column half from its SW128 staging tile -- off the
+      // LSU, which the loaders' gathers and the next item's entry loads share.
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
-        if (lane < 8) bulk_wait_read();  // the previous half's scatter has read the staging
+        if (lane == 0) bulk_wait_read();  // the previous half's store has read the staging
         __syncwarp();
 #pragma unroll
         for (int qq = 0; qq < 2; ++qq) {
@@ -313,18 +312,20 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
         }
         fence_proxy_async();
         __syncwarp();
-        if (lane < 8) {
-          tma_scatter4_hint(&p.tmO, hf * 64, rows, smem_u32(st) + (uint32_t)lane * 512u, l2_evict_first());
+        if (lane == 0) {
+          tma_store_2d_hint(&p.tmO, hf * 64, pitem * kRows + (warp & 3) * 32, smem_u32(st),
+                            l2_evict_first());
           bulk_commit();
         }
       }
-      if (prow >= 0) __stcs(reinterpret_cast<float2*>(p.ml + 2 * prow), make_float2(pm, pl));
+      __stcs(reinterpret_cast<float2*>(p.ml) + (int64_t)pitem * kRows + r, make_float2(pm, pl));
     };
     for (int k = 0;; ++k) {
       const int32_t task = ring.consume(k);
       if (task < 0) break;
       const TaskRows tr = task_rows(task, p.offsets, p.b, p.tpi);
       const int32_t* ql = p.qlist + (int64_t)tr.kh * p.N * p.T + tr.beg;
+      const int32_t ibase = tr.nitems > 0 ? __ldg(p.work + task) : 0;
       // entries of this warpgroup's items (every other item) are loaded one
       // own item ahead
       const int c0 = (int)((wg - n) & 1);
@@ -342,8 +343,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
         int64_t orow = -1;
         int vis = kBK;
         if (kt_row < p.tpi && pos < tr.ntok) {
-          const int t = (int)p.fdT.div((uint32_t)ent), slot = ent - t * p.T;
-          orow = ((int64_t)((int)tr.kh * p.g + hh) * p.N + t) * p.T + slot;
+          const int t = (int)p.fdT.div((uint32_t)ent);
+          orow = (int64_t)(ibase + c) * kRows + r;
           const int v = t - (int)tr.i * kBK + 1;
           vis = v < kBK ? v : kBK;
         }
@@ -398,6 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
         pend = true;
         pend_n = n;
         prow = orow;
+        pitem = ibase + c;
         pm = mx * p.scale;
         pl = sum;
       }
@@ -438,6 +440,7 @@ int tc_sel_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V,
   p.V = (const __half*)V;
   p.offsets = offsets;
   p.qlist = qlist;
+  p.work = work;
   p.obuf = (__half*)obuf;
   p.ml = (float*)ml;
   p.N = (int)s->N;
@@ -452,7 +455,7 @@ int tc_sel_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V,
   p.scale = (float)s->scale;
   p.scale_log2 = (float)(s->scale * 1.4426950408889634);
   p.counter = const_cast<int32_t*>(work) + p.ntask + 1;
-  if (int rc = make_tmap_rows(&p.tmO, obuf, s->h * s->N * s->T, 1)) return rc;
+  if (int rc = make_tmap_rows(&p.tmO, obuf, plan_max_items(*s) * kRows, 32)) return rc;
   cudaMemsetAsync(p.counter, 0, sizeof(int32_t), st);
   static unsigned long long done = 0;
   ensure_smem_attr(tc_sel_fwd_kernel, (int)kSmemBytes, done);

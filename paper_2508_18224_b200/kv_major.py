@@ -111,8 +111,9 @@ def _sel_partials(cfg, dt, q, k, v, inv, v16=None):
     vscale = None
     if ob_code == _lib.DT_F16:
         v, vscale = v16 if v16 is not None else _lib.v_to_f16(cfg, v)
-    obuf = torch.empty((cfg.h, cfg.N, cfg.T, cfg.d_V), dtype=ob_dtype, device=dev)
-    ml = torch.empty((cfg.h, cfg.N, cfg.T, 2), dtype=acc, device=dev)
+    rows = _lib.partial_rows(cfg, dt)  # item-major on the tensor-core path
+    obuf = torch.empty((rows, cfg.d_V), dtype=ob_dtype, device=dev)
+    ml = torch.empty((rows, 2), dtype=acc, device=dev)
     s = _lib.shape_of(cfg)
     _lib.call("fsa_sel_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.FWD_LOCAL, _lib.ptr(q),
               _lib.ptr(k), _lib.ptr(v), _lib.ptr(inv.offsets), _lib.ptr(inv.qlist), _lib.ptr(inv.work),
@@ -131,7 +132,8 @@ def _fused_forward(cfg, dt, q, k, v, sel, inv):
     out = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=acc, device=dev)
     lse = torch.empty((cfg.h, cfg.N), dtype=acc, device=dev)
     _lib.call("fsa_merge_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.MERGE_LOCAL,
-              _lib.ptr(sel.idx), _lib.ptr(obuf), ob_code, _lib.ptr(ml), None, None, _lib.ptr(out),
+              _lib.ptr(sel.idx), _lib.ptr(inv.work), _lib.ptr(obuf), ob_code, _lib.ptr(ml), None,
+              None, _lib.ptr(out),
               _lib.ptr(lse), None, None, 0, _lib.ptr(vscale), st)
     return out, lse
 
@@ -157,7 +159,7 @@ def compute_softmax_stats(Q, K, sel: SelectionTensor, cfg, *, shared_max: bool =
     m = torch.empty((cfg.h, cfg.N), dtype=acc, device=dev)
     l = torch.empty_like(m)
     _lib.call("fsa_merge_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.MERGE_STATS,
-              _lib.ptr(sel.idx), None, acc_code, _lib.ptr(ml), None, None, None, None, _lib.ptr(m),
+              _lib.ptr(sel.idx), _lib.ptr(inv.work), None, acc_code, _lib.ptr(ml), None, None, None, None, _lib.ptr(m),
               _lib.ptr(l), int(bool(shared_max)), None, st)
     if meter is not None:
         meter_stats(meter, inv.n_valid, cfg)
@@ -208,7 +210,7 @@ def reduce_forward(buf: OutputBuffer, inv: InverseIndex, stats: SoftmaxStats, cf
     lse = torch.empty((cfg.h, cfg.N), dtype=acc, device=dev)
     s = _lib.shape_of(cfg)
     _lib.call("fsa_merge_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.MERGE_REDUCE,
-              _lib.ptr(sel_idx), _lib.ptr(data), _lib.dt_code(acc), None, _lib.ptr(mg),
+              _lib.ptr(sel_idx), None, _lib.ptr(data), _lib.dt_code(acc), None, _lib.ptr(mg),
               _lib.ptr(lg), _lib.ptr(out), _lib.ptr(lse), None, None, 0, None, _lib.stream())
     if meter is not None:
         meter_reduce(meter, nv, cfg)

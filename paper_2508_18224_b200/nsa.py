@@ -163,7 +163,7 @@ def nsa_forward(q, k, v, tau, cfg, *, heads=None):
     lse_sel = torch.empty((cfg.h, cfg.N), dtype=acc, device=dev)
     out = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=dt, device=dev)
     _lib.call("fsa_merge_combine_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(sel.idx),
-              _lib.ptr(obuf), ob_code, _lib.ptr(ml), _lib.ptr(vscale), _lib.ptr(out_cmp),
+              _lib.ptr(inv.work), _lib.ptr(obuf), ob_code, _lib.ptr(ml), _lib.ptr(vscale), _lib.ptr(out_cmp),
               _lib.ptr(out_slide), _lib.ptr(tau), _lib.ptr(out_sel), _lib.ptr(lse_sel), _lib.ptr(out),
               st)
     del obuf, ml

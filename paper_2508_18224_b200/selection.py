@@ -169,8 +169,10 @@ def build_inverse_index(sel: SelectionTensor, cfg, *, validate: bool | None = No
     ws = torch.empty(max(1, ws_bytes), dtype=torch.uint8, device=dev)
     offsets = torch.empty((cfg.h_K, cfg.b + 1), dtype=torch.int32, device=dev)
     qlist = torch.empty((cfg.h_K, cfg.N * cfg.T), dtype=torch.int32, device=dev)
-    # work plan prefix [h_K*b + 1] + one scheduler counter slot (tc_sched.cuh)
-    work = torch.zeros((cfg.h_K * cfg.b + 2,), dtype=torch.int32, device=dev)
+    # work plan: item prefix [h_K*b + 1], a scheduler counter slot (tc_sched.cuh)
+    # and the list position of every selection entry (include/fsa_b200.h)
+    nw = _lib.lib().fsa_work_plan_bytes(ctypes.byref(s)) // 4
+    work = torch.empty((nw,), dtype=torch.int32, device=dev)
     flags = torch.zeros(1, dtype=torch.int32, device=dev)
     _lib.call("fsa_build_inverse", ctypes.byref(s), _lib.ptr(sel.idx), _lib.ptr(ws),
               _lib.ptr(offsets), _lib.ptr(qlist), _lib.ptr(work), _lib.ptr(flags), _lib.stream())

@@ -40,14 +40,14 @@ def test_library_exports_every_declared_symbol(built):
     missing = [s for s in syms if s not in exported]
     assert not missing, missing
     assert sorted(_lib.SIGNATURES) == syms
-    assert built.fsa_abi_version() == 3
+    assert built.fsa_abi_version() == 4
 
 
 def _header_prototypes():
     """name -> parameter count of every fsa_* prototype in include/fsa_b200.h."""
     text = re.sub(r"/\*.*?\*/", "", open(HEADER).read(), flags=re.S)
     protos = {}
-    for m in re.finditer(r"\b(?:int|size_t|void|const char\*)\s+(fsa_[a-z0-9_]+)\s*\(([^)]*)\)\s*;",
+    for m in re.finditer(r"\b(?:int64_t|int|size_t|void|const char\*)\s+(fsa_[a-z0-9_]+)\s*\(([^)]*)\)\s*;",
                          text):
         args = m.group(2).strip()
         protos[m.group(1)] = 0 if args in ("", "void") else args.count(",") + 1

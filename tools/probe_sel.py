@@ -43,8 +43,9 @@ def main():
     torch.cuda.synchronize()
     # separate timing of K5 and K6
     (ob_code, ob_dt), _ = _lib.buffer_dtypes(cfg, torch.bfloat16)
-    obuf = torch.empty((cfg.h, cfg.N, cfg.T, 128), dtype=ob_dt, device="cuda")
-    ml = torch.empty((cfg.h, cfg.N, cfg.T, 2), dtype=torch.float32, device="cuda")
+    rows = _lib.partial_rows(cfg, torch.bfloat16)
+    obuf = torch.empty((rows, 128), dtype=ob_dt, device="cuda")
+    ml = torch.empty((rows, 2), dtype=torch.float32, device="cuda")
     s = _lib.shape_of(cfg)
     v16, vscale = _lib.v_to_f16(cfg, v)
     t5, t6 = [], []
@@ -58,7 +59,7 @@ def main():
         l2 = torch.empty((cfg.h, cfg.N), dtype=torch.float32, device="cuda")
         ev[2].record()
         _lib.call("fsa_merge_fwd", ctypes.byref(s), _lib.DT_BF16, _lib.MERGE_LOCAL, _lib.ptr(sel.idx),
-                  _lib.ptr(obuf), ob_code, _lib.ptr(ml), None, None, _lib.ptr(o2), _lib.ptr(l2), None,
+                  _lib.ptr(inv.work), _lib.ptr(obuf), ob_code, _lib.ptr(ml), None, None, _lib.ptr(o2), _lib.ptr(l2), None,
                   None, 0, _lib.ptr(vscale), _lib.stream())
         ev[3].record()
         torch.cuda.synchronize()
