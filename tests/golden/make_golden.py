@@ -189,6 +189,24 @@ def malformed(ba):
     np.savez_compressed(os.path.join(HERE, "malformed.npz"), **out)
 
 
+def selection_fixtures(ba):
+    """Binary selection fixtures written by the reference's save_selection
+    (selection.py:201-206): the files themselves are the golden bytes that
+    paper_2508_18224_b200.save_selection must reproduce and load_selection
+    must read (test_selection.py:178-206)."""
+    meta = {}
+    for tag, cfg_kw, seed in (("sel_n32", dict(N=32, d_K=4, d_V=4, h=4, h_K=2, B_K=8, T=3), 8),
+                              ("sel_n8", dict(N=8, d_K=4, d_V=4, h=4, h_K=2, B_K=2, T=2), 12)):
+        cfg = ba.make_config(**cfg_kw)
+        scores = ba.rng.make_scores(cfg, seed)
+        sel = ba.select_topk_blocks(scores, cfg)
+        ba.save_selection(sel, os.path.join(HERE, tag + ".bin"))
+        meta[tag + "__cfg"] = json.dumps(cfg_kw)
+        meta[tag + "__scores"] = scores
+        meta[tag + "__idx"] = sel.idx
+    np.savez_compressed(os.path.join(HERE, "selection_fixtures.npz"), **meta)
+
+
 def acceptance_sweep(ba):
     """Criterion-3 style random scenarios (tests/helpers.py:75-99): store the
     configs and reference outputs for a size-bounded subset."""
@@ -231,11 +249,15 @@ def acceptance_sweep(ba):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", required=True, help="src dir of a built copy of the reference pkg")
+    ap.add_argument("--only", default=None, help="run one generator (e.g. selection_fixtures)")
     args = ap.parse_args()
     sys.path.insert(0, args.ref)
     import blockattn as ba
     import blockattn.rng  # noqa: F401
     assert ba.get_backend() == "compiled", "build the reference Cython core first"
+    if args.only:
+        globals()[args.only](ba)
+        return
     full_case(ba, "case_kv_small", dict(N=64, d_K=8, d_V=8, h=4, h_K=2, B_K=8, T=2, B_Q=8), 1)
     full_case(ba, "case_rect_dims", dict(N=64, d_K=8, d_V=16, h=4, h_K=2, B_K=8, T=3, B_Q=8), 21)
     full_case(ba, "case_pipeline", dict(N=128, d_K=16, d_V=16, h=8, h_K=2, B_K=16, T=3, W=24), 13,
@@ -248,6 +270,7 @@ def main():
               round_to="bf16", with_dense=False, token_stride=8, store=np.float32)
     selection_kats(ba)
     malformed(ba)
+    selection_fixtures(ba)
     acceptance_sweep(ba)
     total = sum(os.path.getsize(os.path.join(HERE, f)) for f in os.listdir(HERE) if f.endswith(".npz"))
     print(f"fixtures written: {total / 1e6:.2f} MB")

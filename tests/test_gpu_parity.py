@@ -692,3 +692,28 @@ def test_v_to_f16_scales_per_kv_head():
         big = vd[:, kh].abs() * s >= 2.0 ** -14  # fp16 normal range: exact
         got = v16[:, kh].double()
         assert torch.equal(got[big], (vd[:, kh] * s)[big])
+
+
+# ---------------------------------------------------------------------------
+# selection fixtures (selection.py:201-218): byte-identical with the reference
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("tag", ["sel_n32", "sel_n8"])
+def test_selection_fixture_round_trip(tag, tmp_path):
+    """GPU top-k of the stored scores, saved, reproduces the reference-written
+    file byte for byte; loading that file gives the same device selection
+    (test_selection.py:178-196)."""
+    import os
+    from golden_io import GOLDEN
+    z = load("selection_fixtures")
+    kw = json.loads(str(z[tag + "__cfg"]))
+    cfg = _cfg(kw)
+    ref_bytes = open(os.path.join(GOLDEN, tag + ".bin"), "rb").read()
+    sel = fsa.select_topk_blocks(torch.from_numpy(z[tag + "__scores"]).cuda(), cfg)
+    path = tmp_path / "sel.bin"
+    fsa.save_selection(sel, path)
+    assert path.read_bytes() == ref_bytes
+    loaded = fsa.load_selection(os.path.join(GOLDEN, tag + ".bin"))
+    assert loaded.idx.is_cuda
+    np.testing.assert_array_equal(host(loaded.idx), host(sel.idx))
+    fsa.validate_selection(loaded, cfg)

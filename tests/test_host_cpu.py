@@ -177,3 +177,43 @@ def test_bench_reference_arm_json_contract():
     assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
     assert d["e2e"] == {"value": d["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}
+
+
+# ---------------------------------------------------------------------------
+# selection fixture format (selection.py:201-218): reference-written bytes
+# ---------------------------------------------------------------------------
+
+def _fixture(tag):
+    from golden_io import GOLDEN, load
+    z = load("selection_fixtures")
+    raw = open(os.path.join(GOLDEN, tag + ".bin"), "rb").read()
+    return json.loads(str(z[tag + "__cfg"])), z[tag + "__scores"], z[tag + "__idx"], raw
+
+
+@pytest.mark.parametrize("tag", ["sel_n32", "sel_n8"])
+def test_selection_fixture_layout_and_oracle(tag):
+    """The reference wrote header (h_K, N, T) + row-major int32 body
+    (test_selection.py:187-196); the oracle's top-k of the stored scores is
+    that body."""
+    from oracle import fsa_oracle as O
+    kw, scores, idx, raw = _fixture(tag)
+    c = O.cfg_of(**kw)
+    header = np.frombuffer(raw[:12], dtype="<i4")
+    np.testing.assert_array_equal(header, [c.h_K, c.N, c.T])
+    body = np.frombuffer(raw[12:], dtype="<i4").reshape(c.h_K, c.N, c.T)
+    np.testing.assert_array_equal(body, idx)
+    np.testing.assert_array_equal(O.select_topk(scores, c), idx)
+
+
+def test_load_selection_rejects_truncated_and_mismatched(tmp_path):
+    """test_selection.py:199-206: truncated body, short header and a header
+    that disagrees with the body all raise 'malformed selection'."""
+    from paper_2508_18224_b200.selection import SelectionError, load_selection
+    _, _, _, raw = _fixture("sel_n32")
+    cases = {"body": raw[:-8], "header": raw[:10], "mismatch": raw[:4] + (99).to_bytes(4, "little") + raw[8:],
+             "zero": (0).to_bytes(4, "little") + raw[4:12]}
+    for name, data in cases.items():
+        p = tmp_path / f"{name}.bin"
+        p.write_bytes(data)
+        with pytest.raises(SelectionError, match="malformed selection"):
+            load_selection(p)
