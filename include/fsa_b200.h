@@ -323,17 +323,6 @@ int fsa_qm_bwd(const fsa_shape* s, int dtype, const void* Q, const void* K, cons
 /* Finiteness check for as_headed (config.py:146-155): *flag |= 1 on any non-finite. */
 int fsa_check_finite(int dtype, const void* x, int64_t n, int32_t* flag, void* stream);
 
-/* Debugging: record a per-item clock64 timeline of CTA 0 of the next launches
- * of the selected/sliding backward (K8), sliding dQ and window forward kernels
- * into a device int64 buffer (tools/trace_k8.py, trace_dq.py, trace_qo.py);
- * NULL turns it off.  Not for production use. */
-void fsa_debug_bwd_trace(void* device_buf);
-void fsa_debug_dq_trace(void* device_buf);
-void fsa_debug_qo_trace(void* device_buf);
-/* Debugging: TMA tile::gather4 / tile::scatter4 round trip of n rows (tools/gather4_test.py). */
-int fsa_debug_gather4_test(const void* src, int64_t rows, const int32_t* idx, const int32_t* idx2,
-                           int n, int box_rows, void* out, void* out2, int64_t rows2, void* stream);
-
 #ifdef __cplusplus
 }
 #endif

@@ -13,7 +13,10 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfsa_b200.so")
+# FSA_TRACE_LIB=1 loads the trace build (build.py --trace: the product kernels
+# plus the include/fsa_b200_trace.h timeline hooks; development tools only)
+TRACE = os.environ.get("FSA_TRACE_LIB") == "1"
+LIB_PATH = os.path.join(_HERE, "libfsa_b200_trace.so" if TRACE else "libfsa_b200.so")
 
 FSA_OK, FSA_ERR_INVALID, FSA_ERR_CUDA, FSA_ERR_UNSUPPORTED = 0, 1, 2, 3
 DT_F32, DT_F64, DT_BF16, DT_I32, DT_F16, DT_F16R = 0, 1, 2, 3, 4, 5
@@ -79,11 +82,17 @@ SIGNATURES = {
     "fsa_gate_backward_full": ([_sp, _i] + [_vp] * 13, _i),
     "fsa_qm_fwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "fsa_qm_bwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
+    "fsa_check_finite": ([_i, _vp, _i64, _vp, _vp], _i),
+}
+
+
+# include/fsa_b200_trace.h: only in libfsa_b200_trace.so
+TRACE_SIGNATURES = {
     "fsa_debug_bwd_trace": ([_vp], None),
     "fsa_debug_dq_trace": ([_vp], None),
     "fsa_debug_qo_trace": ([_vp], None),
+    "fsa_debug_sel_fwd_trace": ([_vp], None),
     "fsa_debug_gather4_test": ([_vp, ctypes.c_int64, _vp, _vp, _i, _i, _vp, _vp, ctypes.c_int64, _vp], _i),
-    "fsa_check_finite": ([_i, _vp, _i64, _vp, _vp], _i),
 }
 
 
@@ -103,7 +112,7 @@ def lib():
                 f"{LIB_PATH} is not built; run `python -m paper_2508_18224_b200.build` "
                 "(the FSA operators have no CPU fallback)")
         l = ctypes.CDLL(LIB_PATH)
-        for name, (args, res) in SIGNATURES.items():
+        for name, (args, res) in {**SIGNATURES, **(TRACE_SIGNATURES if TRACE else {})}.items():
             fn = getattr(l, name)
             fn.argtypes = args
             fn.restype = res

@@ -2,6 +2,8 @@
 
     python -m paper_2508_18224_b200.build        # incremental
     python -m paper_2508_18224_b200.build --force
+    python -m paper_2508_18224_b200.build --trace   # libfsa_b200_trace.so (-DFSA_TRACE:
+                                                    # include/fsa_b200_trace.h hooks, tools/trace_*.py)
 
 nvcc cross-compiles without a GPU.  Objects go to paper_2508_18224_b200/build/,
 the shared library next to this file so it travels with gpurun snapshots.
@@ -21,6 +23,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "libfsa_b200.so")
+TRACE_OBJ = os.path.join(PKG, "build_trace")
+TRACE_LIB = os.path.join(PKG, "libfsa_b200_trace.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -39,43 +43,46 @@ def _stale(src, obj, deps):
     return any(os.path.getmtime(p) > t for p in [src] + deps)
 
 
-def _compile(src, obj, verbose):
-    cmd = [NVCC] + FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-c", src, "-o", obj]
+def _compile(src, obj, verbose, extra=()):
+    cmd = [NVCC] + FLAGS + list(extra) + (["-Xptxas", "-v"] if verbose else []) + ["-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {os.path.basename(src)}:\n{r.stderr}")
     return r.stderr
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+    obj_dir, lib = (TRACE_OBJ, TRACE_LIB) if trace else (OBJ, LIB)
+    extra = ["-DFSA_TRACE"] if trace else []
+    os.makedirs(obj_dir, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     deps = _headers()
     jobs = []
     for src in srcs:
-        obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
+        obj = os.path.join(obj_dir, os.path.basename(src)[:-3] + ".o")
         if force or _stale(src, obj, deps):
             jobs.append((src, obj))
     if jobs:
         with cf.ThreadPoolExecutor(max_workers=min(8, len(jobs))) as ex:
-            futs = {ex.submit(_compile, s, o, verbose): s for s, o in jobs}
+            futs = {ex.submit(_compile, s, o, verbose, extra): s for s, o in jobs}
             for f in cf.as_completed(futs):
                 log = f.result()
                 if verbose and log:
                     print(os.path.basename(futs[f]), log, file=sys.stderr)
-    objs = [os.path.join(OBJ, os.path.basename(s)[:-3] + ".o") for s in srcs]
-    if force or jobs or not os.path.exists(LIB) or any(
-            os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs
+    objs = [os.path.join(obj_dir, os.path.basename(s)[:-3] + ".o") for s in srcs]
+    if force or jobs or not os.path.exists(lib) or any(
+            os.path.getmtime(o) > os.path.getmtime(lib) for o in objs):
+        cmd = [NVCC] + ARCH + ["-shared", "-o", lib] + objs
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("link failed:\n" + r.stderr)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("-v", "--verbose", action="store_true")
+    ap.add_argument("--trace", action="store_true")
     a = ap.parse_args()
-    print(build(force=a.force, verbose=a.verbose))
+    print(build(force=a.force, verbose=a.verbose, trace=a.trace))

@@ -68,20 +68,76 @@ int check_launch(const char* what);
 
 // ---------------------------------------------------------------------------
 // Work plan of the tensor-core selected branch (fsa_build_inverse's `work`,
-// int32): [0, ntask] the item prefix over head-major tasks (task = kh * b + i;
-// an item is <= 128 rows = tpi tokens x g heads), [ntask + 1] the persistent
-// kernels' scheduler counter, then from plan_pos_offset the position of every
-// live selection entry (kh, t, slot) in its task's query list.  Item n owns
-// rows [128 n, 128 n + 128) of the partial buffers (obuf / ml / dq partials):
-// row 128 n + (p % tpi) g + hh for list position p and group head hh.
+// int32), token-chunked: the tokens are cut into chunks of C (a multiple of
+// 256) and a task is (kv head kh, chunk c, block i) -- the entries of block
+// i's query list whose token lies in chunk c (a contiguous sub-list: lists are
+// token-sorted).  Tasks are numbered kh-major, then chunk, then block, the
+// order the persistent kernels claim them, so at any time every CTA gathers
+// query rows of the same C tokens of one kv head (an L2-resident working set
+// for small C; measured not to pay, so C = N by default).  Chunk c holds the blocks
+// that a token of it can select, i < bic(c) = min(b, (min((c+1) C, N) - 1) / B_K + 1).
+//
+//   [0] C  [1] nc  [2] tasks per kv head  [3] scheduler counter
+//   [64, 64 + nc)            task base of chunk c within a kv head
+//   item  [ntask + 1]        exclusive prefix of item counts (an item is <= 128
+//                            rows = tpi tokens x g heads); item n owns rows
+//                            [128 n, 128 n + 128) of the partial buffers
+//   tbeg  [ntask]            first entry of the task in the kv head's qlist
+//   tn    [ntask]            entries of the task
+//   tki   [ntask]            kh * b + i
+//   pos   [h_K][N][T]        position of entry (kh, t, slot) in its task's
+//                            sub-list: its row is 128 (item[task] + p / tpi)
+//                            + (p % tpi) g + hh
 // ---------------------------------------------------------------------------
-__host__ __device__ inline int64_t plan_ntask(const fsa_shape& s) { return s.h_K * (s.N / s.B_K); }
-__host__ __device__ inline int64_t plan_pos_offset(const fsa_shape& s) {
-  return ((plan_ntask(s) + 2 + 31) / 32) * 32;
-}
+constexpr int kPlanMaxChunks = 64;
+constexpr int64_t kPlanHeader = 128;
 __host__ __device__ inline int64_t plan_tpi(const fsa_shape& s) {
   const int64_t g = s.h / s.h_K;
   return g >= 128 ? 1 : 128 / g;
+}
+// C (inverse.cu): N by default (one chunk); FSA_CHUNK_TOKENS overrides it
+int64_t plan_chunk_tokens(const fsa_shape& s);
+__host__ __device__ inline int64_t plan_bic(const fsa_shape& s, int64_t C, int64_t c) {
+  const int64_t b = s.N / s.B_K;
+  const int64_t tend = (c + 1) * C < s.N ? (c + 1) * C : s.N;
+  const int64_t n = (tend - 1) / s.B_K + 1;
+  return n < b ? n : b;
+}
+inline int64_t plan_nchunks(const fsa_shape& s) {
+  const int64_t C = plan_chunk_tokens(s);
+  return s.N <= 0 ? 0 : (s.N + C - 1) / C;
+}
+inline int64_t plan_tasks_per_head(const fsa_shape& s) {
+  const int64_t C = plan_chunk_tokens(s), nc = plan_nchunks(s);
+  int64_t n = 0;
+  for (int64_t c = 0; c < nc; ++c) n += plan_bic(s, C, c);
+  return n;
+}
+inline int64_t plan_ntask(const fsa_shape& s) { return s.h_K * plan_tasks_per_head(s); }
+inline int64_t align32(int64_t x) { return (x + 31) / 32 * 32; }
+inline int64_t plan_item_offset(const fsa_shape&) { return kPlanHeader; }
+inline int64_t plan_tbeg_offset(const fsa_shape& s) { return align32(kPlanHeader + plan_ntask(s) + 1); }
+inline int64_t plan_tn_offset(const fsa_shape& s) { return plan_tbeg_offset(s) + align32(plan_ntask(s)); }
+inline int64_t plan_tki_offset(const fsa_shape& s) { return plan_tn_offset(s) + align32(plan_ntask(s)); }
+inline int64_t plan_pos_offset(const fsa_shape& s) { return plan_tki_offset(s) + align32(plan_ntask(s)); }
+// device view of a plan (built by fsa_build_inverse)
+struct PlanView {
+  const int32_t *item, *tbeg, *tn, *tki, *pos, *cbase;
+  int32_t* counter;
+  int32_t C, nph;
+};
+inline PlanView plan_view(const fsa_shape& s, const int32_t* work) {
+  PlanView v;
+  v.item = work + plan_item_offset(s);
+  v.tbeg = work + plan_tbeg_offset(s);
+  v.tn = work + plan_tn_offset(s);
+  v.tki = work + plan_tki_offset(s);
+  v.pos = work + plan_pos_offset(s);
+  v.cbase = work + 64;
+  v.counter = const_cast<int32_t*>(work) + 3;
+  v.C = (int32_t)plan_chunk_tokens(s);
+  v.nph = (int32_t)plan_tasks_per_head(s);
+  return v;
 }
 // item count bound: a valid selection has <= min(t / B_K + 1, T) entries per
 // token, so nnz <= B_K * sum_j min(j + 1, T) per kv head, and every task adds
@@ -90,7 +146,7 @@ inline int64_t plan_max_items(const fsa_shape& s) {
   const int64_t b = s.N / s.B_K, T = s.T;
   const int64_t cols = b <= T ? b * (b + 1) / 2 : T * (T + 1) / 2 + (b - T) * T;
   const int64_t nnz = s.B_K * cols, tpi = plan_tpi(s);
-  return s.h_K * ((nnz + tpi - 1) / tpi + b);
+  return s.h_K * ((nnz + tpi - 1) / tpi + plan_tasks_per_head(s));
 }
 
 }  // namespace fsa

@@ -49,14 +49,16 @@ struct Combine {
 
 // item-major partial rows (common.cuh, work plan)
 struct ItemRows {
-  const int32_t* item;  // item prefix per task [h_K b + 1]
-  const int32_t* pos;   // list position per (kh, t, slot) [h_K][N][T]
-  int64_t b, N;
-  int tpi, g;
+  const int32_t* item;   // item prefix per chunked task [ntask + 1]
+  const int32_t* pos;    // sub-list position per (kh, t, slot) [h_K][N][T]
+  const int32_t* cbase;  // task base of each token chunk within a kv head
+  int64_t N;
+  int C, nph, tpi, g;
   // row of slot s of (kh, t) -- its block blk -- for group head hh
   __device__ __forceinline__ int64_t row(int64_t kh, int64_t t, int T, int s, int blk, int hh) const {
     const int p = __ldg(pos + (kh * N + t) * T + s);
-    const int it = __ldg(item + kh * b + blk) + p / tpi;
+    const int64_t task = kh * nph + __ldg(cbase + t / C) + blk;
+    const int it = __ldg(item + task) + p / tpi;
     return (int64_t)it * 128 + (int64_t)(p % tpi) * g + hh;
   }
 };
@@ -248,11 +250,14 @@ __global__ void __launch_bounds__(256) dq_reduce_f16r_kernel(
 bool fast_reduce_ok(const fsa_shape& s) { return s.d_V == kD && s.d_K == kD; }
 
 ItemRows item_rows(const fsa_shape* s, const int32_t* work) {
+  const PlanView v = plan_view(*s, work);
   ItemRows ir;
-  ir.item = work;
-  ir.pos = work + plan_pos_offset(*s);
-  ir.b = s->N / s->B_K;
+  ir.item = v.item;
+  ir.pos = v.pos;
+  ir.cbase = v.cbase;
   ir.N = s->N;
+  ir.C = v.C;
+  ir.nph = v.nph;
   ir.tpi = (int)plan_tpi(*s);
   ir.g = (int)(s->h / s->h_K);
   return ir;

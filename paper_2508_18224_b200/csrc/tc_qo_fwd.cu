@@ -61,11 +61,17 @@ constexpr float kRescale = 8.f;  // exp2 units
 // score_mul at ~fp32 accuracy.
 enum Mode { SLIDE = 0, CMP = 1, SCORES = 2 };
 
+#ifdef FSA_TRACE
 #define QO_TRACE(w, item, slot)                                                          \
   do {                                                                                   \
     if (p.trace && blockIdx.x == 0 && (item) < 128)                                      \
       p.trace[((w) * 128 + (item)) * 8 + (slot)] = clock64();                            \
   } while (0)
+#else
+#define QO_TRACE(w, item, slot) \
+  do {                         \
+  } while (0)
+#endif
 
 struct Params {
   CUtensorMap tmOut;  // out boxes (fp32, 32 columns x g x tpi): the epilogue TMA store
@@ -523,7 +529,11 @@ __global__ void to_bf16_kernel(const float* __restrict__ x, __nv_bfloat16* __res
     y[e] = __float2bfloat16_rn(x[e]);
 }
 
+#ifdef FSA_TRACE
 long long* g_qo_trace = nullptr;
+#else
+constexpr long long* g_qo_trace = nullptr;
+#endif
 int launch(Params& p, cudaStream_t st) {
   p.trace = (p.mode == SLIDE) ? g_qo_trace : nullptr;
   int rc = make_tmap_tokens(&p.tmQ, p.Q, p.N, p.h, (int)p.g, p.tpi);
@@ -704,4 +714,6 @@ int tc_cmp_fwd(const fsa_shape* s, const void* Q, const void* Q16, const float* 
 
 }  // namespace fsa
 
+#ifdef FSA_TRACE
 extern "C" void fsa_debug_qo_trace(void* device_buf) { fsa::g_qo_trace = (long long*)device_buf; }
+#endif

@@ -70,7 +70,7 @@ enum {
   kNumBars = 29
 };
 constexpr uint32_t kOffRing = kOffBar + kNumBars * 8;
-constexpr uint32_t kOffTmem = kOffRing + 16;
+constexpr uint32_t kOffTmem = kOffRing + kRingBytes;
 constexpr uint32_t kSmemBytes = kOffTmem + 16 + 1024;
 
 // TMEM columns: stage t (= item mod 3) at 128 t (S | dP, later dQ), dK^T 384, dV^T 448.
@@ -108,10 +108,16 @@ struct Params {
   float scale, scale_log2;
 };
 
+#ifdef FSA_TRACE
 #define K8_TRACE(item, slot)                                                        \
   do {                                                                              \
     if (p.trace && blockIdx.x == 0 && (item) < 256) p.trace[(item) * 16 + (slot)] = clock64(); \
   } while (0)
+#else
+#define K8_TRACE(item, slot) \
+  do {                     \
+  } while (0)
+#endif
 
 // Rows of a task: the selected mode reads them from the inverse CSR; the
 // sliding mode uses the contiguous window of tokens [64 i, 64 i + 63 + W - 1].
@@ -162,10 +168,10 @@ __device__ __forceinline__ void token_of(const Params& p, const TaskRows& tr, in
 
 // FIFO of non-empty tasks handed from the MMA thread's look-ahead iterator
 struct TaskFifo {
-  int32_t task[4];
+  TaskRows task[4];
   int head = 0, tail = 0;
-  __device__ void push(int32_t t) { task[tail++ & 3] = t; }
-  __device__ int32_t pop() { return task[head++ & 3]; }
+  __device__ void push(const TaskRows& t) { task[tail++ & 3] = t; }
+  __device__ TaskRows pop() { return task[head++ & 3]; }
 };
 
 // kMode: 0 selected (gathered rows, dq partials), 1 sliding window, 2 compressed
@@ -178,7 +184,14 @@ __global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const _
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sb = smem_u32(smem);
   auto bar = [&](int k) { return sb + kOffBar + 8u * (uint32_t)k; };
-  Ring ring{bar(B_RF), bar(B_RE), reinterpret_cast<volatile int32_t*>(smem + kOffRing)};
+  Ring ring{bar(B_RF), bar(B_RE), reinterpret_cast<volatile TaskSlot*>(smem + kOffRing)};
+  auto decode = [&](int32_t t, TaskSlot& ts) {
+    const TaskRows r = rows_of<SL>(p, t);
+    ts.kh = (int32_t)r.kh;
+    ts.i = (int32_t)r.i;
+    ts.beg = (int32_t)r.beg;
+    ts.ntok = (int32_t)r.ntok;
+  };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffTmem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool ACC = SL == 1 && p.accumulate;  // dK/dV += (only the sliding mode reads them back)
@@ -246,10 +259,10 @@ __global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const _
       // the other loader threads just arrive).
       const uint32_t box = 64u * (uint32_t)(p.g * p.tpi) * 2u;
       for (int k = 0;; ++k) {
-        if (lr == 0) ring.produce(k, p.counter, p.ntask);
-        const int32_t task = ring.consume(k);
-        if (task < 0) break;
-        const TaskRows tr = rows_of<SL>(p, task);
+        if (lr == 0) ring.produce(k, p.counter, p.ntask, decode);
+        const TaskSlot ts = ring.consume(k);
+        if (ts.task < 0) break;
+        const TaskRows tr = rows_of_slot(ts, p.tpi);
         if (tr.nitems == 0) continue;
         mbar_spin(bar(B_KVE), (uint32_t)((kseq & 1) ^ 1));
         if (lr == 0) {
@@ -282,10 +295,10 @@ __global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const _
     } else
     for (int k = 0;; ++k) {
       publish();  // nothing in flight across the task ring
-      if (lr == 0) ring.produce(k, p.counter, p.ntask);
-      const int32_t task = ring.consume(k);
-      if (task < 0) break;
-      const TaskRows tr = rows_of<SL>(p, task);
+      if (lr == 0) ring.produce(k, p.counter, p.ntask, decode);
+      const TaskSlot ts = ring.consume(k);
+      if (ts.task < 0) break;
+      const TaskRows tr = rows_of_slot(ts, p.tpi);
       if (tr.nitems == 0) continue;
       mbar_spin(bar(B_KVE), (uint32_t)((kseq & 1) ^ 1));
       {  // warps 8,9: K rows 0-31, 32-63; warps 10,11: V rows 0-31, 32-63
@@ -357,23 +370,23 @@ __global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const _
       long long idle_since = 0;
       for (;;) {
         bool progressed = false;
-        // ---- S stream
+        auto s_stream = [&]() {
         if (!a_done && ns < np + 2) {
           bool have = a_c < a_n;
           while (!have) {
-            int32_t t;
+            TaskSlot t;
             if (!ring.try_consume_warp(ka, t)) break;
             ++ka;
-            if (t < 0) {
+            if (t.task < 0) {
               a_done = true;
               break;
             }
-            const TaskRows tr = rows_of<SL>(p, t);
+            const TaskRows tr = rows_of_slot(t, p.tpi);
             if (tr.nitems == 0) continue;
             a_c = 0;
             a_n = tr.nitems;
             ++a_kseq;
-            fifo.push(t);
+            fifo.push(tr);
             have = true;
           }
           if (have) {
@@ -399,6 +412,7 @@ __global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const _
                 K8_TRACE(ns, 1);  // S/dP issued
               }
               __syncwarp();
+#ifdef FSA_TRACE
               if (p.trace && blockIdx.x == 0 && ns < 256 && (p.trace[255 * 16 + 15] & 1)) {
                 // debug probe: raw S/dP completion latency (serialises the issuer)
                 if (lane == 0) {
@@ -407,13 +421,15 @@ __global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const _
                 }
                 __syncwarp();
               }
+#endif
               ++a_c;
               ++ns;
               progressed = true;
             }
           }
         }
-        // ---- P stream
+        };
+        auto p_stream = [&]() {
         if (np < ns) {
           const bool first = np == 0 || b_c + 1 >= b_tr.nitems;
           const int s = np & 1, tm = np % kTStages;
@@ -421,7 +437,7 @@ __global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const _
                              (!first || mbar_test_warp(bar(B_KAE), (uint32_t)(((kseq_b + 1) & 1) ^ 1)));
           if (ready) {
             if (first) {
-              b_tr = rows_of<SL>(p, fifo.pop());
+              b_tr = fifo.pop();
               b_c = 0;
               ++kseq_b;
             } else {
@@ -461,6 +477,11 @@ __global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const _
             progressed = true;
           }
         }
+        };
+        // products first: they free the item's Q/dO stage, the scarce resource
+        // (2 stages); S/dP first measured 3.5-6 % slower
+        p_stream();
+        s_stream();
         if (a_done && np == ns) break;
         // watchdog: trap instead of hanging if neither stream can move for seconds
         if (progressed) {
@@ -512,9 +533,9 @@ __global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const _
       mbar_arrive(bar(B_KAE));
     };
     for (int k = 0;; ++k) {
-      const int32_t task = ring.consume_warp(k);
-      if (task < 0) break;
-      const TaskRows tr = rows_of<SL>(p, task);
+      const TaskSlot ts = ring.consume_warp(k);
+      if (ts.task < 0) break;
+      const TaskRows tr = rows_of_slot(ts, p.tpi);
       if (ACC && tr.nitems > 0) {
         // the block's dK/dV rows are read back (+=) at the end of the task:
         // pull them into L2 now (512 lines of 128 B over the 256 softmax threads)
@@ -726,7 +747,11 @@ __global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const _
 bool tc_bwd_supported(const fsa_shape& s, int dtype) { return tc_fwd_supported(s, dtype); }
 
 namespace {
+#ifdef FSA_TRACE
 long long* g_trace = nullptr;
+#else
+constexpr long long* g_trace = nullptr;
+#endif
 Params make_params(const fsa_shape* s, const void* Q, const void* K, const void* V,
                    const void* dOut, const void* lse, const void* delta, void* dq_buf, void* dK,
                    void* dV, F16Scales sc) {
@@ -785,7 +810,7 @@ int tc_sel_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V, 
   Params p = make_params(s, Q, K, V, dOut, lse, delta, dq_buf, dK, dV, sc);
   p.offsets = offsets;
   p.qlist = qlist;
-  p.counter = const_cast<int32_t*>(work) + p.ntask + 1;
+  p.counter = plan_view(*s, work).counter;
   int rc = make_tmap_rows(&p.tmDQ, dq_buf, s->h * s->N * s->T, 1);  // scatter4 dq rows
   if (rc) return rc;
   return launch_bwd(p, st);
@@ -854,5 +879,7 @@ int tc_cmp_bwd_kv(const fsa_shape* s, const void* Q, const void* Kb, const void*
 
 }  // namespace fsa
 
+#ifdef FSA_TRACE
 // debug: record a per-item timeline of CTA 0 of the next tc_sel_bwd launches
 extern "C" void fsa_debug_bwd_trace(void* device_buf) { fsa::g_trace = (long long*)device_buf; }
+#endif

@@ -41,22 +41,38 @@ constexpr uint32_t kOffSt = kOffKV + 2 * kKVBytes;  // P lives in TMEM (A operan
 // epilogue staging: per softmax warp one SW128 half tile (32 rows x 128 B), the
 // source of its tile::scatter4 stores
 constexpr uint32_t kOffBar = kOffSt + 8 * 4096;
-enum { B_QF = 0, B_QE = 4, B_KVF = 8, B_KVE = 10, B_SF = 12, B_SE = 14, B_PF = 16, B_PE = 18,
-       B_OF = 20, B_OE = 22, B_RF = 24, B_RE = 28, kNumBars = 32 };
+enum { B_QF = 0, B_QE = 4, B_KVF = 8, B_KVE = 10, B_SF = 12, B_PF = 14, B_PE = 16,
+       B_OF = 18, B_OE = 21, B_RF = 24, B_RE = 28, kNumBars = 32 };
 constexpr uint32_t kOffRing = kOffBar + kNumBars * 8;
-constexpr uint32_t kOffTmem = kOffRing + 16;
+constexpr uint32_t kOffTmem = kOffRing + kRingBytes;
 constexpr uint32_t kSmemBytes = kOffTmem + 16 + 1024;
 
-constexpr uint32_t kColP = 384;  // TMEM: S[2] 0..127, O[2] 128..383, P[2] 384..447
+// TMEM: S/P stages [2] at 0 / 64 (P, fp16 pairs, overwrites its S: the stage is
+// free again once PV has read P), O stages [3] at 128 + 128 o.  Three O stages:
+// PV of item n waits for the epilogue of item n - 3 (the other warpgroup's),
+// not for the same warpgroup's n - 2 epilogue, which runs after softmax(n).
+constexpr int kOStages = 3;
 constexpr uint32_t kIdescS = idesc_bf16(128, 64, false, false);
 constexpr uint32_t kIdescPV = idesc_f16(128, 128, false, true);  // P, V16 in fp16
 
+#ifdef FSA_TRACE
+#define K5_TRACE(item, slot)                                                          \
+  do {                                                                                \
+    if (p.trace && blockIdx.x == 0 && (item) < 256) p.trace[(item) * 8 + (slot)] = clock64(); \
+  } while (0)
+#else
+#define K5_TRACE(item, slot) \
+  do {                       \
+  } while (0)
+#endif
+
 struct Params {
-  CUtensorMap tmO;  // obuf rows [h N T][128] fp16 (tile::scatter4 stores)
+  CUtensorMap tmO;
+  long long* trace;  // debug timeline (CTA 0, trace build only)  // obuf rows [h N T][128] fp16 (tile::scatter4 stores)
   const __nv_bfloat16 *Q, *K;
   const __half* V;  // the scaled fp16 copy (fsa_v_to_f16)
   const int32_t *offsets, *qlist;
-  const int32_t* work;  // item prefix per task (the item's row tile in obuf / ml)
+  PlanView plan;  // token-chunked tasks (common.cuh): item prefix, sub-lists
   int32_t* counter;
   __half* obuf;
   float* ml;
@@ -65,11 +81,22 @@ struct Params {
   float scale_log2, scale;
 };
 
+// chunked task `task` of the work plan: its sub-list of block i's query list
+__device__ __forceinline__ void plan_slot(const Params& p, int32_t task, TaskSlot& ts) {
+  const int32_t ki = __ldg(p.plan.tki + task);
+  ts.kh = ki / p.b;
+  ts.i = ki - ts.kh * p.b;
+  ts.beg = __ldg(p.plan.tbeg + task);
+  ts.ntok = __ldg(p.plan.tn + task);
+  ts.ibase = __ldg(p.plan.item + task);
+}
+
+// non-empty tasks handed from the MMA thread's S stream to its PV stream
 struct TaskFifo {
-  int32_t task[4];
+  TaskRows task[4];
   int head = 0, tail = 0;
-  __device__ void push(int32_t t) { task[tail++ & 3] = t; }
-  __device__ int32_t pop() { return task[head++ & 3]; }
+  __device__ void push(const TaskRows& t) { task[tail++ & 3] = t; }
+  __device__ TaskRows pop() { return task[head++ & 3]; }
 };
 
 __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_constant__ Params p) {
@@ -78,7 +105,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sb = smem_u32(smem);
   auto bar = [&](int k) { return sb + kOffBar + 8u * (uint32_t)k; };
-  Ring ring{bar(B_RF), bar(B_RE), reinterpret_cast<volatile int32_t*>(smem + kOffRing)};
+  Ring ring{bar(B_RF), bar(B_RE), reinterpret_cast<volatile TaskSlot*>(smem + kOffRing)};
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffTmem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -91,9 +118,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
       mbar_init(bar(B_KVF + s), 128);
       mbar_init(bar(B_KVE + s), 1);
       mbar_init(bar(B_SF + s), 1);
-      mbar_init(bar(B_SE + s), 128);
       mbar_init(bar(B_PF + s), 128);
       mbar_init(bar(B_PE + s), 1);
+    }
+    for (int s = 0; s < kOStages; ++s) {
       mbar_init(bar(B_OF + s), 1);
       mbar_init(bar(B_OE + s), 128);
     }
@@ -116,10 +144,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
     int n = 0, kseq = 0;
     int prev_stage = -1;
     for (int k = 0;; ++k) {
-      if (lr == 0) ring.produce(k, p.counter, p.ntask);
-      const int32_t task = ring.consume(k);
-      if (task < 0) break;
-      const TaskRows tr = task_rows(task, p.offsets, p.b, p.tpi);
+      if (lr == 0) ring.produce(k, p.counter, p.ntask, [&](int32_t t, TaskSlot& ts) { plan_slot(p, t, ts); });
+      const TaskSlot ts = ring.consume(k);
+      if (ts.task < 0) break;
+      const TaskRows tr = rows_of_slot(ts, p.tpi);
       if (tr.nitems == 0) continue;
       const int kvs = kseq & 1;
       mbar_wait(bar(B_KVE + kvs), (uint32_t)(((kseq >> 1) & 1) ^ 1));
@@ -148,6 +176,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
         warp_gather_rows32(sb + kOffQ + s * kQBytes, 16384u, lr & ~31,
                            p.Q + (t * p.h + (int)tr.kh * p.g + hh) * kD, ok, lane);
         asm volatile("cp.async.commit_group;" ::: "memory");
+        if (lr == 0) K5_TRACE(n, 0);  // gather issued
         // everything but this item's gather has landed: publish it
         asm volatile("cp.async.wait_group 1;" ::: "memory");
         fence_proxy_async();
@@ -185,26 +214,26 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
         if (!a_done && ns < np + 2) {
           bool have = a_c < a_n;
           while (!have) {
-            int32_t t;
+            TaskSlot t;
             if (!ring.try_consume_warp(ka, t)) break;
             ++ka;
-            if (t < 0) {
+            if (t.task < 0) {
               a_done = true;
               break;
             }
-            const TaskRows tr = task_rows(t, p.offsets, p.b, p.tpi);
+            const TaskRows tr = rows_of_slot(t, p.tpi);
             if (tr.nitems == 0) continue;
             a_c = 0;
             a_n = tr.nitems;
             ++a_kseq;
-            fifo.push(t);
+            fifo.push(tr);
             have = true;
           }
           if (have) {
             const int s = ns % kQStages, v = ns & 1, kvs = a_kseq & 1;
             if (mbar_test_warp(bar(B_KVF + kvs), (uint32_t)((a_kseq >> 1) & 1)) &&
                 mbar_test_warp(bar(B_QF + s), (uint32_t)((ns / kQStages) & 1)) &&
-                mbar_test_warp(bar(B_SE + v), (uint32_t)(((ns >> 1) & 1) ^ 1))) {
+                mbar_test_warp(bar(B_PE + v), (uint32_t)(((ns >> 1) & 1) ^ 1))) {
               tc_fence_after();
               const uint32_t qa = sb + kOffQ + s * kQBytes;
               const uint32_t ka_ = sb + kOffKV + kvs * kKVBytes;
@@ -215,6 +244,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
                            desc_kmajor(ka_ + (k >> 2) * 8192u + (k & 3) * 32u), kIdescS, k > 0);
                 mma_commit(bar(B_SF + v));
                 mma_commit(bar(B_QE + s));
+                K5_TRACE(ns, 1);  // S issued
               }
               __syncwarp();
               ++a_c;
@@ -225,10 +255,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
         }
         if (np < ns) {
           const int v = np & 1;
+          const int o = np % kOStages;
           if (mbar_test_warp(bar(B_PF + v), (uint32_t)((np >> 1) & 1)) &&
-              mbar_test_warp(bar(B_OE + v), (uint32_t)(((np >> 1) & 1) ^ 1))) {
+              mbar_test_warp(bar(B_OE + o), (uint32_t)(((np / kOStages) & 1) ^ 1))) {
             if (np == 0 || b_c + 1 >= b_tr.nitems) {
-              b_tr = task_rows(fifo.pop(), p.offsets, p.b, p.tpi);
+              b_tr = fifo.pop();
               b_c = 0;
               ++b_kseq;
             } else {
@@ -241,10 +272,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
             if (elect_one()) {
 #pragma unroll
               for (int k = 0; k < 4; ++k)
-                mma_bf16_ts(tO + v * 128, tmem + kColP + v * 32 + k * 8,
+                mma_bf16_ts(tO + o * 128, tS + v * 64 + k * 8,
                             desc_mnmajor(va + k * 2048u, 8192u), kIdescPV, k > 0);
-              mma_commit(bar(B_OF + v));
+              mma_commit(bar(B_OF + o));
               mma_commit(bar(B_PE + v));
+              K5_TRACE(np, 4);  // PV issued
               if (last) mma_commit(bar(B_KVE + kvs));
             }
             __syncwarp();
@@ -280,8 +312,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
     int pend_n = 0;
     int n = 0;
     auto epilogue = [&](int m1) {
-      const int s1 = m1 & 1;
-      mbar_wait(bar(B_OF + s1), (uint32_t)((m1 >> 1) & 1));
+      const int o1 = m1 % kOStages;
+      mbar_wait(bar(B_OF + o1), (uint32_t)((m1 / kOStages) & 1));
+      if (r == 0) K5_TRACE(m1, 5);  // O landed (epilogue)
       tc_fence_after();
       const float inv = 1.f / pl;
       // The item's rows are contiguous: each warp's 32 rows leave by one TMA
@@ -295,7 +328,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
         for (int qq = 0; qq < 2; ++qq) {
           const int q = 2 * hf + qq;
           float ov[32];
-          tmem_ld32(tmem + lane_base + 128 + s1 * 128 + q * 32, ov);
+          tmem_ld32(tmem + lane_base + 128 + o1 * 128 + q * 32, ov);
           tmem_wait_ld();
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
@@ -308,7 +341,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
         }
         if (hf == 1) {
           tc_fence_before();
-          mbar_arrive(bar(B_OE + s1));
+          mbar_arrive(bar(B_OE + o1));
         }
         fence_proxy_async();
         __syncwarp();
@@ -319,13 +352,14 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
         }
       }
       __stcs(reinterpret_cast<float2*>(p.ml) + (int64_t)pitem * kRows + r, make_float2(pm, pl));
+      if (r == 0) K5_TRACE(m1, 6);  // rows stored
     };
     for (int k = 0;; ++k) {
-      const int32_t task = ring.consume(k);
-      if (task < 0) break;
-      const TaskRows tr = task_rows(task, p.offsets, p.b, p.tpi);
+      const TaskSlot ts = ring.consume(k);
+      if (ts.task < 0) break;
+      const TaskRows tr = rows_of_slot(ts, p.tpi);
       const int32_t* ql = p.qlist + (int64_t)tr.kh * p.N * p.T + tr.beg;
-      const int32_t ibase = tr.nitems > 0 ? __ldg(p.work + task) : 0;
+      const int32_t ibase = ts.ibase;
       // entries of this warpgroup's items (every other item) are loaded one
       // own item ahead
       const int c0 = (int)((wg - n) & 1);
@@ -349,13 +383,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
           vis = v < kBK ? v : kBK;
         }
         mbar_wait(bar(B_SF + s), (uint32_t)((n >> 1) & 1));
+        if (r == 0) K5_TRACE(n, 2);  // S landed
         tc_fence_after();
         float sv[64];
         tmem_ld32(tmem + lane_base + s * 64, sv);
         tmem_ld32(tmem + lane_base + s * 64 + 32, sv + 32);
         tmem_wait_ld();
-        tc_fence_before();
-        mbar_arrive(bar(B_SE + s));
         // only rows whose token lies in block i see a causal prefix (vis < 64);
         // warps without such rows take the unmasked path
         const bool masked = __any_sync(0xffffffffu, vis < kBK);
@@ -390,11 +423,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
           }
         }
         sum += s2;
-        mbar_wait(bar(B_PE + s), (uint32_t)(((n >> 1) & 1) ^ 1));
-        tmem_st32u(tmem + lane_base + kColP + s * 32, pk);  // fp16 pairs, K-packed
+        tmem_st32u(tmem + lane_base + s * 64, pk);  // fp16 pairs, K-packed, over S
         tmem_wait_st_();
         tc_fence_before();
         mbar_arrive(bar(B_PF + s));
+        if (r == 0) K5_TRACE(n, 3);  // P written
         if (pend) epilogue(pend_n);
         pend = true;
         pend_n = n;
@@ -418,6 +451,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
 
 }  // namespace
 
+#ifdef FSA_TRACE
+long long* g_k5_trace = nullptr;
+#else
+constexpr long long* g_k5_trace = nullptr;
+#endif
+
 int num_sms() {  // of the current device (a process may drive several)
   int dev = 0, n = 0;
   cudaGetDevice(&dev);
@@ -440,7 +479,8 @@ int tc_sel_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V,
   p.V = (const __half*)V;
   p.offsets = offsets;
   p.qlist = qlist;
-  p.work = work;
+  p.plan = plan_view(*s, work);
+  p.trace = g_k5_trace;
   p.obuf = (__half*)obuf;
   p.ml = (float*)ml;
   p.N = (int)s->N;
@@ -449,12 +489,12 @@ int tc_sel_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V,
   p.T = (int)s->T;
   p.b = (int)(s->N / s->B_K);
   p.g = (int)(s->h / s->h_K);
-  p.ntask = p.h_K * p.b;
+  p.ntask = (int)plan_ntask(*s);
   p.tpi = kRows / p.g;
   p.fdT.init((uint32_t)p.T);
   p.scale = (float)s->scale;
   p.scale_log2 = (float)(s->scale * 1.4426950408889634);
-  p.counter = const_cast<int32_t*>(work) + p.ntask + 1;
+  p.counter = p.plan.counter;
   if (int rc = make_tmap_rows(&p.tmO, obuf, plan_max_items(*s) * kRows, 32)) return rc;
   cudaMemsetAsync(p.counter, 0, sizeof(int32_t), st);
   static unsigned long long done = 0;
@@ -465,3 +505,8 @@ int tc_sel_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V,
 }
 
 }  // namespace fsa
+
+#ifdef FSA_TRACE
+// debug: record a per-item timeline of CTA 0 of the next tc_sel_fwd launches
+extern "C" void fsa_debug_sel_fwd_trace(void* device_buf) { fsa::g_k5_trace = (long long*)device_buf; }
+#endif

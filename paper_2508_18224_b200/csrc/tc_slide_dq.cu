@@ -58,11 +58,17 @@ struct Params {
   float scale, scale_log2;
 };
 
+#ifdef FSA_TRACE
 #define DQ_TRACE(w, item, slot)                                                          \
   do {                                                                                   \
     if (p.trace && blockIdx.x == 0 && (item) < 128)                                      \
       p.trace[((w) * 128 + (item)) * 8 + (slot)] = clock64();                            \
   } while (0)
+#else
+#define DQ_TRACE(w, item, slot) \
+  do {                         \
+  } while (0)
+#endif
 
 struct Sub {
   int t0, tlast;  // tokens [t0, tlast]
@@ -370,7 +376,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const __grid_c
 
 }  // namespace
 
+#ifdef FSA_TRACE
 long long* g_dq_trace = nullptr;
+#else
+constexpr long long* g_dq_trace = nullptr;
+#endif
 int tc_slide_dq(const fsa_shape* s, const void* Q, const void* K, const void* V, const void* dOut,
                 const void* lse, const void* delta, void* dQ, int accumulate, F16Scales sc,
                 cudaStream_t st) {
@@ -456,4 +466,6 @@ int tc_cmp_dq(const fsa_shape* s, const void* Q, const void* Kb, const void* Vb,
 
 }  // namespace fsa
 
+#ifdef FSA_TRACE
 extern "C" void fsa_debug_dq_trace(void* device_buf) { fsa::g_dq_trace = (long long*)device_buf; }
+#endif

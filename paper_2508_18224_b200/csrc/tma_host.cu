@@ -156,6 +156,7 @@ __global__ void gather4_test_kernel(const __grid_constant__ CUtensorMap tm,
 
 }  // namespace fsa
 
+#ifdef FSA_TRACE
 extern "C" int fsa_debug_gather4_test(const void* src, int64_t rows, const int32_t* idx,
                                       const int32_t* idx2, int n, int box_rows, void* out,
                                       void* out2, int64_t rows2, void* stream) {
@@ -168,3 +169,4 @@ extern "C" int fsa_debug_gather4_test(const void* src, int64_t rows, const int32
                                                                     (__nv_bfloat16*)out);
   return fsa::check_launch("gather4_test");
 }
+#endif

@@ -243,6 +243,27 @@ def test_selected_fwd_bwd_vs_oracle(kw, run_dt):
         assert_close(host(g_), w_, run_dt, name, grad=True)
 
 
+@pytest.mark.parametrize("chunk", [256, 1024, 4096])
+def test_token_chunked_plan_vs_oracle(chunk, monkeypatch):
+    """Token-chunked work plan (common.cuh): tasks are (kv head, chunk, block)
+    sub-lists.  Forced small chunks give the same forward bit for bit as a
+    single chunk, and match the oracle (kv_major.py:245-261)."""
+    kw = dict(N=8192, d_K=128, d_V=128, h=10, h_K=2, B_K=64, T=16, W=512)
+    c = O.cfg_of(**kw)
+    cfg = _cfg(kw)
+    Q, K, V = (round_inputs(x, "bf16") for x in O.make_qkv(c, 7))
+    idx = O.select_topk(O.make_scores(c, 7), c)
+    tQ, tK, tV = (dev(x, torch.bfloat16) for x in (Q, K, V))
+    monkeypatch.setenv("FSA_CHUNK_TOKENS", str(1 << 30))
+    one, _ = kv_major.selected_forward(tQ, tK, tV, fsa.SelectionTensor(idx), cfg)
+    monkeypatch.setenv("FSA_CHUNK_TOKENS", str(chunk))
+    res, _ = kv_major.selected_forward(tQ, tK, tV, fsa.SelectionTensor(idx), cfg)
+    assert torch.equal(res.out, one.out) and torch.equal(res.lse, one.lse)
+    want_out, want_lse = O.selected_forward(Q, K, V, idx, c)
+    assert_close(host(res.out), want_out, "bf16", "out")
+    assert_close(host(res.lse), want_lse, "f32", "lse")
+
+
 def test_acceptance_sweep_golden():
     z = load("acceptance_sweep")
     for n in range(int(z["count"])):

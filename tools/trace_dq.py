@@ -3,6 +3,7 @@ import ctypes
 import os
 import sys
 
+os.environ["FSA_TRACE_LIB"] = "1"  # the trace build (build.py --trace)
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
