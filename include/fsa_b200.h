@@ -160,6 +160,22 @@ int fsa_sel_fwd(const fsa_shape* s, int dtype, int mode, const void* Q, const vo
                 const void* V, const int32_t* offsets, const int32_t* qlist, const int32_t* work,
                 const void* m_global, void* obuf, int obuf_dtype, void* ml, void* stream);
 
+/* The reference's phase passes on the tensor cores (bf16, d_K = d_V = 128,
+ * B_K = 64: the shapes fsa_buffer_dtypes maps to FSA_DT_F16 partials), the K5
+ * kernel in STATS / GLOBAL mode.  Slot-indexed outputs, as fsa_sel_fwd's:
+ *   FSA_FWD_STATS  (compute_softmax_stats, kv_major.py:105-149): ml
+ *                  [h][N][T][2] f32 local (m_i, l_i) of each live slot, for
+ *                  fsa_merge_fwd FSA_MERGE_STATS; V16 / vscale / m_global unused.
+ *   FSA_FWD_GLOBAL (block_pass_forward, kv_major.py:152-204): obuf
+ *                  [h][N][T][d_V] f32 rows exp(z - m_global) V_i, for
+ *                  FSA_MERGE_REDUCE; m_global [h][N] f32; V16 / vscale the
+ *                  fsa_v_to_f16 copy of V.
+ * work: the fsa_build_inverse work plan (required). */
+int fsa_sel_fwd_phase(const fsa_shape* s, int mode, const void* Q, const void* K, const void* V16,
+                      const float* vscale, const int32_t* offsets, const int32_t* qlist,
+                      const int32_t* work, const float* m_global, float* obuf, float* ml,
+                      void* stream);
+
 /* Merge of per-slot partials in ascending block order (kv_major.py:207-242;
  * stats merge kv_major.py:137-149, shared max :141-146).  out, lse, m_out,
  * l_out in acc dtype; m_out/l_out/lse nullable.  vscale: the V16 scales

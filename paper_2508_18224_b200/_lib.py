@@ -59,6 +59,7 @@ SIGNATURES = {
     "fsa_partial_rows": ([_sp, _i], _i64),
     "fsa_build_inverse": ([_sp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "fsa_sel_fwd": ([_sp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp], _i),
+    "fsa_sel_fwd_phase": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "fsa_merge_fwd": ([_sp, _i, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp], _i),
     "fsa_merge_combine_fwd": ([_sp, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "fsa_bwd_delta": ([_sp, _i, _vp, _vp, _vp, _vp], _i),

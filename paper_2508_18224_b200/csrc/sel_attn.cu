@@ -424,6 +424,23 @@ extern "C" int fsa_sel_fwd(const fsa_shape* s, int dtype, int mode, const void* 
               (cudaStream_t)stream);
 }
 
+extern "C" int fsa_sel_fwd_phase(const fsa_shape* s, int mode, const void* Q, const void* K,
+                                 const void* V16, const float* vscale, const int32_t* offsets,
+                                 const int32_t* qlist, const int32_t* work, const float* m_global,
+                                 float* obuf, float* ml, void* stream) {
+  FSA_REQUIRE(fsa::tc_fwd_supported(*s, FSA_DT_BF16),
+              "sel_fwd_phase: tensor-core shapes only (bf16, d = 128, B_K = 64)");
+  FSA_REQUIRE(mode == FSA_FWD_STATS || mode == FSA_FWD_GLOBAL, "sel_fwd_phase: bad mode %d", mode);
+  FSA_REQUIRE(work != nullptr, "sel_fwd_phase: needs the work plan");
+  if (mode == FSA_FWD_STATS) {
+    FSA_REQUIRE(ml != nullptr, "sel_fwd_phase STATS: ml is required");
+  } else {
+    FSA_REQUIRE(obuf && m_global && V16 && vscale, "sel_fwd_phase GLOBAL: obuf, m_global, V16 and vscale are required");
+  }
+  return fsa::tc_sel_fwd(s, Q, K, V16, offsets, qlist, work, obuf, ml, (cudaStream_t)stream, mode,
+                         m_global, vscale);
+}
+
 extern "C" int fsa_merge_fwd(const fsa_shape* s, int dtype, int mode, const int32_t* idx,
                              const int32_t* work, const void* obuf, int obuf_dtype, const void* ml,
                              const void* m_global, const void* l_global, void* out, void* lse,

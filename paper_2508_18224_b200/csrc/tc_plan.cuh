@@ -18,10 +18,14 @@ inline F16Scales f16_scales_of(const float* scales, int64_t h_K) {
   return F16Scales{scales, scales + 2 * h_K, scales + 4 * h_K, scales + 6 * h_K};
 }
 
-// V: the fp16 staged copy (stage_f16); obuf fp16 [h][N][T][128] in its scale
+// V: the fp16 staged copy (stage_f16).  mode FSA_FWD_LOCAL: obuf fp16
+// item-major partial rows in the V16 scale + item-major (m_i, l_i) in ml;
+// FSA_FWD_STATS: slot-indexed (m_i, l_i) [h][N][T] in ml (V unused);
+// FSA_FWD_GLOBAL: obuf fp32 slot-indexed [h][N][T][128] rows exp(z - m_global) V_i
 int tc_sel_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V16,
                const int32_t* offsets, const int32_t* qlist, const int32_t* work, void* obuf,
-               void* ml, cudaStream_t st);
+               void* ml, cudaStream_t st, int mode = FSA_FWD_LOCAL,
+               const float* m_global = nullptr, const float* vscale = nullptr);
 // Q, K, V, dOut: the fp16 staged copies, sc their scales
 int tc_sel_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V, const void* dOut,
                const void* lse, const void* delta, const int32_t* offsets, const int32_t* qlist,

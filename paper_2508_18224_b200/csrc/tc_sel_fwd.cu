@@ -76,6 +76,12 @@ struct Params {
   int32_t* counter;
   __half* obuf;
   float* ml;
+  // phase API (kv_major.py:105-204): STATS writes slot-indexed (m_i, l_i)
+  // [h][N][T] into ml; GLOBAL writes exp(z - m_global) V_i rows, fp32
+  // slot-indexed [h][N][T][128], into gbuf
+  const float* mg;
+  float* gbuf;
+  const float* vscale;
   int N, h, h_K, T, b, g, ntask, tpi;
   FastDiv fdT;  // entry -> token (entries are t * T + slot)
   float scale_log2, scale;
@@ -99,6 +105,9 @@ struct TaskFifo {
   __device__ TaskRows pop() { return task[head++ & 3]; }
 };
 
+// MODE: FSA_FWD_LOCAL (the fused fast path), FSA_FWD_STATS (softmax statistics
+// only: no PV), FSA_FWD_GLOBAL (rows against the given global row max)
+template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -155,8 +164,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
         const int lw = warp - 8, row0 = (lw & 1) * 32;
         const int64_t off = ((int64_t)(tr.i * kBK + row0 + lane) * p.h_K + tr.kh) * kD;
         const void* src = lw < 2 ? (const void*)(p.K + off) : (const void*)(p.V + off);
-        warp_gather_rows32(sb + kOffKV + kvs * kKVBytes + (lw < 2 ? 0u : 16384u), 8192u, row0, src,
-                           true, lane);
+        if (MODE != FSA_FWD_STATS || lw < 2)  // STATS: no values
+          warp_gather_rows32(sb + kOffKV + kvs * kKVBytes + (lw < 2 ? 0u : 16384u), 8192u, row0,
+                             src, true, lane);
         asm volatile("cp.async.commit_group;" ::: "memory");
       }
       bool kv_pending = true;
@@ -257,7 +267,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
           const int v = np & 1;
           const int o = np % kOStages;
           if (mbar_test_warp(bar(B_PF + v), (uint32_t)((np >> 1) & 1)) &&
-              mbar_test_warp(bar(B_OE + o), (uint32_t)(((np / kOStages) & 1) ^ 1))) {
+              (MODE == FSA_FWD_STATS ||
+               mbar_test_warp(bar(B_OE + o), (uint32_t)(((np / kOStages) & 1) ^ 1)))) {
             if (np == 0 || b_c + 1 >= b_tr.nitems) {
               b_tr = fifo.pop();
               b_c = 0;
@@ -270,12 +281,14 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
             tc_fence_after();
             const uint32_t va = sb + kOffKV + kvs * kKVBytes + 16384u;
             if (elect_one()) {
+              if constexpr (MODE != FSA_FWD_STATS) {
 #pragma unroll
-              for (int k = 0; k < 4; ++k)
-                mma_bf16_ts(tO + o * 128, tS + v * 64 + k * 8,
-                            desc_mnmajor(va + k * 2048u, 8192u), kIdescPV, k > 0);
-              mma_commit(bar(B_OF + o));
-              mma_commit(bar(B_PE + v));
+                for (int k = 0; k < 4; ++k)
+                  mma_bf16_ts(tO + o * 128, tS + v * 64 + k * 8,
+                              desc_mnmajor(va + k * 2048u, 8192u), kIdescPV, k > 0);
+                mma_commit(bar(B_OF + o));
+              }
+              mma_commit(bar(B_PE + v));  // (STATS: the S stage, read by the softmax)
               K5_TRACE(np, 4);  // PV issued
               if (last) mma_commit(bar(B_KVE + kvs));
             }
@@ -316,6 +329,25 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
       mbar_wait(bar(B_OF + o1), (uint32_t)((m1 / kOStages) & 1));
       if (r == 0) K5_TRACE(m1, 5);  // O landed (epilogue)
       tc_fence_after();
+      if constexpr (MODE == FSA_FWD_GLOBAL) {
+        // unnormalised rows exp(z - m) V_i (kv_major.py:194-196), fp32, slot-indexed
+        float* dst = prow >= 0 ? p.gbuf + prow * kD : nullptr;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float ov[32];
+          tmem_ld32(tmem + lane_base + 128 + o1 * 128 + q * 32, ov);
+          tmem_wait_ld();
+          if (dst) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+              reinterpret_cast<float4*>(dst + q * 32)[c] =
+                  make_float4(ov[4 * c] * pl, ov[4 * c + 1] * pl, ov[4 * c + 2] * pl, ov[4 * c + 3] * pl);
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(bar(B_OE + o1));
+        return;
+      }
       const float inv = 1.f / pl;
       // The item's rows are contiguous: each warp's 32 rows leave by one TMA
       // tile store per 64-column half from its SW128 staging tile -- off the
@@ -374,13 +406,19 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
           const int pos2 = pos + 2 * p.tpi;
           ent_next = (kt_row < p.tpi && pos2 < tr.ntok) ? __ldg(ql + pos2) : 0;
         }
-        int64_t orow = -1;
+        int64_t orow = -1, grow = -1;  // item-major row; slot-indexed row (phase modes)
+        float mgl = 0.f;                // GLOBAL: the row's global max (log2 units)
         int vis = kBK;
         if (kt_row < p.tpi && pos < tr.ntok) {
           const int t = (int)p.fdT.div((uint32_t)ent);
           orow = (int64_t)(ibase + c) * kRows + r;
           const int v = t - (int)tr.i * kBK + 1;
           vis = v < kBK ? v : kBK;
+          if (MODE != FSA_FWD_LOCAL) {
+            const int64_t j = (int64_t)tr.kh * p.g + hh;
+            grow = (j * p.N + t) * p.T + (ent - t * p.T);
+            if (MODE == FSA_FWD_GLOBAL) mgl = __ldg(p.mg + j * p.N + t) * 1.4426950408889634f;
+          }
         }
         mbar_wait(bar(B_SF + s), (uint32_t)((n >> 1) & 1));
         if (r == 0) K5_TRACE(n, 2);  // S landed
@@ -395,7 +433,14 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
         float mx = -INFINITY;
         float sum = 0.f, s2 = 0.f;
         uint32_t pk[32];
-        if (!masked) {
+        if (MODE == FSA_FWD_GLOBAL) {  // P = exp(z - m_global) <= 1
+#pragma unroll
+          for (int c2 = 0; c2 < 64; c2 += 2) {
+            const float e0 = c2 < vis && orow >= 0 ? ex2(fmaf(sv[c2], p.scale_log2, -mgl)) : 0.f;
+            const float e1 = c2 + 1 < vis && orow >= 0 ? ex2(fmaf(sv[c2 + 1], p.scale_log2, -mgl)) : 0.f;
+            pk[c2 >> 1] = pack_f16(e0, e1);
+          }
+        } else if (!masked) {
 #pragma unroll
           for (int c2 = 0; c2 < 64; ++c2) mx = fmaxf(mx, sv[c2]);
           if (orow < 0) mx = 0.f;
@@ -423,6 +468,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
           }
         }
         sum += s2;
+        if constexpr (MODE == FSA_FWD_STATS) {  // local (m_i, l_i) only (kv_major.py:131-140)
+          if (grow >= 0) reinterpret_cast<float2*>(p.ml)[grow] = make_float2(mx * p.scale, sum);
+          tc_fence_before();
+          mbar_arrive(bar(B_PF + s));
+          continue;
+        }
         tmem_st32u(tmem + lane_base + s * 64, pk);  // fp16 pairs, K-packed, over S
         tmem_wait_st_();
         tc_fence_before();
@@ -431,10 +482,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
         if (pend) epilogue(pend_n);
         pend = true;
         pend_n = n;
-        prow = orow;
+        prow = MODE == FSA_FWD_GLOBAL ? grow : orow;
         pitem = ibase + c;
         pm = mx * p.scale;
-        pl = sum;
+        pl = MODE == FSA_FWD_GLOBAL ? 1.f / __ldg(p.vscale + tr.kh) : sum;
       }
     }
     if (pend) epilogue(pend_n);
@@ -471,7 +522,7 @@ bool tc_fwd_supported(const fsa_shape& s, int dtype) {
 
 int tc_sel_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V,
                const int32_t* offsets, const int32_t* qlist, const int32_t* work, void* obuf,
-               void* ml, cudaStream_t st) {
+               void* ml, cudaStream_t st, int mode, const float* m_global, const float* vscale) {
   FSA_REQUIRE(work != nullptr, "tensor-core forward needs the inverse work buffer");
   Params p{};
   p.Q = (const __nv_bfloat16*)Q;
@@ -481,8 +532,11 @@ int tc_sel_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V,
   p.qlist = qlist;
   p.plan = plan_view(*s, work);
   p.trace = g_k5_trace;
-  p.obuf = (__half*)obuf;
+  p.obuf = mode == FSA_FWD_LOCAL ? (__half*)obuf : nullptr;
+  p.gbuf = mode == FSA_FWD_GLOBAL ? (float*)obuf : nullptr;
   p.ml = (float*)ml;
+  p.mg = m_global;
+  p.vscale = vscale;
   p.N = (int)s->N;
   p.h = (int)s->h;
   p.h_K = (int)s->h_K;
@@ -495,11 +549,21 @@ int tc_sel_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V,
   p.scale = (float)s->scale;
   p.scale_log2 = (float)(s->scale * 1.4426950408889634);
   p.counter = p.plan.counter;
-  if (int rc = make_tmap_rows(&p.tmO, obuf, plan_max_items(*s) * kRows, 32)) return rc;
+  if (mode == FSA_FWD_LOCAL)
+    if (int rc = make_tmap_rows(&p.tmO, obuf, plan_max_items(*s) * kRows, 32)) return rc;
   cudaMemsetAsync(p.counter, 0, sizeof(int32_t), st);
-  static unsigned long long done = 0;
-  ensure_smem_attr(tc_sel_fwd_kernel, (int)kSmemBytes, done);
-  tc_sel_fwd_kernel<<<num_sms(), kThreads, kSmemBytes, st>>>(p);
+  static unsigned long long done[3] = {0, 0, 0};
+  if (mode == FSA_FWD_STATS) {
+    ensure_smem_attr(tc_sel_fwd_kernel<FSA_FWD_STATS>, (int)kSmemBytes, done[1]);
+    tc_sel_fwd_kernel<FSA_FWD_STATS><<<num_sms(), kThreads, kSmemBytes, st>>>(p);
+  } else if (mode == FSA_FWD_GLOBAL) {
+    FSA_REQUIRE(m_global && vscale, "sel_fwd GLOBAL: needs the global row max and the V scales");
+    ensure_smem_attr(tc_sel_fwd_kernel<FSA_FWD_GLOBAL>, (int)kSmemBytes, done[2]);
+    tc_sel_fwd_kernel<FSA_FWD_GLOBAL><<<num_sms(), kThreads, kSmemBytes, st>>>(p);
+  } else {
+    ensure_smem_attr(tc_sel_fwd_kernel<FSA_FWD_LOCAL>, (int)kSmemBytes, done[0]);
+    tc_sel_fwd_kernel<FSA_FWD_LOCAL><<<num_sms(), kThreads, kSmemBytes, st>>>(p);
+  }
   FSA_LAUNCH_CHECK("tc_sel_fwd");
   return FSA_OK;
 }

@@ -121,6 +121,12 @@ def _sel_partials(cfg, dt, q, k, v, inv, v16=None):
     return obuf, ml, ob_code, vscale
 
 
+def _tc_partials(cfg, dt) -> bool:
+    """bf16 d = 128 B_K = 64: the tensor-core path (fp16 partials)."""
+    (ob_code, _), _ = _lib.buffer_dtypes(cfg, dt)
+    return ob_code == _lib.DT_F16
+
+
 def _fused_forward(cfg, dt, q, k, v, sel, inv):
     """K5 (LOCAL) + K6 (LOCAL merge): returns out storage (N, h, d_V) and lse
     (h, N), both in the accumulator dtype (f32 for bf16 inputs)."""
@@ -152,10 +158,14 @@ def compute_softmax_stats(Q, K, sel: SelectionTensor, cfg, *, shared_max: bool =
     s = _lib.shape_of(cfg)
     st = _lib.stream()
     acc_code = _lib.dt_code(acc)
-    _lib.call("fsa_sel_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.FWD_STATS, _lib.ptr(q),
-              _lib.ptr(k), _lib.ptr(k), _lib.ptr(inv.offsets), _lib.ptr(inv.qlist), _lib.ptr(inv.work),
-              None, None,
-              acc_code, _lib.ptr(ml), st)
+    if _tc_partials(cfg, dt):  # K5 STATS mode on tcgen05
+        _lib.call("fsa_sel_fwd_phase", ctypes.byref(s), _lib.FWD_STATS, _lib.ptr(q), _lib.ptr(k), None,
+                  None, _lib.ptr(inv.offsets), _lib.ptr(inv.qlist), _lib.ptr(inv.work), None, None,
+                  _lib.ptr(ml), st)
+    else:
+        _lib.call("fsa_sel_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.FWD_STATS, _lib.ptr(q),
+                  _lib.ptr(k), _lib.ptr(k), _lib.ptr(inv.offsets), _lib.ptr(inv.qlist),
+                  _lib.ptr(inv.work), None, None, acc_code, _lib.ptr(ml), st)
     m = torch.empty((cfg.h, cfg.N), dtype=acc, device=dev)
     l = torch.empty_like(m)
     _lib.call("fsa_merge_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.MERGE_STATS,
@@ -182,10 +192,16 @@ def block_pass_forward(Q, K, V, inv: InverseIndex, stats: SoftmaxStats, cfg, *,
     mg = to_device(stats.m, acc).contiguous()
     obuf = torch.zeros((cfg.h, cfg.N, cfg.T, cfg.d_V), dtype=acc, device=dev)
     s = _lib.shape_of(cfg)
-    _lib.call("fsa_sel_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.FWD_GLOBAL, _lib.ptr(q),
-              _lib.ptr(k), _lib.ptr(v), _lib.ptr(inv.offsets), _lib.ptr(inv.qlist), _lib.ptr(inv.work),
-              _lib.ptr(mg),
-              _lib.ptr(obuf), _lib.dt_code(acc), None, _lib.stream())
+    if _tc_partials(cfg, dt):  # K5 GLOBAL mode on tcgen05 (P . V in fp16 on the scaled V copy)
+        v16, vscale = _lib.v_to_f16(cfg, v)
+        _lib.call("fsa_sel_fwd_phase", ctypes.byref(s), _lib.FWD_GLOBAL, _lib.ptr(q), _lib.ptr(k),
+                  _lib.ptr(v16), _lib.ptr(vscale), _lib.ptr(inv.offsets), _lib.ptr(inv.qlist),
+                  _lib.ptr(inv.work), _lib.ptr(mg), _lib.ptr(obuf), None, _lib.stream())
+    else:
+        _lib.call("fsa_sel_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.FWD_GLOBAL, _lib.ptr(q),
+                  _lib.ptr(k), _lib.ptr(v), _lib.ptr(inv.offsets), _lib.ptr(inv.qlist),
+                  _lib.ptr(inv.work), _lib.ptr(mg), _lib.ptr(obuf), _lib.dt_code(acc), None,
+                  _lib.stream())
     if meter is not None:
         meter_block_pass(meter, inv.n_valid, cfg)
     return OutputBuffer(obuf, inv, cfg)

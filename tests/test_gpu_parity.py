@@ -197,6 +197,39 @@ def test_phase_api_golden(name):
     assert_close(host(res_sh.out)[::st], z["out_sh"], tol, "shared-max out")
 
 
+@pytest.mark.parametrize("kw", [
+    dict(N=4096, d_K=128, d_V=128, h=8, h_K=2, B_K=64, T=16),   # GQA 4 (Llama-shaped)
+    dict(N=2048, d_K=128, d_V=128, h=5, h_K=1, B_K=64, T=16),   # GQA 5 (Qwen3-shaped)
+])
+def test_phase_api_tensor_core_bf16(kw):
+    """compute_softmax_stats / block_pass_forward (kv_major.py:105-204) on the
+    tcgen05 K5 kernel in STATS / GLOBAL mode for bf16 d = 128, then
+    reduce_forward, against the oracle on the bf16-rounded inputs: m, l in the
+    fp32 tolerance (S products are exact in fp32 accumulation), out in bf16's."""
+    c = O.cfg_of(**kw)
+    cfg = _cfg(kw)
+    Q, K, V = (round_inputs(x, "bf16") for x in O.make_qkv(c, 9))
+    idx = O.select_topk(O.make_scores(c, 9), c)
+    tQ, tK, tV = (dev(x, torch.bfloat16) for x in (Q, K, V))
+    sel = fsa.SelectionTensor(idx)
+    inv = fsa.build_inverse_index(sel, cfg)
+    for shared in (False, True):
+        want = O.softmax_stats(Q, K, idx, c, shared_max=shared)
+        stats = kv_major.compute_softmax_stats(tQ, tK, sel, cfg, shared_max=shared)
+        assert_close(host(stats.m), want.m, "f32", f"tc m shared={shared}")
+        assert_close(host(stats.l), want.l, "f32", f"tc l shared={shared}")
+        buf = kv_major.block_pass_forward(tQ, tK, tV, inv, stats, cfg)
+        res = kv_major.reduce_forward(buf, inv, stats, cfg)
+        regions = O.block_pass(Q, K, V, idx, want, c)
+        want_out, want_lse = O.reduce_regions(regions, want, c, inv=O.build_inverse(idx, c))
+        assert_close(host(res.out), want_out, "bf16", f"tc phase out shared={shared}")
+        assert_close(host(res.lse), want_lse, "f32", f"tc phase lse shared={shared}")
+        # a GLOBAL row of one (head, block) task against the reference region
+        j, i = cfg.h - 1, 3
+        rows = O.build_inverse(idx, c).queries(j // c.g, i)
+        assert_close(host(buf.rows[j][i]), regions[j][i], "bf16", "tc GLOBAL region")
+
+
 @pytest.mark.parametrize("name", FULL_CASES)
 def test_selected_backward_golden(name):
     kw, c, inp, z = case(name)
