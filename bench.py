@@ -24,9 +24,9 @@ operator path has no host synchronisation), so the timed region measures the
 device, not the host's launch rate.  Extra keys time the Llama-3-8B shape at
 32K (configs[1]) and at 64K (the north_star target) the same way.
 
-``--impl reference`` times the reference algorithm on the host CPU (the
-oracle port, oracle/fsa_oracle.py -- the reference is Python + Cython and is
-not present on the GPU box) on a labelled bounded sample, rank 0 only.
+``--impl reference`` times the reference on the host CPU -- the blockattn
+package installed into baseline/_ref (its compiled Cython core), or the
+oracle port when that is absent -- on a labelled bounded sample, rank 0 only.
 """
 
 from __future__ import annotations
@@ -510,9 +510,59 @@ def run_ours(args, rank, world, local_rank):
 
 
 # ---------------------------------------------------------------------------
-# CPU reference arm (the oracle port -- the reference itself is Python and is
-# not present on the GPU box)
+# CPU reference arm: the reference package itself (blockattn, installed
+# offline into baseline/_ref with its compiled Cython core; it travels to the
+# GPU box with the snapshot), through its own public API.  Its sliding branch
+# is dense O(N^2) (oracle.py:39-44, 64-74, 102-131) -- 2 GB of float64 per head
+# at 16K -- so that one branch runs the oracle's banded restatement.  Without
+# baseline/_ref the whole step is the oracle port.
 # ---------------------------------------------------------------------------
+REF_PATH = os.path.join(ROOT, "baseline", "_ref")
+
+
+def _reference_importable():
+    if not os.path.isdir(os.path.join(REF_PATH, "blockattn")):
+        return False
+    sys.path.insert(0, REF_PATH)
+    try:
+        import blockattn  # noqa: F401
+        return blockattn.get_backend() == "compiled"
+    except Exception:
+        return False
+
+
+def _ref_group(args_tuple):
+    """One KV group of the headline workload on its first n_tok tokens, through
+    blockattn's public API: compress_kv -> importance scores -> top-k ->
+    compressed / selected (kv_major) / sliding forward -> gated combine, then
+    the selected backward (kv_major.selected_backward) and the sliding
+    backward -- the reference's differentiable branches."""
+    n_tok, seed = args_tuple
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    sys.path.insert(0, REF_PATH)
+    import blockattn as ba
+    import blockattn.rng as brng
+    from blockattn import kv_major
+    from oracle import fsa_oracle as O
+    w = WORKLOADS[HEADLINE]
+    g = w["h"] // w["h_K"]
+    cfg = ba.make_config(N=n_tok, d_K=w["d"], d_V=w["d"], h=g, h_K=1, B_K=w["B_K"], T=w["T"], W=w["W"])
+    Q, K, V = brng.make_qkv(cfg, seed)
+    dO = brng.make_dout(cfg, seed)
+    tau = brng.make_gates(cfg, seed)
+    c = O.cfg_of(N=n_tok, d_K=w["d"], d_V=w["d"], h=g, h_K=1, B_K=w["B_K"], T=w["T"], W=w["W"])
+    t0 = time.perf_counter()
+    cmp = ba.compress_kv(K, V, cfg)
+    sel = ba.select_topk_blocks(ba.importance_scores_from_compressed(Q, cmp.K_cmp, cfg), cfg)
+    o_cmp = ba.compressed_attention_forward(Q, cmp, cfg)
+    o_sel, _ = kv_major.selected_forward(Q, K, V, sel, cfg)
+    o_sl, _ = O.sliding_forward(Q, K, V, c)  # banded (the reference's is dense O(N^2))
+    ba.gated_combine([o_cmp, o_sel, ba.AttentionOutput(o_sl, None)], tau, cfg)
+    kv_major.selected_backward(Q, K, V, sel, dO * tau[:, 1][:, None, None], cfg)
+    O.sliding_backward(Q, K, V, dO * tau[:, 2][:, None, None], c)
+    return time.perf_counter() - t0
+
+
 def _cpu_group(args_tuple):
     n_tok, seed = args_tuple
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
@@ -529,23 +579,29 @@ def _cpu_group(args_tuple):
 
 
 def cpu_baseline(sample_n=CPU_SAMPLE_N, steps=1):
-    """The oracle port on the host cores: one process per KV group (bit-exact
-    sharding); sample = the first ``sample_n`` tokens of each KV
-    group of the headline workload, fwd+bwd of every branch."""
+    """The reference (or, without baseline/_ref, the oracle port) on the host
+    cores: one process per KV group (bit-exact sharding); sample =
+    the first ``sample_n`` tokens of each KV group of the headline workload."""
     import multiprocessing as mp
     w = WORKLOADS[HEADLINE]
     cores = max(1, min(len(os.sched_getaffinity(0)), w["h_K"]))
+    real = _reference_importable()
+    fn = _ref_group if real else _cpu_group
     times = []
     with mp.get_context("spawn").Pool(cores) as pool:
         for s in range(steps):
             t0 = time.perf_counter()
-            pool.map(_cpu_group, [(sample_n, 100 + s * 16 + kh) for kh in range(w["h_K"])])
+            pool.map(fn, [(sample_n, 100 + s * 16 + kh) for kh in range(w["h_K"])])
             times.append(time.perf_counter() - t0)
     wall = statistics.median(times)
-    return {"value": round(sample_n / wall, 2), "unit": "tokens/s", "cores": cores, "kind": "port",
+    what = ("blockattn (baseline/_ref, compiled Cython core) public API; the sliding branch "
+            "as the oracle's banded restatement (the reference's is dense O(N^2))" if real
+            else "the oracle port (float64 numpy)")
+    return {"value": round(sample_n / wall, 2), "unit": "tokens/s", "cores": cores,
+            "kind": "reference" if real else "port",
             "sample": f"all {w['h_K']} KV groups of {HEADLINE}, first {sample_n} tokens "
                       f"(N={sample_n} causal prefix of the 131072-token sequence), NSA fwd+bwd "
-                      f"in float64 numpy, {cores} processes; {wall:.1f} s wall"}
+                      f"via {what}, {cores} processes; {wall:.1f} s wall"}
 
 
 def arm_config(world, name=HEADLINE, seq_len=None, sample=None):
