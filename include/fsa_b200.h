@@ -328,6 +328,16 @@ int fsa_gate_backward_full_fold(const fsa_shape* s, int dtype, const void* dOut,
 int fsa_qm_fwd(const fsa_shape* s, int dtype, const void* Q, const void* K, const void* V,
                const int32_t* idx, void* out, void* lse, void* stream);
 
+/* The NSA query-major forward on tcgen05 (query_major.py:45-69 with the
+ * min_tile padding of :32-42): bf16, d = 128, B_K = 64, g <= 16, T <= 16.
+ * Per (kv head, token) the g heads (padded to max(g, min_tile), rounded up to
+ * 8) ride on the MMA's N side against pairs of 64-key blocks on M; an exact
+ * two-pass softmax per token.  V16 / vscale: the fsa_v_to_f16 copy of V;
+ * out (N, h, 128) f32, lse (h, N) f32. */
+int fsa_qm_fwd_tc(const fsa_shape* s, const void* Q, const void* K, const void* V16,
+                  const float* vscale, const int32_t* idx, void* out, void* lse, int min_tile,
+                  void* stream);
+
 /* NSA query-major selected backward (query_major.py:72-99, _core.pyx:184-241):
  * per (KV head, token) task, P recomputed from lse, dQ rows written, dK / dV
  * ([N][h_K][d], acc; zeroed here) scattered with atomics.  lse, delta [h][N]

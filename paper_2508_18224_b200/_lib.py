@@ -81,6 +81,7 @@ SIGNATURES = {
     "fsa_cmp_bwd_workspace_bytes": ([_sp, _i], _sz),
     "fsa_cmp_bwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "fsa_gate_backward_full": ([_sp, _i] + [_vp] * 13, _i),
+    "fsa_qm_fwd_tc": ([_sp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp], _i),
     "fsa_qm_fwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "fsa_qm_bwd": ([_sp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "fsa_check_finite": ([_i, _vp, _i64, _vp, _vp], _i),

@@ -41,16 +41,31 @@ def _meter_forward(sel: SelectionTensor, cfg, meter: TrafficMeter) -> None:
     ph.flops += steps * 2 * pad * cfg.B_K * (cfg.d_K + cfg.d_V)
 
 
+def tc_supported(cfg, dt) -> bool:
+    """bf16, d = 128, B_K = 64, g <= 16, T <= 16: the tcgen05 query-major forward."""
+    return (dt == torch.bfloat16 and cfg.d_K == 128 and cfg.d_V == 128 and cfg.B_K == 64
+            and cfg.g <= 16 and max(cfg.g, cfg.min_tile) <= 16 and cfg.T <= 16)
+
+
 def selected_forward(Q, K, V, sel: SelectionTensor, cfg) -> tuple[AttentionOutput, TrafficMeter]:
-    """query_major.py:45-69 on the device: (AttentionOutput, TrafficMeter)."""
+    """query_major.py:45-69 on the device: (AttentionOutput, TrafficMeter).
+    bf16 d = 128 runs the tcgen05 kernel (``fsa_qm_fwd_tc``: the g heads padded
+    to max(g, min_tile) on the MMA's N side, a K/V tile load per (token, block
+    pair)); other shapes the CUDA-core kernel (``fsa_qm_fwd``)."""
     dt, q, k, v, _ = _intake(cfg, Q, K, V)
     validate_selection(sel, cfg)
     acc = _lib.acc_dtype(dt)
     out = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=acc, device=q.device)
     lse = torch.empty((cfg.h, cfg.N), dtype=acc, device=q.device)
     s = _lib.shape_of(cfg)
-    _lib.call("fsa_qm_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(q), _lib.ptr(k),
-              _lib.ptr(v), _lib.ptr(sel.idx), _lib.ptr(out), _lib.ptr(lse), _lib.stream())
+    if tc_supported(cfg, dt):
+        v16, vscale = _lib.v_to_f16(cfg, v)
+        _lib.call("fsa_qm_fwd_tc", ctypes.byref(s), _lib.ptr(q), _lib.ptr(k), _lib.ptr(v16),
+                  _lib.ptr(vscale), _lib.ptr(sel.idx), _lib.ptr(out), _lib.ptr(lse),
+                  int(cfg.min_tile), _lib.stream())
+    else:
+        _lib.call("fsa_qm_fwd", ctypes.byref(s), _lib.dt_code(dt), _lib.ptr(q), _lib.ptr(k),
+                  _lib.ptr(v), _lib.ptr(sel.idx), _lib.ptr(out), _lib.ptr(lse), _lib.stream())
     meter = TrafficMeter()
     _meter_forward(sel, cfg, meter)
     return AttentionOutput(out=logical(out), lse=lse), meter

@@ -529,6 +529,10 @@ def test_tc_sliding_backward_vs_oracle(kw):
     (dict(N=1024, d_K=64, d_V=64, h=4, h_K=4, B_K=32, T=6), "f32"),
     (dict(N=2048, d_K=128, d_V=128, h=16, h_K=2, B_K=64, T=8), "bf16"),
     (dict(N=1024, d_K=128, d_V=128, h=7, h_K=1, B_K=64, T=5), "bf16"),
+    (dict(N=4096, d_K=128, d_V=128, h=8, h_K=2, B_K=64, T=16), "bf16"),    # tcgen05, g = 4
+    (dict(N=2048, d_K=128, d_V=128, h=5, h_K=1, B_K=64, T=16), "bf16"),    # g = 5
+    (dict(N=2048, d_K=128, d_V=128, h=2, h_K=2, B_K=64, T=16), "bf16"),    # g = 1
+    (dict(N=1024, d_K=128, d_V=128, h=32, h_K=2, B_K=64, T=11), "bf16"),   # g = 16: N side 16
 ])
 def test_query_major_forward_vs_oracle(kw, run_dt):
     c = O.cfg_of(**kw)
