@@ -280,6 +280,10 @@ __global__ void __launch_bounds__(256) topk_stream_kernel(const float* __restric
   }
 }
 
+// NCH > 0: the row's candidates stay in registers (NCH chunks of 128, b <= 128 NCH):
+// one global read instead of two and no re-masking in pass 2.  NCH = 0: stream
+// from global twice.  Pass 2 skips the warp scan of chunks without a candidate.
+template <int NCH>
 __global__ void __launch_bounds__(256) topk_stream4_kernel(const float* __restrict__ scores,
                                                           int32_t* __restrict__ idx, int64_t rows,
                                                           int64_t N, int64_t B_K, int64_t b, int T) {
@@ -326,12 +330,25 @@ __global__ void __launch_bounds__(256) topk_stream4_kernel(const float* __restri
   // (no separate "<= T selectable" pass: then theta = 1 and every selectable
   // key is a candidate, which the rank path below returns in index order)
   float lmf = -INFINITY;
-#pragma unroll 2
-  for (int base = 0; base < ncand; base += 128) {
-    float v4[4];
-    vals4(base, v4);
+  float vr[NCH > 0 ? NCH : 1][4];
+  if constexpr (NCH > 0) {
 #pragma unroll
-    for (int e = 0; e < 4; ++e) lmf = fmaxf(lmf, v4[e]);
+    for (int k = 0; k < NCH; ++k)
+      if (k * 128 < ncand) vals4(k * 128, vr[k]);
+#pragma unroll
+    for (int k = 0; k < NCH; ++k)
+      if (k * 128 < ncand) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) lmf = fmaxf(lmf, vr[k][e]);
+      }
+  } else {
+#pragma unroll 2
+    for (int base = 0; base < ncand; base += 128) {
+      float v4[4];
+      vals4(base, v4);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) lmf = fmaxf(lmf, v4[e]);
+    }
   }
   // ---- theta: T-th largest lane maximum (warp bitonic, descending)
   uint32_t lm = score_key32(lmf);  // 0 for an all-unselectable lane
@@ -351,9 +368,7 @@ __global__ void __launch_bounds__(256) topk_stream4_kernel(const float* __restri
   // ---- pass 2: candidates >= theta, packed so that larger = better
   unsigned long long* slots = reinterpret_cast<unsigned long long*>(hist);
   int cand = 0;
-  for (int base = 0; base < ncand; base += 128) {
-    float v4[4];
-    vals4(base, v4);
+  auto chunk = [&](int base, const float (&v4)[4]) {
     bool c[4];
     int cnt = 0;
 #pragma unroll
@@ -361,6 +376,7 @@ __global__ void __launch_bounds__(256) topk_stream4_kernel(const float* __restri
       c[e] = v4[e] > -INFINITY && v4[e] >= thf;
       cnt += c[e];
     }
+    if (!__any_sync(0xffffffffu, cnt > 0)) return;  // no candidate in this chunk
     int tot;
     int pos = cand + excl_scan(cnt, tot);
 #pragma unroll
@@ -372,6 +388,17 @@ __global__ void __launch_bounds__(256) topk_stream4_kernel(const float* __restri
         ++pos;
       }
     cand += tot;
+  };
+  if constexpr (NCH > 0) {
+#pragma unroll
+    for (int k = 0; k < NCH; ++k)
+      if (k * 128 < ncand) chunk(k * 128, vr[k]);
+  } else {
+    for (int base = 0; base < ncand; base += 128) {
+      float v4[4];
+      vals4(base, v4);
+      chunk(base, v4);
+    }
   }
   __syncwarp();
   if (cand <= 32) {
@@ -587,8 +614,14 @@ int topk_impl(const fsa_shape* s, const void* scores, int32_t* idx, cudaStream_t
   const int T = (int)s->T;
   if (rows == 0) return FSA_OK;
   if (sizeof(S) == 4 && T <= 32 && b % 4 == 0) {
-    topk_stream4_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>((const float*)scores, idx, rows,
-                                                                   s->N, s->B_K, b, T);
+    const unsigned grid = (unsigned)((rows + 7) / 8);
+    const float* sc = (const float*)scores;
+    if (b <= 512)
+      topk_stream4_kernel<4><<<grid, 256, 0, st>>>(sc, idx, rows, s->N, s->B_K, b, T);
+    else if (b <= 1024)
+      topk_stream4_kernel<8><<<grid, 256, 0, st>>>(sc, idx, rows, s->N, s->B_K, b, T);
+    else  // longer rows: 64+ registers of candidates cost more occupancy than the re-read
+      topk_stream4_kernel<0><<<grid, 256, 0, st>>>(sc, idx, rows, s->N, s->B_K, b, T);
   } else if (sizeof(S) == 4 && T <= 32) {
     topk_stream_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>((const float*)scores, idx, rows,
                                                                   s->N, s->B_K, b, T);
