@@ -32,10 +32,11 @@
 // Roles: warps 0-7 two softmax warpgroups that ping-pong over items (wg owns
 // items n with n % 2 == wg and its own Q/dO, S/dP and P/dS stages; after its
 // item's products land it stages the dQ epilogue in its now-free P/dS smem),
-// warps 8-11 cp.async gather loaders (one item's gather kept in flight; TMA
-// tile::gather4 measured ~70 cycles per 512 B request -- too slow for 64 KB
-// items), warp 12 the MMA issuer (S/dP of item n+1 issued ahead of the
-// products of item n).
+// warps 8-11 loaders: K_i / V_i of each task by 3-D TMA boxes (one lane),
+// the item's gathered Q / dO rows by cp.async (one item's gather kept in
+// flight; TMA tile::gather4 measured ~70 cycles per 512 B request -- too slow
+// for 64 KB items), warp 12 the MMA issuer (S/dP of item n+1 issued ahead of
+// the products of item n).
 // Tasks are claimed dynamically, head-major (tc_sched.cuh).  The sliding
 // branch's backward runs the same kernel with each block's contiguous token
 // window as its rows and a band mask (oracle.py:102-131).
@@ -85,7 +86,8 @@ constexpr float kP16 = 32768.f;             // P16 = P 2^15
 constexpr float kDS16 = 1.f / 8388608.f;    // dS16 = P (dP16 - delta16) 2^-23
 
 struct Params {
-  CUtensorMap tmQ, tmO, tmK, tmV;  // sliding / compressed modes: TMA token boxes
+  CUtensorMap tmQ, tmO;  // sliding / compressed modes: TMA token boxes of Q / dO
+  CUtensorMap tmK, tmV;  // every mode: the task's 64 key rows (TMA boxes)
   CUtensorMap tmDQ;                 // dq partial rows [h N T][128] fp16 (scatter4 stores)
   long long* trace;  // debug timeline (CTA 0, first 256 items), null in production
   const __half *Q, *K, *V, *dO;  // the fp16 staged copies (fsa_stage_f16_ops)
@@ -244,13 +246,14 @@ __global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const _
     // The newest gather stays in flight (unpublished) while the next one is
     // issued; any wait that could block first publishes it.
     uint32_t pend = 0;      // QDF barrier of the in-flight Q/dO gather
-    bool kv_pend = false;   // the task's K/V gather is not yet published
+    int64_t pend_n = 0;     // (trace) its item
     auto publish = [&]() {
       asm volatile("cp.async.wait_group 0;" ::: "memory");
       fence_proxy_async();
-      if (kv_pend) mbar_arrive(bar(B_KVF));
-      if (pend) mbar_arrive(pend);
-      kv_pend = false;
+      if (pend) {
+        mbar_arrive(pend);
+        if (lr == 0) K8_TRACE(pend_n, 14);  // gather landed (published)
+      }
       pend = 0;
     };
     if (SL != 0) {
@@ -301,14 +304,18 @@ __global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const _
       const TaskRows tr = rows_of_slot(ts, p.tpi);
       if (tr.nitems == 0) continue;
       mbar_spin(bar(B_KVE), (uint32_t)((kseq & 1) ^ 1));
-      {  // warps 8,9: K rows 0-31, 32-63; warps 10,11: V rows 0-31, 32-63
-        const int lw = warp - 8, row0 = (lw & 1) * 32;
-        const __half* src =
-            (lw < 2 ? p.K : p.V) + ((tr.i * kBK + row0 + lane) * p.h_K + tr.kh) * kD;
-        warp_gather_rows32(sb + (lw < 2 ? kOffK : kOffV), 8192u, row0, src, true, lane);
-        asm volatile("cp.async.commit_group;" ::: "memory");
+      // K_i / V_i: the block's 64 contiguous key rows of this kv head, one 3-D
+      // TMA box per 64-column half (loaded once per task, FSA's amortisation)
+      if (lr == 0) {
+        mbar_arrive_expect_tx(bar(B_KVF), 32768u);
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          tma_load_3d(sb + kOffK + hf * 8192u, &p.tmK, hf * 64, (int)tr.kh, (int)(tr.i * kBK), bar(B_KVF));
+          tma_load_3d(sb + kOffV + hf * 8192u, &p.tmV, hf * 64, (int)tr.kh, (int)(tr.i * kBK), bar(B_KVF));
+        }
+      } else {
+        mbar_arrive(bar(B_KVF));
       }
-      kv_pend = true;
       int32_t ent_next = kt < p.tpi ? entry_at<SL>(p, tr, kt) : 0;
       for (int c = 0; c < tr.nitems; ++c, ++n) {
         const int s = (int)(n & 1);
@@ -323,6 +330,7 @@ __global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const _
           token_of<SL>(p, tr, pos, ent, t, slot);
           row = t * p.h + tr.kh * p.g + hh;
         }
+        if (lr == 0) K8_TRACE(n, 15);  // loader ready for this item (before the stage waits)
         // the dO half of the stage frees first (after the dV product): gather it
         // while the dK / dQ products still read Q
         if (!mbar_test(bar(B_DE + s), par)) {
@@ -339,11 +347,26 @@ __global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const _
         // everything but this gather has landed: publish the previous one
         asm volatile("cp.async.wait_group 1;" ::: "memory");
         fence_proxy_async();
-        if (kv_pend) mbar_arrive(bar(B_KVF));
-        if (pend) mbar_arrive(pend);
-        kv_pend = false;
+        if (pend) {
+          mbar_arrive(pend);
+          if (lr == 0) K8_TRACE(pend_n, 14);  // gather landed (published)
+        }
         pend = bar(B_QDF + s);
+        pend_n = n;
         if (lr == 0) K8_TRACE(n, 0);  // gather issued
+        {  // L2 prefetch of the next item's rows: its gather waits for a free stage
+           // (-2 % at 128K where the rows miss L2; neutral at 32K)
+          const int64_t pos1 = pos + p.tpi;
+          if (kt < p.tpi && pos1 < tr.ntok) {
+            int64_t t1, slot1;
+            token_of<SL>(p, tr, pos1, ent_next, t1, slot1);
+            const int64_t row1 = t1 * p.h + tr.kh * p.g + hh;
+            prefetch_l2(p.Q + row1 * kD);
+            prefetch_l2(p.Q + row1 * kD + 64);
+            prefetch_l2(p.dO + row1 * kD);
+            prefetch_l2(p.dO + row1 * kD + 64);
+          }
+        }
       }
       ++kseq;
     }
@@ -398,6 +421,7 @@ __global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const _
               const uint32_t q = sb + kOffQ + s * kTile, o = sb + kOffDO + s * kTile;
               const uint32_t tS = tmem + 128u * (uint32_t)tm;
               if (elect_one()) {
+                K8_TRACE(ns, 12);  // S/dP issue starts
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                   const uint32_t ko = (k >> 2) * 16384u + (k & 3) * 32u, kk = (k >> 2) * 8192u + (k & 3) * 32u;
@@ -484,6 +508,7 @@ __global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const _
         s_stream();
         if (a_done && np == ns) break;
         // watchdog: trap instead of hanging if neither stream can move for seconds
+        // (polling hot or with a 16 ns nap measured the same as 64 ns)
         if (progressed) {
           idle_since = 0;
         } else if (idle_since == 0) {
@@ -665,7 +690,7 @@ __global__ void __launch_bounds__(threads_of<SL>(), 1) tc_sel_bwd_kernel(const _
         }
         fence_proxy_async();
         mbar_arrive(bar(B_PDF + s));
-        if (lane == 0) K8_TRACE(n, 9 + (warp & 3));  // P/dS written by this warp
+        if (lane == 0 && (warp & 3) < 3) K8_TRACE(n, 9 + (warp & 3));  // P/dS written by this warp
         if (r == 0) K8_TRACE(n, 3);  // P/dS written
         // products of this item landed -> dQ partial out of TMEM; stage the
         // bf16 rows in this wg's (now consumed) P buffer for coalesced stores
@@ -812,6 +837,8 @@ int tc_sel_bwd(const fsa_shape* s, const void* Q, const void* K, const void* V, 
   p.qlist = qlist;
   p.counter = plan_view(*s, work).counter;
   int rc = make_tmap_rows(&p.tmDQ, dq_buf, s->h * s->N * s->T, 1);  // scatter4 dq rows
+  if (!rc) rc = make_tmap_tokens(&p.tmK, K, s->N, s->h_K, 1, 64);  // K_i / V_i boxes
+  if (!rc) rc = make_tmap_tokens(&p.tmV, V, s->N, s->h_K, 1, 64);
   if (rc) return rc;
   return launch_bwd(p, st);
 }

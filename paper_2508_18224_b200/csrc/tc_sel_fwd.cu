@@ -15,7 +15,8 @@
 //              operand) and the partial rows leave by TMA tile::scatter4
 //   warps 8-11 loaders: cp.async gather of an item's 128 query rows (TPI
 //              tokens x g group heads); one item's gather stays in flight while
-//              the next is issued (4 Q stages); K_i/V_i per task (2 stages)
+//              the next is issued (4 Q stages); K_i/V_i per task by 3-D TMA
+//              boxes from one lane (2 stages)
 //   warp  12   MMA issuer (one elected lane): S = Q K^T (M128 N64 K128, bf16)
 //              and O = P V (M128 N128 K64, fp16) into TMEM, tcgen05.commit;
 //              S of item n+1 is issued before PV of item n
@@ -68,6 +69,7 @@ constexpr uint32_t kIdescPV = idesc_f16(128, 128, false, true);  // P, V16 in fp
 
 struct Params {
   CUtensorMap tmO;
+  CUtensorMap tmK, tmV;  // the task's 64 key rows of K / V16 (3-D TMA boxes)
   long long* trace;  // debug timeline (CTA 0, trace build only)  // obuf rows [h N T][128] fp16 (tile::scatter4 stores)
   const __nv_bfloat16 *Q, *K;
   const __half* V;  // the scaled fp16 copy (fsa_v_to_f16)
@@ -160,16 +162,20 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
       if (tr.nitems == 0) continue;
       const int kvs = kseq & 1;
       mbar_wait(bar(B_KVE + kvs), (uint32_t)(((kseq >> 1) & 1) ^ 1));
-      {  // warps 4,5: K rows 0-31, 32-63; warps 6,7: V rows 0-31, 32-63
-        const int lw = warp - 8, row0 = (lw & 1) * 32;
-        const int64_t off = ((int64_t)(tr.i * kBK + row0 + lane) * p.h_K + tr.kh) * kD;
-        const void* src = lw < 2 ? (const void*)(p.K + off) : (const void*)(p.V + off);
-        if (MODE != FSA_FWD_STATS || lw < 2)  // STATS: no values
-          warp_gather_rows32(sb + kOffKV + kvs * kKVBytes + (lw < 2 ? 0u : 16384u), 8192u, row0,
-                             src, true, lane);
-        asm volatile("cp.async.commit_group;" ::: "memory");
+      // K_i / V_i: the block's 64 contiguous key rows of this kv head, one 3-D
+      // TMA box per 64-column half (loaded once per task, FSA's amortisation)
+      if (lr == 0) {
+        const uint32_t kv = sb + kOffKV + kvs * kKVBytes;
+        mbar_arrive_expect_tx(bar(B_KVF + kvs), MODE == FSA_FWD_STATS ? 16384u : 32768u);
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          tma_load_3d(kv + hf * 8192u, &p.tmK, hf * 64, (int)tr.kh, (int)(tr.i * kBK), bar(B_KVF + kvs));
+          if (MODE != FSA_FWD_STATS)  // STATS: no values
+            tma_load_3d(kv + 16384u + hf * 8192u, &p.tmV, hf * 64, (int)tr.kh, (int)(tr.i * kBK), bar(B_KVF + kvs));
+        }
+      } else {
+        mbar_arrive(bar(B_KVF + kvs));
       }
-      bool kv_pending = true;
       const int32_t* ql = p.qlist + (int64_t)tr.kh * p.N * p.T + tr.beg;
       // the query-list entry of the next item is loaded one item ahead, so its
       // latency hides behind the current item's stage wait and gather
@@ -190,10 +196,6 @@ __global__ void __launch_bounds__(kThreads, 1) tc_sel_fwd_kernel(const __grid_co
         // everything but this item's gather has landed: publish it
         asm volatile("cp.async.wait_group 1;" ::: "memory");
         fence_proxy_async();
-        if (kv_pending) {
-          mbar_arrive(bar(B_KVF + kvs));
-          kv_pending = false;
-        }
         if (prev_stage >= 0) mbar_arrive(bar(B_QF + prev_stage));
         prev_stage = s;
       }
@@ -551,6 +553,9 @@ int tc_sel_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V,
   p.counter = p.plan.counter;
   if (mode == FSA_FWD_LOCAL)
     if (int rc = make_tmap_rows(&p.tmO, obuf, plan_max_items(*s) * kRows, 32)) return rc;
+  if (int rc = make_tmap_tokens(&p.tmK, K, s->N, s->h_K, 1, kBK)) return rc;  // K_i / V_i boxes
+  if (mode != FSA_FWD_STATS)
+    if (int rc = make_tmap_tokens(&p.tmV, V, s->N, s->h_K, 1, kBK)) return rc;
   cudaMemsetAsync(p.counter, 0, sizeof(int32_t), st);
   static unsigned long long done[3] = {0, 0, 0};
   if (mode == FSA_FWD_STATS) {

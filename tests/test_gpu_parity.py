@@ -654,6 +654,9 @@ def test_query_head_split_matches_unsharded():
     dict(N=1088, d_K=128, d_V=128, h=6, h_K=1, B_K=64, T=3, W=1),
     dict(N=1088, d_K=128, d_V=128, h=2, h_K=2, B_K=64, T=4, W=333),
     dict(N=512, d_K=128, d_V=128, h=128, h_K=1, B_K=64, T=4, W=128),
+    # T > 32 (the dQ reduce of the tensor-core backward at T in (32, b])
+    dict(N=4096, d_K=128, d_V=128, h=8, h_K=2, B_K=64, T=48, W=256),
+    dict(N=4160, d_K=128, d_V=128, h=5, h_K=1, B_K=64, T=64, W=512),
 ])
 def test_nsa_step_shapes_vs_oracle(kw):
     c = O.cfg_of(**kw)

@@ -38,7 +38,7 @@ def main():
     if mode == "sel":
         pass
     t0 = int(t[0, 0])
-    names = ["gather", "sdp_iss", "sdp_land", "pds_done", "prod_iss", "prod_land", "dq_tmem", "dq_store", "prod_rdy", "pds_w0", "pds_w1", "pds_w2", "pds_w3", "sdp_raw", "ld_wait", "ld_free"]
+    names = ["gather", "sdp_iss", "sdp_land", "pds_done", "prod_iss", "prod_land", "dq_tmem", "dq_store", "prod_rdy", "pds_w0", "pds_w1", "pds_w2", "sdp_start", "sdp_raw", "ld_land", "ld_ready"]
     print("item " + " ".join(f"{n:>9}" for n in names) + "   (cycles from item 0 gather)")
     prev = None
     for i in range(0, 120):
