@@ -1,11 +1,12 @@
 #!/bin/bash
 # One GPU verification pass (run under gpurun): GPU tests (without the
 # whole-group oracle runs unless FULL=1), smoke, bench -> gpurun_out/
-K=${FULL:+}
-SEL=${FULL:+-k ""}
-if [ -z "$FULL" ]; then SEL='-k "not whole"'; fi
 rm -f gpurun_out/parity.jsonl
-eval FSA_PARITY_REPORT=gpurun_out/parity.jsonl timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider -rf $SEL > gpurun_out/gputest_all.log 2>&1
+if [ -n "$FULL" ]; then
+  FSA_PARITY_REPORT=gpurun_out/parity.jsonl timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider -rf > gpurun_out/gputest_all.log 2>&1
+else
+  FSA_PARITY_REPORT=gpurun_out/parity.jsonl timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider -rf -k "not whole" > gpurun_out/gputest_all.log 2>&1
+fi
 echo "pytest=$?"; tail -4 gpurun_out/gputest_all.log
 timeout 200 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
 if [ -z "$NOBENCH" ]; then

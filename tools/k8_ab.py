@@ -20,6 +20,11 @@ from paper_2508_18224_b200 import _lib, nsa  # noqa: E402
 from paper_2508_18224_b200.kv_major import _backward_core  # noqa: E402
 
 
+# entries called by nsa_backward (others are timed inside nsa_forward)
+BACKWARD = ("fsa_slide_bwd", "fsa_dq_reduce_add", "fsa_gate_backward_fold", "fsa_bwd_delta",
+            "fsa_stage_f16_ops")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--N", type=int, default=131072)
@@ -60,6 +65,8 @@ def main():
             timed.ev = []
             if a.entry == "fsa_sel_bwd":
                 _backward_core(cfg, torch.bfloat16, q, k, v, do, ctx.sel, ctx.inv, ctx.out_sel, ctx.lse_sel)
+            elif a.entry in BACKWARD:
+                nsa.nsa_backward(ctx, do)
             else:
                 nsa.nsa_forward(q, k, v, tau, cfg)
             torch.cuda.synchronize()
@@ -67,11 +74,11 @@ def main():
                 res[vv].append(sum(e0.elapsed_time(e1) for e0, e1 in timed.ev))
     _lib.call = orig
     rows = int(ctx.inv.offsets[:, -1].sum()) * cfg.g
-    fl = (10 if a.entry == "fsa_sel_bwd" else 4) * 128 * 64 * rows
+    fl = {"fsa_sel_bwd": 10, "fsa_sel_fwd": 4}.get(a.entry, 0) * 128 * 64 * rows
     for vv in variants:
         m = statistics.median(res[vv])
-        print(f"N={a.N} h={a.h} {a.entry} {a.env}={vv}: {m:.3f} ms  {fl / m / 1e9:.0f} TFLOP/s  "
-              f"(min {min(res[vv]):.3f})")
+        tf = f"{fl / m / 1e9:.0f} TFLOP/s  " if fl else ""
+        print(f"N={a.N} h={a.h} {a.entry} {a.env}={vv}: {m:.3f} ms  {tf}(min {min(res[vv]):.3f})")
 
 
 if __name__ == "__main__":
