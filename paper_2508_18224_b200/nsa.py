@@ -85,7 +85,105 @@ def _gates(tau, cfg, acc, dev):
     return tau.to(acc).contiguous()
 
 
-def nsa_forward(q, k, v, tau, cfg, *, heads=None):
+# The tensor-core kernels index (token, head) rows with 32-bit offsets: a
+# problem (or a kv-head chunk of it) runs on them while N * h stays below this.
+TC_MAX_TOKEN_HEADS = 1 << 23
+
+
+@dataclasses.dataclass
+class ChunkedNSAContext:
+    """Forward state of a kv-head-chunked step: one NSAContext per chunk of
+    kv heads [lo, hi) (query heads [g lo, g hi))."""
+    cfg: object
+    dtype: torch.dtype
+    chunks: list  # [(kv_lo, kv_hi, NSAContext)]
+
+
+def kv_chunk_bytes(cfg, kv_heads: int) -> int:
+    """Device bytes of the transient buffers one chunk of ``kv_heads`` kv heads
+    allocates on top of the step's inputs and outputs (bf16 tensor-core path):
+    the importance scores (fp32 [h_K][N][b]), the FSA slot partials of the
+    forward (fp16 O rows + fp32 (m, l), items padded to 128 rows) or of the
+    backward (fp16 dq rows + exponents), whichever is larger, and the chunk's
+    fp16 operand copies and head slices."""
+    g, rows = cfg.g, cfg.g * cfg.N * cfg.T * kv_heads
+    scores = kv_heads * cfg.N * cfg.b * 4
+    partials = max(int(rows * 1.05) * (2 * cfg.d_V + 8), rows * (2 * cfg.d_K + 4))
+    per_token = kv_heads * g * (cfg.d_K * 2 * 4 + cfg.d_V * 4 * 4)  # q/dout slices + fp16 copies, fp32 branch outs
+    return scores + partials + cfg.N * per_token
+
+
+def plan_kv_chunk(cfg, budget_bytes: int | None = None) -> int:
+    """kv heads per chunk: the largest divisor of h_K whose chunk keeps
+    N * h under TC_MAX_TOKEN_HEADS (the tensor-core path) and, when a budget
+    is given, whose transient buffers fit it.  h_K means no chunking."""
+    best = 1
+    for c in range(1, cfg.h_K + 1):
+        if cfg.h_K % c:
+            continue
+        if cfg.N * cfg.g * c >= TC_MAX_TOKEN_HEADS and c > 1:
+            break
+        if budget_bytes is not None and kv_chunk_bytes(cfg, c) > budget_bytes and c > 1:
+            break
+        best = c
+    return best
+
+
+def _chunk_cfg(cfg, kv_heads):
+    return make_config(N=cfg.N, d_K=cfg.d_K, d_V=cfg.d_V, h=cfg.g * kv_heads, h_K=kv_heads,
+                       B_K=cfg.B_K, T=cfg.T, B_Q=cfg.B_Q, W=cfg.W,
+                       bytes_per_elem=cfg.bytes_per_elem, min_tile=cfg.min_tile)
+
+
+def _nsa_forward_chunked(q, k, v, tau, cfg, kv_chunk, keep_scores):
+    """Buffer-reusing schedule (PAPER.md:267 -- "process a subset of query
+    heads at each time, reusing the buffers"): the step runs one chunk of
+    kv heads (and their g query heads each) at a time, so the scores, the
+    slot partials and the dq partials are sized for the chunk and released
+    before the next one.  Every operator is independent per kv head
+    (selection.py:116-119, kv_major.py:127-140), so the result equals the
+    unchunked step bit for bit."""
+    dt = q.dtype
+    dev = q.device
+    _check(q, "Q", (cfg.N, cfg.h, cfg.d_K), dt, dev)
+    _check(k, "K", (cfg.N, cfg.h_K, cfg.d_K), dt, dev)
+    _check(v, "V", (cfg.N, cfg.h_K, cfg.d_V), dt, dev)
+    if cfg.h_K % kv_chunk:
+        raise ValueError(f"kv_chunk={kv_chunk} does not divide h_K={cfg.h_K}")
+    sub = _chunk_cfg(cfg, kv_chunk)
+    out = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=dt, device=dev)
+    chunks = []
+    for lo in range(0, cfg.h_K, kv_chunk):
+        hi = lo + kv_chunk
+        qs = q.narrow(1, lo * cfg.g, kv_chunk * cfg.g).contiguous()
+        ks, vs = k.narrow(1, lo, kv_chunk).contiguous(), v.narrow(1, lo, kv_chunk).contiguous()
+        o, c = nsa_forward(qs, ks, vs, tau, sub, kv_chunk=kv_chunk, keep_scores=keep_scores)
+        out.narrow(1, lo * cfg.g, kv_chunk * cfg.g).copy_(o)
+        chunks.append((lo, hi, c))
+    return out, ChunkedNSAContext(cfg, dt, chunks)
+
+
+def _nsa_backward_chunked(ctx: ChunkedNSAContext, dout, full):
+    cfg, dt = ctx.cfg, ctx.dtype
+    dev = dout.device
+    _check(dout, "dOut", (cfg.N, cfg.h, cfg.d_V), dt, dev)
+    acc = _lib.acc_dtype(dt)
+    dQ = torch.empty((cfg.N, cfg.h, cfg.d_K), dtype=acc, device=dev)
+    dK = torch.empty((cfg.N, cfg.h_K, cfg.d_K), dtype=acc, device=dev)
+    dV = torch.empty((cfg.N, cfg.h_K, cfg.d_V), dtype=acc, device=dev)
+    dtau = torch.zeros((cfg.N, 3), dtype=acc, device=dev) if full else None
+    for lo, hi, c in ctx.chunks:
+        g0, g1 = lo * cfg.g, hi * cfg.g
+        grads = nsa_backward(c, dout.narrow(1, g0, g1 - g0).contiguous(), full=full)
+        dQ.narrow(1, g0, g1 - g0).copy_(grads[0])
+        dK.narrow(1, lo, hi - lo).copy_(grads[1])
+        dV.narrow(1, lo, hi - lo).copy_(grads[2])
+        if full:
+            dtau += grads[3]  # the gate gradient sums over every head of a token
+    return (dQ, dK, dV, dtau) if full else (dQ, dK, dV)
+
+
+def nsa_forward(q, k, v, tau, cfg, *, heads=None, kv_chunk=None, keep_scores=True):
     """Returns (combined out (N, h, d_V), ctx).
 
     Storage-layout inputs: q (N, h, d_K), k (N, h_K, d_K), v (N, h_K, d_V), one
@@ -96,7 +194,24 @@ def nsa_forward(q, k, v, tau, cfg, *, heads=None):
     the block selection still see the whole group -- the importance scores
     sum over all g heads of a group (selection.py:105-120) -- then the
     selected and sliding branches and the combine run on the sub-group only.
-    Out and ctx describe the sub-problem (h = h_K * (hi - lo))."""
+    Out and ctx describe the sub-problem (h = h_K * (hi - lo)).
+
+    ``kv_chunk=c``: the buffer-reusing schedule -- c kv heads at a time (c
+    divides h_K), the ctx a ChunkedNSAContext; "auto" sizes c from the free
+    device memory (plan_kv_chunk).  Problems with N * h >= TC_MAX_TOKEN_HEADS
+    are chunked automatically so that every chunk runs on the tensor-core
+    kernels.  ``keep_scores=False`` drops the importance scores (h_K N b
+    floats) from the ctx once the selection is made."""
+    if kv_chunk == "auto":
+        free, _ = torch.cuda.mem_get_info(q.device)
+        kv_chunk = plan_kv_chunk(cfg, int(free * 0.8))
+    elif kv_chunk is None and heads is None and cfg.N * cfg.h >= TC_MAX_TOKEN_HEADS \
+            and q.dtype == torch.bfloat16:
+        kv_chunk = plan_kv_chunk(cfg)
+    if kv_chunk is not None and kv_chunk < cfg.h_K:
+        if heads is not None:
+            raise ValueError("heads= and kv_chunk= do not combine")
+        return _nsa_forward_chunked(q, k, v, tau, cfg, int(kv_chunk), keep_scores)
     dt = q.dtype
     acc = _lib.acc_dtype(dt)
     dev = q.device
@@ -168,7 +283,7 @@ def nsa_forward(q, k, v, tau, cfg, *, heads=None):
               st)
     del obuf, ml
     ctx = NSAContext(cfg, dt, q, k, v, tau, sel, inv, out_sel, lse_sel, out_slide, lse_slide,
-                     out_cmp, scores, Kc, Vc, lse_cmp, ops)
+                     out_cmp, scores if keep_scores else None, Kc, Vc, lse_cmp, ops)
     return out, ctx
 
 
@@ -185,6 +300,8 @@ def nsa_backward(ctx: NSAContext, dout, *, full: bool = False):
     statistics: tau exp(z - lse) = exp(z - (lse - ln tau)) and delta_c =
     sum out_c * dOut, so every branch backward reads the raw dOut -- no gated
     (and, in bf16, rounded) cotangent copies."""
+    if isinstance(ctx, ChunkedNSAContext):
+        return _nsa_backward_chunked(ctx, dout, full)
     cfg, dt = ctx.cfg, ctx.dtype
     _check(dout, "dOut", (cfg.N, cfg.h, cfg.d_V), dt, ctx.q.device)
     s = _lib.shape_of(cfg)
@@ -263,7 +380,39 @@ def _sel_slide_backward(ctx: NSAContext, dout, delta_sel, delta_slide, lse_sel, 
     return dQ, dK, dV
 
 
-def nsa_forward_backward(q, k, v, tau, dout, cfg, *, full: bool = False):
-    """One full step: forward then backward; returns (out, dQ, dK, dV[, dtau])."""
-    out, ctx = nsa_forward(q, k, v, tau, cfg)
-    return (out,) + tuple(nsa_backward(ctx, dout, full=full))
+def nsa_forward_backward(q, k, v, tau, dout, cfg, *, full: bool = False, kv_chunk=None):
+    """One full step: forward then backward; returns (out, dQ, dK, dV[, dtau]).
+    With ``kv_chunk`` each chunk's backward follows its forward directly, so
+    only one chunk's forward state is alive at a time (the forward's branch
+    outputs and statistics of the other chunks are never held together)."""
+    if kv_chunk == "auto":
+        free, _ = torch.cuda.mem_get_info(q.device)
+        kv_chunk = plan_kv_chunk(cfg, int(free * 0.8))
+    elif kv_chunk is None and cfg.N * cfg.h >= TC_MAX_TOKEN_HEADS and q.dtype == torch.bfloat16:
+        kv_chunk = plan_kv_chunk(cfg)
+    if kv_chunk is None or kv_chunk >= cfg.h_K:
+        out, ctx = nsa_forward(q, k, v, tau, cfg)
+        return (out,) + tuple(nsa_backward(ctx, dout, full=full))
+    dt, dev = q.dtype, q.device
+    _check(dout, "dOut", (cfg.N, cfg.h, cfg.d_V), dt, dev)
+    acc = _lib.acc_dtype(dt)
+    out = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=dt, device=dev)
+    dQ = torch.empty((cfg.N, cfg.h, cfg.d_K), dtype=acc, device=dev)
+    dK = torch.empty((cfg.N, cfg.h_K, cfg.d_K), dtype=acc, device=dev)
+    dV = torch.empty((cfg.N, cfg.h_K, cfg.d_V), dtype=acc, device=dev)
+    dtau = torch.zeros((cfg.N, 3), dtype=acc, device=dev) if full else None
+    for lo in range(0, cfg.h_K, kv_chunk):
+        g0, n = lo * cfg.g, kv_chunk * cfg.g
+        sub = _chunk_cfg(cfg, kv_chunk)
+        o, c = nsa_forward(q.narrow(1, g0, n).contiguous(), k.narrow(1, lo, kv_chunk).contiguous(),
+                           v.narrow(1, lo, kv_chunk).contiguous(), tau, sub, kv_chunk=kv_chunk,
+                           keep_scores=False)
+        out.narrow(1, g0, n).copy_(o)
+        grads = nsa_backward(c, dout.narrow(1, g0, n).contiguous(), full=full)
+        del c
+        dQ.narrow(1, g0, n).copy_(grads[0])
+        dK.narrow(1, lo, kv_chunk).copy_(grads[1])
+        dV.narrow(1, lo, kv_chunk).copy_(grads[2])
+        if full:
+            dtau += grads[3]
+    return (out, dQ, dK, dV, dtau) if full else (out, dQ, dK, dV)

@@ -778,3 +778,46 @@ def test_selection_fixture_round_trip(tag, tmp_path):
     assert loaded.idx.is_cuda
     np.testing.assert_array_equal(host(loaded.idx), host(sel.idx))
     fsa.validate_selection(loaded, cfg)
+
+
+# Buffer-reusing schedule: kv-head chunks of the step reuse the
+# scores / partial buffers; every operator is independent per kv head, so the
+# chunked step equals the unchunked one bit for bit (dtau: the per-token sum
+# over heads is taken chunk by chunk -> fp32 rounding only).
+@pytest.mark.parametrize("kv_chunk", [1, 2])
+def test_kv_chunked_step_matches_unchunked(kv_chunk):
+    kw = dict(N=4096, d_K=128, d_V=128, h=12, h_K=4, B_K=64, T=8, W=256)
+    cfg = _cfg(kw)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    mk = lambda *s: torch.randn(*s, device="cuda", dtype=torch.bfloat16, generator=g)  # noqa: E731
+    q, k, v, do = mk(cfg.N, cfg.h, 128), mk(cfg.N, cfg.h_K, 128), mk(cfg.N, cfg.h_K, 128), mk(cfg.N, cfg.h, 128)
+    tau = torch.rand(cfg.N, 3, device="cuda", generator=g)
+    out, ctx = fsa.nsa_forward(q, k, v, tau, cfg)
+    ref = (out,) + tuple(fsa.nsa_backward(ctx, do, full=True))
+    o2, c2 = fsa.nsa_forward(q, k, v, tau, cfg, kv_chunk=kv_chunk, keep_scores=False)
+    assert isinstance(c2, fsa.ChunkedNSAContext) and len(c2.chunks) == cfg.h_K // kv_chunk
+    got = (o2,) + tuple(fsa.nsa_backward(c2, do, full=True))
+    for a, b, name in zip(got[:4], ref[:4], ("out", "dQ", "dK", "dV")):
+        assert torch.equal(a, b), name
+    assert torch.allclose(got[4], ref[4], rtol=1e-5, atol=1e-6), "dtau"
+    fused = fsa.nsa_forward_backward(q, k, v, tau, do, cfg, full=True, kv_chunk=kv_chunk)
+    for a, b in zip(fused[:4], ref[:4]):
+        assert torch.equal(a, b)
+    assert torch.allclose(fused[4], ref[4], rtol=1e-5, atol=1e-6)
+
+
+def test_kv_chunk_auto_above_the_tensor_core_limit(monkeypatch):
+    """N * h past the 32-bit row-offset limit of the tensor-core kernels is
+    chunked by kv head automatically (here with the limit lowered)."""
+    from paper_2508_18224_b200 import nsa as nsa_mod
+    kw = dict(N=2048, d_K=128, d_V=128, h=8, h_K=4, B_K=64, T=8, W=128)
+    cfg = _cfg(kw)
+    g = torch.Generator(device="cuda").manual_seed(6)
+    mk = lambda *s: torch.randn(*s, device="cuda", dtype=torch.bfloat16, generator=g)  # noqa: E731
+    q, k, v = mk(cfg.N, cfg.h, 128), mk(cfg.N, cfg.h_K, 128), mk(cfg.N, cfg.h_K, 128)
+    tau = torch.rand(cfg.N, 3, device="cuda", generator=g)
+    ref, _ = fsa.nsa_forward(q, k, v, tau, cfg)
+    monkeypatch.setattr(nsa_mod, "TC_MAX_TOKEN_HEADS", cfg.N * 5)  # room for 2 kv heads x g = 2
+    out, ctx = fsa.nsa_forward(q, k, v, tau, cfg)
+    assert isinstance(ctx, fsa.ChunkedNSAContext) and len(ctx.chunks) == 2
+    assert torch.equal(out, ref)

@@ -217,3 +217,23 @@ def test_load_selection_rejects_truncated_and_mismatched(tmp_path):
         p.write_bytes(data)
         with pytest.raises(SelectionError, match="malformed selection"):
             load_selection(p)
+
+
+def test_plan_kv_chunk():
+    """kv-head chunk of the buffer-reusing schedule: the largest divisor of h_K
+    that keeps N * h under the tensor-core kernels' 32-bit row-offset limit
+    and (given a budget) fits the chunk's transient buffers."""
+    from paper_2508_18224_b200.nsa import TC_MAX_TOKEN_HEADS, kv_chunk_bytes
+    mk = lambda N, h, hk: fsa.make_config(N=N, d_K=128, d_V=128, h=h, h_K=hk, B_K=64, T=16, W=512)  # noqa: E731
+    assert fsa.plan_kv_chunk(mk(131072, 40, 8)) == 8          # the 128K headline: unchunked
+    assert fsa.plan_kv_chunk(mk(524288, 40, 8)) == 2          # 512K: 2 kv heads x g = 5
+    assert fsa.plan_kv_chunk(mk(262144, 32, 8)) == 4
+    assert fsa.plan_kv_chunk(mk(1 << 20, 40, 8)) == 1
+    for c in (mk(524288, 40, 8), mk(262144, 32, 8)):
+        k = fsa.plan_kv_chunk(c)
+        assert c.h_K % k == 0 and c.N * c.g * k < TC_MAX_TOKEN_HEADS
+    c = mk(131072, 40, 8)
+    assert kv_chunk_bytes(c, 2) < kv_chunk_bytes(c, 4) < kv_chunk_bytes(c, 8)
+    assert fsa.plan_kv_chunk(c, budget_bytes=kv_chunk_bytes(c, 4)) == 4
+    assert fsa.plan_kv_chunk(c, budget_bytes=kv_chunk_bytes(c, 4) - 1) == 2
+    assert fsa.plan_kv_chunk(c, budget_bytes=1) == 1
