@@ -135,7 +135,7 @@ def _chunk_cfg(cfg, kv_heads):
                        bytes_per_elem=cfg.bytes_per_elem, min_tile=cfg.min_tile)
 
 
-def _nsa_forward_chunked(q, k, v, tau, cfg, kv_chunk, keep_scores):
+def _nsa_forward_chunked(q, k, v, tau, cfg, kv_chunk, keep_scores=False):
     """Buffer-reusing schedule (PAPER.md:267 -- "process a subset of query
     heads at each time, reusing the buffers"): the step runs one chunk of
     kv heads (and their g query heads each) at a time, so the scores, the
@@ -183,7 +183,7 @@ def _nsa_backward_chunked(ctx: ChunkedNSAContext, dout, full):
     return (dQ, dK, dV, dtau) if full else (dQ, dK, dV)
 
 
-def nsa_forward(q, k, v, tau, cfg, *, heads=None, kv_chunk=None, keep_scores=True):
+def nsa_forward(q, k, v, tau, cfg, *, heads=None, kv_chunk=None, keep_scores=False):
     """Returns (combined out (N, h, d_V), ctx).
 
     Storage-layout inputs: q (N, h, d_K), k (N, h_K, d_K), v (N, h_K, d_V), one
@@ -200,8 +200,9 @@ def nsa_forward(q, k, v, tau, cfg, *, heads=None, kv_chunk=None, keep_scores=Tru
     divides h_K), the ctx a ChunkedNSAContext; "auto" sizes c from the free
     device memory (plan_kv_chunk).  Problems with N * h >= TC_MAX_TOKEN_HEADS
     are chunked automatically so that every chunk runs on the tensor-core
-    kernels.  ``keep_scores=False`` drops the importance scores (h_K N b
-    floats) from the ctx once the selection is made."""
+    kernels.  ``keep_scores=True`` keeps the importance scores (h_K N b
+    floats) in ctx.scores; by default they are released once the selection
+    is made."""
     if kv_chunk == "auto":
         free, _ = torch.cuda.mem_get_info(q.device)
         kv_chunk = plan_kv_chunk(cfg, int(free * 0.8))

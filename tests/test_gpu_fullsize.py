@@ -59,7 +59,7 @@ def test_fullsize_nsa_step(name):
     v = torch.randn(c.N, c.h_K, 128, device="cuda", dtype=bf, generator=gen)
     do = torch.randn(c.N, c.h, 128, device="cuda", dtype=bf, generator=gen)
     tau = torch.rand(c.N, 3, device="cuda", generator=gen)
-    out, ctx = nsa.nsa_forward(q, k, v, tau, cfg)
+    out, ctx = nsa.nsa_forward(q, k, v, tau, cfg, keep_scores=True)
     if spec["bwd"]:
         dQ, dK, dV = nsa.nsa_backward(ctx, do)
     torch.cuda.synchronize()
@@ -242,7 +242,7 @@ def test_fullsize_whole_group(name):
     v = torch.randn(N, hk, 128, device="cuda", dtype=bf, generator=gen)
     do = torch.randn(N, h, 128, device="cuda", dtype=bf, generator=gen)
     tau = torch.rand(N, 3, device="cuda", generator=gen)
-    out, ctx = nsa.nsa_forward(q, k, v, tau, cfg)
+    out, ctx = nsa.nsa_forward(q, k, v, tau, cfg, keep_scores=True)
     grads = nsa.nsa_backward(ctx, do) if spec["bwd"] else None
     torch.cuda.synchronize()
     _whole_group(name, spec, q, k, v, do, tau, out, ctx, grads, hk - 1)

@@ -396,7 +396,7 @@ def test_nsa_step_vs_oracle(run_dt):
     tdt = DT[run_dt]
     q, k, v, do = (dev(x, tdt).permute(0, 2, 1).contiguous() for x in (Q, K, V, dO))
     acc = torch.float32
-    out, ctx = fsa.nsa_forward(q, k, v, torch.from_numpy(tau).to("cuda", acc), cfg)
+    out, ctx = fsa.nsa_forward(q, k, v, torch.from_numpy(tau).to("cuda", acc), cfg, keep_scores=True)
     # selection parity on the GPU's own scores (SURVEY 8(c) score-path caveat)
     scores = host(ctx.scores).astype(np.float64)
     idx = O.select_topk(scores, c)
@@ -492,7 +492,7 @@ def test_tc_window_branches_vs_oracle(kw):
     # fused scores of the pipeline: every block a token's top-k reads
     out, ctx = fsa.nsa_forward(tQ.permute(0, 2, 1).contiguous(), tK.permute(0, 2, 1).contiguous(),
                                tV.permute(0, 2, 1).contiguous(),
-                               torch.full((cfg.N, 3), 1.0 / 3, device="cuda"), cfg)
+                               torch.full((cfg.N, 3), 1.0 / 3, device="cuda"), cfg, keep_scores=True)
     fused = host(ctx.scores)
     full = host(sc)
     causal = np.arange(c.b)[None, None, :] < (np.arange(c.N) // c.B_K)[None, :, None]
@@ -665,7 +665,7 @@ def test_nsa_step_shapes_vs_oracle(kw):
     dO = round_inputs(O.make_dout(c, 21), "bf16")
     tau = O.make_gates(c, 21)
     q, k, v, do = (dev(x, torch.bfloat16).permute(0, 2, 1).contiguous() for x in (Q, K, V, dO))
-    out, ctx = fsa.nsa_forward(q, k, v, torch.from_numpy(tau).to("cuda", torch.float32), cfg)
+    out, ctx = fsa.nsa_forward(q, k, v, torch.from_numpy(tau).to("cuda", torch.float32), cfg, keep_scores=True)
     idx = O.select_topk(host(ctx.scores).astype(np.float64), c)
     np.testing.assert_array_equal(host(ctx.sel.idx), idx)
     cmp = O.compress_kv(K, V, c)
@@ -693,7 +693,7 @@ def test_selection_vs_oracle_fp64_scores_near_ties():
     Q, K, V = (round_inputs(x, "bf16") for x in O.make_qkv(c, 1))
     tau = O.make_gates(c, 1)
     q, k, v = (dev(x, torch.bfloat16).permute(0, 2, 1).contiguous() for x in (Q, K, V))
-    _, ctx = fsa.nsa_forward(q, k, v, torch.from_numpy(tau).to("cuda", torch.float32), cfg)
+    _, ctx = fsa.nsa_forward(q, k, v, torch.from_numpy(tau).to("cuda", torch.float32), cfg, keep_scores=True)
     got = host(ctx.sel.idx)
     s_gpu = host(ctx.scores).astype(np.float64)
     s64 = O.importance_scores(Q, O.compress_kv(K, V, c).K_cmp, c)
@@ -821,3 +821,17 @@ def test_kv_chunk_auto_above_the_tensor_core_limit(monkeypatch):
     out, ctx = fsa.nsa_forward(q, k, v, tau, cfg)
     assert isinstance(ctx, fsa.ChunkedNSAContext) and len(ctx.chunks) == 2
     assert torch.equal(out, ref)
+
+
+def test_keep_scores_default_releases_the_scores():
+    kw = dict(N=2048, d_K=128, d_V=128, h=8, h_K=2, B_K=64, T=8, W=128)
+    cfg = _cfg(kw)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    q, k, v = (torch.randn(cfg.N, hh, 128, device="cuda", dtype=torch.bfloat16, generator=g)
+               for hh in (cfg.h, cfg.h_K, cfg.h_K))
+    tau = torch.full((cfg.N, 3), 1.0 / 3, device="cuda")
+    out, ctx = fsa.nsa_forward(q, k, v, tau, cfg)
+    out2, ctx2 = fsa.nsa_forward(q, k, v, tau, cfg, keep_scores=True)
+    assert ctx.scores is None and ctx2.scores.shape == (cfg.h_K, cfg.N, cfg.b)
+    assert torch.equal(out, out2) and torch.equal(ctx.sel.idx, ctx2.sel.idx)
+    assert torch.equal(ctx.sel.idx, fsa.select_topk_blocks(ctx2.scores, cfg).idx)
