@@ -617,15 +617,6 @@ bool tc_qo_supported(const fsa_shape& s, int dtype) {
   return dtype == FSA_DT_BF16 && s.d_K == kD && s.d_V == kD && s.h_K > 0 && s.h % s.h_K == 0 &&
          s.h / s.h_K <= kRows && s.N < (1ll << 30);
 }
-// Fused scores epilogue only for g <= 2: it sums the g rows of a token with
-// warp shuffles (64 values per thread per step) and stores through the LSU;
-// for larger groups the group-summed-query pass on the tensor cores is faster
-// (measured: g = 4 at 32K 0.72 -> 0.65 ms; g = 1 at 64K fused 1.62 vs 2.11 ms).
-bool tc_cmp_scores_fused(const fsa_shape& s) {
-  (void)s;
-  return false;  // every g: the hi/lo scores pass (selection parity with the fp64 reference)
-}
-bool tc_cmp_scores_any_g() { return true; }
 
 int tc_slide_fwd(const fsa_shape* s, const void* Q, const void* K, const void* V16,
                  const float* vscale, void* out, void* lse, cudaStream_t st) {
@@ -681,11 +672,10 @@ int tc_cmp_fwd(const fsa_shape* s, const void* Q, const void* Q16, const float* 
   p.n_keys = p.b;
   p.out = (float*)out;
   p.lse = (float*)lse;
-  const bool fused = scores != nullptr && tc_cmp_scores_fused(*s);
-  p.scores = fused ? (float*)scores : nullptr;
+  p.scores = nullptr;  // the scores come from their own hi/lo pass below
   if (int rc = launch(p, st)) return rc;
   FSA_LAUNCH_CHECK("tc_cmp_fwd");
-  if (scores != nullptr && !fused) {
+  if (scores != nullptr) {
     // scores on the tensor cores for any g: the g query rows of a kv head are
     // summed first (hi/lo), then a g = 2 problem over (Qsum_hi, Qsum_lo) against
     // K_cmp hi (the K slot) + lo (the V slot, overwriting the pooled V copy the
