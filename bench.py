@@ -286,7 +286,7 @@ def max_over_ranks(x, world, dev):
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], device=dev, dtype=torch.float64)
+    t = torch.tensor([x], device=dev if dist.get_backend() == "nccl" else "cpu", dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -296,7 +296,7 @@ def sum_over_ranks(x, world, dev):
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], device=dev, dtype=torch.float64)
+    t = torch.tensor([x], device=dev if dist.get_backend() == "nccl" else "cpu", dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
 
@@ -398,11 +398,19 @@ def count_launches(m):
 def run_ours(args, rank, world, local_rank):
     import torch
 
+    # FSA_BENCH_ONE_GPU=1: every rank on cuda:0 with gloo collectives -- a
+    # functional check of the N > 1 path on a one-GPU box (timings meaningless)
+    one_gpu = os.environ.get("FSA_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     def barrier():
         if world > 1:
