@@ -246,3 +246,52 @@ def test_fullsize_whole_group(name):
     grads = nsa.nsa_backward(ctx, do) if spec["bwd"] else None
     torch.cuda.synchronize()
     _whole_group(name, spec, q, k, v, do, tau, out, ctx, grads, hk - 1)
+
+
+# ---------------------------------------------------------------------------
+# long context through the buffer-reusing kv-head-chunked schedule (512K tokens,
+# Qwen3-14B shape: N h = 21M >= 2^23, so nsa_forward chunks by kv head itself)
+# ---------------------------------------------------------------------------
+
+def test_long_context_512k_chunked_sampled():
+    N, h, h_K = 524288, 40, 8
+    kw = dict(N=N, d_K=128, d_V=128, h=h, h_K=h_K, B_K=64, T=16, W=512)
+    cfg = fsa.make_config(**kw)
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    bf = torch.bfloat16
+    q = torch.randn(N, h, 128, device="cuda", dtype=bf, generator=gen)
+    k = torch.randn(N, h_K, 128, device="cuda", dtype=bf, generator=gen)
+    v = torch.randn(N, h_K, 128, device="cuda", dtype=bf, generator=gen)
+    do = torch.randn(N, h, 128, device="cuda", dtype=bf, generator=gen)
+    tau = torch.rand(N, 3, device="cuda", generator=gen)
+    out, ctx = nsa.nsa_forward(q, k, v, tau, cfg)  # auto-chunked (N h >= 2^23)
+    assert isinstance(ctx, nsa.ChunkedNSAContext)
+    lo, hi, c0 = ctx.chunks[0]
+    assert (lo, hi) == (0, fsa.plan_kv_chunk(cfg))
+    dQ, dK, dV = nsa.nsa_backward(ctx, do)
+    torch.cuda.synchronize()
+    g, sub, idx0 = cfg.g, c0.cfg, c0.sel.idx.clone()
+    del ctx, c0
+    torch.cuda.empty_cache()
+    # the first chunk's sub-problem, re-run with its scores kept: same selection
+    qs, ks, vs = q[:, lo * g:hi * g].contiguous(), k[:, lo:hi].contiguous(), v[:, lo:hi].contiguous()
+    _, cs = nsa.nsa_forward(qs, ks, vs, tau, sub, keep_scores=True)
+    assert torch.equal(cs.sel.idx, idx0)
+    c = O.cfg_of(N=N, d_K=128, d_V=128, h=sub.h, h_K=sub.h_K, B_K=64, T=16, W=512)
+    rng = np.random.default_rng(5)
+    toks = np.unique(np.concatenate([[0, 63, 64, 300000, N - 1], rng.integers(0, N, 11)]))
+    tt = torch.from_numpy(toks).cuda()
+    idx_rows = idx0[:, tt].cpu().numpy()
+    np.testing.assert_array_equal(
+        O.select_topk_rows(cs.scores[:, tt].double().cpu().numpy(), toks, c), idx_rows)
+    del cs
+    Kc, Vc = _np(ks), _np(vs)
+    r = O.nsa_rows(_np(qs[tt]), toks, Kc, Vc, idx_rows, tau.double().cpu().numpy()[toks],
+                   O.pooled_kv(Kc, Vc, c), c, dO_rows=_np(do[tt, lo * g:hi * g]))
+    assert_close(_np(out[tt, lo * g:hi * g]), r["out"], "bf16", "512K out")
+    assert_close(_np(dQ[tt, lo * g:hi * g]), r["dQ"], "bf16", "512K dQ", grad=True)
+    # every kv head: sum_s dV[s] = sum_t (tau1 + tau2) sum_{j in grp} dOut[t, j]
+    w = (tau[:, 1] + tau[:, 2]).double()
+    rhs = (do.double() * w[:, None, None]).sum(0).view(h_K, g, 128).sum(1)
+    err = (dV.double().sum(0) - rhs).norm() / rhs.norm()
+    assert float(err) < 1e-2, f"512K dV column-sum identity off by {float(err):.2e}"
