@@ -8,6 +8,8 @@
 // exact for f32 and f64 inputs alike.
 #include "common.cuh"
 
+#include <cfloat>
+
 namespace fsa {
 
 struct SelKey {
@@ -317,6 +319,15 @@ __global__ void __launch_bounds__(256) topk_stream4_kernel(const float* __restri
       if (c0 + e == own) v4[e] = INFINITY;
     }
   };
+  // chunks wholly below the own block need no masking: a plain 16-byte load
+  auto raw4 = [&](int base, float (&v4)[4]) {
+    const float4 f = __ldg(sr4 + (base >> 2) + lane);
+    v4[0] = f.x; v4[1] = f.y; v4[2] = f.z; v4[3] = f.w;
+  };
+  auto load4 = [&](int base, float (&v4)[4]) {
+    if (base + 128 <= own) raw4(base, v4);
+    else vals4(base, v4);
+  };
   auto excl_scan = [&](int v, int& total) {  // warp exclusive prefix sum
     int incl = v;
 #pragma unroll
@@ -334,7 +345,7 @@ __global__ void __launch_bounds__(256) topk_stream4_kernel(const float* __restri
   if constexpr (NCH > 0) {
 #pragma unroll
     for (int k = 0; k < NCH; ++k)
-      if (k * 128 < ncand) vals4(k * 128, vr[k]);
+      if (k * 128 < ncand) load4(k * 128, vr[k]);
 #pragma unroll
     for (int k = 0; k < NCH; ++k)
       if (k * 128 < ncand) {
@@ -342,8 +353,14 @@ __global__ void __launch_bounds__(256) topk_stream4_kernel(const float* __restri
         for (int e = 0; e < 4; ++e) lmf = fmaxf(lmf, vr[k][e]);
       }
   } else {
-#pragma unroll 2
-    for (int base = 0; base < ncand; base += 128) {
+    int base = 0;
+#pragma unroll 4
+    for (; base + 128 <= own; base += 128) {
+      float v4[4];
+      raw4(base, v4);
+      lmf = fmaxf(lmf, fmaxf(fmaxf(v4[0], v4[1]), fmaxf(v4[2], v4[3])));
+    }
+    for (; base < ncand; base += 128) {  // the chunk(s) holding the own block
       float v4[4];
       vals4(base, v4);
 #pragma unroll
@@ -368,12 +385,14 @@ __global__ void __launch_bounds__(256) topk_stream4_kernel(const float* __restri
   // ---- pass 2: candidates >= theta, packed so that larger = better
   unsigned long long* slots = reinterpret_cast<unsigned long long*>(hist);
   int cand = 0;
+  // v > -inf && v >= thf as one compare (NaN fails both forms)
+  const float thf_eff = thf == -INFINITY ? -FLT_MAX : thf;
   auto chunk = [&](int base, const float (&v4)[4]) {
     bool c[4];
     int cnt = 0;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      c[e] = v4[e] > -INFINITY && v4[e] >= thf;
+      c[e] = v4[e] >= thf_eff;
       cnt += c[e];
     }
     if (!__any_sync(0xffffffffu, cnt > 0)) return;  // no candidate in this chunk
@@ -393,11 +412,15 @@ __global__ void __launch_bounds__(256) topk_stream4_kernel(const float* __restri
 #pragma unroll
     for (int k = 0; k < NCH; ++k)
       if (k * 128 < ncand) chunk(k * 128, vr[k]);
-  } else {
+  } else {  // the next chunk's load is in flight while this one is scanned
+    float cur[4];
+    load4(0, cur);
     for (int base = 0; base < ncand; base += 128) {
-      float v4[4];
-      vals4(base, v4);
-      chunk(base, v4);
+      float nxt[4];
+      load4(base + 128, nxt);  // -inf past the row (no load)
+      chunk(base, cur);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) cur[e] = nxt[e];
     }
   }
   __syncwarp();
