@@ -370,27 +370,33 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
         tmem_wait_ld();
         const int kbase = kt * 64;
         if (M == SCORES) {
-          // the token's rows (hi, lo) are adjacent lanes: summed, written by the first
+          // the token's rows (hi, lo) are adjacent lanes (g = 2): each lane of
+          // the pair sends the half the other one stores -- lane hh sums and
+          // writes columns [32 hh, 32 hh + 32) (hi + lo, lo + hi: the same
+          // float sum), so one shuffle and half a row of stores per column pair
           const float gm = p.score_mul;
-          float* dst = p.scores + ((int64_t)c.it.kh * p.N + t) * p.b + kbase;
-          const bool wr = ok && hh == 0;
+          const int c0 = 32 * hh;
+          float* dst = p.scores + ((int64_t)c.it.kh * p.N + t) * p.b + kbase + c0;
+          const bool wr = ok;
 #pragma unroll
-          for (int cc = 0; cc < 64; cc += 4) {
-            float x0 = sv[cc], x1 = sv[cc + 1], x2 = sv[cc + 2], x3 = sv[cc + 3];
-            for (int o = 1; o < p.g; o <<= 1) {
-              x0 += __shfl_xor_sync(0xffffffffu, x0, o);
-              x1 += __shfl_xor_sync(0xffffffffu, x1, o);
-              x2 += __shfl_xor_sync(0xffffffffu, x2, o);
-              x3 += __shfl_xor_sync(0xffffffffu, x3, o);
+          for (int cc = 0; cc < 32; cc += 8) {
+            float x[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const float mine = hh ? sv[32 + cc + e] : sv[cc + e];
+              const float give = hh ? sv[cc + e] : sv[32 + cc + e];
+              x[e] = (mine + __shfl_xor_sync(0xffffffffu, give, 1)) * gm;
             }
             if (wr) {
-              if (kbase + cc + 3 < p.b && (p.b & 3) == 0) {  // 16 B aligned rows
-                *reinterpret_cast<float4*>(dst + cc) = make_float4(x0 * gm, x1 * gm, x2 * gm, x3 * gm);
+              if (kbase + c0 + cc + 7 < p.b && (p.b & 7) == 0) {  // one full 32 B sector per store
+                asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + cc),
+                             "f"(x[0]), "f"(x[1]), "f"(x[2]), "f"(x[3]), "f"(x[4]), "f"(x[5]), "f"(x[6]),
+                             "f"(x[7])
+                             : "memory");
               } else {
-                if (kbase + cc < p.b) dst[cc] = x0 * gm;
-                if (kbase + cc + 1 < p.b) dst[cc + 1] = x1 * gm;
-                if (kbase + cc + 2 < p.b) dst[cc + 2] = x2 * gm;
-                if (kbase + cc + 3 < p.b) dst[cc + 3] = x3 * gm;
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                  if (kbase + c0 + cc + e < p.b) dst[cc + e] = x[e];
               }
             }
           }
