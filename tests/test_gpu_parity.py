@@ -78,8 +78,9 @@ def test_select_topk_random_vs_oracle(kw, sdt):
 
 @pytest.mark.parametrize("kw", [
     dict(N=16384, d_K=8, d_V=8, h=2, h_K=2, B_K=16, T=16),   # b = 1024 (32 candidates / lane)
-    dict(N=32768, d_K=8, d_V=8, h=1, h_K=1, B_K=16, T=16),   # b = 2048: rows staged by bulk copies
-    dict(N=8192, d_K=8, d_V=8, h=1, h_K=1, B_K=2, T=32),     # b = 4096: 4 warps per block
+    dict(N=32768, d_K=8, d_V=8, h=1, h_K=1, B_K=16, T=16),   # b = 2048: streamed rows
+    dict(N=8192, d_K=8, d_V=8, h=1, h_K=1, B_K=2, T=32),     # b = 4096
+    dict(N=4112, d_K=8, d_V=8, h=1, h_K=1, B_K=4, T=8),      # b = 1028: streamed rows
     dict(N=4800, d_K=8, d_V=8, h=1, h_K=1, B_K=16, T=32),    # b = 300, T = 32
     dict(N=2048, d_K=8, d_V=8, h=1, h_K=1, B_K=64, T=1),     # b = 32, T = 1
 ])
