@@ -148,7 +148,7 @@ def _nsa_forward_chunked(q, k, v, tau, cfg, kv_chunk, keep_scores=False):
     _check(q, "Q", (cfg.N, cfg.h, cfg.d_K), dt, dev)
     _check(k, "K", (cfg.N, cfg.h_K, cfg.d_K), dt, dev)
     _check(v, "V", (cfg.N, cfg.h_K, cfg.d_V), dt, dev)
-    if cfg.h_K % kv_chunk:
+    if kv_chunk < 1 or cfg.h_K % kv_chunk:
         raise ValueError(f"kv_chunk={kv_chunk} does not divide h_K={cfg.h_K}")
     sub = _chunk_cfg(cfg, kv_chunk)
     out = torch.empty((cfg.N, cfg.h, cfg.d_V), dtype=dt, device=dev)
@@ -394,6 +394,8 @@ def nsa_forward_backward(q, k, v, tau, dout, cfg, *, full: bool = False, kv_chun
     if kv_chunk is None or kv_chunk >= cfg.h_K:
         out, ctx = nsa_forward(q, k, v, tau, cfg)
         return (out,) + tuple(nsa_backward(ctx, dout, full=full))
+    if kv_chunk < 1 or cfg.h_K % kv_chunk:
+        raise ValueError(f"kv_chunk={kv_chunk} does not divide h_K={cfg.h_K}")
     dt, dev = q.dtype, q.device
     _check(dout, "dOut", (cfg.N, cfg.h, cfg.d_V), dt, dev)
     acc = _lib.acc_dtype(dt)

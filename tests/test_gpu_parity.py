@@ -803,6 +803,11 @@ def test_kv_chunked_step_matches_unchunked(kv_chunk):
     for a, b, name in zip(got[:4], ref[:4], ("out", "dQ", "dK", "dV")):
         assert torch.equal(a, b), name
     assert torch.allclose(got[4], ref[4], rtol=1e-5, atol=1e-6), "dtau"
+    for bad in (0, 3):
+        with pytest.raises(ValueError, match="does not divide"):
+            fsa.nsa_forward(q, k, v, tau, cfg, kv_chunk=bad)
+    o3, c3 = fsa.nsa_forward(q, k, v, tau, cfg, kv_chunk="auto")  # fits: one chunk (unchunked)
+    assert not isinstance(c3, fsa.ChunkedNSAContext) and torch.equal(o3, out)
     fused = fsa.nsa_forward_backward(q, k, v, tau, do, cfg, full=True, kv_chunk=kv_chunk)
     for a, b in zip(fused[:4], ref[:4]):
         assert torch.equal(a, b)
