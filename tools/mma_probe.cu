@@ -87,13 +87,13 @@ __global__ void probe(Case c, int groups, int rep, unsigned long long* out) {
 }
 
 int main() {
-  static char names[64][64];
-  Case cases[64];
+  static char names[128][64];
+  Case cases[128];
   int nc = 0;
   const char* an[3] = {"Kmaj", "MN", "tmem"};
   for (int N : {64, 128, 256})
     for (int ch : {1, 2, 4})
-      for (int a = 0; a < 3; a += 2)
+      for (int a = 0; a < 3; ++a)
         for (int bm = 0; bm < 2; ++bm) {
           if (N * ch > 256 && ch > 1) continue;
           snprintf(names[nc], 64, "M128 N%-3d A %-4s B %-4s chains %d", N, an[a], bm ? "MN" : "Kmaj", ch);
