@@ -172,7 +172,7 @@ def measure(name, w, rank, world, dev, steps, warmup, barrier, use_graph=True):
     cfg = sh.cfg
     q, k, v, dout, tau = rank_inputs(cfg0, sh.kv_lo, sh.kv_hi, dev)
     orig_call = _lib.call
-    kev = {"fsa_sel_fwd": [], "fsa_sel_bwd": []}
+    kev = {"fsa_sel_fwd": [], "fsa_sel_bwd": [], "fsa_merge_combine_fwd": [], "fsa_dq_reduce_add": []}
     capturing = [False]
 
     def record(e):
@@ -235,7 +235,7 @@ def measure(name, w, rank, world, dev, steps, warmup, barrier, use_graph=True):
             _lib.call = orig_call
             capturing[0] = False
         if graph is None:
-            kev = {"fsa_sel_fwd": [], "fsa_sel_bwd": []}
+            kev = {k_: [] for k_ in kev}
         else:
             graph.replay()  # untimed: first replay uploads the graph
             torch.cuda.synchronize()
@@ -256,13 +256,14 @@ def measure(name, w, rank, world, dev, steps, warmup, barrier, use_graph=True):
         _lib.call = orig_call
     torch.cuda.synchronize()
     ms = start.elapsed_time(stop) / steps
-    k5 = [e0.elapsed_time(e1) for e0, e1 in kev["fsa_sel_fwd"]][-steps:]
-    k8 = [e0.elapsed_time(e1) for e0, e1 in kev["fsa_sel_bwd"]][-steps:]
+    per = {k_: statistics.mean([e0.elapsed_time(e1) for e0, e1 in ev][-steps:])
+           for k_, ev in kev.items() if ev}
     del graph
     torch.cuda.empty_cache()
     return dict(name=name, cfg=cfg, cfg0=cfg0, shard=sh, ms=ms, R=R,
-                k5_ms=statistics.mean(k5), k8_ms=statistics.mean(k8), graph=use_graph,
-                inputs=(q, k, v, dout, tau))
+                k5_ms=per["fsa_sel_fwd"], k8_ms=per["fsa_sel_bwd"],
+                merge_ms=per.get("fsa_merge_combine_fwd"), dqr_ms=per.get("fsa_dq_reduce_add"),
+                graph=use_graph, inputs=(q, k, v, dout, tau))
 
 
 _LIBCUDA = None
@@ -434,6 +435,8 @@ def run_ours(args, rank, world, local_rank):
     ms = max_over_ranks(m["ms"], world, dev)
     k5_ms = max_over_ranks(m["k5_ms"], world, dev)
     k8_ms = max_over_ranks(m["k8_ms"], world, dev)
+    merge_ms = max_over_ranks(m["merge_ms"] or 0.0, world, dev)
+    dqr_ms = max_over_ranks(m["dqr_ms"] or 0.0, world, dev)
     R_rank = m["R"]
     R_all = sum_over_ranks(R_rank, world, dev)
     gpu_launches, kernel_names = count_launches(m)
@@ -455,6 +458,16 @@ def run_ours(args, rank, world, local_rank):
                 "kernel_ms": round(kms, 4), "share_of_step": round(kms / ms, 4),
                 "algorithmic": algo}
 
+    def hbm_roof(nbytes, kms, peak, algo):
+        if not kms:
+            return None
+        ach = nbytes / (kms / 1e3) / 1e9
+        return {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(ach / peak, 4), "kernel_ms": round(kms, 4), "algorithmic": algo}
+
+    nhd = cfg0.N * (cfg0.h // world) * cfg0.d_V
+    merge_bytes = R_rank * (2 * cfg0.d_V + 8) + 2 * nhd * 4 + nhd * 4 + nhd * 2
+    dqr_bytes = R_rank * (2 * cfg0.d_K + 4) + nhd * 4 + nhd * 4
     # per-rank FLOPs of the selected kernels (R of the rank's shard)
     k5_flops = 4.0 * cfg0.d_K * cfg0.B_K * R_rank
     k8_flops = 10.0 * cfg0.d_K * cfg0.B_K * R_rank
@@ -482,6 +495,15 @@ def run_ours(args, rank, world, local_rank):
         "roofline_sel_fwd": roof("sel_fwd (K5, tcgen05)", k5_flops, k5_ms,
                                  "4*d*B_K*R FLOPs per launch, R = %d on this rank" % R_rank,
                                  "tc_sel_fwd"),
+        # the two HBM-bound kernels around the FSA partial buffers
+        "roofline_hbm": {
+            "merge (K6+K12)": hbm_roof(merge_bytes, merge_ms, hbm,
+                                       "R*(2d+8) partial rows + 2 N h d*4 (out_cmp, out_slide) read, "
+                                       "N h d*4 (out_sel) + N h d*2 (out) written"),
+            "dq_reduce (K9)": hbm_roof(dqr_bytes, dqr_ms, hbm,
+                                       "R*(2d+4) dq partial rows + N h d*4 (sliding dQ) read, "
+                                       "N h d*4 (dQ) written"),
+        },
         "e2e": {"value": round(cfg0.N / (e2e_ms / 1e3), 1), "unit": "tokens/s",
                 "ms_per_step": round(e2e_ms, 3), "steps": max(args.steps, 10),
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
