@@ -22,6 +22,7 @@ from paper_2508_18224_b200 import nsa  # noqa: E402
 
 CONFIGS = [
     ("llama3-8b-attn-32k", dict(N=32768, h=32, h_K=8), True),
+    ("llama3-8b-attn-64k (north_star target)", dict(N=65536, h=32, h_K=8), True),
     ("qwen2.5-7b-attn-64k (fwd)", dict(N=65536, h=28, h_K=4), False),
     ("gqa1-stress-64k", dict(N=65536, h=16, h_K=16), True),
     ("qwen3-14b-attn-128k", dict(N=131072, h=40, h_K=8), True),
