@@ -662,6 +662,30 @@ def test_query_head_split_matches_unsharded():
     dict(N=4160, d_K=128, d_V=128, h=5, h_K=1, B_K=64, T=64, W=512),
 ])
 def test_nsa_step_shapes_vs_oracle(kw):
+    _nsa_step_vs_oracle(kw)
+
+
+# seeded random shapes: group sizes 2..12, budgets 1..24, windows 1..900, N up to 3K,
+# B_K 64 (tensor-core path) or 32 / 16 (SIMT path)
+def _fuzz_shapes(n=6, seed=2026):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        B_K = int(rng.choice([64, 64, 64, 32, 16]))
+        b = int(rng.integers(4, 3072 // B_K + 1))
+        h_K = int(rng.integers(1, 4))
+        g = int(rng.integers(2, 13))
+        out.append(dict(N=b * B_K, d_K=128, d_V=128, h=g * h_K, h_K=h_K, B_K=B_K,
+                        T=int(rng.integers(1, min(24, b) + 1)), W=int(rng.integers(1, 900))))
+    return out
+
+
+@pytest.mark.parametrize("kw", _fuzz_shapes())
+def test_nsa_step_fuzz_vs_oracle(kw):
+    _nsa_step_vs_oracle(kw)
+
+
+def _nsa_step_vs_oracle(kw):
     c = O.cfg_of(**kw)
     cfg = _cfg(kw)
     Q, K, V = (round_inputs(x, "bf16") for x in O.make_qkv(c, 21))
