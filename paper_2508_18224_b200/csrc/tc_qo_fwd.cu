@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
   if (threadIdx.x == 0) {
     for (int s = 0; s < 2; ++s) {
       mbar_init(bar(B_QF + s), 1);  // TMA: arrive.expect_tx + bytes
-      mbar_init(bar(B_QE + s), 2);  // one commit per S stream
+      mbar_init(bar(B_QE + s), M == SCORES ? 1 : 2);  // SCORES: one MMA commit; else both epilogues
       mbar_init(bar(B_OF + s), 1);
       mbar_init(bar(B_OE + s), 128);
       mbar_init(bar(B_PV + s), 1);
@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
     }
     for (int s = 0; s < kKVStages; ++s) {
       mbar_init(bar(B_KF + s), 1);
-      mbar_init(bar(B_KE + s), 2);  // one commit per PV stream
+      mbar_init(bar(B_KE + s), 1);  // one commit per union tile, after both PV streams
     }
     fence_mbar_init();
   }
@@ -273,23 +273,17 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
               ++ns[w];
             }
           }
-          if (u > it.u0) {  // ---- PV of tile u-1 (or pass-by KE commits)
+          if (u > it.u0) {  // ---- PV of tile u-1, then the K/V stage release
             const int up = u - 1;
             const int rr = c.rbase + (up - it.u0), kv = rr % kKVStages;
 #pragma unroll
             for (int w = 0; w < 2; ++w) {
               const Sub& sw = it.s[w];
-              if (up < sw.k0 || up >= sw.k1) {
-                if (elect_one()) mma_commit(bar(B_KE + kv));  // pass-by
-                __syncwarp();
-                continue;
-              }
+              if (up < sw.k0 || up >= sw.k1) continue;  // tile outside this sub-item
               const int v = np[w] & 1;
               const bool first = up == sw.k0, last = up + 1 == sw.k1;
               mbar_wait_warp(bar(B_PF + 2 * w + v), (uint32_t)((np[w] >> 1) & 1));
-              if (M == SCORES) {  // no PV: release the K tile once S is consumed
-                if (elect_one()) mma_commit(bar(B_KE + kv));
-                __syncwarp();
+              if (M == SCORES) {  // no PV: the K tile is released once S is consumed
                 ++np[w];
                 continue;
               }
@@ -302,7 +296,6 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
                 for (int kk = 0; kk < 4; ++kk)
                   mma_bf16_ts(tO, tS + kk * 8, desc_mnmajor(vv + kk * 2048u, 8192u), kIdPV,
                               (first && kk == 0) ? 0u : 1u);
-                mma_commit(bar(B_KE + kv));
                 mma_commit(bar(B_PV + w));
                 if (last) mma_commit(bar(B_OF + w));
                 QO_TRACE(w, np[w], 3);  // PV issued
@@ -311,16 +304,17 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
               if (last) ++nsub[w];
               ++np[w];
             }
+            // one commit per union tile frees its K/V stage once every MMA
+            // reading it (both sub-items' S and PV) has completed
+            if (elect_one()) mma_commit(bar(B_KE + kv));
+            __syncwarp();
           }
         }
         // SCORES: both S streams are done with this Q stage.  (SLIDE / CMP: the
         // softmax warpgroups release it after their epilogue has staged the
         // output rows in it and the TMA store has read them.)
         if constexpr (M == SCORES) {
-          if (elect_one()) {
-            mma_commit(bar(B_QE + qs));
-            mma_commit(bar(B_QE + qs));
-          }
+          if (elect_one()) mma_commit(bar(B_QE + qs));
           __syncwarp();
         }
       }
@@ -462,6 +456,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
         tmem_wait_st_();
         tc_fence_before();
         mbar_arrive(bar(B_PF + 2 * w + v));
+        // observe PV(u-1)'s completion every tile (the rescale above waits for
+        // it only when the reference max moves): every commit-driven phase of
+        // B_PV gets a waiter -- long complete by now, so this rarely blocks
+        if (u > 0) mbar_wait_warp(bar(B_PV + w), (uint32_t)((u - 1) & 1));
         if (r == 0) QO_TRACE(w, u, 2);  // P written
         if (lane == 0) QO_TRACE(w + 2, u, 2 + (warp & 3));  // per-warp P arrival
       }

@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const __grid_c
     }
     for (int s = 0; s < kKVStages; ++s) {
       mbar_init(bar(B_KF + s), 1);
-      mbar_init(bar(B_KE + s), 2);
+      mbar_init(bar(B_KE + s), 1);  // one commit per union tile, after both streams
     }
     fence_mbar_init();
   }
@@ -200,8 +200,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const __grid_c
     // Static order with blocking waits (one lane waits; one elected lane
     // issues).  Per union tile u of a super item and per sub-item w: first
     // dQ_w += dS K of tile u-1 (it frees wg w's single S/dP TMEM stage), then
-    // S/dP_w of tile u.  KE: one commit per stream per union tile (pass-by
-    // outside the sub-item's range; KE counts 2); QE: two per super item.
+    // S/dP_w of tile u.  KE: one commit per union tile after both streams;
+    // QE: two arrivals per super item (the softmax warpgroups).
     {
       Cursor<CM> c;
       int ns[2] = {0, 0}, nd[2] = {0, 0}, nsub[2] = {0, 0};
@@ -215,12 +215,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const __grid_c
 #pragma unroll
           for (int w = 0; w < 2; ++w) {
             const Sub& sw = it.s[w];
-            if (u > it.u0) {  // ---- dQ of tile u-1 (or a pass-by KE commit)
+            if (u > it.u0) {  // ---- dQ of tile u-1
               const int up = u - 1, rp = rr - 1, kvp = rp % kKVStages;
-              if (up < sw.k0 || up >= sw.k1) {
-                if (elect_one()) mma_commit(bar(B_KE + kvp));
-                __syncwarp();
-              } else {
+              if (up >= sw.k0 && up < sw.k1) {
                 const bool first = up == sw.k0, last = up + 1 == sw.k1;
                 mbar_wait_warp(bar(B_PF + w), (uint32_t)(nd[w] & 1));
                 if (first) mbar_wait_warp(bar(B_OE + w), (uint32_t)((nsub[w] & 1) ^ 1));
@@ -233,7 +230,6 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const __grid_c
                     mma_bf16_ts(tQ, tS + kk * 8, desc_mnmajor(k + kk * 2048u, 8192u), kIdQ,
                                 (first && kk == 0) ? 0u : 1u);
                   DQ_TRACE(w, nd[w], 3);  // dQ issued
-                  mma_commit(bar(B_KE + kvp));
                   if (last) mma_commit(bar(B_OF + w));
                 }
                 __syncwarp();
@@ -265,6 +261,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const __grid_c
               __syncwarp();
               ++ns[w];
             }
+          }
+          if (u > it.u0) {  // tile u-1's K/V stage: free once both streams' MMAs on it complete
+            if (elect_one()) mma_commit(bar(B_KE + (rr - 1) % kKVStages));
+            __syncwarp();
           }
         }
       }
