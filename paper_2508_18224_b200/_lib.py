@@ -186,7 +186,25 @@ def buffer_dtypes(cfg, dtype):
     s = shape_of(cfg)
     ob, dq = ctypes.c_int(), ctypes.c_int()
     call("fsa_buffer_dtypes", ctypes.byref(s), dt_code(dtype), ctypes.byref(ob), ctypes.byref(dq))
+    if (dtype == torch.bfloat16 and ob.value != DT_F16 and cfg.d_K == 128 and cfg.d_V == 128
+            and cfg.B_K == 64 and cfg.N * cfg.h >= (1 << 23)):
+        _warn_large_once(cfg)
     return (ob.value, _TORCH_OF[ob.value]), (dq.value, _TORCH_OF[dq.value])
+
+
+_WARNED_LARGE = False
+
+
+def _warn_large_once(cfg):
+    """The tensor-core kernels index (token, head) rows with 32-bit offsets
+    (N h < 2^23); a larger single call runs the CUDA-core kernels -- say so once."""
+    global _WARNED_LARGE
+    if not _WARNED_LARGE:
+        import warnings
+        warnings.warn(f"N*h = {cfg.N * cfg.h} >= 2^23: this call runs the CUDA-core kernels, not "
+                      "the tensor-core ones; nsa_forward / nsa_forward_backward chunk by kv head "
+                      "automatically (kv_chunk), or shard the kv heads", RuntimeWarning, stacklevel=3)
+        _WARNED_LARGE = True
 
 
 def partial_rows(cfg, dtype) -> int:

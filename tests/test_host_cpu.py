@@ -237,3 +237,20 @@ def test_plan_kv_chunk():
     assert fsa.plan_kv_chunk(c, budget_bytes=kv_chunk_bytes(c, 4)) == 4
     assert fsa.plan_kv_chunk(c, budget_bytes=kv_chunk_bytes(c, 4) - 1) == 2
     assert fsa.plan_kv_chunk(c, budget_bytes=1) == 1
+
+
+def test_large_call_off_the_tensor_core_path_warns():
+    """N h >= 2^23 on the bf16 d = 128 configuration leaves the tensor-core
+    kernels (32-bit row offsets): the buffer planner says so, once."""
+    import warnings
+    big = fsa.make_config(N=262144, d_K=128, d_V=128, h=40, h_K=8, B_K=64, T=16, W=512)
+    ok = fsa.make_config(N=131072, d_K=128, d_V=128, h=40, h_K=8, B_K=64, T=16, W=512)
+    _lib._WARNED_LARGE = False
+    with warnings.catch_warnings(record=True) as w:
+        warnings.simplefilter("always")
+        assert _lib.buffer_dtypes(ok, torch.bfloat16)[0][0] == _lib.DT_F16
+        assert not w
+        assert _lib.buffer_dtypes(big, torch.bfloat16)[0][0] != _lib.DT_F16
+        assert len(w) == 1 and issubclass(w[0].category, RuntimeWarning) and "kv_chunk" in str(w[0].message)
+        _lib.buffer_dtypes(big, torch.bfloat16)
+        assert len(w) == 1
