@@ -236,6 +236,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const __grid_c
                 if (last) ++nsub[w];
                 ++nd[w];
               }
+              if (w == 1) {  // both streams' dQ of tile u-1 issued: free its K/V stage
+                if (elect_one()) mma_commit(bar(B_KE + kvp));
+                __syncwarp();
+              }
             }
             if (s_step && u >= sw.k0 && u < sw.k1) {  // ---- S/dP of tile u
               if (!q_ready) {
@@ -261,10 +265,6 @@ __global__ void __launch_bounds__(kThreads, 1) tc_slide_dq_kernel(const __grid_c
               __syncwarp();
               ++ns[w];
             }
-          }
-          if (u > it.u0) {  // tile u-1's K/V stage: free once both streams' MMAs on it complete
-            if (elect_one()) mma_commit(bar(B_KE + (rr - 1) % kKVStages));
-            __syncwarp();
           }
         }
       }
