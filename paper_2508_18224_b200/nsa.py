@@ -246,6 +246,8 @@ def nsa_forward(q, k, v, tau, cfg, *, heads=None, kv_chunk=None, keep_scores=Fal
     idx = torch.empty((cfg.h_K, cfg.N, cfg.T), dtype=torch.int32, device=dev)
     _lib.call("fsa_select_topk", ctypes.byref(s), _lib.dt_code(acc), _lib.ptr(scores),
               _lib.ptr(idx), st)
+    if not keep_scores:  # h_K N b floats: release them before the partial buffers are allocated
+        scores = None
     sel = SelectionTensor(idx)
     sel._trusted = True
     if heads is not None:
@@ -284,7 +286,7 @@ def nsa_forward(q, k, v, tau, cfg, *, heads=None, kv_chunk=None, keep_scores=Fal
               st)
     del obuf, ml
     ctx = NSAContext(cfg, dt, q, k, v, tau, sel, inv, out_sel, lse_sel, out_slide, lse_slide,
-                     out_cmp, scores if keep_scores else None, Kc, Vc, lse_cmp, ops)
+                     out_cmp, scores, Kc, Vc, lse_cmp, ops)
     return out, ctx
 
 

@@ -1,7 +1,7 @@
 """Long-context NSA steps on one B200 with the buffer-reusing kv-head-chunked
 schedule (nsa.nsa_forward_backward(kv_chunk=...)).
 
-    python tools/long_context.py [N ...]      (default: Qwen3-14B shape at 128K, 256K, 512K)
+    python tools/long_context.py [N ...]      (default: Qwen3-14B shape at 128K, 256K, 512K, 1M)
 
 Per N: the chunk plan_kv_chunk picks, device ms per fwd+bwd step (CUDA events,
 median of 3 after a warm-up), tokens/s, peak device memory, and -- as a cheap
@@ -13,7 +13,10 @@ import json
 import os
 import sys
 
-import torch
+# one allocation pattern per N: expandable segments keep the 64 GB score
+# buffer of a 1M-token chunk from failing on a fragmented cache
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
+import torch  # noqa: E402
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2508_18224_b200 as fsa  # noqa: E402
@@ -54,7 +57,7 @@ def run(N, h=40, h_K=8):
 
 
 if __name__ == "__main__":
-    Ns = [int(x) for x in sys.argv[1:]] or [131072, 262144, 524288]
+    Ns = [int(x) for x in sys.argv[1:]] or [131072, 262144, 524288, 1048576]
     for N in Ns:
         print(json.dumps(run(N)), flush=True)
         torch.cuda.empty_cache()
