@@ -230,9 +230,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
     // Static order with blocking waits (one lane waits, the warp follows; one
     // elected lane issues): per union tile u of a super item, S of both
     // sub-items for tile u, then PV of both for tile u-1 (S runs one tile
-    // ahead so the softmax of u-1 overlaps the S MMAs of u).  Each PV stream
-    // commits KE once per union tile (pass-by when the tile is outside its
-    // range; KE counts 2), each S stream QE once per super item (QE counts 2).
+    // ahead so the softmax of u-1 overlaps the S MMAs of u).  One KE commit per
+    // union tile after both PV streams frees its K/V stage (a single arrival
+    // per phase: synccheck-clean); SCORES: one QE commit per super item (the
+    // other modes' QE arrivals come from the two epilogues).
     {
       Cursor<M> c;
       int ns[2] = {0, 0}, np[2] = {0, 0}, nsub[2] = {0, 0};
