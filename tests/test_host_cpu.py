@@ -254,3 +254,15 @@ def test_large_call_off_the_tensor_core_path_warns():
         assert len(w) == 1 and issubclass(w[0].category, RuntimeWarning) and "kv_chunk" in str(w[0].message)
         _lib.buffer_dtypes(big, torch.bfloat16)
         assert len(w) == 1
+
+
+@pytest.mark.parametrize("N,h,h_K", [(32768, 32, 8), (65536, 32, 8), (65536, 28, 4),
+                                     (65536, 16, 16), (131072, 40, 8)])
+def test_baseline_shapes_plan_the_tensor_core_path(N, h, h_K):
+    """Every BASELINE.json GPU shape (and the Llama-3-8B 64K target) plans the
+    bf16 tensor-core buffers (fp16 partials, fp16+exponent dq partials) and no
+    kv-head chunking -- a regression into the CUDA-core kernels would show here."""
+    cfg = fsa.make_config(N=N, d_K=128, d_V=128, h=h, h_K=h_K, B_K=64, T=16, W=512)
+    (ob, _), (dq, _) = _lib.buffer_dtypes(cfg, torch.bfloat16)
+    assert (ob, dq) == (_lib.DT_F16, _lib.DT_F16R)
+    assert fsa.plan_kv_chunk(cfg) == h_K
