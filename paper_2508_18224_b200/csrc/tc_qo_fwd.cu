@@ -455,12 +455,14 @@ __global__ void __launch_bounds__(kThreads, 1) tc_qo_fwd_kernel(const __grid_con
         l += l0 + l1;
         tmem_st32u(tS, pk);  // P over S: fp16 pairs, K-packed
         tmem_wait_st_();
+        // observe PV(u-1)'s completion every tile (the rescale above waits for
+        // it only when the reference max moves), so every commit-driven phase
+        // of B_PV gets a waiter.  Before P(u) is published: PV(u) cannot have
+        // completed yet, so the parity test cannot alias a later phase; PV(u-1)
+        // was issued a whole softmax ago and rarely blocks.
+        if (u > 0) mbar_wait_warp(bar(B_PV + w), (uint32_t)((u - 1) & 1));
         tc_fence_before();
         mbar_arrive(bar(B_PF + 2 * w + v));
-        // observe PV(u-1)'s completion every tile (the rescale above waits for
-        // it only when the reference max moves): every commit-driven phase of
-        // B_PV gets a waiter -- long complete by now, so this rarely blocks
-        if (u > 0) mbar_wait_warp(bar(B_PV + w), (uint32_t)((u - 1) & 1));
         if (r == 0) QO_TRACE(w, u, 2);  // P written
         if (lane == 0) QO_TRACE(w + 2, u, 2 + (warp & 3));  // per-warp P arrival
       }
